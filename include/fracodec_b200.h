@@ -1,0 +1,124 @@
+/* fracodec_b200 -- C ABI of the B200-native fractal encoder search.
+ *
+ * Plain C types only (no torch / CUDA types in signatures).  Every entry
+ * point returns an FC_* status; on failure fc_last_error(ctx) holds a one-line
+ * message.  All calls are stream-ordered on the context's CUDA stream and
+ * synchronous at return unless noted.  Host pointers are plain pageable or
+ * pinned memory; device-resident variants say so.
+ *
+ * The reference (`fracodec`, Python + numba) has no FFI of its own; these
+ * entry points replace the interfaces a ctypes binding of the reference hot
+ * path would bind (paths relative to /root/reference/pkg/src/fracodec):
+ *
+ *   fc_scan_candidates  <- _scan.py:14       scan_candidates(...) kernel seam
+ *   fc_pool_build       <- pool.py:155       build_pool(image, params)
+ *   fc_pool_coords      <- pool.py:84        DomainPool.coords(level)
+ *   fc_pool_entries     <- pool.py:138-152   DomainEntry fields per survivor
+ *   fc_pool_set_level   <- tests/oracles.py:29 make_test_pool (synthetic pools)
+ *   fc_level_prepare    <- matcher.py:132    build_candidate_set(pool, level, policy)
+ *   fc_match_tiles      <- matcher.py:162    scan_tiles(tiles, candidate_set)
+ *   fc_match_level      <- codec.py:185-193  match_level(level, origins) incl.
+ *                          codec.py:164 _gather_tiles + matcher.py:162 scan_tiles
+ *   fc_set_entropy_lut  <- pool.py:88-92     the p*log(p) terms numpy produces
+ */
+#ifndef FRACODEC_B200_H_
+#define FRACODEC_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  FC_OK = 0,
+  FC_ERR_CUDA = 1,         /* CUDA runtime / launch failure */
+  FC_ERR_ARG = 2,          /* invalid argument (ValueError in the reference) */
+  FC_ERR_POOL_CONFIG = 3,  /* pool.py:28 PoolConfigError: domain side exceeds image */
+  FC_ERR_EMPTY_POOL = 4,   /* matcher.py:34 EmptyPoolError: no entries at level */
+  FC_ERR_TILE_SIZE = 5,    /* matcher.py:168-169 tile size does not match level */
+  FC_ERR_DIMS = 6,         /* codec.py:173-176 dimensions not multiple of 16 */
+  FC_ERR_NO_DEVICE = 7,    /* no sm_100 device visible */
+  FC_ERR_STATE = 8         /* call order violated (no image / pool / LUT) */
+};
+
+enum { FC_PATH_AUTO = 0, FC_PATH_EXACT = 1, FC_PATH_TENSOR = 2 };
+
+typedef struct fc_ctx fc_ctx;
+
+typedef struct fc_stats {
+  int64_t comparisons;      /* ranges * E * 8 * S of the last fc_match_level */
+  int64_t ranges;
+  int64_t columns;          /* E * S */
+  int32_t path;             /* FC_PATH_EXACT or FC_PATH_TENSOR actually used */
+  int32_t kernel_launches;  /* launches issued by the last call */
+  float scan_ms;            /* device time of the scan kernels (CUDA events) */
+  float main_ms;            /* tensor path: main contraction kernel only */
+  float fix_ms;             /* tensor path: exact clamp-correction kernel */
+  int64_t fix_pairs;        /* (range, column) pairs re-evaluated exactly */
+} fc_stats;
+
+int fc_version(void);
+int fc_ctx_create(int device, fc_ctx** out);
+void fc_ctx_destroy(fc_ctx* ctx);
+const char* fc_last_error(fc_ctx* ctx);
+int fc_synchronize(fc_ctx* ctx);
+/* Device-resident mode for benchmarking: when set, fc_set_image's pixels and
+ * fc_match_level's origins/outputs are DEVICE pointers (no host copies). */
+int fc_set_device_io(fc_ctx* ctx, int device_io);
+
+/* terms[k-1] = (k/n) * log(k/n), k = 1..n, produced by the host's numpy so the
+ * entropy bits equal pool.py:88-92 on the same host.  n in {16,64,256,1024}. */
+int fc_set_entropy_lut(fc_ctx* ctx, int n, const double* terms);
+
+/* Upload (or, in device-io mode, adopt) a row-major uint8 height x width image. */
+int fc_set_image(fc_ctx* ctx, const uint8_t* pixels, int width, int height);
+
+/* Build all four levels' pools (pool.py:155-178).  Per level: keep the top
+ * caps[l] windows by entropy (stable raster tie order), or, when use_tau[l]
+ * is nonzero, every window with entropy > taus[l] (threshold compaction;
+ * equals the reference with level_caps[l] = #{ent > tau}).  out_sizes gets
+ * the pool length per level. */
+int fc_pool_build(fc_ctx* ctx, const int32_t strides[4], const int64_t caps[4],
+                  const double taus[4], const int32_t use_tau[4], int64_t out_sizes[4]);
+/* Replace one level's pool by explicit decimated tiles (E x B x B uint8). */
+int fc_pool_set_level(fc_ctx* ctx, int level, int64_t count, const uint8_t* tiles);
+int fc_pool_size(fc_ctx* ctx, int level, int64_t* out_count);
+/* Origins in rank order, interleaved (x, y) as uint16 -- the stream header. */
+int fc_pool_coords(fc_ctx* ctx, int level, uint16_t* xy);
+/* Inspection of the survivors (any pointer may be NULL). */
+int fc_pool_entries(fc_ctx* ctx, int level, double* entropy, uint8_t* tiles, double* means,
+                    double* cnorm);
+
+/* Quantised candidate operands for a level (matcher.py:132-159).
+ * baseline = 0: proposed mode rint(s*(d - mean)); 1: rint(s*d).
+ * path: FC_PATH_AUTO / FC_PATH_EXACT / FC_PATH_TENSOR. */
+int fc_level_prepare(fc_ctx* ctx, int level, int baseline, const double* svals, int32_t s_count,
+                     int32_t path);
+
+/* Match ranges at `level` whose origins are (x, y) int32 pairs: best error,
+ * flat candidate index (e*8 + iso)*S + si, and exact range mean per origin
+ * (codec.py:185-193).  Requires fc_level_prepare for the level. */
+int fc_match_level(fc_ctx* ctx, int level, const int32_t* origins_xy, int64_t count,
+                   int64_t* out_err, int64_t* out_idx, double* out_rmean);
+
+/* Match explicit range tiles (uint8 [count][B*B], row-major per tile) --
+ * matcher.py:162 scan_tiles(tiles, candidate_set). */
+int fc_match_tiles(fc_ctx* ctx, int level, const uint8_t* tiles, int64_t count, int64_t* out_err,
+                   int64_t* out_idx, double* out_rmean);
+
+/* Kernel-level drop-in for _scan.py:14 with the reference's host layout:
+ * ranges int16 [M, n], rmeans f64 [M], q int16 [E*8*S, n] (isometry copies),
+ * dmeans f64 [E], svals f64 [S].  Exact CUDA-core path; for parity tests. */
+int fc_scan_candidates(fc_ctx* ctx, const int16_t* ranges, const double* rmeans, int64_t M,
+                       int32_t n, const int16_t* q, const double* dmeans, int64_t E,
+                       const double* svals, int32_t s_count, int32_t baseline, int64_t* out_err,
+                       int64_t* out_idx);
+
+int fc_last_stats(fc_ctx* ctx, fc_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FRACODEC_B200_H_ */

@@ -1,0 +1,264 @@
+"""ctypes binding of libfracodec_b200.so (include/fracodec_b200.h).
+
+The product path has no CPU fallback: if the library is missing or no sm_100
+device is visible, every device entry point raises DeviceUnavailableError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_lib", "libfracodec_b200.so")
+
+FC_OK = 0
+FC_ERR_CUDA = 1
+FC_ERR_ARG = 2
+FC_ERR_POOL_CONFIG = 3
+FC_ERR_EMPTY_POOL = 4
+FC_ERR_TILE_SIZE = 5
+FC_ERR_DIMS = 6
+FC_ERR_NO_DEVICE = 7
+FC_ERR_STATE = 8
+
+PATH_AUTO, PATH_EXACT, PATH_TENSOR = 0, 1, 2
+
+
+class DeviceUnavailableError(RuntimeError):
+    """The CUDA library or an sm_100 device is not available (no CPU fallback)."""
+
+
+class DeviceError(RuntimeError):
+    """A CUDA runtime failure inside the native library."""
+
+
+class FcStats(ctypes.Structure):
+    _fields_ = [
+        ("comparisons", ctypes.c_int64),
+        ("ranges", ctypes.c_int64),
+        ("columns", ctypes.c_int64),
+        ("path", ctypes.c_int32),
+        ("kernel_launches", ctypes.c_int32),
+        ("scan_ms", ctypes.c_float),
+        ("main_ms", ctypes.c_float),
+        ("fix_ms", ctypes.c_float),
+        ("fix_pairs", ctypes.c_int64),
+    ]
+
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+
+_SIGNATURES = {
+    "fc_version": ([], ctypes.c_int),
+    "fc_ctx_create": ([ctypes.c_int, ctypes.POINTER(_P)], ctypes.c_int),
+    "fc_ctx_destroy": ([_P], None),
+    "fc_last_error": ([_P], ctypes.c_char_p),
+    "fc_synchronize": ([_P], ctypes.c_int),
+    "fc_set_device_io": ([_P, ctypes.c_int], ctypes.c_int),
+    "fc_set_entropy_lut": ([_P, ctypes.c_int, _P], ctypes.c_int),
+    "fc_set_image": ([_P, _P, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+    "fc_pool_build": ([_P, _P, _P, _P, _P, _P], ctypes.c_int),
+    "fc_pool_set_level": ([_P, ctypes.c_int, _I64, _P], ctypes.c_int),
+    "fc_pool_size": ([_P, ctypes.c_int, _P], ctypes.c_int),
+    "fc_pool_coords": ([_P, ctypes.c_int, _P], ctypes.c_int),
+    "fc_pool_entries": ([_P, ctypes.c_int, _P, _P, _P, _P], ctypes.c_int),
+    "fc_level_prepare": ([_P, ctypes.c_int, ctypes.c_int, _P, _I32, _I32], ctypes.c_int),
+    "fc_match_level": ([_P, ctypes.c_int, _P, _I64, _P, _P, _P], ctypes.c_int),
+    "fc_match_tiles": ([_P, ctypes.c_int, _P, _I64, _P, _P, _P], ctypes.c_int),
+    "fc_scan_candidates": ([_P, _P, _P, _I64, _I32, _P, _P, _I64, _P, _I32, _I32, _P, _P],
+                           ctypes.c_int),
+    "fc_last_stats": ([_P, ctypes.POINTER(FcStats)], ctypes.c_int),
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library():
+    """Load the shared library; raise loudly if it is absent."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise DeviceUnavailableError(
+                f"{LIB_PATH} is missing: run `python -m paper_1502_00324_b200.build` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+        return lib
+
+
+def exported_symbols():
+    return list(_SIGNATURES)
+
+
+def _ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def entropy_lut(n: int) -> np.ndarray:
+    """terms[k-1] = (k/n) * log(k/n) evaluated by this host's numpy with the
+    same array operations pool.py:90-91 applies, so the device reproduces the
+    reference's float64 entropy bits exactly."""
+    p = np.arange(1, n + 1, dtype=np.int64) / n
+    return np.ascontiguousarray(p * np.log(p), dtype=np.float64)
+
+
+class Context:
+    """One fc_ctx: a CUDA stream plus device-resident image, pools and operands."""
+
+    def __init__(self, device: int = 0):
+        from .errors import raise_for_status  # local import (cycle-free)
+
+        self._raise = raise_for_status
+        self.lib = load_library()
+        h = ctypes.c_void_p()
+        rc = self.lib.fc_ctx_create(int(device), ctypes.byref(h))
+        if rc == FC_ERR_NO_DEVICE:
+            raise DeviceUnavailableError("no sm_100 CUDA device visible (no CPU fallback)")
+        if rc != FC_OK:
+            raise DeviceError(f"fc_ctx_create failed with status {rc}")
+        self.handle = h
+        self.device = device
+        for n in (16, 64, 256, 1024):
+            lut = entropy_lut(n)
+            self.check(self.lib.fc_set_entropy_lut(self.handle, n, _ptr(lut)))
+
+    def check(self, rc: int):
+        if rc != FC_OK:
+            msg = self.lib.fc_last_error(self.handle)
+            self._raise(rc, msg.decode() if msg else "")
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.fc_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- thin wrappers -----------------------------------------------------
+    def set_image(self, pixels: np.ndarray):
+        a = np.ascontiguousarray(pixels, dtype=np.uint8)
+        self.check(self.lib.fc_set_image(self.handle, _ptr(a), a.shape[1], a.shape[0]))
+
+    def set_image_device(self, dev_ptr: int, width: int, height: int):
+        self.check(self.lib.fc_set_device_io(self.handle, 1))
+        try:
+            self.check(self.lib.fc_set_image(self.handle, ctypes.c_void_p(dev_ptr), width, height))
+        finally:
+            self.check(self.lib.fc_set_device_io(self.handle, 0))
+
+    def pool_build(self, strides, caps, taus, use_tau):
+        s = np.asarray(strides, dtype=np.int32)
+        c = np.asarray(caps, dtype=np.int64)
+        t = np.asarray(taus, dtype=np.float64)
+        u = np.asarray(use_tau, dtype=np.int32)
+        out = np.zeros(4, dtype=np.int64)
+        self.check(self.lib.fc_pool_build(self.handle, _ptr(s), _ptr(c), _ptr(t), _ptr(u), _ptr(out)))
+        return tuple(int(v) for v in out)
+
+    def pool_set_level(self, level: int, tiles: np.ndarray):
+        t = np.ascontiguousarray(tiles, dtype=np.uint8)
+        self.check(self.lib.fc_pool_set_level(self.handle, level, t.shape[0] if t.size else 0,
+                                              _ptr(t) if t.size else None))
+
+    def pool_coords(self, level: int, count: int) -> np.ndarray:
+        out = np.empty((count, 2), dtype=np.uint16)
+        if count:
+            self.check(self.lib.fc_pool_coords(self.handle, level, _ptr(out)))
+        return out
+
+    def pool_entries(self, level: int, count: int, side: int, want=("entropy", "tiles", "means", "cnorm")):
+        ent = np.empty(count) if "entropy" in want else None
+        tiles = np.empty((count, side, side), dtype=np.uint8) if "tiles" in want else None
+        means = np.empty(count) if "means" in want else None
+        cnorm = np.empty(count) if "cnorm" in want else None
+        if count:
+            self.check(self.lib.fc_pool_entries(self.handle, level, _ptr(ent), _ptr(tiles),
+                                                _ptr(means), _ptr(cnorm)))
+        return ent, tiles, means, cnorm
+
+    def level_prepare(self, level: int, baseline: bool, svals, path: int = PATH_AUTO):
+        s = np.ascontiguousarray(svals, dtype=np.float64)
+        self.check(self.lib.fc_level_prepare(self.handle, level, int(bool(baseline)), _ptr(s),
+                                             len(s), int(path)))
+
+    def match_level(self, level: int, origins):
+        o = np.ascontiguousarray(np.asarray(origins, dtype=np.int32).reshape(-1, 2))
+        M = o.shape[0]
+        err = np.empty(M, dtype=np.int64)
+        idx = np.empty(M, dtype=np.int64)
+        rmean = np.empty(M, dtype=np.float64)
+        self.check(self.lib.fc_match_level(self.handle, level, _ptr(o), M, _ptr(err), _ptr(idx),
+                                           _ptr(rmean)))
+        return err, idx, rmean
+
+    def match_tiles(self, level: int, tiles: np.ndarray):
+        t = np.ascontiguousarray(tiles, dtype=np.uint8)
+        M = t.shape[0]
+        err = np.empty(M, dtype=np.int64)
+        idx = np.empty(M, dtype=np.int64)
+        rmean = np.empty(M, dtype=np.float64)
+        self.check(self.lib.fc_match_tiles(self.handle, level, _ptr(t), M, _ptr(err), _ptr(idx),
+                                           _ptr(rmean)))
+        return err, idx, rmean
+
+    def match_level_device(self, level: int, origins_ptr: int, count: int, err_ptr: int,
+                           idx_ptr: int, rmean_ptr: int):
+        self.check(self.lib.fc_set_device_io(self.handle, 1))
+        try:
+            self.check(self.lib.fc_match_level(self.handle, level, ctypes.c_void_p(origins_ptr), count,
+                                               ctypes.c_void_p(err_ptr), ctypes.c_void_p(idx_ptr),
+                                               ctypes.c_void_p(rmean_ptr)))
+        finally:
+            self.check(self.lib.fc_set_device_io(self.handle, 0))
+
+    def scan_candidates(self, ranges, rmeans, q, dmeans, svals, baseline):
+        r = np.ascontiguousarray(ranges, dtype=np.int16)
+        rm = np.ascontiguousarray(rmeans, dtype=np.float64)
+        qq = np.ascontiguousarray(q, dtype=np.int16)
+        dm = np.ascontiguousarray(dmeans, dtype=np.float64)
+        sv = np.ascontiguousarray(svals, dtype=np.float64)
+        M, n = r.shape
+        err = np.empty(M, dtype=np.int64)
+        idx = np.empty(M, dtype=np.int64)
+        self.check(self.lib.fc_scan_candidates(self.handle, _ptr(r), _ptr(rm), M, n, _ptr(qq),
+                                               _ptr(dm), len(dm), _ptr(sv), len(sv),
+                                               int(bool(baseline)), _ptr(err), _ptr(idx)))
+        return err, idx
+
+    def stats(self) -> FcStats:
+        st = FcStats()
+        self.check(self.lib.fc_last_stats(self.handle, ctypes.byref(st)))
+        return st
+
+    def synchronize(self):
+        self.check(self.lib.fc_synchronize(self.handle))
+
+
+_default = {}
+_default_lock = threading.Lock()
+
+
+def default_context(device: int = 0) -> Context:
+    with _default_lock:
+        ctx = _default.get(device)
+        if ctx is None:
+            ctx = Context(device)
+            _default[device] = ctx
+        return ctx

@@ -1,0 +1,288 @@
+"""Four-step quadtree encoder (device search) and the iterative decoder.
+
+``encode(image, config)`` keeps the reference's entry point and output
+(codec.py:171-254 there): pool construction and every level's exhaustive
+range-domain search run on the B200 through the C ABI; the host keeps the
+quadtree bookkeeping (split rule codec.py:132-141, depth-first leaf order
+codec.py:145-161) and assembles the records and the FRAK stream.
+
+``decode`` is the reference's attractor iteration (codec.py:269-363) on the
+host; it is outside the accelerated path this round and serves the decoded
+PSNR parity check.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+from numpy.lib.stride_tricks import sliding_window_view
+
+from . import _native
+from .image import GrayImage, apply_isometry, decimate_tile
+from .matcher import BASELINE, PATHS, PROPOSED, SPolicy
+from .pool import LEVEL_RANGE_SIDES, CoordTable, PoolParams, build_pool
+from .stream import CompressedStream, MatchRecord, header_bytes, iter_leaves
+
+TOP_SIDE = 16
+
+
+@dataclass(frozen=True)
+class EncoderConfig:
+    pool: PoolParams
+    policy: SPolicy = field(default_factory=SPolicy)
+    thresholds: tuple = (8.0, 8.0, 8.0)
+    threads: int | None = None  # accepted for interface parity; the search runs on the GPU
+    path: str = "auto"  # "auto" | "exact" | "tensor" (device kernel choice)
+
+    def __post_init__(self):
+        if len(self.thresholds) != 3 or any(t <= 0 for t in self.thresholds):
+            raise ValueError("thresholds must be 3 positive RMS values")
+        object.__setattr__(self, "thresholds", tuple(float(t) for t in self.thresholds))
+        if self.path not in PATHS:
+            raise ValueError(f"path must be one of {sorted(PATHS)}")
+
+
+@dataclass
+class EncodeReport:
+    width: int
+    height: int
+    mode: str
+    pool_cap: int
+    pool_sizes: tuple
+    strides: tuple
+    thresholds: tuple
+    step_blocks: tuple
+    record_count: int
+    collage_ssd: int
+    payload_bits: int
+    header_bytes: int
+    file_bytes: int
+    bpp_payload: float
+    bpp_total: float
+    comp_ratio_payload: float
+    comp_ratio_total: float
+    pool_time_s: float
+    encode_time_s: float
+    comparisons: int = 0
+    scan_device_ms: float = 0.0
+
+    def to_lines(self) -> list:
+        rows = [
+            ("width", self.width), ("height", self.height), ("mode", self.mode),
+            ("pool_cap", self.pool_cap),
+            ("pool_sizes", ",".join(str(v) for v in self.pool_sizes)),
+            ("strides", ",".join(str(v) for v in self.strides)),
+            ("thresholds", ",".join(f"{t:g}" for t in self.thresholds)),
+            ("step1_blocks", self.step_blocks[0]), ("step2_blocks", self.step_blocks[1]),
+            ("step3_blocks", self.step_blocks[2]), ("step4_blocks", self.step_blocks[3]),
+            ("records", self.record_count), ("collage_ssd", self.collage_ssd),
+            ("payload_bits", self.payload_bits), ("header_bytes", self.header_bytes),
+            ("file_bytes", self.file_bytes), ("bpp_payload", f"{self.bpp_payload:.6f}"),
+            ("bpp_total", f"{self.bpp_total:.6f}"),
+            ("comp_ratio_payload", f"{self.comp_ratio_payload:.4f}"),
+            ("comp_ratio_total", f"{self.comp_ratio_total:.4f}"),
+            ("pool_time_s", f"{self.pool_time_s:.3f}"),
+            ("encode_time_s", f"{self.encode_time_s:.3f}"),
+        ]
+        return [f"{k}={v}" for k, v in rows]
+
+
+def _quadtree(width: int, height: int, thresholds, match_fn):
+    """Vectorised level loop with the reference's split rule and DFS order.
+
+    match_fn(level, origins[int32 M,2]) -> errs.  Returns (per-level origin
+    arrays, leaves as (level, j) arrays in depth-first order).
+    """
+    ys, xs = np.mgrid[0:height:TOP_SIDE, 0:width:TOP_SIDE]
+    origins = {1: np.stack([xs.ravel(), ys.ravel()], axis=1).astype(np.int32)}
+    # DFS sort code: top index * 64 + d1 * 16 + d2 * 4 + d3 (children TL, TR, BL, BR = 0..3)
+    codes = {1: np.arange(origins[1].shape[0], dtype=np.int64) * 64}
+    leaf_level, leaf_j, leaf_code = [], [], []
+    for level in (1, 2, 3, 4):
+        o = origins.get(level)
+        if o is None or o.shape[0] == 0:
+            break
+        errs = np.asarray(match_fn(level, o))
+        side = LEVEL_RANGE_SIDES[level - 1]
+        if level == 4:
+            split = np.zeros(o.shape[0], dtype=bool)
+        else:
+            split = errs > thresholds[level - 1] ** 2 * side * side
+        keep = np.nonzero(~split)[0]
+        leaf_level.append(np.full(keep.shape[0], level, dtype=np.int64))
+        leaf_j.append(keep)
+        leaf_code.append(codes[level][keep])
+        par = np.nonzero(split)[0]
+        if par.shape[0]:
+            h = side // 2
+            offs = np.array([[0, 0], [h, 0], [0, h], [h, h]], dtype=np.int32)
+            origins[level + 1] = (o[par][:, None, :] + offs[None]).reshape(-1, 2)
+            weight = 4 ** (3 - level)
+            codes[level + 1] = (codes[level][par][:, None]
+                                + np.arange(4, dtype=np.int64)[None] * weight).reshape(-1)
+    lv = np.concatenate(leaf_level)
+    jj = np.concatenate(leaf_j)
+    cc = np.concatenate(leaf_code)
+    order = np.argsort(cc, kind="stable")
+    return origins, lv[order], jj[order]
+
+
+def run_quadtree(width: int, height: int, thresholds, match_level):
+    """Reference-compatible driver (codec.py:114-161): match_level(level,
+    origins as a list of (x, y)) -> errs; returns leaves (level, x, y, j)."""
+    origins, lv, jj = _quadtree(
+        width, height, thresholds,
+        lambda level, o: match_level(level, [(int(x), int(y)) for x, y in o]))
+    leaves = [(int(level), int(origins[level][j, 0]), int(origins[level][j, 1]), int(j))
+              for level, j in zip(lv, jj)]
+    covered = sum(LEVEL_RANGE_SIDES[level - 1] ** 2 for level, _, _, _ in leaves)
+    assert covered == width * height, "leaf footprints must tile the image"
+    return leaves
+
+
+def encode(image: GrayImage, config: EncoderConfig, context=None):
+    """Compress an image whose sides are multiples of 16 -> (CompressedStream, EncodeReport)."""
+    if image.width % 16 or image.height % 16:
+        raise ValueError(f"dimensions not multiple of 16: {image.width}x{image.height}")
+    t_start = time.perf_counter()
+    ctx = context if context is not None else _native.default_context()
+    pool = build_pool(image, config.pool, context=ctx)
+    pool_time = time.perf_counter() - t_start
+    policy = config.policy
+    baseline = policy.mode == BASELINE
+    path = PATHS[config.path]
+    scans = {}
+    comparisons = 0
+    scan_ms = 0.0
+
+    def match_fn(level, o):
+        nonlocal comparisons, scan_ms
+        if pool.size(level) == 0:
+            from .errors import EmptyPoolError
+
+            raise EmptyPoolError(f"no domain entries at level {level}")
+        ctx.level_prepare(level, baseline, policy.s_set(level), path)
+        err, idx, rmean = ctx.match_level(level, o)
+        st = ctx.stats()
+        comparisons += int(st.comparisons)
+        scan_ms += float(st.scan_ms)
+        scans[level] = (err, idx, rmean)
+        return err
+
+    origins, leaf_lv, leaf_j = _quadtree(image.width, image.height, config.thresholds, match_fn)
+
+    n = leaf_lv.shape[0]
+    steps = leaf_lv
+    offs = np.empty(n, dtype=np.int64)
+    isos = np.empty(n, dtype=np.int64)
+    addrs = np.empty(n, dtype=np.int64)
+    sidx = np.empty(n, dtype=np.int64)
+    errs = np.empty(n, dtype=np.int64)
+    for level in (1, 2, 3, 4):
+        sel = np.nonzero(leaf_lv == level)[0]
+        if sel.shape[0] == 0:
+            continue
+        err, idx, rmean = scans[level]
+        j = leaf_j[sel]
+        S = len(policy.s_set(level))
+        e, rem = np.divmod(idx[j], 8 * S)
+        iso, si = np.divmod(rem, S)
+        if baseline:
+            sv = np.asarray(policy.s_set(level), dtype=np.float64)
+            dm = pool.means(level)
+            o = np.clip(np.rint(rmean[j] - sv[si] * dm[e]), 0, 255).astype(np.int64)
+        else:
+            o = np.rint(rmean[j]).astype(np.int64)
+        offs[sel], isos[sel], addrs[sel], sidx[sel], errs[sel] = o, iso, e, si, err[j]
+    records = tuple(MatchRecord(int(a), int(b), int(c), int(d), int(f))
+                    for a, b, c, d, f in zip(steps, offs, isos, addrs, sidx))
+    stream = CompressedStream(
+        width=image.width, height=image.height, mode=policy.mode, strides=pool.params.strides,
+        s_sets=tuple(policy.s_set(level) for level in (1, 2, 3, 4)),
+        pools=tuple(pool.coords(level) for level in (1, 2, 3, 4)), records=records)
+    encode_time = time.perf_counter() - t_start
+    pixels = image.width * image.height
+    payload = stream.payload_bits()
+    head = header_bytes(stream)
+    file_bytes = head + (payload + 7) // 8
+    step_blocks = tuple(int((leaf_lv == lv).sum()) for lv in (1, 2, 3, 4))
+    report = EncodeReport(
+        width=image.width, height=image.height, mode=policy.mode, pool_cap=config.pool.pool_cap,
+        pool_sizes=pool.sizes, strides=pool.params.strides, thresholds=config.thresholds,
+        step_blocks=step_blocks, record_count=n, collage_ssd=int(errs.sum()),
+        payload_bits=payload, header_bytes=head, file_bytes=file_bytes,
+        bpp_payload=payload / pixels, bpp_total=file_bytes * 8 / pixels,
+        comp_ratio_payload=pixels * 8 / payload if payload else float("inf"),
+        comp_ratio_total=pixels / file_bytes, pool_time_s=pool_time, encode_time_s=encode_time,
+        comparisons=comparisons, scan_device_ms=scan_ms)
+    return stream, report
+
+
+# ---------------------------------------------------------------------------
+# decoder (host; codec.py:257-363 semantics)
+# ---------------------------------------------------------------------------
+
+def _plans(stream: CompressedStream):
+    rows = {1: [], 2: [], 3: [], 4: []}
+    for rec, x, y, _side in iter_leaves(stream):
+        rows[rec.step].append((rec.domain_address, rec.isometry, rec.s_index, rec.offset, x, y))
+    plans = []
+    for level in (1, 2, 3, 4):
+        if not rows[level]:
+            continue
+        a = np.array(rows[level], dtype=np.int64)
+        b = LEVEL_RANGE_SIDES[level - 1]
+        coords = np.asarray(CoordTable(stream.pools[level - 1]).array)
+        dom = coords[a[:, 0]]
+        svals = np.asarray(stream.s_sets[level - 1], dtype=np.float64)[a[:, 2]]
+        span = np.arange(b)
+        scatter = ((a[:, 5][:, None, None] + span[None, :, None]) * stream.width
+                   + a[:, 4][:, None, None] + span[None, None, :]).ravel()
+        groups = [(iso, np.nonzero(a[:, 1] == iso)[0]) for iso in range(8)]
+        plans.append((2 * b, dom[:, 0], dom[:, 1], [g for g in groups if g[1].size], svals,
+                      a[:, 3].astype(np.int32), scatter, b * b))
+    return plans
+
+
+def _collage_pass(cur: np.ndarray, plans, proposed: bool) -> np.ndarray:
+    out = np.empty_like(cur)
+    for dside, dx, dy, groups, svals, offs, scatter, n in plans:
+        win = sliding_window_view(cur, (dside, dside))
+        dec = decimate_tile(win[dy, dx])
+        tiles = np.empty_like(dec)
+        for iso, idx in groups:
+            tiles[idx] = apply_isometry(dec[idx], iso)
+        if proposed:
+            means = tiles.reshape(tiles.shape[0], -1).astype(np.int64).sum(axis=1) / n
+            q = np.rint(svals[:, None, None] * (tiles - means[:, None, None]))
+        else:
+            q = np.rint(svals[:, None, None] * tiles.astype(np.float64))
+        v = q.astype(np.int32) + offs[:, None, None]
+        np.clip(v, 0, 255, out=v)
+        out.flat[scatter] = v.ravel()
+    return out
+
+
+def decode_trace(stream: CompressedStream, iterations: int = 15, tolerance: int = 0):
+    if iterations < 1:
+        raise ValueError("iterations must be >= 1")
+    if tolerance < 0:
+        raise ValueError("tolerance must be >= 0")
+    plans = _plans(stream)
+    proposed = stream.mode == PROPOSED
+    cur = np.full((stream.height, stream.width), 128, dtype=np.uint8)
+    deltas = []
+    for _ in range(iterations):
+        new = _collage_pass(cur, plans, proposed)
+        delta = int(np.abs(new.astype(np.int16) - cur.astype(np.int16)).max())
+        cur = new
+        deltas.append(delta)
+        if delta <= tolerance:
+            break
+    return GrayImage(cur), deltas
+
+
+def decode(stream: CompressedStream, iterations: int = 15, tolerance: int = 0) -> GrayImage:
+    return decode_trace(stream, iterations, tolerance)[0]

@@ -1,0 +1,350 @@
+// C ABI of fracodec_b200 (declared in include/fracodec_b200.h).
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "fc_internal.cuh"
+
+namespace fcb {
+
+int set_error(Ctx* c, int code, const std::string& msg) {
+  if (c) {
+    c->st.code = code;
+    c->st.msg = msg;
+  }
+  return code;
+}
+
+int cuda_check(Ctx* c, cudaError_t e, const char* what) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s", cudaGetErrorName(e), cudaGetErrorString(e),
+           what);
+  return set_error(c, FC_ERR_CUDA, buf);
+}
+
+int lut_slot(int n) { return n == 16 ? 0 : n == 64 ? 1 : n == 256 ? 2 : n == 1024 ? 3 : -1; }
+
+namespace {
+
+int check_level(Ctx* c, int level) {
+  if (level < 1 || level > kLevels) return set_error(c, FC_ERR_ARG, "level must be 1..4");
+  return FC_OK;
+}
+
+int level_ready(Ctx* c, int level) {
+  FC_TRY(check_level(c, level));
+  Level& L = c->lv[level - 1];
+  if (L.n == 0) return set_error(c, FC_ERR_STATE, "pool not built");
+  return FC_OK;
+}
+
+}  // namespace
+}  // namespace fcb
+
+using namespace fcb;
+
+struct fc_ctx : public Ctx {};
+
+extern "C" {
+
+int fc_version(void) { return 1; }
+
+int fc_ctx_create(int device, fc_ctx** out) {
+  if (!out) return FC_ERR_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return FC_ERR_NO_DEVICE;
+  if (device < 0 || device >= ndev) return FC_ERR_ARG;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return FC_ERR_CUDA;
+  if (prop.major != 10) return FC_ERR_NO_DEVICE;  // sm_100a build only
+  if (cudaSetDevice(device) != cudaSuccess) return FC_ERR_CUDA;
+  fc_ctx* c = new (std::nothrow) fc_ctx();
+  if (!c) return FC_ERR_ARG;
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
+      cudaEventCreate(&c->ev2) != cudaSuccess) {
+    delete c;
+    return FC_ERR_CUDA;
+  }
+  for (int i = 0; i < kLevels; ++i) {
+    c->lv[i].side = kRangeSide[i];
+    c->lv[i].n = 0;
+  }
+  *out = c;
+  return FC_OK;
+}
+
+void fc_ctx_destroy(fc_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  DevBuf* bufs[] = {&c->img, &c->ent_scratch, &c->key_in, &c->key_out, &c->val_in, &c->val_out,
+                    &c->cub_tmp, &c->count_buf, &c->origins, &c->rtiles, &c->rmean, &c->roff,
+                    &c->rsq, &c->keys, &c->out_err, &c->out_idx, &c->fix_rows, &c->fix_cols,
+                    &c->fix_jobs, &c->svals_dev, &c->iso_inv};
+  for (DevBuf* b : bufs) b->release();
+  for (auto& b : c->lut) b.release();
+  for (auto& L : c->lv) {
+    DevBuf* lb[] = {&L.xy, &L.ent, &L.tiles, &L.sum, &L.sumsq, &L.mean, &L.cnorm, &L.qbase,
+                    &L.tc.b_tiles, &L.tc.col_meta, &L.tc.tile_meta, &L.tc.col_stats,
+                    &L.tc.reach_low, &L.tc.reach_high};
+    for (DevBuf* b : lb) b->release();
+  }
+  cudaEventDestroy(c->ev0);
+  cudaEventDestroy(c->ev1);
+  cudaEventDestroy(c->ev2);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* fc_last_error(fc_ctx* c) { return c ? c->st.msg.c_str() : "null context"; }
+
+int fc_synchronize(fc_ctx* c) {
+  cudaSetDevice(c->device);
+  FC_CUDA(c, cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+int fc_set_device_io(fc_ctx* c, int device_io) {
+  c->device_io = device_io ? 1 : 0;
+  return FC_OK;
+}
+
+int fc_set_entropy_lut(fc_ctx* c, int n, const double* terms) {
+  cudaSetDevice(c->device);
+  const int slot = lut_slot(n);
+  if (slot < 0 || !terms) return set_error(c, FC_ERR_ARG, "LUT size must be 16/64/256/1024");
+  FC_CUDA(c, c->lut[slot].reserve(n * 8));
+  FC_CUDA(c, cudaMemcpy(c->lut[slot].ptr, terms, n * 8, cudaMemcpyHostToDevice));
+  c->lut_set[slot] = true;
+  return FC_OK;
+}
+
+int fc_set_image(fc_ctx* c, const uint8_t* pixels, int width, int height) {
+  cudaSetDevice(c->device);
+  if (width < 1 || height < 1 || !pixels) return set_error(c, FC_ERR_ARG, "bad image");
+  if (width > 65535 || height > 65535)
+    return set_error(c, FC_ERR_ARG, "image sides must fit the u16 stream coordinates");
+  c->width = width;
+  c->height = height;
+  if (c->device_io) {
+    c->img_ptr = pixels;
+  } else {
+    FC_CUDA(c, c->img.reserve((size_t)width * height));
+    FC_CUDA(c, cudaMemcpyAsync(c->img.ptr, pixels, (size_t)width * height, cudaMemcpyHostToDevice,
+                               c->stream));
+    c->img_ptr = c->img.as<uint8_t>();
+  }
+  for (auto& L : c->lv) {
+    L.n = 0;
+    L.count = 0;
+    L.prepared = false;
+    L.tc.ready = false;
+  }
+  return FC_OK;
+}
+
+int fc_pool_build(fc_ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
+                  const int32_t use_tau[4], int64_t out_sizes[4]) {
+  cudaSetDevice(c->device);
+  const double zero_taus[4] = {0, 0, 0, 0};
+  const int32_t no_tau[4] = {0, 0, 0, 0};
+  return pool_build(c, strides, caps, taus ? taus : zero_taus, use_tau ? use_tau : no_tau,
+                    out_sizes);
+}
+
+int fc_pool_set_level(fc_ctx* c, int level, int64_t count, const uint8_t* tiles) {
+  cudaSetDevice(c->device);
+  FC_TRY(check_level(c, level));
+  if (count < 0 || (count > 0 && !tiles)) return set_error(c, FC_ERR_ARG, "bad tiles");
+  return pool_set_level(c, level, count, tiles);
+}
+
+int fc_pool_size(fc_ctx* c, int level, int64_t* out_count) {
+  FC_TRY(level_ready(c, level));
+  *out_count = c->lv[level - 1].count;
+  return FC_OK;
+}
+
+int fc_pool_coords(fc_ctx* c, int level, uint16_t* xy) {
+  cudaSetDevice(c->device);
+  FC_TRY(level_ready(c, level));
+  Level& L = c->lv[level - 1];
+  if (L.count == 0) return FC_OK;
+  std::vector<uint32_t> h(L.count);
+  FC_CUDA(c, cudaMemcpyAsync(h.data(), L.xy.ptr, L.count * 4, cudaMemcpyDeviceToHost, c->stream));
+  FC_CUDA(c, cudaStreamSynchronize(c->stream));
+  for (int64_t i = 0; i < L.count; ++i) {
+    xy[2 * i] = (uint16_t)(h[i] & 0xffff);
+    xy[2 * i + 1] = (uint16_t)(h[i] >> 16);
+  }
+  return FC_OK;
+}
+
+int fc_pool_entries(fc_ctx* c, int level, double* entropy, uint8_t* tiles, double* means,
+                    double* cnorm) {
+  cudaSetDevice(c->device);
+  FC_TRY(level_ready(c, level));
+  Level& L = c->lv[level - 1];
+  if (L.count == 0) return FC_OK;
+  if (entropy)
+    FC_CUDA(c, cudaMemcpyAsync(entropy, L.ent.ptr, L.count * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (tiles)
+    FC_CUDA(c, cudaMemcpyAsync(tiles, L.tiles.ptr, L.count * L.n, cudaMemcpyDeviceToHost, c->stream));
+  if (means)
+    FC_CUDA(c, cudaMemcpyAsync(means, L.mean.ptr, L.count * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (cnorm)
+    FC_CUDA(c, cudaMemcpyAsync(cnorm, L.cnorm.ptr, L.count * 8, cudaMemcpyDeviceToHost, c->stream));
+  FC_CUDA(c, cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+int fc_level_prepare(fc_ctx* c, int level, int baseline, const double* svals, int32_t s_count,
+                     int32_t path) {
+  cudaSetDevice(c->device);
+  FC_TRY(level_ready(c, level));
+  if (s_count < 1 || s_count > kMaxS || !svals)
+    return set_error(c, FC_ERR_ARG, "s set must have 1..16 values");
+  for (int i = 0; i < s_count; ++i)
+    if (!(svals[i] >= 0.0 && svals[i] <= 1.0))
+      return set_error(c, FC_ERR_ARG, "s values must lie in [0, 1]");
+  Level& L = c->lv[level - 1];
+  bool same = L.prepared && L.baseline == baseline && L.s_count == s_count;
+  for (int i = 0; same && i < s_count; ++i) same = L.svals[i] == svals[i];
+  if (same && (path == FC_PATH_AUTO || path == L.path)) return FC_OK;
+  if (L.count == 0) {
+    char buf[64];
+    snprintf(buf, sizeof buf, "no domain entries at level %d", level);
+    return set_error(c, FC_ERR_EMPTY_POOL, buf);
+  }
+  L.baseline = baseline ? 1 : 0;
+  L.s_count = s_count;
+  for (int i = 0; i < s_count; ++i) L.svals[i] = svals[i];
+  L.prepared = false;
+  L.tc.ready = false;
+  FC_TRY(level_prepare_exact(c, L));
+  int use = FC_PATH_EXACT;
+  const bool tc_ok = !L.baseline && L.n >= 16;
+  if (path == FC_PATH_TENSOR && !tc_ok)
+    return set_error(c, FC_ERR_ARG, "tensor path needs proposed mode and B >= 4");
+  if (path == FC_PATH_TENSOR || (path == FC_PATH_AUTO && tc_ok)) {
+    const int r = level_prepare_tc(c, L);
+    if (r == FC_OK) {
+      use = FC_PATH_TENSOR;
+    } else if (path == FC_PATH_TENSOR) {
+      return r;
+    } else {
+      c->st = Status{};  // auto: keep the exact path
+    }
+  }
+  L.path = use;
+  L.prepared = true;
+  return FC_OK;
+}
+
+static int run_match(fc_ctx* c, Level& L, int64_t count, int64_t* out_err, int64_t* out_idx,
+                     double* out_rmean, bool device_out) {
+  FC_CUDA(c, c->keys.reserve(count * 8));
+  FC_CUDA(c, cudaMemsetAsync(c->keys.ptr, 0xff, count * 8, c->stream));
+  FC_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+  if (L.path == FC_PATH_TENSOR) {
+    FC_TRY(scan_tc(c, L, count, c->keys.as<uint64_t>()));
+  } else {
+    FC_TRY(scan_exact(c, L, count, nullptr, 0, nullptr, 0, c->keys.as<uint64_t>()));
+  }
+  FC_CUDA(c, cudaEventRecord(c->ev2, c->stream));
+  int64_t* d_err;
+  int64_t* d_idx;
+  if (device_out) {
+    d_err = out_err;
+    d_idx = out_idx;
+  } else {
+    FC_CUDA(c, c->out_err.reserve(count * 8));
+    FC_CUDA(c, c->out_idx.reserve(count * 8));
+    d_err = c->out_err.as<int64_t>();
+    d_idx = c->out_idx.as<int64_t>();
+  }
+  FC_TRY(decode_keys(c, c->keys.as<uint64_t>(), count, d_err, d_idx));
+  const cudaMemcpyKind kind = device_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (!device_out) {
+    FC_CUDA(c, cudaMemcpyAsync(out_err, d_err, count * 8, kind, c->stream));
+    FC_CUDA(c, cudaMemcpyAsync(out_idx, d_idx, count * 8, kind, c->stream));
+  }
+  if (out_rmean) FC_CUDA(c, cudaMemcpyAsync(out_rmean, c->rmean.ptr, count * 8, kind, c->stream));
+  FC_CUDA(c, cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev0, c->ev2);
+  c->stats.scan_ms = ms;
+  if (L.path != FC_PATH_TENSOR) c->stats.main_ms = ms;
+  return FC_OK;
+}
+
+static int begin_match(fc_ctx* c, int level, int64_t count) {
+  FC_TRY(level_ready(c, level));
+  Level& L = c->lv[level - 1];
+  if (L.count == 0) {
+    char buf[64];
+    snprintf(buf, sizeof buf, "no domain entries at level %d", level);
+    return set_error(c, FC_ERR_EMPTY_POOL, buf);
+  }
+  if (!L.prepared) return set_error(c, FC_ERR_STATE, "level not prepared");
+  if (count < 0) return set_error(c, FC_ERR_ARG, "negative range count");
+  c->stats = fc_stats{};
+  c->stats.ranges = count;
+  c->stats.columns = L.count * L.s_count;
+  c->stats.comparisons = count * L.count * 8 * L.s_count;
+  c->stats.path = L.path;
+  return FC_OK;
+}
+
+int fc_match_level(fc_ctx* c, int level, const int32_t* origins_xy, int64_t count, int64_t* out_err,
+                   int64_t* out_idx, double* out_rmean) {
+  cudaSetDevice(c->device);
+  FC_TRY(begin_match(c, level, count));
+  if (count == 0) return FC_OK;
+  Level& L = c->lv[level - 1];
+  if (!c->img_ptr) return set_error(c, FC_ERR_STATE, "no image set");
+  const int32_t* d_orig = origins_xy;
+  if (!c->device_io) {
+    for (int64_t i = 0; i < count; ++i) {
+      const int x = origins_xy[2 * i], y = origins_xy[2 * i + 1];
+      if (x < 0 || y < 0 || x + L.side > c->width || y + L.side > c->height)
+        return set_error(c, FC_ERR_ARG, "range origin outside the image");
+    }
+    FC_CUDA(c, c->origins.reserve(count * 8));
+    FC_CUDA(c, cudaMemcpyAsync(c->origins.ptr, origins_xy, count * 8, cudaMemcpyHostToDevice,
+                               c->stream));
+    d_orig = c->origins.as<int32_t>();
+  }
+  FC_TRY(gather_ranges(c, L, d_orig, count));
+  return run_match(c, L, count, out_err, out_idx, out_rmean, c->device_io != 0);
+}
+
+int fc_match_tiles(fc_ctx* c, int level, const uint8_t* tiles, int64_t count, int64_t* out_err,
+                   int64_t* out_idx, double* out_rmean) {
+  cudaSetDevice(c->device);
+  FC_TRY(begin_match(c, level, count));
+  if (count == 0) return FC_OK;
+  Level& L = c->lv[level - 1];
+  FC_TRY(load_ranges(c, L, tiles, count));
+  return run_match(c, L, count, out_err, out_idx, out_rmean, false);
+}
+
+int fc_scan_candidates(fc_ctx* c, const int16_t* ranges, const double* rmeans, int64_t M, int32_t n,
+                       const int16_t* q, const double* dmeans, int64_t E, const double* svals,
+                       int32_t s_count, int32_t baseline, int64_t* out_err, int64_t* out_idx) {
+  cudaSetDevice(c->device);
+  if (M < 0 || n < 1 || E < 0 || s_count < 1) return set_error(c, FC_ERR_ARG, "bad scan shape");
+  return scan_rows_dropin(c, ranges, rmeans, M, n, q, dmeans, E, svals, s_count, baseline, out_err,
+                          out_idx);
+}
+
+int fc_last_stats(fc_ctx* c, fc_stats* out) {
+  *out = c->stats;
+  return FC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,149 @@
+// Internal definitions shared by the fracodec_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "fracodec_b200.h"
+
+namespace fcb {
+
+constexpr int kLevels = 4;
+constexpr int kRangeSide[kLevels] = {16, 8, 4, 2};   // pool.py:20 LEVEL_RANGE_SIDES
+constexpr int kDomainSide[kLevels] = {32, 16, 8, 4}; // pool.py:21 LEVEL_DOMAIN_SIDES
+constexpr int kMaxS = 16;
+
+struct Status {
+  int code = FC_OK;
+  std::string msg;
+};
+
+// A growable device buffer.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaError_t reserve(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    size_t cap = want + want / 4 + 256;
+    cudaError_t e = cudaMalloc(&ptr, cap);
+    if (e == cudaSuccess) bytes = cap;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return reinterpret_cast<T*>(ptr); }
+};
+
+// Tensor-core operand set for one level (see fc_scan_tc.cu).
+struct TcOperands {
+  bool ready = false;
+  int planes = 1;        // int8 planes of q (1 or 2)
+  int kpad = 0;          // K bytes per row after plane concat + padding (multiple of 32)
+  int64_t ncols = 0;     // real columns E*S
+  int64_t ntiles = 0;    // 256-column tiles after per-group padding
+  DevBuf b_tiles;        // int8 [ntiles][kpad/16][32 groups][8][16]   (UMMA K-major, no swizzle)
+  DevBuf col_meta;       // int2 [ntiles*256]: {hq = floor(Q2/2), (par<<31) | col}
+  DevBuf tile_meta;      // int4 [ntiles]: {Q1, qmin_tile, qmax_tile, ncols_real}
+  DevBuf col_stats;      // int4 [ncols]: {Q1, Q2, qmin, qmax} (unsorted order)
+  DevBuf reach_low;      // int32 [ncols]: columns sorted by qmin ascending
+  DevBuf reach_high;     // int32 [ncols]: columns sorted by qmax descending
+  std::vector<int> low_qmin_sorted;   // host copy: qmin of reach_low order
+  std::vector<int> high_qmax_sorted;  // host copy: qmax of reach_high order
+};
+
+struct Level {
+  int side = 0;           // range side B
+  int n = 0;              // B*B
+  int stride = 0;
+  int64_t count = 0;      // pool length E
+  bool synthetic = false; // set via fc_pool_set_level
+  DevBuf xy;              // uint32 (x | y << 16), rank order
+  DevBuf ent;             // double
+  DevBuf tiles;           // uint8 [E][n] decimated
+  DevBuf sum;             // int32 [E]
+  DevBuf sumsq;           // int64 [E]
+  DevBuf mean;            // double [E]
+  DevBuf cnorm;           // double [E]
+  // prepared operands
+  bool prepared = false;
+  int baseline = 0;
+  int s_count = 0;
+  double svals[kMaxS] = {0};
+  int path = FC_PATH_EXACT;
+  DevBuf qbase;           // int16 [E*S][n] base operand (column = e*S + si)
+  TcOperands tc;
+};
+
+struct Ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  Status st;
+  int device_io = 0;
+  // image
+  int width = 0, height = 0;
+  DevBuf img;
+  const uint8_t* img_ptr = nullptr;  // img or adopted device pointer
+  // entropy LUTs for n = 16, 64, 256, 1024
+  DevBuf lut[4];
+  bool lut_set[4] = {false, false, false, false};
+  Level lv[kLevels];
+  // scratch
+  DevBuf ent_scratch, key_in, key_out, val_in, val_out, cub_tmp, count_buf;
+  DevBuf origins, rtiles, rmean, roff, rsq, keys, out_err, out_idx;
+  DevBuf fix_rows, fix_cols, fix_jobs, svals_dev;
+  DevBuf iso_inv;  // uint16 [4 sides][8][256] inverse isometry maps
+  bool iso_ready = false;
+  fc_stats stats{};
+};
+
+int set_error(Ctx* c, int code, const std::string& msg);
+int cuda_check(Ctx* c, cudaError_t e, const char* what);
+int lut_slot(int n);
+
+// fc_pool.cu
+int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
+               const int32_t use_tau[4], int64_t out_sizes[4]);
+int pool_set_level(Ctx* c, int level, int64_t count, const uint8_t* tiles);
+
+// fc_scan_exact.cu
+int ensure_iso_tables(Ctx* c);
+int level_prepare_exact(Ctx* c, Level& L);
+int gather_ranges(Ctx* c, Level& L, const int32_t* d_origins, int64_t M);
+int load_ranges(Ctx* c, Level& L, const uint8_t* h_tiles, int64_t M);
+int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t n_range_list,
+               const int32_t* d_col_list, int64_t n_col_list, uint64_t* d_keys);
+int decode_keys(Ctx* c, const uint64_t* d_keys, int64_t M, int64_t* d_err, int64_t* d_idx);
+int iso_table_offset(int side);
+int scan_rows_dropin(Ctx* c, const int16_t* ranges, const double* rmeans, int64_t M, int32_t n,
+                     const int16_t* q, const double* dmeans, int64_t E, const double* svals,
+                     int32_t S, int32_t baseline, int64_t* out_err, int64_t* out_idx);
+
+// fc_scan_tc.cu
+int level_prepare_tc(Ctx* c, Level& L);
+int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys);
+
+}  // namespace fcb
+
+#define FC_CUDA(c, expr)                                  \
+  do {                                                    \
+    cudaError_t _e = (expr);                              \
+    if (_e != cudaSuccess) return fcb::cuda_check(c, _e, #expr); \
+  } while (0)
+
+#define FC_TRY(expr)          \
+  do {                        \
+    int _r = (expr);          \
+    if (_r != FC_OK) return _r; \
+  } while (0)

@@ -1,0 +1,290 @@
+// Domain-pool construction on the device (pool.py:88-178, image.py:116-130).
+//
+//  1. entropy_kernel   : one warp per 2Bx2B lattice window (raster order,
+//                        pool.py:120-135); 256-bin shared-memory histogram,
+//                        then H = -sum_b t[count_b] with t[k] = p*log(p) from the
+//                        host-numpy LUT, summed in numpy's exact pairwise order
+//                        (two 128-bin halves, 8 running accumulators each,
+//                        ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), half0+half1) so the
+//                        float64 bits equal pool.py:88-92 on the same host.
+//  2. CUB stable radix sort on key ~bits(|H|): entropy descending, raster order
+//     among exact ties (np.argsort(-ent, kind="stable"), pool.py:171).
+//  3. survivor_kernel  : one warp per kept window: floor 2x2 decimation,
+//                        exact sum / sum of squares, mean, centered norm
+//                        (pool.py:138-152).
+#include <cub/cub.cuh>
+
+#include "fc_internal.cuh"
+
+namespace fcb {
+
+namespace {
+
+constexpr int kEntWarps = 8;
+
+__device__ __forceinline__ uint64_t entropy_key(double h) {
+  // |h|: maps the -0.0 of a constant window onto +0.0 (they compare equal in numpy).
+  uint64_t bits = static_cast<uint64_t>(__double_as_longlong(h)) & 0x7fffffffffffffffull;
+  return ~bits;  // ascending key == descending entropy
+}
+
+template <int D>
+__global__ void __launch_bounds__(kEntWarps * 32)
+entropy_kernel(const uint8_t* __restrict__ img, int width, int nx, int64_t nwin, int stride,
+               const double* __restrict__ lut, double tau, int use_tau,
+               double* __restrict__ ent_out, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
+               unsigned long long* __restrict__ above) {
+  __shared__ int hist[kEntWarps][256];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  int* h = hist[warp];
+  int local_above = 0;
+  for (int64_t w = (int64_t)blockIdx.x * kEntWarps + warp; w < nwin;
+       w += (int64_t)gridDim.x * kEntWarps) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[lane + 32 * i] = 0;
+    __syncwarp();
+    const int64_t wy = w / nx, wx = w - wy * nx;
+    const uint8_t* base = img + (wy * stride) * (int64_t)width + wx * stride;
+#pragma unroll 4
+    for (int p = lane; p < D * D; p += 32) {
+      const int r = p / D, col = p - r * D;
+      atomicAdd(&h[base[(int64_t)r * width + col]], 1);
+    }
+    __syncwarp();
+    // numpy pairwise sum of the 256 terms (lanes 16..31 mirror lanes 0..15)
+    const int half = (lane >> 3) & 1, j = lane & 7;
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int cnt = h[half * 128 + i * 8 + j];
+      const double t = cnt ? lut[cnt - 1] : 0.0;
+      acc = (i == 0) ? t : acc + t;
+    }
+    acc = acc + __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc = acc + __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc = acc + __shfl_xor_sync(0xffffffffu, acc, 4);
+    acc = acc + __shfl_xor_sync(0xffffffffu, acc, 8);
+    const double hval = -acc;
+    if (lane == 0) {
+      ent_out[w] = hval;
+      keys[w] = entropy_key(hval);
+      vals[w] = static_cast<uint32_t>(w);
+      if (use_tau && hval > tau) ++local_above;
+    }
+    __syncwarp();
+  }
+  if (use_tau && lane == 0 && local_above) atomicAdd(above, (unsigned long long)local_above);
+}
+
+// One warp per survivor: decimate, moments, coordinates.
+__global__ void survivor_kernel(const uint8_t* __restrict__ img, int width, int nx, int stride,
+                                int D, const uint32_t* __restrict__ order,
+                                const double* __restrict__ ent_all, int64_t count,
+                                uint32_t* __restrict__ xy, double* __restrict__ ent,
+                                uint8_t* __restrict__ tiles, int32_t* __restrict__ sum,
+                                int64_t* __restrict__ sumsq, double* __restrict__ mean,
+                                double* __restrict__ cnorm) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= count) return;
+  const uint32_t w = order[warp];
+  const int wy = w / nx, wx = w - wy * nx;
+  const int x0 = wx * stride, y0 = wy * stride;
+  const int B = D / 2, n = B * B;
+  const uint8_t* base = img + (int64_t)y0 * width + x0;
+  uint8_t* out = tiles + (int64_t)warp * n;
+  int s1 = 0;
+  long long s2 = 0;
+  for (int p = lane; p < n; p += 32) {
+    const int r = p / B, c = p - r * B;
+    const uint8_t* q = base + (int64_t)(2 * r) * width + 2 * c;
+    const int v = (q[0] + q[1] + q[width] + q[width + 1]) >> 2;  // floor mean, image.py:125-130
+    out[p] = static_cast<uint8_t>(v);
+    s1 += v;
+    s2 += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if (lane == 0) {
+    xy[warp] = static_cast<uint32_t>(x0) | (static_cast<uint32_t>(y0) << 16);
+    ent[warp] = ent_all[w];
+    sum[warp] = s1;
+    sumsq[warp] = s2;
+    // mean = s1 / n; cnorm = s2 - s1*s1/n with Python float semantics (pool.py:144-151)
+    mean[warp] = __ddiv_rn((double)s1, (double)n);
+    cnorm[warp] = __dsub_rn((double)s2, __ddiv_rn((double)((long long)s1 * s1), (double)n));
+  }
+}
+
+// Moments of explicitly supplied decimated tiles (fc_pool_set_level).
+__global__ void moments_kernel(const uint8_t* __restrict__ tiles, int n, int64_t count,
+                               uint32_t* __restrict__ xy, double* __restrict__ ent,
+                               int32_t* __restrict__ sum, int64_t* __restrict__ sumsq,
+                               double* __restrict__ mean, double* __restrict__ cnorm) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= count) return;
+  const uint8_t* t = tiles + (int64_t)warp * n;
+  int s1 = 0;
+  long long s2 = 0;
+  for (int p = lane; p < n; p += 32) {
+    const int v = t[p];
+    s1 += v;
+    s2 += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if (lane == 0) {
+    xy[warp] = 0;
+    ent[warp] = 0.0;
+    sum[warp] = s1;
+    sumsq[warp] = s2;
+    mean[warp] = __ddiv_rn((double)s1, (double)n);
+    cnorm[warp] = __dsub_rn((double)s2, __ddiv_rn((double)((long long)s1 * s1), (double)n));
+  }
+}
+
+int alloc_level(Ctx* c, Level& L, int64_t E) {
+  const int n = L.n;
+  FC_CUDA(c, L.xy.reserve(E * 4 + 16));
+  FC_CUDA(c, L.ent.reserve(E * 8 + 16));
+  FC_CUDA(c, L.tiles.reserve(E * n + 16));
+  FC_CUDA(c, L.sum.reserve(E * 4 + 16));
+  FC_CUDA(c, L.sumsq.reserve(E * 8 + 16));
+  FC_CUDA(c, L.mean.reserve(E * 8 + 16));
+  FC_CUDA(c, L.cnorm.reserve(E * 8 + 16));
+  return FC_OK;
+}
+
+}  // namespace
+
+int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
+               const int32_t use_tau[4], int64_t out_sizes[4]) {
+  if (!c->img_ptr) return set_error(c, FC_ERR_STATE, "no image set");
+  for (int li = 0; li < kLevels; ++li) {
+    if (strides[li] < 1) return set_error(c, FC_ERR_ARG, "strides must be 4 positive integers");
+    if (!use_tau[li] && caps[li] < 1) return set_error(c, FC_ERR_ARG, "caps must be >= 1");
+  }
+  for (int li = 0; li < kLevels; ++li) {
+    const int D = kDomainSide[li];
+    if (D > c->width || D > c->height) {
+      char buf[160];
+      snprintf(buf, sizeof buf, "level %d domain side %d exceeds image %dx%d", li + 1, D, c->width,
+               c->height);
+      return set_error(c, FC_ERR_POOL_CONFIG, buf);
+    }
+    const int slot = lut_slot(D * D);
+    if (!c->lut_set[slot]) return set_error(c, FC_ERR_STATE, "entropy LUT not set");
+  }
+  for (int li = 0; li < kLevels; ++li) {
+    Level& L = c->lv[li];
+    const int D = kDomainSide[li];
+    L.side = kRangeSide[li];
+    L.n = L.side * L.side;
+    L.stride = strides[li];
+    L.synthetic = false;
+    L.prepared = false;
+    L.tc.ready = false;
+    const int nx = (c->width - D) / L.stride + 1;
+    const int ny = (c->height - D) / L.stride + 1;
+    const int64_t nwin = (int64_t)nx * ny;
+    FC_CUDA(c, c->ent_scratch.reserve(nwin * 8));
+    FC_CUDA(c, c->key_in.reserve(nwin * 8));
+    FC_CUDA(c, c->key_out.reserve(nwin * 8));
+    FC_CUDA(c, c->val_in.reserve(nwin * 4));
+    FC_CUDA(c, c->val_out.reserve(nwin * 4));
+    FC_CUDA(c, c->count_buf.reserve(64));
+    FC_CUDA(c, cudaMemsetAsync(c->count_buf.ptr, 0, 8, c->stream));
+    const double* lut = c->lut[lut_slot(D * D)].as<double>();
+    int64_t blocks64 = (nwin + kEntWarps - 1) / kEntWarps;
+    const int blocks = (int)std::min<int64_t>(blocks64, (int64_t)c->sm_count * 64);
+    const double tau = use_tau[li] ? taus[li] : 0.0;
+    auto* cnt = c->count_buf.as<unsigned long long>();
+    switch (D) {
+      case 32:
+        entropy_kernel<32><<<blocks, kEntWarps * 32, 0, c->stream>>>(
+            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, use_tau[li],
+            c->ent_scratch.as<double>(), c->key_in.as<uint64_t>(), c->val_in.as<uint32_t>(), cnt);
+        break;
+      case 16:
+        entropy_kernel<16><<<blocks, kEntWarps * 32, 0, c->stream>>>(
+            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, use_tau[li],
+            c->ent_scratch.as<double>(), c->key_in.as<uint64_t>(), c->val_in.as<uint32_t>(), cnt);
+        break;
+      case 8:
+        entropy_kernel<8><<<blocks, kEntWarps * 32, 0, c->stream>>>(
+            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, use_tau[li],
+            c->ent_scratch.as<double>(), c->key_in.as<uint64_t>(), c->val_in.as<uint32_t>(), cnt);
+        break;
+      default:
+        entropy_kernel<4><<<blocks, kEntWarps * 32, 0, c->stream>>>(
+            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, use_tau[li],
+            c->ent_scratch.as<double>(), c->key_in.as<uint64_t>(), c->val_in.as<uint32_t>(), cnt);
+        break;
+    }
+    FC_CUDA(c, cudaGetLastError());
+    size_t tmp = 0;
+    FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, c->key_in.as<uint64_t>(),
+                                               c->key_out.as<uint64_t>(), c->val_in.as<uint32_t>(),
+                                               c->val_out.as<uint32_t>(), (int)nwin, 0, 64,
+                                               c->stream));
+    FC_CUDA(c, c->cub_tmp.reserve(tmp));
+    FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, c->key_in.as<uint64_t>(),
+                                               c->key_out.as<uint64_t>(), c->val_in.as<uint32_t>(),
+                                               c->val_out.as<uint32_t>(), (int)nwin, 0, 64,
+                                               c->stream));
+    int64_t E;
+    if (use_tau[li]) {
+      unsigned long long above = 0;
+      FC_CUDA(c, cudaMemcpyAsync(&above, cnt, 8, cudaMemcpyDeviceToHost, c->stream));
+      FC_CUDA(c, cudaStreamSynchronize(c->stream));
+      E = std::max<int64_t>(1, (int64_t)above);  // level caps are >= 1 (pool.py:47-48)
+    } else {
+      E = std::min<int64_t>(caps[li], nwin);
+    }
+    L.count = E;
+    FC_TRY(alloc_level(c, L, E));
+    const int threads = 256;
+    const int64_t grid = (E * 32 + threads - 1) / threads;
+    survivor_kernel<<<(unsigned)grid, threads, 0, c->stream>>>(
+        c->img_ptr, c->width, nx, L.stride, D, c->val_out.as<uint32_t>(),
+        c->ent_scratch.as<double>(), E, L.xy.as<uint32_t>(), L.ent.as<double>(),
+        L.tiles.as<uint8_t>(), L.sum.as<int32_t>(), L.sumsq.as<int64_t>(), L.mean.as<double>(),
+        L.cnorm.as<double>());
+    FC_CUDA(c, cudaGetLastError());
+    out_sizes[li] = E;
+  }
+  FC_CUDA(c, cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+int pool_set_level(Ctx* c, int level, int64_t count, const uint8_t* tiles) {
+  Level& L = c->lv[level - 1];
+  L.side = kRangeSide[level - 1];
+  L.n = L.side * L.side;
+  L.stride = 1;
+  L.count = count;
+  L.synthetic = true;
+  L.prepared = false;
+  L.tc.ready = false;
+  if (count == 0) return FC_OK;
+  FC_TRY(alloc_level(c, L, count));
+  FC_CUDA(c, cudaMemcpyAsync(L.tiles.ptr, tiles, count * L.n, cudaMemcpyHostToDevice, c->stream));
+  const int threads = 256;
+  const int64_t grid = (count * 32 + threads - 1) / threads;
+  moments_kernel<<<(unsigned)grid, threads, 0, c->stream>>>(
+      L.tiles.as<uint8_t>(), L.n, count, L.xy.as<uint32_t>(), L.ent.as<double>(),
+      L.sum.as<int32_t>(), L.sumsq.as<int64_t>(), L.mean.as<double>(), L.cnorm.as<double>());
+  FC_CUDA(c, cudaGetLastError());
+  FC_CUDA(c, cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+}  // namespace fcb

@@ -1,0 +1,461 @@
+// Exact CUDA-core candidate scan (the correctness anchor and the path for
+// levels/modes the tensor contraction does not take: baseline mode, 2x2
+// ranges, clamp-active (range, column) pairs).
+//
+// Semantics follow _scan.py:14-63: for every range and candidate
+// c = (e*8 + iso)*S + si the error is the exact SSD of clip(q + o, 0, 255)
+// against the range; the winner is the lexicographically first minimum.
+// Order independence comes from a packed key (err << 32) | c reduced with
+// warp shuffles and a global atomicMin, so grid shape never changes results.
+//
+// Isometries are applied to the RANGE (one inverse pixel permutation per
+// isometry, precomputed into shared memory) instead of copying the domain
+// pool 8x as matcher.py:148-151 does:  sum_k f(iso(q)[k], r[k]) =
+// sum_j f(q[j], r[src_iso^-1(j)]).
+//
+// Inner loop per 16 pixels of one (column, range): the clipped
+// reconstruction x = clip(q + o) is formed once as packed bytes (vadd2 /
+// vmaxs2 / vmins2 / byte_perm) and reused by all 8 isometries, each costing
+// one broadcast LDS.128 plus 4 x (vabsdiffu4 + dp4a).
+#include "fc_internal.cuh"
+
+namespace fcb {
+
+namespace {
+
+constexpr int kRB = 8;          // ranges per block
+constexpr int kColsPerBlock = 128;
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+__device__ __forceinline__ int rint_offset_baseline(double rmean, double s, double dmean) {
+  // _scan.py:39-43: clip(round(rmean - s*dmean), 0, 255); product rounded first.
+  double v = rint(__dsub_rn(rmean, __dmul_rn(s, dmean)));
+  int o = (int)v;
+  return o < 0 ? 0 : (o > 255 ? 255 : o);
+}
+
+// rtiles: uint8 [M][N]; inv: uint16 [8][N] inverse isometry maps for this side
+template <int N>
+__global__ void __launch_bounds__(kColsPerBlock)
+scan_exact_kernel(const int16_t* __restrict__ qbase, int64_t ncols, int S,
+                  const double* __restrict__ svals, const double* __restrict__ dmean,
+                  const uint8_t* __restrict__ rtiles, const double* __restrict__ rmean,
+                  int64_t M, const uint16_t* __restrict__ inv,
+                  const int32_t* __restrict__ range_list, int64_t n_range_list, int64_t range_base,
+                  const int32_t* __restrict__ col_list, int64_t n_col_list, int baseline,
+                  unsigned long long* __restrict__ keys) {
+  constexpr int CH = N >= 16 ? 16 : N;  // pixels per inner chunk
+  constexpr int W = CH / 4;             // packed words per chunk
+  __shared__ __align__(16) uint8_t rperm[kRB][8][N];
+  __shared__ int s_m[kRB];
+  __shared__ double s_rmean[kRB];
+
+  const int tid = threadIdx.x;
+  const int64_t nrange = range_list ? n_range_list : M;
+  const int64_t r0 = range_base + (int64_t)blockIdx.y * kRB;
+  if (tid < kRB) {
+    const int64_t idx = r0 + tid;
+    int m = -1;
+    if (idx < nrange) m = range_list ? range_list[idx] : (int)idx;
+    s_m[tid] = m;
+    s_rmean[tid] = m >= 0 ? rmean[m] : 0.0;
+  }
+  __syncthreads();
+  for (int i = tid; i < kRB * 8 * N; i += kColsPerBlock) {
+    const int mm = i / (8 * N);
+    const int rem = i - mm * 8 * N;
+    const int iso = rem / N, j = rem - iso * N;
+    const int m = s_m[mm];
+    rperm[mm][iso][j] = m >= 0 ? rtiles[(int64_t)m * N + inv[iso * N + j]] : 0;
+  }
+  __syncthreads();
+
+  const int64_t ci = (int64_t)blockIdx.x * kColsPerBlock + tid;
+  const int64_t ncol_eff = col_list ? n_col_list : ncols;
+  const bool valid = ci < ncol_eff;
+  const int64_t col = valid ? (col_list ? (int64_t)col_list[ci] : ci) : 0;
+  const int64_t e = col / S;
+  const int si = (int)(col - e * S);
+
+  int o[kRB];
+#pragma unroll
+  for (int mm = 0; mm < kRB; ++mm) {
+    o[mm] = baseline ? rint_offset_baseline(s_rmean[mm], svals[si], dmean[e])
+                     : (int)rint(s_rmean[mm]);
+  }
+  unsigned acc[kRB][8];
+#pragma unroll
+  for (int mm = 0; mm < kRB; ++mm)
+#pragma unroll
+    for (int iso = 0; iso < 8; ++iso) acc[mm][iso] = 0u;
+
+  const int16_t* qcol = qbase + col * N;
+#pragma unroll 1
+  for (int k = 0; k < N; k += CH) {
+    unsigned qw[CH / 2];
+    if constexpr (CH == 16) {
+      const uint4 a = *reinterpret_cast<const uint4*>(qcol + k);
+      const uint4 b = *reinterpret_cast<const uint4*>(qcol + k + 8);
+      qw[0] = a.x; qw[1] = a.y; qw[2] = a.z; qw[3] = a.w;
+      qw[4] = b.x; qw[5] = b.y; qw[6] = b.z; qw[7] = b.w;
+    } else {
+      const uint2 a = *reinterpret_cast<const uint2*>(qcol + k);
+      qw[0] = a.x; qw[1] = a.y;
+    }
+#pragma unroll
+    for (int mm = 0; mm < kRB; ++mm) {
+      const unsigned o2 = (unsigned)o[mm] | ((unsigned)o[mm] << 16);
+      unsigned x4[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        unsigned lo = __vmins2(__vmaxs2(__vadd2(qw[2 * w], o2), 0u), 0x00ff00ffu);
+        unsigned hi = __vmins2(__vmaxs2(__vadd2(qw[2 * w + 1], o2), 0u), 0x00ff00ffu);
+        x4[w] = __byte_perm(lo, hi, 0x6420);
+      }
+#pragma unroll
+      for (int iso = 0; iso < 8; ++iso) {
+        unsigned a = acc[mm][iso];
+        if constexpr (W == 4) {
+          const uint4 r4 = *reinterpret_cast<const uint4*>(&rperm[mm][iso][k]);
+          unsigned d;
+          d = __vabsdiffu4(x4[0], r4.x); a = __dp4a(d, d, a);
+          d = __vabsdiffu4(x4[1], r4.y); a = __dp4a(d, d, a);
+          d = __vabsdiffu4(x4[2], r4.z); a = __dp4a(d, d, a);
+          d = __vabsdiffu4(x4[3], r4.w); a = __dp4a(d, d, a);
+        } else {
+          const unsigned r4 = *reinterpret_cast<const unsigned*>(&rperm[mm][iso][k]);
+          const unsigned d = __vabsdiffu4(x4[0], r4);
+          a = __dp4a(d, d, a);
+        }
+        acc[mm][iso] = a;
+      }
+    }
+  }
+  const int lane = tid & 31;
+#pragma unroll
+  for (int mm = 0; mm < kRB; ++mm) {
+    unsigned long long best = ~0ull;
+    if (valid) {
+#pragma unroll
+      for (int iso = 0; iso < 8; ++iso) {
+        const unsigned long long cidx = (unsigned long long)((e * 8 + iso) * S + si);
+        const unsigned long long key = ((unsigned long long)acc[mm][iso] << 32) | cidx;
+        best = key < best ? key : best;
+      }
+    }
+    best = warp_min_u64(best);
+    if (lane == 0 && s_m[mm] >= 0 && best != ~0ull) atomicMin(&keys[s_m[mm]], best);
+  }
+}
+
+// Drop-in for _scan.py:14 with arbitrary candidate rows (reference layout).
+__global__ void __launch_bounds__(128)
+scan_rows_kernel(const int16_t* __restrict__ q, int64_t rows, int n, int S,
+                 const double* __restrict__ svals, const double* __restrict__ dmean,
+                 const int16_t* __restrict__ ranges, const double* __restrict__ rmean, int64_t M,
+                 int baseline, unsigned long long* __restrict__ keys) {
+  extern __shared__ int16_t sr[];  // [kRB][n]
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * kRB;
+  for (int i = tid; i < kRB * n; i += blockDim.x) {
+    const int64_t m = r0 + i / n;
+    sr[i] = m < M ? ranges[m * n + (i % n)] : 0;
+  }
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + tid;
+  const bool valid = c < rows;
+  const int64_t e = valid ? c / (8 * S) : 0;
+  const int si = valid ? (int)(c % S) : 0;
+  const int lane = tid & 31;
+  for (int mm = 0; mm < kRB; ++mm) {
+    const int64_t m = r0 + mm;
+    unsigned long long key = ~0ull;
+    if (valid && m < M) {
+      const int o = baseline ? rint_offset_baseline(rmean[m], svals[si], dmean[e])
+                             : (int)rint(rmean[m]);
+      long long err = 0;
+      for (int k = 0; k < n; ++k) {
+        int v = q[c * n + k] + o;
+        v = v < 0 ? 0 : (v > 255 ? 255 : v);
+        const int d = v - sr[mm * n + k];
+        err += (long long)d * d;
+      }
+      if (err > 0x7fffffffLL) err = 0x7fffffffLL;
+      key = ((unsigned long long)err << 32) | (unsigned long long)c;
+    }
+    key = warp_min_u64(key);
+    if (lane == 0 && m < M && key != ~0ull) atomicMin(&keys[m], key);
+  }
+}
+
+// Gather range tiles at origins and their exact moments (codec.py:164-168,
+// matcher.py:171: rmean = sum / n exactly).
+__global__ void gather_kernel(const uint8_t* __restrict__ img, int width,
+                              const int32_t* __restrict__ origins, int64_t M, int B,
+                              uint8_t* __restrict__ rtiles, double* __restrict__ rmean,
+                              int32_t* __restrict__ roff, int32_t* __restrict__ rsq) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= M) return;
+  const int x = origins[2 * warp], y = origins[2 * warp + 1];
+  const int n = B * B;
+  int s1 = 0, s2 = 0;
+  for (int p = lane; p < n; p += 32) {
+    const int r = p / B, col = p - r * B;
+    const int v = img[(int64_t)(y + r) * width + x + col];
+    rtiles[warp * n + p] = (uint8_t)v;
+    s1 += v;
+    s2 += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if (lane == 0) {
+    const double mean = __ddiv_rn((double)s1, (double)n);
+    rmean[warp] = mean;
+    roff[warp] = (int)rint(mean);
+    rsq[warp] = s2;
+  }
+}
+
+// Moments of explicitly supplied range tiles (fc_match_tiles).
+__global__ void range_moments_kernel(const uint8_t* __restrict__ rtiles, int64_t M, int n,
+                                     double* __restrict__ rmean, int32_t* __restrict__ roff,
+                                     int32_t* __restrict__ rsq) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= M) return;
+  int s1 = 0, s2 = 0;
+  for (int p = lane; p < n; p += 32) {
+    const int v = rtiles[warp * n + p];
+    s1 += v;
+    s2 += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if (lane == 0) {
+    const double mean = __ddiv_rn((double)s1, (double)n);
+    rmean[warp] = mean;
+    roff[warp] = (int)rint(mean);
+    rsq[warp] = s2;
+  }
+}
+
+// q base operand: column (e, si) -> rint(s*(d - mean)) or rint(s*d) (matcher.py:143-152)
+__global__ void qbase_kernel(const uint8_t* __restrict__ tiles, const double* __restrict__ mean,
+                             int64_t E, int n, int S, const double* __restrict__ svals,
+                             int baseline, int16_t* __restrict__ q) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = E * S * n;
+  if (i >= total) return;
+  const int64_t col = i / n;
+  const int j = (int)(i - col * n);
+  const int64_t e = col / S;
+  const int si = (int)(col - e * S);
+  const double d = (double)tiles[e * n + j];
+  const double x = baseline ? d : __dsub_rn(d, mean[e]);
+  q[i] = (int16_t)rint(__dmul_rn(svals[si], x));
+}
+
+__global__ void decode_keys_kernel(const unsigned long long* __restrict__ keys, int64_t M,
+                                   int64_t* __restrict__ err, int64_t* __restrict__ idx) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const unsigned long long k = keys[i];
+  err[i] = (int64_t)(k >> 32);
+  idx[i] = (int64_t)(k & 0xffffffffull);
+}
+
+}  // namespace
+
+int iso_table_offset(int side) {
+  return side == 16 ? 0 : side == 8 ? 8 * 256 : side == 4 ? 8 * (256 + 64) : 8 * (256 + 64 + 16);
+}
+
+// Inverse isometry maps per range side, packed [side][8][n]:
+// inv[iso][j] = output pixel k with src_iso(k) = j, where out[k] = t[src_iso(k)]
+// restates apply_isometry (image.py:140-155).
+int ensure_iso_tables(Ctx* c) {
+  if (c->iso_ready) return FC_OK;
+  std::vector<uint16_t> h(8 * (256 + 64 + 16 + 4), 0);
+  const int sides[4] = {16, 8, 4, 2};
+  for (int s = 0; s < 4; ++s) {
+    const int B = sides[s], b = B - 1, n = B * B;
+    uint16_t* t = h.data() + iso_table_offset(B);
+    for (int iso = 0; iso < 8; ++iso) {
+      for (int i = 0; i < B; ++i)
+        for (int j = 0; j < B; ++j) {
+          int r = 0, cc = 0;  // out[i][j] = t[r][cc]
+          switch (iso) {
+            case 0: r = i; cc = j; break;
+            case 1: r = b - j; cc = i; break;
+            case 2: r = b - i; cc = b - j; break;
+            case 3: r = j; cc = b - i; break;
+            case 4: r = i; cc = b - j; break;
+            case 5: r = j; cc = i; break;
+            case 6: r = b - i; cc = j; break;
+            default: r = b - j; cc = b - i; break;
+          }
+          t[iso * n + r * B + cc] = (uint16_t)(i * B + j);
+        }
+    }
+  }
+  FC_CUDA(c, c->iso_inv.reserve(h.size() * 2));
+  FC_CUDA(c, cudaMemcpy(c->iso_inv.ptr, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+  c->iso_ready = true;
+  return FC_OK;
+}
+
+int level_prepare_exact(Ctx* c, Level& L) {
+  const int64_t cols = L.count * L.s_count;
+  FC_CUDA(c, L.qbase.reserve(cols * L.n * 2 + 64));
+  const int64_t total = cols * L.n;
+  if (total > 0) {
+    FC_CUDA(c, c->svals_dev.reserve(kMaxS * 8));
+    double* d_s = c->svals_dev.as<double>();
+    FC_CUDA(c, cudaMemcpyAsync(d_s, L.svals, L.s_count * 8, cudaMemcpyHostToDevice, c->stream));
+    qbase_kernel<<<(unsigned)((total + 255) / 256), 256, 0, c->stream>>>(
+        L.tiles.as<uint8_t>(), L.mean.as<double>(), L.count, L.n, L.s_count, d_s, L.baseline,
+        L.qbase.as<int16_t>());
+    FC_CUDA(c, cudaGetLastError());
+    FC_CUDA(c, cudaStreamSynchronize(c->stream));
+  }
+  return FC_OK;
+}
+
+int gather_ranges(Ctx* c, Level& L, const int32_t* d_origins, int64_t M) {
+  FC_CUDA(c, c->rtiles.reserve(M * L.n + 64));
+  FC_CUDA(c, c->rmean.reserve(M * 8 + 64));
+  FC_CUDA(c, c->roff.reserve(M * 4 + 64));
+  FC_CUDA(c, c->rsq.reserve(M * 4 + 64));
+  if (M == 0) return FC_OK;
+  const int threads = 256;
+  gather_kernel<<<(unsigned)((M * 32 + threads - 1) / threads), threads, 0, c->stream>>>(
+      c->img_ptr, c->width, d_origins, M, L.side, c->rtiles.as<uint8_t>(), c->rmean.as<double>(),
+      c->roff.as<int32_t>(), c->rsq.as<int32_t>());
+  FC_CUDA(c, cudaGetLastError());
+  c->stats.kernel_launches += 1;
+  return FC_OK;
+}
+
+int load_ranges(Ctx* c, Level& L, const uint8_t* h_tiles, int64_t M) {
+  FC_CUDA(c, c->rtiles.reserve(M * L.n + 64));
+  FC_CUDA(c, c->rmean.reserve(M * 8 + 64));
+  FC_CUDA(c, c->roff.reserve(M * 4 + 64));
+  FC_CUDA(c, c->rsq.reserve(M * 4 + 64));
+  if (M == 0) return FC_OK;
+  FC_CUDA(c, cudaMemcpyAsync(c->rtiles.ptr, h_tiles, M * L.n, cudaMemcpyHostToDevice, c->stream));
+  const int threads = 256;
+  range_moments_kernel<<<(unsigned)((M * 32 + threads - 1) / threads), threads, 0, c->stream>>>(
+      c->rtiles.as<uint8_t>(), M, L.n, c->rmean.as<double>(), c->roff.as<int32_t>(),
+      c->rsq.as<int32_t>());
+  FC_CUDA(c, cudaGetLastError());
+  c->stats.kernel_launches += 1;
+  return FC_OK;
+}
+
+int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t n_range_list,
+               const int32_t* d_col_list, int64_t n_col_list, uint64_t* d_keys) {
+  FC_TRY(ensure_iso_tables(c));
+  const int64_t ncols = L.count * L.s_count;
+  const int64_t nr = d_range_list ? n_range_list : M;
+  const int64_t nc = d_col_list ? n_col_list : ncols;
+  if (nr == 0 || nc == 0) return FC_OK;
+  FC_CUDA(c, c->svals_dev.reserve(kMaxS * 8));
+  double* d_s = c->svals_dev.as<double>();
+  FC_CUDA(c, cudaMemcpyAsync(d_s, L.svals, L.s_count * 8, cudaMemcpyHostToDevice, c->stream));
+  const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
+  auto* keys = reinterpret_cast<unsigned long long*>(d_keys);
+  const unsigned gx = (unsigned)((nc + kColsPerBlock - 1) / kColsPerBlock);
+  const int64_t slab = 65535LL * kRB;
+  for (int64_t base = 0; base < nr; base += slab) {
+    const int64_t cnt = std::min<int64_t>(slab, nr - base);
+    dim3 grid(gx, (unsigned)((cnt + kRB - 1) / kRB));
+    const int64_t nlist = d_range_list ? n_range_list : M;
+#define FC_LAUNCH_EXACT(NN)                                                                     \
+    scan_exact_kernel<NN><<<grid, kColsPerBlock, 0, c->stream>>>(                               \
+        L.qbase.as<int16_t>(), ncols, L.s_count, d_s, L.mean.as<double>(),                      \
+        c->rtiles.as<uint8_t>(), c->rmean.as<double>(), nlist, inv, d_range_list, n_range_list, \
+        base, d_col_list, n_col_list, L.baseline, keys)
+    switch (L.n) {
+      case 256: FC_LAUNCH_EXACT(256); break;
+      case 64: FC_LAUNCH_EXACT(64); break;
+      case 16: FC_LAUNCH_EXACT(16); break;
+      default: FC_LAUNCH_EXACT(4); break;
+    }
+#undef FC_LAUNCH_EXACT
+    FC_CUDA(c, cudaGetLastError());
+    c->stats.kernel_launches += 1;
+  }
+  return FC_OK;
+}
+
+int decode_keys(Ctx* c, const uint64_t* d_keys, int64_t M, int64_t* d_err, int64_t* d_idx) {
+  if (M == 0) return FC_OK;
+  decode_keys_kernel<<<(unsigned)((M + 255) / 256), 256, 0, c->stream>>>(
+      reinterpret_cast<const unsigned long long*>(d_keys), M, d_err, d_idx);
+  FC_CUDA(c, cudaGetLastError());
+  c->stats.kernel_launches += 1;
+  return FC_OK;
+}
+
+int scan_rows_dropin(Ctx* c, const int16_t* ranges, const double* rmeans, int64_t M, int32_t n,
+                     const int16_t* q, const double* dmeans, int64_t E, const double* svals,
+                     int32_t S, int32_t baseline, int64_t* out_err, int64_t* out_idx) {
+  if (M == 0) return FC_OK;
+  const int64_t rows = E * 8 * S;
+  DevBuf dq, dr, drm, ddm, ds, dk, de, di;
+  auto cleanup = [&]() {
+    dq.release(); dr.release(); drm.release(); ddm.release(); ds.release(); dk.release();
+    de.release(); di.release();
+  };
+  cudaError_t e = cudaSuccess;
+  if ((e = dq.reserve(rows * n * 2 + 16)) || (e = dr.reserve(M * n * 2 + 16)) ||
+      (e = drm.reserve(M * 8 + 16)) || (e = ddm.reserve(E * 8 + 16)) || (e = ds.reserve(S * 8 + 16)) ||
+      (e = dk.reserve(M * 8 + 16)) || (e = de.reserve(M * 8 + 16)) || (e = di.reserve(M * 8 + 16))) {
+    cleanup();
+    return cuda_check(c, e, "scan_rows_dropin alloc");
+  }
+  cudaStream_t s = c->stream;
+  cudaMemcpyAsync(dq.ptr, q, rows * n * 2, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(dr.ptr, ranges, M * n * 2, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(drm.ptr, rmeans, M * 8, cudaMemcpyHostToDevice, s);
+  if (E) cudaMemcpyAsync(ddm.ptr, dmeans, E * 8, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(ds.ptr, svals, S * 8, cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(dk.ptr, 0xff, M * 8, s);
+  if (rows > 0) {
+    dim3 grid((unsigned)((rows + 127) / 128), (unsigned)((M + kRB - 1) / kRB));
+    scan_rows_kernel<<<grid, 128, kRB * n * 2, s>>>(
+        dq.as<int16_t>(), rows, n, S, ds.as<double>(), ddm.as<double>(), dr.as<int16_t>(),
+        drm.as<double>(), M, baseline, dk.as<unsigned long long>());
+  }
+  e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    decode_keys_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(
+        dk.as<unsigned long long>(), M, de.as<int64_t>(), di.as<int64_t>());
+    cudaMemcpyAsync(out_err, de.ptr, M * 8, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(out_idx, di.ptr, M * 8, cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+  }
+  cleanup();
+  if (e != cudaSuccess) return cuda_check(c, e, "scan_rows_dropin");
+  if (rows == 0) {
+    for (int64_t i = 0; i < M; ++i) { out_err[i] = (int64_t)1 << 62; out_idx[i] = -1; }
+  }
+  return FC_OK;
+}
+
+}  // namespace fcb

@@ -1,0 +1,208 @@
+"""Entropy-ranked, truncated domain pools built on the device.
+
+Same interface and results as the reference's pool.py (PoolParams,
+DomainEntry, DomainPool, build_pool, block_entropy, candidate_count).  The
+ranking, decimation and moments run in CUDA (csrc/fc_pool.cu) and stay
+resident on the device for the matcher; entries are copied back only when a
+caller inspects them.  Extension: ``PoolParams.entropy_thresholds`` keeps
+every window whose entropy exceeds tau_l (threshold compaction); it equals the
+reference with ``level_caps[l] = #{entropy > tau_l}``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import PoolConfigError  # noqa: F401  (re-export)
+from .image import GrayImage
+
+LEVEL_RANGE_SIDES = (16, 8, 4, 2)
+LEVEL_DOMAIN_SIDES = (32, 16, 8, 4)
+LEVEL_COUNT = 4
+DEFAULT_STRIDES = (8, 4, 2, 2)
+
+
+@dataclass(frozen=True)
+class PoolParams:
+    pool_cap: int
+    strides: tuple = DEFAULT_STRIDES
+    level_caps: tuple | None = None
+    entropy_thresholds: tuple | None = None  # per level float or None
+
+    def __post_init__(self):
+        if self.pool_cap < 1:
+            raise ValueError("pool_cap must be >= 1")
+        if len(self.strides) != LEVEL_COUNT or any(s < 1 for s in self.strides):
+            raise ValueError("strides must be 4 positive integers")
+        if self.level_caps is not None:
+            if len(self.level_caps) != LEVEL_COUNT or any(c < 1 for c in self.level_caps):
+                raise ValueError("level_caps must be 4 positive integers")
+            object.__setattr__(self, "level_caps", tuple(int(c) for c in self.level_caps))
+        if self.entropy_thresholds is not None:
+            if len(self.entropy_thresholds) != LEVEL_COUNT:
+                raise ValueError("entropy_thresholds needs one entry (or None) per level")
+            object.__setattr__(self, "entropy_thresholds", tuple(
+                None if t is None else float(t) for t in self.entropy_thresholds))
+        object.__setattr__(self, "strides", tuple(int(s) for s in self.strides))
+
+    def cap(self, level: int) -> int:
+        if self.level_caps is not None:
+            return self.level_caps[level - 1]
+        return self.pool_cap
+
+    def tau(self, level: int):
+        if self.entropy_thresholds is None:
+            return None
+        return self.entropy_thresholds[level - 1]
+
+
+@dataclass(frozen=True, eq=False)
+class DomainEntry:
+    x: int
+    y: int
+    entropy: float
+    tile: np.ndarray
+    mean: float
+    centered_norm_sq: float
+
+
+class CoordTable:
+    """Read-only sequence of (x, y) pool origins backed by an [E, 2] array.
+
+    Compares equal to another table or to a tuple of (x, y) tuples, so stream
+    objects compare like the reference's tuple-of-tuples headers without
+    materialising millions of Python tuples.
+    """
+
+    __slots__ = ("array",)
+
+    def __init__(self, array):
+        a = np.asarray(array, dtype=np.int64).reshape(-1, 2)
+        a.flags.writeable = False
+        self.array = a
+
+    def __len__(self):
+        return self.array.shape[0]
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return tuple((int(x), int(y)) for x, y in self.array[i])
+        x, y = self.array[i]
+        return (int(x), int(y))
+
+    def __iter__(self):
+        return ((int(x), int(y)) for x, y in self.array)
+
+    def __eq__(self, other):
+        if isinstance(other, CoordTable):
+            return np.array_equal(self.array, other.array)
+        try:
+            o = np.asarray(other, dtype=np.int64).reshape(-1, 2)
+        except (TypeError, ValueError):
+            return NotImplemented
+        return np.array_equal(self.array, o)
+
+    def __hash__(self):
+        return hash(self.array.tobytes())
+
+    def __repr__(self):
+        return f"CoordTable({len(self)} origins)"
+
+
+class DomainPool:
+    """Device-resident per-level pools (entropy-descending, raster tie order)."""
+
+    def __init__(self, params: PoolParams, width: int, height: int, sizes, context):
+        self.params = params
+        self.width = width
+        self.height = height
+        self.sizes = tuple(int(s) for s in sizes)
+        self.context = context
+        self._coords = {}
+        self._entries = {}
+        self._means = {}
+
+    def size(self, level: int) -> int:
+        return self.sizes[level - 1]
+
+    def coords_array(self, level: int) -> np.ndarray:
+        if level not in self._coords:
+            self._coords[level] = self.context.pool_coords(level, self.size(level)).astype(np.int64)
+        return self._coords[level]
+
+    def coords(self, level: int) -> CoordTable:
+        return CoordTable(self.coords_array(level))
+
+    def means(self, level: int) -> np.ndarray:
+        if level not in self._means:
+            _, _, m, _ = self.context.pool_entries(level, self.size(level),
+                                                   LEVEL_RANGE_SIDES[level - 1], want=("means",))
+            self._means[level] = m
+        return self._means[level]
+
+    def entries(self, level: int) -> tuple:
+        if level not in self._entries:
+            side = LEVEL_RANGE_SIDES[level - 1]
+            ent, tiles, means, cnorm = self.context.pool_entries(level, self.size(level), side)
+            xy = self.coords_array(level)
+            self._entries[level] = tuple(
+                DomainEntry(int(xy[i, 0]), int(xy[i, 1]), float(ent[i]), tiles[i], float(means[i]),
+                            float(cnorm[i])) for i in range(self.size(level)))
+        return self._entries[level]
+
+    @property
+    def levels(self):
+        return tuple(self.entries(lv) for lv in (1, 2, 3, 4))
+
+    @classmethod
+    def from_tiles(cls, tiles_by_level: dict, device: int = 0, width: int = 512, height: int = 512):
+        """Synthetic pool from decimated tiles per level (the reference tests'
+        make_test_pool, tests/oracles.py:29-40)."""
+        ctx = _native.Context(device)
+        sizes = []
+        for level in (1, 2, 3, 4):
+            side = LEVEL_RANGE_SIDES[level - 1]
+            tiles = np.asarray(tiles_by_level.get(level, []), dtype=np.uint8).reshape(-1, side, side)
+            ctx.pool_set_level(level, tiles)
+            sizes.append(tiles.shape[0])
+        cap = max(1, max(sizes))
+        return cls(PoolParams(pool_cap=cap), width, height, sizes, ctx)
+
+
+def build_pool(image: GrayImage, params: PoolParams, context=None) -> DomainPool:
+    """Rank every lattice domain by entropy and keep the top cap per level (device)."""
+    ctx = context if context is not None else _native.Context()
+    ctx.set_image(image.pixels)
+    caps, taus, use_tau = [], [], []
+    for level in (1, 2, 3, 4):
+        tau = params.tau(level)
+        caps.append(params.cap(level))
+        taus.append(0.0 if tau is None else tau)
+        use_tau.append(0 if tau is None else 1)
+    sizes = ctx.pool_build(params.strides, caps, taus, use_tau)
+    return DomainPool(params, image.width, image.height, sizes, ctx)
+
+
+def block_entropy(tile) -> float:
+    """Entropy (nats) of the 256-bin histogram of one tile (host helper)."""
+    a = np.asarray(tile)
+    if a.size == 0:
+        raise ValueError("tile must be non-empty")
+    counts = np.bincount(a.astype(np.int64).ravel(), minlength=256)
+    if counts.shape[0] != 256:
+        raise ValueError("pixel values must lie in [0, 255]")
+    p = counts.reshape(1, 256) / a.size
+    return float(-(p * np.log(np.where(counts.reshape(1, 256) > 0, p, 1.0))).sum(axis=1)[0])
+
+
+def candidate_count(image_size, domain_side: int, stride: int) -> int:
+    if isinstance(image_size, (tuple, list)):
+        w, h = image_size
+    else:
+        w = h = image_size
+    if domain_side > w or domain_side > h:
+        return 0
+    return ((w - domain_side) // stride + 1) * ((h - domain_side) // stride + 1)

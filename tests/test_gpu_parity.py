@@ -1,0 +1,164 @@
+"""Device parity against the reference's golden vectors and the CPU oracle.
+
+Bar: bit-exact.  Errors are exact integer SSDs, indices/isometries/s and the
+8-bit offsets are integers, entropies are float64 bits, streams are bytes.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1502_00324_b200 as fc
+from paper_1502_00324_b200 import _native
+from paper_1502_00324_b200 import workloads as W
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+PATHS = ("exact", "tensor", "auto")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return _native.Context(0)
+
+
+def test_pool_entropies_and_order_bit_exact(ctx):
+    g = load_golden("entropy_cases.npz")
+    for name in g["names"]:
+        img = fc.GrayImage(g[f"img_{name}"])
+        for cap in (12, 10**9):
+            pool = fc.build_pool(img, fc.PoolParams(pool_cap=cap), context=ctx)
+            for level in (1, 2, 3, 4):
+                ref = g[f"pool_{name}_{cap}_{level}"].reshape(-1, 2)
+                assert np.array_equal(pool.coords_array(level), ref), (name, cap, level)
+                ents, tiles, means, cnorm = ctx.pool_entries(level, pool.size(level),
+                                                             fc.pool.LEVEL_RANGE_SIDES[level - 1])
+                assert ents.tobytes() == g[f"poolent_{name}_{cap}_{level}"].tobytes()
+                if cap == 12:
+                    assert np.array_equal(tiles, g[f"pooltiles_{name}_{level}"])
+                    assert means.tobytes() == g[f"poolmeans_{name}_{level}"].tobytes()
+                    assert cnorm.tobytes() == g[f"poolcnorm_{name}_{level}"].tobytes()
+
+
+def test_pool_all_window_entropies_bit_exact(ctx):
+    """Every window's entropy (cap = all) at stride 1 and 3 equals numpy's bits."""
+    g = load_golden("entropy_cases.npz")
+    for name in g["names"]:
+        img = g[f"img_{name}"]
+        for stride in (1, 3):
+            pool = fc.build_pool(fc.GrayImage(img), fc.PoolParams(pool_cap=10**9, strides=(stride,) * 4),
+                                 context=ctx)
+            for level in (1, 2, 3, 4):
+                ref = g[f"ent_{name}_{level}_{stride}"]
+                ents, _, _, _ = ctx.pool_entries(level, pool.size(level), 2, want=("entropy",))
+                order = np.argsort(-ref, kind="stable")
+                assert ents.tobytes() == ref[order].tobytes(), (name, stride, level)
+
+
+def test_pool_config_error(ctx):
+    with pytest.raises(fc.PoolConfigError):
+        fc.build_pool(fc.GrayImage.full(16, 16, 0), fc.PoolParams(pool_cap=4), context=ctx)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_matcher_golden_cases(path):
+    g = load_golden("matcher_cases.npz")
+    checked = 0
+    for k in range(int(g["n"])):
+        mode = fc.PROPOSED if int(g[f"mode_{k}"]) else fc.BASELINE
+        level = int(g[f"level_{k}"])
+        if path == "tensor" and (mode == fc.BASELINE or level == 4):
+            continue
+        pool = fc.DomainPool.from_tiles({level: g[f"tiles_{k}"]})
+        res = fc.best_match(g[f"range_{k}"], level, pool, fc.SPolicy(mode=mode), path=path)
+        got = (res.error, res.domain_index, res.isometry, res.s_index, res.offset)
+        assert got == tuple(int(v) for v in g[f"expect_{k}"]), (k, mode, level)
+        checked += 1
+    assert checked >= 80
+
+
+def test_empty_pool_raises():
+    pool = fc.DomainPool.from_tiles({2: [np.zeros((8, 8), np.uint8)]})
+    with pytest.raises(fc.EmptyPoolError):
+        fc.best_match(np.zeros((16, 16), np.uint8), 1, pool, fc.SPolicy())
+
+
+def test_constant_range_tie_breaks_to_first_flat_domain():
+    rng = np.random.default_rng(1234)
+    tiles = [rng.integers(0, 256, (16, 16)).astype(np.uint8) for _ in range(2)]
+    tiles += [np.full((16, 16), 100, np.uint8), rng.integers(0, 256, (16, 16)).astype(np.uint8),
+              np.full((16, 16), 30, np.uint8)]
+    pool = fc.DomainPool.from_tiles({1: tiles})
+    for path in PATHS:
+        res = fc.best_match(np.full((16, 16), 77, np.uint8), 1, pool, fc.SPolicy(), path=path)
+        assert (res.error, res.domain_index, res.isometry, res.s_index, res.offset) == (0, 2, 0, 0, 77)
+
+
+def test_scan_candidates_dropin_reference_layout(ctx):
+    rng = np.random.default_rng(7)
+    for mode in ("proposed", "baseline"):
+        for level in (2, 3, 4):
+            side = O.LEVEL_RANGE_SIDES[level - 1]
+            tiles = rng.integers(0, 256, (13, side, side)).astype(np.uint8)
+            means = tiles.reshape(13, -1).astype(np.int64).sum(axis=1) / (side * side)
+            s_set = O.DEFAULT_PROPOSED_SETS[level - 1] if mode == "proposed" else O.DEFAULT_BASELINE_SET
+            q = O.candidate_operands(tiles, means, s_set, mode == "baseline")
+            r = rng.integers(0, 256, (37, side * side)).astype(np.int16)
+            rm = r.astype(np.int64).sum(axis=1) / (side * side)
+            e_ref, i_ref = O.scan_candidates(r, rm, q, means, s_set, mode == "baseline")
+            e_dev, i_dev = ctx.scan_candidates(r, rm, q, means, s_set, mode == "baseline")
+            assert np.array_equal(e_ref, e_dev) and np.array_equal(i_ref, i_dev)
+
+
+def _encode_golden(g, tag, path, taus=None):
+    img = g[f"image_{tag}"]
+    caps = tuple(int(v) for v in g[f"caps_{tag}"])
+    strides = tuple(int(v) for v in g[f"strides_{tag}"])
+    mode = fc.PROPOSED if int(g[f"mode_{tag}"]) else fc.BASELINE
+    thr = tuple(float(v) for v in g[f"thresholds_{tag}"])
+    params = fc.PoolParams(pool_cap=max(caps), strides=strides, level_caps=caps,
+                           entropy_thresholds=taus)
+    cfg = fc.EncoderConfig(pool=params, policy=fc.SPolicy(mode=mode), thresholds=thr, path=path)
+    return fc.encode(fc.GrayImage(img), cfg)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("tag", ["tiled_proposed", "tiled_baseline", "tiled4_proposed",
+                                 "tiled4_baseline", "noise", "flat", "darkbright_proposed",
+                                 "darkbright_baseline", "c1"])
+def test_encode_bytes_identical(tag, path):
+    g = load_golden("encode_cases.npz")
+    if path == "tensor" and "baseline" in tag:
+        pytest.skip("tensor path is proposed-mode only")
+    stream, report = _encode_golden(g, tag, path if "baseline" not in tag else "auto")
+    assert fc.serialize(stream) == g[f"bytes_{tag}"].tobytes()
+    assert report.collage_ssd == int(g[f"collage_{tag}"])
+    dec = fc.decode(stream)
+    assert abs(fc.psnr(fc.GrayImage(g[f"image_{tag}"]), dec) - float(g[f"psnr_{tag}"])) < 0.01
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_encode_lena_operating_point(path):
+    g = load_golden("encode_lena.npz")
+    stream, report = _encode_golden(g, "lena256", path)
+    assert fc.serialize(stream) == g["bytes_lena256"].tobytes()
+    assert abs(report.comp_ratio_payload - 9.89) < 0.01
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("tag", ["c2", "c3_1"])
+def test_encode_c2_c3_bytes_identical(tag, path):
+    g = load_golden("encode_c2.npz")
+    stream, report = _encode_golden(g, tag, path)
+    assert fc.serialize(stream) == g[f"bytes_{tag}"].tobytes()
+    assert report.collage_ssd == int(g[f"collage_{tag}"])
+
+
+def test_entropy_threshold_compaction_equals_caps():
+    """Device threshold compaction (keep ent > tau) == reference caps #{ent > tau}."""
+    g = load_golden("encode_c2.npz")
+    wl = W.WORKLOADS["c2"]
+    taus = tuple(None if one else t for one, t in zip(wl.cap_one, wl.taus))
+    stream, _ = _encode_golden(g, "c2", "auto", taus=taus)
+    assert fc.serialize(stream) == g["bytes_c2"].tobytes()
