@@ -56,6 +56,7 @@ typedef struct fc_stats {
   float main_ms;            /* tensor path: main contraction kernel only */
   float fix_ms;             /* tensor path: exact clamp-correction kernel */
   int64_t fix_pairs;        /* (range, column) pairs re-evaluated exactly */
+  int64_t rescans;          /* tensor path: epilogue warp rescans (tie / improvement checks) */
 } fc_stats;
 
 int fc_version(void);
@@ -116,6 +117,11 @@ int fc_scan_candidates(fc_ctx* ctx, const int16_t* ranges, const double* rmeans,
                        int64_t* out_idx);
 
 int fc_last_stats(fc_ctx* ctx, fc_stats* out);
+/* The context's CUDA stream (cudaStream_t) so callers can time on it. */
+int fc_get_stream(fc_ctx* ctx, void** out_stream);
+/* Kernels this library launched on the context since creation (excludes CUB
+ * sort internals and memcpy/memset). */
+int fc_launch_count(fc_ctx* ctx, int64_t* out_count);
 
 #ifdef __cplusplus
 }

@@ -47,6 +47,7 @@ class FcStats(ctypes.Structure):
         ("main_ms", ctypes.c_float),
         ("fix_ms", ctypes.c_float),
         ("fix_pairs", ctypes.c_int64),
+        ("rescans", ctypes.c_int64),
     ]
 
 
@@ -74,6 +75,8 @@ _SIGNATURES = {
     "fc_scan_candidates": ([_P, _P, _P, _I64, _I32, _P, _P, _I64, _P, _I32, _I32, _P, _P],
                            ctypes.c_int),
     "fc_last_stats": ([_P, ctypes.POINTER(FcStats)], ctypes.c_int),
+    "fc_get_stream": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
+    "fc_launch_count": ([_P, ctypes.POINTER(_I64)], ctypes.c_int),
 }
 
 _lib = None
@@ -249,6 +252,17 @@ class Context:
 
     def synchronize(self):
         self.check(self.lib.fc_synchronize(self.handle))
+
+    def stream_handle(self) -> int:
+        """cudaStream_t of this context (for timing with events on its stream)."""
+        h = ctypes.c_void_p()
+        self.check(self.lib.fc_get_stream(self.handle, ctypes.byref(h)))
+        return int(h.value or 0)
+
+    def launch_count(self) -> int:
+        n = ctypes.c_int64()
+        self.check(self.lib.fc_launch_count(self.handle, ctypes.byref(n)))
+        return int(n.value)
 
 
 _default = {}

@@ -67,6 +67,7 @@ class EncodeReport:
     encode_time_s: float
     comparisons: int = 0
     scan_device_ms: float = 0.0
+    level_stats: list = field(default_factory=list)  # per matched level: device counters
 
     def to_lines(self) -> list:
         rows = [
@@ -142,13 +143,16 @@ def run_quadtree(width: int, height: int, thresholds, match_level):
     return leaves
 
 
-def encode(image: GrayImage, config: EncoderConfig, context=None):
-    """Compress an image whose sides are multiples of 16 -> (CompressedStream, EncodeReport)."""
+def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=None):
+    """Compress an image whose sides are multiples of 16 -> (CompressedStream, EncodeReport).
+
+    ``device_image``: optional HBM-resident copy of the pixels (see build_pool).
+    """
     if image.width % 16 or image.height % 16:
         raise ValueError(f"dimensions not multiple of 16: {image.width}x{image.height}")
     t_start = time.perf_counter()
     ctx = context if context is not None else _native.default_context()
-    pool = build_pool(image, config.pool, context=ctx)
+    pool = build_pool(image, config.pool, context=ctx, device_image=device_image)
     pool_time = time.perf_counter() - t_start
     policy = config.policy
     baseline = policy.mode == BASELINE
@@ -156,6 +160,7 @@ def encode(image: GrayImage, config: EncoderConfig, context=None):
     scans = {}
     comparisons = 0
     scan_ms = 0.0
+    level_stats = []
 
     def match_fn(level, o):
         nonlocal comparisons, scan_ms
@@ -163,11 +168,19 @@ def encode(image: GrayImage, config: EncoderConfig, context=None):
             from .errors import EmptyPoolError
 
             raise EmptyPoolError(f"no domain entries at level {level}")
-        ctx.level_prepare(level, baseline, policy.s_set(level), path)
+        lvl_path = path
+        if path == _native.PATH_TENSOR and (baseline or level == 4):
+            lvl_path = _native.PATH_EXACT  # the contraction covers proposed mode, B >= 4
+        ctx.level_prepare(level, baseline, policy.s_set(level), lvl_path)
         err, idx, rmean = ctx.match_level(level, o)
         st = ctx.stats()
         comparisons += int(st.comparisons)
         scan_ms += float(st.scan_ms)
+        level_stats.append(dict(level=level, ranges=int(st.ranges), columns=int(st.columns),
+                                comparisons=int(st.comparisons), path=int(st.path),
+                                launches=int(st.kernel_launches), scan_ms=float(st.scan_ms),
+                                main_ms=float(st.main_ms), fix_ms=float(st.fix_ms),
+                                fix_pairs=int(st.fix_pairs), rescans=int(st.rescans)))
         scans[level] = (err, idx, rmean)
         return err
 
@@ -216,7 +229,7 @@ def encode(image: GrayImage, config: EncoderConfig, context=None):
         bpp_payload=payload / pixels, bpp_total=file_bytes * 8 / pixels,
         comp_ratio_payload=pixels * 8 / payload if payload else float("inf"),
         comp_ratio_total=pixels / file_bytes, pool_time_s=pool_time, encode_time_s=encode_time,
-        comparisons=comparisons, scan_device_ms=scan_ms)
+        comparisons=comparisons, scan_device_ms=scan_ms, level_stats=level_stats)
     return stream, report
 
 

@@ -84,12 +84,13 @@ void fc_ctx_destroy(fc_ctx* c) {
   DevBuf* bufs[] = {&c->img, &c->ent_scratch, &c->key_in, &c->key_out, &c->val_in, &c->val_out,
                     &c->cub_tmp, &c->count_buf, &c->origins, &c->rtiles, &c->rmean, &c->roff,
                     &c->rsq, &c->keys, &c->out_err, &c->out_idx, &c->fix_rows, &c->fix_cols,
-                    &c->fix_jobs, &c->svals_dev, &c->iso_inv};
+                    &c->fix_jobs, &c->svals_dev, &c->iso_inv, &c->a_tiles, &c->row_meta,
+                    &c->fix_prefix, &c->tc_scratch};
   for (DevBuf* b : bufs) b->release();
   for (auto& b : c->lut) b.release();
   for (auto& L : c->lv) {
     DevBuf* lb[] = {&L.xy, &L.ent, &L.tiles, &L.sum, &L.sumsq, &L.mean, &L.cnorm, &L.qbase,
-                    &L.tc.b_tiles, &L.tc.col_meta, &L.tc.tile_meta, &L.tc.col_stats,
+                    &L.tc.b_tiles, &L.tc.hq, &L.tc.meta, &L.tc.tile_q1, &L.tc.col_stats,
                     &L.tc.reach_low, &L.tc.reach_high};
     for (DevBuf* b : lb) b->release();
   }
@@ -292,6 +293,7 @@ static int begin_match(fc_ctx* c, int level, int64_t count) {
   }
   if (!L.prepared) return set_error(c, FC_ERR_STATE, "level not prepared");
   if (count < 0) return set_error(c, FC_ERR_ARG, "negative range count");
+  c->total_launches += c->stats.kernel_launches;
   c->stats = fc_stats{};
   c->stats.ranges = count;
   c->stats.columns = L.count * L.s_count;
@@ -344,6 +346,22 @@ int fc_scan_candidates(fc_ctx* c, const int16_t* ranges, const double* rmeans, i
 
 int fc_last_stats(fc_ctx* c, fc_stats* out) {
   *out = c->stats;
+  return FC_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int fc_get_stream(fc_ctx* c, void** out_stream) {
+  if (!out_stream) return set_error(c, FC_ERR_ARG, "null output");
+  *out_stream = reinterpret_cast<void*>(c->stream);
+  return FC_OK;
+}
+
+int fc_launch_count(fc_ctx* c, int64_t* out_count) {
+  if (!out_count) return set_error(c, FC_ERR_ARG, "null output");
+  *out_count = c->total_launches + c->stats.kernel_launches;
   return FC_OK;
 }
 

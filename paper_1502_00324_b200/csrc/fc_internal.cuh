@@ -52,13 +52,14 @@ struct TcOperands {
   int64_t ncols = 0;     // real columns E*S
   int64_t ntiles = 0;    // 256-column tiles after per-group padding
   DevBuf b_tiles;        // int8 [ntiles][kpad/16][32 groups][8][16]   (UMMA K-major, no swizzle)
-  DevBuf col_meta;       // int2 [ntiles*256]: {hq = floor(Q2/2), (par<<31) | col}
-  DevBuf tile_meta;      // int4 [ntiles]: {Q1, qmin_tile, qmax_tile, ncols_real}
+  DevBuf hq;             // int32 [ntiles*256]: floor(Q2/2) (padding: 2^30)
+  DevBuf meta;           // uint32 [ntiles*256]: (Q2 & 1) << 31 | column
+  DevBuf tile_q1;        // int32 [ntiles]: the single Q1 = sum(q) of the tile's columns
   DevBuf col_stats;      // int4 [ncols]: {Q1, Q2, qmin, qmax} (unsorted order)
   DevBuf reach_low;      // int32 [ncols]: columns sorted by qmin ascending
   DevBuf reach_high;     // int32 [ncols]: columns sorted by qmax descending
-  std::vector<int> low_qmin_sorted;   // host copy: qmin of reach_low order
-  std::vector<int> high_qmax_sorted;  // host copy: qmax of reach_high order
+  int64_t low_count[256] = {0};   // #{columns with qmin < -o}      (clamp at 0 possible)
+  int64_t high_count[256] = {0};  // #{columns with qmax > 255 - o} (clamp at 255 possible)
 };
 
 struct Level {
@@ -103,9 +104,12 @@ struct Ctx {
   DevBuf ent_scratch, key_in, key_out, val_in, val_out, cub_tmp, count_buf;
   DevBuf origins, rtiles, rmean, roff, rsq, keys, out_err, out_idx;
   DevBuf fix_rows, fix_cols, fix_jobs, svals_dev;
+  DevBuf a_tiles, row_meta, fix_prefix, tc_scratch;
+  std::vector<int32_t> h_roff;
   DevBuf iso_inv;  // uint16 [4 sides][8][256] inverse isometry maps
   bool iso_ready = false;
   fc_stats stats{};
+  int64_t total_launches = 0;  // kernels launched outside the per-match stats
 };
 
 int set_error(Ctx* c, int code, const std::string& msg);
@@ -124,6 +128,9 @@ int gather_ranges(Ctx* c, Level& L, const int32_t* d_origins, int64_t M);
 int load_ranges(Ctx* c, Level& L, const uint8_t* h_tiles, int64_t M);
 int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t n_range_list,
                const int32_t* d_col_list, int64_t n_col_list, uint64_t* d_keys);
+int scan_exact_jobs(Ctx* c, Level& L, const int4* d_jobs, const int64_t* d_prefix, int n_jobs,
+                    int64_t total_blocks, const int32_t* d_sorted_ranges, const int32_t* d_low,
+                    const int32_t* d_high, uint64_t* d_keys);
 int decode_keys(Ctx* c, const uint64_t* d_keys, int64_t M, int64_t* d_err, int64_t* d_idx);
 int iso_table_offset(int side);
 int scan_rows_dropin(Ctx* c, const int16_t* ranges, const double* rmeans, int64_t M, int32_t n,

@@ -230,6 +230,7 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
         break;
     }
     FC_CUDA(c, cudaGetLastError());
+    c->total_launches += 1;
     size_t tmp = 0;
     FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, c->key_in.as<uint64_t>(),
                                                c->key_out.as<uint64_t>(), c->val_in.as<uint32_t>(),
@@ -259,6 +260,7 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
         L.tiles.as<uint8_t>(), L.sum.as<int32_t>(), L.sumsq.as<int64_t>(), L.mean.as<double>(),
         L.cnorm.as<double>());
     FC_CUDA(c, cudaGetLastError());
+    c->total_launches += 1;
     out_sizes[li] = E;
   }
   FC_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -283,6 +285,7 @@ int pool_set_level(Ctx* c, int level, int64_t count, const uint8_t* tiles) {
       L.tiles.as<uint8_t>(), L.n, count, L.xy.as<uint32_t>(), L.ent.as<double>(),
       L.sum.as<int32_t>(), L.sumsq.as<int64_t>(), L.mean.as<double>(), L.cnorm.as<double>());
   FC_CUDA(c, cudaGetLastError());
+  c->total_launches += 1;
   FC_CUDA(c, cudaStreamSynchronize(c->stream));
   return FC_OK;
 }

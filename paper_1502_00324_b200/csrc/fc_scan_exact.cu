@@ -42,54 +42,45 @@ __device__ __forceinline__ int rint_offset_baseline(double rmean, double s, doub
   return o < 0 ? 0 : (o > 255 ? 255 : o);
 }
 
-// rtiles: uint8 [M][N]; inv: uint16 [8][N] inverse isometry maps for this side
 template <int N>
-__global__ void __launch_bounds__(kColsPerBlock)
-scan_exact_kernel(const int16_t* __restrict__ qbase, int64_t ncols, int S,
-                  const double* __restrict__ svals, const double* __restrict__ dmean,
-                  const uint8_t* __restrict__ rtiles, const double* __restrict__ rmean,
-                  int64_t M, const uint16_t* __restrict__ inv,
-                  const int32_t* __restrict__ range_list, int64_t n_range_list, int64_t range_base,
-                  const int32_t* __restrict__ col_list, int64_t n_col_list, int baseline,
-                  unsigned long long* __restrict__ keys) {
+struct ExactSmem {
+  uint8_t rperm[kRB][8][N];
+  int m[kRB];
+  double rmean[kRB];
+};
+
+// One block: kRB ranges (s.m[], -1 = none) x 128 columns (one per thread,
+// col < 0 = none).  Every (range, column, isometry) error is exact.
+template <int N>
+__device__ __forceinline__ void exact_block(ExactSmem<N>& s, const int16_t* __restrict__ qbase,
+                                            int S, const double* __restrict__ svals,
+                                            const double* __restrict__ dmean,
+                                            const uint8_t* __restrict__ rtiles,
+                                            const uint16_t* __restrict__ inv, int64_t col_in,
+                                            int baseline, unsigned long long* __restrict__ keys) {
   constexpr int CH = N >= 16 ? 16 : N;  // pixels per inner chunk
   constexpr int W = CH / 4;             // packed words per chunk
-  __shared__ __align__(16) uint8_t rperm[kRB][8][N];
-  __shared__ int s_m[kRB];
-  __shared__ double s_rmean[kRB];
-
+  auto& rperm = s.rperm;
   const int tid = threadIdx.x;
-  const int64_t nrange = range_list ? n_range_list : M;
-  const int64_t r0 = range_base + (int64_t)blockIdx.y * kRB;
-  if (tid < kRB) {
-    const int64_t idx = r0 + tid;
-    int m = -1;
-    if (idx < nrange) m = range_list ? range_list[idx] : (int)idx;
-    s_m[tid] = m;
-    s_rmean[tid] = m >= 0 ? rmean[m] : 0.0;
-  }
-  __syncthreads();
   for (int i = tid; i < kRB * 8 * N; i += kColsPerBlock) {
     const int mm = i / (8 * N);
     const int rem = i - mm * 8 * N;
     const int iso = rem / N, j = rem - iso * N;
-    const int m = s_m[mm];
+    const int m = s.m[mm];
     rperm[mm][iso][j] = m >= 0 ? rtiles[(int64_t)m * N + inv[iso * N + j]] : 0;
   }
   __syncthreads();
 
-  const int64_t ci = (int64_t)blockIdx.x * kColsPerBlock + tid;
-  const int64_t ncol_eff = col_list ? n_col_list : ncols;
-  const bool valid = ci < ncol_eff;
-  const int64_t col = valid ? (col_list ? (int64_t)col_list[ci] : ci) : 0;
+  const bool valid = col_in >= 0;
+  const int64_t col = valid ? col_in : 0;
   const int64_t e = col / S;
   const int si = (int)(col - e * S);
 
   int o[kRB];
 #pragma unroll
   for (int mm = 0; mm < kRB; ++mm) {
-    o[mm] = baseline ? rint_offset_baseline(s_rmean[mm], svals[si], dmean[e])
-                     : (int)rint(s_rmean[mm]);
+    o[mm] = baseline ? rint_offset_baseline(s.rmean[mm], svals[si], dmean[e])
+                     : (int)rint(s.rmean[mm]);
   }
   unsigned acc[kRB][8];
 #pragma unroll
@@ -152,8 +143,80 @@ scan_exact_kernel(const int16_t* __restrict__ qbase, int64_t ncols, int S,
       }
     }
     best = warp_min_u64(best);
-    if (lane == 0 && s_m[mm] >= 0 && best != ~0ull) atomicMin(&keys[s_m[mm]], best);
+    if (lane == 0 && s.m[mm] >= 0 && best != ~0ull) atomicMin(&keys[s.m[mm]], best);
   }
+}
+
+// Grid-mapped scan: blockIdx.x = 128-column chunk, blockIdx.y = block of kRB
+// ranges (identity or an explicit range list), optional explicit column list.
+template <int N>
+__global__ void __launch_bounds__(kColsPerBlock)
+scan_exact_kernel(const int16_t* __restrict__ qbase, int64_t ncols, int S,
+                  const double* __restrict__ svals, const double* __restrict__ dmean,
+                  const uint8_t* __restrict__ rtiles, const double* __restrict__ rmean,
+                  int64_t M, const uint16_t* __restrict__ inv,
+                  const int32_t* __restrict__ range_list, int64_t n_range_list, int64_t range_base,
+                  const int32_t* __restrict__ col_list, int64_t n_col_list, int baseline,
+                  unsigned long long* __restrict__ keys) {
+  __shared__ __align__(16) ExactSmem<N> s;
+  const int tid = threadIdx.x;
+  const int64_t nrange = range_list ? n_range_list : M;
+  const int64_t r0 = range_base + (int64_t)blockIdx.y * kRB;
+  if (tid < kRB) {
+    const int64_t idx = r0 + tid;
+    int m = -1;
+    if (idx < nrange) m = range_list ? range_list[idx] : (int)idx;
+    s.m[tid] = m;
+    s.rmean[tid] = m >= 0 ? rmean[m] : 0.0;
+  }
+  const int64_t ci = (int64_t)blockIdx.x * kColsPerBlock + tid;
+  const int64_t ncol_eff = col_list ? n_col_list : ncols;
+  const int64_t col = ci < ncol_eff ? (col_list ? (int64_t)col_list[ci] : ci) : -1;
+  __syncthreads();
+  exact_block<N>(s, qbase, S, svals, dmean, rtiles, inv, col, baseline, keys);
+}
+
+// Job-list scan (tensor-path clamp corrections): job j covers the ranges
+// sorted_ranges[r_off, r_off + r_cnt) against the first col_cnt columns of
+// column list `list` (0 = reach_low, 1 = reach_high).  Blocks are laid out
+// densely: block b belongs to the job whose prefix[j] <= b < prefix[j + 1].
+template <int N>
+__global__ void __launch_bounds__(kColsPerBlock)
+scan_jobs_kernel(const int16_t* __restrict__ qbase, int S, const double* __restrict__ svals,
+                 const double* __restrict__ dmean, const uint8_t* __restrict__ rtiles,
+                 const double* __restrict__ rmean, const uint16_t* __restrict__ inv,
+                 const int4* __restrict__ jobs, const int64_t* __restrict__ prefix, int n_jobs,
+                 const int32_t* __restrict__ sorted_ranges, const int32_t* __restrict__ list_low,
+                 const int32_t* __restrict__ list_high, int baseline,
+                 unsigned long long* __restrict__ keys) {
+  __shared__ __align__(16) ExactSmem<N> s;
+  __shared__ int s_job;
+  const int tid = threadIdx.x;
+  const int64_t b = blockIdx.x;
+  if (tid == 0) {
+    int lo = 0, hi = n_jobs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (prefix[mid] <= b) lo = mid; else hi = mid - 1;
+    }
+    s_job = lo;
+  }
+  __syncthreads();
+  const int4 job = jobs[s_job];  // {list, r_off, r_cnt, col_cnt}
+  const int64_t local = b - prefix[s_job];
+  const int64_t ncc = (job.w + kColsPerBlock - 1) / kColsPerBlock;
+  const int64_t rb = local / ncc, cc = local - rb * ncc;
+  if (tid < kRB) {
+    const int64_t idx = rb * kRB + tid;
+    const int m = idx < job.z ? sorted_ranges[job.y + idx] : -1;
+    s.m[tid] = m;
+    s.rmean[tid] = m >= 0 ? rmean[m] : 0.0;
+  }
+  const int64_t ci = cc * kColsPerBlock + tid;
+  const int32_t* list = job.x ? list_high : list_low;
+  const int64_t col = ci < job.w ? (int64_t)list[ci] : -1;
+  __syncthreads();
+  exact_block<N>(s, qbase, S, svals, dmean, rtiles, inv, col, baseline, keys);
 }
 
 // Drop-in for _scan.py:14 with arbitrary candidate rows (reference layout).
@@ -331,6 +394,7 @@ int level_prepare_exact(Ctx* c, Level& L) {
         L.tiles.as<uint8_t>(), L.mean.as<double>(), L.count, L.n, L.s_count, d_s, L.baseline,
         L.qbase.as<int16_t>());
     FC_CUDA(c, cudaGetLastError());
+    c->total_launches += 1;
     FC_CUDA(c, cudaStreamSynchronize(c->stream));
   }
   return FC_OK;
@@ -400,6 +464,33 @@ int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t
     FC_CUDA(c, cudaGetLastError());
     c->stats.kernel_launches += 1;
   }
+  return FC_OK;
+}
+
+int scan_exact_jobs(Ctx* c, Level& L, const int4* d_jobs, const int64_t* d_prefix, int n_jobs,
+                    int64_t total_blocks, const int32_t* d_sorted_ranges, const int32_t* d_low,
+                    const int32_t* d_high, uint64_t* d_keys) {
+  if (n_jobs == 0 || total_blocks == 0) return FC_OK;
+  FC_TRY(ensure_iso_tables(c));
+  FC_CUDA(c, c->svals_dev.reserve(kMaxS * 8));
+  double* d_s = c->svals_dev.as<double>();
+  FC_CUDA(c, cudaMemcpyAsync(d_s, L.svals, L.s_count * 8, cudaMemcpyHostToDevice, c->stream));
+  const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
+  auto* keys = reinterpret_cast<unsigned long long*>(d_keys);
+#define FC_LAUNCH_JOBS(NN)                                                                      \
+  scan_jobs_kernel<NN><<<(unsigned)total_blocks, kColsPerBlock, 0, c->stream>>>(                 \
+      L.qbase.as<int16_t>(), L.s_count, d_s, L.mean.as<double>(), c->rtiles.as<uint8_t>(),        \
+      c->rmean.as<double>(), inv, d_jobs, d_prefix, n_jobs, d_sorted_ranges, d_low, d_high,       \
+      L.baseline, keys)
+  switch (L.n) {
+    case 256: FC_LAUNCH_JOBS(256); break;
+    case 64: FC_LAUNCH_JOBS(64); break;
+    case 16: FC_LAUNCH_JOBS(16); break;
+    default: FC_LAUNCH_JOBS(4); break;
+  }
+#undef FC_LAUNCH_JOBS
+  FC_CUDA(c, cudaGetLastError());
+  c->stats.kernel_launches += 1;
   return FC_OK;
 }
 

@@ -172,10 +172,18 @@ class DomainPool:
         return cls(PoolParams(pool_cap=cap), width, height, sizes, ctx)
 
 
-def build_pool(image: GrayImage, params: PoolParams, context=None) -> DomainPool:
-    """Rank every lattice domain by entropy and keep the top cap per level (device)."""
+def build_pool(image: GrayImage, params: PoolParams, context=None, device_image=None) -> DomainPool:
+    """Rank every lattice domain by entropy and keep the top cap per level (device).
+
+    ``device_image`` (optional): an object exposing ``data_ptr()`` (e.g. a CUDA
+    uint8 tensor) holding the same pixels already resident in HBM; the
+    context then adopts it instead of copying ``image`` from the host.
+    """
     ctx = context if context is not None else _native.Context()
-    ctx.set_image(image.pixels)
+    if device_image is not None:
+        ctx.set_image_device(int(device_image.data_ptr()), image.width, image.height)
+    else:
+        ctx.set_image(image.pixels)
     caps, taus, use_tau = [], [], []
     for level in (1, 2, 3, 4):
         tau = params.tau(level)
