@@ -48,13 +48,14 @@ struct DevBuf {
 struct TcOperands {
   bool ready = false;
   int planes = 1;        // int8 planes of q (1 or 2)
-  int kpad = 0;          // K bytes per row after plane concat + padding (multiple of 32)
+  int m_digits = 1;      // base-255 digit slots carrying hq = floor(Q2/2) in the K extra block
+  int kpad = 0;          // K bytes per row: planes*B*B + m_digits + 4, padded to 32
   int64_t ncols = 0;     // real columns E*S
-  int64_t ntiles = 0;    // 256-column tiles after per-group padding
+  int64_t ntiles = 0;    // 256-column tiles (the last one padded)
   DevBuf b_tiles;        // int8 [ntiles][kpad/16][32 groups][8][16]   (UMMA K-major, no swizzle)
-  DevBuf hq;             // int32 [ntiles*256]: floor(Q2/2) (padding: 2^30)
-  DevBuf meta;           // uint32 [ntiles*256]: (Q2 & 1) << 31 | column
-  DevBuf tile_q1;        // int32 [ntiles]: the single Q1 = sum(q) of the tile's columns
+  DevBuf hq;             // (unused; kept for ABI-stable struct layout in tools)
+  DevBuf meta;           // uint32 [ntiles*256]: (Q2 & 1) << 31 | column, 0xffffffff = padding
+  DevBuf tile_q1;        // (unused)
   DevBuf col_stats;      // int4 [ncols]: {Q1, Q2, qmin, qmax} (unsorted order)
   DevBuf reach_low;      // int32 [ncols]: columns sorted by qmin ascending
   DevBuf reach_high;     // int32 [ncols]: columns sorted by qmax descending
