@@ -36,10 +36,11 @@
 //   warp 0  producer: cp.async.bulk (TMA engine) of the A row tiles and the
 //           B column tiles + their column map into a STAGES-deep ring
 //   warp 1  MMA issuer (warp-uniform, elect.sync inside the asm):
-//           tcgen05.mma.kind::i8, M=128, N=128, K=32 per instruction, into one
-//           of four TMEM accumulators (4 x 128 columns = all 512 TMEM columns)
+//           tcgen05.mma.kind::i8, M=128, N=256, K=32 per instruction, into one
+//           of two TMEM accumulators (2 x 256 columns = all 512 TMEM columns)
 //   warp 2  TMEM allocator
-//   warps 4..19 epilogue, 4 groups of 4 warps, group k drains accumulator k:
+//   warps 4..19 epilogue, 2 groups of 8 warps (2 per TMEM sub-partition, one
+//           per 128-column half), group k drains accumulator k:
 //           tcgen05.ld 32x32b + VIMNMX3 running minimum, per-range atomicMin
 #include <cub/cub.cuh>
 
@@ -53,10 +54,10 @@ namespace {
 
 constexpr int kTileN = 256;      // columns per B stage tile
 constexpr int kTileM = 128;      // rows per row tile = 16 ranges x 8 isometries
-constexpr int kHalfN = 128;      // columns per MMA / TMEM accumulator
-constexpr int kNumAcc = 4;       // TMEM accumulators (4 x 128 columns = all 512)
-constexpr int kEpiGroups = 4;    // one epilogue group per accumulator
-constexpr int kEpiWarps = 4 * kEpiGroups;
+constexpr int kAccN = 256;       // columns per MMA / TMEM accumulator
+constexpr int kNumAcc = 2;       // TMEM accumulators (2 x 256 columns = all 512)
+constexpr int kEpiGroups = 2;    // one epilogue group (8 warps) per accumulator
+constexpr int kEpiWarps = 8 * kEpiGroups;
 constexpr int kThreads = (4 + kEpiWarps) * 32;
 constexpr int kMaxRG = 8;
 constexpr int kSmemBudget = 220 * 1024;
@@ -92,12 +93,22 @@ __host__ __device__ inline uint32_t smem_bytes(const TcParams& p) {
 
 // One 32-slot chunk of a row: if its minimum strictly improves the row's
 // key2, record the first slot holding that minimum.
+__device__ __forceinline__ int min32(const int (&v)[32]) {
+  // 3-ary tree: 11 + 4 + 2 + 1 VIMNMX3, depth 4
+  int a[11];
+#pragma unroll
+  for (int k = 0; k < 10; ++k) a[k] = __vimin3_s32(v[3 * k], v[3 * k + 1], v[3 * k + 2]);
+  a[10] = min(v[30], v[31]);
+  const int b0 = __vimin3_s32(a[0], a[1], a[2]);
+  const int b1 = __vimin3_s32(a[3], a[4], a[5]);
+  const int b2 = __vimin3_s32(a[6], a[7], a[8]);
+  const int b3 = min(a[9], a[10]);
+  return min(__vimin3_s32(b0, b1, b2), b3);
+}
+
 __device__ __forceinline__ void chunk_update(const int (&v)[32], int par, int slot0,
                                              const int32_t* colmap_s, int& best2, int& bcol) {
-  int m = __vimin3_s32(v[0], v[1], v[2]);
-#pragma unroll
-  for (int j = 3; j < 31; j += 2) m = __vimin3_s32(m, v[j], v[j + 1]);
-  m = min(m, v[31]);
+  const int m = min32(v);
   if (m != kNone && 2 * m + par < best2) {
     int bj = 31;
 #pragma unroll
@@ -109,8 +120,8 @@ __device__ __forceinline__ void chunk_update(const int (&v)[32], int par, int sl
 
 // Work order (all roles derive it identically): unit u -> row group
 // g = u % n_rgroups, column-tile span u / n_rgroups; inside a unit: tiles t,
-// row tiles r, halves h; the half-tile counter H selects accumulator H % 4,
-// which epilogue group H % 4 drains.
+// row tiles r; the (tile, row tile) counter H selects accumulator H % 2,
+// which epilogue group H % 2 drains.
 __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int KPAD = p.kpad, RG = p.rg, STAGES = p.stages;
@@ -137,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     }
     for (int b = 0; b < kNumAcc; ++b) {
       ptx::mbar_init(tfull_bar(b), 1);
-      ptx::mbar_init(tempty_bar(b), 4);
+      ptx::mbar_init(tempty_bar(b), 8);
     }
     ptx::mbar_init(afull_bar, 1);
     ptx::mbar_init(aempty_bar, 1);
@@ -160,12 +171,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
         const int g = (int)(u % n_rg);
         const int t0 = (int)(u / n_rg) * CT;
         const int t1 = min(p.ntiles, t0 + CT);
-        ptx::mbar_wait(aempty_bar, (U & 1) ^ 1);
+        ptx::mbar_wait_sleep(aempty_bar, (U & 1) ^ 1);
         ptx::mbar_expect_tx(afull_bar, kA);
         ptx::bulk_g2s(ptx::smem_u32(sA), p.a_tiles + (size_t)g * kA, kA, afull_bar);
         for (int t = t0; t < t1; ++t, ++L) {
           const int s = L % STAGES;
-          ptx::mbar_wait(empty_bar(s), ((L / STAGES) & 1) ^ 1);
+          ptx::mbar_wait_sleep(empty_bar(s), ((L / STAGES) & 1) ^ 1);
           uint8_t* st = sStage + s * kStage;
           ptx::mbar_expect_tx(full_bar(s), kStage);
           ptx::bulk_g2s(ptx::smem_u32(st), p.b_tiles + (size_t)t * kB, kB, full_bar(s));
@@ -176,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (warp-uniform, one elected lane issues) ----------------
-    constexpr uint32_t kIdesc = ptx::idesc_i8(kTileM, kHalfN);
+    constexpr uint32_t kIdesc = ptx::idesc_i8(kTileM, kAccN);
     const int ksteps = KPAD / 32;
     // descriptor start-address field is addr >> 4: stepping K by 32 bytes
     // (two 16-byte core-matrix chunks) adds 2*LBO >> 4
@@ -187,27 +198,24 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++U) {
       const int t0 = (int)(u / n_rg) * CT;
       const int t1 = min(p.ntiles, t0 + CT);
-      ptx::mbar_wait(afull_bar, U & 1);
+      ptx::mbar_wait_sleep(afull_bar, U & 1);
       ptx::tc_fence_after();
       for (int t = t0; t < t1; ++t, ++L) {
         const int s = L % STAGES;
-        ptx::mbar_wait(full_bar(s), (L / STAGES) & 1);
+        ptx::mbar_wait_sleep(full_bar(s), (L / STAGES) & 1);
         ptx::tc_fence_after();
         const uint32_t b_addr = ptx::smem_u32(sStage + s * kStage);
-        for (int r = 0; r < RG; ++r) {
+        const uint64_t bd0 = ptx::umma_desc(b_addr, kTileN * 16, 128);
+        for (int r = 0; r < RG; ++r, ++H) {
           const uint64_t ad0 = ptx::umma_desc(a_base + r * (kTileM * KPAD), kTileM * 16, 128);
-#pragma unroll
-          for (int h = 0; h < 2; ++h, ++H) {
-            const int acc = H % kNumAcc;
-            const uint64_t bd0 = ptx::umma_desc(b_addr + h * (kHalfN / 8) * 128, kTileN * 16, 128);
-            ptx::mbar_wait(tempty_bar(acc), ((H / kNumAcc) & 1) ^ 1);
-            ptx::tc_fence_after();
-            const uint32_t d = tmem_base + acc * kHalfN;
-            ptx::umma_i8_elect(d, ad0, bd0, kIdesc, 0u);
-            for (int ks = 1; ks < ksteps; ++ks)
-              ptx::umma_i8_elect(d, ad0 + ks * kAStep, bd0 + ks * kBStep, kIdesc, 1u);
-            ptx::umma_commit_elect(tfull_bar(acc));
-          }
+          const int acc = H % kNumAcc;
+          ptx::mbar_wait_sleep(tempty_bar(acc), ((H / kNumAcc) & 1) ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t d = tmem_base + acc * kAccN;
+          ptx::umma_i8_elect(d, ad0, bd0, kIdesc, 0u);
+          for (int ks = 1; ks < ksteps; ++ks)
+            ptx::umma_i8_elect(d, ad0 + ks * kAStep, bd0 + ks * kBStep, kIdesc, 1u);
+          ptx::umma_commit_elect(tfull_bar(acc));
         }
         ptx::umma_commit_elect(empty_bar(s));
       }
@@ -216,13 +224,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   } else if (warp >= 4) {
     // ---------------- epilogue: 4 groups x 4 warps ----------------
     const int e = warp - 4;
-    const int grp = e >> 2;      // accumulator this group drains (H % 4 == grp)
+    const int grp = e >> 3;      // accumulator this group drains (H % 2 == grp)
+    const int ch = (e >> 2) & 1; // column half of the 256-wide accumulator
     const int sp = warp & 3;     // TMEM sub-partition (lanes 32*sp .. 32*sp+31)
     const int row = sp * 32 + lane;
     const int S = p.S;
     const int iso = lane & 7;
-    const uint32_t taddr = tmem_base + ((uint32_t)(sp * 32) << 16) + grp * kHalfN;
-    const int per_tile = 2 * RG;  // half tiles per column tile
+    const uint32_t taddr = tmem_base + ((uint32_t)(sp * 32) << 16) + grp * kAccN + ch * 128;
+    const int per_tile = RG;     // accumulators per column tile
     uint32_t L = 0, H = 0;
     for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
       const int g = (int)(u % n_rg);
@@ -238,23 +247,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
       for (int t = t0; t < t1; ++t, ++L, H += per_tile) {
         const int s = L % STAGES;
         const int2 tinfo = p.tile_info[t];  // {parity, valid slots}
-        ptx::mbar_wait(full_bar(s), (L / STAGES) & 1);
+        ptx::mbar_wait_sleep(full_bar(s), (L / STAGES) & 1);
         const int32_t* colmap_s = reinterpret_cast<const int32_t*>(sStage + s * kStage + kB);
-        // this group's half tiles of column tile t: H + i with (H + i) % 4 == grp
+        // this group's row tiles of column tile t: H + r with (H + r) % 2 == grp
 #pragma unroll 1
-        for (int i = (int)((grp - H) & 3u); i < per_tile; i += kNumAcc) {
-          const int r = i >> 1, h = i & 1;
-          const uint32_t HH = H + i;
-          ptx::mbar_wait(tfull_bar(grp), (HH / kNumAcc) & 1);
+        for (int r = (int)((grp - H) & 1u); r < per_tile; r += kNumAcc) {
+          const uint32_t HH = H + r;
+          ptx::mbar_wait_sleep(tfull_bar(grp), (HH / kNumAcc) & 1);
           ptx::tc_fence_after();
           int b2 = best2[r], bc = bcol[r];
-          const int slot_h = h * kHalfN;
+          const int slot_h = ch * 128;
 #pragma unroll
           for (int c = 0; c < 4; c += 2) {
             int va[32], vb[32];
             ptx::tmem_ld32(taddr + c * 32, va);
             ptx::tmem_ld32(taddr + (c + 1) * 32, vb);
             ptx::tmem_wait_ld();
+            if (c == 2) {
+              // every value of this accumulator is in registers: hand it back
+              // to the MMA warp before the arithmetic
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive(tempty_bar(grp));
+            }
             if (tinfo.y < kTileN) {  // mask padding slots (last tile of a group)
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
@@ -267,9 +282,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
           }
           best2[r] = b2;
           bcol[r] = bc;
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(tempty_bar(grp));
         }
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(empty_bar(s));
