@@ -18,10 +18,11 @@
 // columns are laid out in two groups, even-Q1 then odd-Q1, each in ascending
 // candidate order and padded to whole 256-column tiles.  Inside a tile key2 =
 // 2*kh + par_tile is a monotone function of kh; key2 values of different
-// groups never tie; inside a group later columns never win ties.  So each TMEM
-// row (range, isometry) keeps a running (key2, column) with ONE VIMNMX3 per two
-// accumulator elements, and locates the first argmin column of a 32-column
-// chunk only when the chunk strictly improves the row.  The final packed key
+// groups never tie.  Tiles are scanned in decreasing column order, so inside a
+// group a later-visited (smaller) column wins ties.  Each TMEM row (range,
+// isometry) keeps a running (key2, column) with ONE VIMNMX3 per two
+// accumulator elements and locates the first argmin column of a 64-column
+// block only when the block improves (or ties) the row.  The final packed key
 // (err << 32) | c per range is reduced with shuffles and atomicMin, giving the
 // reference's lexicographically first minimum independent of scheduling.
 //
@@ -39,12 +40,13 @@
 //           tcgen05.mma.kind::i8, M=128, N=256, K=32 per instruction, into one
 //           of two TMEM accumulators (2 x 256 columns = all 512 TMEM columns)
 //   warp 2  TMEM allocator
-//   warps 4..19 epilogue, 2 groups of 8 warps (2 per TMEM sub-partition, one
-//           per 128-column half), group k drains accumulator k:
+//   warps 4..19 epilogue, 4 per TMEM sub-partition (one per 64-column
+//           quarter), all draining each accumulator in turn:
 //           tcgen05.ld 32x32b + VIMNMX3 running minimum, per-range atomicMin
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fc_internal.cuh"
 #include "fc_tc_ptx.cuh"
@@ -56,8 +58,7 @@ constexpr int kTileN = 256;      // columns per B stage tile
 constexpr int kTileM = 128;      // rows per row tile = 16 ranges x 8 isometries
 constexpr int kAccN = 256;       // columns per MMA / TMEM accumulator
 constexpr int kNumAcc = 2;       // TMEM accumulators (2 x 256 columns = all 512)
-constexpr int kEpiGroups = 2;    // one epilogue group (8 warps) per accumulator
-constexpr int kEpiWarps = 8 * kEpiGroups;
+constexpr int kEpiWarps = 16;    // all drain every accumulator (4 per TMEM sub-partition)
 constexpr int kThreads = (4 + kEpiWarps) * 32;
 constexpr int kMaxRG = 8;
 constexpr int kSmemBudget = 220 * 1024;
@@ -78,6 +79,7 @@ struct TcParams {
   int ntiles;
   int tiles_per_unit;
   int64_t n_units;
+  int debug_mode;  // 1: epilogue only drains TMEM (pipeline ceiling probe); results invalid
 };
 
 __host__ __device__ inline uint32_t a_bytes(const TcParams& p) { return p.rg * kTileM * p.kpad; }
@@ -91,10 +93,8 @@ __host__ __device__ inline uint32_t smem_bytes(const TcParams& p) {
   return raw < 116 * 1024 ? 116 * 1024 : raw;  // one CTA (owning all 512 TMEM columns) per SM
 }
 
-// One 32-slot chunk of a row: if its minimum strictly improves the row's
-// key2, record the first slot holding that minimum.
+// 3-ary min tree over 32 values: 10 VIMNMX3 + 1 VIMNMX, then 4 + 1.
 __device__ __forceinline__ int min32(const int (&v)[32]) {
-  // 3-ary tree: 11 + 4 + 2 + 1 VIMNMX3, depth 4
   int a[11];
 #pragma unroll
   for (int k = 0; k < 10; ++k) a[k] = __vimin3_s32(v[3 * k], v[3 * k + 1], v[3 * k + 2]);
@@ -102,20 +102,25 @@ __device__ __forceinline__ int min32(const int (&v)[32]) {
   const int b0 = __vimin3_s32(a[0], a[1], a[2]);
   const int b1 = __vimin3_s32(a[3], a[4], a[5]);
   const int b2 = __vimin3_s32(a[6], a[7], a[8]);
-  const int b3 = min(a[9], a[10]);
-  return min(__vimin3_s32(b0, b1, b2), b3);
+  return min(__vimin3_s32(b0, b1, b2), min(a[9], a[10]));
 }
 
-__device__ __forceinline__ void chunk_update(const int (&v)[32], int par, int slot0,
-                                             const int32_t* colmap_s, int& best2, int& bcol) {
-  const int m = min32(v);
-  if (m != kNone && 2 * m + par < best2) {
-    int bj = 31;
+// First index j with v[j] == m (m is known to occur).
+__device__ __forceinline__ int first_eq(const int (&v)[32], int m) {
+  int j = 31;
 #pragma unroll
-    for (int j = 30; j >= 0; --j) bj = (v[j] == m) ? j : bj;
-    best2 = 2 * m + par;
-    bcol = colmap_s[slot0 + bj];
-  }
+  for (int k = 30; k >= 0; --k) j = (v[k] == m) ? k : j;
+  return j;
+}
+
+// Row state: best2 = 2*kh + par of the row's best so far, bcol its column.
+// Tiles are visited in DECREASING column order (the entropy-ranked pool puts
+// the usually-better low-entropy domains last, so scanning backwards finds
+// them first and the running minimum rarely changes); an equal key2 at a
+// smaller column must then win, so a block updates iff 2*m + par <= best2
+// <=>  m < ((best2 - par) >> 1) + 1.
+__device__ __forceinline__ int improve_limit(int best2, int par) {
+  return (int)((((long long)best2 - par) >> 1) + 1);
 }
 
 // Work order (all roles derive it identically): unit u -> row group
@@ -148,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     }
     for (int b = 0; b < kNumAcc; ++b) {
       ptx::mbar_init(tfull_bar(b), 1);
-      ptx::mbar_init(tempty_bar(b), 8);
+      ptx::mbar_init(tempty_bar(b), kEpiWarps);
     }
     ptx::mbar_init(afull_bar, 1);
     ptx::mbar_init(aempty_bar, 1);
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
         ptx::mbar_wait_sleep(aempty_bar, (U & 1) ^ 1);
         ptx::mbar_expect_tx(afull_bar, kA);
         ptx::bulk_g2s(ptx::smem_u32(sA), p.a_tiles + (size_t)g * kA, kA, afull_bar);
-        for (int t = t0; t < t1; ++t, ++L) {
+        for (int t = t1 - 1; t >= t0; --t, ++L) {
           const int s = L % STAGES;
           ptx::mbar_wait_sleep(empty_bar(s), ((L / STAGES) & 1) ^ 1);
           uint8_t* st = sStage + s * kStage;
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
       const int t1 = min(p.ntiles, t0 + CT);
       ptx::mbar_wait_sleep(afull_bar, U & 1);
       ptx::tc_fence_after();
-      for (int t = t0; t < t1; ++t, ++L) {
+      for (int t = t1 - 1; t >= t0; --t, ++L) {
         const int s = L % STAGES;
         ptx::mbar_wait_sleep(full_bar(s), (L / STAGES) & 1);
         ptx::tc_fence_after();
@@ -222,16 +227,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
       ptx::umma_commit_elect(aempty_bar);
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue: 4 groups x 4 warps ----------------
+    // ---------------- epilogue: 16 warps drain every accumulator ----------------
     const int e = warp - 4;
-    const int grp = e >> 3;      // accumulator this group drains (H % 2 == grp)
-    const int ch = (e >> 2) & 1; // column half of the 256-wide accumulator
+    const int cq = e >> 2;       // 64-column quarter of the 256-wide accumulator
     const int sp = warp & 3;     // TMEM sub-partition (lanes 32*sp .. 32*sp+31)
     const int row = sp * 32 + lane;
     const int S = p.S;
     const int iso = lane & 7;
-    const uint32_t taddr = tmem_base + ((uint32_t)(sp * 32) << 16) + grp * kAccN + ch * 128;
-    const int per_tile = RG;     // accumulators per column tile
+    const uint32_t tbase = tmem_base + ((uint32_t)(sp * 32) << 16) + cq * 64;
+    const int slot_q = cq * 64;
     uint32_t L = 0, H = 0;
     for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
       const int g = (int)(u % n_rg);
@@ -244,44 +248,41 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
         best2[r] = kNone;
         bcol[r] = 0;
       }
-      for (int t = t0; t < t1; ++t, ++L, H += per_tile) {
+      for (int t = t1 - 1; t >= t0; --t, ++L) {
         const int s = L % STAGES;
         const int2 tinfo = p.tile_info[t];  // {parity, valid slots}
         ptx::mbar_wait_sleep(full_bar(s), (L / STAGES) & 1);
         const int32_t* colmap_s = reinterpret_cast<const int32_t*>(sStage + s * kStage + kB);
-        // this group's row tiles of column tile t: H + r with (H + r) % 2 == grp
 #pragma unroll 1
-        for (int r = (int)((grp - H) & 1u); r < per_tile; r += kNumAcc) {
-          const uint32_t HH = H + r;
-          ptx::mbar_wait_sleep(tfull_bar(grp), (HH / kNumAcc) & 1);
+        for (int r = 0; r < RG; ++r, ++H) {
+          const int acc = H % kNumAcc;
+          ptx::mbar_wait_sleep(tfull_bar(acc), (H / kNumAcc) & 1);
           ptx::tc_fence_after();
-          int b2 = best2[r], bc = bcol[r];
-          const int slot_h = ch * 128;
+          int va[32], vb[32];
+          ptx::tmem_ld32(tbase + acc * kAccN, va);
+          ptx::tmem_ld32(tbase + acc * kAccN + 32, vb);
+          ptx::tmem_wait_ld();
+          // all of this warp's values are in registers: release the accumulator
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
+          if (tinfo.y < kTileN) {  // mask padding slots (last tile of a group)
 #pragma unroll
-          for (int c = 0; c < 4; c += 2) {
-            int va[32], vb[32];
-            ptx::tmem_ld32(taddr + c * 32, va);
-            ptx::tmem_ld32(taddr + (c + 1) * 32, vb);
-            ptx::tmem_wait_ld();
-            if (c == 2) {
-              // every value of this accumulator is in registers: hand it back
-              // to the MMA warp before the arithmetic
-              ptx::tc_fence_before();
-              __syncwarp();
-              if (lane == 0) ptx::mbar_arrive(tempty_bar(grp));
+            for (int j = 0; j < 32; ++j) {
+              if (slot_q + j >= tinfo.y) va[j] = kNone;
+              if (slot_q + 32 + j >= tinfo.y) vb[j] = kNone;
             }
-            if (tinfo.y < kTileN) {  // mask padding slots (last tile of a group)
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                if (slot_h + c * 32 + j >= tinfo.y) va[j] = kNone;
-                if (slot_h + (c + 1) * 32 + j >= tinfo.y) vb[j] = kNone;
-              }
-            }
-            chunk_update(va, tinfo.x, slot_h + c * 32, colmap_s, b2, bc);
-            chunk_update(vb, tinfo.x, slot_h + (c + 1) * 32, colmap_s, b2, bc);
           }
-          best2[r] = b2;
-          bcol[r] = bc;
+          if (p.debug_mode == 1) continue;
+          const int ma = min32(va), mb = min32(vb);
+          const int lim = improve_limit(best2[r], tinfo.x);
+          if (min(ma, mb) < lim) {  // rare: this row improves (or ties earlier) in these 64 columns
+            const bool in_a = ma <= mb;
+            const int m = in_a ? ma : mb;
+            const int j = in_a ? first_eq(va, m) : 32 + first_eq(vb, m);
+            best2[r] = 2 * m + tinfo.x;
+            bcol[r] = colmap_s[slot_q + j];
+          }
         }
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(empty_bar(s));
@@ -638,6 +639,7 @@ int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys) {
   }
   const int64_t n_spans = (T.ntiles + prm.tiles_per_unit - 1) / prm.tiles_per_unit;
   prm.n_units = n_spans * n_rgroups;
+  if (const char* dbg = getenv("FC_TC_DEBUG_MODE")) prm.debug_mode = atoi(dbg);
 
   cudaEvent_t m0, m1;
   cudaEventCreate(&m0);
