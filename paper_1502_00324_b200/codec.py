@@ -23,7 +23,7 @@ from . import _native
 from .image import GrayImage, apply_isometry, decimate_tile
 from .matcher import BASELINE, PATHS, PROPOSED, SPolicy
 from .pool import LEVEL_RANGE_SIDES, CoordTable, PoolParams, build_pool
-from .stream import CompressedStream, MatchRecord, header_bytes, iter_leaves
+from .stream import CompressedStream, RecordTable, header_bytes, iter_leaves
 
 TOP_SIDE = 16
 
@@ -68,6 +68,7 @@ class EncodeReport:
     comparisons: int = 0
     scan_device_ms: float = 0.0
     level_stats: list = field(default_factory=list)  # per matched level: device counters
+    phase_ms: dict = field(default_factory=dict)       # host wall time per encode phase
 
     def to_lines(self) -> list:
         rows = [
@@ -161,6 +162,7 @@ def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=N
     comparisons = 0
     scan_ms = 0.0
     level_stats = []
+    phase = {"pool": 1e3 * pool_time}
 
     def match_fn(level, o):
         nonlocal comparisons, scan_ms
@@ -171,8 +173,13 @@ def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=N
         lvl_path = path
         if path == _native.PATH_TENSOR and (baseline or level == 4):
             lvl_path = _native.PATH_EXACT  # the contraction covers proposed mode, B >= 4
+        t0 = time.perf_counter()
         ctx.level_prepare(level, baseline, policy.s_set(level), lvl_path)
+        t1 = time.perf_counter()
         err, idx, rmean = ctx.match_level(level, o)
+        t2 = time.perf_counter()
+        phase[f"prepare_l{level}"] = 1e3 * (t1 - t0)
+        phase[f"match_l{level}"] = 1e3 * (t2 - t1)
         st = ctx.stats()
         comparisons += int(st.comparisons)
         scan_ms += float(st.scan_ms)
@@ -184,7 +191,10 @@ def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=N
         scans[level] = (err, idx, rmean)
         return err
 
+    t_q = time.perf_counter()
     origins, leaf_lv, leaf_j = _quadtree(image.width, image.height, config.thresholds, match_fn)
+    t_r = time.perf_counter()
+    phase["quadtree"] = 1e3 * (t_r - t_q)
 
     n = leaf_lv.shape[0]
     steps = leaf_lv
@@ -209,13 +219,13 @@ def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=N
         else:
             o = np.rint(rmean[j]).astype(np.int64)
         offs[sel], isos[sel], addrs[sel], sidx[sel], errs[sel] = o, iso, e, si, err[j]
-    records = tuple(MatchRecord(int(a), int(b), int(c), int(d), int(f))
-                    for a, b, c, d, f in zip(steps, offs, isos, addrs, sidx))
+    records = RecordTable(np.stack([steps, offs, isos, addrs, sidx], axis=1))
     stream = CompressedStream(
         width=image.width, height=image.height, mode=policy.mode, strides=pool.params.strides,
         s_sets=tuple(policy.s_set(level) for level in (1, 2, 3, 4)),
         pools=tuple(pool.coords(level) for level in (1, 2, 3, 4)), records=records)
     encode_time = time.perf_counter() - t_start
+    phase["records_stream"] = 1e3 * (time.perf_counter() - t_r)
     pixels = image.width * image.height
     payload = stream.payload_bits()
     head = header_bytes(stream)
@@ -229,7 +239,7 @@ def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=N
         bpp_payload=payload / pixels, bpp_total=file_bytes * 8 / pixels,
         comp_ratio_payload=pixels * 8 / payload if payload else float("inf"),
         comp_ratio_total=pixels / file_bytes, pool_time_s=pool_time, encode_time_s=encode_time,
-        comparisons=comparisons, scan_device_ms=scan_ms, level_stats=level_stats)
+        comparisons=comparisons, scan_device_ms=scan_ms, level_stats=level_stats, phase_ms=phase)
     return stream, report
 
 

@@ -29,3 +29,4 @@ for name in sys.argv[1:] or ["c2"]:
         if it == reps - 1:
             for ls in rep.level_stats:
                 print("   ", ls, flush=True)
+            print("    phases(ms):", {k: round(v, 3) for k, v in rep.phase_ms.items()}, flush=True)
