@@ -59,11 +59,11 @@ def dist_env():
 
 def images_for_rank(name: str, rank: int, world: int):
     """Weak scaling: one seeded image per rank; c3 shards its 64 images."""
-    from paper_1502_00324_b200 import workloads as W
+    from paper_1502_00324_b200 import sharding, workloads as W
 
     wl = W.WORKLOADS[name]
     if wl.images > 1:
-        return [wl.image(i) for i in range(rank, wl.images, world)]
+        return [wl.image(i) for i in sharding.images_for_rank(wl.images, rank, world)]
     return [wl.image(rank)]
 
 
@@ -128,7 +128,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
@@ -320,19 +320,13 @@ def main():
                 d2h += 4 * ls["ranges"]                   # offsets for the clamp plan
         d2h += sum(4 * s for s in rep.pool_sizes)         # pool coordinates (stream header)
 
-    t_dev = torch.tensor([total_ms, e2e_t, comps, pixels_per_step, main_ms, alg_ops],
-                         dtype=torch.float64, device="cuda")
-    if world > 1:
-        mx = t_dev.clone()
-        sm = t_dev.clone()
-        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
-        total_ms_all, e2e_all = float(mx[0]), float(mx[1])
-        comps_all, pix_all = float(sm[2]), float(sm[3])
-        main_ms_max, alg_all = float(mx[4]), float(sm[5])
-    else:
-        total_ms_all, e2e_all, comps_all, pix_all = total_ms, e2e_t, float(comps), float(pixels_per_step)
-        main_ms_max, alg_all = main_ms, float(alg_ops)
+    from paper_1502_00324_b200 import sharding
+
+    red = sharding.reduce_metrics(
+        dict(step_ms_total=total_ms, e2e_s_total=e2e_t, kernel_ms_total=main_ms, comparisons=comps,
+             pixels=pixels_per_step * args.steps, alg_ops=alg_ops), device="cuda")
+    total_ms_all, e2e_all = red["step_ms_total"], red["e2e_s_total"]
+    comps_all, pix_all = red["comparisons"], red["pixels"] / args.steps
 
     if rank != 0:
         if world > 1:
@@ -340,7 +334,14 @@ def main():
         return 0
 
     value = comps_all / (total_ms_all * 1e-3)
-    peak, peak_src = measured_int8_peak(torch)
+    peak = ctx.probe_int8_peak()
+    peak_src = ("measured in-run on this B200: dense tcgen05.mma kind::i8 M=128 N=256 from smem, "
+                "all SMs (fc_probe_int8_peak)")
+    try:
+        cublas, _ = measured_int8_peak(torch)
+        peak_src += f"; cuBLASLt int8 8192^3 in the same run: {cublas:.0f} TOP/s"
+    except Exception:  # noqa: BLE001
+        pass
     achieved = (alg_ops / (main_ms * 1e-3)) / 1e12 if main_ms > 0 else None
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")

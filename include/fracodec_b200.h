@@ -122,6 +122,9 @@ int fc_get_stream(fc_ctx* ctx, void** out_stream);
 /* Kernels this library launched on the context since creation (excludes CUB
  * sort internals and memcpy/memset). */
 int fc_launch_count(fc_ctx* ctx, int64_t* out_count);
+/* Roofline denominator measured in-run: dense tcgen05.mma kind::i8 rate
+ * (M=128, N=256, operands in smem, no epilogue) over all SMs, in TOP/s. */
+int fc_probe_int8_peak(fc_ctx* ctx, double* out_tops);
 
 #ifdef __cplusplus
 }

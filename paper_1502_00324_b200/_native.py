@@ -77,6 +77,7 @@ _SIGNATURES = {
     "fc_last_stats": ([_P, ctypes.POINTER(FcStats)], ctypes.c_int),
     "fc_get_stream": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
     "fc_launch_count": ([_P, ctypes.POINTER(_I64)], ctypes.c_int),
+    "fc_probe_int8_peak": ([_P, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
 }
 
 _lib = None
@@ -258,6 +259,12 @@ class Context:
         h = ctypes.c_void_p()
         self.check(self.lib.fc_get_stream(self.handle, ctypes.byref(h)))
         return int(h.value or 0)
+
+    def probe_int8_peak(self) -> float:
+        """Dense tcgen05 kind::i8 rate (TOP/s) measured on this GPU by the library."""
+        v = ctypes.c_double()
+        self.check(self.lib.fc_probe_int8_peak(self.handle, ctypes.byref(v)))
+        return float(v.value)
 
     def launch_count(self) -> int:
         n = ctypes.c_int64()

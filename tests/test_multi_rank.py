@@ -1,0 +1,63 @@
+"""Multi-rank (world size 2, gloo on CPU) coverage of the sharding and the
+timing reduction bench.py uses under torchrun."""
+
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+from paper_1502_00324_b200 import sharding
+
+
+def test_images_and_slabs_partition_the_work():
+    for world in (1, 2, 3, 4, 8):
+        imgs = sorted(i for r in range(world) for i in sharding.images_for_rank(64, r, world))
+        assert imgs == list(range(64))
+        slabs = [sharding.slab_for_rank(1024, r, world) for r in range(world)]
+        assert slabs[0][0] == 0 and slabs[-1][1] == 1024
+        assert all(a[1] == b[0] for a, b in zip(slabs, slabs[1:]))
+        assert max(b - a for a, b in slabs) - min(b - a for a, b in slabs) <= 1
+    with pytest.raises(ValueError):
+        sharding.images_for_rank(4, 2, 2)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = sharding.images_for_rank(64, rank, world)
+    metrics = dict(step_ms_total=10.0 * (rank + 1), e2e_s_total=1.0 + rank, kernel_ms_total=3.0 - rank,
+                   comparisons=1000 * len(mine), pixels=512 * 512 * len(mine), alg_ops=7 * (rank + 1))
+    out = sharding.reduce_metrics(metrics)
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_reduce_metrics_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank in (0, 1):
+        out = results[rank]
+        assert out["step_ms_total"] == 20.0          # max over ranks
+        assert out["e2e_s_total"] == 2.0
+        assert out["kernel_ms_total"] == 3.0
+        assert out["comparisons"] == 64 * 1000       # sum over ranks = whole job
+        assert out["pixels"] == 64 * 512 * 512
+        assert out["alg_ops"] == 21
