@@ -151,6 +151,70 @@ __global__ void moments_kernel(const uint8_t* __restrict__ tiles, int n, int64_t
   }
 }
 
+// Threshold compaction predicate: window index -> entropy > tau (keeps raster order).
+struct AboveTau {
+  const double* ent;
+  double tau;
+  __device__ __forceinline__ bool operator()(const uint32_t& w) const { return ent[w] > tau; }
+};
+
+__global__ void gather_keys_kernel(const uint32_t* __restrict__ idx, const double* __restrict__ ent,
+                                   int64_t n, uint64_t* __restrict__ keys) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = entropy_key(ent[idx[i]]);
+}
+
+__global__ void iota_kernel(uint32_t* __restrict__ v, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (uint32_t)i;
+}
+
+// Lexicographic (key, index) minimum: the first window of the highest
+// entropy, i.e. np.argsort(-ent, kind="stable")[0] (cap = 1 levels).
+__device__ __forceinline__ void lex_min(uint64_t& k, uint32_t& i, uint64_t k2, uint32_t i2) {
+  if (k2 < k || (k2 == k && i2 < i)) {
+    k = k2;
+    i = i2;
+  }
+}
+
+__global__ void argmin_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                              int64_t n, uint64_t* __restrict__ out_k, uint32_t* __restrict__ out_i) {
+  uint64_t bk = ~0ull;
+  uint32_t bi = 0xffffffffu;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    lex_min(bk, bi, keys[i], vals ? vals[i] : (uint32_t)i);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+    const uint32_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+    lex_min(bk, bi, k2, i2);
+  }
+  __shared__ uint64_t sk[32];
+  __shared__ uint32_t si[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sk[warp] = bk;
+    si[warp] = bi;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    bk = lane < (int)(blockDim.x >> 5) ? sk[lane] : ~0ull;
+    bi = lane < (int)(blockDim.x >> 5) ? si[lane] : 0xffffffffu;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+      const uint32_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      lex_min(bk, bi, k2, i2);
+    }
+    if (lane == 0) {
+      out_k[blockIdx.x] = bk;
+      out_i[blockIdx.x] = bi;
+    }
+  }
+}
+
 int alloc_level(Ctx* c, Level& L, int64_t E) {
   const int n = L.n;
   FC_CUDA(c, L.xy.reserve(E * 4 + 16));
@@ -201,61 +265,104 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     FC_CUDA(c, c->val_in.reserve(nwin * 4));
     FC_CUDA(c, c->val_out.reserve(nwin * 4));
     FC_CUDA(c, c->count_buf.reserve(64));
-    FC_CUDA(c, cudaMemsetAsync(c->count_buf.ptr, 0, 8, c->stream));
     const double* lut = c->lut[lut_slot(D * D)].as<double>();
     int64_t blocks64 = (nwin + kEntWarps - 1) / kEntWarps;
     const int blocks = (int)std::min<int64_t>(blocks64, (int64_t)c->sm_count * 64);
     const double tau = use_tau[li] ? taus[li] : 0.0;
+    const int count_above = 0;  // compaction counts survivors
     auto* cnt = c->count_buf.as<unsigned long long>();
     switch (D) {
       case 32:
         entropy_kernel<32><<<blocks, kEntWarps * 32, 0, c->stream>>>(
-            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, use_tau[li],
+            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, count_above,
             c->ent_scratch.as<double>(), c->key_in.as<uint64_t>(), c->val_in.as<uint32_t>(), cnt);
         break;
       case 16:
         entropy_kernel<16><<<blocks, kEntWarps * 32, 0, c->stream>>>(
-            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, use_tau[li],
+            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, count_above,
             c->ent_scratch.as<double>(), c->key_in.as<uint64_t>(), c->val_in.as<uint32_t>(), cnt);
         break;
       case 8:
         entropy_kernel<8><<<blocks, kEntWarps * 32, 0, c->stream>>>(
-            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, use_tau[li],
+            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, count_above,
             c->ent_scratch.as<double>(), c->key_in.as<uint64_t>(), c->val_in.as<uint32_t>(), cnt);
         break;
       default:
         entropy_kernel<4><<<blocks, kEntWarps * 32, 0, c->stream>>>(
-            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, use_tau[li],
+            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, count_above,
             c->ent_scratch.as<double>(), c->key_in.as<uint64_t>(), c->val_in.as<uint32_t>(), cnt);
         break;
     }
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 1;
-    size_t tmp = 0;
-    FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, c->key_in.as<uint64_t>(),
-                                               c->key_out.as<uint64_t>(), c->val_in.as<uint32_t>(),
-                                               c->val_out.as<uint32_t>(), (int)nwin, 0, 64,
-                                               c->stream));
-    FC_CUDA(c, c->cub_tmp.reserve(tmp));
-    FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, c->key_in.as<uint64_t>(),
-                                               c->key_out.as<uint64_t>(), c->val_in.as<uint32_t>(),
-                                               c->val_out.as<uint32_t>(), (int)nwin, 0, 64,
-                                               c->stream));
+    // rank: threshold mode compacts {ent > tau} first (stable) and sorts only
+    // the survivors; cap 1 is a lexicographic argmin; other caps sort all
+    const uint32_t* order = nullptr;
     int64_t E;
+    size_t tmp = 0;
+    const unsigned tpb = 256;
     if (use_tau[li]) {
-      unsigned long long above = 0;
-      FC_CUDA(c, cudaMemcpyAsync(&above, cnt, 8, cudaMemcpyDeviceToHost, c->stream));
+      uint32_t* sel = c->val_out.as<uint32_t>();
+      auto* d_nsel = reinterpret_cast<int*>(c->count_buf.as<unsigned long long>() + 2);
+      iota_kernel<<<(unsigned)((nwin + tpb - 1) / tpb), tpb, 0, c->stream>>>(c->val_in.as<uint32_t>(),
+                                                                            nwin);
+      AboveTau pred{c->ent_scratch.as<double>(), tau};
+      FC_CUDA(c, cub::DeviceSelect::If(nullptr, tmp, c->val_in.as<uint32_t>(), sel, d_nsel, (int)nwin,
+                                        pred, c->stream));
+      FC_CUDA(c, c->cub_tmp.reserve(tmp));
+      FC_CUDA(c, cub::DeviceSelect::If(c->cub_tmp.ptr, tmp, c->val_in.as<uint32_t>(), sel, d_nsel,
+                                        (int)nwin, pred, c->stream));
+      int nsel = 0;
+      FC_CUDA(c, cudaMemcpyAsync(&nsel, d_nsel, 4, cudaMemcpyDeviceToHost, c->stream));
       FC_CUDA(c, cudaStreamSynchronize(c->stream));
-      E = std::max<int64_t>(1, (int64_t)above);  // level caps are >= 1 (pool.py:47-48)
+      if (nsel == 0) {
+        // caps are >= 1 (pool.py:47-48): keep the single highest-entropy window
+        argmin_kernel<<<1, 1024, 0, c->stream>>>(c->key_in.as<uint64_t>(), nullptr, nwin,
+                                                 c->key_out.as<uint64_t>(), c->val_out.as<uint32_t>());
+        E = 1;
+      } else {
+        E = nsel;
+        gather_keys_kernel<<<(unsigned)((E + tpb - 1) / tpb), tpb, 0, c->stream>>>(
+            sel, c->ent_scratch.as<double>(), E, c->key_in.as<uint64_t>());
+        uint32_t* sorted = c->val_in.as<uint32_t>();
+        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, c->key_in.as<uint64_t>(),
+                                                   c->key_out.as<uint64_t>(), sel, sorted, (int)E, 0,
+                                                   64, c->stream));
+        FC_CUDA(c, c->cub_tmp.reserve(tmp));
+        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, c->key_in.as<uint64_t>(),
+                                                   c->key_out.as<uint64_t>(), sel, sorted, (int)E, 0,
+                                                   64, c->stream));
+        order = sorted;
+      }
+      c->total_launches += 2;
+    } else if (caps[li] == 1) {
+      const int nb = (int)std::min<int64_t>((nwin + 1023) / 1024, 1024);
+      uint64_t* bk = c->key_out.as<uint64_t>();
+      uint32_t* bi = c->val_out.as<uint32_t>();
+      argmin_kernel<<<nb, 1024, 0, c->stream>>>(c->key_in.as<uint64_t>(), nullptr, nwin, bk + 1, bi + 1);
+      argmin_kernel<<<1, 1024, 0, c->stream>>>(bk + 1, bi + 1, nb, bk, bi);
+      c->total_launches += 2;
+      E = 1;
     } else {
+      FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, c->key_in.as<uint64_t>(),
+                                                 c->key_out.as<uint64_t>(), c->val_in.as<uint32_t>(),
+                                                 c->val_out.as<uint32_t>(), (int)nwin, 0, 64,
+                                                 c->stream));
+      FC_CUDA(c, c->cub_tmp.reserve(tmp));
+      FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, c->key_in.as<uint64_t>(),
+                                                 c->key_out.as<uint64_t>(), c->val_in.as<uint32_t>(),
+                                                 c->val_out.as<uint32_t>(), (int)nwin, 0, 64,
+                                                 c->stream));
       E = std::min<int64_t>(caps[li], nwin);
     }
+    if (!order) order = c->val_out.as<uint32_t>();
+    FC_CUDA(c, cudaGetLastError());
     L.count = E;
     FC_TRY(alloc_level(c, L, E));
     const int threads = 256;
     const int64_t grid = (E * 32 + threads - 1) / threads;
     survivor_kernel<<<(unsigned)grid, threads, 0, c->stream>>>(
-        c->img_ptr, c->width, nx, L.stride, D, c->val_out.as<uint32_t>(),
+        c->img_ptr, c->width, nx, L.stride, D, order,
         c->ent_scratch.as<double>(), E, L.xy.as<uint32_t>(), L.ent.as<double>(),
         L.tiles.as<uint8_t>(), L.sum.as<int32_t>(), L.sumsq.as<int64_t>(), L.mean.as<double>(),
         L.cnorm.as<double>());

@@ -461,6 +461,18 @@ __global__ void build_a_kernel(const uint8_t* __restrict__ rtiles, const double*
   }
 }
 
+// Clamp-reach lists by counting sort: columns bucketed by qmin (ascending) and
+// by qmax (descending); the order inside a bucket does not matter.
+__global__ void reach_scatter_kernel(const int4* __restrict__ stats, int64_t ncols,
+                                     int32_t* __restrict__ cur_low, int32_t* __restrict__ cur_high,
+                                     int32_t* __restrict__ reach_low, int32_t* __restrict__ reach_high) {
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= ncols) return;
+  const int4 st = stats[col];
+  reach_low[atomicAdd(&cur_low[st.z + 512], 1)] = (int32_t)col;
+  reach_high[atomicAdd(&cur_high[st.w + 512], 1)] = (int32_t)col;
+}
+
 __global__ void fill_i32_kernel(int32_t* __restrict__ p, int64_t n, int32_t v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -542,19 +554,29 @@ int level_prepare_tc(Ctx* c, Level& L) {
     tinfo[t] = make_int2(0, (int)std::min<int64_t>(kTileN, n_even - t * kTileN));
   for (int64_t t = 0; t < tiles_odd; ++t)
     tinfo[tiles_even + t] = make_int2(1, (int)std::min<int64_t>(kTileN, n_odd - t * kTileN));
-  // clamp-reach column lists: sorted by qmin ascending and by qmax descending
-  FC_CUDA(c, T.reach_low.reserve(ncols * 4));
-  FC_CUDA(c, T.reach_high.reserve(ncols * 4));
-  FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, need, k_min, c->key_out.as<uint32_t>(),
-                                             c->val_in.as<int32_t>(), T.reach_low.as<int32_t>(),
-                                             (int)ncols, 0, 11, c->stream));
-  FC_CUDA(c, c->cub_tmp.reserve(need));
-  FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, need, k_min, c->key_out.as<uint32_t>(),
-                                             c->val_in.as<int32_t>(), T.reach_low.as<int32_t>(),
-                                             (int)ncols, 0, 11, c->stream));
-  FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, need, k_max, c->key_out.as<uint32_t>(),
-                                             c->val_in.as<int32_t>(), T.reach_high.as<int32_t>(),
-                                             (int)ncols, 0, 11, c->stream));
+  // clamp-reach column lists: qmin ascending / qmax descending, by counting sort
+  {
+    std::vector<int32_t> cur(2048);
+    int32_t acc_lo = 0, acc_hi = 0;
+    for (int v = 0; v < 1024; ++v) {
+      cur[v] = acc_lo;
+      acc_lo += (int32_t)hmin[v];
+    }
+    for (int v = 1023; v >= 0; --v) {
+      cur[1024 + v] = acc_hi;
+      acc_hi += (int32_t)hmax[v];
+    }
+    FC_CUDA(c, T.reach_low.reserve(ncols * 4));
+    FC_CUDA(c, T.reach_high.reserve(ncols * 4));
+    FC_CUDA(c, c->key_out.reserve(2048 * 4));
+    int32_t* d_cur = c->key_out.as<int32_t>();
+    FC_CUDA(c, cudaMemcpyAsync(d_cur, cur.data(), 2048 * 4, cudaMemcpyHostToDevice, c->stream));
+    reach_scatter_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, c->stream>>>(
+        T.col_stats.as<int4>(), ncols, d_cur, d_cur + 1024, T.reach_low.as<int32_t>(),
+        T.reach_high.as<int32_t>());
+    FC_CUDA(c, cudaGetLastError());
+    c->total_launches += 1;
+  }
   // grouped operand + column map + tile info
   const int64_t slots = T.ntiles * kTileN;
   FC_CUDA(c, T.b_tiles.reserve(slots * T.kpad));
