@@ -20,6 +20,8 @@
  *   fc_match_level      <- codec.py:185-193  match_level(level, origins) incl.
  *                          codec.py:164 _gather_tiles + matcher.py:162 scan_tiles
  *   fc_set_entropy_lut  <- pool.py:88-92     the p*log(p) terms numpy produces
+ *   fc_encode           <- codec.py:114-224  the quadtree level loop (split test,
+ *                          children, depth-first records) around match_level
  */
 #ifndef FRACODEC_B200_H_
 #define FRACODEC_B200_H_
@@ -115,6 +117,25 @@ int fc_scan_candidates(fc_ctx* ctx, const int16_t* ranges, const double* rmeans,
                        int32_t n, const int16_t* q, const double* dmeans, int64_t E,
                        const double* svals, int32_t s_count, int32_t baseline, int64_t* out_err,
                        int64_t* out_idx);
+
+/* Whole quadtree encode on the device (codec.py:114-224) after fc_set_image
+ * and fc_pool_build: for levels 1..3 a range splits into its four quadrants
+ * when its best error exceeds thresholds[l]^2 * B^2; level-4 ranges never
+ * split.  svals holds the four levels' s sets back to back (s_counts[l]
+ * values each); baseline 0 = proposed mode; path FC_PATH_*, where
+ * FC_PATH_TENSOR uses the exact kernel on levels the contraction does not
+ * cover (baseline mode, 2x2 ranges).  Leaf records come out in the
+ * reference's depth-first order as int32 [count][6] =
+ * {step, offset, iso, addr, sidx, err}; records may be NULL (fetch them
+ * later with fc_encode_records).  Raises FC_ERR_EMPTY_POOL when ranges reach
+ * a level whose pool is empty, FC_ERR_DIMS for sides not multiple of 16. */
+int fc_encode(fc_ctx* ctx, const double thresholds[3], int32_t baseline, const double* svals,
+              const int32_t s_counts[4], int32_t path, int32_t* records, int64_t capacity,
+              int64_t* out_count);
+int fc_encode_records(fc_ctx* ctx, int32_t* records, int64_t capacity);
+/* Per-level statistics of the last fc_encode (ranges, comparisons, path,
+ * scan / main / fix device times, clamp pairs). */
+int fc_encode_level_stats(fc_ctx* ctx, int level, fc_stats* out);
 
 int fc_last_stats(fc_ctx* ctx, fc_stats* out);
 /* The context's CUDA stream (cudaStream_t) so callers can time on it. */

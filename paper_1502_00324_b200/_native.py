@@ -74,6 +74,9 @@ _SIGNATURES = {
     "fc_match_tiles": ([_P, ctypes.c_int, _P, _I64, _P, _P, _P], ctypes.c_int),
     "fc_scan_candidates": ([_P, _P, _P, _I64, _I32, _P, _P, _I64, _P, _I32, _I32, _P, _P],
                            ctypes.c_int),
+    "fc_encode": ([_P, _P, _I32, _P, _P, _I32, _P, _I64, ctypes.POINTER(_I64)], ctypes.c_int),
+    "fc_encode_records": ([_P, _P, _I64], ctypes.c_int),
+    "fc_encode_level_stats": ([_P, ctypes.c_int, ctypes.POINTER(FcStats)], ctypes.c_int),
     "fc_last_stats": ([_P, ctypes.POINTER(FcStats)], ctypes.c_int),
     "fc_get_stream": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
     "fc_launch_count": ([_P, ctypes.POINTER(_I64)], ctypes.c_int),
@@ -245,6 +248,33 @@ class Context:
                                                _ptr(dm), len(dm), _ptr(sv), len(sv),
                                                int(bool(baseline)), _ptr(err), _ptr(idx)))
         return err, idx
+
+    def encode(self, thresholds, baseline: bool, s_sets, path: int = PATH_AUTO,
+               capacity: int | None = None) -> np.ndarray:
+        """Device quadtree encode (fc_encode): int32 records [n, 6] =
+        (step, offset, iso, addr, sidx, err) in depth-first order."""
+        th = np.zeros(3, dtype=np.float64)
+        th[:len(thresholds[:3])] = np.asarray(thresholds[:3], dtype=np.float64)
+        counts = np.array([len(s) for s in s_sets], dtype=np.int32)
+        sv = np.ascontiguousarray(np.concatenate([np.asarray(s, dtype=np.float64) for s in s_sets]))
+        if capacity is None:
+            capacity = 1 << 16
+        out = np.empty((capacity, 6), dtype=np.int32)
+        n = ctypes.c_int64()
+        rc = self.lib.fc_encode(self.handle, _ptr(th), int(bool(baseline)), _ptr(sv), _ptr(counts),
+                                int(path), None, 0, ctypes.byref(n))
+        self.check(rc)
+        count = int(n.value)
+        if count > capacity:
+            out = np.empty((count, 6), dtype=np.int32)
+        if count:
+            self.check(self.lib.fc_encode_records(self.handle, _ptr(out), out.shape[0]))
+        return out[:count]
+
+    def encode_level_stats(self, level: int) -> FcStats:
+        st = FcStats()
+        self.check(self.lib.fc_encode_level_stats(self.handle, level, ctypes.byref(st)))
+        return st
 
     def stats(self) -> FcStats:
         st = FcStats()

@@ -147,8 +147,71 @@ def run_quadtree(width: int, height: int, thresholds, match_level):
 def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=None):
     """Compress an image whose sides are multiples of 16 -> (CompressedStream, EncodeReport).
 
-    ``device_image``: optional HBM-resident copy of the pixels (see build_pool).
+    codec.py:114-224 semantics.  The whole quadtree runs on the device
+    (fc_encode: split tests, child ranges and depth-first records never leave
+    HBM; one host synchronisation per level).  ``device_image``: optional
+    HBM-resident copy of the pixels (see build_pool).
     """
+    if image.width % 16 or image.height % 16:
+        raise ValueError(f"dimensions not multiple of 16: {image.width}x{image.height}")
+    t_start = time.perf_counter()
+    ctx = context if context is not None else _native.default_context()
+    pool = build_pool(image, config.pool, context=ctx, device_image=device_image)
+    pool_time = time.perf_counter() - t_start
+    policy = config.policy
+    baseline = policy.mode == BASELINE
+    s_sets = tuple(policy.s_set(level) for level in (1, 2, 3, 4))
+    t_q = time.perf_counter()
+    rec = ctx.encode(config.thresholds, baseline, s_sets, PATHS[config.path],
+                     capacity=image.width * image.height // 4)
+    t_r = time.perf_counter()
+    phase = {"pool": 1e3 * pool_time, "quadtree": 1e3 * (t_r - t_q)}
+    level_stats = []
+    comparisons = 0
+    scan_ms = 0.0
+    for level in (1, 2, 3, 4):
+        st = ctx.encode_level_stats(level)
+        if st.ranges == 0:
+            continue
+        comparisons += int(st.comparisons)
+        scan_ms += float(st.scan_ms)
+        level_stats.append(dict(level=level, ranges=int(st.ranges), columns=int(st.columns),
+                                comparisons=int(st.comparisons), path=int(st.path),
+                                launches=int(st.kernel_launches), scan_ms=float(st.scan_ms),
+                                main_ms=float(st.main_ms), fix_ms=float(st.fix_ms),
+                                fix_pairs=int(st.fix_pairs), rescans=int(st.rescans)))
+    records = RecordTable(rec[:, :5].astype(np.int64))
+    stream = CompressedStream(
+        width=image.width, height=image.height, mode=policy.mode, strides=pool.params.strides,
+        s_sets=s_sets, pools=tuple(pool.coords(level) for level in (1, 2, 3, 4)), records=records)
+    encode_time = time.perf_counter() - t_start
+    phase["records_stream"] = 1e3 * (time.perf_counter() - t_r)
+    step_blocks = tuple(int(v) for v in np.bincount(rec[:, 0], minlength=5)[1:5])
+    return stream, _report(image, config, pool, stream, step_blocks, int(rec[:, 5].astype(np.int64).sum()),
+                           pool_time, encode_time, comparisons, scan_ms, level_stats, phase)
+
+
+def _report(image, config, pool, stream, step_blocks, collage_ssd, pool_time, encode_time,
+            comparisons, scan_ms, level_stats, phase) -> "EncodeReport":
+    pixels = image.width * image.height
+    payload = stream.payload_bits()
+    head = header_bytes(stream)
+    file_bytes = head + (payload + 7) // 8
+    return EncodeReport(
+        width=image.width, height=image.height, mode=config.policy.mode,
+        pool_cap=config.pool.pool_cap, pool_sizes=pool.sizes, strides=pool.params.strides,
+        thresholds=config.thresholds, step_blocks=step_blocks, record_count=len(stream.records),
+        collage_ssd=collage_ssd, payload_bits=payload, header_bytes=head, file_bytes=file_bytes,
+        bpp_payload=payload / pixels, bpp_total=file_bytes * 8 / pixels,
+        comp_ratio_payload=pixels * 8 / payload if payload else float("inf"),
+        comp_ratio_total=pixels / file_bytes, pool_time_s=pool_time, encode_time_s=encode_time,
+        comparisons=comparisons, scan_device_ms=scan_ms, level_stats=level_stats, phase_ms=phase)
+
+
+def encode_levelwise(image: GrayImage, config: EncoderConfig, context=None, device_image=None):
+    """Same result as encode(), driven level by level from the host through the
+    match_level seam (fc_level_prepare + fc_match_level):
+    the host runs the split test and builds the child origins."""
     if image.width % 16 or image.height % 16:
         raise ValueError(f"dimensions not multiple of 16: {image.width}x{image.height}")
     t_start = time.perf_counter()
@@ -226,21 +289,9 @@ def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=N
         pools=tuple(pool.coords(level) for level in (1, 2, 3, 4)), records=records)
     encode_time = time.perf_counter() - t_start
     phase["records_stream"] = 1e3 * (time.perf_counter() - t_r)
-    pixels = image.width * image.height
-    payload = stream.payload_bits()
-    head = header_bytes(stream)
-    file_bytes = head + (payload + 7) // 8
     step_blocks = tuple(int((leaf_lv == lv).sum()) for lv in (1, 2, 3, 4))
-    report = EncodeReport(
-        width=image.width, height=image.height, mode=policy.mode, pool_cap=config.pool.pool_cap,
-        pool_sizes=pool.sizes, strides=pool.params.strides, thresholds=config.thresholds,
-        step_blocks=step_blocks, record_count=n, collage_ssd=int(errs.sum()),
-        payload_bits=payload, header_bytes=head, file_bytes=file_bytes,
-        bpp_payload=payload / pixels, bpp_total=file_bytes * 8 / pixels,
-        comp_ratio_payload=pixels * 8 / payload if payload else float("inf"),
-        comp_ratio_total=pixels / file_bytes, pool_time_s=pool_time, encode_time_s=encode_time,
-        comparisons=comparisons, scan_device_ms=scan_ms, level_stats=level_stats, phase_ms=phase)
-    return stream, report
+    return stream, _report(image, config, pool, stream, step_blocks, int(errs.sum()), pool_time,
+                           encode_time, comparisons, scan_ms, level_stats, phase)
 
 
 # ---------------------------------------------------------------------------
@@ -257,7 +308,7 @@ def _plans(stream: CompressedStream):
             continue
         a = np.array(rows[level], dtype=np.int64)
         b = LEVEL_RANGE_SIDES[level - 1]
-        coords = np.asarray(CoordTable(stream.pools[level - 1]).array)
+        coords = np.asarray(CoordTable(stream.pools[level - 1]).array, dtype=np.int64)
         dom = coords[a[:, 0]]
         svals = np.asarray(stream.s_sets[level - 1], dtype=np.float64)[a[:, 2]]
         span = np.arange(b)

@@ -1,6 +1,7 @@
 // C ABI of fracodec_b200 (declared in include/fracodec_b200.h).
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <new>
 
 #include "fc_internal.cuh"
@@ -22,6 +23,28 @@ int cuda_check(Ctx* c, cudaError_t e, const char* what) {
   return set_error(c, FC_ERR_CUDA, buf);
 }
 
+int sync_stream(Ctx* c) {
+  FC_CUDA(c, cudaStreamSynchronize(c->stream));
+  c->up_off = 0;
+  return FC_OK;
+}
+
+// Copy host bytes into the pinned arena and enqueue the H2D copy from there,
+// so the call never blocks on the stream (a pageable source would).
+int stage_h2d(Ctx* c, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return FC_OK;
+  const size_t padded = (bytes + 255) & ~(size_t)255;
+  if (c->up_off + padded > c->up_arena.bytes) {
+    if (c->up_off > 0) FC_TRY(sync_stream(c));  // recycle the arena
+    FC_CUDA(c, c->up_arena.reserve(std::max<size_t>(padded, 1 << 20)));
+  }
+  char* slot = c->up_arena.as<char>() + c->up_off;
+  memcpy(slot, src, bytes);
+  FC_CUDA(c, cudaMemcpyAsync(dst, slot, bytes, cudaMemcpyHostToDevice, c->stream));
+  c->up_off += padded;
+  return FC_OK;
+}
+
 int lut_slot(int n) { return n == 16 ? 0 : n == 64 ? 1 : n == 256 ? 2 : n == 1024 ? 3 : -1; }
 
 namespace {
@@ -37,6 +60,69 @@ int level_ready(Ctx* c, int level) {
   if (L.n == 0) return set_error(c, FC_ERR_STATE, "pool not built");
   return FC_OK;
 }
+
+}  // namespace
+
+// Operand preparation split around one stream synchronisation so several
+// levels share it (fc_encode).  *pending = 1 when a tensor-path readback is
+// in flight and prepare_finish must run after the next sync.
+int prepare_begin(Ctx* c, Level& L, int level, int baseline, const double* svals, int s_count,
+                  int path, int* pending) {
+  *pending = 0;
+  if (s_count < 1 || s_count > kMaxS || !svals)
+    return set_error(c, FC_ERR_ARG, "s set must have 1..16 values");
+  for (int i = 0; i < s_count; ++i)
+    if (!(svals[i] >= 0.0 && svals[i] <= 1.0))
+      return set_error(c, FC_ERR_ARG, "s values must lie in [0, 1]");
+  if (path < FC_PATH_AUTO || path > FC_PATH_TENSOR) return set_error(c, FC_ERR_ARG, "bad path");
+  bool same = L.prepared && L.baseline == (baseline ? 1 : 0) && L.s_count == s_count;
+  for (int i = 0; same && i < s_count; ++i) same = L.svals[i] == svals[i];
+  if (same && (path == FC_PATH_AUTO || path == L.path)) return FC_OK;
+  if (L.count == 0) {
+    char buf[64];
+    snprintf(buf, sizeof buf, "no domain entries at level %d", level);
+    return set_error(c, FC_ERR_EMPTY_POOL, buf);
+  }
+  L.baseline = baseline ? 1 : 0;
+  L.s_count = s_count;
+  for (int i = 0; i < s_count; ++i) L.svals[i] = svals[i];
+  L.prepared = false;
+  L.tc.ready = false;
+  const bool tc_ok = !L.baseline && L.n >= 16;
+  if (path == FC_PATH_TENSOR && !tc_ok)
+    return set_error(c, FC_ERR_ARG, "tensor path needs proposed mode and B >= 4");
+  const bool want_tc = path == FC_PATH_TENSOR || (path == FC_PATH_AUTO && tc_ok);
+  FC_TRY(level_prepare_exact(c, L, want_tc ? 1 : 0));
+  if (want_tc) {
+    const int r = level_prepare_tc_begin(c, L);
+    if (r == FC_OK) {
+      *pending = 1;
+      return FC_OK;
+    }
+    if (path == FC_PATH_TENSOR) return r;
+    c->st = Status{};  // auto: keep the exact path
+  }
+  L.path = FC_PATH_EXACT;
+  L.prepared = true;
+  return FC_OK;
+}
+
+int prepare_finish(Ctx* c, Level& L, int path, int pending) {
+  if (!pending) return FC_OK;
+  const int r = level_prepare_tc_finish(c, L);
+  if (r == FC_OK) {
+    L.path = FC_PATH_TENSOR;
+  } else if (path == FC_PATH_TENSOR) {
+    return r;
+  } else {
+    c->st = Status{};  // auto: operands out of the two-plane range -> exact path
+    L.path = FC_PATH_EXACT;
+  }
+  L.prepared = true;
+  return FC_OK;
+}
+
+namespace {
 
 }  // namespace
 }  // namespace fcb
@@ -65,7 +151,8 @@ int fc_ctx_create(int device, fc_ctx** out) {
   c->sm_count = prop.multiProcessorCount;
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
-      cudaEventCreate(&c->ev2) != cudaSuccess) {
+      cudaEventCreate(&c->ev2) != cudaSuccess || cudaEventCreate(&c->tc_ev[0]) != cudaSuccess ||
+      cudaEventCreate(&c->tc_ev[1]) != cudaSuccess || cudaEventCreate(&c->tc_ev[2]) != cudaSuccess) {
     delete c;
     return FC_ERR_CUDA;
   }
@@ -85,18 +172,30 @@ void fc_ctx_destroy(fc_ctx* c) {
                     &c->cub_tmp, &c->count_buf, &c->origins, &c->rtiles, &c->rmean, &c->roff,
                     &c->rsq, &c->keys, &c->out_err, &c->out_idx, &c->fix_rows, &c->fix_cols,
                     &c->fix_jobs, &c->svals_dev, &c->iso_inv, &c->a_tiles, &c->row_meta,
-                    &c->fix_prefix, &c->tc_scratch};
+                    &c->fix_prefix, &c->tc_scratch, &c->enc_orig[0], &c->enc_orig[1],
+                    &c->enc_code[0], &c->enc_code[1], &c->enc_flag, &c->enc_pfx,
+                    &c->enc_count, &c->enc_hist, &c->leaf_flag, &c->leaf_pos, &c->leaf_rec,
+                    &c->rec_out};
   for (DevBuf* b : bufs) b->release();
+  c->up_arena.release();
+  c->readback.release();
+  c->pool_rb.release();
+  if (c->enc_ev_ready)
+    for (auto& pr : c->enc_ev)
+      for (auto& e : pr) cudaEventDestroy(e);
   for (auto& b : c->lut) b.release();
   for (auto& L : c->lv) {
     DevBuf* lb[] = {&L.xy, &L.ent, &L.tiles, &L.sum, &L.sumsq, &L.mean, &L.cnorm, &L.qbase,
                     &L.tc.b_tiles, &L.tc.hq, &L.tc.meta, &L.tc.tile_q1, &L.tc.col_stats,
-                    &L.tc.reach_low, &L.tc.reach_high};
+                    &L.tc.reach_low, &L.tc.reach_high, &L.tc.odd, &L.tc.hist, &L.svals_d,
+                    &L.win_ent, &L.win_key, &L.win_key2, &L.win_val, &L.win_val2};
     for (DevBuf* b : lb) b->release();
+    L.tc.readback.release();
   }
   cudaEventDestroy(c->ev0);
   cudaEventDestroy(c->ev1);
   cudaEventDestroy(c->ev2);
+  for (auto& e : c->tc_ev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -119,7 +218,7 @@ int fc_set_entropy_lut(fc_ctx* c, int n, const double* terms) {
   const int slot = lut_slot(n);
   if (slot < 0 || !terms) return set_error(c, FC_ERR_ARG, "LUT size must be 16/64/256/1024");
   FC_CUDA(c, c->lut[slot].reserve(n * 8));
-  FC_CUDA(c, cudaMemcpy(c->lut[slot].ptr, terms, n * 8, cudaMemcpyHostToDevice));
+  FC_TRY(stage_h2d(c, c->lut[slot].ptr, terms, n * 8));
   c->lut_set[slot] = true;
   return FC_OK;
 }
@@ -135,8 +234,7 @@ int fc_set_image(fc_ctx* c, const uint8_t* pixels, int width, int height) {
     c->img_ptr = pixels;
   } else {
     FC_CUDA(c, c->img.reserve((size_t)width * height));
-    FC_CUDA(c, cudaMemcpyAsync(c->img.ptr, pixels, (size_t)width * height, cudaMemcpyHostToDevice,
-                               c->stream));
+    FC_TRY(stage_h2d(c, c->img.ptr, pixels, (size_t)width * height));
     c->img_ptr = c->img.as<uint8_t>();
   }
   for (auto& L : c->lv) {
@@ -175,14 +273,9 @@ int fc_pool_coords(fc_ctx* c, int level, uint16_t* xy) {
   FC_TRY(level_ready(c, level));
   Level& L = c->lv[level - 1];
   if (L.count == 0) return FC_OK;
-  std::vector<uint32_t> h(L.count);
-  FC_CUDA(c, cudaMemcpyAsync(h.data(), L.xy.ptr, L.count * 4, cudaMemcpyDeviceToHost, c->stream));
-  FC_CUDA(c, cudaStreamSynchronize(c->stream));
-  for (int64_t i = 0; i < L.count; ++i) {
-    xy[2 * i] = (uint16_t)(h[i] & 0xffff);
-    xy[2 * i + 1] = (uint16_t)(h[i] >> 16);
-  }
-  return FC_OK;
+  // xy words are x | y << 16: in little-endian memory exactly the (x, y) u16 pair
+  FC_CUDA(c, cudaMemcpyAsync(xy, L.xy.ptr, L.count * 4, cudaMemcpyDeviceToHost, c->stream));
+  return sync_stream(c);
 }
 
 int fc_pool_entries(fc_ctx* c, int level, double* entropy, uint8_t* tiles, double* means,
@@ -207,43 +300,11 @@ int fc_level_prepare(fc_ctx* c, int level, int baseline, const double* svals, in
                      int32_t path) {
   cudaSetDevice(c->device);
   FC_TRY(level_ready(c, level));
-  if (s_count < 1 || s_count > kMaxS || !svals)
-    return set_error(c, FC_ERR_ARG, "s set must have 1..16 values");
-  for (int i = 0; i < s_count; ++i)
-    if (!(svals[i] >= 0.0 && svals[i] <= 1.0))
-      return set_error(c, FC_ERR_ARG, "s values must lie in [0, 1]");
   Level& L = c->lv[level - 1];
-  bool same = L.prepared && L.baseline == baseline && L.s_count == s_count;
-  for (int i = 0; same && i < s_count; ++i) same = L.svals[i] == svals[i];
-  if (same && (path == FC_PATH_AUTO || path == L.path)) return FC_OK;
-  if (L.count == 0) {
-    char buf[64];
-    snprintf(buf, sizeof buf, "no domain entries at level %d", level);
-    return set_error(c, FC_ERR_EMPTY_POOL, buf);
-  }
-  L.baseline = baseline ? 1 : 0;
-  L.s_count = s_count;
-  for (int i = 0; i < s_count; ++i) L.svals[i] = svals[i];
-  L.prepared = false;
-  L.tc.ready = false;
-  FC_TRY(level_prepare_exact(c, L));
-  int use = FC_PATH_EXACT;
-  const bool tc_ok = !L.baseline && L.n >= 16;
-  if (path == FC_PATH_TENSOR && !tc_ok)
-    return set_error(c, FC_ERR_ARG, "tensor path needs proposed mode and B >= 4");
-  if (path == FC_PATH_TENSOR || (path == FC_PATH_AUTO && tc_ok)) {
-    const int r = level_prepare_tc(c, L);
-    if (r == FC_OK) {
-      use = FC_PATH_TENSOR;
-    } else if (path == FC_PATH_TENSOR) {
-      return r;
-    } else {
-      c->st = Status{};  // auto: keep the exact path
-    }
-  }
-  L.path = use;
-  L.prepared = true;
-  return FC_OK;
+  int pending = 0;
+  FC_TRY(prepare_begin(c, L, level, baseline, svals, s_count, path, &pending));
+  if (pending) FC_TRY(sync_stream(c));
+  return prepare_finish(c, L, path, pending);
 }
 
 static int run_match(fc_ctx* c, Level& L, int64_t count, int64_t* out_err, int64_t* out_idx,
@@ -342,6 +403,31 @@ int fc_scan_candidates(fc_ctx* c, const int16_t* ranges, const double* rmeans, i
   if (M < 0 || n < 1 || E < 0 || s_count < 1) return set_error(c, FC_ERR_ARG, "bad scan shape");
   return scan_rows_dropin(c, ranges, rmeans, M, n, q, dmeans, E, svals, s_count, baseline, out_err,
                           out_idx);
+}
+
+int fc_encode(fc_ctx* c, const double thresholds[3], int32_t baseline, const double* svals,
+              const int32_t s_counts[4], int32_t path, int32_t* records, int64_t capacity,
+              int64_t* out_count) {
+  cudaSetDevice(c->device);
+  if (!thresholds || !svals || !s_counts) return set_error(c, FC_ERR_ARG, "null argument");
+  return encode_device(c, thresholds, baseline, svals, s_counts, path, records, capacity,
+                       out_count);
+}
+
+int fc_encode_records(fc_ctx* c, int32_t* records, int64_t capacity) {
+  cudaSetDevice(c->device);
+  if (c->enc_records > capacity) return set_error(c, FC_ERR_ARG, "record buffer too small");
+  if (c->enc_records == 0) return FC_OK;
+  FC_CUDA(c, cudaMemcpyAsync(records, c->rec_out.ptr, c->enc_records * 24, cudaMemcpyDeviceToHost,
+                             c->stream));
+  return sync_stream(c);
+}
+
+int fc_encode_level_stats(fc_ctx* c, int level, fc_stats* out) {
+  FC_TRY(check_level(c, level));
+  if (!out) return set_error(c, FC_ERR_ARG, "null stats");
+  *out = c->enc_stats[level - 1];
+  return FC_OK;
 }
 
 int fc_last_stats(fc_ctx* c, fc_stats* out) {

@@ -1,0 +1,301 @@
+// Device-driven quadtree encode (codec.py:114-161 level loop, codec.py:185-193
+// match_level, codec.py:196-224 record assembly).
+//
+// The host keeps only launch decisions.  Per level it needs the range count M
+// and the histogram of range offsets o (to plan the clamp-correction jobs of
+// the tensor path), read back with ONE stream synchronisation per level; the
+// split test, the child origins and depth-first codes, and the leaf records
+// are produced on the device:
+//
+//   classify_kernel : err = key >> 32; split = err > t^2 * B^2 (levels 1-3);
+//                     leaves write their record into a slot indexed by the
+//                     depth-first code top*64 + d1*16 + d2*4 + d3;
+//   ExclusiveSum    : split flags -> child base (parent order is kept);
+//   children_kernel : four child origins (TL, TR, BL, BR) and codes;
+//   gather (next)   : range tiles, moments and the offset histogram.
+//
+// After level 4 the code-indexed records are compacted in code order, which
+// is the reference's depth-first record order.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "fc_internal.cuh"
+
+namespace fcb {
+
+namespace {
+
+constexpr int kTop = 16;  // codec.py:114 top-level range side
+
+__global__ void top_origins_kernel(int nxt, int32_t n_top, int32_t* __restrict__ origins,
+                                   int32_t* __restrict__ codes, int32_t* __restrict__ d_M) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *d_M = n_top;
+  if (i >= n_top) return;
+  const int32_t ty = i / nxt, tx = i - ty * nxt;
+  origins[2 * i] = tx * kTop;
+  origins[2 * i + 1] = ty * kTop;
+  codes[i] = i * 64;
+}
+
+__device__ __forceinline__ int baseline_offset(double rmean, double s, double dmean) {
+  // codec.py:214-218 (== _scan.py:39-43): clip(rint(rmean - s*dmean), 0, 255)
+  const int o = (int)rint(__dsub_rn(rmean, __dmul_rn(s, dmean)));
+  return o < 0 ? 0 : (o > 255 ? 255 : o);
+}
+
+// Split test and leaf records.  rec = {step, offset, iso, addr, sidx, err}.
+__global__ void classify_kernel(const unsigned long long* __restrict__ keys, int64_t M, int level,
+                                int can_split, double thr2, int S, int baseline,
+                                const double* __restrict__ svals, const double* __restrict__ dmean,
+                                const double* __restrict__ rmean, const int32_t* __restrict__ roff,
+                                const int32_t* __restrict__ codes, int32_t* __restrict__ split,
+                                int32_t* __restrict__ leaf_flag, int32_t* __restrict__ leaf_rec) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const unsigned long long key = keys[i];
+  const int32_t err = (int32_t)(key >> 32);
+  const int64_t cidx = (int64_t)(key & 0xffffffffull);
+  // codec.py:140: errs > thresholds[level-1]**2 * side*side (int64 vs float64)
+  const int sp = can_split && (double)err > thr2;
+  split[i] = sp;
+  if (sp) return;
+  const int64_t e = cidx / (8 * S);
+  const int rem = (int)(cidx - e * 8 * S);
+  const int iso = rem / S, si = rem - iso * S;
+  const int o = baseline ? baseline_offset(rmean[i], svals[si], dmean[e]) : roff[i];
+  const int32_t code = codes[i];
+  int32_t* r = leaf_rec + (int64_t)code * 6;
+  r[0] = level;
+  r[1] = o;
+  r[2] = iso;
+  r[3] = (int32_t)e;
+  r[4] = si;
+  r[5] = err;
+  leaf_flag[code] = 1;
+}
+
+__global__ void children_kernel(int64_t M, const int32_t* __restrict__ split,
+                                const int32_t* __restrict__ pfx, const int32_t* __restrict__ origins,
+                                const int32_t* __restrict__ codes, int half, int weight,
+                                int32_t* __restrict__ next_origins, int32_t* __restrict__ next_codes,
+                                int32_t* __restrict__ d_next_M) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const int32_t p = pfx[i];
+  if (i == M - 1) *d_next_M = 4 * (p + split[i]);
+  if (!split[i]) return;
+  const int32_t x = origins[2 * i], y = origins[2 * i + 1], code = codes[i];
+  // children TL, TR, BL, BR (codec.py:146-150)
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t j = 4 * (int64_t)p + k;
+    next_origins[2 * j] = x + (k & 1) * half;
+    next_origins[2 * j + 1] = y + (k >> 1) * half;
+    next_codes[j] = code + k * weight;
+  }
+}
+
+__global__ void compact_records_kernel(int64_t n_codes, const int32_t* __restrict__ flag,
+                                       const int32_t* __restrict__ pos,
+                                       const int32_t* __restrict__ rec, int32_t* __restrict__ out,
+                                       int32_t* __restrict__ d_count) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_codes) return;
+  if (i == n_codes - 1) *d_count = pos[i] + flag[i];
+  if (!flag[i]) return;
+  const int32_t* src = rec + i * 6;
+  int32_t* dst = out + (int64_t)pos[i] * 6;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) dst[k] = src[k];
+}
+
+inline unsigned blocks_for(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+int encode_device(Ctx* c, const double thresholds[3], int baseline, const double* svals,
+                  const int32_t s_counts[4], int path, int32_t* out_records, int64_t capacity,
+                  int64_t* out_count) {
+  if (!c->img_ptr) return set_error(c, FC_ERR_STATE, "no image set");
+  if (c->width % kTop || c->height % kTop) {
+    char buf[96];
+    snprintf(buf, sizeof buf, "dimensions not multiple of 16: %dx%d", c->width, c->height);
+    return set_error(c, FC_ERR_DIMS, buf);
+  }
+  for (int l = 0; l < kLevels; ++l)
+    if (c->lv[l].n == 0) return set_error(c, FC_ERR_STATE, "pool not built");
+  if (path < FC_PATH_AUTO || path > FC_PATH_TENSOR) return set_error(c, FC_ERR_ARG, "bad path");
+  if (!c->enc_ev_ready) {
+    for (auto& pr : c->enc_ev)
+      for (auto& e : pr) FC_CUDA(c, cudaEventCreate(&e));
+    c->enc_ev_ready = true;
+  }
+  for (auto& st : c->enc_stats) st = fc_stats{};
+  c->enc_records = 0;
+  const int64_t launches0 = c->total_launches;
+  c->stats = fc_stats{};
+
+  // ---- operands for every level, sharing one synchronisation ----
+  int pending[kLevels] = {0, 0, 0, 0};
+  int lpath[kLevels];
+  const double* sv = svals;
+  for (int l = 0; l < kLevels; ++l) {
+    Level& L = c->lv[l];
+    lpath[l] = path;
+    if (path == FC_PATH_TENSOR && (baseline || L.n < 16)) lpath[l] = FC_PATH_EXACT;
+    if (L.count > 0)
+      FC_TRY(prepare_begin(c, L, l + 1, baseline, sv, s_counts[l], lpath[l], &pending[l]));
+    sv += s_counts[l];
+  }
+
+  // ---- top-level ranges ----
+  const int nxt = c->width / kTop, nyt = c->height / kTop;
+  const int64_t n_top = (int64_t)nxt * nyt;
+  const int64_t n_codes = n_top * 64;
+  const int64_t max_ranges = n_top * 64;  // level 4 bound
+  for (int b = 0; b < 2; ++b) {
+    FC_CUDA(c, c->enc_orig[b].reserve(max_ranges * 8 + 64));
+    FC_CUDA(c, c->enc_code[b].reserve(max_ranges * 4 + 64));
+  }
+  FC_CUDA(c, c->enc_flag.reserve(max_ranges * 4 + 64));
+  FC_CUDA(c, c->enc_pfx.reserve(max_ranges * 4 + 64));
+  FC_CUDA(c, c->enc_count.reserve(16 * 4));
+  FC_CUDA(c, c->enc_hist.reserve(256 * 4));
+  FC_CUDA(c, c->leaf_flag.reserve(n_codes * 4 + 64));
+  FC_CUDA(c, c->leaf_pos.reserve(n_codes * 4 + 64));
+  FC_CUDA(c, c->leaf_rec.reserve(n_codes * 24 + 64));
+  FC_CUDA(c, c->readback.reserve(260 * 4));
+  FC_CUDA(c, c->keys.reserve(max_ranges * 8 + 64));
+  int32_t* d_count = c->enc_count.as<int32_t>();
+  int32_t* d_hist = c->enc_hist.as<int32_t>();
+  int32_t* h_rb = c->readback.as<int32_t>();
+  FC_CUDA(c, cudaMemsetAsync(c->leaf_flag.ptr, 0, n_codes * 4, c->stream));
+  top_origins_kernel<<<blocks_for(n_top), 256, 0, c->stream>>>(
+      nxt, (int32_t)n_top, c->enc_orig[0].as<int32_t>(), c->enc_code[0].as<int32_t>(), d_count);
+  FC_CUDA(c, cudaGetLastError());
+  c->total_launches += 1;
+
+  auto gather_and_read = [&](int l, int cur, int slot, int64_t bound) -> int {
+    FC_CUDA(c, cudaMemsetAsync(d_hist, 0, 256 * 4, c->stream));
+    FC_TRY(gather_ranges_dev(c, c->lv[l], c->enc_orig[cur].as<int32_t>(), d_count + slot, bound,
+                             d_hist));
+    FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count + slot, 4, cudaMemcpyDeviceToHost, c->stream));
+    FC_CUDA(c, cudaMemcpyAsync(h_rb + 4, d_hist, 256 * 4, cudaMemcpyDeviceToHost, c->stream));
+    return FC_OK;
+  };
+  FC_TRY(gather_and_read(0, 0, 0, n_top));
+  FC_TRY(sync_stream(c));
+  for (int l = 0; l < kLevels; ++l)
+    if (pending[l]) FC_TRY(prepare_finish(c, c->lv[l], lpath[l], pending[l]));
+
+  // ---- level loop ----
+  int cur = 0;
+  std::vector<int32_t> hist(256);
+  for (int l = 0; l < kLevels; ++l) {
+    Level& L = c->lv[l];
+    const int64_t M = h_rb[0];
+    if (M == 0) break;
+    std::copy(h_rb + 4, h_rb + 4 + 256, hist.begin());
+    if (L.count == 0) {
+      char buf[64];
+      snprintf(buf, sizeof buf, "no domain entries at level %d", l + 1);
+      return set_error(c, FC_ERR_EMPTY_POOL, buf);
+    }
+    fc_stats& st = c->enc_stats[l];
+    st.ranges = M;
+    st.columns = L.count * L.s_count;
+    st.comparisons = M * L.count * 8 * L.s_count;
+    st.path = L.path;
+    const int64_t launches_before = c->total_launches + c->stats.kernel_launches;
+    uint64_t* keys = c->keys.as<uint64_t>();
+    FC_CUDA(c, cudaMemsetAsync(keys, 0xff, M * 8, c->stream));
+    FC_CUDA(c, cudaEventRecord(c->enc_ev[l][0], c->stream));
+    if (L.path == FC_PATH_TENSOR) {
+      FC_TRY(scan_tc_launch(c, L, M, keys, hist.data(), nullptr, c->enc_ev[l][1], &st.fix_pairs));
+    } else {
+      FC_TRY(scan_exact(c, L, M, nullptr, 0, nullptr, 0, keys));
+      FC_CUDA(c, cudaEventRecord(c->enc_ev[l][1], c->stream));
+    }
+    FC_CUDA(c, cudaEventRecord(c->enc_ev[l][2], c->stream));
+    const int side = L.side;
+    const int can_split = l < kLevels - 1;
+    double thr2 = 0.0;
+    if (can_split) {
+      thr2 = thresholds[l] * thresholds[l];
+      thr2 = thr2 * side;
+      thr2 = thr2 * side;
+    }
+    int32_t* codes = c->enc_code[cur].as<int32_t>();
+    int32_t* flag = c->enc_flag.as<int32_t>();
+    classify_kernel<<<blocks_for(M), 256, 0, c->stream>>>(
+        reinterpret_cast<const unsigned long long*>(keys), M, l + 1, can_split, thr2, L.s_count,
+        L.baseline, L.svals_d.as<double>(), L.mean.as<double>(), c->rmean.as<double>(),
+        c->roff.as<int32_t>(), codes, flag, c->leaf_flag.as<int32_t>(), c->leaf_rec.as<int32_t>());
+    FC_CUDA(c, cudaGetLastError());
+    c->total_launches += 1;
+    if (can_split) {
+      int32_t* pfx = c->enc_pfx.as<int32_t>();
+      size_t need = 0;
+      FC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, need, flag, pfx, (int)M, c->stream));
+      FC_CUDA(c, c->cub_tmp.reserve(need));
+      FC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.ptr, need, flag, pfx, (int)M, c->stream));
+      const int nxt_buf = cur ^ 1;
+      children_kernel<<<blocks_for(M), 256, 0, c->stream>>>(
+          M, flag, pfx, c->enc_orig[cur].as<int32_t>(), codes, side / 2, 1 << (2 * (2 - l)),
+          c->enc_orig[nxt_buf].as<int32_t>(), c->enc_code[nxt_buf].as<int32_t>(), d_count + l + 1);
+      FC_CUDA(c, cudaGetLastError());
+      c->total_launches += 2;
+      cur = nxt_buf;
+      FC_TRY(gather_and_read(l + 1, cur, l + 1, 4 * M));
+    }
+    st.kernel_launches = (int32_t)(c->total_launches + c->stats.kernel_launches - launches_before);
+    if (can_split) FC_TRY(sync_stream(c));
+  }
+  c->total_launches += c->stats.kernel_launches;
+  c->stats.kernel_launches = 0;
+
+  // ---- records in depth-first order ----
+  {
+    int32_t* flag = c->leaf_flag.as<int32_t>();
+    int32_t* pos = c->leaf_pos.as<int32_t>();
+    size_t need = 0;
+    FC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, need, flag, pos, (int)n_codes, c->stream));
+    FC_CUDA(c, c->cub_tmp.reserve(need));
+    FC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.ptr, need, flag, pos, (int)n_codes,
+                                             c->stream));
+    FC_CUDA(c, c->rec_out.reserve(n_codes * 24 + 64));
+    compact_records_kernel<<<blocks_for(n_codes), 256, 0, c->stream>>>(
+        n_codes, flag, pos, c->leaf_rec.as<int32_t>(), c->rec_out.as<int32_t>(), d_count + 8);
+    FC_CUDA(c, cudaGetLastError());
+    c->total_launches += 2;
+    FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count + 8, 4, cudaMemcpyDeviceToHost, c->stream));
+    FC_TRY(sync_stream(c));
+  }
+  const int64_t n = h_rb[0];
+  c->enc_records = n;
+  if (out_count) *out_count = n;
+  for (int l = 0; l < kLevels; ++l) {
+    fc_stats& st = c->enc_stats[l];
+    if (st.ranges == 0) continue;
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, c->enc_ev[l][0], c->enc_ev[l][1]);
+    cudaEventElapsedTime(&b, c->enc_ev[l][1], c->enc_ev[l][2]);
+    st.main_ms = a;
+    st.fix_ms = b;
+    st.scan_ms = a + b;
+  }
+  (void)launches0;
+  if (!out_records) return FC_OK;
+  if (n > capacity) return set_error(c, FC_ERR_ARG, "record buffer too small");
+  if (n > 0) {
+    FC_CUDA(c, cudaMemcpyAsync(out_records, c->rec_out.ptr, n * 24, cudaMemcpyDeviceToHost,
+                               c->stream));
+    FC_TRY(sync_stream(c));
+  }
+  return FC_OK;
+}
+
+}  // namespace fcb

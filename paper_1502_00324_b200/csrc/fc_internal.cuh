@@ -15,6 +15,7 @@ constexpr int kLevels = 4;
 constexpr int kRangeSide[kLevels] = {16, 8, 4, 2};   // pool.py:20 LEVEL_RANGE_SIDES
 constexpr int kDomainSide[kLevels] = {32, 16, 8, 4}; // pool.py:21 LEVEL_DOMAIN_SIDES
 constexpr int kMaxS = 16;
+constexpr int kTcHistWords = 1024 + 1024 + 4;  // qmin | qmax histograms, q2max, pad
 
 struct Status {
   int code = FC_OK;
@@ -44,6 +45,29 @@ struct DevBuf {
   T* as() const { return reinterpret_cast<T*>(ptr); }
 };
 
+// A growable pinned host buffer (async D2H/H2D staging).
+struct PinnedBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaError_t reserve(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    size_t cap = want + want / 4 + 256;
+    cudaError_t e = cudaMallocHost(&ptr, cap);
+    if (e == cudaSuccess) bytes = cap;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return reinterpret_cast<T*>(ptr); }
+};
+
 // Tensor-core operand set for one level (see fc_scan_tc.cu).
 struct TcOperands {
   bool ready = false;
@@ -59,6 +83,9 @@ struct TcOperands {
   DevBuf col_stats;      // int4 [ncols]: {Q1, Q2, qmin, qmax} (unsorted order)
   DevBuf reach_low;      // int32 [ncols]: columns sorted by qmin ascending
   DevBuf reach_high;     // int32 [ncols]: columns sorted by qmax descending
+  DevBuf odd;            // int32 [2*ncols]: parity flags, then their exclusive prefix
+  DevBuf hist;           // u32 [1024 qmin | 1024 qmax | q2max | pad]
+  PinnedBuf readback;    // pinned copy of hist + last prefix/flag (prepare begin -> finish)
   int64_t low_count[256] = {0};   // #{columns with qmin < -o}      (clamp at 0 possible)
   int64_t high_count[256] = {0};  // #{columns with qmax > 255 - o} (clamp at 255 possible)
 };
@@ -83,6 +110,9 @@ struct Level {
   double svals[kMaxS] = {0};
   int path = FC_PATH_EXACT;
   DevBuf qbase;           // int16 [E*S][n] base operand (column = e*S + si)
+  DevBuf svals_d;         // double [S] on the device
+  // pool-build scratch over all lattice windows of this level
+  DevBuf win_ent, win_key, win_key2, win_val, win_val2;
   TcOperands tc;
 };
 
@@ -91,6 +121,8 @@ struct Ctx {
   int sm_count = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  cudaEvent_t tc_ev[3] = {nullptr, nullptr, nullptr};
+  bool tc_attr_set = false;
   Status st;
   int device_io = 0;
   // image
@@ -107,6 +139,19 @@ struct Ctx {
   DevBuf fix_rows, fix_cols, fix_jobs, svals_dev;
   DevBuf a_tiles, row_meta, fix_prefix, tc_scratch;
   std::vector<int32_t> h_roff;
+  // pinned staging: uploads go through an arena that is recycled at every
+  // full stream synchronisation (stage_h2d / sync_stream)
+  PinnedBuf up_arena;
+  size_t up_off = 0;
+  PinnedBuf readback;     // small D2H results (counts, histograms)
+  PinnedBuf pool_rb;      // threshold-survivor counts per level
+  // device-driven encode (fc_encode.cu)
+  DevBuf enc_orig[2], enc_code[2], enc_flag, enc_pfx, enc_count, enc_hist;
+  DevBuf leaf_flag, leaf_pos, leaf_rec, rec_out;
+  int64_t enc_records = 0;
+  fc_stats enc_stats[kLevels]{};
+  cudaEvent_t enc_ev[kLevels][3] = {};
+  bool enc_ev_ready = false;
   DevBuf iso_inv;  // uint16 [4 sides][8][256] inverse isometry maps
   bool iso_ready = false;
   fc_stats stats{};
@@ -117,6 +162,15 @@ int set_error(Ctx* c, int code, const std::string& msg);
 int cuda_check(Ctx* c, cudaError_t e, const char* what);
 int lut_slot(int n);
 
+// pinned staging helpers (fc_api.cu)
+int stage_h2d(Ctx* c, void* dst, const void* src, size_t bytes);
+int sync_stream(Ctx* c);
+
+// fc_api.cu: operand preparation around a shared synchronisation
+int prepare_begin(Ctx* c, Level& L, int level, int baseline, const double* svals, int s_count,
+                  int path, int* pending);
+int prepare_finish(Ctx* c, Level& L, int path, int pending);
+
 // fc_pool.cu
 int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
                const int32_t use_tau[4], int64_t out_sizes[4]);
@@ -124,8 +178,13 @@ int pool_set_level(Ctx* c, int level, int64_t count, const uint8_t* tiles);
 
 // fc_scan_exact.cu
 int ensure_iso_tables(Ctx* c);
-int level_prepare_exact(Ctx* c, Level& L);
+int level_prepare_exact(Ctx* c, Level& L, int tc_stats);
 int gather_ranges(Ctx* c, Level& L, const int32_t* d_origins, int64_t M);
+// gather with the range count read on the device (<= M_bound) and the
+// histogram of range offsets o = rint(rmean) accumulated into d_hist[256]
+int gather_ranges_dev(Ctx* c, Level& L, const int32_t* d_origins, const int32_t* d_M,
+                      int64_t M_bound, int32_t* d_hist);
+int roff_hist(Ctx* c, int64_t M, int32_t* d_hist);
 int load_ranges(Ctx* c, Level& L, const uint8_t* h_tiles, int64_t M);
 int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t n_range_list,
                const int32_t* d_col_list, int64_t n_col_list, uint64_t* d_keys);
@@ -139,8 +198,18 @@ int scan_rows_dropin(Ctx* c, const int16_t* ranges, const double* rmeans, int64_
                      int32_t S, int32_t baseline, int64_t* out_err, int64_t* out_idx);
 
 // fc_scan_tc.cu
-int level_prepare_tc(Ctx* c, Level& L);
+int level_prepare_tc_begin(Ctx* c, Level& L);   // device stats + async readback
+int level_prepare_tc_finish(Ctx* c, Level& L);  // after a stream sync: layout + operand build
+// Launch the contraction and its clamp corrections for M gathered ranges;
+// h_hist[o] = #ranges with offset o (host copy).  No synchronisation.
+int scan_tc_launch(Ctx* c, Level& L, int64_t M, uint64_t* d_keys, const int32_t* h_hist,
+                   cudaEvent_t ev_main_begin, cudaEvent_t ev_main_end, int64_t* out_fix_pairs);
 int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys);
+
+// fc_encode.cu
+int encode_device(Ctx* c, const double thresholds[3], int baseline, const double* svals,
+                  const int32_t s_counts[4], int path, int32_t* out_records, int64_t capacity,
+                  int64_t* out_count);
 
 }  // namespace fcb
 

@@ -164,11 +164,6 @@ __global__ void gather_keys_kernel(const uint32_t* __restrict__ idx, const doubl
   if (i < n) keys[i] = entropy_key(ent[idx[i]]);
 }
 
-__global__ void iota_kernel(uint32_t* __restrict__ v, int64_t n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] = (uint32_t)i;
-}
-
 // Lexicographic (key, index) minimum: the first window of the highest
 // entropy, i.e. np.argsort(-ent, kind="stable")[0] (cap = 1 levels).
 __device__ __forceinline__ void lex_min(uint64_t& k, uint32_t& i, uint64_t k2, uint32_t i2) {
@@ -229,6 +224,20 @@ int alloc_level(Ctx* c, Level& L, int64_t E) {
 
 }  // namespace
 
+// Two-level argmin over n keys (index = position): out_k[0], out_i[0].
+static int argmin_windows(Ctx* c, const uint64_t* keys, int64_t n, uint64_t* out_k,
+                          uint32_t* out_i) {
+  const int nb = (int)std::min<int64_t>((n + 1023) / 1024, 1024);
+  argmin_kernel<<<nb, 1024, 0, c->stream>>>(keys, nullptr, n, out_k + 1, out_i + 1);
+  argmin_kernel<<<1, 1024, 0, c->stream>>>(out_k + 1, out_i + 1, nb, out_k, out_i);
+  FC_CUDA(c, cudaGetLastError());
+  c->total_launches += 2;
+  return FC_OK;
+}
+
+// All four levels are launched back to back with per-level scratch; the only
+// synchronisation reads the threshold-survivor counts.  On return the pool
+// sizes are known; the survivor data is produced in stream order.
 int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
                const int32_t use_tau[4], int64_t out_sizes[4]) {
   if (!c->img_ptr) return set_error(c, FC_ERR_STATE, "no image set");
@@ -247,6 +256,12 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     const int slot = lut_slot(D * D);
     if (!c->lut_set[slot]) return set_error(c, FC_ERR_STATE, "entropy LUT not set");
   }
+  FC_CUDA(c, c->count_buf.reserve(64 * 4));
+  FC_CUDA(c, c->pool_rb.reserve(64));
+  int* d_nsel = reinterpret_cast<int*>(c->count_buf.ptr);
+  int* h_nsel = c->pool_rb.as<int>();
+  int nx_l[kLevels], any_tau = 0;
+  // ---- phase 1: entropies and ranking for every level ----
   for (int li = 0; li < kLevels; ++li) {
     Level& L = c->lv[li];
     const int D = kDomainSide[li];
@@ -258,119 +273,108 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     L.tc.ready = false;
     const int nx = (c->width - D) / L.stride + 1;
     const int ny = (c->height - D) / L.stride + 1;
+    nx_l[li] = nx;
     const int64_t nwin = (int64_t)nx * ny;
-    FC_CUDA(c, c->ent_scratch.reserve(nwin * 8));
-    FC_CUDA(c, c->key_in.reserve(nwin * 8));
-    FC_CUDA(c, c->key_out.reserve(nwin * 8));
-    FC_CUDA(c, c->val_in.reserve(nwin * 4));
-    FC_CUDA(c, c->val_out.reserve(nwin * 4));
-    FC_CUDA(c, c->count_buf.reserve(64));
+    FC_CUDA(c, L.win_ent.reserve(nwin * 8));
+    FC_CUDA(c, L.win_key.reserve(nwin * 8));
+    FC_CUDA(c, L.win_key2.reserve(nwin * 8 + 8 * 1032));
+    FC_CUDA(c, L.win_val.reserve(nwin * 4));
+    FC_CUDA(c, L.win_val2.reserve(nwin * 4 + 4 * 1032));
     const double* lut = c->lut[lut_slot(D * D)].as<double>();
-    int64_t blocks64 = (nwin + kEntWarps - 1) / kEntWarps;
+    const int64_t blocks64 = (nwin + kEntWarps - 1) / kEntWarps;
     const int blocks = (int)std::min<int64_t>(blocks64, (int64_t)c->sm_count * 64);
-    const double tau = use_tau[li] ? taus[li] : 0.0;
-    const int count_above = 0;  // compaction counts survivors
-    auto* cnt = c->count_buf.as<unsigned long long>();
+#define FC_LAUNCH_ENT(DD)                                                                       \
+    entropy_kernel<DD><<<blocks, kEntWarps * 32, 0, c->stream>>>(                               \
+        c->img_ptr, c->width, nx, nwin, L.stride, lut, 0.0, 0, L.win_ent.as<double>(),          \
+        L.win_key.as<uint64_t>(), L.win_val.as<uint32_t>(), nullptr)
     switch (D) {
-      case 32:
-        entropy_kernel<32><<<blocks, kEntWarps * 32, 0, c->stream>>>(
-            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, count_above,
-            c->ent_scratch.as<double>(), c->key_in.as<uint64_t>(), c->val_in.as<uint32_t>(), cnt);
-        break;
-      case 16:
-        entropy_kernel<16><<<blocks, kEntWarps * 32, 0, c->stream>>>(
-            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, count_above,
-            c->ent_scratch.as<double>(), c->key_in.as<uint64_t>(), c->val_in.as<uint32_t>(), cnt);
-        break;
-      case 8:
-        entropy_kernel<8><<<blocks, kEntWarps * 32, 0, c->stream>>>(
-            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, count_above,
-            c->ent_scratch.as<double>(), c->key_in.as<uint64_t>(), c->val_in.as<uint32_t>(), cnt);
-        break;
-      default:
-        entropy_kernel<4><<<blocks, kEntWarps * 32, 0, c->stream>>>(
-            c->img_ptr, c->width, nx, nwin, L.stride, lut, tau, count_above,
-            c->ent_scratch.as<double>(), c->key_in.as<uint64_t>(), c->val_in.as<uint32_t>(), cnt);
-        break;
+      case 32: FC_LAUNCH_ENT(32); break;
+      case 16: FC_LAUNCH_ENT(16); break;
+      case 8: FC_LAUNCH_ENT(8); break;
+      default: FC_LAUNCH_ENT(4); break;
     }
+#undef FC_LAUNCH_ENT
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 1;
-    // rank: threshold mode compacts {ent > tau} first (stable) and sorts only
-    // the survivors; cap 1 is a lexicographic argmin; other caps sort all
-    const uint32_t* order = nullptr;
-    int64_t E;
     size_t tmp = 0;
-    const unsigned tpb = 256;
     if (use_tau[li]) {
-      uint32_t* sel = c->val_out.as<uint32_t>();
-      auto* d_nsel = reinterpret_cast<int*>(c->count_buf.as<unsigned long long>() + 2);
-      iota_kernel<<<(unsigned)((nwin + tpb - 1) / tpb), tpb, 0, c->stream>>>(c->val_in.as<uint32_t>(),
-                                                                            nwin);
-      AboveTau pred{c->ent_scratch.as<double>(), tau};
-      FC_CUDA(c, cub::DeviceSelect::If(nullptr, tmp, c->val_in.as<uint32_t>(), sel, d_nsel, (int)nwin,
-                                        pred, c->stream));
+      // threshold compaction {ent > tau} in raster order
+      any_tau = 1;
+      AboveTau pred{L.win_ent.as<double>(), taus[li]};
+      FC_CUDA(c, cub::DeviceSelect::If(nullptr, tmp, L.win_val.as<uint32_t>(),
+                                        L.win_val2.as<uint32_t>(), d_nsel + li, (int)nwin, pred,
+                                        c->stream));
       FC_CUDA(c, c->cub_tmp.reserve(tmp));
-      FC_CUDA(c, cub::DeviceSelect::If(c->cub_tmp.ptr, tmp, c->val_in.as<uint32_t>(), sel, d_nsel,
-                                        (int)nwin, pred, c->stream));
-      int nsel = 0;
-      FC_CUDA(c, cudaMemcpyAsync(&nsel, d_nsel, 4, cudaMemcpyDeviceToHost, c->stream));
-      FC_CUDA(c, cudaStreamSynchronize(c->stream));
+      FC_CUDA(c, cub::DeviceSelect::If(c->cub_tmp.ptr, tmp, L.win_val.as<uint32_t>(),
+                                        L.win_val2.as<uint32_t>(), d_nsel + li, (int)nwin, pred,
+                                        c->stream));
+      FC_CUDA(c, cudaMemcpyAsync(h_nsel + li, d_nsel + li, 4, cudaMemcpyDeviceToHost, c->stream));
+      c->total_launches += 1;
+    } else if (caps[li] == 1) {
+      FC_TRY(argmin_windows(c, L.win_key.as<uint64_t>(), nwin, L.win_key2.as<uint64_t>(),
+                            L.win_val2.as<uint32_t>()));
+      L.count = 1;
+    } else {
+      FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, L.win_key.as<uint64_t>(),
+                                                 L.win_key2.as<uint64_t>(), L.win_val.as<uint32_t>(),
+                                                 L.win_val2.as<uint32_t>(), (int)nwin, 0, 64,
+                                                 c->stream));
+      FC_CUDA(c, c->cub_tmp.reserve(tmp));
+      FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, L.win_key.as<uint64_t>(),
+                                                 L.win_key2.as<uint64_t>(), L.win_val.as<uint32_t>(),
+                                                 L.win_val2.as<uint32_t>(), (int)nwin, 0, 64,
+                                                 c->stream));
+      L.count = std::min<int64_t>(caps[li], nwin);
+    }
+  }
+  if (any_tau) FC_TRY(sync_stream(c));
+  // ---- phase 2: survivors (sorted threshold sets), decimation and moments ----
+  for (int li = 0; li < kLevels; ++li) {
+    Level& L = c->lv[li];
+    const int D = kDomainSide[li];
+    const int nx = nx_l[li];
+    const int64_t nwin = (int64_t)nx * ((c->height - D) / L.stride + 1);
+    const uint32_t* order = L.win_val2.as<uint32_t>();
+    if (use_tau[li]) {
+      const int nsel = h_nsel[li];
       if (nsel == 0) {
         // caps are >= 1 (pool.py:47-48): keep the single highest-entropy window
-        argmin_kernel<<<1, 1024, 0, c->stream>>>(c->key_in.as<uint64_t>(), nullptr, nwin,
-                                                 c->key_out.as<uint64_t>(), c->val_out.as<uint32_t>());
-        E = 1;
+        FC_TRY(argmin_windows(c, L.win_key.as<uint64_t>(), nwin, L.win_key2.as<uint64_t>(),
+                              L.win_val2.as<uint32_t>()));
+        L.count = 1;
       } else {
-        E = nsel;
+        const int64_t E = nsel;
+        const unsigned tpb = 256;
         gather_keys_kernel<<<(unsigned)((E + tpb - 1) / tpb), tpb, 0, c->stream>>>(
-            sel, c->ent_scratch.as<double>(), E, c->key_in.as<uint64_t>());
-        uint32_t* sorted = c->val_in.as<uint32_t>();
-        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, c->key_in.as<uint64_t>(),
-                                                   c->key_out.as<uint64_t>(), sel, sorted, (int)E, 0,
-                                                   64, c->stream));
+            L.win_val2.as<uint32_t>(), L.win_ent.as<double>(), E, L.win_key2.as<uint64_t>());
+        size_t tmp = 0;
+        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, L.win_key2.as<uint64_t>(),
+                                                   L.win_key.as<uint64_t>(), L.win_val2.as<uint32_t>(),
+                                                   L.win_val.as<uint32_t>(), (int)E, 0, 64,
+                                                   c->stream));
         FC_CUDA(c, c->cub_tmp.reserve(tmp));
-        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, c->key_in.as<uint64_t>(),
-                                                   c->key_out.as<uint64_t>(), sel, sorted, (int)E, 0,
-                                                   64, c->stream));
-        order = sorted;
+        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, L.win_key2.as<uint64_t>(),
+                                                   L.win_key.as<uint64_t>(), L.win_val2.as<uint32_t>(),
+                                                   L.win_val.as<uint32_t>(), (int)E, 0, 64,
+                                                   c->stream));
+        order = L.win_val.as<uint32_t>();
+        L.count = E;
+        c->total_launches += 1;
       }
-      c->total_launches += 2;
-    } else if (caps[li] == 1) {
-      const int nb = (int)std::min<int64_t>((nwin + 1023) / 1024, 1024);
-      uint64_t* bk = c->key_out.as<uint64_t>();
-      uint32_t* bi = c->val_out.as<uint32_t>();
-      argmin_kernel<<<nb, 1024, 0, c->stream>>>(c->key_in.as<uint64_t>(), nullptr, nwin, bk + 1, bi + 1);
-      argmin_kernel<<<1, 1024, 0, c->stream>>>(bk + 1, bi + 1, nb, bk, bi);
-      c->total_launches += 2;
-      E = 1;
-    } else {
-      FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, c->key_in.as<uint64_t>(),
-                                                 c->key_out.as<uint64_t>(), c->val_in.as<uint32_t>(),
-                                                 c->val_out.as<uint32_t>(), (int)nwin, 0, 64,
-                                                 c->stream));
-      FC_CUDA(c, c->cub_tmp.reserve(tmp));
-      FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, c->key_in.as<uint64_t>(),
-                                                 c->key_out.as<uint64_t>(), c->val_in.as<uint32_t>(),
-                                                 c->val_out.as<uint32_t>(), (int)nwin, 0, 64,
-                                                 c->stream));
-      E = std::min<int64_t>(caps[li], nwin);
     }
-    if (!order) order = c->val_out.as<uint32_t>();
     FC_CUDA(c, cudaGetLastError());
-    L.count = E;
+    const int64_t E = L.count;
     FC_TRY(alloc_level(c, L, E));
     const int threads = 256;
     const int64_t grid = (E * 32 + threads - 1) / threads;
     survivor_kernel<<<(unsigned)grid, threads, 0, c->stream>>>(
-        c->img_ptr, c->width, nx, L.stride, D, order,
-        c->ent_scratch.as<double>(), E, L.xy.as<uint32_t>(), L.ent.as<double>(),
-        L.tiles.as<uint8_t>(), L.sum.as<int32_t>(), L.sumsq.as<int64_t>(), L.mean.as<double>(),
-        L.cnorm.as<double>());
+        c->img_ptr, c->width, nx, L.stride, D, order, L.win_ent.as<double>(), E,
+        L.xy.as<uint32_t>(), L.ent.as<double>(), L.tiles.as<uint8_t>(), L.sum.as<int32_t>(),
+        L.sumsq.as<int64_t>(), L.mean.as<double>(), L.cnorm.as<double>());
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 1;
     out_sizes[li] = E;
   }
-  FC_CUDA(c, cudaStreamSynchronize(c->stream));
   return FC_OK;
 }
 
@@ -385,7 +389,7 @@ int pool_set_level(Ctx* c, int level, int64_t count, const uint8_t* tiles) {
   L.tc.ready = false;
   if (count == 0) return FC_OK;
   FC_TRY(alloc_level(c, L, count));
-  FC_CUDA(c, cudaMemcpyAsync(L.tiles.ptr, tiles, count * L.n, cudaMemcpyHostToDevice, c->stream));
+  FC_TRY(stage_h2d(c, L.tiles.ptr, tiles, count * L.n));
   const int threads = 256;
   const int64_t grid = (count * 32 + threads - 1) / threads;
   moments_kernel<<<(unsigned)grid, threads, 0, c->stream>>>(
@@ -393,7 +397,6 @@ int pool_set_level(Ctx* c, int level, int64_t count, const uint8_t* tiles) {
       L.sum.as<int32_t>(), L.sumsq.as<int64_t>(), L.mean.as<double>(), L.cnorm.as<double>());
   FC_CUDA(c, cudaGetLastError());
   c->total_launches += 1;
-  FC_CUDA(c, cudaStreamSynchronize(c->stream));
   return FC_OK;
 }
 

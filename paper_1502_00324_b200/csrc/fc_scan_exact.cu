@@ -17,6 +17,8 @@
 // reconstruction x = clip(q + o) is formed once as packed bytes (vadd2 /
 // vmaxs2 / vmins2 / byte_perm) and reused by all 8 isometries, each costing
 // one broadcast LDS.128 plus 4 x (vabsdiffu4 + dp4a).
+#include <algorithm>
+
 #include "fc_internal.cuh"
 
 namespace fcb {
@@ -260,13 +262,17 @@ scan_rows_kernel(const int16_t* __restrict__ q, int64_t rows, int n, int S,
 }
 
 // Gather range tiles at origins and their exact moments (codec.py:164-168,
-// matcher.py:171: rmean = sum / n exactly).
+// matcher.py:171: rmean = sum / n exactly).  The range count is M, or *d_M
+// when given (device-driven quadtree); hist[o] counts offsets o = rint(rmean).
 __global__ void gather_kernel(const uint8_t* __restrict__ img, int width,
-                              const int32_t* __restrict__ origins, int64_t M, int B,
+                              const int32_t* __restrict__ origins, int64_t M,
+                              const int32_t* __restrict__ d_M, int B,
                               uint8_t* __restrict__ rtiles, double* __restrict__ rmean,
-                              int32_t* __restrict__ roff, int32_t* __restrict__ rsq) {
+                              int32_t* __restrict__ roff, int32_t* __restrict__ rsq,
+                              int32_t* __restrict__ hist) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  if (d_M) M = *d_M;
   if (warp >= M) return;
   const int x = origins[2 * warp], y = origins[2 * warp + 1];
   const int n = B * B;
@@ -285,10 +291,25 @@ __global__ void gather_kernel(const uint8_t* __restrict__ img, int width,
   }
   if (lane == 0) {
     const double mean = __ddiv_rn((double)s1, (double)n);
+    const int o = (int)rint(mean);
     rmean[warp] = mean;
-    roff[warp] = (int)rint(mean);
+    roff[warp] = o;
     rsq[warp] = s2;
+    if (hist) atomicAdd(&hist[o], 1);
   }
+}
+
+__global__ void roff_hist_kernel(const int32_t* __restrict__ roff, int64_t M,
+                                 int32_t* __restrict__ hist) {
+  __shared__ int32_t h[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[roff[i]], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
 // Moments of explicitly supplied range tiles (fc_match_tiles).
@@ -317,20 +338,71 @@ __global__ void range_moments_kernel(const uint8_t* __restrict__ rtiles, int64_t
   }
 }
 
-// q base operand: column (e, si) -> rint(s*(d - mean)) or rint(s*d) (matcher.py:143-152)
-__global__ void qbase_kernel(const uint8_t* __restrict__ tiles, const double* __restrict__ mean,
-                             int64_t E, int n, int S, const double* __restrict__ svals,
-                             int baseline, int16_t* __restrict__ q) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t total = E * S * n;
-  if (i >= total) return;
-  const int64_t col = i / n;
-  const int j = (int)(i - col * n);
-  const int64_t e = col / S;
-  const int si = (int)(col - e * S);
-  const double d = (double)tiles[e * n + j];
-  const double x = baseline ? d : __dsub_rn(d, mean[e]);
-  q[i] = (int16_t)rint(__dmul_rn(svals[si], x));
+// q base operand: column (e, si) -> rint(s*(d - mean)) or rint(s*d)
+// (matcher.py:143-152), LPC lanes per column with PPL pixels each (coalesced
+// 8/16-byte loads and stores).  With `stats` it also emits the tensor-path
+// column statistics {Q1 = sum q, Q2 = sum q^2, qmin, qmax}, the parity flag
+// and the qmin / qmax histograms (fc_scan_tc.cu).
+template <int N>
+__global__ void qprep_kernel(const uint8_t* __restrict__ tiles, const double* __restrict__ mean,
+                             int64_t ncols, int S, const double* __restrict__ svals, int baseline,
+                             int16_t* __restrict__ q, int stats, int4* __restrict__ col_stats,
+                             int32_t* __restrict__ odd, unsigned* __restrict__ hist) {
+  constexpr int LPC = N >= 8 ? N / 8 : 1;
+  constexpr int PPL = N / LPC;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t col = t / LPC;
+  const int part = (int)(t - col * LPC);
+  const bool valid = col < ncols;
+  int s1 = 0, s2 = 0, lo = 1 << 20, hi = -(1 << 20);
+  if (valid) {
+    const int64_t e = col / S;
+    const int si = (int)(col - e * S);
+    const double sv = svals[si];
+    const double dm = mean[e];
+    const uint8_t* src = tiles + e * N + part * PPL;
+    uint8_t px[PPL];
+    if constexpr (PPL == 8) {
+      const uint2 w = *reinterpret_cast<const uint2*>(src);
+      *reinterpret_cast<uint2*>(px) = w;
+    } else {
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(src);
+      *reinterpret_cast<uint32_t*>(px) = w;
+    }
+    int16_t qv[PPL];
+#pragma unroll
+    for (int k = 0; k < PPL; ++k) {
+      const double d = (double)px[k];
+      const double x = baseline ? d : __dsub_rn(d, dm);
+      const int v = (int)rint(__dmul_rn(sv, x));
+      qv[k] = (int16_t)v;
+      s1 += v;
+      s2 += v * v;
+      lo = min(lo, v);
+      hi = max(hi, v);
+    }
+    int16_t* dst = q + col * N + part * PPL;
+    if constexpr (PPL == 8) {
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(qv);
+    } else {
+      *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(qv);
+    }
+  }
+  if (!stats) return;
+#pragma unroll
+  for (int o = 1; o < LPC; o <<= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (valid && part == 0) {
+    col_stats[col] = make_int4(s1, s2, lo, hi);
+    odd[col] = s2 & 1;  // == s1 & 1
+    atomicAdd(&hist[lo + 512], 1u);
+    atomicAdd(&hist[1024 + hi + 512], 1u);
+    atomicMax(&hist[2048], (unsigned)s2);
+  }
 }
 
 __global__ void decode_keys_kernel(const unsigned long long* __restrict__ keys, int64_t M,
@@ -377,51 +449,92 @@ int ensure_iso_tables(Ctx* c) {
     }
   }
   FC_CUDA(c, c->iso_inv.reserve(h.size() * 2));
-  FC_CUDA(c, cudaMemcpy(c->iso_inv.ptr, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+  FC_TRY(stage_h2d(c, c->iso_inv.ptr, h.data(), h.size() * 2));
   c->iso_ready = true;
   return FC_OK;
 }
 
-int level_prepare_exact(Ctx* c, Level& L) {
+int level_prepare_exact(Ctx* c, Level& L, int tc_stats) {
   const int64_t cols = L.count * L.s_count;
   FC_CUDA(c, L.qbase.reserve(cols * L.n * 2 + 64));
-  const int64_t total = cols * L.n;
-  if (total > 0) {
-    FC_CUDA(c, c->svals_dev.reserve(kMaxS * 8));
-    double* d_s = c->svals_dev.as<double>();
-    FC_CUDA(c, cudaMemcpyAsync(d_s, L.svals, L.s_count * 8, cudaMemcpyHostToDevice, c->stream));
-    qbase_kernel<<<(unsigned)((total + 255) / 256), 256, 0, c->stream>>>(
-        L.tiles.as<uint8_t>(), L.mean.as<double>(), L.count, L.n, L.s_count, d_s, L.baseline,
-        L.qbase.as<int16_t>());
+  FC_CUDA(c, L.svals_d.reserve(kMaxS * 8));
+  FC_TRY(stage_h2d(c, L.svals_d.ptr, L.svals, L.s_count * 8));
+  TcOperands& T = L.tc;
+  if (tc_stats) {
+    FC_CUDA(c, T.col_stats.reserve(cols * 16 + 16));
+    FC_CUDA(c, T.odd.reserve(cols * 8 + 16));
+    FC_CUDA(c, T.hist.reserve(kTcHistWords * 4));
+    FC_CUDA(c, cudaMemsetAsync(T.hist.ptr, 0, kTcHistWords * 4, c->stream));
+  }
+  if (cols > 0) {
+    const int lpc = L.n >= 8 ? L.n / 8 : 1;
+    const int64_t threads = cols * lpc;
+    const unsigned grid = (unsigned)((threads + 255) / 256);
+#define FC_LAUNCH_QPREP(NN)                                                                   \
+    qprep_kernel<NN><<<grid, 256, 0, c->stream>>>(                                            \
+        L.tiles.as<uint8_t>(), L.mean.as<double>(), cols, L.s_count, L.svals_d.as<double>(),  \
+        L.baseline, L.qbase.as<int16_t>(), tc_stats, T.col_stats.as<int4>(),                  \
+        T.odd.as<int32_t>(), T.hist.as<unsigned>())
+    switch (L.n) {
+      case 256: FC_LAUNCH_QPREP(256); break;
+      case 64: FC_LAUNCH_QPREP(64); break;
+      case 16: FC_LAUNCH_QPREP(16); break;
+      default: FC_LAUNCH_QPREP(4); break;
+    }
+#undef FC_LAUNCH_QPREP
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 1;
-    FC_CUDA(c, cudaStreamSynchronize(c->stream));
   }
   return FC_OK;
 }
 
-int gather_ranges(Ctx* c, Level& L, const int32_t* d_origins, int64_t M) {
+static int reserve_ranges(Ctx* c, Level& L, int64_t M) {
   FC_CUDA(c, c->rtiles.reserve(M * L.n + 64));
   FC_CUDA(c, c->rmean.reserve(M * 8 + 64));
   FC_CUDA(c, c->roff.reserve(M * 4 + 64));
   FC_CUDA(c, c->rsq.reserve(M * 4 + 64));
+  return FC_OK;
+}
+
+int gather_ranges(Ctx* c, Level& L, const int32_t* d_origins, int64_t M) {
+  FC_TRY(reserve_ranges(c, L, M));
   if (M == 0) return FC_OK;
   const int threads = 256;
   gather_kernel<<<(unsigned)((M * 32 + threads - 1) / threads), threads, 0, c->stream>>>(
-      c->img_ptr, c->width, d_origins, M, L.side, c->rtiles.as<uint8_t>(), c->rmean.as<double>(),
-      c->roff.as<int32_t>(), c->rsq.as<int32_t>());
+      c->img_ptr, c->width, d_origins, M, nullptr, L.side, c->rtiles.as<uint8_t>(),
+      c->rmean.as<double>(), c->roff.as<int32_t>(), c->rsq.as<int32_t>(), nullptr);
+  FC_CUDA(c, cudaGetLastError());
+  c->stats.kernel_launches += 1;
+  return FC_OK;
+}
+
+int gather_ranges_dev(Ctx* c, Level& L, const int32_t* d_origins, const int32_t* d_M,
+                      int64_t M_bound, int32_t* d_hist) {
+  FC_TRY(reserve_ranges(c, L, M_bound));
+  if (M_bound == 0) return FC_OK;
+  const int threads = 256;
+  gather_kernel<<<(unsigned)((M_bound * 32 + threads - 1) / threads), threads, 0, c->stream>>>(
+      c->img_ptr, c->width, d_origins, M_bound, d_M, L.side, c->rtiles.as<uint8_t>(),
+      c->rmean.as<double>(), c->roff.as<int32_t>(), c->rsq.as<int32_t>(), d_hist);
+  FC_CUDA(c, cudaGetLastError());
+  c->total_launches += 1;
+  return FC_OK;
+}
+
+int roff_hist(Ctx* c, int64_t M, int32_t* d_hist) {
+  FC_CUDA(c, cudaMemsetAsync(d_hist, 0, 256 * 4, c->stream));
+  if (M == 0) return FC_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>((M + 255) / 256, c->sm_count);
+  roff_hist_kernel<<<grid, 256, 0, c->stream>>>(c->roff.as<int32_t>(), M, d_hist);
   FC_CUDA(c, cudaGetLastError());
   c->stats.kernel_launches += 1;
   return FC_OK;
 }
 
 int load_ranges(Ctx* c, Level& L, const uint8_t* h_tiles, int64_t M) {
-  FC_CUDA(c, c->rtiles.reserve(M * L.n + 64));
-  FC_CUDA(c, c->rmean.reserve(M * 8 + 64));
-  FC_CUDA(c, c->roff.reserve(M * 4 + 64));
-  FC_CUDA(c, c->rsq.reserve(M * 4 + 64));
+  FC_TRY(reserve_ranges(c, L, M));
   if (M == 0) return FC_OK;
-  FC_CUDA(c, cudaMemcpyAsync(c->rtiles.ptr, h_tiles, M * L.n, cudaMemcpyHostToDevice, c->stream));
+  FC_TRY(stage_h2d(c, c->rtiles.ptr, h_tiles, M * L.n));
   const int threads = 256;
   range_moments_kernel<<<(unsigned)((M * 32 + threads - 1) / threads), threads, 0, c->stream>>>(
       c->rtiles.as<uint8_t>(), M, L.n, c->rmean.as<double>(), c->roff.as<int32_t>(),
@@ -438,9 +551,7 @@ int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t
   const int64_t nr = d_range_list ? n_range_list : M;
   const int64_t nc = d_col_list ? n_col_list : ncols;
   if (nr == 0 || nc == 0) return FC_OK;
-  FC_CUDA(c, c->svals_dev.reserve(kMaxS * 8));
-  double* d_s = c->svals_dev.as<double>();
-  FC_CUDA(c, cudaMemcpyAsync(d_s, L.svals, L.s_count * 8, cudaMemcpyHostToDevice, c->stream));
+  const double* d_s = L.svals_d.as<double>();
   const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
   auto* keys = reinterpret_cast<unsigned long long*>(d_keys);
   const unsigned gx = (unsigned)((nc + kColsPerBlock - 1) / kColsPerBlock);
@@ -472,9 +583,7 @@ int scan_exact_jobs(Ctx* c, Level& L, const int4* d_jobs, const int64_t* d_prefi
                     const int32_t* d_high, uint64_t* d_keys) {
   if (n_jobs == 0 || total_blocks == 0) return FC_OK;
   FC_TRY(ensure_iso_tables(c));
-  FC_CUDA(c, c->svals_dev.reserve(kMaxS * 8));
-  double* d_s = c->svals_dev.as<double>();
-  FC_CUDA(c, cudaMemcpyAsync(d_s, L.svals, L.s_count * 8, cudaMemcpyHostToDevice, c->stream));
+  const double* d_s = L.svals_d.as<double>();
   const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
   auto* keys = reinterpret_cast<unsigned long long*>(d_keys);
 #define FC_LAUNCH_JOBS(NN)                                                                      \

@@ -319,32 +319,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
 
 // Per column: Q1, Q2, qmin, qmax; sort keys for the clamp-reach lists; odd-Q1
 // flags for the parity grouping; histograms of qmin / qmax; max of Q2.
-__global__ void col_stats_kernel(const int16_t* __restrict__ qbase, int64_t ncols, int n,
-                                 int4* __restrict__ stats, uint32_t* __restrict__ qmin_key,
-                                 uint32_t* __restrict__ qmax_key, int32_t* __restrict__ ids,
-                                 int32_t* __restrict__ odd, unsigned* __restrict__ hist_qmin,
-                                 unsigned* __restrict__ hist_qmax, unsigned* __restrict__ q2max) {
-  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= ncols) return;
-  const int16_t* q = qbase + col * n;
-  int s1 = 0, s2 = 0, lo = 1 << 20, hi = -(1 << 20);
-  for (int k = 0; k < n; ++k) {
-    const int v = q[k];
-    s1 += v;
-    s2 += v * v;
-    lo = min(lo, v);
-    hi = max(hi, v);
-  }
-  stats[col] = make_int4(s1, s2, lo, hi);
-  qmin_key[col] = (uint32_t)(lo + 512);
-  qmax_key[col] = (uint32_t)(512 - hi);  // ascending key == qmax descending
-  ids[col] = (int32_t)col;
-  odd[col] = s2 & 1;  // == s1 & 1
-  atomicAdd(&hist_qmin[lo + 512], 1u);
-  atomicAdd(&hist_qmax[hi + 512], 1u);
-  atomicMax(q2max, (unsigned)s2);
-}
-
 // B operand in grouped slot order, K-major canonical UMMA layout per tile:
 // k in [0, kbase): -q planes;  then m digits of hq (weight 255), 2 remainder
 // slots (weight 1), 2 halves of Q1 (weight o);  zero up to kpad.
@@ -473,6 +447,13 @@ __global__ void reach_scatter_kernel(const int4* __restrict__ stats, int64_t nco
   reach_high[atomicAdd(&cur_high[st.w + 512], 1)] = (int32_t)col;
 }
 
+// Ranges bucketed by offset o (counting sort; cursors = exclusive bucket starts).
+__global__ void order_scatter_kernel(const int32_t* __restrict__ roff, int64_t M,
+                                     int32_t* __restrict__ cursors, int32_t* __restrict__ order) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < M) order[atomicAdd(&cursors[roff[i]], 1)] = (int32_t)i;
+}
+
 __global__ void fill_i32_kernel(int32_t* __restrict__ p, int64_t n, int32_t v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -480,46 +461,43 @@ __global__ void fill_i32_kernel(int32_t* __restrict__ p, int64_t n, int32_t v) {
 
 }  // namespace
 
-int level_prepare_tc(Ctx* c, Level& L) {
+// Phase 1 (device): parity prefix of the column statistics that qprep_kernel
+// produced, then an async readback of the histograms into pinned memory.
+int level_prepare_tc_begin(Ctx* c, Level& L) {
   TcOperands& T = L.tc;
   T.ready = false;
   if (L.baseline || L.n < 16) return set_error(c, FC_ERR_ARG, "tensor path: proposed mode, B >= 4");
   const int64_t ncols = L.count * L.s_count;
   if (ncols >= (1ll << 31) - 1024) return set_error(c, FC_ERR_ARG, "too many columns");
+  if (ncols == 0) return set_error(c, FC_ERR_EMPTY_POOL, "no domain entries");
   T.ncols = ncols;
-  const size_t hist_words = 1024 + 1024 + 4;
-  FC_CUDA(c, T.col_stats.reserve(ncols * 16));
-  FC_CUDA(c, c->key_in.reserve(ncols * 8));
-  FC_CUDA(c, c->key_out.reserve(ncols * 4));
-  FC_CUDA(c, c->val_in.reserve(ncols * 4));
-  FC_CUDA(c, c->val_out.reserve(ncols * 8 + 16));
-  FC_CUDA(c, c->tc_scratch.reserve(hist_words * 4));
-  uint32_t* k_min = c->key_in.as<uint32_t>();
-  uint32_t* k_max = k_min + ncols;
-  int32_t* odd = c->val_out.as<int32_t>();
+  int32_t* odd = T.odd.as<int32_t>();
   int32_t* odd_prefix = odd + ncols;
-  unsigned* hist = c->tc_scratch.as<unsigned>();
-  FC_CUDA(c, cudaMemsetAsync(hist, 0, hist_words * 4, c->stream));
-  col_stats_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, c->stream>>>(
-      L.qbase.as<int16_t>(), ncols, L.n, T.col_stats.as<int4>(), k_min, k_max,
-      c->val_in.as<int32_t>(), odd, hist, hist + 1024, hist + 2048);
-  FC_CUDA(c, cudaGetLastError());
-  c->total_launches += 1;
-  // parity grouping: exclusive prefix of the odd flags
   size_t need = 0;
   FC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, need, odd, odd_prefix, (int)ncols, c->stream));
   FC_CUDA(c, c->cub_tmp.reserve(need));
   FC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.ptr, need, odd, odd_prefix, (int)ncols,
                                            c->stream));
-  std::vector<unsigned> h(hist_words);
-  int32_t last_prefix = 0, last_odd = 0;
-  FC_CUDA(c, cudaMemcpyAsync(h.data(), hist, hist_words * 4, cudaMemcpyDeviceToHost, c->stream));
-  FC_CUDA(c, cudaMemcpyAsync(&last_prefix, odd_prefix + ncols - 1, 4, cudaMemcpyDeviceToHost,
+  FC_CUDA(c, T.readback.reserve(kTcHistWords * 4 + 16));
+  unsigned* rb = T.readback.as<unsigned>();
+  FC_CUDA(c, cudaMemcpyAsync(rb, T.hist.ptr, kTcHistWords * 4, cudaMemcpyDeviceToHost, c->stream));
+  FC_CUDA(c, cudaMemcpyAsync(rb + kTcHistWords, odd_prefix + ncols - 1, 4, cudaMemcpyDeviceToHost,
                              c->stream));
-  FC_CUDA(c, cudaMemcpyAsync(&last_odd, odd + ncols - 1, 4, cudaMemcpyDeviceToHost, c->stream));
-  FC_CUDA(c, cudaStreamSynchronize(c->stream));
-  const unsigned* hmin = h.data();
-  const unsigned* hmax = h.data() + 1024;
+  FC_CUDA(c, cudaMemcpyAsync(rb + kTcHistWords + 1, odd + ncols - 1, 4, cudaMemcpyDeviceToHost,
+                             c->stream));
+  return FC_OK;
+}
+
+// Phase 2 (host, after the stream reached the readback): K layout, tile
+// table, clamp-reach lists and the grouped B operand.  Nothing blocks.
+int level_prepare_tc_finish(Ctx* c, Level& L) {
+  TcOperands& T = L.tc;
+  const int64_t ncols = T.ncols;
+  const unsigned* h = T.readback.as<unsigned>();
+  const int32_t last_prefix = (int32_t)h[kTcHistWords];
+  const int32_t last_odd = (int32_t)h[kTcHistWords + 1];
+  const unsigned* hmin = h;
+  const unsigned* hmax = h + 1024;
   const unsigned q2max = h[2048];
   int gmin = 1 << 20, gmax = -(1 << 20);
   for (int v = 0; v < 1024; ++v) {
@@ -532,15 +510,19 @@ int level_prepare_tc(Ctx* c, Level& L) {
   T.m_digits = std::max(1, (hq_max / 255 + 126) / 127);
   T.kpad = ((T.planes * L.n + T.m_digits + 4 + 31) / 32) * 32;
   // clamp-reach counts: low_count[o] = #{qmin < -o}, high_count[o] = #{qmax > 255 - o}
-  for (int o = 0; o < 256; ++o) {
-    int64_t lo = 0, hi = 0;
+  {
+    // prefix sums over the histograms (bin v holds q = v - 512)
+    std::vector<int64_t> cmin(1025, 0), cmax(1025, 0);
     for (int v = 0; v < 1024; ++v) {
-      const int q = v - 512;
-      if (q < -o) lo += hmin[v];
-      if (q > 255 - o) hi += hmax[v];
+      cmin[v + 1] = cmin[v] + hmin[v];
+      cmax[v + 1] = cmax[v] + hmax[v];
     }
-    T.low_count[o] = lo;
-    T.high_count[o] = hi;
+    for (int o = 0; o < 256; ++o) {
+      // q < -o  <=>  v = q + 512 < 512 - o
+      T.low_count[o] = cmin[512 - o];
+      // q > 255 - o  <=>  v > 767 - o
+      T.high_count[o] = cmax[1024] - cmax[768 - o];
+    }
   }
   // two parity groups, each padded to whole tiles
   const int64_t n_odd = (int64_t)last_prefix + last_odd;
@@ -570,7 +552,7 @@ int level_prepare_tc(Ctx* c, Level& L) {
     FC_CUDA(c, T.reach_high.reserve(ncols * 4));
     FC_CUDA(c, c->key_out.reserve(2048 * 4));
     int32_t* d_cur = c->key_out.as<int32_t>();
-    FC_CUDA(c, cudaMemcpyAsync(d_cur, cur.data(), 2048 * 4, cudaMemcpyHostToDevice, c->stream));
+    FC_TRY(stage_h2d(c, d_cur, cur.data(), 2048 * 4));
     reach_scatter_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, c->stream>>>(
         T.col_stats.as<int4>(), ncols, d_cur, d_cur + 1024, T.reach_low.as<int32_t>(),
         T.reach_high.as<int32_t>());
@@ -582,25 +564,26 @@ int level_prepare_tc(Ctx* c, Level& L) {
   FC_CUDA(c, T.b_tiles.reserve(slots * T.kpad));
   FC_CUDA(c, T.meta.reserve(slots * 4));
   FC_CUDA(c, T.tile_q1.reserve(T.ntiles * 8 + 16));
+  // only the padding slots of the last tile of each group need zero operands
   FC_CUDA(c, cudaMemsetAsync(T.b_tiles.ptr, 0, slots * T.kpad, c->stream));
   fill_i32_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, c->stream>>>(T.meta.as<int32_t>(),
                                                                          slots, -1);
-  FC_CUDA(c, cudaMemcpyAsync(T.tile_q1.ptr, tinfo.data(), T.ntiles * 8, cudaMemcpyHostToDevice,
-                             c->stream));
+  FC_TRY(stage_h2d(c, T.tile_q1.ptr, tinfo.data(), T.ntiles * 8));
   const int64_t work = ncols * (T.kpad / 16);
   build_b_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
       L.qbase.as<int16_t>(), L.n, T.kpad, T.planes, T.m_digits, ncols, T.col_stats.as<int4>(),
-      odd_prefix, odd_base, T.b_tiles.as<int8_t>(), T.meta.as<int32_t>());
+      T.odd.as<int32_t>() + ncols, odd_base, T.b_tiles.as<int8_t>(), T.meta.as<int32_t>());
   FC_CUDA(c, cudaGetLastError());
   c->total_launches += 2;
-  FC_CUDA(c, cudaStreamSynchronize(c->stream));
   T.ready = true;
   return FC_OK;
 }
 
-int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys) {
+int scan_tc_launch(Ctx* c, Level& L, int64_t M, uint64_t* d_keys, const int32_t* h_hist,
+                   cudaEvent_t ev_main_begin, cudaEvent_t ev_main_end, int64_t* out_fix_pairs) {
   TcOperands& T = L.tc;
   if (!T.ready) return set_error(c, FC_ERR_STATE, "tensor operands not prepared");
+  if (M == 0) return FC_OK;
   FC_TRY(ensure_iso_tables(c));
   TcParams prm{};
   prm.kpad = T.kpad;
@@ -619,10 +602,6 @@ int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys) {
   const int64_t rows_pad = (int64_t)n_rgroups * RG * kTileM;
   FC_CUDA(c, c->a_tiles.reserve(rows_pad * T.kpad));
   FC_CUDA(c, c->row_meta.reserve(rows_pad * 16));
-  // the host needs each range's offset o to plan the clamp corrections
-  c->h_roff.resize(M);
-  FC_CUDA(c, cudaMemcpyAsync(c->h_roff.data(), c->roff.ptr, M * 4, cudaMemcpyDeviceToHost, c->stream));
-  FC_CUDA(c, cudaEventRecord(c->ev1, c->stream));
   const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
   const int64_t work = rows_pad * (T.kpad / 16);
   build_a_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
@@ -663,42 +642,30 @@ int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys) {
   prm.n_units = n_spans * n_rgroups;
   if (const char* dbg = getenv("FC_TC_DEBUG_MODE")) prm.debug_mode = atoi(dbg);
 
-  cudaEvent_t m0, m1;
-  cudaEventCreate(&m0);
-  cudaEventCreate(&m1);
-  cudaEventRecord(m0, c->stream);
+  if (ev_main_begin) FC_CUDA(c, cudaEventRecord(ev_main_begin, c->stream));
   const uint32_t smem = smem_bytes(prm);
-  cudaError_t err = cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
-  if (err == cudaSuccess) {
-    const int grid = (int)std::min<int64_t>(prm.n_units, c->sm_count);
-    tc_scan_kernel<<<grid, kThreads, smem, c->stream>>>(prm);
-    err = cudaGetLastError();
+  if (!c->tc_attr_set) {
+    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    227 * 1024));
+    c->tc_attr_set = true;
   }
-  cudaEventRecord(m1, c->stream);
-  if (err != cudaSuccess) {
-    cudaEventDestroy(m0);
-    cudaEventDestroy(m1);
-    return cuda_check(c, err, "tc_scan_kernel launch");
-  }
+  const int grid = (int)std::min<int64_t>(prm.n_units, c->sm_count);
+  tc_scan_kernel<<<grid, kThreads, smem, c->stream>>>(prm);
+  FC_CUDA(c, cudaGetLastError());
+  if (ev_main_end) FC_CUDA(c, cudaEventRecord(ev_main_end, c->stream));
   c->stats.kernel_launches += 1;
 
   // ---- clamp corrections (exact kernel on clamp-active pairs) ----
-  FC_CUDA(c, cudaEventSynchronize(c->ev1));
-  std::vector<int32_t> order(M);
-  std::vector<int64_t> start(257, 0);
-  for (int64_t i = 0; i < M; ++i) start[c->h_roff[i] + 1]++;
-  for (int o = 0; o < 256; ++o) start[o + 1] += start[o];
-  {
-    std::vector<int64_t> pos(start.begin(), start.end() - 1);
-    for (int64_t i = 0; i < M; ++i) order[pos[c->h_roff[i]]++] = (int32_t)i;
-  }
+  // ranges bucketed by o on the device; jobs planned here from the histogram
+  std::vector<int32_t> start(257, 0);
+  for (int o = 0; o < 256; ++o) start[o + 1] = start[o] + h_hist[o];
+  if ((int64_t)start[256] != M) return set_error(c, FC_ERR_STATE, "offset histogram mismatch");
   std::vector<int4> jobs;
   std::vector<int64_t> prefix(1, 0);
   int64_t fix_pairs = 0;
   const int RB = 8, CB = 128;
   for (int o = 0; o < 256; ++o) {
-    const int64_t cnt = start[o + 1] - start[o];
+    const int64_t cnt = h_hist[o];
     if (!cnt) continue;
     const int64_t lists[2] = {T.low_count[o], T.high_count[o]};
     for (int kind = 0; kind < 2; ++kind) {
@@ -709,35 +676,47 @@ int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys) {
       fix_pairs += cnt * ncol;
     }
   }
-  c->stats.fix_pairs = fix_pairs;
-  float fix_ms = 0.f;
-  int rc = FC_OK;
+  if (out_fix_pairs) *out_fix_pairs = fix_pairs;
   if (!jobs.empty()) {
     FC_CUDA(c, c->fix_rows.reserve(M * 4));
     FC_CUDA(c, c->fix_jobs.reserve(jobs.size() * 16));
     FC_CUDA(c, c->fix_cols.reserve(prefix.size() * 8));
-    FC_CUDA(c, cudaMemcpyAsync(c->fix_rows.ptr, order.data(), M * 4, cudaMemcpyHostToDevice, c->stream));
-    FC_CUDA(c, cudaMemcpyAsync(c->fix_jobs.ptr, jobs.data(), jobs.size() * 16, cudaMemcpyHostToDevice,
-                               c->stream));
-    FC_CUDA(c, cudaMemcpyAsync(c->fix_cols.ptr, prefix.data(), prefix.size() * 8,
-                               cudaMemcpyHostToDevice, c->stream));
-    rc = scan_exact_jobs(c, L, c->fix_jobs.as<int4>(), c->fix_cols.as<int64_t>(), (int)jobs.size(),
-                         prefix.back(), c->fix_rows.as<int32_t>(), T.reach_low.as<int32_t>(),
-                         T.reach_high.as<int32_t>(), d_keys);
-    if (rc == FC_OK) {
-      cudaEventRecord(c->ev1, c->stream);
-      cudaEventSynchronize(c->ev1);
-      cudaEventElapsedTime(&fix_ms, m1, c->ev1);
-    }
+    FC_CUDA(c, c->tc_scratch.reserve(256 * 4));
+    int32_t* d_cursor = c->tc_scratch.as<int32_t>();
+    FC_TRY(stage_h2d(c, d_cursor, start.data(), 256 * 4));
+    order_scatter_kernel<<<(unsigned)((M + 255) / 256), 256, 0, c->stream>>>(
+        c->roff.as<int32_t>(), M, d_cursor, c->fix_rows.as<int32_t>());
+    FC_CUDA(c, cudaGetLastError());
+    c->stats.kernel_launches += 1;
+    FC_TRY(stage_h2d(c, c->fix_jobs.ptr, jobs.data(), jobs.size() * 16));
+    FC_TRY(stage_h2d(c, c->fix_cols.ptr, prefix.data(), prefix.size() * 8));
+    FC_TRY(scan_exact_jobs(c, L, c->fix_jobs.as<int4>(), c->fix_cols.as<int64_t>(),
+                           (int)jobs.size(), prefix.back(), c->fix_rows.as<int32_t>(),
+                           T.reach_low.as<int32_t>(), T.reach_high.as<int32_t>(), d_keys));
   }
-  cudaEventSynchronize(m1);
-  float main_ms = 0.f;
-  cudaEventElapsedTime(&main_ms, m0, m1);
-  cudaEventDestroy(m0);
-  cudaEventDestroy(m1);
-  if (rc != FC_OK) return rc;
+  return FC_OK;
+}
+
+// Per-call API variant: histogram of the gathered ranges' offsets, one sync,
+// then the asynchronous launch; fills the main / fix timings of fc_stats.
+int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys) {
+  FC_CUDA(c, c->enc_hist.reserve(256 * 4));
+  FC_TRY(roff_hist(c, M, c->enc_hist.as<int32_t>()));
+  FC_CUDA(c, c->readback.reserve(256 * 4));
+  FC_CUDA(c, cudaMemcpyAsync(c->readback.ptr, c->enc_hist.ptr, 256 * 4, cudaMemcpyDeviceToHost,
+                             c->stream));
+  FC_TRY(sync_stream(c));
+  std::vector<int32_t> hist(c->readback.as<int32_t>(), c->readback.as<int32_t>() + 256);
+  int64_t fix_pairs = 0;
+  FC_TRY(scan_tc_launch(c, L, M, d_keys, hist.data(), c->tc_ev[0], c->tc_ev[1], &fix_pairs));
+  FC_CUDA(c, cudaEventRecord(c->tc_ev[2], c->stream));
+  FC_CUDA(c, cudaEventSynchronize(c->tc_ev[2]));
+  float main_ms = 0.f, fix_ms = 0.f;
+  cudaEventElapsedTime(&main_ms, c->tc_ev[0], c->tc_ev[1]);
+  cudaEventElapsedTime(&fix_ms, c->tc_ev[1], c->tc_ev[2]);
   c->stats.main_ms = main_ms;
   c->stats.fix_ms = fix_ms;
+  c->stats.fix_pairs = fix_pairs;
   c->stats.rescans = 0;
   return FC_OK;
 }

@@ -80,7 +80,10 @@ class CoordTable:
     __slots__ = ("array",)
 
     def __init__(self, array):
-        a = np.asarray(array, dtype=np.int64).reshape(-1, 2)
+        a = np.asarray(array)
+        if a.dtype != np.uint16:  # device tables arrive as u16 pairs (the stream format)
+            a = a.astype(np.int64)
+        a = a.reshape(-1, 2)
         a.flags.writeable = False
         self.array = a
 
@@ -106,7 +109,7 @@ class CoordTable:
         return np.array_equal(self.array, o)
 
     def __hash__(self):
-        return hash(self.array.tobytes())
+        return hash(self.array.astype(np.int64).tobytes())
 
     def __repr__(self):
         return f"CoordTable({len(self)} origins)"
@@ -130,7 +133,7 @@ class DomainPool:
 
     def coords_array(self, level: int) -> np.ndarray:
         if level not in self._coords:
-            self._coords[level] = self.context.pool_coords(level, self.size(level)).astype(np.int64)
+            self._coords[level] = self.context.pool_coords(level, self.size(level))
         return self._coords[level]
 
     def coords(self, level: int) -> CoordTable:

@@ -111,7 +111,7 @@ def test_scan_candidates_dropin_reference_layout(ctx):
             assert np.array_equal(e_ref, e_dev) and np.array_equal(i_ref, i_dev)
 
 
-def _encode_golden(g, tag, path, taus=None):
+def _encode_golden(g, tag, path, taus=None, driver=None):
     img = g[f"image_{tag}"]
     caps = tuple(int(v) for v in g[f"caps_{tag}"])
     strides = tuple(int(v) for v in g[f"strides_{tag}"])
@@ -120,7 +120,7 @@ def _encode_golden(g, tag, path, taus=None):
     params = fc.PoolParams(pool_cap=max(caps), strides=strides, level_caps=caps,
                            entropy_thresholds=taus)
     cfg = fc.EncoderConfig(pool=params, policy=fc.SPolicy(mode=mode), thresholds=thr, path=path)
-    return fc.encode(fc.GrayImage(img), cfg)
+    return (driver or fc.encode)(fc.GrayImage(img), cfg)
 
 
 @pytest.mark.parametrize("path", PATHS)
@@ -163,3 +163,30 @@ def test_entropy_threshold_compaction_equals_caps():
     taus = tuple(None if one else t for one, t in zip(wl.cap_one, wl.taus))
     stream, _ = _encode_golden(g, "c2", "auto", taus=taus)
     assert fc.serialize(stream) == g["bytes_c2"].tobytes()
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("tag", ["tiled4_proposed", "tiled_baseline", "noise", "c1"])
+def test_levelwise_driver_bytes_identical(tag, path):
+    """The host-driven level seam (fc_match_level) gives the same stream as fc_encode."""
+    from paper_1502_00324_b200.codec import encode_levelwise
+
+    g = load_golden("encode_cases.npz")
+    if path == "tensor" and "baseline" in tag:
+        pytest.skip("tensor path is proposed-mode only")
+    stream, report = _encode_golden(g, tag, path, driver=encode_levelwise)
+    assert fc.serialize(stream) == g[f"bytes_{tag}"].tobytes()
+    assert report.collage_ssd == int(g[f"collage_{tag}"])
+
+
+def test_encode_records_layout_and_stats():
+    """fc_encode records: steps tile the image; per-level stats are consistent."""
+    g = load_golden("encode_c2.npz")
+    stream, report = _encode_golden(g, "c2", "auto")
+    rec = stream.records.array
+    side = np.array([0, 16, 8, 4, 2])[rec[:, 0]]
+    assert int((side * side).sum()) == report.width * report.height
+    assert sum(report.step_blocks) == rec.shape[0]
+    for ls in report.level_stats:
+        assert ls["comparisons"] == ls["ranges"] * ls["columns"] * 8
+        assert ls["scan_ms"] > 0
