@@ -1,7 +1,9 @@
 // C ABI of fracodec_b200 (declared in include/fracodec_b200.h).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <chrono>
 #include <new>
 
 #include "fc_internal.cuh"
@@ -21,6 +23,43 @@ int cuda_check(Ctx* c, cudaError_t e, const char* what) {
   snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s", cudaGetErrorName(e), cudaGetErrorString(e),
            what);
   return set_error(c, FC_ERR_CUDA, buf);
+}
+
+static double host_us() {
+  return std::chrono::duration<double, std::micro>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+void trace_reset(Ctx* c) {
+  if (!c->trace) return;
+  c->trace_name.clear();
+  c->trace_host_us.clear();
+}
+
+void trace_mark(Ctx* c, const char* name) {
+  if (!c->trace) return;
+  const size_t k = c->trace_name.size();
+  if (k >= c->trace_ev.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    c->trace_ev.push_back(e);
+  }
+  cudaEventRecord(c->trace_ev[k], c->stream);
+  c->trace_name.push_back(name);
+  c->trace_host_us.push_back(host_us());
+}
+
+void trace_dump(Ctx* c) {
+  if (!c->trace || c->trace_name.empty()) return;
+  cudaStreamSynchronize(c->stream);
+  fprintf(stderr, "[fc_trace] %-22s %10s %10s\n", "mark", "host_us", "dev_us");
+  for (size_t k = 0; k < c->trace_name.size(); ++k) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->trace_ev[0], c->trace_ev[k]);
+    fprintf(stderr, "[fc_trace] %-22s %10.1f %10.1f\n", c->trace_name[k].c_str(),
+            c->trace_host_us[k] - c->trace_host_us[0], 1e3 * ms);
+  }
 }
 
 int sync_stream(Ctx* c) {
@@ -149,6 +188,9 @@ int fc_ctx_create(int device, fc_ctx** out) {
   if (!c) return FC_ERR_ARG;
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
+  if (const char* w = getenv("FC_TC_WAIT")) c->tc_wait_mode = atoi(w);
+  if (const char* f = getenv("FC_TC_FORWARD")) c->tc_forward = atoi(f);
+  if (const char* t = getenv("FC_TRACE")) c->trace = atoi(t);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaEventCreate(&c->ev2) != cudaSuccess || cudaEventCreate(&c->tc_ev[0]) != cudaSuccess ||
@@ -175,11 +217,12 @@ void fc_ctx_destroy(fc_ctx* c) {
                     &c->fix_prefix, &c->tc_scratch, &c->enc_orig[0], &c->enc_orig[1],
                     &c->enc_code[0], &c->enc_code[1], &c->enc_flag, &c->enc_pfx,
                     &c->enc_count, &c->enc_hist, &c->leaf_flag, &c->leaf_pos, &c->leaf_rec,
-                    &c->rec_out};
+                    &c->rec_out, &c->tc_plan, &c->enc_fix};
   for (DevBuf* b : bufs) b->release();
   c->up_arena.release();
   c->readback.release();
   c->pool_rb.release();
+  c->coords_pinned.release();
   if (c->enc_ev_ready)
     for (auto& pr : c->enc_ev)
       for (auto& e : pr) cudaEventDestroy(e);
@@ -187,7 +230,7 @@ void fc_ctx_destroy(fc_ctx* c) {
   for (auto& L : c->lv) {
     DevBuf* lb[] = {&L.xy, &L.ent, &L.tiles, &L.sum, &L.sumsq, &L.mean, &L.cnorm, &L.qbase,
                     &L.tc.b_tiles, &L.tc.hq, &L.tc.meta, &L.tc.tile_q1, &L.tc.col_stats,
-                    &L.tc.reach_low, &L.tc.reach_high, &L.tc.odd, &L.tc.hist, &L.svals_d,
+                    &L.tc.reach_low, &L.tc.reach_high, &L.tc.odd, &L.tc.hist, &L.svals_d, &L.tc.reach_counts,
                     &L.win_ent, &L.win_key, &L.win_key2, &L.win_val, &L.win_val2};
     for (DevBuf* b : lb) b->release();
     L.tc.readback.release();
@@ -196,6 +239,7 @@ void fc_ctx_destroy(fc_ctx* c) {
   cudaEventDestroy(c->ev1);
   cudaEventDestroy(c->ev2);
   for (auto& e : c->tc_ev) cudaEventDestroy(e);
+  for (auto& e : c->trace_ev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -228,6 +272,9 @@ int fc_set_image(fc_ctx* c, const uint8_t* pixels, int width, int height) {
   if (width < 1 || height < 1 || !pixels) return set_error(c, FC_ERR_ARG, "bad image");
   if (width > 65535 || height > 65535)
     return set_error(c, FC_ERR_ARG, "image sides must fit the u16 stream coordinates");
+  trace_reset(c);
+  trace_mark(c, "set_image");
+  c->coords_valid = false;
   c->width = width;
   c->height = height;
   if (c->device_io) {
@@ -249,6 +296,7 @@ int fc_set_image(fc_ctx* c, const uint8_t* pixels, int width, int height) {
 int fc_pool_build(fc_ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
                   const int32_t use_tau[4], int64_t out_sizes[4]) {
   cudaSetDevice(c->device);
+  c->coords_valid = false;
   const double zero_taus[4] = {0, 0, 0, 0};
   const int32_t no_tau[4] = {0, 0, 0, 0};
   return pool_build(c, strides, caps, taus ? taus : zero_taus, use_tau ? use_tau : no_tau,
@@ -259,6 +307,7 @@ int fc_pool_set_level(fc_ctx* c, int level, int64_t count, const uint8_t* tiles)
   cudaSetDevice(c->device);
   FC_TRY(check_level(c, level));
   if (count < 0 || (count > 0 && !tiles)) return set_error(c, FC_ERR_ARG, "bad tiles");
+  c->coords_valid = false;
   return pool_set_level(c, level, count, tiles);
 }
 
@@ -274,6 +323,10 @@ int fc_pool_coords(fc_ctx* c, int level, uint16_t* xy) {
   Level& L = c->lv[level - 1];
   if (L.count == 0) return FC_OK;
   // xy words are x | y << 16: in little-endian memory exactly the (x, y) u16 pair
+  if (c->coords_valid) {  // prefetched by fc_encode
+    memcpy(xy, c->coords_pinned.as<uint32_t>() + c->coords_off[level - 1], L.count * 4);
+    return FC_OK;
+  }
   FC_CUDA(c, cudaMemcpyAsync(xy, L.xy.ptr, L.count * 4, cudaMemcpyDeviceToHost, c->stream));
   return sync_stream(c);
 }

@@ -1,11 +1,12 @@
 // Device-driven quadtree encode (codec.py:114-161 level loop, codec.py:185-193
 // match_level, codec.py:196-224 record assembly).
 //
-// The host keeps only launch decisions.  Per level it needs the range count M
-// and the histogram of range offsets o (to plan the clamp-correction jobs of
-// the tensor path), read back with ONE stream synchronisation per level; the
-// split test, the child origins and depth-first codes, and the leaf records
-// are produced on the device:
+// The host keeps only launch decisions and never waits inside the level loop:
+// every kernel reads the level's range count from device memory and is
+// launched for the level's upper bound (n_top * 4^(level-1) ranges); the
+// tensor path plans its unit decomposition and clamp-correction jobs on the
+// device.  The split test, child origins, depth-first codes and leaf records
+// are all produced on the device:
 //
 //   classify_kernel : err = key >> 32; split = err > t^2 * B^2 (levels 1-3);
 //                     leaves write their record into a slot indexed by the
@@ -47,14 +48,19 @@ __device__ __forceinline__ int baseline_offset(double rmean, double s, double dm
 }
 
 // Split test and leaf records.  rec = {step, offset, iso, addr, sidx, err}.
-__global__ void classify_kernel(const unsigned long long* __restrict__ keys, int64_t M, int level,
+__global__ void classify_kernel(const unsigned long long* __restrict__ keys,
+                                const int32_t* __restrict__ d_M, int64_t bound, int level,
                                 int can_split, double thr2, int S, int baseline,
                                 const double* __restrict__ svals, const double* __restrict__ dmean,
                                 const double* __restrict__ rmean, const int32_t* __restrict__ roff,
                                 const int32_t* __restrict__ codes, int32_t* __restrict__ split,
                                 int32_t* __restrict__ leaf_flag, int32_t* __restrict__ leaf_rec) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M) return;
+  if (i >= bound) return;
+  if (i >= *d_M) {  // keep the flag scan over the launch bound exact
+    split[i] = 0;
+    return;
+  }
   const unsigned long long key = keys[i];
   const int32_t err = (int32_t)(key >> 32);
   const int64_t cidx = (int64_t)(key & 0xffffffffull);
@@ -77,12 +83,14 @@ __global__ void classify_kernel(const unsigned long long* __restrict__ keys, int
   leaf_flag[code] = 1;
 }
 
-__global__ void children_kernel(int64_t M, const int32_t* __restrict__ split,
+__global__ void children_kernel(const int32_t* __restrict__ d_M, const int32_t* __restrict__ split,
                                 const int32_t* __restrict__ pfx, const int32_t* __restrict__ origins,
                                 const int32_t* __restrict__ codes, int half, int weight,
                                 int32_t* __restrict__ next_origins, int32_t* __restrict__ next_codes,
                                 int32_t* __restrict__ d_next_M) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t M = *d_M;
+  if (i == 0 && M == 0) *d_next_M = 0;
   if (i >= M) return;
   const int32_t p = pfx[i];
   if (i == M - 1) *d_next_M = 4 * (p + split[i]);
@@ -138,6 +146,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   const int64_t launches0 = c->total_launches;
   c->stats = fc_stats{};
 
+  trace_mark(c, "encode_begin");
   // ---- operands for every level, sharing one synchronisation ----
   int pending[kLevels] = {0, 0, 0, 0};
   int lpath[kLevels];
@@ -162,12 +171,12 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   }
   FC_CUDA(c, c->enc_flag.reserve(max_ranges * 4 + 64));
   FC_CUDA(c, c->enc_pfx.reserve(max_ranges * 4 + 64));
-  FC_CUDA(c, c->enc_count.reserve(16 * 4));
-  FC_CUDA(c, c->enc_hist.reserve(256 * 4));
+  FC_CUDA(c, c->enc_count.reserve(64 * 4));
+  FC_CUDA(c, c->enc_hist.reserve(256 * 4 * kLevels));
   FC_CUDA(c, c->leaf_flag.reserve(n_codes * 4 + 64));
   FC_CUDA(c, c->leaf_pos.reserve(n_codes * 4 + 64));
   FC_CUDA(c, c->leaf_rec.reserve(n_codes * 24 + 64));
-  FC_CUDA(c, c->readback.reserve(260 * 4));
+  FC_CUDA(c, c->readback.reserve(64 * 4));
   FC_CUDA(c, c->keys.reserve(max_ranges * 8 + 64));
   int32_t* d_count = c->enc_count.as<int32_t>();
   int32_t* d_hist = c->enc_hist.as<int32_t>();
@@ -178,45 +187,49 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   FC_CUDA(c, cudaGetLastError());
   c->total_launches += 1;
 
-  auto gather_and_read = [&](int l, int cur, int slot, int64_t bound) -> int {
-    FC_CUDA(c, cudaMemsetAsync(d_hist, 0, 256 * 4, c->stream));
-    FC_TRY(gather_ranges_dev(c, c->lv[l], c->enc_orig[cur].as<int32_t>(), d_count + slot, bound,
-                             d_hist));
-    FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count + slot, 4, cudaMemcpyDeviceToHost, c->stream));
-    FC_CUDA(c, cudaMemcpyAsync(h_rb + 4, d_hist, 256 * 4, cudaMemcpyDeviceToHost, c->stream));
-    return FC_OK;
+  FC_CUDA(c, c->enc_fix.reserve(kLevels * 8 + 64));
+  int64_t* d_fix = c->enc_fix.as<int64_t>();
+  FC_CUDA(c, cudaMemsetAsync(d_fix, 0, kLevels * 8, c->stream));
+  auto gather = [&](int l, int cur, int64_t bound) -> int {
+    FC_CUDA(c, cudaMemsetAsync(d_hist + 256 * l, 0, 256 * 4, c->stream));
+    return gather_ranges_dev(c, c->lv[l], c->enc_orig[cur].as<int32_t>(), d_count + l, bound,
+                             d_hist + 256 * l);
   };
-  FC_TRY(gather_and_read(0, 0, 0, n_top));
+  FC_TRY(gather(0, 0, n_top));
+  trace_mark(c, "prep_launched");
   FC_TRY(sync_stream(c));
-  for (int l = 0; l < kLevels; ++l)
-    if (pending[l]) FC_TRY(prepare_finish(c, c->lv[l], lpath[l], pending[l]));
+  trace_mark(c, "prep_sync");
 
-  // ---- level loop ----
+  // ---- level loop: no host synchronisation ----
   int cur = 0;
-  std::vector<int32_t> hist(256);
+  int64_t bound = n_top;
+  int levels_run = 0;
   for (int l = 0; l < kLevels; ++l) {
     Level& L = c->lv[l];
-    const int64_t M = h_rb[0];
-    if (M == 0) break;
-    std::copy(h_rb + 4, h_rb + 4 + 256, hist.begin());
     if (L.count == 0) {
-      char buf[64];
-      snprintf(buf, sizeof buf, "no domain entries at level %d", l + 1);
-      return set_error(c, FC_ERR_EMPTY_POOL, buf);
+      // rare: an empty pool errors only if ranges reach it (matcher.py:34)
+      FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count + l, 4, cudaMemcpyDeviceToHost, c->stream));
+      FC_TRY(sync_stream(c));
+      if (h_rb[0] > 0) {
+        char buf[64];
+        snprintf(buf, sizeof buf, "no domain entries at level %d", l + 1);
+        return set_error(c, FC_ERR_EMPTY_POOL, buf);
+      }
+      break;
     }
-    fc_stats& st = c->enc_stats[l];
-    st.ranges = M;
-    st.columns = L.count * L.s_count;
-    st.comparisons = M * L.count * 8 * L.s_count;
-    st.path = L.path;
+    levels_run = l + 1;
+    // finish this level's operands only now: the host work overlaps the
+    // previous level's kernels instead of idling the GPU after the sync
+    if (pending[l]) FC_TRY(prepare_finish(c, L, lpath[l], pending[l]));
+    const int32_t* d_M = d_count + l;
     const int64_t launches_before = c->total_launches + c->stats.kernel_launches;
     uint64_t* keys = c->keys.as<uint64_t>();
-    FC_CUDA(c, cudaMemsetAsync(keys, 0xff, M * 8, c->stream));
+    FC_CUDA(c, cudaMemsetAsync(keys, 0xff, bound * 8, c->stream));
     FC_CUDA(c, cudaEventRecord(c->enc_ev[l][0], c->stream));
     if (L.path == FC_PATH_TENSOR) {
-      FC_TRY(scan_tc_launch(c, L, M, keys, hist.data(), nullptr, c->enc_ev[l][1], &st.fix_pairs));
+      FC_TRY(scan_tc_launch(c, L, bound, d_M, d_hist + 256 * l, keys, c->enc_ev[l][1], d_fix + l));
     } else {
-      FC_TRY(scan_exact(c, L, M, nullptr, 0, nullptr, 0, keys));
+      FC_TRY(scan_exact(c, L, bound, nullptr, 0, nullptr, 0, keys, d_M));
       FC_CUDA(c, cudaEventRecord(c->enc_ev[l][1], c->stream));
     }
     FC_CUDA(c, cudaEventRecord(c->enc_ev[l][2], c->stream));
@@ -230,29 +243,35 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     }
     int32_t* codes = c->enc_code[cur].as<int32_t>();
     int32_t* flag = c->enc_flag.as<int32_t>();
-    classify_kernel<<<blocks_for(M), 256, 0, c->stream>>>(
-        reinterpret_cast<const unsigned long long*>(keys), M, l + 1, can_split, thr2, L.s_count,
-        L.baseline, L.svals_d.as<double>(), L.mean.as<double>(), c->rmean.as<double>(),
+    classify_kernel<<<blocks_for(bound), 256, 0, c->stream>>>(
+        reinterpret_cast<const unsigned long long*>(keys), d_M, bound, l + 1, can_split, thr2,
+        L.s_count, L.baseline, L.svals_d.as<double>(), L.mean.as<double>(), c->rmean.as<double>(),
         c->roff.as<int32_t>(), codes, flag, c->leaf_flag.as<int32_t>(), c->leaf_rec.as<int32_t>());
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 1;
     if (can_split) {
       int32_t* pfx = c->enc_pfx.as<int32_t>();
       size_t need = 0;
-      FC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, need, flag, pfx, (int)M, c->stream));
+      FC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, need, flag, pfx, (int)bound, c->stream));
       FC_CUDA(c, c->cub_tmp.reserve(need));
-      FC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.ptr, need, flag, pfx, (int)M, c->stream));
+      FC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.ptr, need, flag, pfx, (int)bound,
+                                               c->stream));
       const int nxt_buf = cur ^ 1;
-      children_kernel<<<blocks_for(M), 256, 0, c->stream>>>(
-          M, flag, pfx, c->enc_orig[cur].as<int32_t>(), codes, side / 2, 1 << (2 * (2 - l)),
+      children_kernel<<<blocks_for(bound), 256, 0, c->stream>>>(
+          d_M, flag, pfx, c->enc_orig[cur].as<int32_t>(), codes, side / 2, 1 << (2 * (2 - l)),
           c->enc_orig[nxt_buf].as<int32_t>(), c->enc_code[nxt_buf].as<int32_t>(), d_count + l + 1);
       FC_CUDA(c, cudaGetLastError());
       c->total_launches += 2;
       cur = nxt_buf;
-      FC_TRY(gather_and_read(l + 1, cur, l + 1, 4 * M));
+      bound *= 4;
+      FC_TRY(gather(l + 1, cur, bound));
     }
-    st.kernel_launches = (int32_t)(c->total_launches + c->stats.kernel_launches - launches_before);
-    if (can_split) FC_TRY(sync_stream(c));
+    c->enc_stats[l].kernel_launches =
+        (int32_t)(c->total_launches + c->stats.kernel_launches - launches_before);
+    c->enc_stats[l].path = L.path;
+    static const char* kLevelMark[4] = {"level1_launched", "level2_launched", "level3_launched",
+                                        "level4_launched"};
+    trace_mark(c, kLevelMark[l]);
   }
   c->total_launches += c->stats.kernel_launches;
   c->stats.kernel_launches = 0;
@@ -271,10 +290,38 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
         n_codes, flag, pos, c->leaf_rec.as<int32_t>(), c->rec_out.as<int32_t>(), d_count + 8);
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 2;
-    FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count + 8, 4, cudaMemcpyDeviceToHost, c->stream));
+    FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count, 16 * 4, cudaMemcpyDeviceToHost, c->stream));
+    FC_CUDA(c, cudaMemcpyAsync(h_rb + 16, d_fix, kLevels * 8, cudaMemcpyDeviceToHost, c->stream));
+    // the stream header needs every pool's origins: fetch them with this sync
+    {
+      int64_t total = 0;
+      for (int l = 0; l < kLevels; ++l) {
+        c->coords_off[l] = total;
+        total += c->lv[l].count;
+      }
+      FC_CUDA(c, c->coords_pinned.reserve(total * 4 + 16));
+      for (int l = 0; l < kLevels; ++l)
+        if (c->lv[l].count)
+          FC_CUDA(c, cudaMemcpyAsync(c->coords_pinned.as<uint32_t>() + c->coords_off[l],
+                                     c->lv[l].xy.ptr, c->lv[l].count * 4, cudaMemcpyDeviceToHost,
+                                     c->stream));
+      c->coords_valid = true;
+    }
+    trace_mark(c, "records_launched");
     FC_TRY(sync_stream(c));
+    trace_mark(c, "records_sync");
   }
-  const int64_t n = h_rb[0];
+  const int64_t n = h_rb[8];
+  const int64_t* h_fix = reinterpret_cast<const int64_t*>(h_rb + 16);
+  for (int l = 0; l < levels_run; ++l) {
+    Level& L = c->lv[l];
+    fc_stats& st = c->enc_stats[l];
+    const int64_t M = h_rb[l];
+    st.ranges = M;
+    st.columns = L.count * L.s_count;
+    st.comparisons = M * L.count * 8 * L.s_count;
+    st.fix_pairs = h_fix[l];
+  }
   c->enc_records = n;
   if (out_count) *out_count = n;
   for (int l = 0; l < kLevels; ++l) {
@@ -288,6 +335,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     st.scan_ms = a + b;
   }
   (void)launches0;
+  trace_dump(c);
   if (!out_records) return FC_OK;
   if (n > capacity) return set_error(c, FC_ERR_ARG, "record buffer too small");
   if (n > 0) {

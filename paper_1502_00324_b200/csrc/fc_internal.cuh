@@ -84,6 +84,7 @@ struct TcOperands {
   DevBuf reach_low;      // int32 [ncols]: columns sorted by qmin ascending
   DevBuf reach_high;     // int32 [ncols]: columns sorted by qmax descending
   DevBuf odd;            // int32 [2*ncols]: parity flags, then their exclusive prefix
+  DevBuf reach_counts;   // int64 [512]: low_count | high_count on the device
   DevBuf hist;           // u32 [1024 qmin | 1024 qmax | q2max | pad]
   PinnedBuf readback;    // pinned copy of hist + last prefix/flag (prepare begin -> finish)
   int64_t low_count[256] = {0};   // #{columns with qmin < -o}      (clamp at 0 possible)
@@ -122,7 +123,15 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
   cudaEvent_t tc_ev[3] = {nullptr, nullptr, nullptr};
+  // FC_TRACE=1: host / device timestamps of the encode phases (stderr)
+  int trace = 0;
+  std::vector<std::string> trace_name;
+  std::vector<double> trace_host_us;
+  std::vector<cudaEvent_t> trace_ev;
   bool tc_attr_set = false;
+  int tc_wait_mode = 0;
+  int tc_forward = 0;    // FC_TC_FORWARD: tile scan order of the tensor kernel  // FC_TC_WAIT: spin-wait roles of the tensor kernel
+  bool ent_attr_set = false;
   Status st;
   int device_io = 0;
   // image
@@ -137,7 +146,7 @@ struct Ctx {
   DevBuf ent_scratch, key_in, key_out, val_in, val_out, cub_tmp, count_buf;
   DevBuf origins, rtiles, rmean, roff, rsq, keys, out_err, out_idx;
   DevBuf fix_rows, fix_cols, fix_jobs, svals_dev;
-  DevBuf a_tiles, row_meta, fix_prefix, tc_scratch;
+  DevBuf a_tiles, row_meta, fix_prefix, tc_scratch, tc_plan;
   std::vector<int32_t> h_roff;
   // pinned staging: uploads go through an arena that is recycled at every
   // full stream synchronisation (stage_h2d / sync_stream)
@@ -145,8 +154,11 @@ struct Ctx {
   size_t up_off = 0;
   PinnedBuf readback;     // small D2H results (counts, histograms)
   PinnedBuf pool_rb;      // threshold-survivor counts per level
+  PinnedBuf coords_pinned;  // pool origins of all levels, fetched with fc_encode's last sync
+  int64_t coords_off[kLevels] = {0, 0, 0, 0};
+  bool coords_valid = false;
   // device-driven encode (fc_encode.cu)
-  DevBuf enc_orig[2], enc_code[2], enc_flag, enc_pfx, enc_count, enc_hist;
+  DevBuf enc_orig[2], enc_code[2], enc_flag, enc_pfx, enc_count, enc_hist, enc_fix;
   DevBuf leaf_flag, leaf_pos, leaf_rec, rec_out;
   int64_t enc_records = 0;
   fc_stats enc_stats[kLevels]{};
@@ -161,6 +173,11 @@ struct Ctx {
 int set_error(Ctx* c, int code, const std::string& msg);
 int cuda_check(Ctx* c, cudaError_t e, const char* what);
 int lut_slot(int n);
+
+// phase tracing (fc_api.cu); no-ops unless FC_TRACE is set
+void trace_reset(Ctx* c);
+void trace_mark(Ctx* c, const char* name);
+void trace_dump(Ctx* c);
 
 // pinned staging helpers (fc_api.cu)
 int stage_h2d(Ctx* c, void* dst, const void* src, size_t bytes);
@@ -186,11 +203,14 @@ int gather_ranges_dev(Ctx* c, Level& L, const int32_t* d_origins, const int32_t*
                       int64_t M_bound, int32_t* d_hist);
 int roff_hist(Ctx* c, int64_t M, int32_t* d_hist);
 int load_ranges(Ctx* c, Level& L, const uint8_t* h_tiles, int64_t M);
+// d_M (optional): device range count <= M (M is then the launch bound)
 int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t n_range_list,
-               const int32_t* d_col_list, int64_t n_col_list, uint64_t* d_keys);
-int scan_exact_jobs(Ctx* c, Level& L, const int4* d_jobs, const int64_t* d_prefix, int n_jobs,
-                    int64_t total_blocks, const int32_t* d_sorted_ranges, const int32_t* d_low,
-                    const int32_t* d_high, uint64_t* d_keys);
+               const int32_t* d_col_list, int64_t n_col_list, uint64_t* d_keys,
+               const int32_t* d_M = nullptr);
+int scan_exact_jobs(Ctx* c, Level& L, const int4* d_jobs, const int64_t* d_prefix,
+                    const int* d_n_jobs, const long long* d_total_blocks,
+                    const int32_t* d_sorted_ranges, const int32_t* d_low, const int32_t* d_high,
+                    uint64_t* d_keys);
 int decode_keys(Ctx* c, const uint64_t* d_keys, int64_t M, int64_t* d_err, int64_t* d_idx);
 int iso_table_offset(int side);
 int scan_rows_dropin(Ctx* c, const int16_t* ranges, const double* rmeans, int64_t M, int32_t n,
@@ -200,10 +220,11 @@ int scan_rows_dropin(Ctx* c, const int16_t* ranges, const double* rmeans, int64_
 // fc_scan_tc.cu
 int level_prepare_tc_begin(Ctx* c, Level& L);   // device stats + async readback
 int level_prepare_tc_finish(Ctx* c, Level& L);  // after a stream sync: layout + operand build
-// Launch the contraction and its clamp corrections for M gathered ranges;
-// h_hist[o] = #ranges with offset o (host copy).  No synchronisation.
-int scan_tc_launch(Ctx* c, Level& L, int64_t M, uint64_t* d_keys, const int32_t* h_hist,
-                   cudaEvent_t ev_main_begin, cudaEvent_t ev_main_end, int64_t* out_fix_pairs);
+// Launch the contraction and its clamp corrections for *d_M (<= M_bound)
+// gathered ranges; d_hist[o] = #ranges with offset o.  No synchronisation:
+// the unit decomposition and the correction jobs are planned on the device.
+int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const int32_t* d_hist,
+                   uint64_t* d_keys, cudaEvent_t ev_main_end, int64_t* d_fix_pairs);
 int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys);
 
 // fc_encode.cu

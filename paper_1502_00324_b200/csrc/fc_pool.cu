@@ -1,17 +1,21 @@
 // Domain-pool construction on the device (pool.py:88-178, image.py:116-130).
 //
-//  1. entropy_kernel   : one warp per 2Bx2B lattice window (raster order,
-//                        pool.py:120-135); 256-bin shared-memory histogram,
-//                        then H = -sum_b t[count_b] with t[k] = p*log(p) from the
-//                        host-numpy LUT, summed in numpy's exact pairwise order
-//                        (two 128-bin halves, 8 running accumulators each,
-//                        ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), half0+half1) so the
-//                        float64 bits equal pool.py:88-92 on the same host.
-//  2. CUB stable radix sort on key ~bits(|H|): entropy descending, raster order
-//     among exact ties (np.argsort(-ent, kind="stable"), pool.py:171).
+//  1. entropy_all_kernel (one launch for all four levels): a warp owns 32
+//     adjacent window columns x 16 window rows; every lane keeps its window's
+//     256-bin histogram in shared memory (hist[bin][lane], conflict-free) and
+//     slides it down the lattice (remove the rows that leave, add the rows
+//     that enter).  H = -sum_b t[count_b] with t[k] = p*log(p) from the
+//     host-numpy LUT, summed in numpy's exact pairwise order (two 128-bin
+//     halves, 8 running accumulators each, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+//     half0+half1) so the float64 bits equal pool.py:88-92 on the same host.
+//     Threshold levels append {ent > tau} survivors with warp-aggregated
+//     atomics (order-free; the ranking below restores the reference order).
+//  2. ranking, key = ~bits(|H|) (ascending == entropy descending), ties by
+//     raster index (np.argsort(-ent, kind="stable"), pool.py:171):
+//     threshold survivors: chunk bitonic sort + cross-chunk rank (2 launches
+//     for all levels); general caps: CUB stable radix sort; cap 1: argmin.
 //  3. survivor_kernel  : one warp per kept window: floor 2x2 decimation,
-//                        exact sum / sum of squares, mean, centered norm
-//                        (pool.py:138-152).
+//     exact sum / sum of squares, mean, centered norm (pool.py:138-152).
 #include <cub/cub.cuh>
 
 #include "fc_internal.cuh"
@@ -20,7 +24,9 @@ namespace fcb {
 
 namespace {
 
-constexpr int kEntWarps = 8;
+constexpr int kEntWarps = 6;       // warps per block of the entropy kernel (2 blocks / SM)
+constexpr int kStripRows = 16;     // window rows one lane slides through
+constexpr int kLutWords = 4 + 16 + 64 + 256 + 1024;  // the four [0, p*log(p)...] LUTs in smem
 
 __device__ __forceinline__ uint64_t entropy_key(double h) {
   // |h|: maps the -0.0 of a constant window onto +0.0 (they compare equal in numpy).
@@ -28,53 +34,286 @@ __device__ __forceinline__ uint64_t entropy_key(double h) {
   return ~bits;  // ascending key == descending entropy
 }
 
+// Per-level description for the fused entropy kernel.
+struct EntLevel {
+  int D, stride, nx, ny, strips_x, task_begin, lut_off;
+  int mode;  // 0: write key/val of every window (sort / argmin), 1: append {ent > tau}
+  double tau;
+  double* ent;
+  uint64_t* key;
+  uint32_t* val;
+  int* sel_count;
+};
+struct EntParams {
+  EntLevel lv[4];
+  const double* lut[4];  // device LUTs for n = 16, 64, 256, 1024
+  int total_tasks;
+};
+
+// Shared-memory accesses with explicit 32-bit shared addresses (generic
+// pointers into shared memory cost an address-window conversion per access).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+// Pin a value in a register (keeps the compiler from re-deriving a shared
+// address from SR_CgaCtaId inside hot loops).
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
+  uint32_t y;
+  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32_ordered(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void reds_add(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u32_ordered(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Lane-private histogram: word (v >> 1) * 32 + lane packs the u16 counts of
+// bins v & ~1 (low half) and v | 1 (high half), so every access of a warp
+// hits bank = lane (conflict-free).  Updates are shared-memory reductions
+// without return (pipelined); a removal never borrows across halves because
+// only counted pixels are removed.  hw = shared address of this lane's word 0.
 template <int D>
-__global__ void __launch_bounds__(kEntWarps * 32)
-entropy_kernel(const uint8_t* __restrict__ img, int width, int nx, int64_t nwin, int stride,
-               const double* __restrict__ lut, double tau, int use_tau,
-               double* __restrict__ ent_out, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
-               unsigned long long* __restrict__ above) {
-  __shared__ int hist[kEntWarps][256];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  int* h = hist[warp];
-  int local_above = 0;
-  for (int64_t w = (int64_t)blockIdx.x * kEntWarps + warp; w < nwin;
-       w += (int64_t)gridDim.x * kEntWarps) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) h[lane + 32 * i] = 0;
-    __syncwarp();
-    const int64_t wy = w / nx, wx = w - wy * nx;
-    const uint8_t* base = img + (wy * stride) * (int64_t)width + wx * stride;
-#pragma unroll 4
-    for (int p = lane; p < D * D; p += 32) {
-      const int r = p / D, col = p - r * D;
-      atomicAdd(&h[base[(int64_t)r * width + col]], 1);
+__device__ __forceinline__ void hist_rows(uint32_t hw, const uint8_t* __restrict__ img, int width,
+                                          int x, int r0, int r1, uint32_t lo, uint32_t hi) {
+  for (int r = r0; r < r1; ++r) {
+    const uint8_t* row = img + (int64_t)r * width + x;
+#pragma unroll 8
+    for (int k = 0; k < D; ++k) {
+      const uint32_t v = __ldg(row + k);
+      reds_add(hw + (v >> 1) * 128, (v & 1) ? hi : lo);
     }
-    __syncwarp();
-    // numpy pairwise sum of the 256 terms (lanes 16..31 mirror lanes 0..15)
-    const int half = (lane >> 3) & 1, j = lane & 7;
-    double acc = 0.0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int cnt = h[half * 128 + i * 8 + j];
-      const double t = cnt ? lut[cnt - 1] : 0.0;
-      acc = (i == 0) ? t : acc + t;
-    }
-    acc = acc + __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc = acc + __shfl_xor_sync(0xffffffffu, acc, 2);
-    acc = acc + __shfl_xor_sync(0xffffffffu, acc, 4);
-    acc = acc + __shfl_xor_sync(0xffffffffu, acc, 8);
-    const double hval = -acc;
-    if (lane == 0) {
-      ent_out[w] = hval;
-      keys[w] = entropy_key(hval);
-      vals[w] = static_cast<uint32_t>(w);
-      if (use_tau && hval > tau) ++local_above;
-    }
-    __syncwarp();
   }
-  if (use_tau && lane == 0 && local_above) atomicAdd(above, (unsigned long long)local_above);
+}
+
+// numpy pairwise sum of the 256 terms t[count] (pool.py:88-92): two 128-bin
+// halves, 8 running accumulators each, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)).
+// Zero bins add +0.0 (exact): lut[0] holds 0.0 and lut[k] = t(k), so every
+// bin is one unconditional load + add (no predication).
+__device__ __forceinline__ double window_entropy(uint32_t hw, uint32_t lut) {
+  double half_sum[2];
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+#pragma unroll
+    for (int p = 0; p < 64; ++p) {
+      const uint32_t w = lds_u32_ordered(hw + (half * 64 + p) * 128);
+      // counts <= 1024 < 2^13, so (w >> 13) == 8 * (w >> 16)
+      const uint32_t a0 = lut + ((w & 0xffffu) << 3), a1 = lut + (w >> 13);
+      const int j0 = (2 * p) & 7;
+      acc[j0] = acc[j0] + lds_f64(a0);
+      acc[j0 + 1] = acc[j0 + 1] + lds_f64(a1);
+    }
+    half_sum[half] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  }
+  return -(half_sum[0] + half_sum[1]);
+}
+
+// One warp per task = 32 adjacent window columns x kStripRows window rows of
+// one level.  Each lane keeps its window's 256-bin histogram and slides it
+// down by `stride` rows (remove the rows that leave, add the rows that
+// enter), so a window costs 2*stride*D updates instead of D*D.
+template <int D>
+__device__ __forceinline__ void entropy_task(const EntLevel& L, const uint8_t* __restrict__ img,
+                                             int width, int task, uint32_t h, uint32_t lut,
+                                             int lane) {
+  const int t = task - L.task_begin;
+  const int sy = t / L.strips_x, sx = t - sy * L.strips_x;
+  const int wx = sx * 32 + lane;
+  const bool active = wx < L.nx;
+  const int wy0 = sy * kStripRows;
+  const int wy1 = min(wy0 + kStripRows, L.ny);
+  const int s = L.stride;
+  const int x = wx * s;
+#pragma unroll 8
+  for (int b = 0; b < 128; ++b) sts_u32_ordered(h + b * 128, 0u);
+  if (active) hist_rows<D>(h, img, width, x, wy0 * s, wy0 * s + D, 1u, 0x10000u);
+  for (int wy = wy0; wy < wy1; ++wy) {
+    if (wy > wy0 && active) {
+      const int yp = (wy - 1) * s, yn = wy * s;
+      hist_rows<D>(h, img, width, x, yp, yp + min(s, D), 0xffffffffu, 0xffff0000u);
+      hist_rows<D>(h, img, width, x, max(yp + D, yn), yn + D, 1u, 0x10000u);
+    }
+    double H = 0.0;
+    if (active) H = window_entropy(h, lut);
+    const int64_t w = (int64_t)wy * L.nx + wx;
+    if (L.mode == 0) {
+      if (active) {
+        L.ent[w] = H;
+        L.key[w] = entropy_key(H);
+        L.val[w] = (uint32_t)w;
+      }
+    } else {
+      if (active) L.ent[w] = H;
+      const bool keep = active && H > L.tau;
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (bal) {
+        int base = 0;
+        if (lane == __ffs(bal) - 1) base = atomicAdd(L.sel_count, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+        if (keep) {
+          const int slot = base + __popc(bal & ((1u << lane) - 1));
+          L.key[slot] = entropy_key(H);
+          L.val[slot] = (uint32_t)w;
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kEntWarps * 32)
+entropy_all_kernel(const uint8_t* __restrict__ img, int width, EntParams P) {
+  extern __shared__ __align__(16) uint8_t ent_smem[];
+  double* lut_s = reinterpret_cast<double*>(ent_smem);
+  uint32_t* hist_all = reinterpret_cast<uint32_t*>(ent_smem + kLutWords * 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int l = 0; l < 4; ++l) {
+    const int n = P.lv[l].D * P.lv[l].D;
+    for (int i = threadIdx.x; i <= n; i += blockDim.x)
+      lut_s[P.lv[l].lut_off + i] = i ? P.lut[l][i - 1] : 0.0;
+  }
+  __syncthreads();
+  const uint32_t h = opaque_u32(smem_addr(hist_all + warp * (128 * 32) + lane));
+  const uint32_t lut_base = opaque_u32(smem_addr(lut_s));
+  for (int task = blockIdx.x * kEntWarps + warp; task < P.total_tasks;
+       task += gridDim.x * kEntWarps) {
+    int l = 0;
+#pragma unroll
+    for (int k = 1; k < 4; ++k)
+      if (task >= P.lv[k].task_begin) l = k;
+    const EntLevel& L = P.lv[l];
+    const uint32_t lut = lut_base + L.lut_off * 8;
+    switch (L.D) {
+      case 32: entropy_task<32>(L, img, width, task, h, lut, lane); break;
+      case 16: entropy_task<16>(L, img, width, task, h, lut, lane); break;
+      case 8: entropy_task<8>(L, img, width, task, h, lut, lane); break;
+      default: entropy_task<4>(L, img, width, task, h, lut, lane); break;
+    }
+  }
+}
+
+constexpr int kEntSmem = kLutWords * 8 + kEntWarps * 128 * 32 * 4;
+
+// ---- rank sort of the threshold survivors: (key asc, window asc) ----
+constexpr int kChunk = 2048;
+constexpr int kMaxChunks = 64;
+
+struct SortLevel {
+  uint64_t* key;      // survivors (unordered), sorted in place per chunk
+  uint32_t* val;
+  uint32_t* out;      // window ids in rank order
+  int count;
+  int chunk_begin;    // first chunk (block) index of this level
+};
+struct SortParams {
+  SortLevel lv[4];
+  int n_levels;
+  int total_chunks;
+};
+
+__device__ __forceinline__ bool lex_less(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+__device__ __forceinline__ int sort_level_of(const SortParams& P, int chunk) {
+  int l = 0;
+  for (int k = 1; k < P.n_levels; ++k)
+    if (chunk >= P.lv[k].chunk_begin) l = k;
+  return l;
+}
+
+// Bitonic sort of one chunk in shared memory.
+__global__ void __launch_bounds__(1024) chunk_sort_kernel(SortParams P) {
+  __shared__ uint64_t sk[kChunk];
+  __shared__ uint32_t si[kChunk];
+  const int l = sort_level_of(P, blockIdx.x);
+  const SortLevel& L = P.lv[l];
+  const int c = blockIdx.x - L.chunk_begin;
+  const int base = c * kChunk;
+  const int n = min(kChunk, L.count - base);
+  for (int i = threadIdx.x; i < kChunk; i += blockDim.x) {
+    sk[i] = i < n ? L.key[base + i] : ~0ull;
+    si[i] = i < n ? L.val[base + i] : 0xffffffffu;
+  }
+  __syncthreads();
+  for (int size = 2; size <= kChunk; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < kChunk / 2; t += blockDim.x) {
+        const int i = 2 * t - (t & (stride - 1));
+        const int j = i + stride;
+        const bool up = (i & size) == 0;
+        const uint64_t ka = sk[i], kb = sk[j];
+        const uint32_t ia = si[i], ib = si[j];
+        if (lex_less(kb, ib, ka, ia) == up) {
+          sk[i] = kb; sk[j] = ka;
+          si[i] = ib; si[j] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    L.key[base + i] = sk[i];
+    L.val[base + i] = si[i];
+  }
+}
+
+// Global rank of every element = its chunk position + the number of smaller
+// elements in each other chunk (binary search over chunks staged in smem).
+__global__ void __launch_bounds__(1024) chunk_rank_kernel(SortParams P) {
+  __shared__ uint64_t sk[kChunk];
+  __shared__ uint32_t si[kChunk];
+  const int l = sort_level_of(P, blockIdx.x);
+  const SortLevel& L = P.lv[l];
+  const int c = blockIdx.x - L.chunk_begin;
+  const int nch = (L.count + kChunk - 1) / kChunk;
+  const int base = c * kChunk;
+  const int n = min(kChunk, L.count - base);
+  uint64_t mk[2];
+  uint32_t mi[2];
+  int rank[2];
+  for (int e = 0; e < 2; ++e) {
+    const int p = threadIdx.x + e * 1024;
+    mk[e] = p < n ? L.key[base + p] : ~0ull;
+    mi[e] = p < n ? L.val[base + p] : 0xffffffffu;
+    rank[e] = p;
+  }
+  for (int b = 0; b < nch; ++b) {
+    if (b == c) continue;
+    const int bb = b * kChunk;
+    const int nb = min(kChunk, L.count - bb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+      sk[i] = L.key[bb + i];
+      si[i] = L.val[bb + i];
+    }
+    __syncthreads();
+    for (int e = 0; e < 2; ++e) {
+      int lo = 0, hi = nb;  // first index with element >= mine
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (lex_less(sk[mid], si[mid], mk[e], mi[e])) lo = mid + 1; else hi = mid;
+      }
+      rank[e] += lo;
+    }
+  }
+  for (int e = 0; e < 2; ++e) {
+    const int p = threadIdx.x + e * 1024;
+    if (p < n) L.out[rank[e]] = mi[e];
+  }
 }
 
 // One warp per survivor: decimate, moments, coordinates.
@@ -151,17 +390,10 @@ __global__ void moments_kernel(const uint8_t* __restrict__ tiles, int n, int64_t
   }
 }
 
-// Threshold compaction predicate: window index -> entropy > tau (keeps raster order).
-struct AboveTau {
-  const double* ent;
-  double tau;
-  __device__ __forceinline__ bool operator()(const uint32_t& w) const { return ent[w] > tau; }
-};
-
-__global__ void gather_keys_kernel(const uint32_t* __restrict__ idx, const double* __restrict__ ent,
-                                   int64_t n, uint64_t* __restrict__ keys) {
+__global__ void gather_all_keys_kernel(const double* __restrict__ ent, int64_t n,
+                                       uint64_t* __restrict__ keys) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) keys[i] = entropy_key(ent[idx[i]]);
+  if (i < n) keys[i] = entropy_key(ent[i]);
 }
 
 // Lexicographic (key, index) minimum: the first window of the highest
@@ -260,8 +492,11 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
   FC_CUDA(c, c->pool_rb.reserve(64));
   int* d_nsel = reinterpret_cast<int*>(c->count_buf.ptr);
   int* h_nsel = c->pool_rb.as<int>();
-  int nx_l[kLevels], any_tau = 0;
-  // ---- phase 1: entropies and ranking for every level ----
+  int nx_l[kLevels], ny_l[kLevels], any_tau = 0;
+  // ---- phase 1: every window's entropy, all levels in one launch ----
+  EntParams P{};
+  int tasks = 0;
+  int lut_off = 0;
   for (int li = 0; li < kLevels; ++li) {
     Level& L = c->lv[li];
     const int D = kDomainSide[li];
@@ -274,43 +509,53 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     const int nx = (c->width - D) / L.stride + 1;
     const int ny = (c->height - D) / L.stride + 1;
     nx_l[li] = nx;
+    ny_l[li] = ny;
     const int64_t nwin = (int64_t)nx * ny;
+    if (nwin >= (1ll << 31)) return set_error(c, FC_ERR_ARG, "too many lattice windows");
     FC_CUDA(c, L.win_ent.reserve(nwin * 8));
-    FC_CUDA(c, L.win_key.reserve(nwin * 8));
+    FC_CUDA(c, L.win_key.reserve(nwin * 8 + 8 * 1032));
     FC_CUDA(c, L.win_key2.reserve(nwin * 8 + 8 * 1032));
-    FC_CUDA(c, L.win_val.reserve(nwin * 4));
+    FC_CUDA(c, L.win_val.reserve(nwin * 4 + 4 * 1032));
     FC_CUDA(c, L.win_val2.reserve(nwin * 4 + 4 * 1032));
-    const double* lut = c->lut[lut_slot(D * D)].as<double>();
-    const int64_t blocks64 = (nwin + kEntWarps - 1) / kEntWarps;
-    const int blocks = (int)std::min<int64_t>(blocks64, (int64_t)c->sm_count * 64);
-#define FC_LAUNCH_ENT(DD)                                                                       \
-    entropy_kernel<DD><<<blocks, kEntWarps * 32, 0, c->stream>>>(                               \
-        c->img_ptr, c->width, nx, nwin, L.stride, lut, 0.0, 0, L.win_ent.as<double>(),          \
-        L.win_key.as<uint64_t>(), L.win_val.as<uint32_t>(), nullptr)
-    switch (D) {
-      case 32: FC_LAUNCH_ENT(32); break;
-      case 16: FC_LAUNCH_ENT(16); break;
-      case 8: FC_LAUNCH_ENT(8); break;
-      default: FC_LAUNCH_ENT(4); break;
-    }
-#undef FC_LAUNCH_ENT
+    EntLevel& E = P.lv[li];
+    E.D = D;
+    E.stride = L.stride;
+    E.nx = nx;
+    E.ny = ny;
+    E.strips_x = (nx + 31) / 32;
+    E.task_begin = tasks;
+    E.lut_off = lut_off;
+    E.mode = use_tau[li] ? 1 : 0;
+    E.tau = use_tau[li] ? taus[li] : 0.0;
+    E.ent = L.win_ent.as<double>();
+    E.key = L.win_key.as<uint64_t>();
+    E.val = L.win_val.as<uint32_t>();
+    E.sel_count = d_nsel + li;
+    P.lut[li] = c->lut[lut_slot(D * D)].as<double>();
+    tasks += E.strips_x * ((ny + kStripRows - 1) / kStripRows);
+    lut_off += D * D + 1;
+    any_tau |= use_tau[li];
+  }
+  P.total_tasks = tasks;
+  trace_mark(c, "pool_begin");
+  FC_CUDA(c, cudaMemsetAsync(d_nsel, 0, 4 * kLevels, c->stream));
+  if (!c->ent_attr_set) {
+    FC_CUDA(c, cudaFuncSetAttribute(entropy_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kEntSmem));
+    c->ent_attr_set = true;
+  }
+  {
+    const int blocks = std::max(1, std::min((tasks + kEntWarps - 1) / kEntWarps, c->sm_count * 2));
+    entropy_all_kernel<<<blocks, kEntWarps * 32, kEntSmem, c->stream>>>(c->img_ptr, c->width, P);
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 1;
+  }
+  for (int li = 0; li < kLevels; ++li) {
+    Level& L = c->lv[li];
+    const int64_t nwin = (int64_t)nx_l[li] * ny_l[li];
     size_t tmp = 0;
-    if (use_tau[li]) {
-      // threshold compaction {ent > tau} in raster order
-      any_tau = 1;
-      AboveTau pred{L.win_ent.as<double>(), taus[li]};
-      FC_CUDA(c, cub::DeviceSelect::If(nullptr, tmp, L.win_val.as<uint32_t>(),
-                                        L.win_val2.as<uint32_t>(), d_nsel + li, (int)nwin, pred,
-                                        c->stream));
-      FC_CUDA(c, c->cub_tmp.reserve(tmp));
-      FC_CUDA(c, cub::DeviceSelect::If(c->cub_tmp.ptr, tmp, L.win_val.as<uint32_t>(),
-                                        L.win_val2.as<uint32_t>(), d_nsel + li, (int)nwin, pred,
-                                        c->stream));
-      FC_CUDA(c, cudaMemcpyAsync(h_nsel + li, d_nsel + li, 4, cudaMemcpyDeviceToHost, c->stream));
-      c->total_launches += 1;
-    } else if (caps[li] == 1) {
+    if (use_tau[li]) continue;
+    if (caps[li] == 1) {
       FC_TRY(argmin_windows(c, L.win_key.as<uint64_t>(), nwin, L.win_key2.as<uint64_t>(),
                             L.win_val2.as<uint32_t>()));
       L.count = 1;
@@ -327,41 +572,76 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
       L.count = std::min<int64_t>(caps[li], nwin);
     }
   }
-  if (any_tau) FC_TRY(sync_stream(c));
-  // ---- phase 2: survivors (sorted threshold sets), decimation and moments ----
+  if (any_tau) {
+    FC_CUDA(c, cudaMemcpyAsync(h_nsel, d_nsel, 4 * kLevels, cudaMemcpyDeviceToHost, c->stream));
+    trace_mark(c, "pool_entropy_done");
+    FC_TRY(sync_stream(c));
+    trace_mark(c, "pool_sync");
+  }
+  // ---- phase 2: rank the threshold survivors (entropy desc, raster asc) ----
+  {
+    SortParams SP{};
+    int chunks = 0;
+    for (int li = 0; li < kLevels; ++li) {
+      if (!use_tau[li]) continue;
+      Level& L = c->lv[li];
+      const int64_t nwin = (int64_t)nx_l[li] * ny_l[li];
+      const int nsel = h_nsel[li];
+      if (nsel == 0) {
+        // caps are >= 1 (pool.py:47-48): keep the single highest-entropy window;
+        // the entropy kernel wrote no keys for this level, so rebuild them
+        gather_all_keys_kernel<<<(unsigned)((nwin + 255) / 256), 256, 0, c->stream>>>(
+            L.win_ent.as<double>(), nwin, L.win_key.as<uint64_t>());
+        c->total_launches += 1;
+        FC_TRY(argmin_windows(c, L.win_key.as<uint64_t>(), nwin, L.win_key2.as<uint64_t>(),
+                              L.win_val2.as<uint32_t>()));
+        L.count = 1;
+        continue;
+      }
+      L.count = nsel;
+      const int nch = (nsel + kChunk - 1) / kChunk;
+      if (nch <= kMaxChunks) {
+        SortLevel& S = SP.lv[SP.n_levels++];
+        S.key = L.win_key.as<uint64_t>();
+        S.val = L.win_val.as<uint32_t>();
+        S.out = L.win_val2.as<uint32_t>();
+        S.count = nsel;
+        S.chunk_begin = chunks;
+        chunks += nch;
+      } else {
+        // large sets: two stable radix sorts (window id, then key) == lexicographic order
+        size_t tmp = 0;
+        uint32_t* ids = L.win_val.as<uint32_t>();
+        uint32_t* ids2 = L.win_val2.as<uint32_t>();
+        uint64_t* k1 = L.win_key.as<uint64_t>();
+        uint64_t* k2 = L.win_key2.as<uint64_t>();
+        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, ids, ids2, k1, k2, nsel, 0, 32,
+                                                   c->stream));
+        FC_CUDA(c, c->cub_tmp.reserve(tmp));
+        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, ids, ids2, k1, k2, nsel, 0,
+                                                   32, c->stream));
+        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, k2, k1, ids2, ids, nsel, 0, 64,
+                                                   c->stream));
+        FC_CUDA(c, c->cub_tmp.reserve(tmp));
+        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, k2, k1, ids2, ids, nsel, 0,
+                                                   64, c->stream));
+        FC_CUDA(c, cudaMemcpyAsync(ids2, ids, (size_t)nsel * 4, cudaMemcpyDeviceToDevice,
+                                   c->stream));
+      }
+    }
+    SP.total_chunks = chunks;
+    if (chunks > 0) {
+      chunk_sort_kernel<<<chunks, 1024, 0, c->stream>>>(SP);
+      chunk_rank_kernel<<<chunks, 1024, 0, c->stream>>>(SP);
+      FC_CUDA(c, cudaGetLastError());
+      c->total_launches += 2;
+    }
+  }
   for (int li = 0; li < kLevels; ++li) {
     Level& L = c->lv[li];
     const int D = kDomainSide[li];
     const int nx = nx_l[li];
-    const int64_t nwin = (int64_t)nx * ((c->height - D) / L.stride + 1);
     const uint32_t* order = L.win_val2.as<uint32_t>();
-    if (use_tau[li]) {
-      const int nsel = h_nsel[li];
-      if (nsel == 0) {
-        // caps are >= 1 (pool.py:47-48): keep the single highest-entropy window
-        FC_TRY(argmin_windows(c, L.win_key.as<uint64_t>(), nwin, L.win_key2.as<uint64_t>(),
-                              L.win_val2.as<uint32_t>()));
-        L.count = 1;
-      } else {
-        const int64_t E = nsel;
-        const unsigned tpb = 256;
-        gather_keys_kernel<<<(unsigned)((E + tpb - 1) / tpb), tpb, 0, c->stream>>>(
-            L.win_val2.as<uint32_t>(), L.win_ent.as<double>(), E, L.win_key2.as<uint64_t>());
-        size_t tmp = 0;
-        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, L.win_key2.as<uint64_t>(),
-                                                   L.win_key.as<uint64_t>(), L.win_val2.as<uint32_t>(),
-                                                   L.win_val.as<uint32_t>(), (int)E, 0, 64,
-                                                   c->stream));
-        FC_CUDA(c, c->cub_tmp.reserve(tmp));
-        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, L.win_key2.as<uint64_t>(),
-                                                   L.win_key.as<uint64_t>(), L.win_val2.as<uint32_t>(),
-                                                   L.win_val.as<uint32_t>(), (int)E, 0, 64,
-                                                   c->stream));
-        order = L.win_val.as<uint32_t>();
-        L.count = E;
-        c->total_launches += 1;
-      }
-    }
     FC_CUDA(c, cudaGetLastError());
     const int64_t E = L.count;
     FC_TRY(alloc_level(c, L, E));
@@ -375,6 +655,7 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     c->total_launches += 1;
     out_sizes[li] = E;
   }
+  trace_mark(c, "pool_launched");
   return FC_OK;
 }
 

@@ -156,14 +156,16 @@ __global__ void __launch_bounds__(kColsPerBlock)
 scan_exact_kernel(const int16_t* __restrict__ qbase, int64_t ncols, int S,
                   const double* __restrict__ svals, const double* __restrict__ dmean,
                   const uint8_t* __restrict__ rtiles, const double* __restrict__ rmean,
-                  int64_t M, const uint16_t* __restrict__ inv,
+                  int64_t M, const int32_t* __restrict__ d_M, const uint16_t* __restrict__ inv,
                   const int32_t* __restrict__ range_list, int64_t n_range_list, int64_t range_base,
                   const int32_t* __restrict__ col_list, int64_t n_col_list, int baseline,
                   unsigned long long* __restrict__ keys) {
   __shared__ __align__(16) ExactSmem<N> s;
   const int tid = threadIdx.x;
+  if (d_M) M = *d_M;
   const int64_t nrange = range_list ? n_range_list : M;
   const int64_t r0 = range_base + (int64_t)blockIdx.y * kRB;
+  if (r0 >= nrange) return;  // block-uniform (device range count below the launch bound)
   if (tid < kRB) {
     const int64_t idx = r0 + tid;
     int m = -1;
@@ -187,38 +189,44 @@ __global__ void __launch_bounds__(kColsPerBlock)
 scan_jobs_kernel(const int16_t* __restrict__ qbase, int S, const double* __restrict__ svals,
                  const double* __restrict__ dmean, const uint8_t* __restrict__ rtiles,
                  const double* __restrict__ rmean, const uint16_t* __restrict__ inv,
-                 const int4* __restrict__ jobs, const int64_t* __restrict__ prefix, int n_jobs,
+                 const int4* __restrict__ jobs, const int64_t* __restrict__ prefix,
+                 const int* __restrict__ d_n_jobs, const long long* __restrict__ d_total,
                  const int32_t* __restrict__ sorted_ranges, const int32_t* __restrict__ list_low,
                  const int32_t* __restrict__ list_high, int baseline,
                  unsigned long long* __restrict__ keys) {
   __shared__ __align__(16) ExactSmem<N> s;
   __shared__ int s_job;
   const int tid = threadIdx.x;
-  const int64_t b = blockIdx.x;
-  if (tid == 0) {
-    int lo = 0, hi = n_jobs - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (prefix[mid] <= b) lo = mid; else hi = mid - 1;
+  const int n_jobs = *d_n_jobs;
+  const long long total = *d_total;
+  // persistent: the block count is only known on the device
+  for (long long b = blockIdx.x; b < total; b += gridDim.x) {
+    __syncthreads();  // the previous block's shared state is consumed
+    if (tid == 0) {
+      int lo = 0, hi = n_jobs - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (prefix[mid] <= b) lo = mid; else hi = mid - 1;
+      }
+      s_job = lo;
     }
-    s_job = lo;
+    __syncthreads();
+    const int4 job = jobs[s_job];  // {list, r_off, r_cnt, col_cnt}
+    const int64_t local = b - prefix[s_job];
+    const int64_t ncc = (job.w + kColsPerBlock - 1) / kColsPerBlock;
+    const int64_t rb = local / ncc, cc = local - rb * ncc;
+    if (tid < kRB) {
+      const int64_t idx = rb * kRB + tid;
+      const int m = idx < job.z ? sorted_ranges[job.y + idx] : -1;
+      s.m[tid] = m;
+      s.rmean[tid] = m >= 0 ? rmean[m] : 0.0;
+    }
+    const int64_t ci = cc * kColsPerBlock + tid;
+    const int32_t* list = job.x ? list_high : list_low;
+    const int64_t col = ci < job.w ? (int64_t)list[ci] : -1;
+    __syncthreads();
+    exact_block<N>(s, qbase, S, svals, dmean, rtiles, inv, col, baseline, keys);
   }
-  __syncthreads();
-  const int4 job = jobs[s_job];  // {list, r_off, r_cnt, col_cnt}
-  const int64_t local = b - prefix[s_job];
-  const int64_t ncc = (job.w + kColsPerBlock - 1) / kColsPerBlock;
-  const int64_t rb = local / ncc, cc = local - rb * ncc;
-  if (tid < kRB) {
-    const int64_t idx = rb * kRB + tid;
-    const int m = idx < job.z ? sorted_ranges[job.y + idx] : -1;
-    s.m[tid] = m;
-    s.rmean[tid] = m >= 0 ? rmean[m] : 0.0;
-  }
-  const int64_t ci = cc * kColsPerBlock + tid;
-  const int32_t* list = job.x ? list_high : list_low;
-  const int64_t col = ci < job.w ? (int64_t)list[ci] : -1;
-  __syncthreads();
-  exact_block<N>(s, qbase, S, svals, dmean, rtiles, inv, col, baseline, keys);
 }
 
 // Drop-in for _scan.py:14 with arbitrary candidate rows (reference layout).
@@ -344,65 +352,80 @@ __global__ void range_moments_kernel(const uint8_t* __restrict__ rtiles, int64_t
 // column statistics {Q1 = sum q, Q2 = sum q^2, qmin, qmax}, the parity flag
 // and the qmin / qmax histograms (fc_scan_tc.cu).
 template <int N>
-__global__ void qprep_kernel(const uint8_t* __restrict__ tiles, const double* __restrict__ mean,
-                             int64_t ncols, int S, const double* __restrict__ svals, int baseline,
-                             int16_t* __restrict__ q, int stats, int4* __restrict__ col_stats,
-                             int32_t* __restrict__ odd, unsigned* __restrict__ hist) {
+__global__ void __launch_bounds__(256)
+qprep_kernel(const uint8_t* __restrict__ tiles, const double* __restrict__ mean, int64_t ncols,
+             int S, const double* __restrict__ svals, int baseline, int16_t* __restrict__ q,
+             int stats, int4* __restrict__ col_stats, int32_t* __restrict__ odd,
+             unsigned* __restrict__ hist) {
   constexpr int LPC = N >= 8 ? N / 8 : 1;
   constexpr int PPL = N / LPC;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t col = t / LPC;
-  const int part = (int)(t - col * LPC);
-  const bool valid = col < ncols;
-  int s1 = 0, s2 = 0, lo = 1 << 20, hi = -(1 << 20);
-  if (valid) {
-    const int64_t e = col / S;
-    const int si = (int)(col - e * S);
-    const double sv = svals[si];
-    const double dm = mean[e];
-    const uint8_t* src = tiles + e * N + part * PPL;
-    uint8_t px[PPL];
-    if constexpr (PPL == 8) {
-      const uint2 w = *reinterpret_cast<const uint2*>(src);
-      *reinterpret_cast<uint2*>(px) = w;
-    } else {
-      const uint32_t w = *reinterpret_cast<const uint32_t*>(src);
-      *reinterpret_cast<uint32_t*>(px) = w;
-    }
-    int16_t qv[PPL];
+  // block-private histograms (flushed once): qmin | qmax | q2max
+  __shared__ unsigned sh[2048 + 1];
+  if (stats) {
+    for (int i = threadIdx.x; i < 2049; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+  }
+  const int64_t total = ncols * LPC;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // every lane of a warp runs the same trip count (shuffles below)
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += stride) {
+    const int64_t t = base + threadIdx.x;
+    const int64_t col = t / LPC;
+    const int part = (int)(t - col * LPC);
+    const bool valid = col < ncols;
+    int s1 = 0, s2 = 0, lo = 1 << 20, hi = -(1 << 20);
+    if (valid) {
+      const int64_t e = col / S;
+      const int si = (int)(col - e * S);
+      const double sv = svals[si];
+      const double dm = mean[e];
+      const uint8_t* src = tiles + e * N + part * PPL;
+      uint8_t px[PPL];
+      if constexpr (PPL == 8) {
+        *reinterpret_cast<uint2*>(px) = *reinterpret_cast<const uint2*>(src);
+      } else {
+        *reinterpret_cast<uint32_t*>(px) = *reinterpret_cast<const uint32_t*>(src);
+      }
+      int16_t qv[PPL];
 #pragma unroll
-    for (int k = 0; k < PPL; ++k) {
-      const double d = (double)px[k];
-      const double x = baseline ? d : __dsub_rn(d, dm);
-      const int v = (int)rint(__dmul_rn(sv, x));
-      qv[k] = (int16_t)v;
-      s1 += v;
-      s2 += v * v;
-      lo = min(lo, v);
-      hi = max(hi, v);
+      for (int k = 0; k < PPL; ++k) {
+        const double d = (double)px[k];
+        const double x = baseline ? d : __dsub_rn(d, dm);
+        const int v = (int)rint(__dmul_rn(sv, x));
+        qv[k] = (int16_t)v;
+        s1 += v;
+        s2 += v * v;
+        lo = min(lo, v);
+        hi = max(hi, v);
+      }
+      int16_t* dst = q + col * N + part * PPL;
+      if constexpr (PPL == 8) {
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(qv);
+      } else {
+        *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(qv);
+      }
     }
-    int16_t* dst = q + col * N + part * PPL;
-    if constexpr (PPL == 8) {
-      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(qv);
-    } else {
-      *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(qv);
+    if (!stats) continue;
+#pragma unroll
+    for (int o = 1; o < LPC; o <<= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (valid && part == 0) {
+      col_stats[col] = make_int4(s1, s2, lo, hi);
+      odd[col] = s2 & 1;  // == s1 & 1
+      atomicAdd(&sh[lo + 512], 1u);
+      atomicAdd(&sh[1024 + hi + 512], 1u);
+      atomicMax(&sh[2048], (unsigned)s2);
     }
   }
   if (!stats) return;
-#pragma unroll
-  for (int o = 1; o < LPC; o <<= 1) {
-    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  if (valid && part == 0) {
-    col_stats[col] = make_int4(s1, s2, lo, hi);
-    odd[col] = s2 & 1;  // == s1 & 1
-    atomicAdd(&hist[lo + 512], 1u);
-    atomicAdd(&hist[1024 + hi + 512], 1u);
-    atomicMax(&hist[2048], (unsigned)s2);
-  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+  if (threadIdx.x == 0) atomicMax(&hist[2048], sh[2048]);
 }
 
 __global__ void decode_keys_kernel(const unsigned long long* __restrict__ keys, int64_t M,
@@ -469,7 +492,7 @@ int level_prepare_exact(Ctx* c, Level& L, int tc_stats) {
   if (cols > 0) {
     const int lpc = L.n >= 8 ? L.n / 8 : 1;
     const int64_t threads = cols * lpc;
-    const unsigned grid = (unsigned)((threads + 255) / 256);
+    const unsigned grid = (unsigned)std::min<int64_t>((threads + 255) / 256, c->sm_count * 4);
 #define FC_LAUNCH_QPREP(NN)                                                                   \
     qprep_kernel<NN><<<grid, 256, 0, c->stream>>>(                                            \
         L.tiles.as<uint8_t>(), L.mean.as<double>(), cols, L.s_count, L.svals_d.as<double>(),  \
@@ -545,7 +568,8 @@ int load_ranges(Ctx* c, Level& L, const uint8_t* h_tiles, int64_t M) {
 }
 
 int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t n_range_list,
-               const int32_t* d_col_list, int64_t n_col_list, uint64_t* d_keys) {
+               const int32_t* d_col_list, int64_t n_col_list, uint64_t* d_keys,
+               const int32_t* d_M) {
   FC_TRY(ensure_iso_tables(c));
   const int64_t ncols = L.count * L.s_count;
   const int64_t nr = d_range_list ? n_range_list : M;
@@ -563,7 +587,8 @@ int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t
 #define FC_LAUNCH_EXACT(NN)                                                                     \
     scan_exact_kernel<NN><<<grid, kColsPerBlock, 0, c->stream>>>(                               \
         L.qbase.as<int16_t>(), ncols, L.s_count, d_s, L.mean.as<double>(),                      \
-        c->rtiles.as<uint8_t>(), c->rmean.as<double>(), nlist, inv, d_range_list, n_range_list, \
+        c->rtiles.as<uint8_t>(), c->rmean.as<double>(), nlist, d_M, inv, d_range_list,          \
+        n_range_list,                                                                           \
         base, d_col_list, n_col_list, L.baseline, keys)
     switch (L.n) {
       case 256: FC_LAUNCH_EXACT(256); break;
@@ -578,19 +603,20 @@ int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t
   return FC_OK;
 }
 
-int scan_exact_jobs(Ctx* c, Level& L, const int4* d_jobs, const int64_t* d_prefix, int n_jobs,
-                    int64_t total_blocks, const int32_t* d_sorted_ranges, const int32_t* d_low,
-                    const int32_t* d_high, uint64_t* d_keys) {
-  if (n_jobs == 0 || total_blocks == 0) return FC_OK;
+int scan_exact_jobs(Ctx* c, Level& L, const int4* d_jobs, const int64_t* d_prefix,
+                    const int* d_n_jobs, const long long* d_total_blocks,
+                    const int32_t* d_sorted_ranges, const int32_t* d_low, const int32_t* d_high,
+                    uint64_t* d_keys) {
   FC_TRY(ensure_iso_tables(c));
   const double* d_s = L.svals_d.as<double>();
   const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
   auto* keys = reinterpret_cast<unsigned long long*>(d_keys);
+  const unsigned grid = (unsigned)(c->sm_count * 8);
 #define FC_LAUNCH_JOBS(NN)                                                                      \
-  scan_jobs_kernel<NN><<<(unsigned)total_blocks, kColsPerBlock, 0, c->stream>>>(                 \
+  scan_jobs_kernel<NN><<<grid, kColsPerBlock, 0, c->stream>>>(                                  \
       L.qbase.as<int16_t>(), L.s_count, d_s, L.mean.as<double>(), c->rtiles.as<uint8_t>(),        \
-      c->rmean.as<double>(), inv, d_jobs, d_prefix, n_jobs, d_sorted_ranges, d_low, d_high,       \
-      L.baseline, keys)
+      c->rmean.as<double>(), inv, d_jobs, d_prefix, d_n_jobs, d_total_blocks, d_sorted_ranges,    \
+      d_low, d_high, L.baseline, keys)
   switch (L.n) {
     case 256: FC_LAUNCH_JOBS(256); break;
     case 64: FC_LAUNCH_JOBS(64); break;

@@ -64,6 +64,17 @@ constexpr int kMaxRG = 8;
 constexpr int kSmemBudget = 220 * 1024;
 constexpr int kNone = 0x7fffffff;
 
+// Unit decomposition of one launch, computed on the device from the range
+// count (tc_plan_kernel) so the host never waits for it.
+struct TcPlan {
+  int M;           // ranges
+  int n_rgroups;   // groups of RG row tiles
+  int tiles_per_unit;
+  int n_units;
+  int rows_pad;    // n_rgroups * RG * 128
+  int pad[3];
+};
+
 struct TcParams {
   const uint8_t* a_tiles;    // [rt_pad][128 * kpad]
   const int4* row_meta;      // [rt_pad * 128] {o, R, m, unused}
@@ -75,11 +86,12 @@ struct TcParams {
   int kpad;
   int rg;          // row tiles per unit (A resident in smem)
   int stages;      // B ring depth
-  int n_rgroups;
   int ntiles;
-  int tiles_per_unit;
-  int64_t n_units;
-  int debug_mode;  // 1: epilogue only drains TMEM (pipeline ceiling probe); results invalid
+  const TcPlan* plan;
+  int forward;     // 1: ascending tile order (strict updates), 0: descending (ties update)
+  int wait_mode;   // spin-wait roles: 1 = MMA issuer, 2 = epilogue, 4 = producer
+  int debug_mode;  // pipeline probes (results invalid): 1 = no epilogue arithmetic,
+                   // 2 = no MMA issue, 3 = both
 };
 
 __host__ __device__ inline uint32_t a_bytes(const TcParams& p) { return p.rg * kTileM * p.kpad; }
@@ -91,6 +103,12 @@ __host__ __device__ inline uint32_t bar_offset(const TcParams& p) {
 __host__ __device__ inline uint32_t smem_bytes(const TcParams& p) {
   const uint32_t raw = bar_offset(p) + (2 * p.stages + 2 * kNumAcc + 2) * 8 + 16;
   return raw < 116 * 1024 ? 116 * 1024 : raw;  // one CTA (owning all 512 TMEM columns) per SM
+}
+
+// mbarrier wait: spin (latency-critical roles) or suspend-hinted (saves issue slots)
+__device__ __forceinline__ void wait_bar(int spin, uint32_t bar, uint32_t parity) {
+  if (spin) ptx::mbar_wait(bar, parity);
+  else ptx::mbar_wait_sleep(bar, parity);
 }
 
 // 3-ary min tree over 32 values: 10 VIMNMX3 + 1 VIMNMX, then 4 + 1.
@@ -121,6 +139,11 @@ __device__ __forceinline__ int first_eq(const int (&v)[32], int m) {
 // <=>  m < ((best2 - par) >> 1) + 1.
 __device__ __forceinline__ int improve_limit(int best2, int par) {
   return (int)((((long long)best2 - par) >> 1) + 1);
+}
+// Ascending column order: only a strictly smaller key2 = 2*m + par updates
+// (equal keys keep the earlier, smaller column): m < (best2 - par + 1) >> 1.
+__device__ __forceinline__ int strict_limit(int best2, int par) {
+  return (int)(((long long)best2 - par + 1) >> 1);
 }
 
 // Work order (all roles derive it identically): unit u -> row group
@@ -165,23 +188,26 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int n_rg = p.n_rgroups;
-  const int CT = p.tiles_per_unit;
+  const TcPlan plan = *p.plan;
+  const int n_rg = plan.n_rgroups;
+  const int CT = plan.tiles_per_unit;
+  const int n_units = plan.n_units;
 
   if (warp == 0) {
     // ---------------- producer (TMA engine bulk copies) ----------------
     if (lane == 0) {
       uint32_t L = 0, U = 0;
-      for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++U) {
-        const int g = (int)(u % n_rg);
-        const int t0 = (int)(u / n_rg) * CT;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++U) {
+        const int g = u % n_rg;
+        const int t0 = (u / n_rg) * CT;
         const int t1 = min(p.ntiles, t0 + CT);
-        ptx::mbar_wait_sleep(aempty_bar, (U & 1) ^ 1);
+        wait_bar(p.wait_mode & 4, aempty_bar, (U & 1) ^ 1);
         ptx::mbar_expect_tx(afull_bar, kA);
         ptx::bulk_g2s(ptx::smem_u32(sA), p.a_tiles + (size_t)g * kA, kA, afull_bar);
-        for (int t = t1 - 1; t >= t0; --t, ++L) {
+        for (int ti = 0; ti < t1 - t0; ++ti, ++L) {
+        const int t = p.forward ? t0 + ti : t1 - 1 - ti;
           const int s = L % STAGES;
-          ptx::mbar_wait_sleep(empty_bar(s), ((L / STAGES) & 1) ^ 1);
+          wait_bar(p.wait_mode & 4, empty_bar(s), ((L / STAGES) & 1) ^ 1);
           uint8_t* st = sStage + s * kStage;
           ptx::mbar_expect_tx(full_bar(s), kStage);
           ptx::bulk_g2s(ptx::smem_u32(st), p.b_tiles + (size_t)t * kB, kB, full_bar(s));
@@ -200,26 +226,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     constexpr uint64_t kBStep = (2 * kTileN * 16) >> 4;
     const uint32_t a_base = ptx::smem_u32(sA);
     uint32_t L = 0, H = 0, U = 0;
-    for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++U) {
-      const int t0 = (int)(u / n_rg) * CT;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++U) {
+      const int t0 = (u / n_rg) * CT;
       const int t1 = min(p.ntiles, t0 + CT);
-      ptx::mbar_wait_sleep(afull_bar, U & 1);
+      wait_bar(p.wait_mode & 1, afull_bar, U & 1);
       ptx::tc_fence_after();
-      for (int t = t1 - 1; t >= t0; --t, ++L) {
+      for (int ti = 0; ti < t1 - t0; ++ti, ++L) {
+        const int t = p.forward ? t0 + ti : t1 - 1 - ti;
         const int s = L % STAGES;
-        ptx::mbar_wait_sleep(full_bar(s), (L / STAGES) & 1);
+        wait_bar(p.wait_mode & 1, full_bar(s), (L / STAGES) & 1);
         ptx::tc_fence_after();
         const uint32_t b_addr = ptx::smem_u32(sStage + s * kStage);
         const uint64_t bd0 = ptx::umma_desc(b_addr, kTileN * 16, 128);
         for (int r = 0; r < RG; ++r, ++H) {
           const uint64_t ad0 = ptx::umma_desc(a_base + r * (kTileM * KPAD), kTileM * 16, 128);
           const int acc = H % kNumAcc;
-          ptx::mbar_wait_sleep(tempty_bar(acc), ((H / kNumAcc) & 1) ^ 1);
+          wait_bar(p.wait_mode & 1, tempty_bar(acc), ((H / kNumAcc) & 1) ^ 1);
           ptx::tc_fence_after();
           const uint32_t d = tmem_base + acc * kAccN;
-          ptx::umma_i8_elect(d, ad0, bd0, kIdesc, 0u);
-          for (int ks = 1; ks < ksteps; ++ks)
-            ptx::umma_i8_elect(d, ad0 + ks * kAStep, bd0 + ks * kBStep, kIdesc, 1u);
+          if (p.debug_mode < 2) {
+            ptx::umma_i8_elect(d, ad0, bd0, kIdesc, 0u);
+            for (int ks = 1; ks < ksteps; ++ks)
+              ptx::umma_i8_elect(d, ad0 + ks * kAStep, bd0 + ks * kBStep, kIdesc, 1u);
+          }
           ptx::umma_commit_elect(tfull_bar(acc));
         }
         ptx::umma_commit_elect(empty_bar(s));
@@ -237,9 +266,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     const uint32_t tbase = tmem_base + ((uint32_t)(sp * 32) << 16) + cq * 64;
     const int slot_q = cq * 64;
     uint32_t L = 0, H = 0;
-    for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int g = (int)(u % n_rg);
-      const int t0 = (int)(u / n_rg) * CT;
+      const int t0 = (u / n_rg) * CT;
       const int t1 = min(p.ntiles, t0 + CT);
       // running best per (row tile): key2 and column
       int best2[kMaxRG], bcol[kMaxRG];
@@ -248,15 +277,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
         best2[r] = kNone;
         bcol[r] = 0;
       }
-      for (int t = t1 - 1; t >= t0; --t, ++L) {
+      for (int ti = 0; ti < t1 - t0; ++ti, ++L) {
+        const int t = p.forward ? t0 + ti : t1 - 1 - ti;
         const int s = L % STAGES;
         const int2 tinfo = p.tile_info[t];  // {parity, valid slots}
-        ptx::mbar_wait_sleep(full_bar(s), (L / STAGES) & 1);
+        wait_bar(p.wait_mode & 2, full_bar(s), (L / STAGES) & 1);
         const int32_t* colmap_s = reinterpret_cast<const int32_t*>(sStage + s * kStage + kB);
 #pragma unroll 1
         for (int r = 0; r < RG; ++r, ++H) {
           const int acc = H % kNumAcc;
-          ptx::mbar_wait_sleep(tfull_bar(acc), (H / kNumAcc) & 1);
+          wait_bar(p.wait_mode & 2, tfull_bar(acc), (H / kNumAcc) & 1);
           ptx::tc_fence_after();
           int va[32], vb[32];
           ptx::tmem_ld32(tbase + acc * kAccN, va);
@@ -273,9 +303,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
               if (slot_q + 32 + j >= tinfo.y) vb[j] = kNone;
             }
           }
-          if (p.debug_mode == 1) continue;
+          if (p.debug_mode & 1) continue;
           const int ma = min32(va), mb = min32(vb);
-          const int lim = improve_limit(best2[r], tinfo.x);
+          const int lim = p.forward ? strict_limit(best2[r], tinfo.x) : improve_limit(best2[r], tinfo.x);
           if (min(ma, mb) < lim) {  // rare: this row improves (or ties earlier) in these 64 columns
             const bool in_a = ma <= mb;
             const int m = in_a ? ma : mb;
@@ -326,10 +356,26 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
 __global__ void build_b_kernel(const int16_t* __restrict__ qbase, int n, int kpad, int planes,
                                int m_digits, int64_t ncols, const int4* __restrict__ stats,
                                const int32_t* __restrict__ odd_prefix, int64_t odd_base,
+                               int64_t n_even, int64_t n_odd, int64_t n_pad,
                                int8_t* __restrict__ b_tiles, int32_t* __restrict__ colmap) {
   const int chunks = kpad / 16;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ncols * chunks) return;
+  if (i >= ncols * chunks) {
+    // padding slots of the last tile of each parity group: zero operand, no column
+    const int64_t pi = i - ncols * chunks;
+    if (pi >= n_pad * chunks) return;
+    const int64_t p = pi / chunks;
+    const int kc = (int)(pi - p * chunks);
+    const int64_t pad_even = ((n_even + kTileN - 1) / kTileN) * kTileN - n_even;
+    const int64_t slot = p < pad_even ? n_even + p : odd_base + n_odd + (p - pad_even);
+    const int64_t tile = slot / kTileN;
+    const int cc = (int)(slot - tile * kTileN);
+    int8_t* dst = b_tiles + tile * ((int64_t)kTileN * kpad) + (int64_t)kc * (kTileN * 16) +
+                  (cc >> 3) * 128 + (cc & 7) * 16;
+    *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    if (kc == 0) colmap[slot] = -1;
+    return;
+  }
   const int64_t col = i / chunks;
   const int kc = (int)(i - col * chunks);
   const int4 st = stats[col];
@@ -381,11 +427,13 @@ __global__ void build_b_kernel(const int16_t* __restrict__ qbase, int n, int kpa
 // A operand: row (range, iso) of each 128-row tile = 16 ranges x 8 isometries:
 // r_iso bytes (again for a second plane), then 255 x m, 1, 1, o, o, zeros.
 __global__ void build_a_kernel(const uint8_t* __restrict__ rtiles, const double* __restrict__ rmean,
-                               const int32_t* __restrict__ rsq, int64_t M, int n, int kpad,
-                               int planes, int m_digits, const uint16_t* __restrict__ inv,
-                               int64_t rows_pad, uint8_t* __restrict__ a_tiles,
+                               const int32_t* __restrict__ rsq, const TcPlan* __restrict__ plan,
+                               int n, int kpad, int planes, int m_digits,
+                               const uint16_t* __restrict__ inv, uint8_t* __restrict__ a_tiles,
                                int4* __restrict__ row_meta) {
   const int chunks = kpad / 16;
+  const int64_t M = plan->M;
+  const int64_t rows_pad = plan->rows_pad;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rows_pad * chunks) return;
   const int64_t row = i / chunks;
@@ -435,29 +483,148 @@ __global__ void build_a_kernel(const uint8_t* __restrict__ rtiles, const double*
   }
 }
 
+// Counting-sort scatter with warp-aggregated cursor updates: lanes holding the
+// same bucket take consecutive slots from one atomic (bucket order is free).
+__device__ __forceinline__ void bucket_scatter(bool valid, int bucket, int32_t* __restrict__ cursors,
+                                               int32_t* __restrict__ out, int32_t value) {
+  const int key = valid ? bucket : -1 - (int)(threadIdx.x & 31);
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(peers) - 1;
+  int base = 0;
+  if (valid && lane == leader) base = atomicAdd(&cursors[bucket], __popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  if (valid) out[base + __popc(peers & ((1u << lane) - 1))] = value;
+}
+
 // Clamp-reach lists by counting sort: columns bucketed by qmin (ascending) and
 // by qmax (descending); the order inside a bucket does not matter.
 __global__ void reach_scatter_kernel(const int4* __restrict__ stats, int64_t ncols,
                                      int32_t* __restrict__ cur_low, int32_t* __restrict__ cur_high,
                                      int32_t* __restrict__ reach_low, int32_t* __restrict__ reach_high) {
   const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= ncols) return;
-  const int4 st = stats[col];
-  reach_low[atomicAdd(&cur_low[st.z + 512], 1)] = (int32_t)col;
-  reach_high[atomicAdd(&cur_high[st.w + 512], 1)] = (int32_t)col;
+  const bool valid = col < ncols;
+  const int4 st = valid ? stats[col] : make_int4(0, 0, 0, 0);
+  bucket_scatter(valid, st.z + 512, cur_low, reach_low, (int32_t)col);
+  bucket_scatter(valid, st.w + 512, cur_high, reach_high, (int32_t)col);
 }
 
 // Ranges bucketed by offset o (counting sort; cursors = exclusive bucket starts).
-__global__ void order_scatter_kernel(const int32_t* __restrict__ roff, int64_t M,
+__global__ void order_scatter_kernel(const int32_t* __restrict__ roff, const int32_t* __restrict__ d_M,
                                      int32_t* __restrict__ cursors, int32_t* __restrict__ order) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < M) order[atomicAdd(&cursors[roff[i]], 1)] = (int32_t)i;
+  const bool valid = i < *d_M;
+  bucket_scatter(valid, valid ? roff[i] : 0, cursors, order, (int32_t)i);
 }
 
-__global__ void fill_i32_kernel(int32_t* __restrict__ p, int64_t n, int32_t v) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) p[i] = v;
+// Unit decomposition: RG row tiles per group, the column tiles split into
+// spans minimising the per-CTA makespan ceil(units / grid) * (tiles + 2);
+// the first (smallest) span count wins ties.
+__global__ void __launch_bounds__(256) tc_plan_kernel(const int32_t* __restrict__ d_M, int RG,
+                                                      int ntiles, int grid,
+                                                      TcPlan* __restrict__ plan) {
+  __shared__ unsigned long long best[256];
+  const int M = *d_M;
+  const int n_rtiles = (M * 8 + kTileM - 1) / kTileM;
+  const int n_rg = (n_rtiles + RG - 1) / RG;
+  unsigned long long mine = ~0ull;
+  const int smax = min(ntiles, 8192);
+  for (int sc = threadIdx.x + 1; sc <= smax; sc += blockDim.x) {
+    const long long ct = (ntiles + sc - 1) / sc;
+    const long long nsp = (ntiles + ct - 1) / ct;
+    const long long units = nsp * n_rg;
+    const long long cost = ((units + grid - 1) / grid) * (ct + 2);
+    const unsigned long long key = ((unsigned long long)cost << 24) | (unsigned long long)sc;
+    mine = key < mine ? key : mine;
+  }
+  best[threadIdx.x] = mine;
+  __syncthreads();
+  for (int o = 128; o; o >>= 1) {
+    if (threadIdx.x < o) best[threadIdx.x] = min(best[threadIdx.x], best[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const int sc = (int)(best[0] & 0xffffff);
+    const int ct = (ntiles + sc - 1) / sc;
+    const int nsp = (ntiles + ct - 1) / ct;
+    TcPlan pl{};
+    pl.M = M;
+    pl.n_rgroups = M > 0 ? n_rg : 0;
+    pl.tiles_per_unit = ct;
+    pl.n_units = M > 0 ? nsp * n_rg : 0;
+    pl.rows_pad = n_rg * RG * kTileM;
+    *plan = pl;
+  }
 }
+
+// Clamp-correction jobs from the offset histogram (one block, thread = o):
+// ranges with offset o against the columns whose qmin < -o (list 0) or
+// qmax > 255 - o (list 1); blocks of 8 ranges x 128 columns.
+struct FixPlan {
+  int n_jobs;
+  int pad;
+  long long total_blocks;
+  long long fix_pairs;
+};
+__global__ void __launch_bounds__(256) fix_plan_kernel(const int32_t* __restrict__ hist,
+                                                       const long long* __restrict__ reach_counts,
+                                                       int4* __restrict__ jobs,
+                                                       long long* __restrict__ prefix,
+                                                       int32_t* __restrict__ cursors,
+                                                       FixPlan* __restrict__ out) {
+  using Scan = cub::BlockScan<long long, 256>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_start[257];
+  const int o = threadIdx.x;
+  const int cnt = hist[o];
+  {
+    using IScan = cub::BlockScan<int, 256>;
+    __shared__ typename IScan::TempStorage itmp;
+    int excl;
+    IScan(itmp).ExclusiveSum(cnt, excl);
+    s_start[o] = excl;
+    cursors[o] = excl;
+  }
+  const long long lists[2] = {reach_counts[o], reach_counts[256 + o]};
+  int njob = 0;
+  long long blocks = 0, pairs = 0;
+  for (int k = 0; k < 2; ++k)
+    if (cnt && lists[k]) {
+      ++njob;
+      blocks += (long long)((cnt + 7) / 8) * ((lists[k] + 127) / 128);
+      pairs += (long long)cnt * lists[k];
+    }
+  __syncthreads();
+  int jbase;
+  {
+    using IScan = cub::BlockScan<int, 256>;
+    __shared__ typename IScan::TempStorage itmp2;
+    IScan(itmp2).ExclusiveSum(njob, jbase);
+  }
+  long long bbase, agg;
+  Scan(tmp).ExclusiveSum(blocks, bbase, agg);
+  __syncthreads();
+  long long pbase, pagg;
+  Scan(tmp).ExclusiveSum(pairs, pbase, pagg);
+  int j = jbase;
+  long long b = bbase;
+  for (int k = 0; k < 2; ++k)
+    if (cnt && lists[k]) {
+      jobs[j] = make_int4(k, s_start[o], cnt, (int)lists[k]);
+      prefix[j] = b;
+      b += (long long)((cnt + 7) / 8) * ((lists[k] + 127) / 128);
+      ++j;
+    }
+  if (o == 255) {
+    prefix[j] = b;
+    FixPlan fp{};
+    fp.n_jobs = j;
+    fp.total_blocks = b;
+    fp.fix_pairs = pagg;
+    *out = fp;
+  }
+}
+
 
 }  // namespace
 
@@ -524,6 +691,15 @@ int level_prepare_tc_finish(Ctx* c, Level& L) {
       T.high_count[o] = cmax[1024] - cmax[768 - o];
     }
   }
+  FC_CUDA(c, T.reach_counts.reserve(512 * 8));
+  {
+    long long rc[512];
+    for (int o = 0; o < 256; ++o) {
+      rc[o] = T.low_count[o];
+      rc[256 + o] = T.high_count[o];
+    }
+    FC_TRY(stage_h2d(c, T.reach_counts.ptr, rc, sizeof rc));
+  }
   // two parity groups, each padded to whole tiles
   const int64_t n_odd = (int64_t)last_prefix + last_odd;
   const int64_t n_even = ncols - n_odd;
@@ -564,26 +740,26 @@ int level_prepare_tc_finish(Ctx* c, Level& L) {
   FC_CUDA(c, T.b_tiles.reserve(slots * T.kpad));
   FC_CUDA(c, T.meta.reserve(slots * 4));
   FC_CUDA(c, T.tile_q1.reserve(T.ntiles * 8 + 16));
-  // only the padding slots of the last tile of each group need zero operands
-  FC_CUDA(c, cudaMemsetAsync(T.b_tiles.ptr, 0, slots * T.kpad, c->stream));
-  fill_i32_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, c->stream>>>(T.meta.as<int32_t>(),
-                                                                         slots, -1);
   FC_TRY(stage_h2d(c, T.tile_q1.ptr, tinfo.data(), T.ntiles * 8));
-  const int64_t work = ncols * (T.kpad / 16);
+  const int64_t n_pad = slots - ncols;
+  const int64_t work = (ncols + n_pad) * (T.kpad / 16);
   build_b_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
       L.qbase.as<int16_t>(), L.n, T.kpad, T.planes, T.m_digits, ncols, T.col_stats.as<int4>(),
-      T.odd.as<int32_t>() + ncols, odd_base, T.b_tiles.as<int8_t>(), T.meta.as<int32_t>());
+      T.odd.as<int32_t>() + ncols, odd_base, n_even, n_odd, n_pad, T.b_tiles.as<int8_t>(),
+      T.meta.as<int32_t>());
   FC_CUDA(c, cudaGetLastError());
-  c->total_launches += 2;
+  c->total_launches += 1;
   T.ready = true;
   return FC_OK;
 }
 
-int scan_tc_launch(Ctx* c, Level& L, int64_t M, uint64_t* d_keys, const int32_t* h_hist,
-                   cudaEvent_t ev_main_begin, cudaEvent_t ev_main_end, int64_t* out_fix_pairs) {
+// Device-driven launch: range count d_M (<= M_bound) and the offset
+// histogram d_hist live on the device; nothing here waits for the GPU.
+int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const int32_t* d_hist,
+                   uint64_t* d_keys, cudaEvent_t ev_main_end, int64_t* d_fix_pairs) {
   TcOperands& T = L.tc;
   if (!T.ready) return set_error(c, FC_ERR_STATE, "tensor operands not prepared");
-  if (M == 0) return FC_OK;
+  if (M_bound == 0) return FC_OK;
   FC_TRY(ensure_iso_tables(c));
   TcParams prm{};
   prm.kpad = T.kpad;
@@ -597,18 +773,21 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M, uint64_t* d_keys, const int32_t*
   }
   if ((int)smem_bytes(prm) > 227 * 1024) return set_error(c, FC_ERR_ARG, "K too large for smem");
   const int RG = prm.rg;
-  const int64_t n_rtiles = (M * 8 + kTileM - 1) / kTileM;
-  const int n_rgroups = (int)((n_rtiles + RG - 1) / RG);
-  const int64_t rows_pad = (int64_t)n_rgroups * RG * kTileM;
-  FC_CUDA(c, c->a_tiles.reserve(rows_pad * T.kpad));
-  FC_CUDA(c, c->row_meta.reserve(rows_pad * 16));
+  const int64_t rtiles_max = (M_bound * 8 + kTileM - 1) / kTileM;
+  const int64_t rows_max = ((rtiles_max + RG - 1) / RG) * RG * kTileM;
+  FC_CUDA(c, c->a_tiles.reserve(rows_max * T.kpad));
+  FC_CUDA(c, c->row_meta.reserve(rows_max * 16));
+  FC_CUDA(c, c->tc_plan.reserve(sizeof(TcPlan) + sizeof(FixPlan) + 64));
+  TcPlan* d_plan = c->tc_plan.as<TcPlan>();
+  FixPlan* d_fplan = reinterpret_cast<FixPlan*>(c->tc_plan.as<uint8_t>() + sizeof(TcPlan));
+  tc_plan_kernel<<<1, 256, 0, c->stream>>>(d_M, RG, (int)T.ntiles, c->sm_count, d_plan);
   const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
-  const int64_t work = rows_pad * (T.kpad / 16);
+  const int64_t work = rows_max * (T.kpad / 16);
   build_a_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
-      c->rtiles.as<uint8_t>(), c->rmean.as<double>(), c->rsq.as<int32_t>(), M, L.n, T.kpad, T.planes,
-      T.m_digits, inv, rows_pad, c->a_tiles.as<uint8_t>(), c->row_meta.as<int4>());
+      c->rtiles.as<uint8_t>(), c->rmean.as<double>(), c->rsq.as<int32_t>(), d_plan, L.n, T.kpad,
+      T.planes, T.m_digits, inv, c->a_tiles.as<uint8_t>(), c->row_meta.as<int4>());
   FC_CUDA(c, cudaGetLastError());
-  c->stats.kernel_launches += 1;
+  c->stats.kernel_launches += 2;
 
   prm.a_tiles = c->a_tiles.as<uint8_t>();
   prm.row_meta = c->row_meta.as<int4>();
@@ -617,106 +796,65 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M, uint64_t* d_keys, const int32_t*
   prm.tile_info = T.tile_q1.as<int2>();
   prm.keys = reinterpret_cast<unsigned long long*>(d_keys);
   prm.S = L.s_count;
-  prm.n_rgroups = n_rgroups;
   prm.ntiles = (int)T.ntiles;
-  // split the column tiles into spans: minimise the per-CTA makespan
-  // ceil(units / grid) * (tiles per unit + unit overhead) over the span count
-  {
-    const int64_t grid = c->sm_count;
-    double best_cost = 1e300;
-    int64_t best_ct = T.ntiles;
-    for (int64_t s = 1; s <= std::min<int64_t>(T.ntiles, 8192); ++s) {
-      const int64_t ct = (T.ntiles + s - 1) / s;
-      const int64_t nsp = (T.ntiles + ct - 1) / ct;
-      const int64_t units = nsp * n_rgroups;
-      const int64_t per_cta = (units + grid - 1) / grid;
-      const double cost = (double)per_cta * (double)(ct + 2);
-      if (cost < best_cost - 1e-9) {
-        best_cost = cost;
-        best_ct = ct;
-      }
-    }
-    prm.tiles_per_unit = (int)best_ct;
-  }
-  const int64_t n_spans = (T.ntiles + prm.tiles_per_unit - 1) / prm.tiles_per_unit;
-  prm.n_units = n_spans * n_rgroups;
+  prm.plan = d_plan;
   if (const char* dbg = getenv("FC_TC_DEBUG_MODE")) prm.debug_mode = atoi(dbg);
-
-  if (ev_main_begin) FC_CUDA(c, cudaEventRecord(ev_main_begin, c->stream));
+  prm.wait_mode = c->tc_wait_mode;
+  prm.forward = c->tc_forward;
   const uint32_t smem = smem_bytes(prm);
   if (!c->tc_attr_set) {
     FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     227 * 1024));
     c->tc_attr_set = true;
   }
-  const int grid = (int)std::min<int64_t>(prm.n_units, c->sm_count);
-  tc_scan_kernel<<<grid, kThreads, smem, c->stream>>>(prm);
+  tc_scan_kernel<<<c->sm_count, kThreads, smem, c->stream>>>(prm);
   FC_CUDA(c, cudaGetLastError());
   if (ev_main_end) FC_CUDA(c, cudaEventRecord(ev_main_end, c->stream));
   c->stats.kernel_launches += 1;
 
-  // ---- clamp corrections (exact kernel on clamp-active pairs) ----
-  // ranges bucketed by o on the device; jobs planned here from the histogram
-  std::vector<int32_t> start(257, 0);
-  for (int o = 0; o < 256; ++o) start[o + 1] = start[o] + h_hist[o];
-  if ((int64_t)start[256] != M) return set_error(c, FC_ERR_STATE, "offset histogram mismatch");
-  std::vector<int4> jobs;
-  std::vector<int64_t> prefix(1, 0);
-  int64_t fix_pairs = 0;
-  const int RB = 8, CB = 128;
-  for (int o = 0; o < 256; ++o) {
-    const int64_t cnt = h_hist[o];
-    if (!cnt) continue;
-    const int64_t lists[2] = {T.low_count[o], T.high_count[o]};
-    for (int kind = 0; kind < 2; ++kind) {
-      const int64_t ncol = lists[kind];
-      if (!ncol) continue;
-      jobs.push_back(make_int4(kind, (int)start[o], (int)cnt, (int)ncol));
-      prefix.push_back(prefix.back() + ((cnt + RB - 1) / RB) * ((ncol + CB - 1) / CB));
-      fix_pairs += cnt * ncol;
-    }
-  }
-  if (out_fix_pairs) *out_fix_pairs = fix_pairs;
-  if (!jobs.empty()) {
-    FC_CUDA(c, c->fix_rows.reserve(M * 4));
-    FC_CUDA(c, c->fix_jobs.reserve(jobs.size() * 16));
-    FC_CUDA(c, c->fix_cols.reserve(prefix.size() * 8));
-    FC_CUDA(c, c->tc_scratch.reserve(256 * 4));
-    int32_t* d_cursor = c->tc_scratch.as<int32_t>();
-    FC_TRY(stage_h2d(c, d_cursor, start.data(), 256 * 4));
-    order_scatter_kernel<<<(unsigned)((M + 255) / 256), 256, 0, c->stream>>>(
-        c->roff.as<int32_t>(), M, d_cursor, c->fix_rows.as<int32_t>());
-    FC_CUDA(c, cudaGetLastError());
-    c->stats.kernel_launches += 1;
-    FC_TRY(stage_h2d(c, c->fix_jobs.ptr, jobs.data(), jobs.size() * 16));
-    FC_TRY(stage_h2d(c, c->fix_cols.ptr, prefix.data(), prefix.size() * 8));
-    FC_TRY(scan_exact_jobs(c, L, c->fix_jobs.as<int4>(), c->fix_cols.as<int64_t>(),
-                           (int)jobs.size(), prefix.back(), c->fix_rows.as<int32_t>(),
-                           T.reach_low.as<int32_t>(), T.reach_high.as<int32_t>(), d_keys));
-  }
+  // ---- clamp corrections (exact kernel on clamp-active pairs), planned on the device ----
+  FC_CUDA(c, c->fix_rows.reserve(M_bound * 4 + 64));
+  FC_CUDA(c, c->fix_jobs.reserve(512 * 16 + 64));
+  FC_CUDA(c, c->fix_cols.reserve(513 * 8 + 64));
+  FC_CUDA(c, c->tc_scratch.reserve(256 * 4));
+  int32_t* d_cursor = c->tc_scratch.as<int32_t>();
+  fix_plan_kernel<<<1, 256, 0, c->stream>>>(d_hist, T.reach_counts.as<long long>(),
+                                            c->fix_jobs.as<int4>(), c->fix_cols.as<long long>(),
+                                            d_cursor, d_fplan);
+  order_scatter_kernel<<<(unsigned)((M_bound + 255) / 256), 256, 0, c->stream>>>(
+      c->roff.as<int32_t>(), d_M, d_cursor, c->fix_rows.as<int32_t>());
+  FC_CUDA(c, cudaGetLastError());
+  c->stats.kernel_launches += 2;
+  FC_TRY(scan_exact_jobs(c, L, c->fix_jobs.as<int4>(), c->fix_cols.as<int64_t>(),
+                         &d_fplan->n_jobs, &d_fplan->total_blocks, c->fix_rows.as<int32_t>(),
+                         T.reach_low.as<int32_t>(), T.reach_high.as<int32_t>(), d_keys));
+  if (d_fix_pairs)
+    FC_CUDA(c, cudaMemcpyAsync(d_fix_pairs, &d_fplan->fix_pairs, 8, cudaMemcpyDeviceToDevice,
+                               c->stream));
   return FC_OK;
 }
 
-// Per-call API variant: histogram of the gathered ranges' offsets, one sync,
-// then the asynchronous launch; fills the main / fix timings of fc_stats.
+// Per-call API variant (fc_match_level / fc_match_tiles): M is known here.
 int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys) {
-  FC_CUDA(c, c->enc_hist.reserve(256 * 4));
+  FC_CUDA(c, c->enc_hist.reserve(256 * 4 + 64));
+  FC_CUDA(c, c->enc_count.reserve(64 * 4));
+  int32_t* d_M = c->enc_count.as<int32_t>() + 16;
+  auto* d_fix = reinterpret_cast<int64_t*>(c->enc_count.as<int32_t>() + 20);
+  const int32_t m32 = (int32_t)M;
+  FC_TRY(stage_h2d(c, d_M, &m32, 4));
   FC_TRY(roff_hist(c, M, c->enc_hist.as<int32_t>()));
-  FC_CUDA(c, c->readback.reserve(256 * 4));
-  FC_CUDA(c, cudaMemcpyAsync(c->readback.ptr, c->enc_hist.ptr, 256 * 4, cudaMemcpyDeviceToHost,
-                             c->stream));
-  FC_TRY(sync_stream(c));
-  std::vector<int32_t> hist(c->readback.as<int32_t>(), c->readback.as<int32_t>() + 256);
-  int64_t fix_pairs = 0;
-  FC_TRY(scan_tc_launch(c, L, M, d_keys, hist.data(), c->tc_ev[0], c->tc_ev[1], &fix_pairs));
+  FC_CUDA(c, cudaEventRecord(c->tc_ev[0], c->stream));
+  FC_TRY(scan_tc_launch(c, L, M, d_M, c->enc_hist.as<int32_t>(), d_keys, c->tc_ev[1], d_fix));
   FC_CUDA(c, cudaEventRecord(c->tc_ev[2], c->stream));
-  FC_CUDA(c, cudaEventSynchronize(c->tc_ev[2]));
+  FC_CUDA(c, c->readback.reserve(64));
+  FC_CUDA(c, cudaMemcpyAsync(c->readback.ptr, d_fix, 8, cudaMemcpyDeviceToHost, c->stream));
+  FC_TRY(sync_stream(c));
   float main_ms = 0.f, fix_ms = 0.f;
   cudaEventElapsedTime(&main_ms, c->tc_ev[0], c->tc_ev[1]);
   cudaEventElapsedTime(&fix_ms, c->tc_ev[1], c->tc_ev[2]);
   c->stats.main_ms = main_ms;
   c->stats.fix_ms = fix_ms;
-  c->stats.fix_pairs = fix_pairs;
+  c->stats.fix_pairs = *c->readback.as<int64_t>();
   c->stats.rescans = 0;
   return FC_OK;
 }

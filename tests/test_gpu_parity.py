@@ -56,6 +56,47 @@ def test_pool_all_window_entropies_bit_exact(ctx):
                 assert ents.tobytes() == ref[order].tobytes(), (name, stride, level)
 
 
+def test_pool_threshold_rank_order_bit_exact(ctx):
+    """Threshold pools (device compaction + rank sort) keep {ent > tau} in the
+    reference's stable descending order, ties by raster index."""
+    g = load_golden("entropy_cases.npz")
+    checked = 0
+    for name in g["names"]:
+        img = g[f"img_{name}"]
+        h, w = img.shape
+        for stride in (1, 3):
+            taus, expect = [], []
+            for level in (1, 2, 3, 4):
+                ref = g[f"ent_{name}_{level}_{stride}"]
+                D = fc.pool.LEVEL_DOMAIN_SIDES[level - 1]
+                nx = (w - D) // stride + 1
+                tau = float(np.median(ref))
+                if not (ref > tau).any():
+                    tau = float(np.min(ref)) - 1.0
+                order = np.argsort(-ref, kind="stable")
+                keep = order[ref[order] > tau]
+                expect.append(np.stack([(keep % nx) * stride, (keep // nx) * stride], axis=1))
+                taus.append(tau)
+            pool = fc.build_pool(fc.GrayImage(img), fc.PoolParams(
+                pool_cap=10**9, strides=(stride,) * 4, entropy_thresholds=tuple(taus)), context=ctx)
+            for level in (1, 2, 3, 4):
+                got = pool.coords_array(level).astype(np.int64)
+                assert np.array_equal(got, expect[level - 1]), (name, stride, level)
+                checked += 1
+    assert checked > 0
+
+
+def test_pool_threshold_large_set_matches_cap_order(ctx):
+    """> 131072 survivors take the two-pass radix path; order equals the cap sort."""
+    rng = np.random.default_rng(7)
+    img = fc.GrayImage(rng.integers(0, 256, (640, 640)).astype(np.uint8))
+    a = fc.build_pool(img, fc.PoolParams(pool_cap=10**9), context=ctx)
+    ref = {lv: a.coords_array(lv).copy() for lv in (1, 2, 3, 4)}
+    b = fc.build_pool(img, fc.PoolParams(pool_cap=10**9, entropy_thresholds=(-1.0,) * 4), context=ctx)
+    for lv in (1, 2, 3, 4):
+        assert np.array_equal(b.coords_array(lv), ref[lv]), lv
+
+
 def test_pool_config_error(ctx):
     with pytest.raises(fc.PoolConfigError):
         fc.build_pool(fc.GrayImage.full(16, 16, 0), fc.PoolParams(pool_cap=4), context=ctx)
