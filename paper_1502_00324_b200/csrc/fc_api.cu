@@ -188,8 +188,6 @@ int fc_ctx_create(int device, fc_ctx** out) {
   if (!c) return FC_ERR_ARG;
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
-  if (const char* w = getenv("FC_TC_WAIT")) c->tc_wait_mode = atoi(w);
-  if (const char* f = getenv("FC_TC_FORWARD")) c->tc_forward = atoi(f);
   if (const char* t = getenv("FC_TRACE")) c->trace = atoi(t);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||

@@ -129,7 +129,6 @@ struct Ctx {
   std::vector<double> trace_host_us;
   std::vector<cudaEvent_t> trace_ev;
   bool tc_attr_set = false;
-  int tc_wait_mode = 0;
   int tc_forward = 0;    // FC_TC_FORWARD: tile scan order of the tensor kernel  // FC_TC_WAIT: spin-wait roles of the tensor kernel
   bool ent_attr_set = false;
   Status st;

@@ -46,6 +46,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "fc_internal.cuh"
@@ -61,7 +62,7 @@ constexpr int kNumAcc = 2;       // TMEM accumulators (2 x 256 columns = all 512
 constexpr int kEpiWarps = 16;    // all drain every accumulator (4 per TMEM sub-partition)
 constexpr int kThreads = (4 + kEpiWarps) * 32;
 constexpr int kMaxRG = 8;
-constexpr int kSmemBudget = 220 * 1024;
+constexpr int kSmemBudget = 227 * 1024;  // the opt-in maximum per block
 constexpr int kNone = 0x7fffffff;
 
 // Unit decomposition of one launch, computed on the device from the range
@@ -88,39 +89,30 @@ struct TcParams {
   int stages;      // B ring depth
   int ntiles;
   const TcPlan* plan;
-  int forward;     // 1: ascending tile order (strict updates), 0: descending (ties update)
-  int wait_mode;   // spin-wait roles: 1 = MMA issuer, 2 = epilogue, 4 = producer
-  int debug_mode;  // pipeline probes (results invalid): 1 = no epilogue arithmetic,
-                   // 2 = no MMA issue, 3 = both
+  int deferred;    // 1: resolve the winning column once per unit (short K)
+  int debug_mode;  // 1: epilogue only drains TMEM (pipeline probe; results invalid)
 };
 
 __host__ __device__ inline uint32_t a_bytes(const TcParams& p) { return p.rg * kTileM * p.kpad; }
 __host__ __device__ inline uint32_t b_bytes(const TcParams& p) { return kTileN * p.kpad; }
 __host__ __device__ inline uint32_t stage_bytes(const TcParams& p) { return b_bytes(p) + kTileN * 4; }
-__host__ __device__ inline uint32_t bar_offset(const TcParams& p) {
+// per epilogue thread and resident row tile: {best key2, tile * 8 + 8-column group}
+__host__ __device__ inline uint32_t best_offset(const TcParams& p) {
   return a_bytes(p) + p.stages * stage_bytes(p);
+}
+__host__ __device__ inline uint32_t bar_offset(const TcParams& p) {
+  return best_offset(p) + p.rg * kEpiWarps * 32 * 8;
 }
 __host__ __device__ inline uint32_t smem_bytes(const TcParams& p) {
   const uint32_t raw = bar_offset(p) + (2 * p.stages + 2 * kNumAcc + 2) * 8 + 16;
   return raw < 116 * 1024 ? 116 * 1024 : raw;  // one CTA (owning all 512 TMEM columns) per SM
 }
 
-// mbarrier wait: spin (latency-critical roles) or suspend-hinted (saves issue slots)
-__device__ __forceinline__ void wait_bar(int spin, uint32_t bar, uint32_t parity) {
-  if (spin) ptx::mbar_wait(bar, parity);
-  else ptx::mbar_wait_sleep(bar, parity);
-}
-
-// 3-ary min tree over 32 values: 10 VIMNMX3 + 1 VIMNMX, then 4 + 1.
-__device__ __forceinline__ int min32(const int (&v)[32]) {
-  int a[11];
-#pragma unroll
-  for (int k = 0; k < 10; ++k) a[k] = __vimin3_s32(v[3 * k], v[3 * k + 1], v[3 * k + 2]);
-  a[10] = min(v[30], v[31]);
-  const int b0 = __vimin3_s32(a[0], a[1], a[2]);
-  const int b1 = __vimin3_s32(a[3], a[4], a[5]);
-  const int b2 = __vimin3_s32(a[6], a[7], a[8]);
-  return min(__vimin3_s32(b0, b1, b2), min(a[9], a[10]));
+// Minimum of 8 consecutive values v[o..o+7]: 3 VIMNMX3 + 1 VIMNMX.
+template <int O>
+__device__ __forceinline__ int min8(const int (&v)[32]) {
+  return __vimin3_s32(__vimin3_s32(v[O], v[O + 1], v[O + 2]), __vimin3_s32(v[O + 3], v[O + 4], v[O + 5]),
+                      min(v[O + 6], v[O + 7]));
 }
 
 // First index j with v[j] == m (m is known to occur).
@@ -131,19 +123,24 @@ __device__ __forceinline__ int first_eq(const int (&v)[32], int m) {
   return j;
 }
 
-// Row state: best2 = 2*kh + par of the row's best so far, bcol its column.
+// u8 x s8 four-way dot product accumulate (the MMA's kind::i8 arithmetic).
+__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
+  int d;
+  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// Row state: best2 = 2*kh + par of the row's best so far and where it lies
+// (tile, 8-column group of this thread's quarter); the exact column inside
+// the group is resolved once per unit by recomputing its 8 dot products.
 // Tiles are visited in DECREASING column order (the entropy-ranked pool puts
 // the usually-better low-entropy domains last, so scanning backwards finds
 // them first and the running minimum rarely changes); an equal key2 at a
 // smaller column must then win, so a block updates iff 2*m + par <= best2
 // <=>  m < ((best2 - par) >> 1) + 1.
+// (32-bit: best2 <= 0x7fffffff and par in {0, 1} cannot overflow.)
 __device__ __forceinline__ int improve_limit(int best2, int par) {
-  return (int)((((long long)best2 - par) >> 1) + 1);
-}
-// Ascending column order: only a strictly smaller key2 = 2*m + par updates
-// (equal keys keep the earlier, smaller column): m < (best2 - par + 1) >> 1.
-__device__ __forceinline__ int strict_limit(int best2, int par) {
-  return (int)(((long long)best2 - par + 1) >> 1);
+  return ((best2 - par) >> 1) + 1;
 }
 
 // Work order (all roles derive it identically): unit u -> row group
@@ -201,13 +198,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
         const int g = u % n_rg;
         const int t0 = (u / n_rg) * CT;
         const int t1 = min(p.ntiles, t0 + CT);
-        wait_bar(p.wait_mode & 4, aempty_bar, (U & 1) ^ 1);
+        ptx::mbar_wait_sleep(aempty_bar, (U & 1) ^ 1);
         ptx::mbar_expect_tx(afull_bar, kA);
         ptx::bulk_g2s(ptx::smem_u32(sA), p.a_tiles + (size_t)g * kA, kA, afull_bar);
-        for (int ti = 0; ti < t1 - t0; ++ti, ++L) {
-        const int t = p.forward ? t0 + ti : t1 - 1 - ti;
+        for (int t = t1 - 1; t >= t0; --t, ++L) {
           const int s = L % STAGES;
-          wait_bar(p.wait_mode & 4, empty_bar(s), ((L / STAGES) & 1) ^ 1);
+          ptx::mbar_wait_sleep(empty_bar(s), ((L / STAGES) & 1) ^ 1);
           uint8_t* st = sStage + s * kStage;
           ptx::mbar_expect_tx(full_bar(s), kStage);
           ptx::bulk_g2s(ptx::smem_u32(st), p.b_tiles + (size_t)t * kB, kB, full_bar(s));
@@ -229,26 +225,23 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++U) {
       const int t0 = (u / n_rg) * CT;
       const int t1 = min(p.ntiles, t0 + CT);
-      wait_bar(p.wait_mode & 1, afull_bar, U & 1);
+      ptx::mbar_wait_sleep(afull_bar, U & 1);
       ptx::tc_fence_after();
-      for (int ti = 0; ti < t1 - t0; ++ti, ++L) {
-        const int t = p.forward ? t0 + ti : t1 - 1 - ti;
+      for (int t = t1 - 1; t >= t0; --t, ++L) {
         const int s = L % STAGES;
-        wait_bar(p.wait_mode & 1, full_bar(s), (L / STAGES) & 1);
+        ptx::mbar_wait_sleep(full_bar(s), (L / STAGES) & 1);
         ptx::tc_fence_after();
         const uint32_t b_addr = ptx::smem_u32(sStage + s * kStage);
         const uint64_t bd0 = ptx::umma_desc(b_addr, kTileN * 16, 128);
         for (int r = 0; r < RG; ++r, ++H) {
           const uint64_t ad0 = ptx::umma_desc(a_base + r * (kTileM * KPAD), kTileM * 16, 128);
           const int acc = H % kNumAcc;
-          wait_bar(p.wait_mode & 1, tempty_bar(acc), ((H / kNumAcc) & 1) ^ 1);
+          ptx::mbar_wait_sleep(tempty_bar(acc), ((H / kNumAcc) & 1) ^ 1);
           ptx::tc_fence_after();
           const uint32_t d = tmem_base + acc * kAccN;
-          if (p.debug_mode < 2) {
-            ptx::umma_i8_elect(d, ad0, bd0, kIdesc, 0u);
-            for (int ks = 1; ks < ksteps; ++ks)
-              ptx::umma_i8_elect(d, ad0 + ks * kAStep, bd0 + ks * kBStep, kIdesc, 1u);
-          }
+          ptx::umma_i8_elect(d, ad0, bd0, kIdesc, 0u);
+          for (int ks = 1; ks < ksteps; ++ks)
+            ptx::umma_i8_elect(d, ad0 + ks * kAStep, bd0 + ks * kBStep, kIdesc, 1u);
           ptx::umma_commit_elect(tfull_bar(acc));
         }
         ptx::umma_commit_elect(empty_bar(s));
@@ -264,38 +257,41 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     const int S = p.S;
     const int iso = lane & 7;
     const uint32_t tbase = tmem_base + ((uint32_t)(sp * 32) << 16) + cq * 64;
+    // this thread's {best2, loc} per resident row tile, stride = 512 threads
+    int2* bstate = reinterpret_cast<int2*>(smem + best_offset(p)) + (e * 32 + lane);
+    constexpr int kBS = kEpiWarps * 32;
+    // loop-invariant barrier / TMEM addresses; accumulator H & 1, phase (H >> 1) & 1
+    const uint32_t tfull0 = tfull_bar(0), tfull1 = tfull_bar(1);
+    const uint32_t tempty0 = tempty_bar(0), tempty1 = tempty_bar(1);
+    const uint32_t tm0 = tbase, tm1 = tbase + kAccN;
     const int slot_q = cq * 64;
-    uint32_t L = 0, H = 0;
+    uint32_t H = 0;
+    int stg = 0;
+    uint32_t stg_phase = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      const int g = (int)(u % n_rg);
+      const int g = u % n_rg;
       const int t0 = (u / n_rg) * CT;
       const int t1 = min(p.ntiles, t0 + CT);
-      // running best per (row tile): key2 and column
-      int best2[kMaxRG], bcol[kMaxRG];
-#pragma unroll
-      for (int r = 0; r < kMaxRG; ++r) {
-        best2[r] = kNone;
-        bcol[r] = 0;
-      }
-      for (int ti = 0; ti < t1 - t0; ++ti, ++L) {
-        const int t = p.forward ? t0 + ti : t1 - 1 - ti;
-        const int s = L % STAGES;
+      for (int r = 0; r < RG; ++r) bstate[r * kBS] = make_int2(kNone, 0);
+      // tiles in DECREASING order (see improve_limit)
+      for (int t = t1 - 1; t >= t0; --t) {
         const int2 tinfo = p.tile_info[t];  // {parity, valid slots}
-        wait_bar(p.wait_mode & 2, full_bar(s), (L / STAGES) & 1);
-        const int32_t* colmap_s = reinterpret_cast<const int32_t*>(sStage + s * kStage + kB);
+        ptx::mbar_wait_sleep(full_bar(stg), stg_phase);
 #pragma unroll 1
         for (int r = 0; r < RG; ++r, ++H) {
-          const int acc = H % kNumAcc;
-          wait_bar(p.wait_mode & 2, tfull_bar(acc), (H / kNumAcc) & 1);
+          const int2 bs = bstate[r * kBS];  // issued before the waits: latency hidden
+          const bool a1 = H & 1;
+          ptx::mbar_wait_sleep(a1 ? tfull1 : tfull0, (H >> 1) & 1);
           ptx::tc_fence_after();
           int va[32], vb[32];
-          ptx::tmem_ld32(tbase + acc * kAccN, va);
-          ptx::tmem_ld32(tbase + acc * kAccN + 32, vb);
+          const uint32_t tm = a1 ? tm1 : tm0;
+          ptx::tmem_ld32(tm, va);
+          ptx::tmem_ld32(tm + 32, vb);
           ptx::tmem_wait_ld();
           // all of this warp's values are in registers: release the accumulator
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
+          if (lane == 0) ptx::mbar_arrive(a1 ? tempty1 : tempty0);
           if (tinfo.y < kTileN) {  // mask padding slots (last tile of a group)
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -304,26 +300,81 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
             }
           }
           if (p.debug_mode & 1) continue;
-          const int ma = min32(va), mb = min32(vb);
-          const int lim = p.forward ? strict_limit(best2[r], tinfo.x) : improve_limit(best2[r], tinfo.x);
-          if (min(ma, mb) < lim) {  // rare: this row improves (or ties earlier) in these 64 columns
-            const bool in_a = ma <= mb;
-            const int m = in_a ? ma : mb;
+          int gm[8];
+          gm[0] = min8<0>(va);
+          gm[1] = min8<8>(va);
+          gm[2] = min8<16>(va);
+          gm[3] = min8<24>(va);
+          gm[4] = min8<0>(vb);
+          gm[5] = min8<8>(vb);
+          gm[6] = min8<16>(vb);
+          gm[7] = min8<24>(vb);
+          const int m = min(__vimin3_s32(gm[0], gm[1], gm[2]),
+                            __vimin3_s32(__vimin3_s32(gm[3], gm[4], gm[5]), gm[6], gm[7]));
+          const int lim = improve_limit(bs.x, tinfo.x);
+          if (p.deferred) {
+            // branch-free: record the 8-column group, resolve at the unit end
+            int gi = 7;
+#pragma unroll
+            for (int k = 6; k >= 0; --k) gi = (gm[k] == m) ? k : gi;
+            if (m < lim) bstate[r * kBS] = make_int2(2 * m + tinfo.x, t * 8 + gi);
+          } else if (m < lim) {
+            // long K: the per-unit recompute would cost more than resolving now
+            const bool in_a = min(min(gm[0], gm[1]), min(gm[2], gm[3])) == m;
             const int j = in_a ? first_eq(va, m) : 32 + first_eq(vb, m);
-            best2[r] = 2 * m + tinfo.x;
-            bcol[r] = colmap_s[slot_q + j];
+            const int32_t* colmap_s = reinterpret_cast<const int32_t*>(sStage + stg * kStage + kB);
+            bstate[r * kBS] = make_int2(2 * m + tinfo.x, colmap_s[slot_q + j]);
           }
         }
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(empty_bar(s));
+        if (lane == 0) ptx::mbar_arrive(empty_bar(stg));
+        if (++stg == STAGES) {
+          stg = 0;
+          stg_phase ^= 1;
+        }
       }
+      // resolve each row's winning 8-column group: recompute its dot products
+      // from the global copies of A and B (the shared A slot is already being
+      // refilled for the next unit) and take the first column whose value
+      // equals the recorded minimum
+      const int chunks = KPAD / 16;
 #pragma unroll 1
       for (int r = 0; r < RG; ++r) {
         unsigned long long key = ~0ull;
+        const int2 bs = bstate[r * kBS];
         const int4 rm = p.row_meta[(size_t)(g * RG + r) * kTileM + row];  // {o, R, m, -}
-        if (best2[r] != kNone && rm.z >= 0) {
-          const long long err = (long long)best2[r] + rm.y;
-          const int col = bcol[r];
+        if (bs.x != kNone && rm.z >= 0 && !(p.debug_mode & 1) && !p.deferred) {
+          const long long err = (long long)bs.x + rm.y;
+          const int col = bs.y;
+          const int e_idx = col / S, si = col - e_idx * S;
+          key = ((unsigned long long)err << 32) | (unsigned long long)((e_idx * 8 + iso) * S + si);
+        } else if (bs.x != kNone && rm.z >= 0 && !(p.debug_mode & 1)) {
+          const int t = bs.y >> 3, gi = bs.y & 7;
+          const int par = p.tile_info[t].x;
+          const int m = (int)(((long long)bs.x - par) >> 1);
+          const int slot0 = cq * 64 + gi * 8;
+          const uint8_t* arow = p.a_tiles + (size_t)(g * RG + r) * (kTileM * KPAD) +
+                                (row >> 3) * 128 + (row & 7) * 16;
+          const int8_t* bgrp = p.b_tiles + (size_t)t * kB + (slot0 >> 3) * 128;
+          int kh[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 1
+          for (int kc = 0; kc < chunks; ++kc) {
+            const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(arow + kc * (kTileM * 16)));
+            const int8_t* bk = bgrp + kc * (kTileN * 16);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint4 b4 = __ldg(reinterpret_cast<const uint4*>(bk + j * 16));
+              kh[j] = dp4a_us(a4.x, b4.x, kh[j]);
+              kh[j] = dp4a_us(a4.y, b4.y, kh[j]);
+              kh[j] = dp4a_us(a4.z, b4.z, kh[j]);
+              kh[j] = dp4a_us(a4.w, b4.w, kh[j]);
+            }
+          }
+          int jj = 7;
+#pragma unroll
+          for (int j = 6; j >= 0; --j) jj = (kh[j] == m) ? j : jj;
+          const int col = p.colmap[(size_t)t * kTileN + slot0 + jj];
+          const long long err = (long long)bs.x + rm.y;
           const int e_idx = col / S, si = col - e_idx * S;
           key = ((unsigned long long)err << 32) | (unsigned long long)((e_idx * 8 + iso) * S + si);
         }
@@ -676,6 +727,9 @@ int level_prepare_tc_finish(Ctx* c, Level& L) {
   const int hq_max = (int)(q2max >> 1);
   T.m_digits = std::max(1, (hq_max / 255 + 126) / 127);
   T.kpad = ((T.planes * L.n + T.m_digits + 4 + 31) / 32) * 32;
+  if (c->trace)
+    fprintf(stderr, "[fc_trace] tc operands B=%d cols=%lld planes=%d m_digits=%d kpad=%d\n", L.side,
+            (long long)ncols, T.planes, T.m_digits, T.kpad);
   // clamp-reach counts: low_count[o] = #{qmin < -o}, high_count[o] = #{qmax > 255 - o}
   {
     // prefix sums over the histograms (bin v holds q = v - 512)
@@ -799,8 +853,8 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   prm.ntiles = (int)T.ntiles;
   prm.plan = d_plan;
   if (const char* dbg = getenv("FC_TC_DEBUG_MODE")) prm.debug_mode = atoi(dbg);
-  prm.wait_mode = c->tc_wait_mode;
-  prm.forward = c->tc_forward;
+  prm.deferred = T.kpad <= 64 ? 1 : 0;  // measured: recompute wins only for short K
+  if (const char* d = getenv("FC_TC_DEFERRED")) prm.deferred = atoi(d);
   const uint32_t smem = smem_bytes(prm);
   if (!c->tc_attr_set) {
     FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
