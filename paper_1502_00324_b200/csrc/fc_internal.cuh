@@ -15,6 +15,9 @@ constexpr int kLevels = 4;
 constexpr int kRangeSide[kLevels] = {16, 8, 4, 2};   // pool.py:20 LEVEL_RANGE_SIDES
 constexpr int kDomainSide[kLevels] = {32, 16, 8, 4}; // pool.py:21 LEVEL_DOMAIN_SIDES
 constexpr int kMaxS = 16;
+// exact CUDA-core kernel: ranges per 128-column block (fewer for long ranges
+// so small correction sets still spread over the SMs)
+__host__ __device__ constexpr int ranges_per_block(int n) { return n >= 256 ? 2 : n >= 64 ? 4 : 8; }
 constexpr int kTcHistWords = 1024 + 1024 + 4;  // qmin | qmax histograms, q2max, pad
 
 struct Status {

@@ -25,7 +25,7 @@ namespace fcb {
 
 namespace {
 
-constexpr int kRB = 8;          // ranges per block
+constexpr int kRB = 8;          // ranges per block (drop-in row kernel)
 constexpr int kColsPerBlock = 128;
 
 __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
@@ -46,13 +46,17 @@ __device__ __forceinline__ int rint_offset_baseline(double rmean, double s, doub
 
 template <int N>
 struct ExactSmem {
-  uint8_t rperm[kRB][8][N];
-  int m[kRB];
-  double rmean[kRB];
+  static constexpr int RB = ranges_per_block(N);
+  uint8_t rperm[RB][8][N];
+  int m[RB];
+  double rmean[RB];
 };
 
-// One block: kRB ranges (s.m[], -1 = none) x 128 columns (one per thread,
-// col < 0 = none).  Every (range, column, isometry) error is exact.
+// One block: RB ranges (s.m[], -1 = none) x 128 columns (one per thread,
+// col < 0 = none).  Every (range, column, isometry) error is exact.  The
+// reduction packs (err << 3 | iso) so one 3-input min tree yields the
+// first-isometry minimum per thread; the warp then takes the minimum error
+// and, among the lanes holding it, the minimum candidate index (REDUX).
 template <int N>
 __device__ __forceinline__ void exact_block(ExactSmem<N>& s, const int16_t* __restrict__ qbase,
                                             int S, const double* __restrict__ svals,
@@ -60,11 +64,12 @@ __device__ __forceinline__ void exact_block(ExactSmem<N>& s, const int16_t* __re
                                             const uint8_t* __restrict__ rtiles,
                                             const uint16_t* __restrict__ inv, int64_t col_in,
                                             int baseline, unsigned long long* __restrict__ keys) {
+  constexpr int RB = ExactSmem<N>::RB;
   constexpr int CH = N >= 16 ? 16 : N;  // pixels per inner chunk
   constexpr int W = CH / 4;             // packed words per chunk
   auto& rperm = s.rperm;
   const int tid = threadIdx.x;
-  for (int i = tid; i < kRB * 8 * N; i += kColsPerBlock) {
+  for (int i = tid; i < RB * 8 * N; i += kColsPerBlock) {
     const int mm = i / (8 * N);
     const int rem = i - mm * 8 * N;
     const int iso = rem / N, j = rem - iso * N;
@@ -78,15 +83,15 @@ __device__ __forceinline__ void exact_block(ExactSmem<N>& s, const int16_t* __re
   const int64_t e = col / S;
   const int si = (int)(col - e * S);
 
-  int o[kRB];
+  int o[RB];
 #pragma unroll
-  for (int mm = 0; mm < kRB; ++mm) {
+  for (int mm = 0; mm < RB; ++mm) {
     o[mm] = baseline ? rint_offset_baseline(s.rmean[mm], svals[si], dmean[e])
                      : (int)rint(s.rmean[mm]);
   }
-  unsigned acc[kRB][8];
+  unsigned acc[RB][8];
 #pragma unroll
-  for (int mm = 0; mm < kRB; ++mm)
+  for (int mm = 0; mm < RB; ++mm)
 #pragma unroll
     for (int iso = 0; iso < 8; ++iso) acc[mm][iso] = 0u;
 
@@ -104,7 +109,7 @@ __device__ __forceinline__ void exact_block(ExactSmem<N>& s, const int16_t* __re
       qw[0] = a.x; qw[1] = a.y;
     }
 #pragma unroll
-    for (int mm = 0; mm < kRB; ++mm) {
+    for (int mm = 0; mm < RB; ++mm) {
       const unsigned o2 = (unsigned)o[mm] | ((unsigned)o[mm] << 16);
       unsigned x4[W];
 #pragma unroll
@@ -134,18 +139,19 @@ __device__ __forceinline__ void exact_block(ExactSmem<N>& s, const int16_t* __re
   }
   const int lane = tid & 31;
 #pragma unroll
-  for (int mm = 0; mm < kRB; ++mm) {
-    unsigned long long best = ~0ull;
-    if (valid) {
-#pragma unroll
-      for (int iso = 0; iso < 8; ++iso) {
-        const unsigned long long cidx = (unsigned long long)((e * 8 + iso) * S + si);
-        const unsigned long long key = ((unsigned long long)acc[mm][iso] << 32) | cidx;
-        best = key < best ? key : best;
-      }
-    }
-    best = warp_min_u64(best);
-    if (lane == 0 && s.m[mm] >= 0 && best != ~0ull) atomicMin(&keys[s.m[mm]], best);
+  for (int mm = 0; mm < RB; ++mm) {
+    // err <= 256 * 255^2 < 2^24, so (err << 3 | iso) fits 27 bits
+    const unsigned k01 = min(acc[mm][0] << 3, (acc[mm][1] << 3) | 1u);
+    const unsigned k = __vimin3_u32(__vimin3_u32(k01, (acc[mm][2] << 3) | 2u, (acc[mm][3] << 3) | 3u),
+                                    __vimin3_u32((acc[mm][4] << 3) | 4u, (acc[mm][5] << 3) | 5u,
+                                                 (acc[mm][6] << 3) | 6u),
+                                    (acc[mm][7] << 3) | 7u);
+    const unsigned err = valid ? (k >> 3) : 0xffffffffu;
+    const unsigned cidx = (unsigned)((e * 8 + (k & 7)) * S + si);
+    const unsigned werr = __reduce_min_sync(0xffffffffu, err);
+    const unsigned wcidx = __reduce_min_sync(0xffffffffu, err == werr ? cidx : 0xffffffffu);
+    if (lane == 0 && s.m[mm] >= 0 && werr != 0xffffffffu)
+      atomicMin(&keys[s.m[mm]], ((unsigned long long)werr << 32) | wcidx);
   }
 }
 
@@ -161,12 +167,13 @@ scan_exact_kernel(const int16_t* __restrict__ qbase, int64_t ncols, int S,
                   const int32_t* __restrict__ col_list, int64_t n_col_list, int baseline,
                   unsigned long long* __restrict__ keys) {
   __shared__ __align__(16) ExactSmem<N> s;
+  constexpr int RB = ExactSmem<N>::RB;
   const int tid = threadIdx.x;
   if (d_M) M = *d_M;
   const int64_t nrange = range_list ? n_range_list : M;
-  const int64_t r0 = range_base + (int64_t)blockIdx.y * kRB;
+  const int64_t r0 = range_base + (int64_t)blockIdx.y * RB;
   if (r0 >= nrange) return;  // block-uniform (device range count below the launch bound)
-  if (tid < kRB) {
+  if (tid < RB) {
     const int64_t idx = r0 + tid;
     int m = -1;
     if (idx < nrange) m = range_list ? range_list[idx] : (int)idx;
@@ -215,8 +222,8 @@ scan_jobs_kernel(const int16_t* __restrict__ qbase, int S, const double* __restr
     const int64_t local = b - prefix[s_job];
     const int64_t ncc = (job.w + kColsPerBlock - 1) / kColsPerBlock;
     const int64_t rb = local / ncc, cc = local - rb * ncc;
-    if (tid < kRB) {
-      const int64_t idx = rb * kRB + tid;
+    if (tid < ExactSmem<N>::RB) {
+      const int64_t idx = rb * ExactSmem<N>::RB + tid;
       const int m = idx < job.z ? sorted_ranges[job.y + idx] : -1;
       s.m[tid] = m;
       s.rmean[tid] = m >= 0 ? rmean[m] : 0.0;
@@ -579,10 +586,11 @@ int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t
   const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
   auto* keys = reinterpret_cast<unsigned long long*>(d_keys);
   const unsigned gx = (unsigned)((nc + kColsPerBlock - 1) / kColsPerBlock);
-  const int64_t slab = 65535LL * kRB;
+  const int RB = ranges_per_block(L.n);
+  const int64_t slab = 65535LL * RB;
   for (int64_t base = 0; base < nr; base += slab) {
     const int64_t cnt = std::min<int64_t>(slab, nr - base);
-    dim3 grid(gx, (unsigned)((cnt + kRB - 1) / kRB));
+    dim3 grid(gx, (unsigned)((cnt + RB - 1) / RB));
     const int64_t nlist = d_range_list ? n_range_list : M;
 #define FC_LAUNCH_EXACT(NN)                                                                     \
     scan_exact_kernel<NN><<<grid, kColsPerBlock, 0, c->stream>>>(                               \

@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(256) tc_plan_kernel(const int32_t* __restrict_
 
 // Clamp-correction jobs from the offset histogram (one block, thread = o):
 // ranges with offset o against the columns whose qmin < -o (list 0) or
-// qmax > 255 - o (list 1); blocks of 8 ranges x 128 columns.
+// qmax > 255 - o (list 1); blocks of RB ranges x 128 columns.
 struct FixPlan {
   int n_jobs;
   int pad;
@@ -619,6 +619,7 @@ struct FixPlan {
 };
 __global__ void __launch_bounds__(256) fix_plan_kernel(const int32_t* __restrict__ hist,
                                                        const long long* __restrict__ reach_counts,
+                                                       int RB,
                                                        int4* __restrict__ jobs,
                                                        long long* __restrict__ prefix,
                                                        int32_t* __restrict__ cursors,
@@ -642,7 +643,7 @@ __global__ void __launch_bounds__(256) fix_plan_kernel(const int32_t* __restrict
   for (int k = 0; k < 2; ++k)
     if (cnt && lists[k]) {
       ++njob;
-      blocks += (long long)((cnt + 7) / 8) * ((lists[k] + 127) / 128);
+      blocks += (long long)((cnt + RB - 1) / RB) * ((lists[k] + 127) / 128);
       pairs += (long long)cnt * lists[k];
     }
   __syncthreads();
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(256) fix_plan_kernel(const int32_t* __restrict
     if (cnt && lists[k]) {
       jobs[j] = make_int4(k, s_start[o], cnt, (int)lists[k]);
       prefix[j] = b;
-      b += (long long)((cnt + 7) / 8) * ((lists[k] + 127) / 128);
+      b += (long long)((cnt + RB - 1) / RB) * ((lists[k] + 127) / 128);
       ++j;
     }
   if (o == 255) {
@@ -873,6 +874,7 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   FC_CUDA(c, c->tc_scratch.reserve(256 * 4));
   int32_t* d_cursor = c->tc_scratch.as<int32_t>();
   fix_plan_kernel<<<1, 256, 0, c->stream>>>(d_hist, T.reach_counts.as<long long>(),
+                                            ranges_per_block(L.n),
                                             c->fix_jobs.as<int4>(), c->fix_cols.as<long long>(),
                                             d_cursor, d_fplan);
   order_scatter_kernel<<<(unsigned)((M_bound + 255) / 256), 256, 0, c->stream>>>(
