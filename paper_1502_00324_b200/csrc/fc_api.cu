@@ -215,7 +215,7 @@ void fc_ctx_destroy(fc_ctx* c) {
                     &c->fix_prefix, &c->tc_scratch, &c->enc_orig[0], &c->enc_orig[1],
                     &c->enc_code[0], &c->enc_code[1], &c->enc_flag, &c->enc_pfx,
                     &c->enc_count, &c->enc_hist, &c->leaf_flag, &c->leaf_pos, &c->leaf_rec,
-                    &c->rec_out, &c->tc_plan, &c->enc_fix};
+                    &c->rec_out, &c->tc_plan, &c->enc_fix, &c->pool_rank};
   for (DevBuf* b : bufs) b->release();
   c->up_arena.release();
   c->readback.release();

@@ -148,7 +148,7 @@ struct Ctx {
   DevBuf ent_scratch, key_in, key_out, val_in, val_out, cub_tmp, count_buf;
   DevBuf origins, rtiles, rmean, roff, rsq, keys, out_err, out_idx;
   DevBuf fix_rows, fix_cols, fix_jobs, svals_dev;
-  DevBuf a_tiles, row_meta, fix_prefix, tc_scratch, tc_plan;
+  DevBuf a_tiles, row_meta, fix_prefix, tc_scratch, tc_plan, pool_rank;
   std::vector<int32_t> h_roff;
   // pinned staging: uploads go through an arena that is recycled at every
   // full stream synchronisation (stage_h2d / sync_stream)

@@ -14,8 +14,9 @@
 //     raster index (np.argsort(-ent, kind="stable"), pool.py:171):
 //     threshold survivors: chunk bitonic sort + cross-chunk rank (2 launches
 //     for all levels); general caps: CUB stable radix sort; cap 1: argmin.
-//  3. survivor_kernel  : one warp per kept window: floor 2x2 decimation,
-//     exact sum / sum of squares, mean, centered norm (pool.py:138-152).
+//  3. survivors_all_kernel (one launch, all levels): a thread per decimated
+//     pixel (floor 2x2 mean), segmented reductions for the exact sum / sum of
+//     squares, mean and centred norm per survivor (pool.py:138-152).
 #include <cub/cub.cuh>
 
 #include "fc_internal.cuh"
@@ -271,91 +272,136 @@ __global__ void __launch_bounds__(1024) chunk_sort_kernel(SortParams P) {
   }
 }
 
-// Global rank of every element = its chunk position + the number of smaller
-// elements in each other chunk (binary search over chunks staged in smem).
-__global__ void __launch_bounds__(1024) chunk_rank_kernel(SortParams P) {
+// Global rank = position in the own sorted chunk + number of smaller elements
+// in every other chunk: one block per (chunk a, chunk b) pair stages chunk b
+// in shared memory and adds, for each element of a, its lower bound in b.
+struct RankLevel {
+  int nch;          // chunks of this level
+  int pair_begin;   // first (a, b) pair block of this level
+};
+__global__ void __launch_bounds__(1024) chunk_pair_rank_kernel(SortParams P, RankLevel R0,
+                                                               RankLevel R1, RankLevel R2,
+                                                               RankLevel R3,
+                                                               int32_t* __restrict__ rank_all) {
   __shared__ uint64_t sk[kChunk];
   __shared__ uint32_t si[kChunk];
-  const int l = sort_level_of(P, blockIdx.x);
+  const RankLevel RL[4] = {R0, R1, R2, R3};
+  int l = 0;
+  for (int k = 1; k < P.n_levels; ++k)
+    if ((int)blockIdx.x >= RL[k].pair_begin) l = k;
   const SortLevel& L = P.lv[l];
-  const int c = blockIdx.x - L.chunk_begin;
-  const int nch = (L.count + kChunk - 1) / kChunk;
-  const int base = c * kChunk;
-  const int n = min(kChunk, L.count - base);
-  uint64_t mk[2];
-  uint32_t mi[2];
-  int rank[2];
-  for (int e = 0; e < 2; ++e) {
-    const int p = threadIdx.x + e * 1024;
-    mk[e] = p < n ? L.key[base + p] : ~0ull;
-    mi[e] = p < n ? L.val[base + p] : 0xffffffffu;
-    rank[e] = p;
+  const int pr = blockIdx.x - RL[l].pair_begin;
+  const int ca = pr / RL[l].nch, cb = pr - ca * RL[l].nch;
+  const int na = min(kChunk, L.count - ca * kChunk);
+  const int nb = min(kChunk, L.count - cb * kChunk);
+  int32_t* rank = rank_all + L.chunk_begin * kChunk;  // this level's rank slots
+  if (ca == cb) {
+    for (int p = threadIdx.x; p < na; p += blockDim.x) atomicAdd(&rank[ca * kChunk + p], p);
+    return;
   }
-  for (int b = 0; b < nch; ++b) {
-    if (b == c) continue;
-    const int bb = b * kChunk;
-    const int nb = min(kChunk, L.count - bb);
-    __syncthreads();
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
-      sk[i] = L.key[bb + i];
-      si[i] = L.val[bb + i];
-    }
-    __syncthreads();
-    for (int e = 0; e < 2; ++e) {
-      int lo = 0, hi = nb;  // first index with element >= mine
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (lex_less(sk[mid], si[mid], mk[e], mi[e])) lo = mid + 1; else hi = mid;
-      }
-      rank[e] += lo;
-    }
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    sk[i] = L.key[cb * kChunk + i];
+    si[i] = L.val[cb * kChunk + i];
   }
-  for (int e = 0; e < 2; ++e) {
-    const int p = threadIdx.x + e * 1024;
-    if (p < n) L.out[rank[e]] = mi[e];
+  __syncthreads();
+  for (int p = threadIdx.x; p < na; p += blockDim.x) {
+    const uint64_t k = L.key[ca * kChunk + p];
+    const uint32_t v = L.val[ca * kChunk + p];
+    int lo = 0, hi = nb;  // first element of b that is >= (k, v)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (lex_less(sk[mid], si[mid], k, v)) lo = mid + 1; else hi = mid;
+    }
+    if (lo) atomicAdd(&rank[ca * kChunk + p], lo);
   }
 }
 
-// One warp per survivor: decimate, moments, coordinates.
-__global__ void survivor_kernel(const uint8_t* __restrict__ img, int width, int nx, int stride,
-                                int D, const uint32_t* __restrict__ order,
-                                const double* __restrict__ ent_all, int64_t count,
-                                uint32_t* __restrict__ xy, double* __restrict__ ent,
-                                uint8_t* __restrict__ tiles, int32_t* __restrict__ sum,
-                                int64_t* __restrict__ sumsq, double* __restrict__ mean,
-                                double* __restrict__ cnorm) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= count) return;
-  const uint32_t w = order[warp];
-  const int wy = w / nx, wx = w - wy * nx;
-  const int x0 = wx * stride, y0 = wy * stride;
-  const int B = D / 2, n = B * B;
-  const uint8_t* base = img + (int64_t)y0 * width + x0;
-  uint8_t* out = tiles + (int64_t)warp * n;
-  int s1 = 0;
-  long long s2 = 0;
-  for (int p = lane; p < n; p += 32) {
-    const int r = p / B, c = p - r * B;
-    const uint8_t* q = base + (int64_t)(2 * r) * width + 2 * c;
-    const int v = (q[0] + q[1] + q[width] + q[width + 1]) >> 2;  // floor mean, image.py:125-130
-    out[p] = static_cast<uint8_t>(v);
-    s1 += v;
-    s2 += v * v;
-  }
+__global__ void rank_scatter_kernel(SortParams P, const int32_t* __restrict__ rank_all) {
+  const int l = sort_level_of(P, blockIdx.x / (kChunk / 256));
+  const SortLevel& L = P.lv[l];
+  const int64_t i = (int64_t)(blockIdx.x - L.chunk_begin * (kChunk / 256)) * 256 + threadIdx.x;
+  if (i >= L.count) return;
+  L.out[rank_all[L.chunk_begin * kChunk + i]] = L.val[i];
+}
+
+// Survivors of all levels in one launch, one thread per decimated pixel
+// (floor 2x2 mean, image.py:125-130), then per survivor: coordinates, entropy,
+// exact sum / sum of squares, mean and centred norm (pool.py:138-152).
+struct SurvLevel {
+  const uint32_t* order;
+  const double* ent_all;
+  int64_t count;
+  int B, lb, nx, stride;  // range side B = 1 << lb
+  int64_t block_begin;
+  uint32_t* xy;
+  double* ent;
+  uint8_t* tiles;
+  int32_t* sum;
+  int64_t* sumsq;
+  double* mean;
+  double* cnorm;
+};
+struct SurvParams {
+  SurvLevel lv[4];
+};
+
+__global__ void __launch_bounds__(256) survivors_all_kernel(const uint8_t* __restrict__ img,
+                                                            int width, SurvParams P) {
+  __shared__ int ps1[256], ps2[256];
+  int l = 0;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
+  for (int k = 1; k < 4; ++k)
+    if ((int64_t)blockIdx.x >= P.lv[k].block_begin) l = k;
+  const SurvLevel& L = P.lv[l];
+  const int lb = L.lb, B = 1 << lb, n = 1 << (2 * lb);
+  const int64_t idx = ((int64_t)blockIdx.x - L.block_begin) * 256 + threadIdx.x;
+  const int64_t sv = idx >> (2 * lb);
+  const int p = (int)(idx & (n - 1));
+  const bool valid = sv < L.count;
+  int v = 0;
+  uint32_t w = 0;
+  if (valid) {
+    w = __ldg(L.order + sv);
+    const int wy = w / L.nx, wx = w - wy * L.nx;
+    const int x0 = wx * L.stride, y0 = wy * L.stride;
+    const int r = p >> lb, cc = p & (B - 1);
+    const uint8_t* q = img + (int64_t)(y0 + 2 * r) * width + x0 + 2 * cc;
+    v = (q[0] + q[1] + q[width] + q[width + 1]) >> 2;
+    L.tiles[sv * n + p] = (uint8_t)v;
+  }
+  // segmented reduction: groups of min(n, 32) lanes, then per-survivor partials
+  int s1 = v, s2 = v * v;
+  const int width_r = n < 32 ? n : 32;
+  for (int o = width_r >> 1; o; o >>= 1) {
     s1 += __shfl_xor_sync(0xffffffffu, s1, o);
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
   }
-  if (lane == 0) {
-    xy[warp] = static_cast<uint32_t>(x0) | (static_cast<uint32_t>(y0) << 16);
-    ent[warp] = ent_all[w];
-    sum[warp] = s1;
-    sumsq[warp] = s2;
-    // mean = s1 / n; cnorm = s2 - s1*s1/n with Python float semantics (pool.py:144-151)
-    mean[warp] = __ddiv_rn((double)s1, (double)n);
-    cnorm[warp] = __dsub_rn((double)s2, __ddiv_rn((double)((long long)s1 * s1), (double)n));
+  const int part = threadIdx.x / width_r;
+  if ((threadIdx.x & (width_r - 1)) == 0) {
+    ps1[part] = s1;
+    ps2[part] = s2;
+  }
+  __syncthreads();
+  const int per = n / width_r;  // partials per survivor
+  const int spb = 256 / n;      // survivors per block (n <= 256)
+  if ((int)threadIdx.x < (spb > 0 ? spb : 1)) {
+    const int64_t s_here = ((int64_t)blockIdx.x - L.block_begin) * 256 / n + threadIdx.x;
+    if (s_here < L.count) {
+      int t1 = 0, t2 = 0;
+      for (int k = 0; k < per; ++k) {
+        t1 += ps1[threadIdx.x * per + k];
+        t2 += ps2[threadIdx.x * per + k];
+      }
+      const uint32_t ww = L.order[s_here];
+      const int wy = ww / L.nx, wx = ww - wy * L.nx;
+      L.xy[s_here] = (uint32_t)(wx * L.stride) | ((uint32_t)(wy * L.stride) << 16);
+      L.ent[s_here] = L.ent_all[ww];
+      L.sum[s_here] = t1;
+      L.sumsq[s_here] = t2;
+      // mean = s1 / n; cnorm = s2 - s1*s1/n with Python float semantics (pool.py:144-151)
+      L.mean[s_here] = __ddiv_rn((double)t1, (double)n);
+      L.cnorm[s_here] = __dsub_rn((double)t2, __ddiv_rn((double)((long long)t1 * t1), (double)n));
+    }
   }
 }
 
@@ -631,30 +677,53 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     }
     SP.total_chunks = chunks;
     if (chunks > 0) {
+      RankLevel RL[4] = {};
+      int pairs = 0;
+      for (int k = 0; k < SP.n_levels; ++k) {
+        RL[k].nch = (SP.lv[k].count + kChunk - 1) / kChunk;
+        RL[k].pair_begin = pairs;
+        pairs += RL[k].nch * RL[k].nch;
+      }
+      for (int k = SP.n_levels; k < 4; ++k) RL[k].pair_begin = 1 << 30;
+      FC_CUDA(c, c->pool_rank.reserve((size_t)chunks * kChunk * 4));
+      FC_CUDA(c, cudaMemsetAsync(c->pool_rank.ptr, 0, (size_t)chunks * kChunk * 4, c->stream));
       chunk_sort_kernel<<<chunks, 1024, 0, c->stream>>>(SP);
-      chunk_rank_kernel<<<chunks, 1024, 0, c->stream>>>(SP);
+      chunk_pair_rank_kernel<<<pairs, 1024, 0, c->stream>>>(SP, RL[0], RL[1], RL[2], RL[3],
+                                                            c->pool_rank.as<int32_t>());
+      rank_scatter_kernel<<<chunks * (kChunk / 256), 256, 0, c->stream>>>(SP,
+                                                                        c->pool_rank.as<int32_t>());
       FC_CUDA(c, cudaGetLastError());
-      c->total_launches += 2;
+      c->total_launches += 3;
     }
   }
+  SurvParams SV{};
+  int64_t sblocks = 0;
   for (int li = 0; li < kLevels; ++li) {
     Level& L = c->lv[li];
-    const int D = kDomainSide[li];
-    const int nx = nx_l[li];
-    const uint32_t* order = L.win_val2.as<uint32_t>();
-    FC_CUDA(c, cudaGetLastError());
     const int64_t E = L.count;
     FC_TRY(alloc_level(c, L, E));
-    const int threads = 256;
-    const int64_t grid = (E * 32 + threads - 1) / threads;
-    survivor_kernel<<<(unsigned)grid, threads, 0, c->stream>>>(
-        c->img_ptr, c->width, nx, L.stride, D, order, L.win_ent.as<double>(), E,
-        L.xy.as<uint32_t>(), L.ent.as<double>(), L.tiles.as<uint8_t>(), L.sum.as<int32_t>(),
-        L.sumsq.as<int64_t>(), L.mean.as<double>(), L.cnorm.as<double>());
-    FC_CUDA(c, cudaGetLastError());
-    c->total_launches += 1;
+    SurvLevel& V = SV.lv[li];
+    V.order = L.win_val2.as<uint32_t>();
+    V.ent_all = L.win_ent.as<double>();
+    V.count = E;
+    V.B = L.side;
+    V.lb = L.side == 16 ? 4 : L.side == 8 ? 3 : L.side == 4 ? 2 : 1;
+    V.nx = nx_l[li];
+    V.stride = L.stride;
+    V.block_begin = sblocks;
+    V.xy = L.xy.as<uint32_t>();
+    V.ent = L.ent.as<double>();
+    V.tiles = L.tiles.as<uint8_t>();
+    V.sum = L.sum.as<int32_t>();
+    V.sumsq = L.sumsq.as<int64_t>();
+    V.mean = L.mean.as<double>();
+    V.cnorm = L.cnorm.as<double>();
+    sblocks += (E * L.n + 255) / 256;
     out_sizes[li] = E;
   }
+  survivors_all_kernel<<<(unsigned)sblocks, 256, 0, c->stream>>>(c->img_ptr, c->width, SV);
+  FC_CUDA(c, cudaGetLastError());
+  c->total_launches += 1;
   trace_mark(c, "pool_launched");
   return FC_OK;
 }
