@@ -9,10 +9,10 @@
 // are all produced on the device:
 //
 //   classify_kernel : err = key >> 32; split = err > t^2 * B^2 (levels 1-3);
+//                     split ranges append their four children (origins and
+//                     codes) to the next level with warp-aggregated atomics;
 //                     leaves write their record into a slot indexed by the
 //                     depth-first code top*64 + d1*16 + d2*4 + d3;
-//   ExclusiveSum    : split flags -> child base (parent order is kept);
-//   children_kernel : four child origins (TL, TR, BL, BR) and codes;
 //   gather (next)   : range tiles, moments and the offset histogram.
 //
 // After level 4 the code-indexed records are compacted in code order, which
@@ -47,27 +47,53 @@ __device__ __forceinline__ int baseline_offset(double rmean, double s, double dm
   return o < 0 ? 0 : (o > 255 ? 255 : o);
 }
 
-// Split test and leaf records.  rec = {step, offset, iso, addr, sidx, err}.
+// Split test, leaf records and children in one pass.  A leaf writes its
+// record {step, offset, iso, addr, sidx, err} into the slot of its depth-first
+// code; a split range appends its four children (TL, TR, BL, BR,
+// codec.py:146-150) to the next level with a warp-aggregated atomic: the
+// order of ranges inside a level never affects results (keys are reduced by
+// value, records are ordered by code), so no prefix scan is needed.
 __global__ void classify_kernel(const unsigned long long* __restrict__ keys,
                                 const int32_t* __restrict__ d_M, int64_t bound, int level,
                                 int can_split, double thr2, int S, int baseline,
                                 const double* __restrict__ svals, const double* __restrict__ dmean,
                                 const double* __restrict__ rmean, const int32_t* __restrict__ roff,
-                                const int32_t* __restrict__ codes, int32_t* __restrict__ split,
-                                int32_t* __restrict__ leaf_flag, int32_t* __restrict__ leaf_rec) {
+                                const int32_t* __restrict__ origins,
+                                const int32_t* __restrict__ codes, int half, int weight,
+                                int32_t* __restrict__ leaf_flag, int32_t* __restrict__ leaf_rec,
+                                int32_t* __restrict__ next_origins,
+                                int32_t* __restrict__ next_codes, int32_t* __restrict__ d_next_M) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= bound) return;
-  if (i >= *d_M) {  // keep the flag scan over the launch bound exact
-    split[i] = 0;
-    return;
+  const bool in = i < bound && i < *d_M;
+  int sp = 0;
+  unsigned long long key = 0;
+  if (in) {
+    key = keys[i];
+    const int32_t err = (int32_t)(key >> 32);
+    // codec.py:140: errs > thresholds[level-1]**2 * side*side (int64 vs float64)
+    sp = can_split && (double)err > thr2;
   }
-  const unsigned long long key = keys[i];
+  const int lane = threadIdx.x & 31;
+  const unsigned bal = __ballot_sync(0xffffffffu, sp);
+  if (bal) {
+    int base = 0;
+    const int leader = __ffs(bal) - 1;
+    if (lane == leader) base = atomicAdd(d_next_M, 4 * __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (sp) {
+      const int64_t j0 = base + 4 * __popc(bal & ((1u << lane) - 1));
+      const int32_t x = origins[2 * i], y = origins[2 * i + 1], code = codes[i];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        next_origins[2 * (j0 + k)] = x + (k & 1) * half;
+        next_origins[2 * (j0 + k) + 1] = y + (k >> 1) * half;
+        next_codes[j0 + k] = code + k * weight;
+      }
+    }
+  }
+  if (!in || sp) return;
   const int32_t err = (int32_t)(key >> 32);
   const int64_t cidx = (int64_t)(key & 0xffffffffull);
-  // codec.py:140: errs > thresholds[level-1]**2 * side*side (int64 vs float64)
-  const int sp = can_split && (double)err > thr2;
-  split[i] = sp;
-  if (sp) return;
   const int64_t e = cidx / (8 * S);
   const int rem = (int)(cidx - e * 8 * S);
   const int iso = rem / S, si = rem - iso * S;
@@ -81,29 +107,6 @@ __global__ void classify_kernel(const unsigned long long* __restrict__ keys,
   r[4] = si;
   r[5] = err;
   leaf_flag[code] = 1;
-}
-
-__global__ void children_kernel(const int32_t* __restrict__ d_M, const int32_t* __restrict__ split,
-                                const int32_t* __restrict__ pfx, const int32_t* __restrict__ origins,
-                                const int32_t* __restrict__ codes, int half, int weight,
-                                int32_t* __restrict__ next_origins, int32_t* __restrict__ next_codes,
-                                int32_t* __restrict__ d_next_M) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t M = *d_M;
-  if (i == 0 && M == 0) *d_next_M = 0;
-  if (i >= M) return;
-  const int32_t p = pfx[i];
-  if (i == M - 1) *d_next_M = 4 * (p + split[i]);
-  if (!split[i]) return;
-  const int32_t x = origins[2 * i], y = origins[2 * i + 1], code = codes[i];
-  // children TL, TR, BL, BR (codec.py:146-150)
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int64_t j = 4 * (int64_t)p + k;
-    next_origins[2 * j] = x + (k & 1) * half;
-    next_origins[2 * j + 1] = y + (k >> 1) * half;
-    next_codes[j] = code + k * weight;
-  }
 }
 
 __global__ void compact_records_kernel(int64_t n_codes, const int32_t* __restrict__ flag,
@@ -169,8 +172,6 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     FC_CUDA(c, c->enc_orig[b].reserve(max_ranges * 8 + 64));
     FC_CUDA(c, c->enc_code[b].reserve(max_ranges * 4 + 64));
   }
-  FC_CUDA(c, c->enc_flag.reserve(max_ranges * 4 + 64));
-  FC_CUDA(c, c->enc_pfx.reserve(max_ranges * 4 + 64));
   FC_CUDA(c, c->enc_count.reserve(64 * 4));
   FC_CUDA(c, c->enc_hist.reserve(256 * 4 * kLevels));
   FC_CUDA(c, c->leaf_flag.reserve(n_codes * 4 + 64));
@@ -182,6 +183,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   int32_t* d_hist = c->enc_hist.as<int32_t>();
   int32_t* h_rb = c->readback.as<int32_t>();
   FC_CUDA(c, cudaMemsetAsync(c->leaf_flag.ptr, 0, n_codes * 4, c->stream));
+  FC_CUDA(c, cudaMemsetAsync(d_count, 0, 16 * 4, c->stream));  // per-level range counters
   top_origins_kernel<<<blocks_for(n_top), 256, 0, c->stream>>>(
       nxt, (int32_t)n_top, c->enc_orig[0].as<int32_t>(), c->enc_code[0].as<int32_t>(), d_count);
   FC_CUDA(c, cudaGetLastError());
@@ -242,26 +244,16 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
       thr2 = thr2 * side;
     }
     int32_t* codes = c->enc_code[cur].as<int32_t>();
-    int32_t* flag = c->enc_flag.as<int32_t>();
+    const int nxt_buf = cur ^ 1;
     classify_kernel<<<blocks_for(bound), 256, 0, c->stream>>>(
         reinterpret_cast<const unsigned long long*>(keys), d_M, bound, l + 1, can_split, thr2,
         L.s_count, L.baseline, L.svals_d.as<double>(), L.mean.as<double>(), c->rmean.as<double>(),
-        c->roff.as<int32_t>(), codes, flag, c->leaf_flag.as<int32_t>(), c->leaf_rec.as<int32_t>());
+        c->roff.as<int32_t>(), c->enc_orig[cur].as<int32_t>(), codes, side / 2,
+        can_split ? 1 << (2 * (2 - l)) : 0, c->leaf_flag.as<int32_t>(), c->leaf_rec.as<int32_t>(),
+        c->enc_orig[nxt_buf].as<int32_t>(), c->enc_code[nxt_buf].as<int32_t>(), d_count + l + 1);
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 1;
     if (can_split) {
-      int32_t* pfx = c->enc_pfx.as<int32_t>();
-      size_t need = 0;
-      FC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, need, flag, pfx, (int)bound, c->stream));
-      FC_CUDA(c, c->cub_tmp.reserve(need));
-      FC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.ptr, need, flag, pfx, (int)bound,
-                                               c->stream));
-      const int nxt_buf = cur ^ 1;
-      children_kernel<<<blocks_for(bound), 256, 0, c->stream>>>(
-          d_M, flag, pfx, c->enc_orig[cur].as<int32_t>(), codes, side / 2, 1 << (2 * (2 - l)),
-          c->enc_orig[nxt_buf].as<int32_t>(), c->enc_code[nxt_buf].as<int32_t>(), d_count + l + 1);
-      FC_CUDA(c, cudaGetLastError());
-      c->total_launches += 2;
       cur = nxt_buf;
       bound *= 4;
       FC_TRY(gather(l + 1, cur, bound));

@@ -66,7 +66,7 @@ constexpr int kSmemBudget = 227 * 1024;  // the opt-in maximum per block
 constexpr int kNone = 0x7fffffff;
 
 // Unit decomposition of one launch, computed on the device from the range
-// count (tc_plan_kernel) so the host never waits for it.
+// count (level_plan_kernel) so the host never waits for it.
 struct TcPlan {
   int M;           // ranges
   int n_rgroups;   // groups of RG row tiles
@@ -560,27 +560,43 @@ __global__ void reach_scatter_kernel(const int4* __restrict__ stats, int64_t nco
   bucket_scatter(valid, st.w + 512, cur_high, reach_high, (int32_t)col);
 }
 
-// Ranges bucketed by offset o (counting sort; cursors = exclusive bucket starts).
-__global__ void order_scatter_kernel(const int32_t* __restrict__ roff, const int32_t* __restrict__ d_M,
-                                     int32_t* __restrict__ cursors, int32_t* __restrict__ order) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = i < *d_M;
-  bucket_scatter(valid, valid ? roff[i] : 0, cursors, order, (int32_t)i);
-}
+// Clamp-correction plan (FixPlan) of one level.
+struct FixPlan {
+  int n_jobs;
+  int pad;
+  long long total_blocks;
+  long long fix_pairs;
+};
 
-// Unit decomposition: RG row tiles per group, the column tiles split into
-// spans minimising the per-CTA makespan ceil(units / grid) * (tiles + 2);
-// the first (smallest) span count wins ties.
-__global__ void __launch_bounds__(256) tc_plan_kernel(const int32_t* __restrict__ d_M, int RG,
-                                                      int ntiles, int grid,
-                                                      TcPlan* __restrict__ plan) {
-  __shared__ unsigned long long best[256];
+// All per-level launch planning in ONE single-block kernel (the host never
+// waits for it):
+//  * unit decomposition of the contraction: RG row tiles per group, column
+//    tiles split into spans minimising the per-CTA makespan
+//    ceil(units / grid) * (tiles + 2) (first, i.e. smallest, span count wins);
+//  * clamp-correction jobs from the offset histogram: ranges with offset o
+//    against the columns whose qmin < -o (list 0) or qmax > 255 - o (list 1),
+//    blocks of RB ranges x 128 columns;
+//  * the ranges bucketed by offset (counting sort, bucket order free).
+constexpr int kPlanThreads = 1024;
+__global__ void __launch_bounds__(kPlanThreads)
+level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
+                  const int32_t* __restrict__ hist, const long long* __restrict__ reach_counts,
+                  int RB, const int32_t* __restrict__ roff, TcPlan* __restrict__ plan,
+                  int4* __restrict__ jobs, long long* __restrict__ prefix,
+                  FixPlan* __restrict__ fplan, int32_t* __restrict__ order,
+                  long long* __restrict__ fix_pairs_out) {
+  __shared__ unsigned long long best[kPlanThreads / 32];
+  __shared__ int cursor[256];
+  __shared__ int njob_s[256];
+  __shared__ long long blocks_s[256], pairs_s[256];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = *d_M;
+  // ---- unit decomposition ----
   const int n_rtiles = (M * 8 + kTileM - 1) / kTileM;
   const int n_rg = (n_rtiles + RG - 1) / RG;
   unsigned long long mine = ~0ull;
   const int smax = min(ntiles, 8192);
-  for (int sc = threadIdx.x + 1; sc <= smax; sc += blockDim.x) {
+  for (int sc = tid + 1; sc <= smax; sc += kPlanThreads) {
     const long long ct = (ntiles + sc - 1) / sc;
     const long long nsp = (ntiles + ct - 1) / ct;
     const long long units = nsp * n_rg;
@@ -588,16 +604,60 @@ __global__ void __launch_bounds__(256) tc_plan_kernel(const int32_t* __restrict_
     const unsigned long long key = ((unsigned long long)cost << 24) | (unsigned long long)sc;
     mine = key < mine ? key : mine;
   }
-  best[threadIdx.x] = mine;
-  __syncthreads();
-  for (int o = 128; o; o >>= 1) {
-    if (threadIdx.x < o) best[threadIdx.x] = min(best[threadIdx.x], best[threadIdx.x + o]);
-    __syncthreads();
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, mine, o);
+    mine = w < mine ? w : mine;
   }
-  if (threadIdx.x == 0) {
-    const int sc = (int)(best[0] & 0xffffff);
-    const int ct = (ntiles + sc - 1) / sc;
-    const int nsp = (ntiles + ct - 1) / ct;
+  if (lane == 0) best[warp] = mine;
+  // ---- correction jobs: thread o < 256 owns offset bucket o ----
+  int cnt = 0;
+  long long lists[2] = {0, 0};
+  if (tid < 256) {
+    cnt = hist[tid];
+    lists[0] = reach_counts[tid];
+    lists[1] = reach_counts[256 + tid];
+    int njob = 0;
+    long long blocks = 0, pairs = 0;
+    for (int k = 0; k < 2; ++k)
+      if (cnt && lists[k]) {
+        ++njob;
+        blocks += (long long)((cnt + RB - 1) / RB) * ((lists[k] + 127) / 128);
+        pairs += (long long)cnt * lists[k];
+      }
+    cursor[tid] = cnt;
+    njob_s[tid] = njob;
+    blocks_s[tid] = blocks;
+    pairs_s[tid] = pairs;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // serial exclusive scans over the 256 buckets
+    int ac = 0, aj = 0;
+    long long ab = 0, ap = 0;
+    for (int o = 0; o < 256; ++o) {
+      const int c0 = cursor[o], j0 = njob_s[o];
+      const long long b0 = blocks_s[o], p0 = pairs_s[o];
+      cursor[o] = ac;
+      njob_s[o] = aj;
+      blocks_s[o] = ab;
+      ac += c0;
+      aj += j0;
+      ab += b0;
+      ap += p0;
+    }
+    FixPlan fp{};
+    fp.n_jobs = aj;
+    fp.total_blocks = ab;
+    fp.fix_pairs = ap;
+    *fplan = fp;
+    if (fix_pairs_out) *fix_pairs_out = ap;
+    prefix[aj] = ab;
+    unsigned long long bk = best[0];
+    for (int w = 1; w < kPlanThreads / 32; ++w) bk = best[w] < bk ? best[w] : bk;
+    const int sc = (int)(bk & 0xffffff);
+    const int ct = sc > 0 ? (ntiles + sc - 1) / sc : ntiles;
+    const int nsp = ct > 0 ? (ntiles + ct - 1) / ct : 0;
     TcPlan pl{};
     pl.M = M;
     pl.n_rgroups = M > 0 ? n_rg : 0;
@@ -606,77 +666,22 @@ __global__ void __launch_bounds__(256) tc_plan_kernel(const int32_t* __restrict_
     pl.rows_pad = n_rg * RG * kTileM;
     *plan = pl;
   }
-}
-
-// Clamp-correction jobs from the offset histogram (one block, thread = o):
-// ranges with offset o against the columns whose qmin < -o (list 0) or
-// qmax > 255 - o (list 1); blocks of RB ranges x 128 columns.
-struct FixPlan {
-  int n_jobs;
-  int pad;
-  long long total_blocks;
-  long long fix_pairs;
-};
-__global__ void __launch_bounds__(256) fix_plan_kernel(const int32_t* __restrict__ hist,
-                                                       const long long* __restrict__ reach_counts,
-                                                       int RB,
-                                                       int4* __restrict__ jobs,
-                                                       long long* __restrict__ prefix,
-                                                       int32_t* __restrict__ cursors,
-                                                       FixPlan* __restrict__ out) {
-  using Scan = cub::BlockScan<long long, 256>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int s_start[257];
-  const int o = threadIdx.x;
-  const int cnt = hist[o];
-  {
-    using IScan = cub::BlockScan<int, 256>;
-    __shared__ typename IScan::TempStorage itmp;
-    int excl;
-    IScan(itmp).ExclusiveSum(cnt, excl);
-    s_start[o] = excl;
-    cursors[o] = excl;
-  }
-  const long long lists[2] = {reach_counts[o], reach_counts[256 + o]};
-  int njob = 0;
-  long long blocks = 0, pairs = 0;
-  for (int k = 0; k < 2; ++k)
-    if (cnt && lists[k]) {
-      ++njob;
-      blocks += (long long)((cnt + RB - 1) / RB) * ((lists[k] + 127) / 128);
-      pairs += (long long)cnt * lists[k];
-    }
   __syncthreads();
-  int jbase;
-  {
-    using IScan = cub::BlockScan<int, 256>;
-    __shared__ typename IScan::TempStorage itmp2;
-    IScan(itmp2).ExclusiveSum(njob, jbase);
+  if (tid < 256) {
+    int j = njob_s[tid];
+    long long b = blocks_s[tid];
+    for (int k = 0; k < 2; ++k)
+      if (cnt && lists[k]) {
+        jobs[j] = make_int4(k, cursor[tid], cnt, (int)lists[k]);
+        prefix[j] = b;
+        b += (long long)((cnt + RB - 1) / RB) * ((lists[k] + 127) / 128);
+        ++j;
+      }
   }
-  long long bbase, agg;
-  Scan(tmp).ExclusiveSum(blocks, bbase, agg);
   __syncthreads();
-  long long pbase, pagg;
-  Scan(tmp).ExclusiveSum(pairs, pbase, pagg);
-  int j = jbase;
-  long long b = bbase;
-  for (int k = 0; k < 2; ++k)
-    if (cnt && lists[k]) {
-      jobs[j] = make_int4(k, s_start[o], cnt, (int)lists[k]);
-      prefix[j] = b;
-      b += (long long)((cnt + RB - 1) / RB) * ((lists[k] + 127) / 128);
-      ++j;
-    }
-  if (o == 255) {
-    prefix[j] = b;
-    FixPlan fp{};
-    fp.n_jobs = j;
-    fp.total_blocks = b;
-    fp.fix_pairs = pagg;
-    *out = fp;
-  }
+  // ---- ranges bucketed by offset ----
+  for (int i = tid; i < M; i += kPlanThreads) order[atomicAdd(&cursor[roff[i]], 1)] = i;
 }
-
 
 }  // namespace
 
@@ -835,7 +840,14 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   FC_CUDA(c, c->tc_plan.reserve(sizeof(TcPlan) + sizeof(FixPlan) + 64));
   TcPlan* d_plan = c->tc_plan.as<TcPlan>();
   FixPlan* d_fplan = reinterpret_cast<FixPlan*>(c->tc_plan.as<uint8_t>() + sizeof(TcPlan));
-  tc_plan_kernel<<<1, 256, 0, c->stream>>>(d_M, RG, (int)T.ntiles, c->sm_count, d_plan);
+  FC_CUDA(c, c->fix_rows.reserve(M_bound * 4 + 64));
+  FC_CUDA(c, c->fix_jobs.reserve(512 * 16 + 64));
+  FC_CUDA(c, c->fix_cols.reserve(513 * 8 + 64));
+  level_plan_kernel<<<1, kPlanThreads, 0, c->stream>>>(
+      d_M, RG, (int)T.ntiles, c->sm_count, d_hist, T.reach_counts.as<long long>(),
+      ranges_per_block(L.n), c->roff.as<int32_t>(), d_plan, c->fix_jobs.as<int4>(),
+      c->fix_cols.as<long long>(), d_fplan, c->fix_rows.as<int32_t>(),
+      reinterpret_cast<long long*>(d_fix_pairs));
   const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
   const int64_t work = rows_max * (T.kpad / 16);
   build_a_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
@@ -867,26 +879,10 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   if (ev_main_end) FC_CUDA(c, cudaEventRecord(ev_main_end, c->stream));
   c->stats.kernel_launches += 1;
 
-  // ---- clamp corrections (exact kernel on clamp-active pairs), planned on the device ----
-  FC_CUDA(c, c->fix_rows.reserve(M_bound * 4 + 64));
-  FC_CUDA(c, c->fix_jobs.reserve(512 * 16 + 64));
-  FC_CUDA(c, c->fix_cols.reserve(513 * 8 + 64));
-  FC_CUDA(c, c->tc_scratch.reserve(256 * 4));
-  int32_t* d_cursor = c->tc_scratch.as<int32_t>();
-  fix_plan_kernel<<<1, 256, 0, c->stream>>>(d_hist, T.reach_counts.as<long long>(),
-                                            ranges_per_block(L.n),
-                                            c->fix_jobs.as<int4>(), c->fix_cols.as<long long>(),
-                                            d_cursor, d_fplan);
-  order_scatter_kernel<<<(unsigned)((M_bound + 255) / 256), 256, 0, c->stream>>>(
-      c->roff.as<int32_t>(), d_M, d_cursor, c->fix_rows.as<int32_t>());
-  FC_CUDA(c, cudaGetLastError());
-  c->stats.kernel_launches += 2;
+  // ---- clamp corrections (exact kernel on clamp-active pairs), planned above ----
   FC_TRY(scan_exact_jobs(c, L, c->fix_jobs.as<int4>(), c->fix_cols.as<int64_t>(),
                          &d_fplan->n_jobs, &d_fplan->total_blocks, c->fix_rows.as<int32_t>(),
                          T.reach_low.as<int32_t>(), T.reach_high.as<int32_t>(), d_keys));
-  if (d_fix_pairs)
-    FC_CUDA(c, cudaMemcpyAsync(d_fix_pairs, &d_fplan->fix_pairs, 8, cudaMemcpyDeviceToDevice,
-                               c->stream));
   return FC_OK;
 }
 
