@@ -324,15 +324,19 @@ __global__ void rank_scatter_kernel(SortParams P, const int32_t* __restrict__ ra
   L.out[rank_all[L.chunk_begin * kChunk + i]] = L.val[i];
 }
 
-// Survivors of all levels in one launch, one thread per decimated pixel
-// (floor 2x2 mean, image.py:125-130), then per survivor: coordinates, entropy,
-// exact sum / sum of squares, mean and centred norm (pool.py:138-152).
+// Survivors of all levels in one launch.  A survivor's 2B x 2B window is
+// handled by D = 2B lanes, lane = input row: the row is read as aligned words
+// (funnel-shifted into place), horizontal pixel pairs are summed as packed
+// 16-bit lanes, the partner row arrives by one shuffle, and even lanes emit
+// an output row (floor 2x2 mean, image.py:125-130).  Then per survivor:
+// coordinates, entropy, exact sum / sum of squares, mean and centred norm
+// (pool.py:138-152).
 struct SurvLevel {
   const uint32_t* order;
   const double* ent_all;
   int64_t count;
-  int B, lb, nx, stride;  // range side B = 1 << lb
-  int64_t block_begin;
+  int B, nx, stride;
+  int64_t warp_begin;
   uint32_t* xy;
   double* ent;
   uint8_t* tiles;
@@ -343,65 +347,107 @@ struct SurvLevel {
 };
 struct SurvParams {
   SurvLevel lv[4];
+  int64_t total_warps;
 };
 
-__global__ void __launch_bounds__(256) survivors_all_kernel(const uint8_t* __restrict__ img,
-                                                            int width, SurvParams P) {
-  __shared__ int ps1[256], ps2[256];
-  int l = 0;
-#pragma unroll
-  for (int k = 1; k < 4; ++k)
-    if ((int64_t)blockIdx.x >= P.lv[k].block_begin) l = k;
-  const SurvLevel& L = P.lv[l];
-  const int lb = L.lb, B = 1 << lb, n = 1 << (2 * lb);
-  const int64_t idx = ((int64_t)blockIdx.x - L.block_begin) * 256 + threadIdx.x;
-  const int64_t sv = idx >> (2 * lb);
-  const int p = (int)(idx & (n - 1));
-  const bool valid = sv < L.count;
-  int v = 0;
+__device__ __forceinline__ uint32_t load_word_guarded(const uint8_t* img, int64_t off,
+                                                      int64_t img_bytes) {
+  if (off + 4 <= img_bytes) return __ldg(reinterpret_cast<const uint32_t*>(img + off));
   uint32_t w = 0;
+  for (int k = 0; k < 4; ++k)
+    if (off + k < img_bytes) w |= (uint32_t)img[off + k] << (8 * k);
+  return w;
+}
+
+template <int D>
+__device__ __forceinline__ void survivor_rows(const SurvLevel& L, const uint8_t* __restrict__ img,
+                                              int width, int64_t img_bytes, int64_t warp_in_level,
+                                              int lane) {
+  constexpr int B = D / 2, n = B * B, PER = 32 / D, NW = D / 4;
+  const int grp = lane / D, row = lane % D;
+  const int64_t sv = warp_in_level * PER + grp;
+  const bool valid = sv < L.count;
+  uint32_t w = 0;
+  uint32_t pq[NW > 0 ? NW : 1];
   if (valid) {
     w = __ldg(L.order + sv);
     const int wy = w / L.nx, wx = w - wy * L.nx;
-    const int x0 = wx * L.stride, y0 = wy * L.stride;
-    const int r = p >> lb, cc = p & (B - 1);
-    const uint8_t* q = img + (int64_t)(y0 + 2 * r) * width + x0 + 2 * cc;
-    v = (q[0] + q[1] + q[width] + q[width + 1]) >> 2;
-    L.tiles[sv * n + p] = (uint8_t)v;
+    const int64_t a = (int64_t)(wy * L.stride + row) * width + wx * L.stride;
+    const int64_t a0 = a & ~3ll;
+    const int sh = (int)(a - a0) * 8;
+    uint32_t raw[NW + 1];
+#pragma unroll
+    for (int k = 0; k <= NW; ++k)
+      raw[k] = (k < NW || sh) ? load_word_guarded(img, a0 + 4 * k, img_bytes) : 0u;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      const uint32_t rw = __funnelshift_r(raw[k], raw[k + 1], sh);
+      pq[k] = (rw & 0x00ff00ffu) + ((rw >> 8) & 0x00ff00ffu);  // [b0+b1 | b2+b3]
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < NW; ++k) pq[k] = 0;
   }
-  // segmented reduction: groups of min(n, 32) lanes, then per-survivor partials
-  int s1 = v, s2 = v * v;
-  const int width_r = n < 32 ? n : 32;
-  for (int o = width_r >> 1; o; o >>= 1) {
+  int s1 = 0, s2 = 0;
+  uint32_t outw[NW > 1 ? NW / 2 : 1];
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+    const uint32_t dn = __shfl_down_sync(0xffffffffu, pq[k], 1);
+    const uint32_t q = ((pq[k] + dn) >> 2) & 0x00ff00ffu;  // two output pixels (16-bit lanes)
+    const int v0 = (int)(q & 0xffu), v1 = (int)(q >> 16);
+    s1 += v0 + v1;
+    s2 += v0 * v0 + v1 * v1;
+    if (k & 1) outw[k >> 1] = __byte_perm(outw[k >> 1], q, 0x6420);
+    else outw[k >> 1] = q;
+  }
+  const bool emits = valid && (row & 1) == 0;
+  if (!emits) s1 = s2 = 0;
+  if (emits) {
+    uint8_t* dst = L.tiles + sv * n + (row >> 1) * B;
+    if constexpr (B == 16) {
+      *reinterpret_cast<uint4*>(dst) = make_uint4(outw[0], outw[1], outw[2], outw[3]);
+    } else if constexpr (B == 8) {
+      *reinterpret_cast<uint2*>(dst) = make_uint2(outw[0], outw[1]);
+    } else if constexpr (B == 4) {
+      *reinterpret_cast<uint32_t*>(dst) = outw[0];
+    } else {
+      *reinterpret_cast<uint16_t*>(dst) = (uint16_t)(outw[0] | (outw[0] >> 8));
+    }
+  }
+#pragma unroll
+  for (int o = D >> 1; o; o >>= 1) {
     s1 += __shfl_xor_sync(0xffffffffu, s1, o);
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
   }
-  const int part = threadIdx.x / width_r;
-  if ((threadIdx.x & (width_r - 1)) == 0) {
-    ps1[part] = s1;
-    ps2[part] = s2;
+  if (valid && row == 0) {
+    const int wy = w / L.nx, wx = w - wy * L.nx;
+    L.xy[sv] = (uint32_t)(wx * L.stride) | ((uint32_t)(wy * L.stride) << 16);
+    L.ent[sv] = L.ent_all[w];
+    L.sum[sv] = s1;
+    L.sumsq[sv] = s2;
+    // mean = s1 / n; cnorm = s2 - s1*s1/n with Python float semantics (pool.py:144-151)
+    L.mean[sv] = __ddiv_rn((double)s1, (double)n);
+    L.cnorm[sv] = __dsub_rn((double)s2, __ddiv_rn((double)((long long)s1 * s1), (double)n));
   }
-  __syncthreads();
-  const int per = n / width_r;  // partials per survivor
-  const int spb = 256 / n;      // survivors per block (n <= 256)
-  if ((int)threadIdx.x < (spb > 0 ? spb : 1)) {
-    const int64_t s_here = ((int64_t)blockIdx.x - L.block_begin) * 256 / n + threadIdx.x;
-    if (s_here < L.count) {
-      int t1 = 0, t2 = 0;
-      for (int k = 0; k < per; ++k) {
-        t1 += ps1[threadIdx.x * per + k];
-        t2 += ps2[threadIdx.x * per + k];
-      }
-      const uint32_t ww = L.order[s_here];
-      const int wy = ww / L.nx, wx = ww - wy * L.nx;
-      L.xy[s_here] = (uint32_t)(wx * L.stride) | ((uint32_t)(wy * L.stride) << 16);
-      L.ent[s_here] = L.ent_all[ww];
-      L.sum[s_here] = t1;
-      L.sumsq[s_here] = t2;
-      // mean = s1 / n; cnorm = s2 - s1*s1/n with Python float semantics (pool.py:144-151)
-      L.mean[s_here] = __ddiv_rn((double)t1, (double)n);
-      L.cnorm[s_here] = __dsub_rn((double)t2, __ddiv_rn((double)((long long)t1 * t1), (double)n));
-    }
+}
+
+__global__ void __launch_bounds__(256) survivors_all_kernel(const uint8_t* __restrict__ img,
+                                                            int width, int64_t img_bytes,
+                                                            SurvParams P) {
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= P.total_warps) return;
+  int l = 0;
+#pragma unroll
+  for (int k = 1; k < 4; ++k)
+    if (gw >= P.lv[k].warp_begin) l = k;
+  const SurvLevel& L = P.lv[l];
+  const int64_t wl = gw - L.warp_begin;
+  switch (L.B) {
+    case 16: survivor_rows<32>(L, img, width, img_bytes, wl, lane); break;
+    case 8: survivor_rows<16>(L, img, width, img_bytes, wl, lane); break;
+    case 4: survivor_rows<8>(L, img, width, img_bytes, wl, lane); break;
+    default: survivor_rows<4>(L, img, width, img_bytes, wl, lane); break;
   }
 }
 
@@ -697,7 +743,7 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     }
   }
   SurvParams SV{};
-  int64_t sblocks = 0;
+  int64_t swarps = 0;
   for (int li = 0; li < kLevels; ++li) {
     Level& L = c->lv[li];
     const int64_t E = L.count;
@@ -707,10 +753,9 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     V.ent_all = L.win_ent.as<double>();
     V.count = E;
     V.B = L.side;
-    V.lb = L.side == 16 ? 4 : L.side == 8 ? 3 : L.side == 4 ? 2 : 1;
     V.nx = nx_l[li];
     V.stride = L.stride;
-    V.block_begin = sblocks;
+    V.warp_begin = swarps;
     V.xy = L.xy.as<uint32_t>();
     V.ent = L.ent.as<double>();
     V.tiles = L.tiles.as<uint8_t>();
@@ -718,12 +763,17 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     V.sumsq = L.sumsq.as<int64_t>();
     V.mean = L.mean.as<double>();
     V.cnorm = L.cnorm.as<double>();
-    sblocks += (E * L.n + 255) / 256;
+    const int per = 32 / (2 * L.side);  // survivors per warp
+    swarps += (E + per - 1) / per;
     out_sizes[li] = E;
   }
-  survivors_all_kernel<<<(unsigned)sblocks, 256, 0, c->stream>>>(c->img_ptr, c->width, SV);
-  FC_CUDA(c, cudaGetLastError());
-  c->total_launches += 1;
+  SV.total_warps = swarps;
+  if (swarps > 0) {
+    survivors_all_kernel<<<(unsigned)((swarps * 32 + 255) / 256), 256, 0, c->stream>>>(
+        c->img_ptr, c->width, (int64_t)c->width * c->height, SV);
+    FC_CUDA(c, cudaGetLastError());
+    c->total_launches += 1;
+  }
   trace_mark(c, "pool_launched");
   return FC_OK;
 }

@@ -61,7 +61,6 @@ constexpr int kAccN = 256;       // columns per MMA / TMEM accumulator
 constexpr int kNumAcc = 2;       // TMEM accumulators (2 x 256 columns = all 512)
 constexpr int kEpiWarps = 16;    // all drain every accumulator (4 per TMEM sub-partition)
 constexpr int kThreads = (4 + kEpiWarps) * 32;
-constexpr int kMaxRG = 8;
 constexpr int kSmemBudget = 227 * 1024;  // the opt-in maximum per block
 constexpr int kNone = 0x7fffffff;
 
@@ -587,8 +586,6 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
                   long long* __restrict__ fix_pairs_out) {
   __shared__ unsigned long long best[kPlanThreads / 32];
   __shared__ int cursor[256];
-  __shared__ int njob_s[256];
-  __shared__ long long blocks_s[256], pairs_s[256];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = *d_M;
   // ---- unit decomposition ----
@@ -597,10 +594,10 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
   unsigned long long mine = ~0ull;
   const int smax = min(ntiles, 8192);
   for (int sc = tid + 1; sc <= smax; sc += kPlanThreads) {
-    const long long ct = (ntiles + sc - 1) / sc;
-    const long long nsp = (ntiles + ct - 1) / ct;
-    const long long units = nsp * n_rg;
-    const long long cost = ((units + grid - 1) / grid) * (ct + 2);
+    const unsigned ct = ((unsigned)ntiles + sc - 1) / (unsigned)sc;
+    const unsigned nsp = ((unsigned)ntiles + ct - 1) / ct;
+    const unsigned long long units = (unsigned long long)nsp * (unsigned)n_rg;
+    const unsigned long long cost = ((units + grid - 1) / (unsigned)grid) * (ct + 2);
     const unsigned long long key = ((unsigned long long)cost << 24) | (unsigned long long)sc;
     mine = key < mine ? key : mine;
   }
@@ -611,48 +608,75 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
   }
   if (lane == 0) best[warp] = mine;
   // ---- correction jobs: thread o < 256 owns offset bucket o ----
-  int cnt = 0;
-  long long lists[2] = {0, 0};
+  int cnt = 0, njob = 0;
+  long long lists[2] = {0, 0}, blocks = 0, pairs = 0;
   if (tid < 256) {
     cnt = hist[tid];
     lists[0] = reach_counts[tid];
     lists[1] = reach_counts[256 + tid];
-    int njob = 0;
-    long long blocks = 0, pairs = 0;
     for (int k = 0; k < 2; ++k)
       if (cnt && lists[k]) {
         ++njob;
         blocks += (long long)((cnt + RB - 1) / RB) * ((lists[k] + 127) / 128);
         pairs += (long long)cnt * lists[k];
       }
-    cursor[tid] = cnt;
-    njob_s[tid] = njob;
-    blocks_s[tid] = blocks;
-    pairs_s[tid] = pairs;
+  }
+  // exclusive scans over the 256 buckets: warp scans + warp totals
+  __shared__ int wt_c[8], wt_j[8];
+  __shared__ long long wt_b[8], wt_p[8];
+  int ic = cnt, ij = njob;
+  long long ib = blocks, ip = pairs;
+  if (tid < 256) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int c2 = __shfl_up_sync(0xffffffffu, ic, o), j2 = __shfl_up_sync(0xffffffffu, ij, o);
+      const long long b2 = __shfl_up_sync(0xffffffffu, ib, o), p2 = __shfl_up_sync(0xffffffffu, ip, o);
+      if (lane >= o) {
+        ic += c2;
+        ij += j2;
+        ib += b2;
+        ip += p2;
+      }
+    }
+    if (lane == 31) {
+      wt_c[warp] = ic;
+      wt_j[warp] = ij;
+      wt_b[warp] = ib;
+      wt_p[warp] = ip;
+    }
   }
   __syncthreads();
-  if (tid == 0) {
-    // serial exclusive scans over the 256 buckets
-    int ac = 0, aj = 0;
-    long long ab = 0, ap = 0;
-    for (int o = 0; o < 256; ++o) {
-      const int c0 = cursor[o], j0 = njob_s[o];
-      const long long b0 = blocks_s[o], p0 = pairs_s[o];
-      cursor[o] = ac;
-      njob_s[o] = aj;
-      blocks_s[o] = ab;
-      ac += c0;
-      aj += j0;
-      ab += b0;
-      ap += p0;
+  if (tid < 256) {
+    int pc = 0, pj = 0;
+    long long pb = 0;
+    for (int w2 = 0; w2 < warp; ++w2) {
+      pc += wt_c[w2];
+      pj += wt_j[w2];
+      pb += wt_b[w2];
     }
-    FixPlan fp{};
-    fp.n_jobs = aj;
-    fp.total_blocks = ab;
-    fp.fix_pairs = ap;
-    *fplan = fp;
-    if (fix_pairs_out) *fix_pairs_out = ap;
-    prefix[aj] = ab;
+    cursor[tid] = pc + ic - cnt;  // exclusive
+    int j = pj + ij - njob;
+    long long b = pb + ib - blocks;
+    for (int k = 0; k < 2; ++k)
+      if (cnt && lists[k]) {
+        jobs[j] = make_int4(k, cursor[tid], cnt, (int)lists[k]);
+        prefix[j] = b;
+        b += (long long)((cnt + RB - 1) / RB) * ((lists[k] + 127) / 128);
+        ++j;
+      }
+    if (tid == 255) {
+      long long tp = 0;
+      for (int w2 = 0; w2 < 8; ++w2) tp += wt_p[w2];
+      FixPlan fp{};
+      fp.n_jobs = j;
+      fp.total_blocks = b;
+      fp.fix_pairs = tp;
+      *fplan = fp;
+      if (fix_pairs_out) *fix_pairs_out = tp;
+      prefix[j] = b;
+    }
+  }
+  if (tid == 0) {
     unsigned long long bk = best[0];
     for (int w = 1; w < kPlanThreads / 32; ++w) bk = best[w] < bk ? best[w] : bk;
     const int sc = (int)(bk & 0xffffff);
@@ -665,18 +689,6 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
     pl.n_units = M > 0 ? nsp * n_rg : 0;
     pl.rows_pad = n_rg * RG * kTileM;
     *plan = pl;
-  }
-  __syncthreads();
-  if (tid < 256) {
-    int j = njob_s[tid];
-    long long b = blocks_s[tid];
-    for (int k = 0; k < 2; ++k)
-      if (cnt && lists[k]) {
-        jobs[j] = make_int4(k, cursor[tid], cnt, (int)lists[k]);
-        prefix[j] = b;
-        b += (long long)((cnt + RB - 1) / RB) * ((lists[k] + 127) / 128);
-        ++j;
-      }
   }
   __syncthreads();
   // ---- ranges bucketed by offset ----
