@@ -340,10 +340,14 @@ def main():
     except Exception:  # noqa: BLE001
         pass
     achieved = (alg_ops / (main_ms * 1e-3)) / 1e12 if main_ms > 0 else None
+    # DRAM bytes per tc_scan_kernel launch from the committed ncu --set full capture
+    # (dram__bytes_read.sum + dram__bytes_write.sum, averaged over the c2 levels)
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(args.workload)
+    tpath = os.path.join(ROOT, "profiles", "r01", "tc_scan_c2_traffic.json")
+    if args.workload == "c2" and os.path.exists(tpath):
+        launches = json.load(open(tpath))["launches"]
+        if launches:
+            traffic = sum(x["dram_read_bytes"] + x["dram_write_bytes"] for x in launches) / len(launches)
     line = {
         "metric": "range-domain comparisons/sec",
         "value": value,
