@@ -69,6 +69,9 @@ int fc_synchronize(fc_ctx* ctx);
 /* Device-resident mode for benchmarking: when set, fc_set_image's pixels and
  * fc_match_level's origins/outputs are DEVICE pointers (no host copies). */
 int fc_set_device_io(fc_ctx* ctx, int device_io);
+/* Execution options: "graph" (1 = run fc_encode's level loop as one CUDA
+ * graph, the default; 0 = eager launches).  Results never depend on them. */
+int fc_set_option(fc_ctx* ctx, const char* name, int64_t value);
 
 /* terms[k-1] = (k/n) * log(k/n), k = 1..n, produced by the host's numpy so the
  * entropy bits equal pool.py:88-92 on the same host.  n in {16,64,256,1024}. */

@@ -62,6 +62,7 @@ _SIGNATURES = {
     "fc_last_error": ([_P], ctypes.c_char_p),
     "fc_synchronize": ([_P], ctypes.c_int),
     "fc_set_device_io": ([_P, ctypes.c_int], ctypes.c_int),
+    "fc_set_option": ([_P, ctypes.c_char_p, _I64], ctypes.c_int),
     "fc_set_entropy_lut": ([_P, ctypes.c_int, _P], ctypes.c_int),
     "fc_set_image": ([_P, _P, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "fc_pool_build": ([_P, _P, _P, _P, _P, _P], ctypes.c_int),
@@ -159,6 +160,9 @@ class Context:
             pass
 
     # -- thin wrappers -----------------------------------------------------
+    def set_option(self, name: str, value: int):
+        self.check(self.lib.fc_set_option(self.handle, name.encode(), int(value)))
+
     def set_image(self, pixels: np.ndarray):
         a = np.ascontiguousarray(pixels, dtype=np.uint8)
         self.check(self.lib.fc_set_image(self.handle, _ptr(a), a.shape[1], a.shape[0]))

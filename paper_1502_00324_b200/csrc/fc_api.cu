@@ -45,7 +45,7 @@ void trace_mark(Ctx* c, const char* name) {
     if (cudaEventCreate(&e) != cudaSuccess) return;
     c->trace_ev.push_back(e);
   }
-  cudaEventRecord(c->trace_ev[k], c->stream);
+  record_event(c, c->trace_ev[k]);
   c->trace_name.push_back(name);
   c->trace_host_us.push_back(host_us());
 }
@@ -189,6 +189,7 @@ int fc_ctx_create(int device, fc_ctx** out) {
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
   if (const char* t = getenv("FC_TRACE")) c->trace = atoi(t);
+  if (const char* g = getenv("FC_GRAPH")) c->use_graph = atoi(g) != 0;
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaEventCreate(&c->ev2) != cudaSuccess || cudaEventCreate(&c->tc_ev[0]) != cudaSuccess ||
@@ -238,6 +239,7 @@ void fc_ctx_destroy(fc_ctx* c) {
   cudaEventDestroy(c->ev2);
   for (auto& e : c->tc_ev) cudaEventDestroy(e);
   for (auto& e : c->trace_ev) cudaEventDestroy(e);
+  if (c->enc_exec) cudaGraphExecDestroy(c->enc_exec);
   cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -253,6 +255,15 @@ int fc_synchronize(fc_ctx* c) {
 int fc_set_device_io(fc_ctx* c, int device_io) {
   c->device_io = device_io ? 1 : 0;
   return FC_OK;
+}
+
+int fc_set_option(fc_ctx* c, const char* name, int64_t value) {
+  if (!name) return set_error(c, FC_ERR_ARG, "null option name");
+  if (strcmp(name, "graph") == 0) {
+    c->use_graph = value != 0;
+    return FC_OK;
+  }
+  return set_error(c, FC_ERR_ARG, std::string("unknown option ") + name);
 }
 
 int fc_set_entropy_lut(fc_ctx* c, int n, const double* terms) {

@@ -197,15 +197,53 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     return gather_ranges_dev(c, c->lv[l], c->enc_orig[cur].as<int32_t>(), d_count + l, bound,
                              d_hist + 256 * l);
   };
+  // every range buffer is sized for the level-4 bound BEFORE the first gather:
+  // a later reserve must never reallocate (and so drop) gathered ranges
+  FC_TRY(reserve_ranges(c, c->lv[kLevels - 1], max_ranges));
+  FC_TRY(reserve_ranges(c, c->lv[0], n_top));
   FC_TRY(gather(0, 0, n_top));
   trace_mark(c, "prep_launched");
   FC_TRY(sync_stream(c));
   trace_mark(c, "prep_sync");
+  for (int l = 0; l < kLevels; ++l)
+    if (pending[l]) FC_TRY(prepare_finish(c, c->lv[l], lpath[l], pending[l]));
+
+  // ---- the level loop and the record compaction run as ONE CUDA graph ----
+  // (~45 stream operations per encode; a graph launch cuts the per-operation
+  // launch cost from ~3.7 us to ~0.5-1 us, tools/microbench/launch_gap.cu).
+  // Every buffer is reserved for the level's upper bound first, so nothing
+  // allocates while the stream is being captured.
+  bool use_graph = c->use_graph;
+  {
+    // range buffers were sized for the largest level before the first gather
+    int64_t b = n_top;
+    for (int l = 0; l < kLevels; ++l, b *= 4) {
+      Level& L = c->lv[l];
+      if (L.count == 0) {  // the empty-pool check needs a host sync: run eagerly
+        use_graph = false;
+        break;
+      }
+      FC_TRY(reserve_level_scan(c, L, b));
+    }
+    size_t need = 0;
+    FC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, need, c->leaf_flag.as<int32_t>(),
+                                             c->leaf_pos.as<int32_t>(), (int)n_codes, c->stream));
+    FC_CUDA(c, c->cub_tmp.reserve(need));
+    FC_CUDA(c, c->rec_out.reserve(n_codes * 24 + 64));
+    int64_t total = 0;
+    for (int l = 0; l < kLevels; ++l) total += c->lv[l].count;
+    FC_CUDA(c, c->coords_pinned.reserve(total * 4 + 16));
+  }
+  if (use_graph) {
+    FC_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    c->capturing = true;
+  }
+  int levels_run = 0;
+  const int body_rc = [&]() -> int {
 
   // ---- level loop: no host synchronisation ----
   int cur = 0;
   int64_t bound = n_top;
-  int levels_run = 0;
   for (int l = 0; l < kLevels; ++l) {
     Level& L = c->lv[l];
     if (L.count == 0) {
@@ -220,21 +258,18 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
       break;
     }
     levels_run = l + 1;
-    // finish this level's operands only now: the host work overlaps the
-    // previous level's kernels instead of idling the GPU after the sync
-    if (pending[l]) FC_TRY(prepare_finish(c, L, lpath[l], pending[l]));
     const int32_t* d_M = d_count + l;
     const int64_t launches_before = c->total_launches + c->stats.kernel_launches;
     uint64_t* keys = c->keys.as<uint64_t>();
     FC_CUDA(c, cudaMemsetAsync(keys, 0xff, bound * 8, c->stream));
-    FC_CUDA(c, cudaEventRecord(c->enc_ev[l][0], c->stream));
+    FC_CUDA(c, record_event(c, c->enc_ev[l][0]));
     if (L.path == FC_PATH_TENSOR) {
       FC_TRY(scan_tc_launch(c, L, bound, d_M, d_hist + 256 * l, keys, c->enc_ev[l][1], d_fix + l));
     } else {
       FC_TRY(scan_exact(c, L, bound, nullptr, 0, nullptr, 0, keys, d_M));
-      FC_CUDA(c, cudaEventRecord(c->enc_ev[l][1], c->stream));
+      FC_CUDA(c, record_event(c, c->enc_ev[l][1]));
     }
-    FC_CUDA(c, cudaEventRecord(c->enc_ev[l][2], c->stream));
+    FC_CUDA(c, record_event(c, c->enc_ev[l][2]));
     const int side = L.side;
     const int can_split = l < kLevels - 1;
     double thr2 = 0.0;
@@ -274,10 +309,8 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     int32_t* pos = c->leaf_pos.as<int32_t>();
     size_t need = 0;
     FC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, need, flag, pos, (int)n_codes, c->stream));
-    FC_CUDA(c, c->cub_tmp.reserve(need));
     FC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.ptr, need, flag, pos, (int)n_codes,
                                              c->stream));
-    FC_CUDA(c, c->rec_out.reserve(n_codes * 24 + 64));
     compact_records_kernel<<<blocks_for(n_codes), 256, 0, c->stream>>>(
         n_codes, flag, pos, c->leaf_rec.as<int32_t>(), c->rec_out.as<int32_t>(), d_count + 8);
     FC_CUDA(c, cudaGetLastError());
@@ -291,7 +324,6 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
         c->coords_off[l] = total;
         total += c->lv[l].count;
       }
-      FC_CUDA(c, c->coords_pinned.reserve(total * 4 + 16));
       for (int l = 0; l < kLevels; ++l)
         if (c->lv[l].count)
           FC_CUDA(c, cudaMemcpyAsync(c->coords_pinned.as<uint32_t>() + c->coords_off[l],
@@ -299,10 +331,44 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
                                      c->stream));
       c->coords_valid = true;
     }
-    trace_mark(c, "records_launched");
-    FC_TRY(sync_stream(c));
-    trace_mark(c, "records_sync");
   }
+  return FC_OK;
+  }();
+  if (use_graph) {
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+    c->capturing = false;
+    if (body_rc != FC_OK) {
+      if (g) cudaGraphDestroy(g);
+      return body_rc;
+    }
+    FC_CUDA(c, ce);
+    bool ok = false;
+    if (c->enc_exec) {
+      cudaGraphExecUpdateResultInfo info;
+      ok = cudaGraphExecUpdate(c->enc_exec, g, &info) == cudaSuccess;
+      if (!ok) {
+        cudaGetLastError();  // clear the update failure
+        cudaGraphExecDestroy(c->enc_exec);
+        c->enc_exec = nullptr;
+      }
+    }
+    if (!ok) {
+      const cudaError_t ie = cudaGraphInstantiate(&c->enc_exec, g, 0);
+      if (ie != cudaSuccess) {
+        cudaGraphDestroy(g);
+        c->enc_exec = nullptr;
+        return cuda_check(c, ie, "cudaGraphInstantiate");
+      }
+    }
+    cudaGraphDestroy(g);
+    FC_CUDA(c, cudaGraphLaunch(c->enc_exec, c->stream));
+  } else if (body_rc != FC_OK) {
+    return body_rc;
+  }
+  trace_mark(c, "records_launched");
+  FC_TRY(sync_stream(c));
+  trace_mark(c, "records_sync");
   const int64_t n = h_rb[8];
   const int64_t* h_fix = reinterpret_cast<const int64_t*>(h_rb + 16);
   for (int l = 0; l < levels_run; ++l) {

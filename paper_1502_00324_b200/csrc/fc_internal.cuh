@@ -166,6 +166,9 @@ struct Ctx {
   fc_stats enc_stats[kLevels]{};
   cudaEvent_t enc_ev[kLevels][3] = {};
   bool enc_ev_ready = false;
+  bool use_graph = true;               // FC_GRAPH=0 launches the level loop eagerly
+  bool capturing = false;              // the stream is being captured into a graph
+  cudaGraphExec_t enc_exec = nullptr;  // instantiated level-loop graph, updated per encode
   DevBuf iso_inv;  // uint16 [4 sides][8][256] inverse isometry maps
   bool iso_ready = false;
   fc_stats stats{};
@@ -175,6 +178,14 @@ struct Ctx {
 int set_error(Ctx* c, int code, const std::string& msg);
 int cuda_check(Ctx* c, cudaError_t e, const char* what);
 int lut_slot(int n);
+
+// Timing event on the context stream.  Inside a stream capture a plain
+// cudaEventRecord only marks a dependency; the External flag turns it into a
+// real event-record node of the graph, so elapsed times still work.
+inline cudaError_t record_event(Ctx* c, cudaEvent_t ev) {
+  return c->capturing ? cudaEventRecordWithFlags(ev, c->stream, cudaEventRecordExternal)
+                      : cudaEventRecord(ev, c->stream);
+}
 
 // phase tracing (fc_api.cu); no-ops unless FC_TRACE is set
 void trace_reset(Ctx* c);
@@ -204,6 +215,7 @@ int gather_ranges(Ctx* c, Level& L, const int32_t* d_origins, int64_t M);
 int gather_ranges_dev(Ctx* c, Level& L, const int32_t* d_origins, const int32_t* d_M,
                       int64_t M_bound, int32_t* d_hist);
 int roff_hist(Ctx* c, int64_t M, int32_t* d_hist);
+int reserve_ranges(Ctx* c, Level& L, int64_t M);
 int load_ranges(Ctx* c, Level& L, const uint8_t* h_tiles, int64_t M);
 // d_M (optional): device range count <= M (M is then the launch bound)
 int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t n_range_list,
@@ -228,6 +240,8 @@ int level_prepare_tc_finish(Ctx* c, Level& L);  // after a stream sync: layout +
 int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const int32_t* d_hist,
                    uint64_t* d_keys, cudaEvent_t ev_main_end, int64_t* d_fix_pairs);
 int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys);
+// reserve every buffer the level's scan may touch for `bound` ranges (graph capture)
+int reserve_level_scan(Ctx* c, Level& L, int64_t bound);
 
 // fc_encode.cu
 int encode_device(Ctx* c, const double thresholds[3], int baseline, const double* svals,

@@ -518,7 +518,7 @@ int level_prepare_exact(Ctx* c, Level& L, int tc_stats) {
   return FC_OK;
 }
 
-static int reserve_ranges(Ctx* c, Level& L, int64_t M) {
+int reserve_ranges(Ctx* c, Level& L, int64_t M) {
   FC_CUDA(c, c->rtiles.reserve(M * L.n + 64));
   FC_CUDA(c, c->rmean.reserve(M * 8 + 64));
   FC_CUDA(c, c->roff.reserve(M * 4 + 64));

@@ -825,6 +825,44 @@ int level_prepare_tc_finish(Ctx* c, Level& L) {
   return FC_OK;
 }
 
+// Resident A row tiles and B ring depth within the shared-memory budget.
+static int tc_config(Ctx* c, int kpad, TcParams* prm) {
+  prm->kpad = kpad;
+  prm->rg = kpad <= 64 ? 8 : kpad <= 128 ? 4 : kpad <= 320 ? 2 : 1;
+  for (;;) {
+    prm->stages = 8;
+    while (prm->stages > 2 && (int)smem_bytes(*prm) > kSmemBudget) --prm->stages;
+    if ((int)smem_bytes(*prm) <= kSmemBudget || prm->rg == 1) break;
+    prm->rg /= 2;
+  }
+  if ((int)smem_bytes(*prm) > 227 * 1024) return set_error(c, FC_ERR_ARG, "K too large for smem");
+  return FC_OK;
+}
+
+// Every buffer a level's scan may touch, reserved for `bound` ranges ahead of
+// a CUDA-graph capture (nothing may allocate while the stream is captured).
+int reserve_level_scan(Ctx* c, Level& L, int64_t bound) {
+  FC_TRY(ensure_iso_tables(c));
+  FC_TRY(reserve_ranges(c, L, bound));
+  if (L.path != FC_PATH_TENSOR) return FC_OK;
+  TcParams prm{};
+  FC_TRY(tc_config(c, L.tc.kpad, &prm));
+  const int64_t rtiles_max = (bound * 8 + kTileM - 1) / kTileM;
+  const int64_t rows_max = ((rtiles_max + prm.rg - 1) / prm.rg) * prm.rg * kTileM;
+  FC_CUDA(c, c->a_tiles.reserve(rows_max * L.tc.kpad));
+  FC_CUDA(c, c->row_meta.reserve(rows_max * 16));
+  FC_CUDA(c, c->tc_plan.reserve(sizeof(TcPlan) + sizeof(FixPlan) + 64));
+  FC_CUDA(c, c->fix_rows.reserve(bound * 4 + 64));
+  FC_CUDA(c, c->fix_jobs.reserve(512 * 16 + 64));
+  FC_CUDA(c, c->fix_cols.reserve(513 * 8 + 64));
+  if (!c->tc_attr_set) {
+    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    227 * 1024));
+    c->tc_attr_set = true;
+  }
+  return FC_OK;
+}
+
 // Device-driven launch: range count d_M (<= M_bound) and the offset
 // histogram d_hist live on the device; nothing here waits for the GPU.
 int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const int32_t* d_hist,
@@ -834,16 +872,7 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   if (M_bound == 0) return FC_OK;
   FC_TRY(ensure_iso_tables(c));
   TcParams prm{};
-  prm.kpad = T.kpad;
-  // resident A row tiles and B ring depth within the shared-memory budget
-  prm.rg = T.kpad <= 64 ? 8 : T.kpad <= 128 ? 4 : T.kpad <= 320 ? 2 : 1;
-  for (;;) {
-    prm.stages = 8;
-    while (prm.stages > 2 && (int)smem_bytes(prm) > kSmemBudget) --prm.stages;
-    if ((int)smem_bytes(prm) <= kSmemBudget || prm.rg == 1) break;
-    prm.rg /= 2;
-  }
-  if ((int)smem_bytes(prm) > 227 * 1024) return set_error(c, FC_ERR_ARG, "K too large for smem");
+  FC_TRY(tc_config(c, T.kpad, &prm));
   const int RG = prm.rg;
   const int64_t rtiles_max = (M_bound * 8 + kTileM - 1) / kTileM;
   const int64_t rows_max = ((rtiles_max + RG - 1) / RG) * RG * kTileM;
@@ -888,7 +917,7 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   }
   tc_scan_kernel<<<c->sm_count, kThreads, smem, c->stream>>>(prm);
   FC_CUDA(c, cudaGetLastError());
-  if (ev_main_end) FC_CUDA(c, cudaEventRecord(ev_main_end, c->stream));
+  if (ev_main_end) FC_CUDA(c, record_event(c, ev_main_end));
   c->stats.kernel_launches += 1;
 
   // ---- clamp corrections (exact kernel on clamp-active pairs), planned above ----

@@ -231,3 +231,20 @@ def test_encode_records_layout_and_stats():
     for ls in report.level_stats:
         assert ls["comparisons"] == ls["ranges"] * ls["columns"] * 8
         assert ls["scan_ms"] > 0
+
+
+@pytest.mark.parametrize("graph", [0, 1])
+def test_encode_graph_and_eager_identical(graph):
+    """The CUDA-graph level loop and eager launches give the same stream."""
+    g = load_golden("encode_c2.npz")
+    ctx = _native.Context(0)
+    ctx.set_option("graph", graph)
+    img = g["image_c2"]
+    caps = tuple(int(v) for v in g["caps_c2"])
+    strides = tuple(int(v) for v in g["strides_c2"])
+    thr = tuple(float(v) for v in g["thresholds_c2"])
+    params = fc.PoolParams(pool_cap=max(caps), strides=strides, level_caps=caps)
+    cfg = fc.EncoderConfig(pool=params, thresholds=thr)
+    for _ in range(2):  # the second encode exercises the graph update path
+        stream, _ = fc.encode(fc.GrayImage(img), cfg, context=ctx)
+        assert fc.serialize(stream) == g["bytes_c2"].tobytes()
