@@ -146,9 +146,9 @@ int prepare_begin(Ctx* c, Level& L, int level, int baseline, const double* svals
   return FC_OK;
 }
 
-int prepare_finish(Ctx* c, Level& L, int path, int pending) {
+int prepare_finish(Ctx* c, Level& L, int path, int pending, bool launch) {
   if (!pending) return FC_OK;
-  const int r = level_prepare_tc_finish(c, L);
+  const int r = launch ? level_prepare_tc_finish(c, L) : level_prepare_tc_host(c, L);
   if (r == FC_OK) {
     L.path = FC_PATH_TENSOR;
   } else if (path == FC_PATH_TENSOR) {
@@ -190,6 +190,8 @@ int fc_ctx_create(int device, fc_ctx** out) {
   c->sm_count = prop.multiProcessorCount;
   if (const char* t = getenv("FC_TRACE")) c->trace = atoi(t);
   if (const char* g = getenv("FC_GRAPH")) c->use_graph = atoi(g) != 0;
+  if (const char* d = getenv("FC_TC_DEBUG_MODE")) c->tc_debug_mode = atoi(d);
+  if (const char* d = getenv("FC_TC_DEFERRED")) c->tc_deferred = atoi(d);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaEventCreate(&c->ev2) != cudaSuccess || cudaEventCreate(&c->tc_ev[0]) != cudaSuccess ||
@@ -229,10 +231,11 @@ void fc_ctx_destroy(fc_ctx* c) {
   for (auto& L : c->lv) {
     DevBuf* lb[] = {&L.xy, &L.ent, &L.tiles, &L.sum, &L.sumsq, &L.mean, &L.cnorm, &L.qbase,
                     &L.tc.b_tiles, &L.tc.hq, &L.tc.meta, &L.tc.tile_q1, &L.tc.col_stats,
-                    &L.tc.reach_low, &L.tc.reach_high, &L.tc.odd, &L.tc.hist, &L.svals_d, &L.tc.reach_counts,
+                    &L.tc.reach_low, &L.tc.reach_high, &L.tc.odd, &L.tc.hist, &L.svals_d, 
                     &L.win_ent, &L.win_key, &L.win_key2, &L.win_val, &L.win_val2};
     for (DevBuf* b : lb) b->release();
     L.tc.readback.release();
+    L.tc.upload.release();
   }
   cudaEventDestroy(c->ev0);
   cudaEventDestroy(c->ev1);

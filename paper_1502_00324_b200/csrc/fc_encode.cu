@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 
 #include "fc_internal.cuh"
 
@@ -39,6 +40,19 @@ __global__ void top_origins_kernel(int nxt, int32_t n_top, int32_t* __restrict__
   origins[2 * i] = tx * kTop;
   origins[2 * i + 1] = ty * kTop;
   codes[i] = i * 64;
+}
+
+// Level start: candidate keys to "none" and the level's span slots reset
+// (start = max, ends = 0) -- one node instead of a memset.
+__global__ void level_begin_kernel(unsigned long long* __restrict__ keys, int64_t bound,
+                                   unsigned long long* __restrict__ tspan) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < bound) keys[i] = ~0ull;
+  if (i == 0) {
+    tspan[0] = ~0ull;
+    tspan[1] = 0;
+    tspan[2] = 0;
+  }
 }
 
 __device__ __forceinline__ int baseline_offset(double rmean, double s, double dmean) {
@@ -172,26 +186,25 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     FC_CUDA(c, c->enc_orig[b].reserve(max_ranges * 8 + 64));
     FC_CUDA(c, c->enc_code[b].reserve(max_ranges * 4 + 64));
   }
-  FC_CUDA(c, c->enc_count.reserve(64 * 4));
+  FC_CUDA(c, c->enc_count.reserve(kEncBytes + 64));
   FC_CUDA(c, c->enc_hist.reserve(256 * 4 * kLevels));
   FC_CUDA(c, c->leaf_flag.reserve(n_codes * 4 + 64));
   FC_CUDA(c, c->leaf_pos.reserve(n_codes * 4 + 64));
   FC_CUDA(c, c->leaf_rec.reserve(n_codes * 24 + 64));
-  FC_CUDA(c, c->readback.reserve(64 * 4));
+  FC_CUDA(c, c->readback.reserve(kEncBytes + 64));
   FC_CUDA(c, c->keys.reserve(max_ranges * 8 + 64));
   int32_t* d_count = c->enc_count.as<int32_t>();
   int32_t* d_hist = c->enc_hist.as<int32_t>();
   int32_t* h_rb = c->readback.as<int32_t>();
   FC_CUDA(c, cudaMemsetAsync(c->leaf_flag.ptr, 0, n_codes * 4, c->stream));
-  FC_CUDA(c, cudaMemsetAsync(d_count, 0, 16 * 4, c->stream));  // per-level range counters
+  FC_CUDA(c, cudaMemsetAsync(d_count, 0, kEncBytes, c->stream));  // counters, pairs, spans
   top_origins_kernel<<<blocks_for(n_top), 256, 0, c->stream>>>(
       nxt, (int32_t)n_top, c->enc_orig[0].as<int32_t>(), c->enc_code[0].as<int32_t>(), d_count);
   FC_CUDA(c, cudaGetLastError());
   c->total_launches += 1;
 
-  FC_CUDA(c, c->enc_fix.reserve(kLevels * 8 + 64));
-  int64_t* d_fix = c->enc_fix.as<int64_t>();
-  FC_CUDA(c, cudaMemsetAsync(d_fix, 0, kLevels * 8, c->stream));
+  int64_t* d_fix = reinterpret_cast<int64_t*>(c->enc_count.as<uint8_t>() + kEncFixOff);
+  auto* d_time = reinterpret_cast<unsigned long long*>(c->enc_count.as<uint8_t>() + kEncTimeOff);
   auto gather = [&](int l, int cur, int64_t bound) -> int {
     FC_CUDA(c, cudaMemsetAsync(d_hist + 256 * l, 0, 256 * 4, c->stream));
     return gather_ranges_dev(c, c->lv[l], c->enc_orig[cur].as<int32_t>(), d_count + l, bound,
@@ -205,14 +218,18 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   trace_mark(c, "prep_launched");
   FC_TRY(sync_stream(c));
   trace_mark(c, "prep_sync");
-  for (int l = 0; l < kLevels; ++l)
-    if (pending[l]) FC_TRY(prepare_finish(c, c->lv[l], lpath[l], pending[l]));
-
-  // ---- the level loop and the record compaction run as ONE CUDA graph ----
-  // (~45 stream operations per encode; a graph launch cuts the per-operation
-  // launch cost from ~3.7 us to ~0.5-1 us, tools/microbench/launch_gap.cu).
-  // Every buffer is reserved for the level's upper bound first, so nothing
-  // allocates while the stream is being captured.
+  bool tc_launch[kLevels] = {false, false, false, false};
+  for (int l = 0; l < kLevels; ++l) {
+    if (!pending[l]) continue;
+    FC_TRY(prepare_finish(c, c->lv[l], lpath[l], pending[l], /*launch=*/false));
+    tc_launch[l] = c->lv[l].path == FC_PATH_TENSOR;
+  }
+  trace_mark(c, "prep_finished");
+  // ---- operand builds, the level loop and the record compaction run as ONE
+  // CUDA graph (~50 stream operations per encode; a graph launch cuts the
+  // per-operation cost from ~3.7 us to ~0.5-1 us, tools/microbench/launch_gap.cu).
+  // Every buffer is reserved for its upper bound first, so nothing allocates
+  // while the stream is being captured.
   bool use_graph = c->use_graph;
   {
     // range buffers were sized for the largest level before the first gather
@@ -231,15 +248,87 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     FC_CUDA(c, c->cub_tmp.reserve(need));
     FC_CUDA(c, c->rec_out.reserve(n_codes * 24 + 64));
     int64_t total = 0;
-    for (int l = 0; l < kLevels; ++l) total += c->lv[l].count;
+    for (int l = 0; l < kLevels; ++l) {
+      c->coords_off[l] = total;
+      total += c->lv[l].count;
+    }
     FC_CUDA(c, c->coords_pinned.reserve(total * 4 + 16));
   }
+  trace_mark(c, "reserved");
+  // A graph whose every launch parameter (sizes, scalars, buffer addresses)
+  // is unchanged is relaunched as it is: same image geometry, same pools.
+  std::vector<uint64_t> sig;
   if (use_graph) {
+    auto put = [&](uint64_t v) { sig.push_back(v); };
+    auto putd = [&](double v) {
+      uint64_t u;
+      memcpy(&u, &v, 8);
+      put(u);
+    };
+    auto putp = [&](const void* p) { put((uint64_t)(uintptr_t)p); };
+    put(c->width);
+    put(c->height);
+    putp(c->img_ptr);
+    put(baseline);
+    put(path);
+    put(c->sm_count);
+    for (int l = 0; l < 3; ++l) putd(thresholds[l]);
+    for (int l = 0; l < kLevels; ++l) {
+      const Level& L = c->lv[l];
+      const TcOperands& T = L.tc;
+      put(L.count);
+      put(L.n);
+      put(L.s_count);
+      for (int k = 0; k < L.s_count; ++k) putd(L.svals[k]);
+      put(L.path);
+      put(L.baseline);
+      put(tc_launch[l]);
+      put(T.kpad);
+      put(T.planes);
+      put(T.m_digits);
+      put(T.ntiles);
+      put(T.ncols);
+      put(T.n_even);
+      const DevBuf* lb[] = {&L.xy, &L.tiles, &L.mean, &L.qbase, &L.svals_d, &T.b_tiles, &T.meta,
+                            &T.tile_q1, &T.col_stats, &T.reach_low, &T.reach_high, &T.odd};
+      for (const DevBuf* b : lb) putp(b->ptr);
+      putp(T.upload.ptr);
+    }
+    const DevBuf* cb[] = {&c->keys, &c->rtiles, &c->rmean, &c->roff, &c->rsq, &c->a_tiles,
+                          &c->row_meta, &c->tc_plan, &c->fix_rows, &c->fix_jobs, &c->fix_cols,
+                          &c->enc_orig[0], &c->enc_orig[1], &c->enc_code[0], &c->enc_code[1],
+                          &c->enc_count, &c->enc_hist, &c->enc_fix, &c->leaf_flag, &c->leaf_pos,
+                          &c->leaf_rec, &c->rec_out, &c->cub_tmp, &c->iso_inv};
+    for (const DevBuf* b : cb) {
+      putp(b->ptr);
+      put(b->bytes);
+    }
+    putp(c->coords_pinned.ptr);
+    putp(c->readback.ptr);
+    put(c->tc_debug_mode);
+    put(c->tc_deferred);
+  }
+  const bool reuse = use_graph && !c->trace && c->enc_exec && sig == c->enc_sig;
+  int levels_run = 0;
+  const int64_t launches_body0 = c->total_launches;
+  if (reuse) {
+    levels_run = c->enc_levels_run;
+    c->total_launches += c->enc_body_launches;
+    for (int l = 0; l < kLevels; ++l) {
+      c->enc_stats[l].kernel_launches = c->enc_level_launches[l];
+      c->enc_stats[l].path = c->lv[l].path;
+      if (tc_launch[l]) c->lv[l].tc.ready = true;
+    }
+    c->coords_valid = true;
+    FC_CUDA(c, cudaGraphLaunch(c->enc_exec, c->stream));
+  }
+  if (!reuse && use_graph) {
     FC_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     c->capturing = true;
   }
-  int levels_run = 0;
-  const int body_rc = [&]() -> int {
+  const int body_rc = reuse ? FC_OK : [&]() -> int {
+  for (int l = 0; l < kLevels; ++l)
+    if (tc_launch[l]) FC_TRY(level_prepare_tc_launch(c, c->lv[l]));
 
   // ---- level loop: no host synchronisation ----
   int cur = 0;
@@ -261,15 +350,15 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     const int32_t* d_M = d_count + l;
     const int64_t launches_before = c->total_launches + c->stats.kernel_launches;
     uint64_t* keys = c->keys.as<uint64_t>();
-    FC_CUDA(c, cudaMemsetAsync(keys, 0xff, bound * 8, c->stream));
-    FC_CUDA(c, record_event(c, c->enc_ev[l][0]));
+    unsigned long long* tspan = d_time + 4 * l;
+    level_begin_kernel<<<blocks_for(bound), 256, 0, c->stream>>>(
+        reinterpret_cast<unsigned long long*>(keys), bound, tspan);
+    c->total_launches += 1;
     if (L.path == FC_PATH_TENSOR) {
-      FC_TRY(scan_tc_launch(c, L, bound, d_M, d_hist + 256 * l, keys, c->enc_ev[l][1], d_fix + l));
+      FC_TRY(scan_tc_launch(c, L, bound, d_M, d_hist + 256 * l, keys, nullptr, d_fix + l, tspan));
     } else {
-      FC_TRY(scan_exact(c, L, bound, nullptr, 0, nullptr, 0, keys, d_M));
-      FC_CUDA(c, record_event(c, c->enc_ev[l][1]));
+      FC_TRY(scan_exact(c, L, bound, nullptr, 0, nullptr, 0, keys, d_M, tspan));
     }
-    FC_CUDA(c, record_event(c, c->enc_ev[l][2]));
     const int side = L.side;
     const int can_split = l < kLevels - 1;
     double thr2 = 0.0;
@@ -315,15 +404,9 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
         n_codes, flag, pos, c->leaf_rec.as<int32_t>(), c->rec_out.as<int32_t>(), d_count + 8);
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 2;
-    FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count, 16 * 4, cudaMemcpyDeviceToHost, c->stream));
-    FC_CUDA(c, cudaMemcpyAsync(h_rb + 16, d_fix, kLevels * 8, cudaMemcpyDeviceToHost, c->stream));
+    FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count, kEncBytes, cudaMemcpyDeviceToHost, c->stream));
     // the stream header needs every pool's origins: fetch them with this sync
     {
-      int64_t total = 0;
-      for (int l = 0; l < kLevels; ++l) {
-        c->coords_off[l] = total;
-        total += c->lv[l].count;
-      }
       for (int l = 0; l < kLevels; ++l)
         if (c->lv[l].count)
           FC_CUDA(c, cudaMemcpyAsync(c->coords_pinned.as<uint32_t>() + c->coords_off[l],
@@ -334,7 +417,12 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   }
   return FC_OK;
   }();
-  if (use_graph) {
+  if (!reuse) {
+    c->enc_levels_run = levels_run;
+    c->enc_body_launches = c->total_launches - launches_body0;
+    for (int l = 0; l < kLevels; ++l) c->enc_level_launches[l] = c->enc_stats[l].kernel_launches;
+  }
+  if (use_graph && !reuse) {
     cudaGraph_t g = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
     c->capturing = false;
@@ -342,7 +430,9 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
       if (g) cudaGraphDestroy(g);
       return body_rc;
     }
+    c->enc_sig.clear();
     FC_CUDA(c, ce);
+    trace_mark(c, "captured");
     bool ok = false;
     if (c->enc_exec) {
       cudaGraphExecUpdateResultInfo info;
@@ -362,6 +452,8 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
       }
     }
     cudaGraphDestroy(g);
+    c->enc_sig = sig;
+    trace_mark(c, "exec_ready");
     FC_CUDA(c, cudaGraphLaunch(c->enc_exec, c->stream));
   } else if (body_rc != FC_OK) {
     return body_rc;
@@ -370,7 +462,9 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   FC_TRY(sync_stream(c));
   trace_mark(c, "records_sync");
   const int64_t n = h_rb[8];
-  const int64_t* h_fix = reinterpret_cast<const int64_t*>(h_rb + 16);
+  const int64_t* h_fix = reinterpret_cast<const int64_t*>(c->readback.as<uint8_t>() + kEncFixOff);
+  const auto* h_time =
+      reinterpret_cast<const unsigned long long*>(c->readback.as<uint8_t>() + kEncTimeOff);
   for (int l = 0; l < levels_run; ++l) {
     Level& L = c->lv[l];
     fc_stats& st = c->enc_stats[l];
@@ -385,12 +479,13 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   for (int l = 0; l < kLevels; ++l) {
     fc_stats& st = c->enc_stats[l];
     if (st.ranges == 0) continue;
-    float a = 0.f, b = 0.f;
-    cudaEventElapsedTime(&a, c->enc_ev[l][0], c->enc_ev[l][1]);
-    cudaEventElapsedTime(&b, c->enc_ev[l][1], c->enc_ev[l][2]);
-    st.main_ms = a;
-    st.fix_ms = b;
-    st.scan_ms = a + b;
+    // spans stamped by the kernels themselves (global ns): contraction or exact
+    // scan, then the clamp corrections
+    const unsigned long long* t = h_time + 4 * l;
+    const double t0 = (double)t[0], t1 = (double)t[1], t2 = (double)std::max(t[2], t[1]);
+    st.main_ms = t[1] > t[0] ? (float)((t1 - t0) * 1e-6) : 0.f;
+    st.fix_ms = t[1] > t[0] ? (float)((t2 - t1) * 1e-6) : 0.f;
+    st.scan_ms = st.main_ms + st.fix_ms;
   }
   (void)launches0;
   trace_dump(c);

@@ -19,6 +19,8 @@ constexpr int kMaxS = 16;
 // so small correction sets still spread over the SMs)
 __host__ __device__ constexpr int ranges_per_block(int n) { return n >= 256 ? 2 : n >= 64 ? 4 : 8; }
 constexpr int kTcHistWords = 1024 + 1024 + 4;  // qmin | qmax histograms, q2max, pad
+constexpr int kUpCursorBytes = 2048 * 4;        // tensor-operand upload image layout
+constexpr int kUpReachBytes = 512 * 8;
 
 struct Status {
   int code = FC_OK;
@@ -82,12 +84,13 @@ struct TcOperands {
   DevBuf b_tiles;        // int8 [ntiles][kpad/16][32 groups][8][16]   (UMMA K-major, no swizzle)
   DevBuf hq;             // (unused; kept for ABI-stable struct layout in tools)
   DevBuf meta;           // uint32 [ntiles*256]: (Q2 & 1) << 31 | column, 0xffffffff = padding
-  DevBuf tile_q1;        // (unused)
+  DevBuf tile_q1;        // device upload image: cursors [2048 i32] | reach counts [512 i64] | tile info
   DevBuf col_stats;      // int4 [ncols]: {Q1, Q2, qmin, qmax} (unsorted order)
   DevBuf reach_low;      // int32 [ncols]: columns sorted by qmin ascending
   DevBuf reach_high;     // int32 [ncols]: columns sorted by qmax descending
   DevBuf odd;            // int32 [2*ncols]: parity flags, then their exclusive prefix
-  DevBuf reach_counts;   // int64 [512]: low_count | high_count on the device
+  PinnedBuf upload;      // pinned image of cursors | reach counts | tile info
+  int64_t n_even = 0, n_odd = 0;  // columns per parity group
   DevBuf hist;           // u32 [1024 qmin | 1024 qmax | q2max | pad]
   PinnedBuf readback;    // pinned copy of hist + last prefix/flag (prepare begin -> finish)
   int64_t low_count[256] = {0};   // #{columns with qmin < -o}      (clamp at 0 possible)
@@ -168,7 +171,13 @@ struct Ctx {
   bool enc_ev_ready = false;
   bool use_graph = true;               // FC_GRAPH=0 launches the level loop eagerly
   bool capturing = false;              // the stream is being captured into a graph
+  int tc_debug_mode = 0;               // FC_TC_DEBUG_MODE (pipeline probes)
+  int tc_deferred = -1;                // FC_TC_DEFERRED: -1 = by K, 0/1 forced
   cudaGraphExec_t enc_exec = nullptr;  // instantiated level-loop graph, updated per encode
+  std::vector<uint64_t> enc_sig;       // launch signature of enc_exec (reuse when equal)
+  int enc_levels_run = 0;              // host-side results of the captured body
+  int64_t enc_body_launches = 0;
+  int32_t enc_level_launches[kLevels] = {0, 0, 0, 0};
   DevBuf iso_inv;  // uint16 [4 sides][8][256] inverse isometry maps
   bool iso_ready = false;
   fc_stats stats{};
@@ -178,6 +187,20 @@ struct Ctx {
 int set_error(Ctx* c, int code, const std::string& msg);
 int cuda_check(Ctx* c, cudaError_t e, const char* what);
 int lut_slot(int n);
+
+// Device timestamps (ns) for per-kernel spans inside CUDA graphs: kernels
+// atomicMin their start / atomicMax their end into u64 slots.
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+// enc_count buffer layout: int32 counters [16] | int64 clamp pairs [4] | u64 spans [4][4]
+constexpr int kEncFixOff = 64;
+constexpr int kEncTimeOff = 96;
+constexpr int kEncBytes = 96 + 4 * 4 * 8;
 
 // Timing event on the context stream.  Inside a stream capture a plain
 // cudaEventRecord only marks a dependency; the External flag turns it into a
@@ -199,7 +222,8 @@ int sync_stream(Ctx* c);
 // fc_api.cu: operand preparation around a shared synchronisation
 int prepare_begin(Ctx* c, Level& L, int level, int baseline, const double* svals, int s_count,
                   int path, int* pending);
-int prepare_finish(Ctx* c, Level& L, int path, int pending);
+// launch = false: host half only (fc_encode issues level_prepare_tc_launch itself)
+int prepare_finish(Ctx* c, Level& L, int path, int pending, bool launch = true);
 
 // fc_pool.cu
 int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
@@ -220,11 +244,11 @@ int load_ranges(Ctx* c, Level& L, const uint8_t* h_tiles, int64_t M);
 // d_M (optional): device range count <= M (M is then the launch bound)
 int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t n_range_list,
                const int32_t* d_col_list, int64_t n_col_list, uint64_t* d_keys,
-               const int32_t* d_M = nullptr);
+               const int32_t* d_M = nullptr, unsigned long long* d_time = nullptr);
 int scan_exact_jobs(Ctx* c, Level& L, const int4* d_jobs, const int64_t* d_prefix,
                     const int* d_n_jobs, const long long* d_total_blocks,
                     const int32_t* d_sorted_ranges, const int32_t* d_low, const int32_t* d_high,
-                    uint64_t* d_keys);
+                    uint64_t* d_keys, unsigned long long* d_time_end = nullptr);
 int decode_keys(Ctx* c, const uint64_t* d_keys, int64_t M, int64_t* d_err, int64_t* d_idx);
 int iso_table_offset(int side);
 int scan_rows_dropin(Ctx* c, const int16_t* ranges, const double* rmeans, int64_t M, int32_t n,
@@ -234,11 +258,15 @@ int scan_rows_dropin(Ctx* c, const int16_t* ranges, const double* rmeans, int64_
 // fc_scan_tc.cu
 int level_prepare_tc_begin(Ctx* c, Level& L);   // device stats + async readback
 int level_prepare_tc_finish(Ctx* c, Level& L);  // after a stream sync: layout + operand build
+int level_prepare_tc_host(Ctx* c, Level& L);    // the host half of it (no launches)
+int level_prepare_tc_launch(Ctx* c, Level& L);  // the stream half (capturable)
 // Launch the contraction and its clamp corrections for *d_M (<= M_bound)
 // gathered ranges; d_hist[o] = #ranges with offset o.  No synchronisation:
 // the unit decomposition and the correction jobs are planned on the device.
+// d_time (optional): u64 [3] span slots {contraction start, contraction end, fix end}
 int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const int32_t* d_hist,
-                   uint64_t* d_keys, cudaEvent_t ev_main_end, int64_t* d_fix_pairs);
+                   uint64_t* d_keys, cudaEvent_t ev_main_end, int64_t* d_fix_pairs,
+                   unsigned long long* d_time = nullptr);
 int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys);
 // reserve every buffer the level's scan may touch for `bound` ranges (graph capture)
 int reserve_level_scan(Ctx* c, Level& L, int64_t bound);

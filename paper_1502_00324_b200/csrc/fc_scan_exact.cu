@@ -165,7 +165,7 @@ scan_exact_kernel(const int16_t* __restrict__ qbase, int64_t ncols, int S,
                   int64_t M, const int32_t* __restrict__ d_M, const uint16_t* __restrict__ inv,
                   const int32_t* __restrict__ range_list, int64_t n_range_list, int64_t range_base,
                   const int32_t* __restrict__ col_list, int64_t n_col_list, int baseline,
-                  unsigned long long* __restrict__ keys) {
+                  unsigned long long* __restrict__ keys, unsigned long long* __restrict__ tspan) {
   __shared__ __align__(16) ExactSmem<N> s;
   constexpr int RB = ExactSmem<N>::RB;
   const int tid = threadIdx.x;
@@ -173,6 +173,7 @@ scan_exact_kernel(const int16_t* __restrict__ qbase, int64_t ncols, int S,
   const int64_t nrange = range_list ? n_range_list : M;
   const int64_t r0 = range_base + (int64_t)blockIdx.y * RB;
   if (r0 >= nrange) return;  // block-uniform (device range count below the launch bound)
+  if (tspan && tid == 0) atomicMin(&tspan[0], global_ns());
   if (tid < RB) {
     const int64_t idx = r0 + tid;
     int m = -1;
@@ -185,6 +186,11 @@ scan_exact_kernel(const int16_t* __restrict__ qbase, int64_t ncols, int S,
   const int64_t col = ci < ncol_eff ? (col_list ? (int64_t)col_list[ci] : ci) : -1;
   __syncthreads();
   exact_block<N>(s, qbase, S, svals, dmean, rtiles, inv, col, baseline, keys);
+  if (tspan && tid == 0) {
+    const unsigned long long t = global_ns();
+    atomicMax(&tspan[1], t);
+    atomicMax(&tspan[2], t);
+  }
 }
 
 // Job-list scan (tensor-path clamp corrections): job j covers the ranges
@@ -200,7 +206,7 @@ scan_jobs_kernel(const int16_t* __restrict__ qbase, int S, const double* __restr
                  const int* __restrict__ d_n_jobs, const long long* __restrict__ d_total,
                  const int32_t* __restrict__ sorted_ranges, const int32_t* __restrict__ list_low,
                  const int32_t* __restrict__ list_high, int baseline,
-                 unsigned long long* __restrict__ keys) {
+                 unsigned long long* __restrict__ keys, unsigned long long* __restrict__ t_end) {
   __shared__ __align__(16) ExactSmem<N> s;
   __shared__ int s_job;
   const int tid = threadIdx.x;
@@ -234,6 +240,7 @@ scan_jobs_kernel(const int16_t* __restrict__ qbase, int S, const double* __restr
     __syncthreads();
     exact_block<N>(s, qbase, S, svals, dmean, rtiles, inv, col, baseline, keys);
   }
+  if (t_end && tid == 0) atomicMax(t_end, global_ns());
 }
 
 // Drop-in for _scan.py:14 with arbitrary candidate rows (reference layout).
@@ -576,7 +583,7 @@ int load_ranges(Ctx* c, Level& L, const uint8_t* h_tiles, int64_t M) {
 
 int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t n_range_list,
                const int32_t* d_col_list, int64_t n_col_list, uint64_t* d_keys,
-               const int32_t* d_M) {
+               const int32_t* d_M, unsigned long long* d_time) {
   FC_TRY(ensure_iso_tables(c));
   const int64_t ncols = L.count * L.s_count;
   const int64_t nr = d_range_list ? n_range_list : M;
@@ -597,7 +604,7 @@ int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t
         L.qbase.as<int16_t>(), ncols, L.s_count, d_s, L.mean.as<double>(),                      \
         c->rtiles.as<uint8_t>(), c->rmean.as<double>(), nlist, d_M, inv, d_range_list,          \
         n_range_list,                                                                           \
-        base, d_col_list, n_col_list, L.baseline, keys)
+        base, d_col_list, n_col_list, L.baseline, keys, d_time)
     switch (L.n) {
       case 256: FC_LAUNCH_EXACT(256); break;
       case 64: FC_LAUNCH_EXACT(64); break;
@@ -614,7 +621,7 @@ int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t
 int scan_exact_jobs(Ctx* c, Level& L, const int4* d_jobs, const int64_t* d_prefix,
                     const int* d_n_jobs, const long long* d_total_blocks,
                     const int32_t* d_sorted_ranges, const int32_t* d_low, const int32_t* d_high,
-                    uint64_t* d_keys) {
+                    uint64_t* d_keys, unsigned long long* d_time_end) {
   FC_TRY(ensure_iso_tables(c));
   const double* d_s = L.svals_d.as<double>();
   const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
@@ -624,7 +631,7 @@ int scan_exact_jobs(Ctx* c, Level& L, const int4* d_jobs, const int64_t* d_prefi
   scan_jobs_kernel<NN><<<grid, kColsPerBlock, 0, c->stream>>>(                                  \
       L.qbase.as<int16_t>(), L.s_count, d_s, L.mean.as<double>(), c->rtiles.as<uint8_t>(),        \
       c->rmean.as<double>(), inv, d_jobs, d_prefix, d_n_jobs, d_total_blocks, d_sorted_ranges,    \
-      d_low, d_high, L.baseline, keys)
+      d_low, d_high, L.baseline, keys, d_time_end)
   switch (L.n) {
     case 256: FC_LAUNCH_JOBS(256); break;
     case 64: FC_LAUNCH_JOBS(64); break;

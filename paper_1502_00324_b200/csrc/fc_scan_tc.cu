@@ -89,6 +89,7 @@ struct TcParams {
   int ntiles;
   const TcPlan* plan;
   int deferred;    // 1: resolve the winning column once per unit (short K)
+  unsigned long long* tspan;  // optional {start, end} slots (global ns)
   int debug_mode;  // 1: epilogue only drains TMEM (pipeline probe; results invalid)
 };
 
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (p.tspan && threadIdx.x == 0) atomicMin(&p.tspan[0], global_ns());
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -391,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   __syncthreads();
   ptx::tc_fence_after();
   if (warp == 2) ptx::tmem_dealloc(tmem_base, 512);
+  if (p.tspan && threadIdx.x == 0) atomicMax(&p.tspan[1], global_ns());
 }
 
 // ---------------------------------------------------------------------------
@@ -724,9 +727,10 @@ int level_prepare_tc_begin(Ctx* c, Level& L) {
   return FC_OK;
 }
 
-// Phase 2 (host, after the stream reached the readback): K layout, tile
-// table, clamp-reach lists and the grouped B operand.  Nothing blocks.
-int level_prepare_tc_finish(Ctx* c, Level& L) {
+// Phase 2a (host, after the stream reached the readback): K layout, tile
+// table and clamp-reach counts, written into the level's pinned upload
+// buffer; every device buffer of the operand set is reserved.  No launches.
+int level_prepare_tc_host(Ctx* c, Level& L) {
   TcOperands& T = L.tc;
   const int64_t ncols = T.ncols;
   const unsigned* h = T.readback.as<unsigned>();
@@ -748,81 +752,83 @@ int level_prepare_tc_finish(Ctx* c, Level& L) {
   if (c->trace)
     fprintf(stderr, "[fc_trace] tc operands B=%d cols=%lld planes=%d m_digits=%d kpad=%d\n", L.side,
             (long long)ncols, T.planes, T.m_digits, T.kpad);
-  // clamp-reach counts: low_count[o] = #{qmin < -o}, high_count[o] = #{qmax > 255 - o}
-  {
-    // prefix sums over the histograms (bin v holds q = v - 512)
-    std::vector<int64_t> cmin(1025, 0), cmax(1025, 0);
-    for (int v = 0; v < 1024; ++v) {
-      cmin[v + 1] = cmin[v] + hmin[v];
-      cmax[v + 1] = cmax[v] + hmax[v];
-    }
-    for (int o = 0; o < 256; ++o) {
-      // q < -o  <=>  v = q + 512 < 512 - o
-      T.low_count[o] = cmin[512 - o];
-      // q > 255 - o  <=>  v > 767 - o
-      T.high_count[o] = cmax[1024] - cmax[768 - o];
-    }
-  }
-  FC_CUDA(c, T.reach_counts.reserve(512 * 8));
-  {
-    long long rc[512];
-    for (int o = 0; o < 256; ++o) {
-      rc[o] = T.low_count[o];
-      rc[256 + o] = T.high_count[o];
-    }
-    FC_TRY(stage_h2d(c, T.reach_counts.ptr, rc, sizeof rc));
-  }
   // two parity groups, each padded to whole tiles
   const int64_t n_odd = (int64_t)last_prefix + last_odd;
-  const int64_t n_even = ncols - n_odd;
-  const int64_t tiles_even = (n_even + kTileN - 1) / kTileN;
+  T.n_even = ncols - n_odd;
+  T.n_odd = n_odd;
+  const int64_t tiles_even = (T.n_even + kTileN - 1) / kTileN;
   const int64_t tiles_odd = (n_odd + kTileN - 1) / kTileN;
   T.ntiles = tiles_even + tiles_odd;
-  const int64_t odd_base = tiles_even * kTileN;
-  std::vector<int2> tinfo(T.ntiles);
+  // pinned upload image: cursors [2048 i32] | reach counts [512 i64] | tile info [ntiles int2]
+  FC_CUDA(c, T.upload.reserve(kUpCursorBytes + kUpReachBytes + T.ntiles * 8 + 16));
+  int32_t* cur = T.upload.as<int32_t>();
+  long long* rc = reinterpret_cast<long long*>(T.upload.as<uint8_t>() + kUpCursorBytes);
+  int2* tinfo = reinterpret_cast<int2*>(T.upload.as<uint8_t>() + kUpCursorBytes + kUpReachBytes);
+  // clamp-reach counts: low_count[o] = #{qmin < -o}, high_count[o] = #{qmax > 255 - o};
+  // counting-sort cursors: qmin ascending | qmax descending
+  int64_t cmin[1025], cmax[1025];
+  cmin[0] = cmax[0] = 0;
+  int32_t acc_lo = 0;
+  for (int v = 0; v < 1024; ++v) {
+    cmin[v + 1] = cmin[v] + hmin[v];
+    cmax[v + 1] = cmax[v] + hmax[v];
+    cur[v] = acc_lo;
+    acc_lo += (int32_t)hmin[v];
+  }
+  int32_t acc_hi = 0;
+  for (int v = 1023; v >= 0; --v) {
+    cur[1024 + v] = acc_hi;
+    acc_hi += (int32_t)hmax[v];
+  }
+  for (int o = 0; o < 256; ++o) {
+    T.low_count[o] = cmin[512 - o];                    // q < -o      <=> v < 512 - o
+    T.high_count[o] = cmax[1024] - cmax[768 - o];      // q > 255 - o <=> v > 767 - o
+    rc[o] = T.low_count[o];
+    rc[256 + o] = T.high_count[o];
+  }
   for (int64_t t = 0; t < tiles_even; ++t)
-    tinfo[t] = make_int2(0, (int)std::min<int64_t>(kTileN, n_even - t * kTileN));
+    tinfo[t] = make_int2(0, (int)std::min<int64_t>(kTileN, T.n_even - t * kTileN));
   for (int64_t t = 0; t < tiles_odd; ++t)
     tinfo[tiles_even + t] = make_int2(1, (int)std::min<int64_t>(kTileN, n_odd - t * kTileN));
-  // clamp-reach column lists: qmin ascending / qmax descending, by counting sort
-  {
-    std::vector<int32_t> cur(2048);
-    int32_t acc_lo = 0, acc_hi = 0;
-    for (int v = 0; v < 1024; ++v) {
-      cur[v] = acc_lo;
-      acc_lo += (int32_t)hmin[v];
-    }
-    for (int v = 1023; v >= 0; --v) {
-      cur[1024 + v] = acc_hi;
-      acc_hi += (int32_t)hmax[v];
-    }
-    FC_CUDA(c, T.reach_low.reserve(ncols * 4));
-    FC_CUDA(c, T.reach_high.reserve(ncols * 4));
-    FC_CUDA(c, c->key_out.reserve(2048 * 4));
-    int32_t* d_cur = c->key_out.as<int32_t>();
-    FC_TRY(stage_h2d(c, d_cur, cur.data(), 2048 * 4));
-    reach_scatter_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, c->stream>>>(
-        T.col_stats.as<int4>(), ncols, d_cur, d_cur + 1024, T.reach_low.as<int32_t>(),
-        T.reach_high.as<int32_t>());
-    FC_CUDA(c, cudaGetLastError());
-    c->total_launches += 1;
-  }
-  // grouped operand + column map + tile info
   const int64_t slots = T.ntiles * kTileN;
+  FC_CUDA(c, T.reach_low.reserve(ncols * 4));
+  FC_CUDA(c, T.reach_high.reserve(ncols * 4));
   FC_CUDA(c, T.b_tiles.reserve(slots * T.kpad));
   FC_CUDA(c, T.meta.reserve(slots * 4));
-  FC_CUDA(c, T.tile_q1.reserve(T.ntiles * 8 + 16));
-  FC_TRY(stage_h2d(c, T.tile_q1.ptr, tinfo.data(), T.ntiles * 8));
+  // device copy of the upload image (same layout): cursors | reach counts | tile info
+  FC_CUDA(c, T.tile_q1.reserve(kUpCursorBytes + kUpReachBytes + T.ntiles * 8 + 16));
+  return FC_OK;
+}
+
+// Phase 2b (stream-ordered, capturable): upload the pinned image, build the
+// clamp-reach lists and the grouped B operand (+ column map).
+int level_prepare_tc_launch(Ctx* c, Level& L) {
+  TcOperands& T = L.tc;
+  const int64_t ncols = T.ncols;
+  const uint8_t* up = T.upload.as<uint8_t>();
+  FC_CUDA(c, cudaMemcpyAsync(T.tile_q1.ptr, up, kUpCursorBytes + kUpReachBytes + T.ntiles * 8,
+                             cudaMemcpyHostToDevice, c->stream));
+  int32_t* d_cur = T.tile_q1.as<int32_t>();
+  reach_scatter_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, c->stream>>>(
+      T.col_stats.as<int4>(), ncols, d_cur, d_cur + 1024, T.reach_low.as<int32_t>(),
+      T.reach_high.as<int32_t>());
+  const int64_t slots = T.ntiles * kTileN;
+  const int64_t odd_base = ((T.n_even + kTileN - 1) / kTileN) * kTileN;
   const int64_t n_pad = slots - ncols;
   const int64_t work = (ncols + n_pad) * (T.kpad / 16);
   build_b_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
       L.qbase.as<int16_t>(), L.n, T.kpad, T.planes, T.m_digits, ncols, T.col_stats.as<int4>(),
-      T.odd.as<int32_t>() + ncols, odd_base, n_even, n_odd, n_pad, T.b_tiles.as<int8_t>(),
+      T.odd.as<int32_t>() + ncols, odd_base, T.n_even, T.n_odd, n_pad, T.b_tiles.as<int8_t>(),
       T.meta.as<int32_t>());
   FC_CUDA(c, cudaGetLastError());
-  c->total_launches += 1;
+  c->total_launches += 2;
   T.ready = true;
   return FC_OK;
+}
+
+int level_prepare_tc_finish(Ctx* c, Level& L) {
+  FC_TRY(level_prepare_tc_host(c, L));
+  return level_prepare_tc_launch(c, L);
 }
 
 // Resident A row tiles and B ring depth within the shared-memory budget.
@@ -866,7 +872,8 @@ int reserve_level_scan(Ctx* c, Level& L, int64_t bound) {
 // Device-driven launch: range count d_M (<= M_bound) and the offset
 // histogram d_hist live on the device; nothing here waits for the GPU.
 int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const int32_t* d_hist,
-                   uint64_t* d_keys, cudaEvent_t ev_main_end, int64_t* d_fix_pairs) {
+                   uint64_t* d_keys, cudaEvent_t ev_main_end, int64_t* d_fix_pairs,
+                   unsigned long long* d_time) {
   TcOperands& T = L.tc;
   if (!T.ready) return set_error(c, FC_ERR_STATE, "tensor operands not prepared");
   if (M_bound == 0) return FC_OK;
@@ -885,7 +892,8 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   FC_CUDA(c, c->fix_jobs.reserve(512 * 16 + 64));
   FC_CUDA(c, c->fix_cols.reserve(513 * 8 + 64));
   level_plan_kernel<<<1, kPlanThreads, 0, c->stream>>>(
-      d_M, RG, (int)T.ntiles, c->sm_count, d_hist, T.reach_counts.as<long long>(),
+      d_M, RG, (int)T.ntiles, c->sm_count, d_hist,
+      reinterpret_cast<const long long*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes),
       ranges_per_block(L.n), c->roff.as<int32_t>(), d_plan, c->fix_jobs.as<int4>(),
       c->fix_cols.as<long long>(), d_fplan, c->fix_rows.as<int32_t>(),
       reinterpret_cast<long long*>(d_fix_pairs));
@@ -901,14 +909,16 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   prm.row_meta = c->row_meta.as<int4>();
   prm.b_tiles = T.b_tiles.as<int8_t>();
   prm.colmap = T.meta.as<int32_t>();
-  prm.tile_info = T.tile_q1.as<int2>();
+  prm.tile_info = reinterpret_cast<const int2*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes +
+                                                kUpReachBytes);
   prm.keys = reinterpret_cast<unsigned long long*>(d_keys);
   prm.S = L.s_count;
   prm.ntiles = (int)T.ntiles;
   prm.plan = d_plan;
-  if (const char* dbg = getenv("FC_TC_DEBUG_MODE")) prm.debug_mode = atoi(dbg);
-  prm.deferred = T.kpad <= 64 ? 1 : 0;  // measured: recompute wins only for short K
-  if (const char* d = getenv("FC_TC_DEFERRED")) prm.deferred = atoi(d);
+  prm.tspan = d_time;
+  prm.debug_mode = c->tc_debug_mode;
+  // measured: the per-unit recompute wins only for short K
+  prm.deferred = c->tc_deferred >= 0 ? c->tc_deferred : (T.kpad <= 64 ? 1 : 0);
   const uint32_t smem = smem_bytes(prm);
   if (!c->tc_attr_set) {
     FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -923,7 +933,8 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   // ---- clamp corrections (exact kernel on clamp-active pairs), planned above ----
   FC_TRY(scan_exact_jobs(c, L, c->fix_jobs.as<int4>(), c->fix_cols.as<int64_t>(),
                          &d_fplan->n_jobs, &d_fplan->total_blocks, c->fix_rows.as<int32_t>(),
-                         T.reach_low.as<int32_t>(), T.reach_high.as<int32_t>(), d_keys));
+                         T.reach_low.as<int32_t>(), T.reach_high.as<int32_t>(), d_keys,
+                         d_time ? d_time + 2 : nullptr));
   return FC_OK;
 }
 
