@@ -106,8 +106,9 @@ int level_ready(Ctx* c, int level) {
 // levels share it (fc_encode).  *pending = 1 when a tensor-path readback is
 // in flight and prepare_finish must run after the next sync.
 int prepare_begin(Ctx* c, Level& L, int level, int baseline, const double* svals, int s_count,
-                  int path, int* pending) {
+                  int path, int* pending, int* needs_prep) {
   *pending = 0;
+  *needs_prep = 0;
   if (s_count < 1 || s_count > kMaxS || !svals)
     return set_error(c, FC_ERR_ARG, "s set must have 1..16 values");
   for (int i = 0; i < s_count; ++i)
@@ -127,19 +128,18 @@ int prepare_begin(Ctx* c, Level& L, int level, int baseline, const double* svals
   for (int i = 0; i < s_count; ++i) L.svals[i] = svals[i];
   L.prepared = false;
   L.tc.ready = false;
+  *needs_prep = 1;
   const bool tc_ok = !L.baseline && L.n >= 16;
   if (path == FC_PATH_TENSOR && !tc_ok)
     return set_error(c, FC_ERR_ARG, "tensor path needs proposed mode and B >= 4");
-  const bool want_tc = path == FC_PATH_TENSOR || (path == FC_PATH_AUTO && tc_ok);
-  FC_TRY(level_prepare_exact(c, L, want_tc ? 1 : 0));
+  bool want_tc = path == FC_PATH_TENSOR || (path == FC_PATH_AUTO && tc_ok);
+  if (want_tc && L.count * L.s_count >= (1ll << 31) - 1024) {
+    if (path == FC_PATH_TENSOR) return set_error(c, FC_ERR_ARG, "too many columns");
+    want_tc = false;  // auto: keep the exact path
+  }
   if (want_tc) {
-    const int r = level_prepare_tc_begin(c, L);
-    if (r == FC_OK) {
-      *pending = 1;
-      return FC_OK;
-    }
-    if (path == FC_PATH_TENSOR) return r;
-    c->st = Status{};  // auto: keep the exact path
+    *pending = 1;
+    return FC_OK;
   }
   L.path = FC_PATH_EXACT;
   L.prepared = true;
@@ -223,6 +223,9 @@ void fc_ctx_destroy(fc_ctx* c) {
   c->up_arena.release();
   c->readback.release();
   c->pool_rb.release();
+  c->prep_dev.release();
+  c->chunk_odd.release();
+  c->prep_rb.release();
   c->coords_pinned.release();
   if (c->enc_ev_ready)
     for (auto& pr : c->enc_ev)
@@ -231,10 +234,9 @@ void fc_ctx_destroy(fc_ctx* c) {
   for (auto& L : c->lv) {
     DevBuf* lb[] = {&L.xy, &L.ent, &L.tiles, &L.sum, &L.sumsq, &L.mean, &L.cnorm, &L.qbase,
                     &L.tc.b_tiles, &L.tc.hq, &L.tc.meta, &L.tc.tile_q1, &L.tc.col_stats,
-                    &L.tc.reach_low, &L.tc.reach_high, &L.tc.odd, &L.tc.hist, &L.svals_d, 
+                    &L.tc.reach_low, &L.tc.reach_high, &L.tc.odd, &L.svals_d, 
                     &L.win_ent, &L.win_key, &L.win_key2, &L.win_val, &L.win_val2};
     for (DevBuf* b : lb) b->release();
-    L.tc.readback.release();
     L.tc.upload.release();
   }
   cudaEventDestroy(c->ev0);
@@ -366,8 +368,13 @@ int fc_level_prepare(fc_ctx* c, int level, int baseline, const double* svals, in
   cudaSetDevice(c->device);
   FC_TRY(level_ready(c, level));
   Level& L = c->lv[level - 1];
-  int pending = 0;
-  FC_TRY(prepare_begin(c, L, level, baseline, svals, s_count, path, &pending));
+  int pending = 0, needs = 0;
+  FC_TRY(prepare_begin(c, L, level, baseline, svals, s_count, path, &pending, &needs));
+  if (needs) {
+    Level* lv[1] = {&L};
+    const int st[1] = {pending};
+    FC_TRY(prep_launch(c, lv, st, 1));
+  }
   if (pending) FC_TRY(sync_stream(c));
   return prepare_finish(c, L, path, pending);
 }

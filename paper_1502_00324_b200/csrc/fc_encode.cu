@@ -167,15 +167,24 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   // ---- operands for every level, sharing one synchronisation ----
   int pending[kLevels] = {0, 0, 0, 0};
   int lpath[kLevels];
+  Level* prep_lv[kLevels];
+  int prep_stats[kLevels];
+  int n_prep = 0;
   const double* sv = svals;
   for (int l = 0; l < kLevels; ++l) {
     Level& L = c->lv[l];
     lpath[l] = path;
     if (path == FC_PATH_TENSOR && (baseline || L.n < 16)) lpath[l] = FC_PATH_EXACT;
+    int needs = 0;
     if (L.count > 0)
-      FC_TRY(prepare_begin(c, L, l + 1, baseline, sv, s_counts[l], lpath[l], &pending[l]));
+      FC_TRY(prepare_begin(c, L, l + 1, baseline, sv, s_counts[l], lpath[l], &pending[l], &needs));
+    if (needs) {
+      prep_lv[n_prep] = &L;
+      prep_stats[n_prep++] = pending[l];
+    }
     sv += s_counts[l];
   }
+  if (n_prep) FC_TRY(prep_launch(c, prep_lv, prep_stats, n_prep));
 
   // ---- top-level ranges ----
   const int nxt = c->width / kTop, nyt = c->height / kTop;

@@ -91,8 +91,6 @@ struct TcOperands {
   DevBuf odd;            // int32 [2*ncols]: parity flags, then their exclusive prefix
   PinnedBuf upload;      // pinned image of cursors | reach counts | tile info
   int64_t n_even = 0, n_odd = 0;  // columns per parity group
-  DevBuf hist;           // u32 [1024 qmin | 1024 qmax | q2max | pad]
-  PinnedBuf readback;    // pinned copy of hist + last prefix/flag (prepare begin -> finish)
   int64_t low_count[256] = {0};   // #{columns with qmin < -o}      (clamp at 0 possible)
   int64_t high_count[256] = {0};  // #{columns with qmax > 255 - o} (clamp at 255 possible)
 };
@@ -159,6 +157,8 @@ struct Ctx {
   size_t up_off = 0;
   PinnedBuf readback;     // small D2H results (counts, histograms)
   PinnedBuf pool_rb;      // threshold-survivor counts per level
+  DevBuf prep_dev, chunk_odd;  // per-level qmin/qmax histograms + q2max + odd total; chunk counts
+  PinnedBuf prep_rb;           // pinned copy of prep_dev
   PinnedBuf coords_pinned;  // pool origins of all levels, fetched with fc_encode's last sync
   int64_t coords_off[kLevels] = {0, 0, 0, 0};
   bool coords_valid = false;
@@ -220,8 +220,10 @@ int stage_h2d(Ctx* c, void* dst, const void* src, size_t bytes);
 int sync_stream(Ctx* c);
 
 // fc_api.cu: operand preparation around a shared synchronisation
+// host half: validation and level state; *needs_prep = q operands must be
+// (re)built, *pending = 1 when the tensor path waits for prep_launch's readback
 int prepare_begin(Ctx* c, Level& L, int level, int baseline, const double* svals, int s_count,
-                  int path, int* pending);
+                  int path, int* pending, int* needs_prep);
 // launch = false: host half only (fc_encode issues level_prepare_tc_launch itself)
 int prepare_finish(Ctx* c, Level& L, int path, int pending, bool launch = true);
 
@@ -232,7 +234,9 @@ int pool_set_level(Ctx* c, int level, int64_t count, const uint8_t* tiles);
 
 // fc_scan_exact.cu
 int ensure_iso_tables(Ctx* c);
-int level_prepare_exact(Ctx* c, Level& L, int tc_stats);
+// device half of the operand preparation for several levels (one qprep launch,
+// one parity-slot launch, one readback of the tensor-path statistics)
+int prep_launch(Ctx* c, Level* const* levels, const int* stats, int count);
 int gather_ranges(Ctx* c, Level& L, const int32_t* d_origins, int64_t M);
 // gather with the range count read on the device (<= M_bound) and the
 // histogram of range offsets o = rint(rmean) accumulated into d_hist[256]
@@ -256,7 +260,6 @@ int scan_rows_dropin(Ctx* c, const int16_t* ranges, const double* rmeans, int64_
                      int32_t S, int32_t baseline, int64_t* out_err, int64_t* out_idx);
 
 // fc_scan_tc.cu
-int level_prepare_tc_begin(Ctx* c, Level& L);   // device stats + async readback
 int level_prepare_tc_finish(Ctx* c, Level& L);  // after a stream sync: layout + operand build
 int level_prepare_tc_host(Ctx* c, Level& L);    // the host half of it (no launches)
 int level_prepare_tc_launch(Ctx* c, Level& L);  // the stream half (capturable)

@@ -17,6 +17,8 @@
 // reconstruction x = clip(q + o) is formed once as packed bytes (vadd2 /
 // vmaxs2 / vmins2 / byte_perm) and reused by all 8 isometries, each costing
 // one broadcast LDS.128 plus 4 x (vabsdiffu4 + dp4a).
+#include <cub/cub.cuh>
+
 #include <algorithm>
 
 #include "fc_internal.cuh"
@@ -365,24 +367,45 @@ __global__ void range_moments_kernel(const uint8_t* __restrict__ rtiles, int64_t
 // 8/16-byte loads and stores).  With `stats` it also emits the tensor-path
 // column statistics {Q1 = sum q, Q2 = sum q^2, qmin, qmax}, the parity flag
 // and the qmin / qmax histograms (fc_scan_tc.cu).
+struct QLevel {
+  const uint8_t* tiles;
+  const double* mean;
+  const double* svals;
+  int16_t* q;
+  int4* col_stats;
+  int32_t* odd;
+  unsigned* hist;       // qmin | qmax | q2max (block-aggregated), stats levels only
+  int32_t* chunk_odd;   // odd columns per 1024-column chunk, stats levels only
+  int64_t ncols;
+  int S, n, baseline, stats;
+  int block_begin, nblocks;
+};
+struct QParams {
+  QLevel lv[4];
+  int n_levels;
+};
+
+// q base operand: column (e, si) -> rint(s*(d - mean)) or rint(s*d)
+// (matcher.py:143-152), LPC lanes per column with PPL pixels each (coalesced
+// 8/16-byte loads and stores).  Stats levels also emit the tensor-path column
+// statistics {Q1 = sum q, Q2 = sum q^2, qmin, qmax}, the parity flag, the
+// qmin / qmax histograms and the per-chunk parity counts.
 template <int N>
-__global__ void __launch_bounds__(256)
-qprep_kernel(const uint8_t* __restrict__ tiles, const double* __restrict__ mean, int64_t ncols,
-             int S, const double* __restrict__ svals, int baseline, int16_t* __restrict__ q,
-             int stats, int4* __restrict__ col_stats, int32_t* __restrict__ odd,
-             unsigned* __restrict__ hist) {
+__device__ __forceinline__ void qprep_level(const QLevel& L, int block, unsigned* sh) {
   constexpr int LPC = N >= 8 ? N / 8 : 1;
   constexpr int PPL = N / LPC;
-  // block-private histograms (flushed once): qmin | qmax | q2max
-  __shared__ unsigned sh[2048 + 1];
+  const int S = L.S;
+  const int64_t ncols = L.ncols;
+  const int stats = L.stats;
   if (stats) {
     for (int i = threadIdx.x; i < 2049; i += blockDim.x) sh[i] = 0;
     __syncthreads();
   }
   const int64_t total = ncols * LPC;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t stride = (int64_t)L.nblocks * blockDim.x;
+  const int lane = threadIdx.x & 31;
   // every lane of a warp runs the same trip count (shuffles below)
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += stride) {
+  for (int64_t base = (int64_t)block * blockDim.x; base < total; base += stride) {
     const int64_t t = base + threadIdx.x;
     const int64_t col = t / LPC;
     const int part = (int)(t - col * LPC);
@@ -391,9 +414,9 @@ qprep_kernel(const uint8_t* __restrict__ tiles, const double* __restrict__ mean,
     if (valid) {
       const int64_t e = col / S;
       const int si = (int)(col - e * S);
-      const double sv = svals[si];
-      const double dm = mean[e];
-      const uint8_t* src = tiles + e * N + part * PPL;
+      const double sv = L.svals[si];
+      const double dm = L.mean[e];
+      const uint8_t* src = L.tiles + e * N + part * PPL;
       uint8_t px[PPL];
       if constexpr (PPL == 8) {
         *reinterpret_cast<uint2*>(px) = *reinterpret_cast<const uint2*>(src);
@@ -404,7 +427,7 @@ qprep_kernel(const uint8_t* __restrict__ tiles, const double* __restrict__ mean,
 #pragma unroll
       for (int k = 0; k < PPL; ++k) {
         const double d = (double)px[k];
-        const double x = baseline ? d : __dsub_rn(d, dm);
+        const double x = L.baseline ? d : __dsub_rn(d, dm);
         const int v = (int)rint(__dmul_rn(sv, x));
         qv[k] = (int16_t)v;
         s1 += v;
@@ -412,7 +435,7 @@ qprep_kernel(const uint8_t* __restrict__ tiles, const double* __restrict__ mean,
         lo = min(lo, v);
         hi = max(hi, v);
       }
-      int16_t* dst = q + col * N + part * PPL;
+      int16_t* dst = L.q + col * N + part * PPL;
       if constexpr (PPL == 8) {
         *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(qv);
       } else {
@@ -427,19 +450,81 @@ qprep_kernel(const uint8_t* __restrict__ tiles, const double* __restrict__ mean,
       lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
       hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
-    if (valid && part == 0) {
-      col_stats[col] = make_int4(s1, s2, lo, hi);
-      odd[col] = s2 & 1;  // == s1 & 1
+    const bool lead = valid && part == 0;
+    if (lead) {
+      L.col_stats[col] = make_int4(s1, s2, lo, hi);
+      L.odd[col] = s2 & 1;  // == s1 & 1
       atomicAdd(&sh[lo + 512], 1u);
       atomicAdd(&sh[1024 + hi + 512], 1u);
       atomicMax(&sh[2048], (unsigned)s2);
+    }
+    // a warp's columns never straddle a 1024-column chunk (32 / LPC divides 1024)
+    const unsigned oddb = __ballot_sync(0xffffffffu, lead && (s2 & 1));
+    if (lane == 0 && oddb) {
+      const int64_t col0 = (base + (threadIdx.x & ~31)) / LPC;
+      atomicAdd(&L.chunk_odd[col0 >> 10], __popc(oddb));
     }
   }
   if (!stats) return;
   __syncthreads();
   for (int i = threadIdx.x; i < 2048; i += blockDim.x)
-    if (sh[i]) atomicAdd(&hist[i], sh[i]);
-  if (threadIdx.x == 0) atomicMax(&hist[2048], sh[2048]);
+    if (sh[i]) atomicAdd(&L.hist[i], sh[i]);
+  if (threadIdx.x == 0) atomicMax(&L.hist[2048], sh[2048]);
+}
+
+__global__ void __launch_bounds__(256) qprep_multi_kernel(QParams P) {
+  __shared__ unsigned sh[2048 + 1];
+  int l = 0;
+  for (int k = 1; k < P.n_levels; ++k)
+    if ((int)blockIdx.x >= P.lv[k].block_begin) l = k;
+  const QLevel& L = P.lv[l];
+  const int block = blockIdx.x - L.block_begin;
+  switch (L.n) {
+    case 256: qprep_level<256>(L, block, sh); break;
+    case 64: qprep_level<64>(L, block, sh); break;
+    case 16: qprep_level<16>(L, block, sh); break;
+    default: qprep_level<4>(L, block, sh); break;
+  }
+}
+
+// Parity slots: odd_prefix[col] = #odd columns before col (exclusive scan of
+// the parity flags, in column order), one 1024-column chunk per block; the
+// chunk's base sums the per-chunk counts qprep produced.  The last chunk of a
+// level stores the level's odd total next to its histograms.
+struct SlotLevel {
+  const int32_t* odd;
+  int32_t* odd_prefix;
+  const int32_t* chunk_odd;
+  unsigned* n_odd_out;
+  int64_t ncols;
+  int chunk_begin;
+};
+struct SlotParams {
+  SlotLevel lv[4];
+  int n_levels;
+};
+__global__ void __launch_bounds__(1024) parity_slot_kernel(SlotParams P) {
+  using Scan = cub::BlockScan<int, 1024>;
+  using Red = cub::BlockReduce<int, 1024>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ typename Red::TempStorage red_tmp;
+  int l = 0;
+  for (int k = 1; k < P.n_levels; ++k)
+    if ((int)blockIdx.x >= P.lv[k].chunk_begin) l = k;
+  const SlotLevel& L = P.lv[l];
+  const int chunk = blockIdx.x - L.chunk_begin;
+  int part = 0;
+  for (int k = threadIdx.x; k < chunk; k += blockDim.x) part += L.chunk_odd[k];
+  const int base = Red(red_tmp).Sum(part);
+  __shared__ int s_base;
+  if (threadIdx.x == 0) s_base = base;
+  __syncthreads();
+  const int64_t col = (int64_t)chunk * 1024 + threadIdx.x;
+  const int f = col < L.ncols ? L.odd[col] : 0;
+  int excl, agg;
+  Scan(scan_tmp).ExclusiveSum(f, excl, agg);
+  if (col < L.ncols) L.odd_prefix[col] = s_base + excl;
+  if (threadIdx.x == 0 && (int64_t)(chunk + 1) * 1024 >= L.ncols) *L.n_odd_out = s_base + agg;
 }
 
 __global__ void decode_keys_kernel(const unsigned long long* __restrict__ keys, int64_t M,
@@ -491,37 +576,81 @@ int ensure_iso_tables(Ctx* c) {
   return FC_OK;
 }
 
-int level_prepare_exact(Ctx* c, Level& L, int tc_stats) {
-  const int64_t cols = L.count * L.s_count;
-  FC_CUDA(c, L.qbase.reserve(cols * L.n * 2 + 64));
-  FC_CUDA(c, L.svals_d.reserve(kMaxS * 8));
-  FC_TRY(stage_h2d(c, L.svals_d.ptr, L.svals, L.s_count * 8));
-  TcOperands& T = L.tc;
-  if (tc_stats) {
-    FC_CUDA(c, T.col_stats.reserve(cols * 16 + 16));
-    FC_CUDA(c, T.odd.reserve(cols * 8 + 16));
-    FC_CUDA(c, T.hist.reserve(kTcHistWords * 4));
-    FC_CUDA(c, cudaMemsetAsync(T.hist.ptr, 0, kTcHistWords * 4, c->stream));
-  }
-  if (cols > 0) {
-    const int lpc = L.n >= 8 ? L.n / 8 : 1;
-    const int64_t threads = cols * lpc;
-    const unsigned grid = (unsigned)std::min<int64_t>((threads + 255) / 256, c->sm_count * 4);
-#define FC_LAUNCH_QPREP(NN)                                                                   \
-    qprep_kernel<NN><<<grid, 256, 0, c->stream>>>(                                            \
-        L.tiles.as<uint8_t>(), L.mean.as<double>(), cols, L.s_count, L.svals_d.as<double>(),  \
-        L.baseline, L.qbase.as<int16_t>(), tc_stats, T.col_stats.as<int4>(),                  \
-        T.odd.as<int32_t>(), T.hist.as<unsigned>())
-    switch (L.n) {
-      case 256: FC_LAUNCH_QPREP(256); break;
-      case 64: FC_LAUNCH_QPREP(64); break;
-      case 16: FC_LAUNCH_QPREP(16); break;
-      default: FC_LAUNCH_QPREP(4); break;
+// Device half of the operand preparation for several levels at once:
+// s values, q operands (+ tensor-path statistics for `stats` levels), parity
+// slots, and ONE readback of every stats level's histograms and odd total
+// into c->prep_rb (read by level_prepare_tc_host after the next sync).
+int prep_launch(Ctx* c, Level* const* levels, const int* stats, int count) {
+  QParams QP{};
+  SlotParams SP{};
+  int qblocks = 0, chunks = 0, any_stats = 0;
+  int64_t chunk_total = 0;
+  for (int i = 0; i < count; ++i)
+    if (stats[i]) chunk_total += (levels[i]->count * levels[i]->s_count + 1023) / 1024;
+  FC_CUDA(c, c->prep_dev.reserve(kLevels * kTcHistWords * 4));
+  FC_CUDA(c, c->prep_rb.reserve(kLevels * kTcHistWords * 4));
+  FC_CUDA(c, c->chunk_odd.reserve(chunk_total * 4 + 64));
+  for (int i = 0; i < count; ++i) {
+    Level& L = *levels[i];
+    const int li = (int)(&L - c->lv);
+    const int64_t cols = L.count * L.s_count;
+    FC_CUDA(c, L.qbase.reserve(cols * L.n * 2 + 64));
+    FC_CUDA(c, L.svals_d.reserve(kMaxS * 8));
+    FC_TRY(stage_h2d(c, L.svals_d.ptr, L.svals, L.s_count * 8));
+    TcOperands& T = L.tc;
+    if (stats[i]) {
+      FC_CUDA(c, T.col_stats.reserve(cols * 16 + 16));
+      FC_CUDA(c, T.odd.reserve(cols * 8 + 16));
+      T.ncols = cols;
+      any_stats = 1;
     }
-#undef FC_LAUNCH_QPREP
+    if (cols == 0) continue;
+    QLevel& Q = QP.lv[QP.n_levels++];
+    Q.tiles = L.tiles.as<uint8_t>();
+    Q.mean = L.mean.as<double>();
+    Q.svals = L.svals_d.as<double>();
+    Q.q = L.qbase.as<int16_t>();
+    Q.col_stats = T.col_stats.as<int4>();
+    Q.odd = T.odd.as<int32_t>();
+    Q.hist = c->prep_dev.as<unsigned>() + li * kTcHistWords;
+    Q.chunk_odd = c->chunk_odd.as<int32_t>() + chunks * 1;
+    Q.ncols = cols;
+    Q.S = L.s_count;
+    Q.n = L.n;
+    Q.baseline = L.baseline;
+    Q.stats = stats[i];
+    const int lpc = L.n >= 8 ? L.n / 8 : 1;
+    Q.nblocks = (int)std::min<int64_t>((cols * lpc + 255) / 256, c->sm_count * 2);
+    Q.block_begin = qblocks;
+    qblocks += Q.nblocks;
+    if (stats[i]) {
+      SlotLevel& Sl = SP.lv[SP.n_levels++];
+      Sl.odd = T.odd.as<int32_t>();
+      Sl.odd_prefix = T.odd.as<int32_t>() + cols;
+      Sl.chunk_odd = Q.chunk_odd;
+      Sl.n_odd_out = c->prep_dev.as<unsigned>() + li * kTcHistWords + 2049;
+      Sl.ncols = cols;
+      Sl.chunk_begin = chunks;
+      chunks += (int)((cols + 1023) / 1024);
+    }
+  }
+  if (any_stats) {
+    FC_CUDA(c, cudaMemsetAsync(c->prep_dev.ptr, 0, kLevels * kTcHistWords * 4, c->stream));
+    FC_CUDA(c, cudaMemsetAsync(c->chunk_odd.ptr, 0, chunk_total * 4 + 4, c->stream));
+  }
+  if (qblocks > 0) {
+    qprep_multi_kernel<<<qblocks, 256, 0, c->stream>>>(QP);
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 1;
   }
+  if (chunks > 0) {
+    parity_slot_kernel<<<chunks, 1024, 0, c->stream>>>(SP);
+    FC_CUDA(c, cudaGetLastError());
+    c->total_launches += 1;
+  }
+  if (any_stats)
+    FC_CUDA(c, cudaMemcpyAsync(c->prep_rb.ptr, c->prep_dev.ptr, kLevels * kTcHistWords * 4,
+                               cudaMemcpyDeviceToHost, c->stream));
   return FC_OK;
 }
 

@@ -700,42 +700,15 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
 
 }  // namespace
 
-// Phase 1 (device): parity prefix of the column statistics that qprep_kernel
-// produced, then an async readback of the histograms into pinned memory.
-int level_prepare_tc_begin(Ctx* c, Level& L) {
-  TcOperands& T = L.tc;
-  T.ready = false;
-  if (L.baseline || L.n < 16) return set_error(c, FC_ERR_ARG, "tensor path: proposed mode, B >= 4");
-  const int64_t ncols = L.count * L.s_count;
-  if (ncols >= (1ll << 31) - 1024) return set_error(c, FC_ERR_ARG, "too many columns");
-  if (ncols == 0) return set_error(c, FC_ERR_EMPTY_POOL, "no domain entries");
-  T.ncols = ncols;
-  int32_t* odd = T.odd.as<int32_t>();
-  int32_t* odd_prefix = odd + ncols;
-  size_t need = 0;
-  FC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, need, odd, odd_prefix, (int)ncols, c->stream));
-  FC_CUDA(c, c->cub_tmp.reserve(need));
-  FC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.ptr, need, odd, odd_prefix, (int)ncols,
-                                           c->stream));
-  FC_CUDA(c, T.readback.reserve(kTcHistWords * 4 + 16));
-  unsigned* rb = T.readback.as<unsigned>();
-  FC_CUDA(c, cudaMemcpyAsync(rb, T.hist.ptr, kTcHistWords * 4, cudaMemcpyDeviceToHost, c->stream));
-  FC_CUDA(c, cudaMemcpyAsync(rb + kTcHistWords, odd_prefix + ncols - 1, 4, cudaMemcpyDeviceToHost,
-                             c->stream));
-  FC_CUDA(c, cudaMemcpyAsync(rb + kTcHistWords + 1, odd + ncols - 1, 4, cudaMemcpyDeviceToHost,
-                             c->stream));
-  return FC_OK;
-}
-
 // Phase 2a (host, after the stream reached the readback): K layout, tile
 // table and clamp-reach counts, written into the level's pinned upload
 // buffer; every device buffer of the operand set is reserved.  No launches.
 int level_prepare_tc_host(Ctx* c, Level& L) {
   TcOperands& T = L.tc;
   const int64_t ncols = T.ncols;
-  const unsigned* h = T.readback.as<unsigned>();
-  const int32_t last_prefix = (int32_t)h[kTcHistWords];
-  const int32_t last_odd = (int32_t)h[kTcHistWords + 1];
+  if (ncols == 0) return set_error(c, FC_ERR_EMPTY_POOL, "no domain entries");
+  const int li = (int)(&L - c->lv);
+  const unsigned* h = c->prep_rb.as<unsigned>() + li * kTcHistWords;
   const unsigned* hmin = h;
   const unsigned* hmax = h + 1024;
   const unsigned q2max = h[2048];
@@ -753,7 +726,7 @@ int level_prepare_tc_host(Ctx* c, Level& L) {
     fprintf(stderr, "[fc_trace] tc operands B=%d cols=%lld planes=%d m_digits=%d kpad=%d\n", L.side,
             (long long)ncols, T.planes, T.m_digits, T.kpad);
   // two parity groups, each padded to whole tiles
-  const int64_t n_odd = (int64_t)last_prefix + last_odd;
+  const int64_t n_odd = (int64_t)h[2049];
   T.n_even = ncols - n_odd;
   T.n_odd = n_odd;
   const int64_t tiles_even = (T.n_even + kTileN - 1) / kTileN;
