@@ -345,9 +345,9 @@ def main():
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "r01", "tc_scan_c2_traffic.json")
     if args.workload == "c2" and os.path.exists(tpath):
-        launches = json.load(open(tpath))["launches"]
-        if launches:
-            traffic = sum(x["dram_read_bytes"] + x["dram_write_bytes"] for x in launches) / len(launches)
+        prof = json.load(open(tpath))["launches"]
+        if prof:
+            traffic = sum(x["dram_read_bytes"] + x["dram_write_bytes"] for x in prof) / len(prof)
     line = {
         "metric": "range-domain comparisons/sec",
         "value": value,
