@@ -248,3 +248,46 @@ def test_encode_graph_and_eager_identical(graph):
     for _ in range(2):  # the second encode exercises the graph update path
         stream, _ = fc.encode(fc.GrayImage(img), cfg, context=ctx)
         assert fc.serialize(stream) == g["bytes_c2"].tobytes()
+
+
+def test_graph_reuse_across_images_abab():
+    """Alternating images on one context: the cached level-loop graph is only
+    replayed when every launch parameter matches, so results never go stale."""
+    g = load_golden("encode_cases.npz")
+    ctx = _native.Context(0)
+    tags = ["noise", "tiled_proposed", "noise", "c1", "tiled_proposed"]
+    for tag in tags:
+        img = g[f"image_{tag}"]
+        caps = tuple(int(v) for v in g[f"caps_{tag}"])
+        strides = tuple(int(v) for v in g[f"strides_{tag}"])
+        thr = tuple(float(v) for v in g[f"thresholds_{tag}"])
+        params = fc.PoolParams(pool_cap=max(caps), strides=strides, level_caps=caps)
+        cfg = fc.EncoderConfig(pool=params, thresholds=thr)
+        stream, _ = fc.encode(fc.GrayImage(img), cfg, context=ctx)
+        assert fc.serialize(stream) == g[f"bytes_{tag}"].tobytes(), tag
+
+
+def test_encode_rectangular_image_matches_oracle():
+    """A 256x128 image (non-square lattice) against the CPU oracle, stream bytes."""
+    rng = np.random.default_rng(11)
+    y, x = np.mgrid[0:128, 0:256]
+    img = np.clip(0.6 * x + 0.3 * y + rng.normal(0, 12, (128, 256)), 0, 255).astype(np.uint8)
+    caps = (40, 60, 80, 100)
+    enc = O.encode(img, caps, strides=(2, 2, 2, 2), thresholds=(6.0, 6.0, 6.0))
+    params = fc.PoolParams(pool_cap=max(caps), strides=(2, 2, 2, 2), level_caps=caps)
+    cfg = fc.EncoderConfig(pool=params, thresholds=(6.0, 6.0, 6.0))
+    stream, _ = fc.encode(fc.GrayImage(img), cfg)
+    assert fc.serialize(stream) == O.serialize(enc)
+
+
+def test_encode_empty_pool_level_raises():
+    """fc_encode raises EmptyPoolError when ranges reach a level with no pool."""
+    ctx = _native.Context(0)
+    rng = np.random.default_rng(5)
+    img = rng.integers(0, 256, (64, 64)).astype(np.uint8)
+    ctx.set_image(img)
+    ctx.pool_build((1, 1, 1, 1), (8, 8, 8, 8), (0.0,) * 4, (0,) * 4)
+    ctx.pool_set_level(2, np.zeros((0, 8, 8), dtype=np.uint8))
+    s_sets = tuple(fc.SPolicy().s_set(level) for level in (1, 2, 3, 4))
+    with pytest.raises(fc.EmptyPoolError):
+        ctx.encode((0.0, 0.0, 0.0), False, s_sets)  # threshold 0: every range splits
