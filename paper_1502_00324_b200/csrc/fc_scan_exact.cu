@@ -211,23 +211,26 @@ scan_jobs_kernel(const int16_t* __restrict__ qbase, int S, const double* __restr
                  unsigned long long* __restrict__ keys, unsigned long long* __restrict__ t_end) {
   __shared__ __align__(16) ExactSmem<N> s;
   __shared__ int s_job;
+  __shared__ long long s_prefix[513];  // at most 2 jobs per offset bucket, + the total
   const int tid = threadIdx.x;
   const int n_jobs = *d_n_jobs;
   const long long total = *d_total;
+  if ((long long)blockIdx.x >= total) return;
+  for (int j = tid; j <= n_jobs; j += blockDim.x) s_prefix[j] = prefix[j];
   // persistent: the block count is only known on the device
   for (long long b = blockIdx.x; b < total; b += gridDim.x) {
-    __syncthreads();  // the previous block's shared state is consumed
+    __syncthreads();  // the previous block's shared state is consumed (and s_prefix is loaded)
     if (tid == 0) {
       int lo = 0, hi = n_jobs - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (prefix[mid] <= b) lo = mid; else hi = mid - 1;
+        if (s_prefix[mid] <= b) lo = mid; else hi = mid - 1;
       }
       s_job = lo;
     }
     __syncthreads();
     const int4 job = jobs[s_job];  // {list, r_off, r_cnt, col_cnt}
-    const int64_t local = b - prefix[s_job];
+    const int64_t local = b - s_prefix[s_job];
     const int64_t ncc = (job.w + kColsPerBlock - 1) / kColsPerBlock;
     const int64_t rb = local / ncc, cc = local - rb * ncc;
     if (tid < ExactSmem<N>::RB) {
