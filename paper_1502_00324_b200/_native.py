@@ -266,13 +266,13 @@ class Context:
         out = np.empty((capacity, 6), dtype=np.int32)
         n = ctypes.c_int64()
         rc = self.lib.fc_encode(self.handle, _ptr(th), int(bool(baseline)), _ptr(sv), _ptr(counts),
-                                int(path), None, 0, ctypes.byref(n))
-        self.check(rc)
+                                int(path), _ptr(out), capacity, ctypes.byref(n))
         count = int(n.value)
-        if count > capacity:
+        if rc == FC_ERR_ARG and count > capacity:  # undersized buffer: fetch again
             out = np.empty((count, 6), dtype=np.int32)
-        if count:
-            self.check(self.lib.fc_encode_records(self.handle, _ptr(out), out.shape[0]))
+            self.check(self.lib.fc_encode_records(self.handle, _ptr(out), count))
+            return out
+        self.check(rc)
         return out[:count]
 
     def encode_level_stats(self, level: int) -> FcStats:

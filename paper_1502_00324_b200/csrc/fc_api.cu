@@ -217,8 +217,7 @@ void fc_ctx_destroy(fc_ctx* c) {
                     &c->fix_jobs, &c->svals_dev, &c->iso_inv, &c->a_tiles, &c->row_meta,
                     &c->fix_prefix, &c->tc_scratch, &c->enc_orig[0], &c->enc_orig[1],
                     &c->enc_code[0], &c->enc_code[1], &c->enc_flag, &c->enc_pfx,
-                    &c->enc_count, &c->enc_hist, &c->leaf_flag, &c->leaf_pos, &c->leaf_rec,
-                    &c->rec_out, &c->tc_plan, &c->enc_fix, &c->pool_rank};
+                    &c->enc_count, &c->enc_hist, &c->leaf_flag, &c->leaf_pos, &c->leaf_rec, &c->tc_plan, &c->enc_fix, &c->pool_rank};
   for (DevBuf* b : bufs) b->release();
   c->up_arena.release();
   c->readback.release();
@@ -227,6 +226,7 @@ void fc_ctx_destroy(fc_ctx* c) {
   c->chunk_odd.release();
   c->prep_rb.release();
   c->coords_pinned.release();
+  c->rec_pinned.release();
   if (c->enc_ev_ready)
     for (auto& pr : c->enc_ev)
       for (auto& e : pr) cudaEventDestroy(e);
@@ -490,9 +490,8 @@ int fc_encode_records(fc_ctx* c, int32_t* records, int64_t capacity) {
   cudaSetDevice(c->device);
   if (c->enc_records > capacity) return set_error(c, FC_ERR_ARG, "record buffer too small");
   if (c->enc_records == 0) return FC_OK;
-  FC_CUDA(c, cudaMemcpyAsync(records, c->rec_out.ptr, c->enc_records * 24, cudaMemcpyDeviceToHost,
-                             c->stream));
-  return sync_stream(c);
+  memcpy(records, c->rec_pinned.ptr, c->enc_records * 24);
+  return FC_OK;
 }
 
 int fc_encode_level_stats(fc_ctx* c, int level, fc_stats* out) {

@@ -123,6 +123,8 @@ __global__ void classify_kernel(const unsigned long long* __restrict__ keys,
   leaf_flag[code] = 1;
 }
 
+// Records in code (= depth-first) order, written straight into pinned host
+// memory (no device staging buffer, no copy node).
 __global__ void compact_records_kernel(int64_t n_codes, const int32_t* __restrict__ flag,
                                        const int32_t* __restrict__ pos,
                                        const int32_t* __restrict__ rec, int32_t* __restrict__ out,
@@ -255,7 +257,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     FC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, need, c->leaf_flag.as<int32_t>(),
                                              c->leaf_pos.as<int32_t>(), (int)n_codes, c->stream));
     FC_CUDA(c, c->cub_tmp.reserve(need));
-    FC_CUDA(c, c->rec_out.reserve(n_codes * 24 + 64));
+    FC_CUDA(c, c->rec_pinned.reserve(n_codes * 24 + 64));
     int64_t total = 0;
     for (int l = 0; l < kLevels; ++l) {
       c->coords_off[l] = total;
@@ -307,12 +309,13 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
                           &c->row_meta, &c->tc_plan, &c->fix_rows, &c->fix_jobs, &c->fix_cols,
                           &c->enc_orig[0], &c->enc_orig[1], &c->enc_code[0], &c->enc_code[1],
                           &c->enc_count, &c->enc_hist, &c->enc_fix, &c->leaf_flag, &c->leaf_pos,
-                          &c->leaf_rec, &c->rec_out, &c->cub_tmp, &c->iso_inv};
+                          &c->leaf_rec, &c->cub_tmp, &c->iso_inv};
     for (const DevBuf* b : cb) {
       putp(b->ptr);
       put(b->bytes);
     }
     putp(c->coords_pinned.ptr);
+    putp(c->rec_pinned.ptr);
     putp(c->readback.ptr);
     put(c->tc_debug_mode);
     put(c->tc_deferred);
@@ -410,7 +413,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     FC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.ptr, need, flag, pos, (int)n_codes,
                                              c->stream));
     compact_records_kernel<<<blocks_for(n_codes), 256, 0, c->stream>>>(
-        n_codes, flag, pos, c->leaf_rec.as<int32_t>(), c->rec_out.as<int32_t>(), d_count + 8);
+        n_codes, flag, pos, c->leaf_rec.as<int32_t>(), c->rec_pinned.as<int32_t>(), d_count + 8);
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 2;
     FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count, kEncBytes, cudaMemcpyDeviceToHost, c->stream));
@@ -500,11 +503,8 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   trace_dump(c);
   if (!out_records) return FC_OK;
   if (n > capacity) return set_error(c, FC_ERR_ARG, "record buffer too small");
-  if (n > 0) {
-    FC_CUDA(c, cudaMemcpyAsync(out_records, c->rec_out.ptr, n * 24, cudaMemcpyDeviceToHost,
-                               c->stream));
-    FC_TRY(sync_stream(c));
-  }
+  // the compaction kernel wrote the records straight into pinned host memory
+  if (n > 0) memcpy(out_records, c->rec_pinned.ptr, n * 24);
   return FC_OK;
 }
 

@@ -164,7 +164,8 @@ struct Ctx {
   bool coords_valid = false;
   // device-driven encode (fc_encode.cu)
   DevBuf enc_orig[2], enc_code[2], enc_flag, enc_pfx, enc_count, enc_hist, enc_fix;
-  DevBuf leaf_flag, leaf_pos, leaf_rec, rec_out;
+  DevBuf leaf_flag, leaf_pos, leaf_rec;
+  PinnedBuf rec_pinned;   // depth-first records, written by the compaction kernel
   int64_t enc_records = 0;
   fc_stats enc_stats[kLevels]{};
   cudaEvent_t enc_ev[kLevels][3] = {};
