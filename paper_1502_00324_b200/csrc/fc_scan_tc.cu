@@ -158,58 +158,62 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
   const uint32_t kStage = x.kStage, kB = x.kB, bar_base = x.bar_base, tmem_base = x.tmem_base;
   const int STAGES = x.STAGES, RG = x.RG, KPAD = x.KPAD, n_units = x.n_units, n_rg = x.n_rg,
             CT = x.CT, warp = x.warp, lane = x.lane;
-  auto full_bar = [&](int s) { return bar_base + 8u * s; };
-  auto empty_bar = [&](int s) { return bar_base + 8u * (STAGES + s); };
-  auto tfull_bar = [&](int b) { return bar_base + 8u * (2 * STAGES + b); };
-  auto tempty_bar = [&](int b) { return bar_base + 8u * (2 * STAGES + kNumAcc + b); };
-    // ---------------- epilogue: 16 warps drain every accumulator ----------------
-    const int e = warp - 4;
-    const int cq = e >> 2;       // 64-column quarter of the 256-wide accumulator
-    const int sp = warp & 3;     // TMEM sub-partition (lanes 32*sp .. 32*sp+31)
-    const int row = sp * 32 + lane;
-    const int S = p.S;
-    const int iso = lane & 7;
-    const uint32_t tbase = tmem_base + ((uint32_t)(sp * 32) << 16) + cq * 64;
-    // this thread's {best2, loc} per resident row tile, stride = 512 threads
-    int2* bstate = reinterpret_cast<int2*>(smem + best_offset(p)) + (e * 32 + lane);
-    constexpr int kBS = kEpiWarps * 32;
-    // loop-invariant barrier / TMEM addresses; accumulator H & 1, phase (H >> 1) & 1
-    const uint32_t tfull0 = tfull_bar(0), tfull1 = tfull_bar(1);
-    const uint32_t tempty0 = tempty_bar(0), tempty1 = tempty_bar(1);
-    const uint32_t tm0 = tbase, tm1 = tbase + kAccN;
-    const int slot_q = cq * 64;
-    uint32_t H = 0;
-    int stg = 0;
-    uint32_t stg_phase = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      const int g = u % n_rg;
-      const int t0 = (u / n_rg) * CT;
-      const int t1 = min(p.ntiles, t0 + CT);
-      for (int r = 0; r < RG; ++r) bstate[r * kBS] = make_int2(kNone, 0);
-      // tiles in DECREASING order (see improve_limit)
-      for (int t = t1 - 1; t >= t0; --t) {
-        const int2 tinfo = p.tile_info[t];  // {parity, valid slots}
-        ptx::mbar_wait_sleep(full_bar(stg), stg_phase);
+  // Two groups of 8 warps alternate over the accumulators (group gq drains the
+  // (tile, row tile) pairs with H & 1 == gq, i.e. accumulator gq): one group
+  // computes while the other loads, and every barrier wait / release covers
+  // 128 columns per thread (two 64-column waves).
+  const int e = warp - 4;
+  const int gq = e >> 3;          // accumulator / group
+  const int hq = (e >> 2) & 1;    // 128-column half of the 256-column tile
+  const int sp = warp & 3;        // TMEM sub-partition (lanes 32*sp .. 32*sp+31)
+  const int row = sp * 32 + lane;
+  const int S = p.S;
+  const int iso = lane & 7;
+  const uint32_t tm = tmem_base + ((uint32_t)(sp * 32) << 16) + gq * kAccN + hq * 128;
+  const int slot_h = hq * 128;
+  // this thread's {best2, loc} per resident row tile, stride = 512 threads
+  int2* bstate = reinterpret_cast<int2*>(smem + best_offset(p)) + (e * 32 + lane);
+  constexpr int kBS = kEpiWarps * 32;
+  const uint32_t tfull = bar_base + 8u * (2 * STAGES + gq);
+  const uint32_t tempty = bar_base + 8u * (2 * STAGES + kNumAcc + gq);
+  uint32_t H = 0;
+  int stg = 0;
+  uint32_t stg_phase = 0;
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const int g = u % n_rg;
+    const int t0 = (u / n_rg) * CT;
+    const int t1 = min(p.ntiles, t0 + CT);
+    for (int r = 0; r < RG; ++r) bstate[r * kBS] = make_int2(kNone, 0);
+    // tiles in DECREASING order (see improve_limit)
+    for (int t = t1 - 1; t >= t0; --t) {
+      const int2 tinfo = p.tile_info[t];  // {parity, valid slots}
+      if constexpr (!DEFERRED) ptx::mbar_wait_sleep(bar_base + 8u * stg, stg_phase);
+      const int32_t* colmap_s = reinterpret_cast<const int32_t*>(sStage + stg * kStage + kB);
 #pragma unroll 1
-        for (int r = 0; r < RG; ++r, ++H) {
-          const int2 bs = bstate[r * kBS];  // issued before the waits: latency hidden
-          const bool a1 = H & 1;
-          ptx::mbar_wait_sleep(a1 ? tfull1 : tfull0, (H >> 1) & 1);
-          ptx::tc_fence_after();
-          int va[32], vb[32];
-          const uint32_t tm = a1 ? tm1 : tm0;
-          ptx::tmem_ld32(tm, va);
-          ptx::tmem_ld32(tm + 32, vb);
+      for (int r = 0; r < RG; ++r, ++H) {
+        if ((int)(H & 1) != gq) continue;
+        const int2 bs = bstate[r * kBS];  // issued before the wait: latency hidden
+        ptx::mbar_wait_sleep(tfull, (H >> 1) & 1);
+        ptx::tc_fence_after();
+        int va[32], vb[32];
+        int m_best = kNone, gi_best = 0;
+#pragma unroll
+        for (int wv = 0; wv < 2; ++wv) {
+          ptx::tmem_ld32(tm + wv * 64, va);
+          ptx::tmem_ld32(tm + wv * 64 + 32, vb);
           ptx::tmem_wait_ld();
-          // all of this warp's values are in registers: release the accumulator
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(a1 ? tempty1 : tempty0);
+          if (wv == 1) {
+            // every value of this half is in registers: release the accumulator
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty);
+          }
+          const int sq = slot_h + wv * 64;
           if (tinfo.y < kTileN) {  // mask padding slots (last tile of a group)
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              if (slot_q + j >= tinfo.y) va[j] = kNone;
-              if (slot_q + 32 + j >= tinfo.y) vb[j] = kNone;
+              if (sq + j >= tinfo.y) va[j] = kNone;
+              if (sq + 32 + j >= tinfo.y) vb[j] = kNone;
             }
           }
           int gm[8];
@@ -223,83 +227,99 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
           gm[7] = min8<24>(vb);
           const int m = min(__vimin3_s32(gm[0], gm[1], gm[2]),
                             __vimin3_s32(__vimin3_s32(gm[3], gm[4], gm[5]), gm[6], gm[7]));
-          const int lim = improve_limit(bs.x, tinfo.x);
           if constexpr (DEFERRED) {
-            // branch-free: record the 8-column group, resolve at the unit end
+            // first group of this wave holding m; waves are visited in column order
             int gi = 7;
 #pragma unroll
             for (int k = 6; k >= 0; --k) gi = (gm[k] == m) ? k : gi;
-            if (m < lim) bstate[r * kBS] = make_int2(2 * m + tinfo.x, t * 8 + gi);
-          } else if (m < lim) {
-            // long K: the per-unit recompute would cost more than resolving now
-            const bool in_a = min(min(gm[0], gm[1]), min(gm[2], gm[3])) == m;
-            const int j = in_a ? first_eq(va, m) : 32 + first_eq(vb, m);
-            const int32_t* colmap_s = reinterpret_cast<const int32_t*>(sStage + stg * kStage + kB);
-            bstate[r * kBS] = make_int2(2 * m + tinfo.x, colmap_s[slot_q + j]);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(empty_bar(stg));
-        if (++stg == STAGES) {
-          stg = 0;
-          stg_phase ^= 1;
-        }
-      }
-      // resolve each row's winning 8-column group: recompute its dot products
-      // from the global copies of A and B (the shared A slot is already being
-      // refilled for the next unit) and take the first column whose value
-      // equals the recorded minimum
-      const int chunks = KPAD / 16;
-#pragma unroll 1
-      for (int r = 0; r < RG; ++r) {
-        unsigned long long key = ~0ull;
-        const int2 bs = bstate[r * kBS];
-        const int4 rm = p.row_meta[(size_t)(g * RG + r) * kTileM + row];  // {o, R, m, -}
-        if (!DEFERRED && bs.x != kNone && rm.z >= 0) {
-          const long long err = (long long)bs.x + rm.y;
-          const int col = bs.y;
-          const int e_idx = col / S, si = col - e_idx * S;
-          key = ((unsigned long long)err << 32) | (unsigned long long)((e_idx * 8 + iso) * S + si);
-        } else if (DEFERRED && bs.x != kNone && rm.z >= 0) {
-          const int t = bs.y >> 3, gi = bs.y & 7;
-          const int par = p.tile_info[t].x;
-          const int m = (int)(((long long)bs.x - par) >> 1);
-          const int slot0 = cq * 64 + gi * 8;
-          const uint8_t* arow = p.a_tiles + (size_t)(g * RG + r) * (kTileM * KPAD) +
-                                (row >> 3) * 128 + (row & 7) * 16;
-          const int8_t* bgrp = p.b_tiles + (size_t)t * kB + (slot0 >> 3) * 128;
-          int kh[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 1
-          for (int kc = 0; kc < chunks; ++kc) {
-            const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(arow + kc * (kTileM * 16)));
-            const int8_t* bk = bgrp + kc * (kTileN * 16);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const uint4 b4 = __ldg(reinterpret_cast<const uint4*>(bk + j * 16));
-              kh[j] = dp4a_us(a4.x, b4.x, kh[j]);
-              kh[j] = dp4a_us(a4.y, b4.y, kh[j]);
-              kh[j] = dp4a_us(a4.z, b4.z, kh[j]);
-              kh[j] = dp4a_us(a4.w, b4.w, kh[j]);
+            if (m < m_best) {
+              m_best = m;
+              gi_best = wv * 8 + gi;
+            }
+          } else {
+            // vs earlier tiles: improve_limit (ties go to the later-visited,
+            // smaller columns); vs the first wave of this tile: strictly smaller
+            if (m < improve_limit(bs.x, tinfo.x) && m < m_best) {
+              // the rare improving lanes resolve the column at once
+              const bool in_a = min(min(gm[0], gm[1]), min(gm[2], gm[3])) == m;
+              const int j = in_a ? first_eq(va, m) : 32 + first_eq(vb, m);
+              m_best = m;
+              gi_best = colmap_s[sq + j];
             }
           }
-          int jj = 7;
-#pragma unroll
-          for (int j = 6; j >= 0; --j) jj = (kh[j] == m) ? j : jj;
-          const int col = p.colmap[(size_t)t * kTileN + slot0 + jj];
-          const long long err = (long long)bs.x + rm.y;
-          const int e_idx = col / S, si = col - e_idx * S;
-          key = ((unsigned long long)err << 32) | (unsigned long long)((e_idx * 8 + iso) * S + si);
         }
-        unsigned long long w = __shfl_xor_sync(0xffffffffu, key, 1);
-        key = w < key ? w : key;
-        w = __shfl_xor_sync(0xffffffffu, key, 2);
-        key = w < key ? w : key;
-        w = __shfl_xor_sync(0xffffffffu, key, 4);
-        key = w < key ? w : key;
-        if ((lane & 7) == 0 && key != ~0ull) atomicMin(&p.keys[rm.z], key);
+        if constexpr (DEFERRED) {
+          // branch-free: record the 8-column group, resolve at the unit end
+          if (m_best < improve_limit(bs.x, tinfo.x))
+            bstate[r * kBS] = make_int2(2 * m_best + tinfo.x, t * 16 + gi_best);
+        } else {
+          if (m_best != kNone) bstate[r * kBS] = make_int2(2 * m_best + tinfo.x, gi_best);
+        }
+      }
+      if constexpr (!DEFERRED) {
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(bar_base + 8u * (STAGES + stg));
+      }
+      if (++stg == STAGES) {
+        stg = 0;
+        stg_phase ^= 1;
       }
     }
+    // resolve each row's winning 8-column group: recompute its dot products
+    // from the global copies of A and B (the shared A slot is already being
+    // refilled for the next unit) and take the first column whose value
+    // equals the recorded minimum
+    const int chunks = KPAD / 16;
+#pragma unroll 1
+    for (int r = 0; r < RG; ++r) {
+      unsigned long long key = ~0ull;
+      const int2 bs = bstate[r * kBS];
+      const int4 rm = p.row_meta[(size_t)(g * RG + r) * kTileM + row];  // {o, R, m, -}
+      if (!DEFERRED && bs.x != kNone && rm.z >= 0) {
+        const long long err = (long long)bs.x + rm.y;
+        const int col = bs.y;
+        const int e_idx = col / S, si = col - e_idx * S;
+        key = ((unsigned long long)err << 32) | (unsigned long long)((e_idx * 8 + iso) * S + si);
+      } else if (DEFERRED && bs.x != kNone && rm.z >= 0) {
+        const int t = bs.y >> 4, gi = bs.y & 15;
+        const int par = p.tile_info[t].x;
+        const int m = (int)(((long long)bs.x - par) >> 1);
+        const int slot0 = slot_h + gi * 8;
+        const uint8_t* arow = p.a_tiles + (size_t)(g * RG + r) * (kTileM * KPAD) +
+                              (row >> 3) * 128 + (row & 7) * 16;
+        const int8_t* bgrp = p.b_tiles + (size_t)t * kB + (slot0 >> 3) * 128;
+        int kh[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 1
+        for (int kc = 0; kc < chunks; ++kc) {
+          const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(arow + kc * (kTileM * 16)));
+          const int8_t* bk = bgrp + kc * (kTileN * 16);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint4 b4 = __ldg(reinterpret_cast<const uint4*>(bk + j * 16));
+            kh[j] = dp4a_us(a4.x, b4.x, kh[j]);
+            kh[j] = dp4a_us(a4.y, b4.y, kh[j]);
+            kh[j] = dp4a_us(a4.z, b4.z, kh[j]);
+            kh[j] = dp4a_us(a4.w, b4.w, kh[j]);
+          }
+        }
+        int jj = 7;
+#pragma unroll
+        for (int j = 6; j >= 0; --j) jj = (kh[j] == m) ? j : jj;
+        const int col = p.colmap[(size_t)t * kTileN + slot0 + jj];
+        const long long err = (long long)bs.x + rm.y;
+        const int e_idx = col / S, si = col - e_idx * S;
+        key = ((unsigned long long)err << 32) | (unsigned long long)((e_idx * 8 + iso) * S + si);
+      }
+      unsigned long long w = __shfl_xor_sync(0xffffffffu, key, 1);
+      key = w < key ? w : key;
+      w = __shfl_xor_sync(0xffffffffu, key, 2);
+      key = w < key ? w : key;
+      w = __shfl_xor_sync(0xffffffffu, key, 4);
+      key = w < key ? w : key;
+      if ((lane & 7) == 0 && key != ~0ull) atomicMin(&p.keys[rm.z], key);
+    }
   }
+}
 
 // Work order (all roles derive it identically): unit u -> row group
 // g = u % n_rgroups, column-tile span u / n_rgroups; inside a unit: tiles t,
@@ -328,11 +348,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(full_bar(s), 1);
-      ptx::mbar_init(empty_bar(s), 1 + kEpiWarps);
+      // the MMA commit; plus every epilogue warp when it reads the stage's column map
+      ptx::mbar_init(empty_bar(s), 1 + (p.deferred ? 0 : kEpiWarps));
     }
     for (int b = 0; b < kNumAcc; ++b) {
       ptx::mbar_init(tfull_bar(b), 1);
-      ptx::mbar_init(tempty_bar(b), kEpiWarps);
+      ptx::mbar_init(tempty_bar(b), kEpiWarps / 2);  // one group of 8 warps per accumulator
     }
     ptx::mbar_init(afull_bar, 1);
     ptx::mbar_init(aempty_bar, 1);
@@ -915,7 +936,7 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   prm.plan = d_plan;
   prm.tspan = d_time;
   // measured: the per-unit recompute wins only for short K
-  prm.deferred = c->tc_deferred >= 0 ? c->tc_deferred : (T.kpad <= 64 ? 1 : 0);
+  prm.deferred = c->tc_deferred >= 0 ? c->tc_deferred : (T.kpad <= 128 ? 1 : 0);
   const uint32_t smem = smem_bytes(prm);
   if (!c->tc_attr_set) {
     FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
