@@ -42,19 +42,6 @@ __global__ void top_origins_kernel(int nxt, int32_t n_top, int32_t* __restrict__
   codes[i] = i * 64;
 }
 
-// Level start: candidate keys to "none" and the level's span slots reset
-// (start = max, ends = 0) -- one node instead of a memset.
-__global__ void level_begin_kernel(unsigned long long* __restrict__ keys, int64_t bound,
-                                   unsigned long long* __restrict__ tspan) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < bound) keys[i] = ~0ull;
-  if (i == 0) {
-    tspan[0] = ~0ull;
-    tspan[1] = 0;
-    tspan[2] = 0;
-  }
-}
-
 __device__ __forceinline__ int baseline_offset(double rmean, double s, double dmean) {
   // codec.py:214-218 (== _scan.py:39-43): clip(rint(rmean - s*dmean), 0, 255)
   const int o = (int)rint(__dsub_rn(rmean, __dmul_rn(s, dmean)));
@@ -198,17 +185,16 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     FC_CUDA(c, c->enc_code[b].reserve(max_ranges * 4 + 64));
   }
   FC_CUDA(c, c->enc_count.reserve(kEncBytes + 64));
-  FC_CUDA(c, c->enc_hist.reserve(256 * 4 * kLevels));
   FC_CUDA(c, c->leaf_flag.reserve(n_codes * 4 + 64));
   FC_CUDA(c, c->leaf_pos.reserve(n_codes * 4 + 64));
   FC_CUDA(c, c->leaf_rec.reserve(n_codes * 24 + 64));
   FC_CUDA(c, c->readback.reserve(kEncBytes + 64));
   FC_CUDA(c, c->keys.reserve(max_ranges * 8 + 64));
   int32_t* d_count = c->enc_count.as<int32_t>();
-  int32_t* d_hist = c->enc_hist.as<int32_t>();
+  int32_t* d_hist = reinterpret_cast<int32_t*>(c->enc_count.as<uint8_t>() + kEncHistOff);
   int32_t* h_rb = c->readback.as<int32_t>();
   FC_CUDA(c, cudaMemsetAsync(c->leaf_flag.ptr, 0, n_codes * 4, c->stream));
-  FC_CUDA(c, cudaMemsetAsync(d_count, 0, kEncBytes, c->stream));  // counters, pairs, spans
+  FC_CUDA(c, cudaMemsetAsync(d_count, 0, kEncBytes, c->stream));  // counters, pairs, spans, hists
   top_origins_kernel<<<blocks_for(n_top), 256, 0, c->stream>>>(
       nxt, (int32_t)n_top, c->enc_orig[0].as<int32_t>(), c->enc_code[0].as<int32_t>(), d_count);
   FC_CUDA(c, cudaGetLastError());
@@ -216,16 +202,14 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
 
   int64_t* d_fix = reinterpret_cast<int64_t*>(c->enc_count.as<uint8_t>() + kEncFixOff);
   auto* d_time = reinterpret_cast<unsigned long long*>(c->enc_count.as<uint8_t>() + kEncTimeOff);
-  auto gather = [&](int l, int cur, int64_t bound) -> int {
-    FC_CUDA(c, cudaMemsetAsync(d_hist + 256 * l, 0, 256 * 4, c->stream));
-    return gather_ranges_dev(c, c->lv[l], c->enc_orig[cur].as<int32_t>(), d_count + l, bound,
-                             d_hist + 256 * l);
-  };
-  // every range buffer is sized for the level-4 bound BEFORE the first gather:
-  // a later reserve must never reallocate (and so drop) gathered ranges
+  // every range buffer is sized for the level-4 bound up front: a later
+  // reserve must never reallocate (and so drop) gathered ranges
   FC_TRY(reserve_ranges(c, c->lv[kLevels - 1], max_ranges));
   FC_TRY(reserve_ranges(c, c->lv[0], n_top));
-  FC_TRY(gather(0, 0, n_top));
+  auto gather = [&](int l, int cur, int64_t bound) -> int {
+    return gather_build(c, c->lv[l], c->enc_orig[cur].as<int32_t>(), d_count + l, bound,
+                        d_hist + 256 * l, c->keys.as<uint64_t>(), d_time + 4 * l);
+  };
   trace_mark(c, "prep_launched");
   FC_TRY(sync_stream(c));
   trace_mark(c, "prep_sync");
@@ -308,7 +292,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     const DevBuf* cb[] = {&c->keys, &c->rtiles, &c->rmean, &c->roff, &c->rsq, &c->a_tiles,
                           &c->row_meta, &c->tc_plan, &c->fix_rows, &c->fix_jobs, &c->fix_cols,
                           &c->enc_orig[0], &c->enc_orig[1], &c->enc_code[0], &c->enc_code[1],
-                          &c->enc_count, &c->enc_hist, &c->enc_fix, &c->leaf_flag, &c->leaf_pos,
+                          &c->enc_count, &c->leaf_flag, &c->leaf_pos,
                           &c->leaf_rec, &c->cub_tmp, &c->iso_inv};
     for (const DevBuf* b : cb) {
       putp(b->ptr);
@@ -341,6 +325,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   const int body_rc = reuse ? FC_OK : [&]() -> int {
   for (int l = 0; l < kLevels; ++l)
     if (tc_launch[l]) FC_TRY(level_prepare_tc_launch(c, c->lv[l]));
+  if (c->lv[0].count > 0) FC_TRY(gather(0, 0, n_top));
 
   // ---- level loop: no host synchronisation ----
   int cur = 0;
@@ -363,11 +348,9 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     const int64_t launches_before = c->total_launches + c->stats.kernel_launches;
     uint64_t* keys = c->keys.as<uint64_t>();
     unsigned long long* tspan = d_time + 4 * l;
-    level_begin_kernel<<<blocks_for(bound), 256, 0, c->stream>>>(
-        reinterpret_cast<unsigned long long*>(keys), bound, tspan);
-    c->total_launches += 1;
     if (L.path == FC_PATH_TENSOR) {
-      FC_TRY(scan_tc_launch(c, L, bound, d_M, d_hist + 256 * l, keys, nullptr, d_fix + l, tspan));
+      FC_TRY(scan_tc_launch(c, L, bound, d_M, d_hist + 256 * l, keys, nullptr, d_fix + l, tspan,
+                            /*a_built=*/true));
     } else {
       FC_TRY(scan_exact(c, L, bound, nullptr, 0, nullptr, 0, keys, d_M, tspan));
     }
@@ -416,7 +399,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
         n_codes, flag, pos, c->leaf_rec.as<int32_t>(), c->rec_pinned.as<int32_t>(), d_count + 8);
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 2;
-    FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count, kEncBytes, cudaMemcpyDeviceToHost, c->stream));
+    FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count, kEncReadBytes, cudaMemcpyDeviceToHost, c->stream));
     // the stream header needs every pool's origins: fetch them with this sync
     {
       for (int l = 0; l < kLevels; ++l)

@@ -199,9 +199,12 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 #endif
 // enc_count buffer layout: int32 counters [16] | int64 clamp pairs [4] | u64 spans [4][4]
+// | int32 range-offset histograms [4][256]; the first kEncReadBytes are read back
 constexpr int kEncFixOff = 64;
 constexpr int kEncTimeOff = 96;
-constexpr int kEncBytes = 96 + 4 * 4 * 8;
+constexpr int kEncReadBytes = 96 + 4 * 4 * 8;
+constexpr int kEncHistOff = kEncReadBytes;
+constexpr int kEncBytes = kEncHistOff + 4 * 256 * 4;
 
 // Timing event on the context stream.  Inside a stream capture a plain
 // cudaEventRecord only marks a dependency; the External flag turns it into a
@@ -270,7 +273,12 @@ int level_prepare_tc_launch(Ctx* c, Level& L);  // the stream half (capturable)
 // d_time (optional): u64 [3] span slots {contraction start, contraction end, fix end}
 int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const int32_t* d_hist,
                    uint64_t* d_keys, cudaEvent_t ev_main_end, int64_t* d_fix_pairs,
-                   unsigned long long* d_time = nullptr);
+                   unsigned long long* d_time = nullptr, bool a_built = false);
+// fc_encode's fused level start: gather the level's ranges (tiles, moments,
+// offset histogram), reset their candidate keys and the level's span slots,
+// and for tensor levels write the A operand tiles + row meta (build_a_kernel)
+int gather_build(Ctx* c, Level& L, const int32_t* d_origins, const int32_t* d_M, int64_t bound,
+                 int32_t* d_hist, uint64_t* d_keys, unsigned long long* d_time);
 int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys);
 // reserve every buffer the level's scan may touch for `bound` ranges (graph capture)
 int reserve_level_scan(Ctx* c, Level& L, int64_t bound);

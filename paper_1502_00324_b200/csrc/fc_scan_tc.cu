@@ -744,7 +744,157 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
   for (int i = tid; i < M; i += kPlanThreads) order[atomicAdd(&cursor[roff[i]], 1)] = i;
 }
 
+// fc_encode's fused level start (one warp per range slot):
+//  * range m < M: gather its B x B tile from the image, exact moments, offset
+//    histogram, candidate key reset (gather_kernel + level reset);
+//  * tensor levels, m < rows_pad / 8: its 8 A rows (one per isometry, inverse
+//    permutation of the staged tile, K extra block) and row meta; padding
+//    rows are zero with m = -1 (build_a_kernel).
+struct GatherBuild {
+  const uint8_t* img;
+  int width, B, n;
+  const int32_t* origins;
+  const int32_t* d_M;
+  int64_t slots;          // warps launched (>= bound and >= the padded row groups)
+  uint8_t* rtiles;
+  double* rmean;
+  int32_t* roff;
+  int32_t* rsq;
+  int32_t* hist;
+  unsigned long long* keys;
+  unsigned long long* tspan;
+  // tensor operand (kpad == 0: exact level)
+  int kpad, planes, m_digits, RG;
+  const uint16_t* inv;
+  uint8_t* a_tiles;
+  int4* row_meta;
+};
+
+__global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
+  __shared__ uint8_t tile_s[8][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    P.tspan[0] = ~0ull;
+    P.tspan[1] = 0;
+    P.tspan[2] = 0;
+  }
+  if (m >= P.slots) return;
+  const int64_t M = *P.d_M;
+  const int n = P.n, B = P.B;
+  uint8_t* ts = tile_s[warp];
+  int o = 0, s1 = 0, s2 = 0;
+  if (m < M) {
+    const int x = P.origins[2 * m], y = P.origins[2 * m + 1];
+    for (int p = lane; p < n; p += 32) {
+      const int r = p / B, col = p - r * B;
+      const int v = P.img[(int64_t)(y + r) * P.width + x + col];
+      P.rtiles[m * n + p] = (uint8_t)v;
+      ts[p] = (uint8_t)v;
+      s1 += v;
+      s2 += v * v;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+    }
+    const double mean = __ddiv_rn((double)s1, (double)n);
+    o = (int)rint(mean);
+    if (lane == 0) {
+      P.rmean[m] = mean;
+      P.roff[m] = o;
+      P.rsq[m] = s2;
+      P.keys[m] = ~0ull;
+      atomicAdd(&P.hist[o], 1);
+    }
+  }
+  if (P.kpad == 0) return;
+  const int n_rtiles = (int)((M * 8 + kTileM - 1) / kTileM);
+  const int64_t mpad = (int64_t)((n_rtiles + P.RG - 1) / P.RG) * P.RG * kTileM / 8;
+  if (m >= mpad) return;
+  __syncwarp();
+  const int chunks = P.kpad / 16;
+  const int kbase = P.planes * n;
+  const bool real = m < M;
+  for (int it = lane; it < 8 * chunks; it += 32) {
+    const int iso = it / chunks, kc = it - iso * chunks;
+    const int64_t row = m * 8 + iso;
+    const int64_t tile = row / kTileM;
+    const int rrow = (int)(row - tile * kTileM);
+    uint32_t w[4] = {0, 0, 0, 0};
+    if (real) {
+#pragma unroll
+      for (int b4 = 0; b4 < 4; ++b4) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          const int k = kc * 16 + b4 * 4 + bb;
+          uint32_t v = 0;
+          if (k < kbase) {
+            const int kk = k < n ? k : k - n;
+            v = ts[P.inv[iso * n + kk]];
+          } else {
+            const int sl = k - kbase;
+            if (sl < P.m_digits) v = 255;
+            else if (sl < P.m_digits + 2) v = 1;
+            else if (sl < P.m_digits + 4) v = (uint32_t)o;
+          }
+          word |= v << (8 * bb);
+        }
+        w[b4] = word;
+      }
+    }
+    uint8_t* dst = P.a_tiles + tile * ((int64_t)kTileM * P.kpad) + (int64_t)kc * (kTileM * 16) +
+                   (rrow >> 3) * 128 + (rrow & 7) * 16;
+    *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  if (lane < 8) {
+    const int R = s2 - 2 * o * s1 + n * o * o;
+    P.row_meta[m * 8 + lane] = real ? make_int4(o, R, (int)m, 0) : make_int4(0, 0, -1, 0);
+  }
+}
+
 }  // namespace
+
+static int tc_config(Ctx* c, int kpad, TcParams* prm);
+
+int gather_build(Ctx* c, Level& L, const int32_t* d_origins, const int32_t* d_M, int64_t bound,
+                 int32_t* d_hist, uint64_t* d_keys, unsigned long long* d_time) {
+  GatherBuild P{};
+  P.img = c->img_ptr;
+  P.width = c->width;
+  P.B = L.side;
+  P.n = L.n;
+  P.origins = d_origins;
+  P.d_M = d_M;
+  P.rtiles = c->rtiles.as<uint8_t>();
+  P.rmean = c->rmean.as<double>();
+  P.roff = c->roff.as<int32_t>();
+  P.rsq = c->rsq.as<int32_t>();
+  P.hist = d_hist;
+  P.keys = reinterpret_cast<unsigned long long*>(d_keys);
+  P.tspan = d_time;
+  int64_t slots = bound;
+  if (L.path == FC_PATH_TENSOR) {
+    TcParams prm{};
+    FC_TRY(tc_config(c, L.tc.kpad, &prm));
+    P.kpad = L.tc.kpad;
+    P.planes = L.tc.planes;
+    P.m_digits = L.tc.m_digits;
+    P.RG = prm.rg;
+    P.inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
+    P.a_tiles = c->a_tiles.as<uint8_t>();
+    P.row_meta = c->row_meta.as<int4>();
+    const int64_t rtiles_max = (bound * 8 + kTileM - 1) / kTileM;
+    slots = std::max<int64_t>(slots, ((rtiles_max + prm.rg - 1) / prm.rg) * prm.rg * kTileM / 8);
+  }
+  P.slots = slots;
+  gather_build_kernel<<<(unsigned)((slots * 32 + 255) / 256), 256, 0, c->stream>>>(P);
+  FC_CUDA(c, cudaGetLastError());
+  c->total_launches += 1;
+  return FC_OK;
+}
 
 // Phase 2a (host, after the stream reached the readback): K layout, tile
 // table and clamp-reach counts, written into the level's pinned upload
@@ -892,7 +1042,7 @@ int reserve_level_scan(Ctx* c, Level& L, int64_t bound) {
 // histogram d_hist live on the device; nothing here waits for the GPU.
 int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const int32_t* d_hist,
                    uint64_t* d_keys, cudaEvent_t ev_main_end, int64_t* d_fix_pairs,
-                   unsigned long long* d_time) {
+                   unsigned long long* d_time, bool a_built) {
   TcOperands& T = L.tc;
   if (!T.ready) return set_error(c, FC_ERR_STATE, "tensor operands not prepared");
   if (M_bound == 0) return FC_OK;
@@ -916,13 +1066,16 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
       ranges_per_block(L.n), c->roff.as<int32_t>(), d_plan, c->fix_jobs.as<int4>(),
       c->fix_cols.as<long long>(), d_fplan, c->fix_rows.as<int32_t>(),
       reinterpret_cast<long long*>(d_fix_pairs));
-  const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
-  const int64_t work = rows_max * (T.kpad / 16);
-  build_a_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
-      c->rtiles.as<uint8_t>(), c->rmean.as<double>(), c->rsq.as<int32_t>(), d_plan, L.n, T.kpad,
-      T.planes, T.m_digits, inv, c->a_tiles.as<uint8_t>(), c->row_meta.as<int4>());
-  FC_CUDA(c, cudaGetLastError());
-  c->stats.kernel_launches += 2;
+  c->stats.kernel_launches += 1;
+  if (!a_built) {
+    const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
+    const int64_t work = rows_max * (T.kpad / 16);
+    build_a_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
+        c->rtiles.as<uint8_t>(), c->rmean.as<double>(), c->rsq.as<int32_t>(), d_plan, L.n, T.kpad,
+        T.planes, T.m_digits, inv, c->a_tiles.as<uint8_t>(), c->row_meta.as<int4>());
+    FC_CUDA(c, cudaGetLastError());
+    c->stats.kernel_launches += 1;
+  }
 
   prm.a_tiles = c->a_tiles.as<uint8_t>();
   prm.row_meta = c->row_meta.as<int4>();
