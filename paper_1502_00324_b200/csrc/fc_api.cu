@@ -337,7 +337,8 @@ int fc_pool_coords(fc_ctx* c, int level, uint16_t* xy) {
   Level& L = c->lv[level - 1];
   if (L.count == 0) return FC_OK;
   // xy words are x | y << 16: in little-endian memory exactly the (x, y) u16 pair
-  if (c->coords_valid) {  // prefetched by fc_encode
+  if (c->coords_valid) {  // written to pinned memory by the pool build's survivors kernel
+    FC_TRY(sync_stream(c));
     memcpy(xy, c->coords_pinned.as<uint32_t>() + c->coords_off[level - 1], L.count * 4);
     return FC_OK;
   }

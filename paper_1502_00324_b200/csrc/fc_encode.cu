@@ -242,12 +242,6 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
                                              c->leaf_pos.as<int32_t>(), (int)n_codes, c->stream));
     FC_CUDA(c, c->cub_tmp.reserve(need));
     FC_CUDA(c, c->rec_pinned.reserve(n_codes * 24 + 64));
-    int64_t total = 0;
-    for (int l = 0; l < kLevels; ++l) {
-      c->coords_off[l] = total;
-      total += c->lv[l].count;
-    }
-    FC_CUDA(c, c->coords_pinned.reserve(total * 4 + 16));
   }
   trace_mark(c, "reserved");
   // A graph whose every launch parameter (sizes, scalars, buffer addresses)
@@ -315,7 +309,6 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
       c->enc_stats[l].path = c->lv[l].path;
       if (tc_launch[l]) c->lv[l].tc.ready = true;
     }
-    c->coords_valid = true;
     FC_CUDA(c, cudaGraphLaunch(c->enc_exec, c->stream));
   }
   if (!reuse && use_graph) {
@@ -400,15 +393,6 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 2;
     FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count, kEncReadBytes, cudaMemcpyDeviceToHost, c->stream));
-    // the stream header needs every pool's origins: fetch them with this sync
-    {
-      for (int l = 0; l < kLevels; ++l)
-        if (c->lv[l].count)
-          FC_CUDA(c, cudaMemcpyAsync(c->coords_pinned.as<uint32_t>() + c->coords_off[l],
-                                     c->lv[l].xy.ptr, c->lv[l].count * 4, cudaMemcpyDeviceToHost,
-                                     c->stream));
-      c->coords_valid = true;
-    }
   }
   return FC_OK;
   }();

@@ -744,6 +744,17 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
   }
   SurvParams SV{};
   int64_t swarps = 0;
+  // pool origins go straight to pinned host memory (the stream header needs
+  // them on the host; no copy nodes later)
+  {
+    int64_t total = 0;
+    for (int li = 0; li < kLevels; ++li) {
+      c->coords_off[li] = total;
+      total += c->lv[li].count;
+    }
+    FC_CUDA(c, c->coords_pinned.reserve(total * 4 + 16));
+    c->coords_valid = true;  // valid once the stream has passed the survivors kernel
+  }
   for (int li = 0; li < kLevels; ++li) {
     Level& L = c->lv[li];
     const int64_t E = L.count;
@@ -756,7 +767,7 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     V.nx = nx_l[li];
     V.stride = L.stride;
     V.warp_begin = swarps;
-    V.xy = L.xy.as<uint32_t>();
+    V.xy = c->coords_pinned.as<uint32_t>() + c->coords_off[li];
     V.ent = L.ent.as<double>();
     V.tiles = L.tiles.as<uint8_t>();
     V.sum = L.sum.as<int32_t>();
