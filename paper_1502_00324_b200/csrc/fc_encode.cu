@@ -111,19 +111,30 @@ __global__ void classify_kernel(const unsigned long long* __restrict__ keys,
 }
 
 // Records in code (= depth-first) order, written straight into pinned host
-// memory (no device staging buffer, no copy node).
-__global__ void compact_records_kernel(int64_t n_codes, const int32_t* __restrict__ flag,
-                                       const int32_t* __restrict__ pos,
-                                       const int32_t* __restrict__ rec, int32_t* __restrict__ out,
-                                       int32_t* __restrict__ d_count) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_codes) return;
+// memory: a block's records are contiguous in the output, so they are staged
+// in shared memory and written as one coalesced run (no copy node).
+__global__ void __launch_bounds__(256) compact_records_kernel(int64_t n_codes,
+                                                              const int32_t* __restrict__ flag,
+                                                              const int32_t* __restrict__ pos,
+                                                              const int32_t* __restrict__ rec,
+                                                              int32_t* __restrict__ out,
+                                                              int32_t* __restrict__ d_count) {
+  __shared__ int32_t rs[256 * 6];
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x;
+  const int64_t i = i0 + threadIdx.x;
+  const int64_t last = min(i0 + (int64_t)blockDim.x, n_codes) - 1;
+  const int32_t base = pos[i0];
+  const int32_t cnt = pos[last] + flag[last] - base;
   if (i == n_codes - 1) *d_count = pos[i] + flag[i];
-  if (!flag[i]) return;
-  const int32_t* src = rec + i * 6;
-  int32_t* dst = out + (int64_t)pos[i] * 6;
+  if (i < n_codes && flag[i]) {
+    const int32_t* src = rec + i * 6;
+    int32_t* dst = rs + (pos[i] - base) * 6;
 #pragma unroll
-  for (int k = 0; k < 6; ++k) dst[k] = src[k];
+    for (int k = 0; k < 6; ++k) dst[k] = src[k];
+  }
+  __syncthreads();
+  int32_t* o = out + (int64_t)base * 6;
+  for (int w = threadIdx.x; w < cnt * 6; w += blockDim.x) o[w] = rs[w];
 }
 
 inline unsigned blocks_for(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }

@@ -362,7 +362,7 @@ __device__ __forceinline__ uint32_t load_word_guarded(const uint8_t* img, int64_
 template <int D>
 __device__ __forceinline__ void survivor_rows(const SurvLevel& L, const uint8_t* __restrict__ img,
                                               int width, int64_t img_bytes, int64_t warp_in_level,
-                                              int lane) {
+                                              int lane, uint32_t* __restrict__ xy_s) {
   constexpr int B = D / 2, n = B * B, PER = 32 / D, NW = D / 4;
   const int grp = lane / D, row = lane % D;
   const int64_t sv = warp_in_level * PER + grp;
@@ -421,7 +421,8 @@ __device__ __forceinline__ void survivor_rows(const SurvLevel& L, const uint8_t*
   }
   if (valid && row == 0) {
     const int wy = w / L.nx, wx = w - wy * L.nx;
-    L.xy[sv] = (uint32_t)(wx * L.stride) | ((uint32_t)(wy * L.stride) << 16);
+    // staged: the block writes its survivors' origins as one coalesced run
+    xy_s[(threadIdx.x >> 5) * PER + grp] = (uint32_t)(wx * L.stride) | ((uint32_t)(wy * L.stride) << 16);
     L.ent[sv] = L.ent_all[w];
     L.sum[sv] = s1;
     L.sumsq[sv] = s2;
@@ -434,21 +435,30 @@ __device__ __forceinline__ void survivor_rows(const SurvLevel& L, const uint8_t*
 __global__ void __launch_bounds__(256) survivors_all_kernel(const uint8_t* __restrict__ img,
                                                             int width, int64_t img_bytes,
                                                             SurvParams P) {
+  __shared__ uint32_t xy_s[8 * 8];  // 8 warps x up to 8 survivors per warp
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (gw >= P.total_warps) return;
+  // levels start on block boundaries (warp_begin is a multiple of 8)
   int l = 0;
 #pragma unroll
   for (int k = 1; k < 4; ++k)
-    if (gw >= P.lv[k].warp_begin) l = k;
+    if ((int64_t)blockIdx.x * 8 >= P.lv[k].warp_begin) l = k;
   const SurvLevel& L = P.lv[l];
   const int64_t wl = gw - L.warp_begin;
-  switch (L.B) {
-    case 16: survivor_rows<32>(L, img, width, img_bytes, wl, lane); break;
-    case 8: survivor_rows<16>(L, img, width, img_bytes, wl, lane); break;
-    case 4: survivor_rows<8>(L, img, width, img_bytes, wl, lane); break;
-    default: survivor_rows<4>(L, img, width, img_bytes, wl, lane); break;
+  const int per = 32 / (2 * L.B);
+  const int64_t level_warps = (L.count + per - 1) / per;
+  if (wl < level_warps) {
+    switch (L.B) {
+      case 16: survivor_rows<32>(L, img, width, img_bytes, wl, lane, xy_s); break;
+      case 8: survivor_rows<16>(L, img, width, img_bytes, wl, lane, xy_s); break;
+      case 4: survivor_rows<8>(L, img, width, img_bytes, wl, lane, xy_s); break;
+      default: survivor_rows<4>(L, img, width, img_bytes, wl, lane, xy_s); break;
+    }
   }
+  __syncthreads();
+  const int64_t sv0 = ((int64_t)blockIdx.x * 8 - L.warp_begin) * per;
+  const int64_t nblk = min((int64_t)8 * per, L.count - sv0);
+  if ((int64_t)threadIdx.x < nblk) L.xy[sv0 + threadIdx.x] = xy_s[threadIdx.x];
 }
 
 // Moments of explicitly supplied decimated tiles (fc_pool_set_level).
@@ -775,7 +785,7 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     V.mean = L.mean.as<double>();
     V.cnorm = L.cnorm.as<double>();
     const int per = 32 / (2 * L.side);  // survivors per warp
-    swarps += (E + per - 1) / per;
+    swarps += ((E + per - 1) / per + 7) / 8 * 8;  // levels start on block boundaries
     out_sizes[li] = E;
   }
   SV.total_warps = swarps;
