@@ -173,6 +173,7 @@ struct Ctx {
   bool use_graph = true;               // FC_GRAPH=0 launches the level loop eagerly
   bool capturing = false;              // the stream is being captured into a graph
   int tc_debug_mode = 0;               // FC_TC_DEBUG_MODE (pipeline probes)
+  int pool_chunk = 0;                  // FC_POOL_CHUNK=512: smaller rank-sort chunks
   int tc_deferred = -1;                // FC_TC_DEFERRED: -1 = by K, 0/1 forced
   cudaGraphExec_t enc_exec = nullptr;  // instantiated level-loop graph, updated per encode
   std::vector<uint64_t> enc_sig;       // launch signature of enc_exec (reuse when equal)

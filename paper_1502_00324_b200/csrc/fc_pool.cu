@@ -209,6 +209,8 @@ entropy_all_kernel(const uint8_t* __restrict__ img, int width, EntParams P) {
 constexpr int kEntSmem = kLutWords * 8 + kEntWarps * 128 * 32 * 4;
 
 // ---- rank sort of the threshold survivors: (key asc, window asc) ----
+// chunk size: 2048 elements (1024 threads); 512 with FC_POOL_CHUNK=512
+constexpr int kChunkSmall = 512;
 constexpr int kChunk = 2048;
 constexpr int kMaxChunks = 64;
 
@@ -236,39 +238,41 @@ __device__ __forceinline__ int sort_level_of(const SortParams& P, int chunk) {
   return l;
 }
 
-// Bitonic sort of one chunk in shared memory.
-__global__ void __launch_bounds__(1024) chunk_sort_kernel(SortParams P) {
-  __shared__ uint64_t sk[kChunk];
-  __shared__ uint32_t si[kChunk];
+// One chunk sorted by (key, window) with CUB's block merge sort (CHUNK / 2
+// threads, 2 items each).
+struct KeyIdx {
+  uint64_t k;
+  uint32_t v;
+};
+struct KeyIdxLess {
+  __device__ __forceinline__ bool operator()(const KeyIdx& a, const KeyIdx& b) const {
+    return a.k < b.k || (a.k == b.k && a.v < b.v);
+  }
+};
+
+template <int kChunk>
+__global__ void __launch_bounds__(kChunk / 2) chunk_sort_kernel(SortParams P) {
+  using Sorter = cub::BlockMergeSort<KeyIdx, kChunk / 2, 2>;
+  __shared__ typename Sorter::TempStorage tmp;
   const int l = sort_level_of(P, blockIdx.x);
   const SortLevel& L = P.lv[l];
   const int c = blockIdx.x - L.chunk_begin;
   const int base = c * kChunk;
   const int n = min(kChunk, L.count - base);
-  for (int i = threadIdx.x; i < kChunk; i += blockDim.x) {
-    sk[i] = i < n ? L.key[base + i] : ~0ull;
-    si[i] = i < n ? L.val[base + i] : 0xffffffffu;
+  KeyIdx items[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = threadIdx.x * 2 + k;  // blocked arrangement
+    items[k] = i < n ? KeyIdx{L.key[base + i], L.val[base + i]} : KeyIdx{~0ull, 0xffffffffu};
   }
-  __syncthreads();
-  for (int size = 2; size <= kChunk; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < kChunk / 2; t += blockDim.x) {
-        const int i = 2 * t - (t & (stride - 1));
-        const int j = i + stride;
-        const bool up = (i & size) == 0;
-        const uint64_t ka = sk[i], kb = sk[j];
-        const uint32_t ia = si[i], ib = si[j];
-        if (lex_less(kb, ib, ka, ia) == up) {
-          sk[i] = kb; sk[j] = ka;
-          si[i] = ib; si[j] = ia;
-        }
-      }
-      __syncthreads();
+  Sorter(tmp).Sort(items, KeyIdxLess());
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = threadIdx.x * 2 + k;
+    if (i < n) {
+      L.key[base + i] = items[k].k;
+      L.val[base + i] = items[k].v;
     }
-  }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    L.key[base + i] = sk[i];
-    L.val[base + i] = si[i];
   }
 }
 
@@ -279,7 +283,8 @@ struct RankLevel {
   int nch;          // chunks of this level
   int pair_begin;   // first (a, b) pair block of this level
 };
-__global__ void __launch_bounds__(1024) chunk_pair_rank_kernel(SortParams P, RankLevel R0,
+template <int kChunk>
+__global__ void __launch_bounds__(kChunk / 2) chunk_pair_rank_kernel(SortParams P, RankLevel R0,
                                                                RankLevel R1, RankLevel R2,
                                                                RankLevel R3,
                                                                int32_t* __restrict__ rank_all) {
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(1024) chunk_pair_rank_kernel(SortParams P, Ran
   }
 }
 
+template <int kChunk>
 __global__ void rank_scatter_kernel(SortParams P, const int32_t* __restrict__ rank_all) {
   const int l = sort_level_of(P, blockIdx.x / (kChunk / 256));
   const SortLevel& L = P.lv[l];
@@ -684,6 +690,13 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
   {
     SortParams SP{};
     int chunks = 0;
+    int max_sel = 0;
+    for (int li = 0; li < kLevels; ++li)
+      if (use_tau[li]) max_sel = std::max(max_sel, h_nsel[li]);
+    // 512-element chunks measured no faster on c2 (more pair blocks offset the
+    // shorter sorts); kept selectable for pools of very different sizes
+    const int chunk = c->pool_chunk == kChunkSmall ? kChunkSmall : kChunk;
+    (void)max_sel;
     for (int li = 0; li < kLevels; ++li) {
       if (!use_tau[li]) continue;
       Level& L = c->lv[li];
@@ -701,7 +714,7 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
         continue;
       }
       L.count = nsel;
-      const int nch = (nsel + kChunk - 1) / kChunk;
+      const int nch = (nsel + chunk - 1) / chunk;
       if (nch <= kMaxChunks) {
         SortLevel& S = SP.lv[SP.n_levels++];
         S.key = L.win_key.as<uint64_t>();
@@ -736,18 +749,26 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
       RankLevel RL[4] = {};
       int pairs = 0;
       for (int k = 0; k < SP.n_levels; ++k) {
-        RL[k].nch = (SP.lv[k].count + kChunk - 1) / kChunk;
+        RL[k].nch = (SP.lv[k].count + chunk - 1) / chunk;
         RL[k].pair_begin = pairs;
         pairs += RL[k].nch * RL[k].nch;
       }
       for (int k = SP.n_levels; k < 4; ++k) RL[k].pair_begin = 1 << 30;
-      FC_CUDA(c, c->pool_rank.reserve((size_t)chunks * kChunk * 4));
-      FC_CUDA(c, cudaMemsetAsync(c->pool_rank.ptr, 0, (size_t)chunks * kChunk * 4, c->stream));
-      chunk_sort_kernel<<<chunks, 1024, 0, c->stream>>>(SP);
-      chunk_pair_rank_kernel<<<pairs, 1024, 0, c->stream>>>(SP, RL[0], RL[1], RL[2], RL[3],
-                                                            c->pool_rank.as<int32_t>());
-      rank_scatter_kernel<<<chunks * (kChunk / 256), 256, 0, c->stream>>>(SP,
-                                                                        c->pool_rank.as<int32_t>());
+      FC_CUDA(c, c->pool_rank.reserve((size_t)chunks * chunk * 4));
+      FC_CUDA(c, cudaMemsetAsync(c->pool_rank.ptr, 0, (size_t)chunks * chunk * 4, c->stream));
+      int32_t* rank = c->pool_rank.as<int32_t>();
+      if (chunk == kChunkSmall) {
+        chunk_sort_kernel<kChunkSmall><<<chunks, kChunkSmall / 2, 0, c->stream>>>(SP);
+        chunk_pair_rank_kernel<kChunkSmall><<<pairs, kChunkSmall / 2, 0, c->stream>>>(
+            SP, RL[0], RL[1], RL[2], RL[3], rank);
+        rank_scatter_kernel<kChunkSmall>
+            <<<chunks * (kChunkSmall / 256), 256, 0, c->stream>>>(SP, rank);
+      } else {
+        chunk_sort_kernel<kChunk><<<chunks, kChunk / 2, 0, c->stream>>>(SP);
+        chunk_pair_rank_kernel<kChunk><<<pairs, kChunk / 2, 0, c->stream>>>(SP, RL[0], RL[1], RL[2],
+                                                                           RL[3], rank);
+        rank_scatter_kernel<kChunk><<<chunks * (kChunk / 256), 256, 0, c->stream>>>(SP, rank);
+      }
       FC_CUDA(c, cudaGetLastError());
       c->total_launches += 3;
     }
