@@ -189,11 +189,17 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
       const int2 tinfo = p.tile_info[t];  // {parity, valid slots}
       if constexpr (!DEFERRED) ptx::mbar_wait_sleep(bar_base + 8u * stg, stg_phase);
       const int32_t* colmap_s = reinterpret_cast<const int32_t*>(sStage + stg * kStage + kB);
+      // this group's (tile, row tile) pairs: H & 1 == gq.  H advances by RG per
+      // tile, so for even RG the row-tile parity is fixed; for odd RG (= 1)
+      // the tiles alternate between the groups.
+      const uint32_t Ht = H;
+      H += RG;
+      const int r_first = (int)((gq - (int)(Ht & 1)) & 1);
 #pragma unroll 1
-      for (int r = 0; r < RG; ++r, ++H) {
-        if ((int)(H & 1) != gq) continue;
+      for (int r = r_first; r < RG; r += 2) {
+        const uint32_t Hr = Ht + r;
         const int2 bs = bstate[r * kBS];  // issued before the wait: latency hidden
-        ptx::mbar_wait_sleep(tfull, (H >> 1) & 1);
+        ptx::mbar_wait_sleep(tfull, (Hr >> 1) & 1);
         ptx::tc_fence_after();
         int va[32], vb[32];
         int m_best = kNone, gi_best = 0;
