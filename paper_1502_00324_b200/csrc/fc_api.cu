@@ -192,6 +192,7 @@ int fc_ctx_create(int device, fc_ctx** out) {
   if (const char* g = getenv("FC_GRAPH")) c->use_graph = atoi(g) != 0;
   if (const char* d = getenv("FC_TC_DEBUG_MODE")) c->tc_debug_mode = atoi(d);
   if (const char* d = getenv("FC_TC_DEFERRED")) c->tc_deferred = atoi(d);
+  if (const char* o = getenv("FC_OVERLAP")) c->overlap = atoi(o) != 0;
   if (const char* d = getenv("FC_POOL_CHUNK")) c->pool_chunk = atoi(d);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
@@ -245,6 +246,16 @@ void fc_ctx_destroy(fc_ctx* c) {
   cudaEventDestroy(c->ev2);
   for (auto& e : c->tc_ev) cudaEventDestroy(e);
   for (auto& e : c->trace_ev) cudaEventDestroy(e);
+  if (c->aux) {
+    cudaStreamSynchronize(c->aux);
+    cudaStreamDestroy(c->aux);
+    cudaEventDestroy(c->ev_fork);
+    for (int l = 0; l < kLevels; ++l) {
+      cudaEventDestroy(c->ev_prep[l]);
+      cudaEventDestroy(c->ev_plan[l]);
+      cudaEventDestroy(c->ev_jobs[l]);
+    }
+  }
   if (c->enc_exec) cudaGraphExecDestroy(c->enc_exec);
   cudaStreamDestroy(c->stream);
   delete c;
@@ -267,6 +278,10 @@ int fc_set_option(fc_ctx* c, const char* name, int64_t value) {
   if (!name) return set_error(c, FC_ERR_ARG, "null option name");
   if (strcmp(name, "graph") == 0) {
     c->use_graph = value != 0;
+    return FC_OK;
+  }
+  if (strcmp(name, "overlap") == 0) {
+    c->overlap = value != 0;
     return FC_OK;
   }
   return set_error(c, FC_ERR_ARG, std::string("unknown option ") + name);

@@ -156,6 +156,13 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   if (!c->enc_ev_ready) {
     for (auto& pr : c->enc_ev)
       for (auto& e : pr) FC_CUDA(c, cudaEventCreate(&e));
+    FC_CUDA(c, cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    FC_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    for (int l = 0; l < kLevels; ++l) {
+      FC_CUDA(c, cudaEventCreateWithFlags(&c->ev_prep[l], cudaEventDisableTiming));
+      FC_CUDA(c, cudaEventCreateWithFlags(&c->ev_plan[l], cudaEventDisableTiming));
+      FC_CUDA(c, cudaEventCreateWithFlags(&c->ev_jobs[l], cudaEventDisableTiming));
+    }
     c->enc_ev_ready = true;
   }
   for (auto& st : c->enc_stats) st = fc_stats{};
@@ -272,6 +279,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     put(baseline);
     put(path);
     put(c->sm_count);
+    put(c->overlap);
     for (int l = 0; l < 3; ++l) putd(thresholds[l]);
     for (int l = 0; l < kLevels; ++l) {
       const Level& L = c->lv[l];
@@ -327,8 +335,26 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     c->capturing = true;
   }
   const int body_rc = reuse ? FC_OK : [&]() -> int {
-  for (int l = 0; l < kLevels; ++l)
-    if (tc_launch[l]) FC_TRY(level_prepare_tc_launch(c, c->lv[l]));
+  // fork the second stream: later levels' operand builds run there while the
+  // first level is gathered and contracted
+  const bool overlap = c->overlap;
+  if (overlap) {
+    FC_CUDA(c, cudaEventRecord(c->ev_fork, c->stream));
+    FC_CUDA(c, cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+  }
+  for (int l = 0; l < kLevels; ++l) {
+    if (!tc_launch[l]) continue;
+    if (overlap && l > 0) {
+      cudaStream_t main = c->stream;
+      c->stream = c->aux;
+      const int r = level_prepare_tc_launch(c, c->lv[l]);
+      c->stream = main;
+      FC_TRY(r);
+      FC_CUDA(c, cudaEventRecord(c->ev_prep[l], c->aux));
+    } else {
+      FC_TRY(level_prepare_tc_launch(c, c->lv[l]));
+    }
+  }
   if (c->lv[0].count > 0) FC_TRY(gather(0, 0, n_top));
 
   // ---- level loop: no host synchronisation ----
@@ -353,8 +379,11 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     uint64_t* keys = c->keys.as<uint64_t>();
     unsigned long long* tspan = d_time + 4 * l;
     if (L.path == FC_PATH_TENSOR) {
+      if (overlap && l > 0 && tc_launch[l]) FC_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_prep[l], 0));
       FC_TRY(scan_tc_launch(c, L, bound, d_M, d_hist + 256 * l, keys, nullptr, d_fix + l, tspan,
-                            /*a_built=*/true));
+                            /*a_built=*/true, overlap ? c->aux : nullptr, c->ev_plan[l],
+                            c->ev_jobs[l]));
+      if (overlap) FC_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_jobs[l], 0));
     } else {
       FC_TRY(scan_exact(c, L, bound, nullptr, 0, nullptr, 0, keys, d_M, tspan));
     }

@@ -172,6 +172,12 @@ struct Ctx {
   bool enc_ev_ready = false;
   bool use_graph = true;               // FC_GRAPH=0 launches the level loop eagerly
   bool capturing = false;              // the stream is being captured into a graph
+  // second stream for work that overlaps the contraction inside fc_encode
+  // (operand builds of later levels, clamp corrections); joined per level
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_prep[kLevels] = {}, ev_plan[kLevels] = {},
+              ev_jobs[kLevels] = {};
+  bool overlap = true;                 // FC_OVERLAP=0 / option "overlap": single stream
   int tc_debug_mode = 0;               // FC_TC_DEBUG_MODE (pipeline probes)
   int pool_chunk = 0;                  // FC_POOL_CHUNK=512: smaller rank-sort chunks
   int tc_deferred = -1;                // FC_TC_DEFERRED: -1 = by K, 0/1 forced
@@ -272,9 +278,13 @@ int level_prepare_tc_launch(Ctx* c, Level& L);  // the stream half (capturable)
 // gathered ranges; d_hist[o] = #ranges with offset o.  No synchronisation:
 // the unit decomposition and the correction jobs are planned on the device.
 // d_time (optional): u64 [3] span slots {contraction start, contraction end, fix end}
+// jobs_stream (optional): the clamp corrections run there, after ev_plan, and
+// signal ev_jobs (they only atomicMin into the same keys as the contraction)
 int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const int32_t* d_hist,
                    uint64_t* d_keys, cudaEvent_t ev_main_end, int64_t* d_fix_pairs,
-                   unsigned long long* d_time = nullptr, bool a_built = false);
+                   unsigned long long* d_time = nullptr, bool a_built = false,
+                   cudaStream_t jobs_stream = nullptr, cudaEvent_t ev_plan = nullptr,
+                   cudaEvent_t ev_jobs = nullptr);
 // fc_encode's fused level start: gather the level's ranges (tiles, moments,
 // offset histogram), reset their candidate keys and the level's span slots,
 // and for tensor levels write the A operand tiles + row meta (build_a_kernel)

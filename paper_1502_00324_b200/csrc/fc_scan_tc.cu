@@ -1048,7 +1048,8 @@ int reserve_level_scan(Ctx* c, Level& L, int64_t bound) {
 // histogram d_hist live on the device; nothing here waits for the GPU.
 int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const int32_t* d_hist,
                    uint64_t* d_keys, cudaEvent_t ev_main_end, int64_t* d_fix_pairs,
-                   unsigned long long* d_time, bool a_built) {
+                   unsigned long long* d_time, bool a_built, cudaStream_t jobs_stream,
+                   cudaEvent_t ev_plan, cudaEvent_t ev_jobs) {
   TcOperands& T = L.tc;
   if (!T.ready) return set_error(c, FC_ERR_STATE, "tensor operands not prepared");
   if (M_bound == 0) return FC_OK;
@@ -1108,10 +1109,21 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   c->stats.kernel_launches += 1;
 
   // ---- clamp corrections (exact kernel on clamp-active pairs), planned above ----
-  FC_TRY(scan_exact_jobs(c, L, c->fix_jobs.as<int4>(), c->fix_cols.as<int64_t>(),
-                         &d_fplan->n_jobs, &d_fplan->total_blocks, c->fix_rows.as<int32_t>(),
-                         T.reach_low.as<int32_t>(), T.reach_high.as<int32_t>(), d_keys,
-                         d_time ? d_time + 2 : nullptr));
+  // With a jobs stream they run concurrently with the contraction (both only
+  // atomicMin into the same keys) on the SMs the contraction leaves idle.
+  cudaStream_t main = c->stream;
+  if (jobs_stream) {
+    FC_CUDA(c, cudaEventRecord(ev_plan, main));
+    FC_CUDA(c, cudaStreamWaitEvent(jobs_stream, ev_plan, 0));
+    c->stream = jobs_stream;
+  }
+  const int rc = scan_exact_jobs(c, L, c->fix_jobs.as<int4>(), c->fix_cols.as<int64_t>(),
+                                 &d_fplan->n_jobs, &d_fplan->total_blocks,
+                                 c->fix_rows.as<int32_t>(), T.reach_low.as<int32_t>(),
+                                 T.reach_high.as<int32_t>(), d_keys, d_time ? d_time + 2 : nullptr);
+  c->stream = main;
+  FC_TRY(rc);
+  if (jobs_stream) FC_CUDA(c, cudaEventRecord(ev_jobs, jobs_stream));
   return FC_OK;
 }
 
