@@ -46,6 +46,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -66,14 +67,35 @@ constexpr int kNone = 0x7fffffff;
 
 // Unit decomposition of one launch, computed on the device from the range
 // count (level_plan_kernel) so the host never waits for it.
+// The work is the (row group, column tile) pairs in the linear order
+// p = g * ntiles + j, j-th tile of group g counted from the LAST tile; CTA b
+// takes the contiguous share [P*b/grid, P*(b+1)/grid), i.e. at most a few
+// segments (one per row group it touches), so every CTA gets the same number
+// of tile MMAs to within one pair.
 struct TcPlan {
   int M;           // ranges
   int n_rgroups;   // groups of RG row tiles
-  int tiles_per_unit;
-  int n_units;
+  int n_pairs;     // n_rgroups * ntiles
   int rows_pad;    // n_rgroups * RG * 128
-  int pad[3];
+  int pad[4];
 };
+
+__device__ __forceinline__ void cta_share(int P, int& p0, int& p1) {
+  p0 = (int)((long long)P * blockIdx.x / gridDim.x);
+  p1 = (int)((long long)P * (blockIdx.x + 1) / gridDim.x);
+}
+
+// Next segment of the share: row group g, tiles t1-1 down to t0.
+__device__ __forceinline__ bool next_seg(int& p, int p1, int ntiles, int& g, int& t0, int& t1) {
+  if (p >= p1) return false;
+  g = p / ntiles;
+  const int gb = g * ntiles;
+  const int pe = min(p1, gb + ntiles);
+  t1 = ntiles - (p - gb);
+  t0 = ntiles - (pe - gb);
+  p = pe;
+  return true;
+}
 
 struct TcParams {
   const uint8_t* a_tiles;    // [rt_pad][128 * kpad]
@@ -148,7 +170,7 @@ struct EpiCtx {
   uint8_t* smem;
   uint8_t* sStage;
   uint32_t kStage, kB, bar_base, tmem_base;
-  int STAGES, RG, KPAD, n_units, n_rg, CT, warp, lane;
+  int STAGES, RG, KPAD, n_pairs, warp, lane;
 };
 
 template <bool DEFERRED>
@@ -156,8 +178,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
   uint8_t* smem = x.smem;
   uint8_t* sStage = x.sStage;
   const uint32_t kStage = x.kStage, kB = x.kB, bar_base = x.bar_base, tmem_base = x.tmem_base;
-  const int STAGES = x.STAGES, RG = x.RG, KPAD = x.KPAD, n_units = x.n_units, n_rg = x.n_rg,
-            CT = x.CT, warp = x.warp, lane = x.lane;
+  const int STAGES = x.STAGES, RG = x.RG, KPAD = x.KPAD, warp = x.warp, lane = x.lane;
   // Two groups of 8 warps alternate over the accumulators (group gq drains the
   // (tile, row tile) pairs with H & 1 == gq, i.e. accumulator gq): one group
   // computes while the other loads, and every barrier wait / release covers
@@ -179,14 +200,15 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
   uint32_t H = 0;
   int stg = 0;
   uint32_t stg_phase = 0;
-  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-    const int g = u % n_rg;
-    const int t0 = (u / n_rg) * CT;
-    const int t1 = min(p.ntiles, t0 + CT);
+  int p0, p1, g, t0, t1;
+  cta_share(x.n_pairs, p0, p1);
+  for (int pp = p0; next_seg(pp, p1, p.ntiles, g, t0, t1);) {
     for (int r = 0; r < RG; ++r) bstate[r * kBS] = make_int2(kNone, 0);
-    // tiles in DECREASING order (see improve_limit)
+    // tiles in DECREASING order (see improve_limit); tile_info one tile ahead
+    int2 tinfo_next = p.tile_info[t1 - 1];
     for (int t = t1 - 1; t >= t0; --t) {
-      const int2 tinfo = p.tile_info[t];  // {parity, valid slots}
+      const int2 tinfo = tinfo_next;  // {parity, valid slots}
+      if (t > t0) tinfo_next = p.tile_info[t - 1];
       if constexpr (!DEFERRED) ptx::mbar_wait_sleep(bar_base + 8u * stg, stg_phase);
       const int32_t* colmap_s = reinterpret_cast<const int32_t*>(sStage + stg * kStage + kB);
       // this group's (tile, row tile) pairs: H & 1 == gq.  H advances by RG per
@@ -273,48 +295,68 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
     }
     // resolve each row's winning 8-column group: recompute its dot products
     // from the global copies of A and B (the shared A slot is already being
-    // refilled for the next unit) and take the first column whose value
-    // equals the recorded minimum
+    // refilled for the next segment) and take the first column whose value
+    // equals the recorded minimum.  Only the candidates at the minimal error
+    // of their range (the 8 isometry rows = lanes 8k..8k+7) can win, so just
+    // those are resolved, the range's 8 lanes computing the candidate group's
+    // 8 dot products together (one L2 round trip per candidate, not 8 x K/16).
     const int chunks = KPAD / 16;
 #pragma unroll 1
     for (int r = 0; r < RG; ++r) {
       unsigned long long key = ~0ull;
       const int2 bs = bstate[r * kBS];
       const int4 rm = p.row_meta[(size_t)(g * RG + r) * kTileM + row];  // {o, R, m, -}
-      if (!DEFERRED && bs.x != kNone && rm.z >= 0) {
-        const long long err = (long long)bs.x + rm.y;
-        const int col = bs.y;
-        const int e_idx = col / S, si = col - e_idx * S;
-        key = ((unsigned long long)err << 32) | (unsigned long long)((e_idx * 8 + iso) * S + si);
-      } else if (DEFERRED && bs.x != kNone && rm.z >= 0) {
-        const int t = bs.y >> 4, gi = bs.y & 15;
-        const int par = p.tile_info[t].x;
-        const int m = (int)(((long long)bs.x - par) >> 1);
-        const int slot0 = slot_h + gi * 8;
-        const uint8_t* arow = p.a_tiles + (size_t)(g * RG + r) * (kTileM * KPAD) +
-                              (row >> 3) * 128 + (row & 7) * 16;
-        const int8_t* bgrp = p.b_tiles + (size_t)t * kB + (slot0 >> 3) * 128;
-        int kh[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 1
-        for (int kc = 0; kc < chunks; ++kc) {
-          const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(arow + kc * (kTileM * 16)));
-          const int8_t* bk = bgrp + kc * (kTileN * 16);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint4 b4 = __ldg(reinterpret_cast<const uint4*>(bk + j * 16));
-            kh[j] = dp4a_us(a4.x, b4.x, kh[j]);
-            kh[j] = dp4a_us(a4.y, b4.y, kh[j]);
-            kh[j] = dp4a_us(a4.z, b4.z, kh[j]);
-            kh[j] = dp4a_us(a4.w, b4.w, kh[j]);
+      const bool valid = bs.x != kNone && rm.z >= 0;
+      if constexpr (!DEFERRED) {
+        if (valid) {
+          const long long err = (long long)bs.x + rm.y;
+          const int col = bs.y;
+          const int e_idx = col / S, si = col - e_idx * S;
+          key = ((unsigned long long)err << 32) | (unsigned long long)((e_idx * 8 + iso) * S + si);
+        }
+      } else {
+        long long gmin = valid ? (long long)bs.x + rm.y : LLONG_MAX;
+        gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, 1));
+        gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, 2));
+        gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, 4));
+        const int gbase = lane & ~7;
+        const int j = lane & 7;
+        unsigned tied =
+            (__ballot_sync(0xffffffffu, valid && (long long)bs.x + rm.y == gmin) >> gbase) & 0xffu;
+        while (__any_sync(0xffffffffu, tied != 0)) {
+          const int src = tied ? gbase + __ffs(tied) - 1 : lane;
+          const int loc = __shfl_sync(0xffffffffu, bs.y, src);
+          const int b2 = __shfl_sync(0xffffffffu, bs.x, src);
+          const int t = loc >> 4;
+          const int slot0 = slot_h + (loc & 15) * 8;
+          int m = 0, kh = 0;
+          if (tied) {
+            m = (b2 - p.tile_info[t].x) >> 1;
+            const int srow = sp * 32 + src;
+            const uint8_t* arow = p.a_tiles + (size_t)(g * RG + r) * (kTileM * KPAD) +
+                                  (srow >> 3) * 128 + (srow & 7) * 16;
+            const int8_t* bcol = p.b_tiles + (size_t)t * kB + (slot0 >> 3) * 128 + j * 16;
+#pragma unroll 4
+            for (int kc = 0; kc < chunks; ++kc) {
+              const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(arow + kc * (kTileM * 16)));
+              const uint4 b4 = __ldg(reinterpret_cast<const uint4*>(bcol + kc * (kTileN * 16)));
+              kh = dp4a_us(a4.x, b4.x, kh);
+              kh = dp4a_us(a4.y, b4.y, kh);
+              kh = dp4a_us(a4.z, b4.z, kh);
+              kh = dp4a_us(a4.w, b4.w, kh);
+            }
+          }
+          const unsigned hits = (__ballot_sync(0xffffffffu, tied && kh == m) >> gbase) & 0xffu;
+          if (tied) {
+            const int col = p.colmap[(size_t)t * kTileN + slot0 + __ffs(hits) - 1];
+            const int e_idx = col / S, si = col - e_idx * S;
+            const unsigned long long k2 =
+                ((unsigned long long)gmin << 32) |
+                (unsigned long long)((e_idx * 8 + (src & 7)) * S + si);
+            key = k2 < key ? k2 : key;
+            tied &= tied - 1;
           }
         }
-        int jj = 7;
-#pragma unroll
-        for (int j = 6; j >= 0; --j) jj = (kh[j] == m) ? j : jj;
-        const int col = p.colmap[(size_t)t * kTileN + slot0 + jj];
-        const long long err = (long long)bs.x + rm.y;
-        const int e_idx = col / S, si = col - e_idx * S;
-        key = ((unsigned long long)err << 32) | (unsigned long long)((e_idx * 8 + iso) * S + si);
       }
       unsigned long long w = __shfl_xor_sync(0xffffffffu, key, 1);
       key = w < key ? w : key;
@@ -327,8 +369,9 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
   }
 }
 
-// Work order (all roles derive it identically): unit u -> row group
-// g = u % n_rgroups, column-tile span u / n_rgroups; inside a unit: tiles t,
+// Work order (all roles derive it identically): the CTA's share of
+// (row group, tile) pairs as segments (cta_share / next_seg; one A load and
+// one column resolution per segment); inside a segment: tiles t descending,
 // row tiles r; the (tile, row tile) counter H selects accumulator H % 2,
 // which epilogue group H % 2 drains.
 __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) {
@@ -372,18 +415,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   const uint32_t tmem_base = *tmem_slot;
 
   const TcPlan plan = *p.plan;
-  const int n_rg = plan.n_rgroups;
-  const int CT = plan.tiles_per_unit;
-  const int n_units = plan.n_units;
+  int p0, p1, g, t0, t1;
+  cta_share(plan.n_pairs, p0, p1);
 
   if (warp == 0) {
     // ---------------- producer (TMA engine bulk copies) ----------------
     if (lane == 0) {
       uint32_t L = 0, U = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++U) {
-        const int g = u % n_rg;
-        const int t0 = (u / n_rg) * CT;
-        const int t1 = min(p.ntiles, t0 + CT);
+      for (int pp = p0; next_seg(pp, p1, p.ntiles, g, t0, t1); ++U) {
         ptx::mbar_wait_sleep(aempty_bar, (U & 1) ^ 1);
         ptx::mbar_expect_tx(afull_bar, kA);
         ptx::bulk_g2s(ptx::smem_u32(sA), p.a_tiles + (size_t)g * kA, kA, afull_bar);
@@ -408,9 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     constexpr uint64_t kBStep = (2 * kTileN * 16) >> 4;
     const uint32_t a_base = ptx::smem_u32(sA);
     uint32_t L = 0, H = 0, U = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++U) {
-      const int t0 = (u / n_rg) * CT;
-      const int t1 = min(p.ntiles, t0 + CT);
+    for (int pp = p0; next_seg(pp, p1, p.ntiles, g, t0, t1); ++U) {
       ptx::mbar_wait_sleep(afull_bar, U & 1);
       ptx::tc_fence_after();
       for (int t = t1 - 1; t >= t0; --t, ++L) {
@@ -437,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   } else if (warp >= 4) {
     // ---------------- epilogue: 16 warps drain every accumulator ----------------
     const EpiCtx x{smem, sStage, kStage, kB, bar_base, tmem_base, STAGES, RG, KPAD,
-                   n_units, n_rg, CT, warp, lane};
+                   plan.n_pairs, warp, lane};
     if (p.deferred) epilogue_role<true>(p, x);
     else epilogue_role<false>(p, x);
   }
@@ -624,9 +661,8 @@ struct FixPlan {
 
 // All per-level launch planning in ONE single-block kernel (the host never
 // waits for it):
-//  * unit decomposition of the contraction: RG row tiles per group, column
-//    tiles split into spans minimising the per-CTA makespan
-//    ceil(units / grid) * (tiles + 2) (first, i.e. smallest, span count wins);
+//  * work decomposition of the contraction: RG row tiles per group and the
+//    (group, tile) pair count the CTAs split evenly (see TcPlan);
 //  * clamp-correction jobs from the offset histogram: ranges with offset o
 //    against the columns whose qmin < -o (list 0) or qmax > 255 - o (list 1),
 //    blocks of RB ranges x 128 columns;
@@ -639,29 +675,12 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
                   int4* __restrict__ jobs, long long* __restrict__ prefix,
                   FixPlan* __restrict__ fplan, int32_t* __restrict__ order,
                   long long* __restrict__ fix_pairs_out) {
-  __shared__ unsigned long long best[kPlanThreads / 32];
   __shared__ int cursor[256];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = *d_M;
   // ---- unit decomposition ----
   const int n_rtiles = (M * 8 + kTileM - 1) / kTileM;
   const int n_rg = (n_rtiles + RG - 1) / RG;
-  unsigned long long mine = ~0ull;
-  const int smax = min(ntiles, 8192);
-  for (int sc = tid + 1; sc <= smax; sc += kPlanThreads) {
-    const unsigned ct = ((unsigned)ntiles + sc - 1) / (unsigned)sc;
-    const unsigned nsp = ((unsigned)ntiles + ct - 1) / ct;
-    const unsigned long long units = (unsigned long long)nsp * (unsigned)n_rg;
-    const unsigned long long cost = ((units + grid - 1) / (unsigned)grid) * (ct + 2);
-    const unsigned long long key = ((unsigned long long)cost << 24) | (unsigned long long)sc;
-    mine = key < mine ? key : mine;
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const unsigned long long w = __shfl_xor_sync(0xffffffffu, mine, o);
-    mine = w < mine ? w : mine;
-  }
-  if (lane == 0) best[warp] = mine;
   // ---- correction jobs: thread o < 256 owns offset bucket o ----
   int cnt = 0, njob = 0;
   long long lists[2] = {0, 0}, blocks = 0, pairs = 0;
@@ -732,16 +751,10 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
     }
   }
   if (tid == 0) {
-    unsigned long long bk = best[0];
-    for (int w = 1; w < kPlanThreads / 32; ++w) bk = best[w] < bk ? best[w] : bk;
-    const int sc = (int)(bk & 0xffffff);
-    const int ct = sc > 0 ? (ntiles + sc - 1) / sc : ntiles;
-    const int nsp = ct > 0 ? (ntiles + ct - 1) / ct : 0;
     TcPlan pl{};
     pl.M = M;
     pl.n_rgroups = M > 0 ? n_rg : 0;
-    pl.tiles_per_unit = ct;
-    pl.n_units = M > 0 ? nsp * n_rg : 0;
+    pl.n_pairs = M > 0 ? n_rg * ntiles : 0;
     pl.rows_pad = n_rg * RG * kTileM;
     *plan = pl;
   }
