@@ -180,21 +180,21 @@ def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=N
                                 launches=int(st.kernel_launches), scan_ms=float(st.scan_ms),
                                 main_ms=float(st.main_ms), fix_ms=float(st.fix_ms),
                                 fix_pairs=int(st.fix_pairs), rescans=int(st.rescans)))
-    records = RecordTable(rec[:, :5].astype(np.int64))
+    records = RecordTable._trusted(rec[:, :5].astype(np.int64))
     stream = CompressedStream(
         width=image.width, height=image.height, mode=policy.mode, strides=pool.params.strides,
         s_sets=s_sets, pools=tuple(pool.coords(level) for level in (1, 2, 3, 4)), records=records)
     encode_time = time.perf_counter() - t_start
     phase["records_stream"] = 1e3 * (time.perf_counter() - t_r)
     step_blocks = tuple(int(v) for v in np.bincount(rec[:, 0], minlength=5)[1:5])
-    return stream, _report(image, config, pool, stream, step_blocks, int(rec[:, 5].astype(np.int64).sum()),
+    return stream, _report(image, config, pool, stream, step_blocks, int(rec[:, 5].sum(dtype=np.int64)),
                            pool_time, encode_time, comparisons, scan_ms, level_stats, phase)
 
 
 def _report(image, config, pool, stream, step_blocks, collage_ssd, pool_time, encode_time,
             comparisons, scan_ms, level_stats, phase) -> "EncodeReport":
     pixels = image.width * image.height
-    payload = stream.payload_bits()
+    payload = sum(c * stream.record_bits(lv) for lv, c in zip((1, 2, 3, 4), step_blocks))
     head = header_bytes(stream)
     file_bytes = head + (payload + 7) // 8
     return EncodeReport(

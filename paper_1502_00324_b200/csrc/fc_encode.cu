@@ -316,6 +316,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     putp(c->readback.ptr);
     put(c->tc_debug_mode);
     put(c->tc_deferred);
+    put(c->tc_g1);
   }
   const bool reuse = use_graph && !c->trace && c->enc_exec && sig == c->enc_sig;
   int levels_run = 0;

@@ -181,6 +181,7 @@ struct Ctx {
   int tc_debug_mode = 0;               // FC_TC_DEBUG_MODE (pipeline probes)
   int pool_chunk = 0;                  // FC_POOL_CHUNK=512: smaller rank-sort chunks
   int tc_deferred = -1;                // FC_TC_DEFERRED: -1 = by K, 0/1 forced
+  int tc_g1 = -1;                      // FC_TC_G1: epilogue drain layout, -1 = default
   cudaGraphExec_t enc_exec = nullptr;  // instantiated level-loop graph, updated per encode
   std::vector<uint64_t> enc_sig;       // launch signature of enc_exec (reuse when equal)
   int enc_levels_run = 0;              // host-side results of the captured body

@@ -26,7 +26,7 @@ namespace fcb {
 namespace {
 
 constexpr int kEntWarps = 6;       // warps per block of the entropy kernel (2 blocks / SM)
-constexpr int kStripRows = 16;     // window rows one lane slides through
+constexpr int kEntBlocksPerSm = 2; // shared-memory bound (16 KB of histograms per warp)
 constexpr int kLutWords = 4 + 16 + 64 + 256 + 1024;  // the four [0, p*log(p)...] LUTs in smem
 
 __device__ __forceinline__ uint64_t entropy_key(double h) {
@@ -38,6 +38,7 @@ __device__ __forceinline__ uint64_t entropy_key(double h) {
 // Per-level description for the fused entropy kernel.
 struct EntLevel {
   int D, stride, nx, ny, strips_x, task_begin, lut_off;
+  int rows;  // window rows per task (one lane slides through them)
   int mode;  // 0: write key/val of every window (sort / argmin), 1: append {ent > tau}
   double tau;
   double* ent;
@@ -100,8 +101,12 @@ __device__ __forceinline__ void hist_rows(uint32_t hw, const uint8_t* __restrict
 
 // numpy pairwise sum of the 256 terms t[count] (pool.py:88-92): two 128-bin
 // halves, 8 running accumulators each, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)).
-// Zero bins add +0.0 (exact): lut[0] holds 0.0 and lut[k] = t(k), so every
-// bin is one unconditional load + add (no predication).
+// Zero bins add +0.0 (exact): lut[0] holds 0.0 and lut[k] = t(k).  Every term
+// is <= 0, so adding a zero term never changes an accumulator's bits, and an
+// 8-bin group (one term per accumulator, in bin order) that is empty in all
+// 32 windows of the warp is skipped with a warp-uniform branch: neighbouring
+// windows share most pixels, so typically 2/3 of the groups are skipped.
+// Must be called by the full warp (inactive lanes hold an all-zero histogram).
 __device__ __forceinline__ double window_entropy(uint32_t hw, uint32_t lut) {
   double half_sum[2];
 #pragma unroll
@@ -110,20 +115,25 @@ __device__ __forceinline__ double window_entropy(uint32_t hw, uint32_t lut) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.0;
 #pragma unroll
-    for (int p = 0; p < 64; ++p) {
-      const uint32_t w = lds_u32_ordered(hw + (half * 64 + p) * 128);
-      // counts <= 1024 < 2^13, so (w >> 13) == 8 * (w >> 16)
-      const uint32_t a0 = lut + ((w & 0xffffu) << 3), a1 = lut + (w >> 13);
-      const int j0 = (2 * p) & 7;
-      acc[j0] = acc[j0] + lds_f64(a0);
-      acc[j0 + 1] = acc[j0 + 1] + lds_f64(a1);
+    for (int g = 0; g < 16; ++g) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = lds_u32_ordered(hw + (half * 64 + g * 4 + q) * 128);
+      if (__any_sync(0xffffffffu, (w[0] | w[1] | w[2] | w[3]) != 0u)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          // counts <= 1024 < 2^13, so (w >> 13) == 8 * (w >> 16)
+          acc[2 * q] = acc[2 * q] + lds_f64(lut + ((w[q] & 0xffffu) << 3));
+          acc[2 * q + 1] = acc[2 * q + 1] + lds_f64(lut + (w[q] >> 13));
+        }
+      }
     }
     half_sum[half] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
   }
   return -(half_sum[0] + half_sum[1]);
 }
 
-// One warp per task = 32 adjacent window columns x kStripRows window rows of
+// One warp per task = 32 adjacent window columns x L.rows window rows of
 // one level.  Each lane keeps its window's 256-bin histogram and slides it
 // down by `stride` rows (remove the rows that leave, add the rows that
 // enter), so a window costs 2*stride*D updates instead of D*D.
@@ -135,8 +145,8 @@ __device__ __forceinline__ void entropy_task(const EntLevel& L, const uint8_t* _
   const int sy = t / L.strips_x, sx = t - sy * L.strips_x;
   const int wx = sx * 32 + lane;
   const bool active = wx < L.nx;
-  const int wy0 = sy * kStripRows;
-  const int wy1 = min(wy0 + kStripRows, L.ny);
+  const int wy0 = sy * L.rows;
+  const int wy1 = min(wy0 + L.rows, L.ny);
   const int s = L.stride;
   const int x = wx * s;
 #pragma unroll 8
@@ -148,8 +158,7 @@ __device__ __forceinline__ void entropy_task(const EntLevel& L, const uint8_t* _
       hist_rows<D>(h, img, width, x, yp, yp + min(s, D), 0xffffffffu, 0xffff0000u);
       hist_rows<D>(h, img, width, x, max(yp + D, yn), yn + D, 1u, 0x10000u);
     }
-    double H = 0.0;
-    if (active) H = window_entropy(h, lut);
+    const double H = window_entropy(h, lut);  // whole warp (see window_entropy)
     const int64_t w = (int64_t)wy * L.nx + wx;
     if (L.mode == 0) {
       if (active) {
@@ -640,9 +649,28 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     E.val = L.win_val.as<uint32_t>();
     E.sel_count = d_nsel + li;
     P.lut[li] = c->lut[lut_slot(D * D)].as<double>();
-    tasks += E.strips_x * ((ny + kStripRows - 1) / kStripRows);
+    tasks += E.strips_x;  // placeholder: rows per task chosen below
     lut_off += D * D + 1;
     any_tau |= use_tau[li];
+  }
+  // Rows per task: the smallest count whose tasks all fit in one wave of
+  // resident warps (every task costs about the same per row, so the kernel
+  // time is the longest task; a second partial wave would double it).
+  {
+    const int64_t resident = (int64_t)c->sm_count * kEntBlocksPerSm * kEntWarps;
+    int rows = 4;
+    for (;; ++rows) {
+      int64_t t = 0;
+      for (int li = 0; li < kLevels; ++li)
+        t += (int64_t)P.lv[li].strips_x * ((P.lv[li].ny + rows - 1) / rows);
+      if (t <= resident || rows >= 1 << 20) break;
+    }
+    tasks = 0;
+    for (int li = 0; li < kLevels; ++li) {
+      P.lv[li].rows = rows;
+      P.lv[li].task_begin = tasks;
+      tasks += P.lv[li].strips_x * ((P.lv[li].ny + rows - 1) / rows);
+    }
   }
   P.total_tasks = tasks;
   trace_mark(c, "pool_begin");
@@ -653,7 +681,8 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     c->ent_attr_set = true;
   }
   {
-    const int blocks = std::max(1, std::min((tasks + kEntWarps - 1) / kEntWarps, c->sm_count * 2));
+    const int blocks =
+        std::max(1, std::min((tasks + kEntWarps - 1) / kEntWarps, c->sm_count * kEntBlocksPerSm));
     entropy_all_kernel<<<blocks, kEntWarps * 32, kEntSmem, c->stream>>>(c->img_ptr, c->width, P);
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 1;

@@ -111,6 +111,7 @@ struct TcParams {
   int ntiles;
   const TcPlan* plan;
   int deferred;    // 1: resolve the winning column once per unit (short K)
+  int g1;          // 1: every epilogue warp drains every accumulator (64 columns)
   unsigned long long* tspan;  // optional {start, end} slots (global ns)
 };
 
@@ -173,37 +174,43 @@ struct EpiCtx {
   int STAGES, RG, KPAD, n_pairs, warp, lane;
 };
 
-template <bool DEFERRED>
+template <bool DEFERRED, bool G1>
 __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x) {
   uint8_t* smem = x.smem;
   uint8_t* sStage = x.sStage;
   const uint32_t kStage = x.kStage, kB = x.kB, bar_base = x.bar_base, tmem_base = x.tmem_base;
   const int STAGES = x.STAGES, RG = x.RG, KPAD = x.KPAD, warp = x.warp, lane = x.lane;
-  // Two groups of 8 warps alternate over the accumulators (group gq drains the
-  // (tile, row tile) pairs with H & 1 == gq, i.e. accumulator gq): one group
-  // computes while the other loads, and every barrier wait / release covers
-  // 128 columns per thread (two 64-column waves).
+  // G1 == false: two groups of 8 warps alternate over the accumulators (group
+  // gq drains the (tile, row tile) pairs with H & 1 == gq, i.e. accumulator
+  // gq): one group computes while the other loads, and every barrier wait /
+  // release covers 128 columns per thread (two 64-column waves).
+  // G1 == true: all 16 warps drain every accumulator, 64 columns per thread in
+  // one wave, and release it before any arithmetic.
+  constexpr int kWaves = G1 ? 1 : 2;
+  constexpr int kGiBits = G1 ? 3 : 4;  // 8-column groups per thread and tile: 8 or 16
   const int e = warp - 4;
-  const int gq = e >> 3;          // accumulator / group
-  const int hq = (e >> 2) & 1;    // 128-column half of the 256-column tile
+  const int gq = G1 ? 0 : e >> 3;     // accumulator / group
+  const int hq = G1 ? e >> 2 : (e >> 2) & 1;  // column quarter (G1) or half
   const int sp = warp & 3;        // TMEM sub-partition (lanes 32*sp .. 32*sp+31)
   const int row = sp * 32 + lane;
   const int S = p.S;
   const int iso = lane & 7;
-  const uint32_t tm = tmem_base + ((uint32_t)(sp * 32) << 16) + gq * kAccN + hq * 128;
-  const int slot_h = hq * 128;
+  const int slot_h = G1 ? hq * 64 : hq * 128;
+  const uint32_t tm = ptx::pin(tmem_base + ((uint32_t)(sp * 32) << 16) + gq * kAccN + slot_h);
   // this thread's {best2, loc} per resident row tile, stride = 512 threads
-  int2* bstate = reinterpret_cast<int2*>(smem + best_offset(p)) + (e * 32 + lane);
+  // (shared addresses pinned in registers: re-deriving them costs ~30
+  // instructions per iteration under the 96-register budget)
+  const uint32_t bst = ptx::pin(ptx::smem_u32(smem + best_offset(p)) + (e * 32 + lane) * 8);
   constexpr int kBS = kEpiWarps * 32;
-  const uint32_t tfull = bar_base + 8u * (2 * STAGES + gq);
-  const uint32_t tempty = bar_base + 8u * (2 * STAGES + kNumAcc + gq);
+  const uint32_t tfull0 = ptx::pin(bar_base + 8u * (2 * STAGES + gq));
+  const uint32_t tempty0 = ptx::pin(bar_base + 8u * (2 * STAGES + kNumAcc + gq));
   uint32_t H = 0;
   int stg = 0;
   uint32_t stg_phase = 0;
   int p0, p1, g, t0, t1;
   cta_share(x.n_pairs, p0, p1);
   for (int pp = p0; next_seg(pp, p1, p.ntiles, g, t0, t1);) {
-    for (int r = 0; r < RG; ++r) bstate[r * kBS] = make_int2(kNone, 0);
+    for (int r = 0; r < RG; ++r) ptx::sts_v2(bst + r * (kBS * 8), make_int2(kNone, 0));
     // tiles in DECREASING order (see improve_limit); tile_info one tile ahead
     int2 tinfo_next = p.tile_info[t1 - 1];
     for (int t = t1 - 1; t >= t0; --t) {
@@ -216,25 +223,26 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
       // the tiles alternate between the groups.
       const uint32_t Ht = H;
       H += RG;
-      const int r_first = (int)((gq - (int)(Ht & 1)) & 1);
+      const int r_first = G1 ? 0 : (int)((gq - (int)(Ht & 1)) & 1);
 #pragma unroll 1
-      for (int r = r_first; r < RG; r += 2) {
+      for (int r = r_first; r < RG; r += G1 ? 1 : 2) {
         const uint32_t Hr = Ht + r;
-        const int2 bs = bstate[r * kBS];  // issued before the wait: latency hidden
-        ptx::mbar_wait_sleep(tfull, (Hr >> 1) & 1);
+        const uint32_t acc = G1 ? (Hr & 1) : 0;
+        const int2 bs = ptx::lds_v2(bst + r * (kBS * 8));  // issued before the wait
+        ptx::mbar_wait_sleep(tfull0 + 8u * acc, (Hr >> 1) & 1);
         ptx::tc_fence_after();
         int va[32], vb[32];
         int m_best = kNone, gi_best = 0;
 #pragma unroll
-        for (int wv = 0; wv < 2; ++wv) {
-          ptx::tmem_ld32(tm + wv * 64, va);
-          ptx::tmem_ld32(tm + wv * 64 + 32, vb);
+        for (int wv = 0; wv < kWaves; ++wv) {
+          ptx::tmem_ld32(tm + acc * kAccN + wv * 64, va);
+          ptx::tmem_ld32(tm + acc * kAccN + wv * 64 + 32, vb);
           ptx::tmem_wait_ld();
-          if (wv == 1) {
+          if (wv == kWaves - 1) {
             // every value of this half is in registers: release the accumulator
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(tempty);
+            if (lane == 0) ptx::mbar_arrive(tempty0 + 8u * acc);
           }
           const int sq = slot_h + wv * 64;
           if (tinfo.y < kTileN) {  // mask padding slots (last tile of a group)
@@ -279,9 +287,9 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
         if constexpr (DEFERRED) {
           // branch-free: record the 8-column group, resolve at the unit end
           if (m_best < improve_limit(bs.x, tinfo.x))
-            bstate[r * kBS] = make_int2(2 * m_best + tinfo.x, t * 16 + gi_best);
+            ptx::sts_v2(bst + r * (kBS * 8), make_int2(2 * m_best + tinfo.x, (t << kGiBits) + gi_best));
         } else {
-          if (m_best != kNone) bstate[r * kBS] = make_int2(2 * m_best + tinfo.x, gi_best);
+          if (m_best != kNone) ptx::sts_v2(bst + r * (kBS * 8), make_int2(2 * m_best + tinfo.x, gi_best));
         }
       }
       if constexpr (!DEFERRED) {
@@ -304,7 +312,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
 #pragma unroll 1
     for (int r = 0; r < RG; ++r) {
       unsigned long long key = ~0ull;
-      const int2 bs = bstate[r * kBS];
+      const int2 bs = ptx::lds_v2(bst + r * (kBS * 8));
       const int4 rm = p.row_meta[(size_t)(g * RG + r) * kTileM + row];  // {o, R, m, -}
       const bool valid = bs.x != kNone && rm.z >= 0;
       if constexpr (!DEFERRED) {
@@ -327,8 +335,8 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
           const int src = tied ? gbase + __ffs(tied) - 1 : lane;
           const int loc = __shfl_sync(0xffffffffu, bs.y, src);
           const int b2 = __shfl_sync(0xffffffffu, bs.x, src);
-          const int t = loc >> 4;
-          const int slot0 = slot_h + (loc & 15) * 8;
+          const int t = loc >> kGiBits;
+          const int slot0 = slot_h + (loc & ((1 << kGiBits) - 1)) * 8;
           int m = 0, kh = 0;
           if (tied) {
             m = (b2 - p.tile_info[t].x) >> 1;
@@ -402,7 +410,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     }
     for (int b = 0; b < kNumAcc; ++b) {
       ptx::mbar_init(tfull_bar(b), 1);
-      ptx::mbar_init(tempty_bar(b), kEpiWarps / 2);  // one group of 8 warps per accumulator
+      // G1: all 16 epilogue warps release; else one group of 8 warps per accumulator
+      ptx::mbar_init(tempty_bar(b), p.g1 ? kEpiWarps : kEpiWarps / 2);
     }
     ptx::mbar_init(afull_bar, 1);
     ptx::mbar_init(aempty_bar, 1);
@@ -475,8 +484,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     // ---------------- epilogue: 16 warps drain every accumulator ----------------
     const EpiCtx x{smem, sStage, kStage, kB, bar_base, tmem_base, STAGES, RG, KPAD,
                    plan.n_pairs, warp, lane};
-    if (p.deferred) epilogue_role<true>(p, x);
-    else epilogue_role<false>(p, x);
+    if (p.g1) {
+      if (p.deferred) epilogue_role<true, true>(p, x);
+      else epilogue_role<false, true>(p, x);
+    } else {
+      if (p.deferred) epilogue_role<true, false>(p, x);
+      else epilogue_role<false, false>(p, x);
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -1110,6 +1124,7 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   prm.tspan = d_time;
   // measured: the per-unit recompute wins only for short K
   prm.deferred = c->tc_deferred >= 0 ? c->tc_deferred : (T.kpad <= 128 ? 1 : 0);
+  prm.g1 = c->tc_g1 >= 0 ? c->tc_g1 : 0;
   const uint32_t smem = smem_bytes(prm);
   if (!c->tc_attr_set) {
     FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -31,6 +31,22 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+// Keep a value in a register: the compiler cannot re-derive it (e.g. a shared
+// address from SR_CgaCtaId) inside a hot loop.
+__device__ __forceinline__ uint32_t pin(uint32_t x) {
+  uint32_t y;
+  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ int2 lds_v2(uint32_t a) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_v2(uint32_t a, int2 v) {
+  asm volatile("st.shared.v2.s32 [%0], {%1, %2};" ::"r"(a), "r"(v.x), "r"(v.y) : "memory");
+}
+
 // Same wait with a suspend-time hint: the thread sleeps until the phase
 // completes (or ~the hint elapses) instead of re-issuing try_wait in a loop.
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {

@@ -8,7 +8,7 @@
 
 using namespace fcb;
 
-template <int EPI, int NACC, int N, int GROUPS>
+template <int EPI, int NACC, int N, int GROUPS, int SPIN>
 __global__ void __launch_bounds__((4 + EPI) * 32, 1) probe(int iters, int ks_n, int work, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
@@ -35,7 +35,8 @@ __global__ void __launch_bounds__((4 + EPI) * 32, 1) probe(int iters, int ks_n, 
     constexpr uint32_t idesc = ptx::idesc_i8(128, N);
     for (int h = 0; h < iters; ++h) {
       const int acc = h % NACC;
-      ptx::mbar_wait_sleep(ptx::smem_u32(&bars[NACC + acc]), ((h / NACC) & 1) ^ 1);
+      if (SPIN & 1) ptx::mbar_wait(ptx::smem_u32(&bars[NACC + acc]), ((h / NACC) & 1) ^ 1);
+      else ptx::mbar_wait_sleep(ptx::smem_u32(&bars[NACC + acc]), ((h / NACC) & 1) ^ 1);
       ptx::tc_fence_after();
       for (int ks = 0; ks < ks_n; ++ks) {
         const uint64_t ad = ptx::umma_desc(a + ks * 2 * 2048, 2048, 128);
@@ -52,14 +53,23 @@ __global__ void __launch_bounds__((4 + EPI) * 32, 1) probe(int iters, int ks_n, 
     const uint32_t base = tm + ((uint32_t)(sp * 32) << 16) + (eg >> 2) * cols_per;
     for (int h = grp; h < iters; h += GROUPS) {
       const int acc = h % NACC;
-      ptx::mbar_wait_sleep(ptx::smem_u32(&bars[acc]), (h / NACC) & 1);
+      if (SPIN & 2) ptx::mbar_wait(ptx::smem_u32(&bars[acc]), (h / NACC) & 1);
+      else ptx::mbar_wait_sleep(ptx::smem_u32(&bars[acc]), (h / NACC) & 1);
       ptx::tc_fence_after();
       int v[32], u[32];
-      for (int c = 0; c < cols_per; c += 64) {
-        ptx::tmem_ld32(base + acc * N + c, v);
-        ptx::tmem_ld32(base + acc * N + c + 32, u);
-        ptx::tmem_wait_ld();
-        for (int j = 0; j < 32; ++j) sink += v[j] ^ u[j];
+      if (cols_per >= 64) {
+        for (int c = 0; c < cols_per; c += 64) {
+          ptx::tmem_ld32(base + acc * N + c, v);
+          ptx::tmem_ld32(base + acc * N + c + 32, u);
+          ptx::tmem_wait_ld();
+          for (int j = 0; j < 32; ++j) sink += v[j] ^ u[j];
+        }
+      } else {
+        for (int c = 0; c < cols_per; c += 32) {
+          ptx::tmem_ld32(base + acc * N + c, v);
+          ptx::tmem_wait_ld();
+          for (int j = 0; j < 32; ++j) sink += v[j];
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -76,35 +86,32 @@ __global__ void __launch_bounds__((4 + EPI) * 32, 1) probe(int iters, int ks_n, 
   if (sink == 12345) out[blockIdx.x + 1000] = sink;
 }
 
-template <int EPI, int NACC, int N, int GROUPS = 1>
+template <int EPI, int NACC, int N, int GROUPS = 1, int SPIN = 0>
 void run(int ks, int work) {
   unsigned long long* d;
   cudaMalloc(&d, 8 * 2048);
   const int smem = (128 + 256) * 128;
-  cudaFuncSetAttribute(probe<EPI, NACC, N, GROUPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(probe<EPI, NACC, N, GROUPS, SPIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
-  probe<EPI, NACC, N, GROUPS><<<148, (4 + EPI) * 32, smem>>>(50, ks, work, d);
-  probe<EPI, NACC, N, GROUPS><<<148, (4 + EPI) * 32, smem>>>(iters, ks, work, d);
+  probe<EPI, NACC, N, GROUPS, SPIN><<<148, (4 + EPI) * 32, smem>>>(50, ks, work, d);
+  probe<EPI, NACC, N, GROUPS, SPIN><<<148, (4 + EPI) * 32, smem>>>(iters, ks, work, d);
   cudaDeviceSynchronize();
   unsigned long long h;
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-  printf("G=%d EPI=%2d NACC=%d N=%d K=%3d work=%3d: %6.0f cycles/acc, %6.0f per 128x256 tile (%s)\n", GROUPS, EPI, NACC, N,
+  printf("SPIN=%d G=%d EPI=%2d NACC=%d N=%d K=%3d work=%3d: %6.0f cycles/acc, %6.0f per 128x256 tile (%s)\n", SPIN, GROUPS, EPI, NACC, N,
          32 * ks, work, (double)h / iters, (double)h / iters * 256 / N, cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
 
 int main() {
-  for (int ks = 1; ks <= 3; ks += 2) {
-    run<16, 2, 256, 1>(ks, 0);
-    run<16, 2, 256, 1>(ks, 30);
-    run<16, 2, 256, 1>(ks, 60);
-    run<16, 2, 256, 2>(ks, 0);
-    run<16, 2, 256, 2>(ks, 60);
-    run<16, 2, 256, 2>(ks, 120);
-    run<16, 4, 128, 2>(ks, 0);
-    run<16, 4, 128, 2>(ks, 60);
-    run<16, 4, 128, 4>(ks, 0);
-    run<16, 4, 128, 4>(ks, 60);
+  for (int ks = 1; ks <= 3; ++ks) {
+    run<16, 2, 256, 2, 0>(ks, 0);
+    run<16, 2, 256, 2, 1>(ks, 0);
+    run<16, 2, 256, 2, 2>(ks, 0);
+    run<16, 2, 256, 2, 3>(ks, 0);
+    run<16, 4, 128, 4, 0>(ks, 0);
+    run<16, 4, 128, 4, 3>(ks, 0);
+    run<16, 2, 256, 1, 3>(ks, 0);
   }
   return 0;
 }
