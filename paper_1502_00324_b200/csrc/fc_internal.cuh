@@ -261,10 +261,6 @@ int load_ranges(Ctx* c, Level& L, const uint8_t* h_tiles, int64_t M);
 int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t n_range_list,
                const int32_t* d_col_list, int64_t n_col_list, uint64_t* d_keys,
                const int32_t* d_M = nullptr, unsigned long long* d_time = nullptr);
-int scan_exact_jobs(Ctx* c, Level& L, const int4* d_jobs, const int64_t* d_prefix,
-                    const int* d_n_jobs, const long long* d_total_blocks,
-                    const int32_t* d_sorted_ranges, const int32_t* d_low, const int32_t* d_high,
-                    uint64_t* d_keys, unsigned long long* d_time_end = nullptr);
 int decode_keys(Ctx* c, const uint64_t* d_keys, int64_t M, int64_t* d_err, int64_t* d_idx);
 int iso_table_offset(int side);
 int scan_rows_dropin(Ctx* c, const int16_t* ranges, const double* rmeans, int64_t M, int32_t n,

@@ -195,59 +195,6 @@ scan_exact_kernel(const int16_t* __restrict__ qbase, int64_t ncols, int S,
   }
 }
 
-// Job-list scan (tensor-path clamp corrections): job j covers the ranges
-// sorted_ranges[r_off, r_off + r_cnt) against the first col_cnt columns of
-// column list `list` (0 = reach_low, 1 = reach_high).  Blocks are laid out
-// densely: block b belongs to the job whose prefix[j] <= b < prefix[j + 1].
-template <int N>
-__global__ void __launch_bounds__(kColsPerBlock)
-scan_jobs_kernel(const int16_t* __restrict__ qbase, int S, const double* __restrict__ svals,
-                 const double* __restrict__ dmean, const uint8_t* __restrict__ rtiles,
-                 const double* __restrict__ rmean, const uint16_t* __restrict__ inv,
-                 const int4* __restrict__ jobs, const int64_t* __restrict__ prefix,
-                 const int* __restrict__ d_n_jobs, const long long* __restrict__ d_total,
-                 const int32_t* __restrict__ sorted_ranges, const int32_t* __restrict__ list_low,
-                 const int32_t* __restrict__ list_high, int baseline,
-                 unsigned long long* __restrict__ keys, unsigned long long* __restrict__ t_end) {
-  __shared__ __align__(16) ExactSmem<N> s;
-  __shared__ int s_job;
-  __shared__ long long s_prefix[513];  // at most 2 jobs per offset bucket, + the total
-  const int tid = threadIdx.x;
-  const int n_jobs = *d_n_jobs;
-  const long long total = *d_total;
-  if ((long long)blockIdx.x >= total) return;
-  for (int j = tid; j <= n_jobs; j += blockDim.x) s_prefix[j] = prefix[j];
-  // persistent: the block count is only known on the device
-  for (long long b = blockIdx.x; b < total; b += gridDim.x) {
-    __syncthreads();  // the previous block's shared state is consumed (and s_prefix is loaded)
-    if (tid == 0) {
-      int lo = 0, hi = n_jobs - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_prefix[mid] <= b) lo = mid; else hi = mid - 1;
-      }
-      s_job = lo;
-    }
-    __syncthreads();
-    const int4 job = jobs[s_job];  // {list, r_off, r_cnt, col_cnt}
-    const int64_t local = b - s_prefix[s_job];
-    const int64_t ncc = (job.w + kColsPerBlock - 1) / kColsPerBlock;
-    const int64_t rb = local / ncc, cc = local - rb * ncc;
-    if (tid < ExactSmem<N>::RB) {
-      const int64_t idx = rb * ExactSmem<N>::RB + tid;
-      const int m = idx < job.z ? sorted_ranges[job.y + idx] : -1;
-      s.m[tid] = m;
-      s.rmean[tid] = m >= 0 ? rmean[m] : 0.0;
-    }
-    const int64_t ci = cc * kColsPerBlock + tid;
-    const int32_t* list = job.x ? list_high : list_low;
-    const int64_t col = ci < job.w ? (int64_t)list[ci] : -1;
-    __syncthreads();
-    exact_block<N>(s, qbase, S, svals, dmean, rtiles, inv, col, baseline, keys);
-  }
-  if (t_end && tid == 0) atomicMax(t_end, global_ns());
-}
-
 // Drop-in for _scan.py:14 with arbitrary candidate rows (reference layout).
 __global__ void __launch_bounds__(128)
 scan_rows_kernel(const int16_t* __restrict__ q, int64_t rows, int n, int S,
@@ -747,32 +694,6 @@ int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t
     FC_CUDA(c, cudaGetLastError());
     c->stats.kernel_launches += 1;
   }
-  return FC_OK;
-}
-
-int scan_exact_jobs(Ctx* c, Level& L, const int4* d_jobs, const int64_t* d_prefix,
-                    const int* d_n_jobs, const long long* d_total_blocks,
-                    const int32_t* d_sorted_ranges, const int32_t* d_low, const int32_t* d_high,
-                    uint64_t* d_keys, unsigned long long* d_time_end) {
-  FC_TRY(ensure_iso_tables(c));
-  const double* d_s = L.svals_d.as<double>();
-  const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
-  auto* keys = reinterpret_cast<unsigned long long*>(d_keys);
-  const unsigned grid = (unsigned)(c->sm_count * 8);
-#define FC_LAUNCH_JOBS(NN)                                                                      \
-  scan_jobs_kernel<NN><<<grid, kColsPerBlock, 0, c->stream>>>(                                  \
-      L.qbase.as<int16_t>(), L.s_count, d_s, L.mean.as<double>(), c->rtiles.as<uint8_t>(),        \
-      c->rmean.as<double>(), inv, d_jobs, d_prefix, d_n_jobs, d_total_blocks, d_sorted_ranges,    \
-      d_low, d_high, L.baseline, keys, d_time_end)
-  switch (L.n) {
-    case 256: FC_LAUNCH_JOBS(256); break;
-    case 64: FC_LAUNCH_JOBS(64); break;
-    case 16: FC_LAUNCH_JOBS(16); break;
-    default: FC_LAUNCH_JOBS(4); break;
-  }
-#undef FC_LAUNCH_JOBS
-  FC_CUDA(c, cudaGetLastError());
-  c->stats.kernel_launches += 1;
   return FC_OK;
 }
 

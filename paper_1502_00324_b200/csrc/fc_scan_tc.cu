@@ -665,11 +665,16 @@ __global__ void reach_scatter_kernel(const int4* __restrict__ stats, int64_t nco
   bucket_scatter(valid, st.w + 512, cur_high, reach_high, (int32_t)col);
 }
 
+// Clamp corrections: a warp handles one range x fix_cols(n) columns per unit
+// (n = 256: one column per lane, the few pairs of B = 16 need parallelism).
+__host__ __device__ constexpr int fix_cpl(int n) { return n >= 256 ? 1 : 4; }
+__host__ __device__ constexpr int fix_cols(int n) { return 32 * fix_cpl(n); }
+
 // Clamp-correction plan (FixPlan) of one level.
 struct FixPlan {
   int n_jobs;
   int pad;
-  long long total_blocks;
+  long long total_units;  // (range, fix_cols(n)-column chunk) units; prefix[] counts them too
   long long fix_pairs;
 };
 
@@ -679,13 +684,13 @@ struct FixPlan {
 //    (group, tile) pair count the CTAs split evenly (see TcPlan);
 //  * clamp-correction jobs from the offset histogram: ranges with offset o
 //    against the columns whose qmin < -o (list 0) or qmax > 255 - o (list 1),
-//    blocks of RB ranges x 128 columns;
+//    units of one range x fix_cols(n) columns (fix_pairs_kernel);
 //  * the ranges bucketed by offset (counting sort, bucket order free).
 constexpr int kPlanThreads = 1024;
 __global__ void __launch_bounds__(kPlanThreads)
 level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
                   const int32_t* __restrict__ hist, const long long* __restrict__ reach_counts,
-                  int RB, const int32_t* __restrict__ roff, TcPlan* __restrict__ plan,
+                  int fcols, const int32_t* __restrict__ roff, TcPlan* __restrict__ plan,
                   int4* __restrict__ jobs, long long* __restrict__ prefix,
                   FixPlan* __restrict__ fplan, int32_t* __restrict__ order,
                   long long* __restrict__ fix_pairs_out) {
@@ -705,7 +710,7 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
     for (int k = 0; k < 2; ++k)
       if (cnt && lists[k]) {
         ++njob;
-        blocks += (long long)((cnt + RB - 1) / RB) * ((lists[k] + 127) / 128);
+        blocks += (long long)cnt * ((lists[k] + fcols - 1) / fcols);  // range x fcols columns
         pairs += (long long)cnt * lists[k];
       }
   }
@@ -749,7 +754,7 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
       if (cnt && lists[k]) {
         jobs[j] = make_int4(k, cursor[tid], cnt, (int)lists[k]);
         prefix[j] = b;
-        b += (long long)((cnt + RB - 1) / RB) * ((lists[k] + 127) / 128);
+        b += (long long)cnt * ((lists[k] + fcols - 1) / fcols);
         ++j;
       }
     if (tid == 255) {
@@ -757,7 +762,7 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
       for (int w2 = 0; w2 < 8; ++w2) tp += wt_p[w2];
       FixPlan fp{};
       fp.n_jobs = j;
-      fp.total_blocks = b;
+      fp.total_units = b;
       fp.fix_pairs = tp;
       *fplan = fp;
       if (fix_pairs_out) *fix_pairs_out = tp;
@@ -775,6 +780,119 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
   __syncthreads();
   // ---- ranges bucketed by offset ----
   for (int i = tid; i < M; i += kPlanThreads) order[atomicAdd(&cursor[roff[i]], 1)] = i;
+}
+
+// Clamp corrections: one warp per unit = one range x kFixCols consecutive
+// columns of a job (job j: ranges sorted_ranges[r_off, r_off + r_cnt) x the
+// first col_cnt columns of reach list `list`), kFixCpl columns per lane.  The
+// exact error of all 8 isometries follows _scan.py:47-55 (clip(q + o) - r,
+// squared, summed): a column's clipped pixels are packed to bytes once per
+// 16-pixel chunk and compared with the range's isometry rows, read straight
+// from the A operand (its first n bytes of K are r[inv_iso[k]]; warp-uniform
+// broadcast loads, shared by the lane's columns).  Minimum over the lane's
+// columns, then the warp (err, then candidate index), one atomicMin per unit.
+constexpr int kFixThreads = 256;
+template <int N>
+__global__ void __launch_bounds__(kFixThreads)
+fix_pairs_kernel(const int16_t* __restrict__ qbase, int S, const uint8_t* __restrict__ a_tiles,
+                 int kpad, const int32_t* __restrict__ roff, const int4* __restrict__ jobs,
+                 const long long* __restrict__ prefix, const FixPlan* __restrict__ fplan,
+                 const int32_t* __restrict__ sorted_ranges, const int32_t* __restrict__ list_low,
+                 const int32_t* __restrict__ list_high, unsigned long long* __restrict__ keys,
+                 unsigned long long* __restrict__ t_end) {
+  static_assert(N % 16 == 0, "tensor levels have n >= 16");
+  constexpr int kWarps = kFixThreads / 32;
+  constexpr int kFixCpl = fix_cpl(N), kFixCols = fix_cols(N);
+  __shared__ long long s_prefix[513];  // at most 2 jobs per offset bucket, + the total
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int n_jobs = fplan->n_jobs;
+  const long long total = fplan->total_units;
+  if ((long long)blockIdx.x * kWarps >= total) return;
+  for (int j = tid; j <= n_jobs; j += kFixThreads) s_prefix[j] = prefix[j];
+  __syncthreads();
+  for (long long u = (long long)blockIdx.x * kWarps + (tid >> 5); u < total;
+       u += (long long)gridDim.x * kWarps) {
+    int lo = 0, hi = n_jobs - 1;  // last job with prefix <= u (warp-uniform)
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_prefix[mid] <= u) lo = mid; else hi = mid - 1;
+    }
+    const int4 job = jobs[lo];  // {list, r_off, r_cnt, col_cnt}
+    const long long local = u - s_prefix[lo];
+    const unsigned ncc = (unsigned)(job.w + kFixCols - 1) / kFixCols;
+    const unsigned ri = local < 0x7fffffffll ? (unsigned)local / ncc : (unsigned)(local / ncc);
+    const int c0 = (int)((unsigned)(local - (long long)ri * ncc) * (unsigned)kFixCols);
+    const int m = sorted_ranges[job.y + ri];
+    const int32_t* list = job.x ? list_high : list_low;
+    int col[kFixCpl];
+    bool valid[kFixCpl];
+#pragma unroll
+    for (int c = 0; c < kFixCpl; ++c) {
+      const int ci = c0 + c * 32 + lane;
+      valid[c] = ci < job.w;
+      col[c] = valid[c] ? list[ci] : list[c0];  // padding lanes repeat a real column
+    }
+    const int o = roff[m];
+    const unsigned o2 = (unsigned)o | ((unsigned)o << 16);
+    const int64_t row0 = (int64_t)m * 8;  // the range's 8 isometry rows: one 8-row core block
+    const uint8_t* abase = a_tiles + (row0 >> 7) * ((int64_t)kTileM * kpad) +
+                           ((int)(row0 & 127) >> 3) * 128;
+    unsigned acc[kFixCpl][8];
+#pragma unroll
+    for (int c = 0; c < kFixCpl; ++c)
+#pragma unroll
+      for (int iso = 0; iso < 8; ++iso) acc[c][iso] = 0u;
+#pragma unroll 1
+    for (int kc = 0; kc < N / 16; ++kc) {
+      uint4 r4[8];
+      const uint8_t* ak = abase + kc * (kTileM * 16);
+#pragma unroll
+      for (int iso = 0; iso < 8; ++iso) r4[iso] = __ldg(reinterpret_cast<const uint4*>(ak + iso * 16));
+#pragma unroll
+      for (int c = 0; c < kFixCpl; ++c) {
+        const int16_t* qc = qbase + (int64_t)col[c] * N + kc * 16;
+        const uint4 qa = __ldg(reinterpret_cast<const uint4*>(qc));
+        const uint4 qb = __ldg(reinterpret_cast<const uint4*>(qc + 8));
+        const unsigned qw[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+        unsigned x4[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          // clip(q + o, 0, 255) on int16 pairs, then packed to 4 bytes
+          const unsigned lo2 = __vmins2(__vmaxs2(__vadd2(qw[2 * w], o2), 0u), 0x00ff00ffu);
+          const unsigned hi2 = __vmins2(__vmaxs2(__vadd2(qw[2 * w + 1], o2), 0u), 0x00ff00ffu);
+          x4[w] = __byte_perm(lo2, hi2, 0x6420);
+        }
+#pragma unroll
+        for (int iso = 0; iso < 8; ++iso) {
+          unsigned a = acc[c][iso], d;
+          d = __vabsdiffu4(x4[0], r4[iso].x); a = __dp4a(d, d, a);
+          d = __vabsdiffu4(x4[1], r4[iso].y); a = __dp4a(d, d, a);
+          d = __vabsdiffu4(x4[2], r4[iso].z); a = __dp4a(d, d, a);
+          d = __vabsdiffu4(x4[3], r4[iso].w); a = __dp4a(d, d, a);
+          acc[c][iso] = a;
+        }
+      }
+    }
+    unsigned long long best = ~0ull;
+#pragma unroll
+    for (int c = 0; c < kFixCpl; ++c) {
+      // err <= 256 * 255^2 < 2^24: (err << 3 | iso) orders by err, then iso
+      unsigned k = acc[c][0] << 3;
+#pragma unroll
+      for (int iso = 1; iso < 8; ++iso) k = min(k, (acc[c][iso] << 3) | (unsigned)iso);
+      // candidate index (e * 8 + iso) * S + si with e * S = col - si
+      const int si = S == 1 ? 0 : (S == 2 ? (col[c] & 1) : col[c] % S);
+      const unsigned cidx = (unsigned)(8 * (col[c] - si) + (int)(k & 7) * S + si);
+      const unsigned long long key = ((unsigned long long)(k >> 3) << 32) | cidx;
+      if (valid[c] && key < best) best = key;
+    }
+    const unsigned err = (unsigned)(best >> 32);  // 0xffffffff: no valid column
+    const unsigned werr = __reduce_min_sync(0xffffffffu, err);
+    const unsigned widx = __reduce_min_sync(0xffffffffu, err == werr ? (unsigned)best : 0xffffffffu);
+    if (lane == 0 && werr != 0xffffffffu)
+      atomicMin(&keys[m], ((unsigned long long)werr << 32) | widx);
+  }
+  if (t_end && tid == 0) atomicMax(t_end, global_ns());
 }
 
 // fc_encode's fused level start (one warp per range slot):
@@ -1097,7 +1215,7 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   level_plan_kernel<<<1, kPlanThreads, 0, c->stream>>>(
       d_M, RG, (int)T.ntiles, c->sm_count, d_hist,
       reinterpret_cast<const long long*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes),
-      ranges_per_block(L.n), c->roff.as<int32_t>(), d_plan, c->fix_jobs.as<int4>(),
+      fix_cols(L.n), c->roff.as<int32_t>(), d_plan, c->fix_jobs.as<int4>(),
       c->fix_cols.as<long long>(), d_fplan, c->fix_rows.as<int32_t>(),
       reinterpret_cast<long long*>(d_fix_pairs));
   c->stats.kernel_launches += 1;
@@ -1145,12 +1263,26 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
     FC_CUDA(c, cudaStreamWaitEvent(jobs_stream, ev_plan, 0));
     c->stream = jobs_stream;
   }
-  const int rc = scan_exact_jobs(c, L, c->fix_jobs.as<int4>(), c->fix_cols.as<int64_t>(),
-                                 &d_fplan->n_jobs, &d_fplan->total_blocks,
-                                 c->fix_rows.as<int32_t>(), T.reach_low.as<int32_t>(),
-                                 T.reach_high.as<int32_t>(), d_keys, d_time ? d_time + 2 : nullptr);
-  c->stream = main;
-  FC_TRY(rc);
+  {
+    auto* keys = reinterpret_cast<unsigned long long*>(d_keys);
+    const unsigned grid = (unsigned)(c->sm_count * (2048 / kFixThreads));
+#define FC_LAUNCH_FIX(NN)                                                                          \
+  fix_pairs_kernel<NN><<<grid, kFixThreads, 0, c->stream>>>(                                      \
+      L.qbase.as<int16_t>(), L.s_count, c->a_tiles.as<uint8_t>(), T.kpad,                         \
+      c->roff.as<int32_t>(), c->fix_jobs.as<int4>(), c->fix_cols.as<long long>(), d_fplan,       \
+      c->fix_rows.as<int32_t>(), T.reach_low.as<int32_t>(), T.reach_high.as<int32_t>(), keys,    \
+      d_time ? d_time + 2 : nullptr)
+    switch (L.n) {
+      case 256: FC_LAUNCH_FIX(256); break;
+      case 64: FC_LAUNCH_FIX(64); break;
+      default: FC_LAUNCH_FIX(16); break;
+    }
+#undef FC_LAUNCH_FIX
+    const cudaError_t err = cudaGetLastError();
+    c->stream = main;
+    if (err != cudaSuccess) return set_error(c, FC_ERR_CUDA, cudaGetErrorString(err));
+    c->stats.kernel_launches += 1;
+  }
   if (jobs_stream) FC_CUDA(c, cudaEventRecord(ev_jobs, jobs_stream));
   return FC_OK;
 }
