@@ -64,6 +64,7 @@ __global__ void classify_kernel(const unsigned long long* __restrict__ keys,
                                 int32_t* __restrict__ leaf_flag, int32_t* __restrict__ leaf_rec,
                                 int32_t* __restrict__ next_origins,
                                 int32_t* __restrict__ next_codes, int32_t* __restrict__ d_next_M) {
+  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool in = i < bound && i < *d_M;
   int sp = 0;
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(256) compact_records_kernel(int64_t n_codes,
                                                               int32_t* __restrict__ out,
                                                               int32_t* __restrict__ d_count) {
   __shared__ int32_t rs[256 * 6];
+  pdl_enter();
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x;
   const int64_t i = i0 + threadIdx.x;
   const int64_t last = min(i0 + (int64_t)blockDim.x, n_codes) - 1;
@@ -280,6 +282,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     put(path);
     put(c->sm_count);
     put(c->overlap);
+    put(c->pdl);
     for (int l = 0; l < 3; ++l) putd(thresholds[l]);
     for (int l = 0; l < kLevels; ++l) {
       const Level& L = c->lv[l];
@@ -398,13 +401,12 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     }
     int32_t* codes = c->enc_code[cur].as<int32_t>();
     const int nxt_buf = cur ^ 1;
-    classify_kernel<<<blocks_for(bound), 256, 0, c->stream>>>(
+    FC_CUDA(c, launch_k(c, classify_kernel, dim3(blocks_for(bound)), dim3(256), 0,
         reinterpret_cast<const unsigned long long*>(keys), d_M, bound, l + 1, can_split, thr2,
         L.s_count, L.baseline, L.svals_d.as<double>(), L.mean.as<double>(), c->rmean.as<double>(),
         c->roff.as<int32_t>(), c->enc_orig[cur].as<int32_t>(), codes, side / 2,
         can_split ? 1 << (2 * (2 - l)) : 0, c->leaf_flag.as<int32_t>(), c->leaf_rec.as<int32_t>(),
-        c->enc_orig[nxt_buf].as<int32_t>(), c->enc_code[nxt_buf].as<int32_t>(), d_count + l + 1);
-    FC_CUDA(c, cudaGetLastError());
+        c->enc_orig[nxt_buf].as<int32_t>(), c->enc_code[nxt_buf].as<int32_t>(), d_count + l + 1));
     c->total_launches += 1;
     if (can_split) {
       cur = nxt_buf;
@@ -429,9 +431,10 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     FC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, need, flag, pos, (int)n_codes, c->stream));
     FC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.ptr, need, flag, pos, (int)n_codes,
                                              c->stream));
-    compact_records_kernel<<<blocks_for(n_codes), 256, 0, c->stream>>>(
-        n_codes, flag, pos, c->leaf_rec.as<int32_t>(), c->rec_pinned.as<int32_t>(), d_count + 8);
-    FC_CUDA(c, cudaGetLastError());
+    FC_CUDA(c, launch_k(c, compact_records_kernel, dim3(blocks_for(n_codes)), dim3(256), 0,
+                        n_codes, (const int32_t*)flag, (const int32_t*)pos,
+                        (const int32_t*)c->leaf_rec.as<int32_t>(), c->rec_pinned.as<int32_t>(),
+                        d_count + 8));
     c->total_launches += 2;
     FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count, kEncReadBytes, cudaMemcpyDeviceToHost, c->stream));
   }

@@ -178,6 +178,7 @@ struct Ctx {
   cudaEvent_t ev_fork = nullptr, ev_prep[kLevels] = {}, ev_plan[kLevels] = {},
               ev_jobs[kLevels] = {};
   bool overlap = true;                 // FC_OVERLAP=0 / option "overlap": single stream
+  bool pdl = false;                    // FC_PDL=1: programmatic dependent launches (measured no gain)
   int tc_debug_mode = 0;               // FC_TC_DEBUG_MODE (pipeline probes)
   int pool_chunk = 0;                  // FC_POOL_CHUNK=512: smaller rank-sort chunks
   int tc_deferred = -1;                // FC_TC_DEFERRED: -1 = by K, 0/1 forced
@@ -206,6 +207,39 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 #endif
+#ifdef __CUDACC__
+// Programmatic dependent launch (PDL).  Kernels launched with launch_k() may
+// start while their stream predecessor is still running: they call
+// pdl_trigger() (let their own successor launch) and pdl_wait() (block until
+// the predecessor completed and its memory is visible) before touching any
+// data the predecessor produces.  Both are no-ops without a programmatic edge.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_enter() {
+  pdl_trigger();
+  pdl_wait();
+}
+
+// Kernel launch on the context stream, with the PDL attribute when enabled.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(const Ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block,
+                            size_t smem, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+#endif
+
 // enc_count buffer layout: int32 counters [16] | int64 clamp pairs [4] | u64 spans [4][4]
 // | int32 range-offset histograms [4][256]; the first kEncReadBytes are read back
 constexpr int kEncFixOff = 64;

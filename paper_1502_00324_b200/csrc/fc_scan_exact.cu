@@ -169,6 +169,7 @@ scan_exact_kernel(const int16_t* __restrict__ qbase, int64_t ncols, int S,
                   const int32_t* __restrict__ col_list, int64_t n_col_list, int baseline,
                   unsigned long long* __restrict__ keys, unsigned long long* __restrict__ tspan) {
   __shared__ __align__(16) ExactSmem<N> s;
+  pdl_enter();
   constexpr int RB = ExactSmem<N>::RB;
   const int tid = threadIdx.x;
   if (d_M) M = *d_M;
@@ -679,11 +680,11 @@ int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t
     dim3 grid(gx, (unsigned)((cnt + RB - 1) / RB));
     const int64_t nlist = d_range_list ? n_range_list : M;
 #define FC_LAUNCH_EXACT(NN)                                                                     \
-    scan_exact_kernel<NN><<<grid, kColsPerBlock, 0, c->stream>>>(                               \
+    FC_CUDA(c, launch_k(c, scan_exact_kernel<NN>, grid, dim3(kColsPerBlock), 0,                 \
         L.qbase.as<int16_t>(), ncols, L.s_count, d_s, L.mean.as<double>(),                      \
         c->rtiles.as<uint8_t>(), c->rmean.as<double>(), nlist, d_M, inv, d_range_list,          \
         n_range_list,                                                                           \
-        base, d_col_list, n_col_list, L.baseline, keys, d_time)
+        base, d_col_list, n_col_list, L.baseline, keys, d_time))
     switch (L.n) {
       case 256: FC_LAUNCH_EXACT(256); break;
       case 64: FC_LAUNCH_EXACT(64); break;

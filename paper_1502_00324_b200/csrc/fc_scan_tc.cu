@@ -117,7 +117,7 @@ struct TcParams {
 
 __host__ __device__ inline uint32_t a_bytes(const TcParams& p) { return p.rg * kTileM * p.kpad; }
 __host__ __device__ inline uint32_t b_bytes(const TcParams& p) { return kTileN * p.kpad; }
-__host__ __device__ inline uint32_t stage_bytes(const TcParams& p) { return b_bytes(p) + kTileN * 4; }
+__host__ __device__ inline uint32_t stage_bytes(const TcParams& p) { return b_bytes(p); }
 // per epilogue thread and resident row tile: {best key2, tile * 8 + 8-column group}
 __host__ __device__ inline uint32_t best_offset(const TcParams& p) {
   return a_bytes(p) + p.stages * stage_bytes(p);
@@ -205,8 +205,6 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
   const uint32_t tfull0 = ptx::pin(bar_base + 8u * (2 * STAGES + gq));
   const uint32_t tempty0 = ptx::pin(bar_base + 8u * (2 * STAGES + kNumAcc + gq));
   uint32_t H = 0;
-  int stg = 0;
-  uint32_t stg_phase = 0;
   int p0, p1, g, t0, t1;
   cta_share(x.n_pairs, p0, p1);
   for (int pp = p0; next_seg(pp, p1, p.ntiles, g, t0, t1);) {
@@ -216,8 +214,10 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
     for (int t = t1 - 1; t >= t0; --t) {
       const int2 tinfo = tinfo_next;  // {parity, valid slots}
       if (t > t0) tinfo_next = p.tile_info[t - 1];
-      if constexpr (!DEFERRED) ptx::mbar_wait_sleep(bar_base + 8u * stg, stg_phase);
-      const int32_t* colmap_s = reinterpret_cast<const int32_t*>(sStage + stg * kStage + kB);
+      // the B stage belongs to the MMA alone (released by its commit): the
+      // rare improving lanes of the immediate mode read the column map from
+      // global memory (L2), not from the stage
+      const int32_t* colmap_t = p.colmap + (size_t)t * kTileN;
       // this group's (tile, row tile) pairs: H & 1 == gq.  H advances by RG per
       // tile, so for even RG the row-tile parity is fixed; for odd RG (= 1)
       // the tiles alternate between the groups.
@@ -280,7 +280,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
               const bool in_a = min(min(gm[0], gm[1]), min(gm[2], gm[3])) == m;
               const int j = in_a ? first_eq(va, m) : 32 + first_eq(vb, m);
               m_best = m;
-              gi_best = colmap_s[sq + j];
+              gi_best = __ldg(colmap_t + sq + j);
             }
           }
         }
@@ -291,14 +291,6 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
         } else {
           if (m_best != kNone) ptx::sts_v2(bst + r * (kBS * 8), make_int2(2 * m_best + tinfo.x, gi_best));
         }
-      }
-      if constexpr (!DEFERRED) {
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(bar_base + 8u * (STAGES + stg));
-      }
-      if (++stg == STAGES) {
-        stg = 0;
-        stg_phase ^= 1;
       }
     }
     // resolve each row's winning 8-column group: recompute its dot products
@@ -400,13 +392,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  if (p.tspan && threadIdx.x == 0) atomicMin(&p.tspan[0], global_ns());
+  pdl_trigger();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(full_bar(s), 1);
       // the MMA commit; plus every epilogue warp when it reads the stage's column map
-      ptx::mbar_init(empty_bar(s), 1 + (p.deferred ? 0 : kEpiWarps));
+      ptx::mbar_init(empty_bar(s), 1);  // the MMA commit
     }
     for (int b = 0; b < kNumAcc; ++b) {
       ptx::mbar_init(tfull_bar(b), 1);
@@ -422,6 +414,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // setup above overlaps the predecessor's tail; its outputs are read below
+  pdl_wait();
+  if (p.tspan && threadIdx.x == 0) atomicMin(&p.tspan[0], global_ns());
 
   const TcPlan plan = *p.plan;
   int p0, p1, g, t0, t1;
@@ -441,8 +436,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
           uint8_t* st = sStage + s * kStage;
           ptx::mbar_expect_tx(full_bar(s), kStage);
           ptx::bulk_g2s(ptx::smem_u32(st), p.b_tiles + (size_t)t * kB, kB, full_bar(s));
-          ptx::bulk_g2s(ptx::smem_u32(st + kB), p.colmap + (size_t)t * kTileN, kTileN * 4,
-                        full_bar(s));
         }
       }
     }
@@ -695,6 +688,7 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
                   FixPlan* __restrict__ fplan, int32_t* __restrict__ order,
                   long long* __restrict__ fix_pairs_out) {
   __shared__ int cursor[256];
+  pdl_enter();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = *d_M;
   // ---- unit decomposition ----
@@ -923,6 +917,7 @@ struct GatherBuild {
 
 __global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
   __shared__ uint8_t tile_s[8][256];
+  pdl_enter();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1041,8 +1036,8 @@ int gather_build(Ctx* c, Level& L, const int32_t* d_origins, const int32_t* d_M,
     slots = std::max<int64_t>(slots, ((rtiles_max + prm.rg - 1) / prm.rg) * prm.rg * kTileM / 8);
   }
   P.slots = slots;
-  gather_build_kernel<<<(unsigned)((slots * 32 + 255) / 256), 256, 0, c->stream>>>(P);
-  FC_CUDA(c, cudaGetLastError());
+  FC_CUDA(c, launch_k(c, gather_build_kernel, dim3((unsigned)((slots * 32 + 255) / 256)), dim3(256),
+                      0, P));
   c->total_launches += 1;
   return FC_OK;
 }
@@ -1212,12 +1207,12 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   FC_CUDA(c, c->fix_rows.reserve(M_bound * 4 + 64));
   FC_CUDA(c, c->fix_jobs.reserve(512 * 16 + 64));
   FC_CUDA(c, c->fix_cols.reserve(513 * 8 + 64));
-  level_plan_kernel<<<1, kPlanThreads, 0, c->stream>>>(
+  FC_CUDA(c, launch_k(c, level_plan_kernel, dim3(1), dim3(kPlanThreads), 0,
       d_M, RG, (int)T.ntiles, c->sm_count, d_hist,
       reinterpret_cast<const long long*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes),
       fix_cols(L.n), c->roff.as<int32_t>(), d_plan, c->fix_jobs.as<int4>(),
       c->fix_cols.as<long long>(), d_fplan, c->fix_rows.as<int32_t>(),
-      reinterpret_cast<long long*>(d_fix_pairs));
+      reinterpret_cast<long long*>(d_fix_pairs)));
   c->stats.kernel_launches += 1;
   if (!a_built) {
     const uint16_t* inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
@@ -1249,8 +1244,7 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
                                     227 * 1024));
     c->tc_attr_set = true;
   }
-  tc_scan_kernel<<<c->sm_count, kThreads, smem, c->stream>>>(prm);
-  FC_CUDA(c, cudaGetLastError());
+  FC_CUDA(c, launch_k(c, tc_scan_kernel, dim3(c->sm_count), dim3(kThreads), smem, prm));
   if (ev_main_end) FC_CUDA(c, record_event(c, ev_main_end));
   c->stats.kernel_launches += 1;
 
