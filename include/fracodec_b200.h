@@ -92,6 +92,14 @@ int fc_pool_set_level(fc_ctx* ctx, int level, int64_t count, const uint8_t* tile
 int fc_pool_size(fc_ctx* ctx, int level, int64_t* out_count);
 /* Origins in rank order, interleaved (x, y) as uint16 -- the stream header. */
 int fc_pool_coords(fc_ctx* ctx, int level, uint16_t* xy);
+/* All four levels' origins in one call, level 1 first (sum of the pool
+ * sizes x 2 uint16); the per-level runs are in fc_pool_coords order. */
+int fc_pool_coords_all(fc_ctx* ctx, uint16_t* xy);
+/* Zero-copy variant: *out points at the same runs in the context's pinned
+ * host memory (after a stream synchronisation).  Valid until the next
+ * fc_pool_build or fc_ctx_destroy; NULL when the pool was not built by
+ * fc_pool_build (e.g. fc_pool_set_level). */
+int fc_pool_coords_view(fc_ctx* ctx, const uint16_t** out);
 /* Inspection of the survivors (any pointer may be NULL). */
 int fc_pool_entries(fc_ctx* ctx, int level, double* entropy, uint8_t* tiles, double* means,
                     double* cnorm);
@@ -139,6 +147,9 @@ int fc_encode_records(fc_ctx* ctx, int32_t* records, int64_t capacity);
 /* Per-level statistics of the last fc_encode (ranges, comparisons, path,
  * scan / main / fix device times, clamp pairs). */
 int fc_encode_level_stats(fc_ctx* ctx, int level, fc_stats* out);
+/* Summary of the last fc_encode's records: out[0..3] = leaf count per step
+ * 1..4 (codec.py step_blocks), out[4] = collage SSD (sum of the leaf errors). */
+int fc_encode_summary(fc_ctx* ctx, int64_t out[5]);
 
 int fc_last_stats(fc_ctx* ctx, fc_stats* out);
 /* The context's CUDA stream (cudaStream_t) so callers can time on it. */

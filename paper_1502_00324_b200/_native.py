@@ -9,6 +9,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import weakref
 
 import numpy as np
 
@@ -69,6 +70,8 @@ _SIGNATURES = {
     "fc_pool_set_level": ([_P, ctypes.c_int, _I64, _P], ctypes.c_int),
     "fc_pool_size": ([_P, ctypes.c_int, _P], ctypes.c_int),
     "fc_pool_coords": ([_P, ctypes.c_int, _P], ctypes.c_int),
+    "fc_pool_coords_all": ([_P, _P], ctypes.c_int),
+    "fc_pool_coords_view": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
     "fc_pool_entries": ([_P, ctypes.c_int, _P, _P, _P, _P], ctypes.c_int),
     "fc_level_prepare": ([_P, ctypes.c_int, ctypes.c_int, _P, _I32, _I32], ctypes.c_int),
     "fc_match_level": ([_P, ctypes.c_int, _P, _I64, _P, _P, _P], ctypes.c_int),
@@ -78,6 +81,7 @@ _SIGNATURES = {
     "fc_encode": ([_P, _P, _I32, _P, _P, _I32, _P, _I64, ctypes.POINTER(_I64)], ctypes.c_int),
     "fc_encode_records": ([_P, _P, _I64], ctypes.c_int),
     "fc_encode_level_stats": ([_P, ctypes.c_int, ctypes.POINTER(FcStats)], ctypes.c_int),
+    "fc_encode_summary": ([_P, _P], ctypes.c_int),
     "fc_last_stats": ([_P, ctypes.POINTER(FcStats)], ctypes.c_int),
     "fc_get_stream": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
     "fc_launch_count": ([_P, ctypes.POINTER(_I64)], ctypes.c_int),
@@ -139,6 +143,10 @@ class Context:
             raise DeviceError(f"fc_ctx_create failed with status {rc}")
         self.handle = h
         self.device = device
+        # CoordTables viewing the context's pinned coordinate buffer; they get
+        # their own copy before anything can overwrite or free that buffer
+        self._views = []  # weakref.ref (identity, not the tables' content hash)
+        self.pool_generation = 0  # bumped whenever the device pool is replaced
         for n in (16, 64, 256, 1024):
             lut = entropy_lut(n)
             self.check(self.lib.fc_set_entropy_lut(self.handle, n, _ptr(lut)))
@@ -148,7 +156,18 @@ class Context:
             msg = self.lib.fc_last_error(self.handle)
             self._raise(rc, msg.decode() if msg else "")
 
+    def _detach_views(self):
+        views = getattr(self, "_views", None)
+        if not views:
+            return
+        for ref in views:
+            t = ref()
+            if t is not None:
+                t._detach()
+        views.clear()
+
     def close(self):
+        self._detach_views()
         if getattr(self, "handle", None):
             self.lib.fc_ctx_destroy(self.handle)
             self.handle = None
@@ -180,11 +199,14 @@ class Context:
         t = np.asarray(taus, dtype=np.float64)
         u = np.asarray(use_tau, dtype=np.int32)
         out = np.zeros(4, dtype=np.int64)
+        self._detach_views()  # the build rewrites (and may reallocate) the pinned coordinates
+        self.pool_generation += 1
         self.check(self.lib.fc_pool_build(self.handle, _ptr(s), _ptr(c), _ptr(t), _ptr(u), _ptr(out)))
         return tuple(int(v) for v in out)
 
     def pool_set_level(self, level: int, tiles: np.ndarray):
         t = np.ascontiguousarray(tiles, dtype=np.uint8)
+        self.pool_generation += 1
         self.check(self.lib.fc_pool_set_level(self.handle, level, t.shape[0] if t.size else 0,
                                               _ptr(t) if t.size else None))
 
@@ -193,6 +215,33 @@ class Context:
         if count:
             self.check(self.lib.fc_pool_coords(self.handle, level, _ptr(out)))
         return out
+
+    def pool_coords_all(self, sizes) -> tuple:
+        """(x, y) uint16 origins of all four levels in one call -> per-level views."""
+        total = int(sum(sizes))
+        out = np.empty((total, 2), dtype=np.uint16)
+        if total:
+            self.check(self.lib.fc_pool_coords_all(self.handle, _ptr(out)))
+        bounds = np.cumsum((0,) + tuple(int(s) for s in sizes))
+        return tuple(out[bounds[k]:bounds[k + 1]] for k in range(len(sizes)))
+
+    def pool_coord_tables(self, sizes, table_cls) -> tuple | None:
+        """Per-level ``table_cls`` objects viewing the pinned coordinates of the
+        last fc_pool_build without a copy (None when there is no such view);
+        each is detached (copied) before the next pool build or close()."""
+        p = _P()
+        self.check(self.lib.fc_pool_coords_view(self.handle, ctypes.byref(p)))
+        if not p.value:
+            return None
+        total = int(sum(sizes))
+        if total == 0:
+            return tuple(table_cls(np.zeros((0, 2), dtype=np.uint16)) for _ in sizes)
+        buf = (ctypes.c_uint16 * (2 * total)).from_address(p.value)
+        arr = np.frombuffer(buf, dtype=np.uint16).reshape(total, 2)
+        bounds = np.cumsum((0,) + tuple(int(s) for s in sizes))
+        tables = tuple(table_cls(arr[bounds[k]:bounds[k + 1]]) for k in range(len(sizes)))
+        self._views.extend(weakref.ref(t) for t in tables)
+        return tables
 
     def pool_entries(self, level: int, count: int, side: int, want=("entropy", "tiles", "means", "cnorm")):
         ent = np.empty(count) if "entropy" in want else None
@@ -279,6 +328,12 @@ class Context:
         st = FcStats()
         self.check(self.lib.fc_encode_level_stats(self.handle, level, ctypes.byref(st)))
         return st
+
+    def encode_summary(self) -> tuple:
+        """(leaf counts per step 1..4, collage SSD) of the last encode."""
+        out = np.zeros(5, dtype=np.int64)
+        self.check(self.lib.fc_encode_summary(self.handle, _ptr(out)))
+        return tuple(int(v) for v in out[:4]), int(out[4])
 
     def stats(self) -> FcStats:
         st = FcStats()

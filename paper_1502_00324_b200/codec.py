@@ -180,14 +180,14 @@ def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=N
                                 launches=int(st.kernel_launches), scan_ms=float(st.scan_ms),
                                 main_ms=float(st.main_ms), fix_ms=float(st.fix_ms),
                                 fix_pairs=int(st.fix_pairs), rescans=int(st.rescans)))
-    records = RecordTable._trusted(rec[:, :5].astype(np.int64))
+    records = RecordTable._trusted(rec[:, :5])  # int32 view of the device records
     stream = CompressedStream(
         width=image.width, height=image.height, mode=policy.mode, strides=pool.params.strides,
-        s_sets=s_sets, pools=tuple(pool.coords(level) for level in (1, 2, 3, 4)), records=records)
+        s_sets=s_sets, pools=pool.all_coords(), records=records)
     encode_time = time.perf_counter() - t_start
     phase["records_stream"] = 1e3 * (time.perf_counter() - t_r)
-    step_blocks = tuple(int(v) for v in np.bincount(rec[:, 0], minlength=5)[1:5])
-    return stream, _report(image, config, pool, stream, step_blocks, int(rec[:, 5].sum(dtype=np.int64)),
+    step_blocks, collage_ssd = ctx.encode_summary()
+    return stream, _report(image, config, pool, stream, step_blocks, collage_ssd,
                            pool_time, encode_time, comparisons, scan_ms, level_stats, phase)
 
 

@@ -38,7 +38,8 @@ void trace_reset(Ctx* c) {
 }
 
 void trace_mark(Ctx* c, const char* name) {
-  if (!c->trace) return;
+  // FC_TRACE=2: marks outside graph capture only, graph reuse kept
+  if (!c->trace || (c->trace == 2 && c->capturing)) return;
   const size_t k = c->trace_name.size();
   if (k >= c->trace_ev.size()) {
     cudaEvent_t e;
@@ -364,6 +365,34 @@ int fc_pool_coords(fc_ctx* c, int level, uint16_t* xy) {
   return sync_stream(c);
 }
 
+int fc_pool_coords_all(fc_ctx* c, uint16_t* xy) {
+  cudaSetDevice(c->device);
+  if (!xy) return set_error(c, FC_ERR_ARG, "null output");
+  if (c->coords_valid) {  // one run per level, level 1 first, in pinned memory
+    int64_t total = 0;
+    for (int l = 0; l < kLevels; ++l) total += c->lv[l].count;
+    FC_TRY(sync_stream(c));
+    if (total) memcpy(xy, c->coords_pinned.ptr, total * 4);
+    return FC_OK;
+  }
+  int64_t off = 0;
+  for (int l = 0; l < kLevels; ++l) {
+    FC_TRY(fc_pool_coords(c, l + 1, xy + 2 * off));
+    off += c->lv[l].count;
+  }
+  return FC_OK;
+}
+
+int fc_pool_coords_view(fc_ctx* c, const uint16_t** out) {
+  cudaSetDevice(c->device);
+  if (!out) return set_error(c, FC_ERR_ARG, "null output");
+  *out = nullptr;
+  if (!c->coords_valid) return FC_OK;
+  FC_TRY(sync_stream(c));
+  *out = c->coords_pinned.as<uint16_t>();
+  return FC_OK;
+}
+
 int fc_pool_entries(fc_ctx* c, int level, double* entropy, uint8_t* tiles, double* means,
                     double* cnorm) {
   cudaSetDevice(c->device);
@@ -517,6 +546,12 @@ int fc_encode_level_stats(fc_ctx* c, int level, fc_stats* out) {
   FC_TRY(check_level(c, level));
   if (!out) return set_error(c, FC_ERR_ARG, "null stats");
   *out = c->enc_stats[level - 1];
+  return FC_OK;
+}
+
+int fc_encode_summary(fc_ctx* c, int64_t out[5]) {
+  if (!out) return set_error(c, FC_ERR_ARG, "null output");
+  for (int k = 0; k < 5; ++k) out[k] = c->enc_summary[k];
   return FC_OK;
 }
 

@@ -321,7 +321,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     put(c->tc_deferred);
     put(c->tc_g1);
   }
-  const bool reuse = use_graph && !c->trace && c->enc_exec && sig == c->enc_sig;
+  const bool reuse = use_graph && c->trace != 1 && c->enc_exec && sig == c->enc_sig;
   int levels_run = 0;
   const int64_t launches_body0 = c->total_launches;
   if (reuse) {
@@ -333,6 +333,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
       if (tc_launch[l]) c->lv[l].tc.ready = true;
     }
     FC_CUDA(c, cudaGraphLaunch(c->enc_exec, c->stream));
+    trace_mark(c, "graph_launched");
   }
   if (!reuse && use_graph) {
     FC_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -511,6 +512,17 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     st.scan_ms = st.main_ms + st.fix_ms;
   }
   (void)launches0;
+  {
+    // summary of the records (step counts, collage SSD) for the report
+    const int32_t* r = c->rec_pinned.as<int32_t>();
+    int64_t sm[5] = {0, 0, 0, 0, 0};
+    for (int64_t i = 0; i < n; ++i, r += 6) {
+      const int step = r[0];
+      if (step >= 1 && step <= 4) ++sm[step - 1];
+      sm[4] += r[5];
+    }
+    for (int k = 0; k < 5; ++k) c->enc_summary[k] = sm[k];
+  }
   trace_dump(c);
   if (!out_records) return FC_OK;
   if (n > capacity) return set_error(c, FC_ERR_ARG, "record buffer too small");

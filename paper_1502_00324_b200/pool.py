@@ -77,13 +77,19 @@ class CoordTable:
     materialising millions of Python tuples.
     """
 
-    __slots__ = ("array",)
+    __slots__ = ("array", "__weakref__")
 
     def __init__(self, array):
         a = np.asarray(array)
         if a.dtype != np.uint16:  # device tables arrive as u16 pairs (the stream format)
             a = a.astype(np.int64)
         a = a.reshape(-1, 2)
+        a.flags.writeable = False
+        self.array = a
+
+    def _detach(self):
+        """Own a private copy (the table was a view of context memory)."""
+        a = self.array.copy()
         a.flags.writeable = False
         self.array = a
 
@@ -124,23 +130,45 @@ class DomainPool:
         self.height = height
         self.sizes = tuple(int(s) for s in sizes)
         self.context = context
+        # device data is fetched lazily: it must still be this pool's
+        self._generation = context.pool_generation
         self._coords = {}
         self._entries = {}
         self._means = {}
+        self._tables = None
+
+    def _check_current(self):
+        if self.context.pool_generation != self._generation:
+            raise RuntimeError("this pool was superseded by a later pool build on its context")
 
     def size(self, level: int) -> int:
         return self.sizes[level - 1]
 
     def coords_array(self, level: int) -> np.ndarray:
         if level not in self._coords:
+            self._check_current()
             self._coords[level] = self.context.pool_coords(level, self.size(level))
         return self._coords[level]
 
     def coords(self, level: int) -> CoordTable:
         return CoordTable(self.coords_array(level))
 
+    def all_coords(self) -> tuple:
+        """CoordTable of every level without a host copy when the context can
+        lend its pinned buffer (copied on the next pool build), else one call."""
+        if self._tables is None and len(self._coords) < 4:
+            self._check_current()
+            self._tables = self.context.pool_coord_tables(self.sizes, CoordTable)
+        if self._tables is not None:
+            return self._tables
+        if len(self._coords) < 4:
+            for level, arr in zip((1, 2, 3, 4), self.context.pool_coords_all(self.sizes)):
+                self._coords.setdefault(level, arr)
+        return tuple(CoordTable(self._coords[level]) for level in (1, 2, 3, 4))
+
     def means(self, level: int) -> np.ndarray:
         if level not in self._means:
+            self._check_current()
             _, _, m, _ = self.context.pool_entries(level, self.size(level),
                                                    LEVEL_RANGE_SIDES[level - 1], want=("means",))
             self._means[level] = m
@@ -148,6 +176,7 @@ class DomainPool:
 
     def entries(self, level: int) -> tuple:
         if level not in self._entries:
+            self._check_current()
             side = LEVEL_RANGE_SIDES[level - 1]
             ent, tiles, means, cnorm = self.context.pool_entries(level, self.size(level), side)
             xy = self.coords_array(level)
