@@ -161,6 +161,18 @@ int fc_launch_count(fc_ctx* ctx, int64_t* out_count);
  * (M=128, N=256, operands in smem, no epilogue) over all SMs, in TOP/s. */
 int fc_probe_int8_peak(fc_ctx* ctx, double* out_tops);
 
+/* Host-only (no context, no device): the FRAK record payload (stream.py:175-207
+ * serialisation).  Each record (step, offset, iso, addr, s_index) becomes one
+ * MSB-first field of 13 + abits[step-1] + sbits[step-1] bits: step-1 (2),
+ * offset (8), iso (3), addr, s_index; fields are concatenated and the last
+ * byte zero-padded.  rec: int32 rows of `stride` ints (the first five used).
+ * Validates every field (addr < plen[step-1], s_index < slen[step-1]); on a
+ * bad record returns FC_ERR_ARG and *bad_index = its row.  out must hold
+ * (sum of widths + 7) / 8 bytes (+ 8 bytes of slack). */
+int fc_pack_records(const int32_t* rec, int64_t stride, int64_t n, const int32_t abits[4],
+                    const int32_t sbits[4], const int64_t plen[4], const int64_t slen[4],
+                    uint8_t* out, int64_t out_bytes, int64_t* out_bits, int64_t* bad_index);
+
 #ifdef __cplusplus
 }
 #endif

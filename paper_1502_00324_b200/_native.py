@@ -71,6 +71,9 @@ _SIGNATURES = {
     "fc_pool_size": ([_P, ctypes.c_int, _P], ctypes.c_int),
     "fc_pool_coords": ([_P, ctypes.c_int, _P], ctypes.c_int),
     "fc_pool_coords_all": ([_P, _P], ctypes.c_int),
+    "fc_pack_records": ([_P, ctypes.c_int64, ctypes.c_int64, _P, _P, _P, _P, _P, ctypes.c_int64,
+                         ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)],
+                        ctypes.c_int),
     "fc_pool_coords_view": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
     "fc_pool_entries": ([_P, ctypes.c_int, _P, _P, _P, _P], ctypes.c_int),
     "fc_level_prepare": ([_P, ctypes.c_int, ctypes.c_int, _P, _I32, _I32], ctypes.c_int),
@@ -363,6 +366,26 @@ class Context:
 
 _default = {}
 _default_lock = threading.Lock()
+
+
+def pack_records(r: np.ndarray, abits, sbits, plen, slen):
+    """FRAK payload of int32 records (host C, stream.py serialisation) ->
+    (bytes, nbits); raises IndexError(row) for an out-of-range record."""
+    lib = load_library()
+    n = r.shape[0]
+    stride = r.strides[0] // 4
+    ab = np.ascontiguousarray(abits, dtype=np.int32)
+    sb = np.ascontiguousarray(sbits, dtype=np.int32)
+    pl = np.ascontiguousarray(plen, dtype=np.int64)
+    sl = np.ascontiguousarray(slen, dtype=np.int64)
+    cap = (n * (13 + int(ab.max()) + int(sb.max())) + 7) // 8 + 16
+    out = np.empty(cap, dtype=np.uint8)
+    nbits, bad = ctypes.c_int64(), ctypes.c_int64()
+    rc = lib.fc_pack_records(ctypes.c_void_p(r.ctypes.data), stride, n, _ptr(ab), _ptr(sb), _ptr(pl),
+                             _ptr(sl), _ptr(out), cap, ctypes.byref(nbits), ctypes.byref(bad))
+    if rc != FC_OK:
+        raise IndexError(int(bad.value))
+    return out[:(nbits.value + 7) // 8].tobytes(), int(nbits.value)
 
 
 def default_context(device: int = 0) -> Context:

@@ -175,6 +175,49 @@ extern "C" {
 
 int fc_version(void) { return 1; }
 
+int fc_pack_records(const int32_t* rec, int64_t stride, int64_t n, const int32_t abits[4],
+                    const int32_t sbits[4], const int64_t plen[4], const int64_t slen[4],
+                    uint8_t* out, int64_t out_bytes, int64_t* out_bits, int64_t* bad_index) {
+  if (bad_index) *bad_index = -1;
+  if (!out_bits || (n > 0 && (!rec || !out))) return FC_ERR_ARG;
+  int64_t total = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t* r = rec + i * stride;
+    const int step = r[0];
+    if (step < 1 || step > 4 || r[1] < 0 || r[1] > 255 || r[2] < 0 || r[2] > 7 || r[3] < 0 ||
+        r[3] >= plen[step - 1] || r[4] < 0 || r[4] >= slen[step - 1]) {
+      if (bad_index) *bad_index = i;
+      return FC_ERR_ARG;
+    }
+    total += 13 + abits[step - 1] + sbits[step - 1];
+  }
+  *out_bits = total;
+  if ((total + 7) / 8 + 8 > out_bytes) return FC_ERR_ARG;
+  // MSB-first bit writer: `acc` holds `nacc` pending bits (right-aligned)
+  unsigned __int128 acc = 0;
+  int nacc = 0;
+  uint8_t* o = out;
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t* r = rec + i * stride;
+    const int l = r[0] - 1;
+    const int ab = abits[l], sb = sbits[l];
+    uint64_t v = (uint64_t)l;
+    v = (v << 8) | (uint64_t)r[1];
+    v = (v << 3) | (uint64_t)r[2];
+    v = (ab ? (v << ab) : v) | (uint64_t)r[3];
+    v = (sb ? (v << sb) : v) | (uint64_t)r[4];
+    acc = (acc << (13 + ab + sb)) | v;
+    nacc += 13 + ab + sb;
+    while (nacc >= 8) {
+      nacc -= 8;
+      *o++ = (uint8_t)(acc >> nacc);
+    }
+    acc &= ((unsigned __int128)1 << nacc) - 1;
+  }
+  if (nacc > 0) *o++ = (uint8_t)(acc << (8 - nacc));
+  return FC_OK;
+}
+
 int fc_ctx_create(int device, fc_ctx** out) {
   if (!out) return FC_ERR_ARG;
   *out = nullptr;

@@ -140,3 +140,34 @@ def test_workload_generators_are_deterministic():
     assert a.shape == (128, 128) and a.dtype == np.uint8
     assert np.array_equal(a, W.make_image("c1"))
     assert set(W.WORKLOADS) == {"c1", "c2", "c3", "c4", "c5"}
+
+
+def test_native_record_packer_matches_numpy_packer():
+    """fc_pack_records (host C, used by serialize for the device encoder's int32
+    records) produces the bytes of the numpy word packer, and rejects records
+    outside their level's pool / s set."""
+    rng = np.random.default_rng(7)
+    abits = np.array([0, 5, 17, 23], dtype=np.int64)
+    sbits = np.array([0, 1, 1, 3], dtype=np.int64)
+    plen = np.array([1, 20, 100000, 5000000], dtype=np.int64)
+    slen = np.array([1, 2, 2, 7], dtype=np.int64)
+    for n in (1, 2, 7, 1000, 4099):
+        steps = rng.integers(1, 5, n)
+        rec = np.stack([steps, rng.integers(0, 256, n), rng.integers(0, 8, n),
+                        rng.integers(0, plen[steps - 1]), rng.integers(0, slen[steps - 1]),
+                        rng.integers(0, 1 << 20, n)], axis=1).astype(np.int32)
+        r = rec[:, :5]  # strided int32 view, as codec.encode hands it over
+        got, nbits = _native.pack_records(r, abits, sbits, plen, slen)
+        lv = steps - 1
+        u = r.astype(np.uint64)
+        val = (lv.astype(np.uint64) << np.uint64(8)) | u[:, 1]
+        val = (val << np.uint64(3)) | u[:, 2]
+        val = (val << abits[lv].astype(np.uint64)) | u[:, 3]
+        val = (val << sbits[lv].astype(np.uint64)) | u[:, 4]
+        widths = 13 + abits[lv] + sbits[lv]
+        assert nbits == int(widths.sum())
+        assert got == st._pack_words(val, widths)
+    bad = rec.copy()
+    bad[3, 3] = plen[bad[3, 0] - 1]
+    with pytest.raises(IndexError):
+        _native.pack_records(bad[:, :5], abits, sbits, plen, slen)
