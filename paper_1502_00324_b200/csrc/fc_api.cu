@@ -272,7 +272,6 @@ void fc_ctx_destroy(fc_ctx* c) {
   c->pool_rb.release();
   c->prep_dev.release();
   c->chunk_odd.release();
-  c->prep_rb.release();
   c->coords_pinned.release();
   c->rec_pinned.release();
   if (c->enc_ev_ready)
@@ -285,7 +284,6 @@ void fc_ctx_destroy(fc_ctx* c) {
                     &L.tc.reach_low, &L.tc.reach_high, &L.tc.odd, &L.svals_d, 
                     &L.win_ent, &L.win_key, &L.win_key2, &L.win_val, &L.win_val2};
     for (DevBuf* b : lb) b->release();
-    L.tc.upload.release();
   }
   cudaEventDestroy(c->ev0);
   cudaEventDestroy(c->ev1);
@@ -466,7 +464,6 @@ int fc_level_prepare(fc_ctx* c, int level, int baseline, const double* svals, in
     const int st[1] = {pending};
     FC_TRY(prep_launch(c, lv, st, 1));
   }
-  if (pending) FC_TRY(sync_stream(c));
   return prepare_finish(c, L, path, pending);
 }
 

@@ -231,8 +231,8 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
                         d_hist + 256 * l, c->keys.as<uint64_t>(), d_time + 4 * l);
   };
   trace_mark(c, "prep_launched");
-  FC_TRY(sync_stream(c));
-  trace_mark(c, "prep_sync");
+  // no synchronisation: the K layout is fixed by the s values and the tables
+  // that depend on the operand statistics are built on the device
   bool tc_launch[kLevels] = {false, false, false, false};
   for (int l = 0; l < kLevels; ++l) {
     if (!pending[l]) continue;
@@ -299,17 +299,15 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
       put(T.m_digits);
       put(T.ntiles);
       put(T.ncols);
-      put(T.n_even);
       const DevBuf* lb[] = {&L.xy, &L.tiles, &L.mean, &L.qbase, &L.svals_d, &T.b_tiles, &T.meta,
                             &T.tile_q1, &T.col_stats, &T.reach_low, &T.reach_high, &T.odd};
       for (const DevBuf* b : lb) putp(b->ptr);
-      putp(T.upload.ptr);
     }
     const DevBuf* cb[] = {&c->keys, &c->rtiles, &c->rmean, &c->roff, &c->rsq, &c->a_tiles,
                           &c->row_meta, &c->tc_plan, &c->fix_rows, &c->fix_jobs, &c->fix_cols,
                           &c->enc_orig[0], &c->enc_orig[1], &c->enc_code[0], &c->enc_code[1],
                           &c->enc_count, &c->leaf_flag, &c->leaf_pos,
-                          &c->leaf_rec, &c->cub_tmp, &c->iso_inv};
+                          &c->leaf_rec, &c->cub_tmp, &c->iso_inv, &c->prep_dev};
     for (const DevBuf* b : cb) {
       putp(b->ptr);
       put(b->bytes);

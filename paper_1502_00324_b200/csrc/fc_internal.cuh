@@ -19,8 +19,9 @@ constexpr int kMaxS = 16;
 // so small correction sets still spread over the SMs)
 __host__ __device__ constexpr int ranges_per_block(int n) { return n >= 256 ? 2 : n >= 64 ? 4 : 8; }
 constexpr int kTcHistWords = 1024 + 1024 + 4;  // qmin | qmax histograms, q2max, pad
-constexpr int kUpCursorBytes = 2048 * 4;        // tensor-operand upload image layout
+constexpr int kUpCursorBytes = 2048 * 4;        // tensor-operand table image layout
 constexpr int kUpReachBytes = 512 * 8;
+constexpr int kUpDimsBytes = 64;                // TcDims (device-computed group sizes)
 
 struct Status {
   int code = FC_OK;
@@ -80,19 +81,17 @@ struct TcOperands {
   int m_digits = 1;      // base-255 digit slots carrying hq = floor(Q2/2) in the K extra block
   int kpad = 0;          // K bytes per row: planes*B*B + m_digits + 4, padded to 32
   int64_t ncols = 0;     // real columns E*S
-  int64_t ntiles = 0;    // 256-column tiles (the last one padded)
+  int64_t ntiles = 0;    // bound on the 256-column tiles: ceil(ncols / 256) + 1 (the
+                         // two parity groups are each padded; the exact count and
+                         // group sizes are computed on the device, TcDims)
   DevBuf b_tiles;        // int8 [ntiles][kpad/16][32 groups][8][16]   (UMMA K-major, no swizzle)
   DevBuf hq;             // (unused; kept for ABI-stable struct layout in tools)
   DevBuf meta;           // uint32 [ntiles*256]: (Q2 & 1) << 31 | column, 0xffffffff = padding
-  DevBuf tile_q1;        // device upload image: cursors [2048 i32] | reach counts [512 i64] | tile info
+  DevBuf tile_q1;        // device tables: cursors [2048 i32] | reach counts [512 i64] | TcDims | tile info
   DevBuf col_stats;      // int4 [ncols]: {Q1, Q2, qmin, qmax} (unsorted order)
   DevBuf reach_low;      // int32 [ncols]: columns sorted by qmin ascending
   DevBuf reach_high;     // int32 [ncols]: columns sorted by qmax descending
   DevBuf odd;            // int32 [2*ncols]: parity flags, then their exclusive prefix
-  PinnedBuf upload;      // pinned image of cursors | reach counts | tile info
-  int64_t n_even = 0, n_odd = 0;  // columns per parity group
-  int64_t low_count[256] = {0};   // #{columns with qmin < -o}      (clamp at 0 possible)
-  int64_t high_count[256] = {0};  // #{columns with qmax > 255 - o} (clamp at 255 possible)
 };
 
 struct Level {
@@ -158,7 +157,6 @@ struct Ctx {
   PinnedBuf readback;     // small D2H results (counts, histograms)
   PinnedBuf pool_rb;      // threshold-survivor counts per level
   DevBuf prep_dev, chunk_odd;  // per-level qmin/qmax histograms + q2max + odd total; chunk counts
-  PinnedBuf prep_rb;           // pinned copy of prep_dev
   PinnedBuf coords_pinned;  // pool origins of all levels, fetched with fc_encode's last sync
   int64_t coords_off[kLevels] = {0, 0, 0, 0};
   bool coords_valid = false;

@@ -528,9 +528,9 @@ int ensure_iso_tables(Ctx* c) {
 }
 
 // Device half of the operand preparation for several levels at once:
-// s values, q operands (+ tensor-path statistics for `stats` levels), parity
-// slots, and ONE readback of every stats level's histograms and odd total
-// into c->prep_rb (read by level_prepare_tc_host after the next sync).
+// s values, q operands (+ tensor-path statistics for `stats` levels: the
+// qmin / qmax histograms, max Q2 and odd total in c->prep_dev, which
+// tc_tables_kernel turns into the level's tables on the device), parity slots.
 int prep_launch(Ctx* c, Level* const* levels, const int* stats, int count) {
   QParams QP{};
   SlotParams SP{};
@@ -539,7 +539,6 @@ int prep_launch(Ctx* c, Level* const* levels, const int* stats, int count) {
   for (int i = 0; i < count; ++i)
     if (stats[i]) chunk_total += (levels[i]->count * levels[i]->s_count + 1023) / 1024;
   FC_CUDA(c, c->prep_dev.reserve(kLevels * kTcHistWords * 4));
-  FC_CUDA(c, c->prep_rb.reserve(kLevels * kTcHistWords * 4));
   FC_CUDA(c, c->chunk_odd.reserve(chunk_total * 4 + 64));
   for (int i = 0; i < count; ++i) {
     Level& L = *levels[i];
@@ -599,9 +598,6 @@ int prep_launch(Ctx* c, Level* const* levels, const int* stats, int count) {
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 1;
   }
-  if (any_stats)
-    FC_CUDA(c, cudaMemcpyAsync(c->prep_rb.ptr, c->prep_dev.ptr, kLevels * kTcHistWords * 4,
-                               cudaMemcpyDeviceToHost, c->stream));
   return FC_OK;
 }
 

@@ -77,7 +77,8 @@ struct TcPlan {
   int n_rgroups;   // groups of RG row tiles
   int n_pairs;     // n_rgroups * ntiles
   int rows_pad;    // n_rgroups * RG * 128
-  int pad[4];
+  int ntiles;      // B tiles of the level (TcDims)
+  int pad[3];
 };
 
 __device__ __forceinline__ void cta_share(int P, int& p0, int& p1) {
@@ -108,7 +109,6 @@ struct TcParams {
   int kpad;
   int rg;          // row tiles per unit (A resident in smem)
   int stages;      // B ring depth
-  int ntiles;
   const TcPlan* plan;
   int deferred;    // 1: resolve the winning column once per unit (short K)
   int g1;          // 1: every epilogue warp drains every accumulator (64 columns)
@@ -171,7 +171,7 @@ struct EpiCtx {
   uint8_t* smem;
   uint8_t* sStage;
   uint32_t kStage, kB, bar_base, tmem_base;
-  int STAGES, RG, KPAD, n_pairs, warp, lane;
+  int STAGES, RG, KPAD, n_pairs, ntiles, warp, lane;
 };
 
 template <bool DEFERRED, bool G1>
@@ -207,7 +207,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
   uint32_t H = 0;
   int p0, p1, g, t0, t1;
   cta_share(x.n_pairs, p0, p1);
-  for (int pp = p0; next_seg(pp, p1, p.ntiles, g, t0, t1);) {
+  for (int pp = p0; next_seg(pp, p1, x.ntiles, g, t0, t1);) {
     for (int r = 0; r < RG; ++r) ptx::sts_v2(bst + r * (kBS * 8), make_int2(kNone, 0));
     // tiles in DECREASING order (see improve_limit); tile_info one tile ahead
     int2 tinfo_next = p.tile_info[t1 - 1];
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     // ---------------- producer (TMA engine bulk copies) ----------------
     if (lane == 0) {
       uint32_t L = 0, U = 0;
-      for (int pp = p0; next_seg(pp, p1, p.ntiles, g, t0, t1); ++U) {
+      for (int pp = p0; next_seg(pp, p1, plan.ntiles, g, t0, t1); ++U) {
         ptx::mbar_wait_sleep(aempty_bar, (U & 1) ^ 1);
         ptx::mbar_expect_tx(afull_bar, kA);
         ptx::bulk_g2s(ptx::smem_u32(sA), p.a_tiles + (size_t)g * kA, kA, afull_bar);
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     constexpr uint64_t kBStep = (2 * kTileN * 16) >> 4;
     const uint32_t a_base = ptx::smem_u32(sA);
     uint32_t L = 0, H = 0, U = 0;
-    for (int pp = p0; next_seg(pp, p1, p.ntiles, g, t0, t1); ++U) {
+    for (int pp = p0; next_seg(pp, p1, plan.ntiles, g, t0, t1); ++U) {
       ptx::mbar_wait_sleep(afull_bar, U & 1);
       ptx::tc_fence_after();
       for (int t = t1 - 1; t >= t0; --t, ++L) {
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   } else if (warp >= 4) {
     // ---------------- epilogue: 16 warps drain every accumulator ----------------
     const EpiCtx x{smem, sStage, kStage, kB, bar_base, tmem_base, STAGES, RG, KPAD,
-                   plan.n_pairs, warp, lane};
+                   plan.n_pairs, plan.ntiles, warp, lane};
     if (p.g1) {
       if (p.deferred) epilogue_role<true, true>(p, x);
       else epilogue_role<false, true>(p, x);
@@ -496,6 +496,65 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
 // operand preparation
 // ---------------------------------------------------------------------------
 
+// Parity-group sizes of a level's columns (computed on the device).
+struct TcDims {
+  long long n_even, n_odd;  // columns with even / odd Q1
+  long long ntiles;         // ceil(n_even / 256) + ceil(n_odd / 256)
+  long long odd_base;       // first slot of the odd group
+  long long n_pad;          // padding slots (last tile of each group)
+  long long pad[3];
+};
+static_assert(sizeof(TcDims) == kUpDimsBytes, "table image layout");
+
+// One block of 1024 threads: the level's table image from the operand
+// statistics histogram (qprep / parity_slot): counting-sort cursors for the
+// clamp-reach lists (qmin ascending | qmax descending), the reach counts
+// low[o] = #{qmin < -o}, high[o] = #{qmax > 255 - o}, the group sizes and the
+// per-tile {parity, valid slots} table for every tile below the bound.
+__global__ void __launch_bounds__(1024)
+tc_tables_kernel(const unsigned* __restrict__ hist, int64_t ncols, int64_t ntiles_max,
+                 uint8_t* __restrict__ tab) {
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int lo_ex[1025], hi_ex[1025];
+  const int v = threadIdx.x;
+  int32_t* cur = reinterpret_cast<int32_t*>(tab);
+  auto* rc = reinterpret_cast<long long*>(tab + kUpCursorBytes);
+  auto* dims = reinterpret_cast<TcDims*>(tab + kUpCursorBytes + kUpReachBytes);
+  int2* tinfo = reinterpret_cast<int2*>(tab + kUpCursorBytes + kUpReachBytes + kUpDimsBytes);
+  int lo, hi;
+  Scan(tmp).ExclusiveSum((int)hist[v], lo);             // sum of hmin[u], u < v
+  __syncthreads();
+  Scan(tmp).ExclusiveSum((int)hist[1024 + 1023 - v], hi);  // sum of hmax[u], u > 1023 - v
+  cur[v] = lo;
+  cur[1024 + (1023 - v)] = hi;
+  lo_ex[v] = lo;
+  hi_ex[1023 - v] = hi;
+  __syncthreads();
+  if (v < 256) {
+    rc[v] = lo_ex[512 - v];        // q < -o       <=> bin < 512 - o
+    rc[256 + v] = hi_ex[767 - v];  // q > 255 - o  <=> bin > 767 - o
+  }
+  const long long n_odd = hist[2049];
+  const long long n_even = ncols - n_odd;
+  const long long te = (n_even + kTileN - 1) / kTileN, to = (n_odd + kTileN - 1) / kTileN;
+  if (v == 0) {
+    TcDims d{};
+    d.n_even = n_even;
+    d.n_odd = n_odd;
+    d.ntiles = te + to;
+    d.odd_base = te * kTileN;
+    d.n_pad = (te + to) * kTileN - ncols;
+    *dims = d;
+  }
+  for (long long t = v; t < ntiles_max; t += 1024) {
+    int2 ti = make_int2(0, 0);
+    if (t < te) ti = make_int2(0, (int)(n_even - t * kTileN < kTileN ? n_even - t * kTileN : kTileN));
+    else if (t < te + to) ti = make_int2(1, (int)(n_odd - (t - te) * kTileN < kTileN ? n_odd - (t - te) * kTileN : kTileN));
+    tinfo[t] = ti;
+  }
+}
+
 // Per column: Q1, Q2, qmin, qmax; sort keys for the clamp-reach lists; odd-Q1
 // flags for the parity grouping; histograms of qmin / qmax; max of Q2.
 // B operand in grouped slot order, K-major canonical UMMA layout per tile:
@@ -504,11 +563,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
 // slot = even/odd group base + rank of the column inside its parity group.
 __global__ void build_b_kernel(const int16_t* __restrict__ qbase, int n, int kpad, int planes,
                                int m_digits, int64_t ncols, const int4* __restrict__ stats,
-                               const int32_t* __restrict__ odd_prefix, int64_t odd_base,
-                               int64_t n_even, int64_t n_odd, int64_t n_pad,
-                               int8_t* __restrict__ b_tiles, int32_t* __restrict__ colmap) {
+                               const int32_t* __restrict__ odd_prefix,
+                               const TcDims* __restrict__ dims, int8_t* __restrict__ b_tiles,
+                               int32_t* __restrict__ colmap) {
   const int chunks = kpad / 16;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_even = dims->n_even, n_odd = dims->n_odd;
+  const int64_t odd_base = dims->odd_base, n_pad = dims->n_pad;
   if (i >= ncols * chunks) {
     // padding slots of the last tile of each parity group: zero operand, no column
     const int64_t pi = i - ncols * chunks;
@@ -681,7 +742,7 @@ struct FixPlan {
 //  * the ranges bucketed by offset (counting sort, bucket order free).
 constexpr int kPlanThreads = 1024;
 __global__ void __launch_bounds__(kPlanThreads)
-level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
+level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restrict__ dims, int grid,
                   const int32_t* __restrict__ hist, const long long* __restrict__ reach_counts,
                   int fcols, const int32_t* __restrict__ roff, TcPlan* __restrict__ plan,
                   int4* __restrict__ jobs, long long* __restrict__ prefix,
@@ -767,7 +828,8 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, int ntiles, int grid,
     TcPlan pl{};
     pl.M = M;
     pl.n_rgroups = M > 0 ? n_rg : 0;
-    pl.n_pairs = M > 0 ? n_rg * ntiles : 0;
+    pl.ntiles = (int)dims->ntiles;
+    pl.n_pairs = M > 0 ? n_rg * pl.ntiles : 0;
     pl.rows_pad = n_rg * RG * kTileM;
     *plan = pl;
   }
@@ -1042,101 +1104,59 @@ int gather_build(Ctx* c, Level& L, const int32_t* d_origins, const int32_t* d_M,
   return FC_OK;
 }
 
-// Phase 2a (host, after the stream reached the readback): K layout, tile
-// table and clamp-reach counts, written into the level's pinned upload
-// buffer; every device buffer of the operand set is reserved.  No launches.
+// Phase 2a (host, no readback): the K layout from the proposed-mode bound on
+// the candidates (|q| = |rint(s (d - mean))| <= rint(s 255 (n-1)/n), since
+// one pixel can differ from the mean of n by at most 255 (n-1)/n), and every
+// device buffer of the operand set reserved for the tile-count bound.  The
+// exact parity-group sizes, tile table and clamp-reach cursors are computed
+// on the device (tc_tables_kernel), so no host synchronisation is needed.
 int level_prepare_tc_host(Ctx* c, Level& L) {
   TcOperands& T = L.tc;
   const int64_t ncols = T.ncols;
   if (ncols == 0) return set_error(c, FC_ERR_EMPTY_POOL, "no domain entries");
-  const int li = (int)(&L - c->lv);
-  const unsigned* h = c->prep_rb.as<unsigned>() + li * kTcHistWords;
-  const unsigned* hmin = h;
-  const unsigned* hmax = h + 1024;
-  const unsigned q2max = h[2048];
-  int gmin = 1 << 20, gmax = -(1 << 20);
-  for (int v = 0; v < 1024; ++v) {
-    if (hmin[v]) gmin = std::min(gmin, v - 512);
-    if (hmax[v]) gmax = std::max(gmax, v - 512);
-  }
-  if (gmin < -254 || gmax > 254) return set_error(c, FC_ERR_ARG, "operand outside two s8 planes");
-  T.planes = (gmin >= -127 && gmax <= 127) ? 1 : 2;
-  const int hq_max = (int)(q2max >> 1);
-  T.m_digits = std::max(1, (hq_max / 255 + 126) / 127);
+  double smax = 0.0;
+  for (int k = 0; k < L.s_count; ++k) smax = std::max(smax, std::fabs(L.svals[k]));
+  const int qabs = (int)std::rint(smax * 255.0 * (double)(L.n - 1) / (double)L.n);
+  if (qabs > 254) return set_error(c, FC_ERR_ARG, "operand outside two s8 planes");
+  T.planes = qabs <= 127 ? 1 : 2;
+  const long long hq_max = (long long)L.n * qabs * qabs / 2;  // >= floor(sum q^2 / 2)
+  T.m_digits = std::max(1, (int)((hq_max / 255 + 126) / 127));
   T.kpad = ((T.planes * L.n + T.m_digits + 4 + 31) / 32) * 32;
   if (c->trace)
     fprintf(stderr, "[fc_trace] tc operands B=%d cols=%lld planes=%d m_digits=%d kpad=%d\n", L.side,
             (long long)ncols, T.planes, T.m_digits, T.kpad);
-  // two parity groups, each padded to whole tiles
-  const int64_t n_odd = (int64_t)h[2049];
-  T.n_even = ncols - n_odd;
-  T.n_odd = n_odd;
-  const int64_t tiles_even = (T.n_even + kTileN - 1) / kTileN;
-  const int64_t tiles_odd = (n_odd + kTileN - 1) / kTileN;
-  T.ntiles = tiles_even + tiles_odd;
-  // pinned upload image: cursors [2048 i32] | reach counts [512 i64] | tile info [ntiles int2]
-  FC_CUDA(c, T.upload.reserve(kUpCursorBytes + kUpReachBytes + T.ntiles * 8 + 16));
-  int32_t* cur = T.upload.as<int32_t>();
-  long long* rc = reinterpret_cast<long long*>(T.upload.as<uint8_t>() + kUpCursorBytes);
-  int2* tinfo = reinterpret_cast<int2*>(T.upload.as<uint8_t>() + kUpCursorBytes + kUpReachBytes);
-  // clamp-reach counts: low_count[o] = #{qmin < -o}, high_count[o] = #{qmax > 255 - o};
-  // counting-sort cursors: qmin ascending | qmax descending
-  int64_t cmin[1025], cmax[1025];
-  cmin[0] = cmax[0] = 0;
-  int32_t acc_lo = 0;
-  for (int v = 0; v < 1024; ++v) {
-    cmin[v + 1] = cmin[v] + hmin[v];
-    cmax[v + 1] = cmax[v] + hmax[v];
-    cur[v] = acc_lo;
-    acc_lo += (int32_t)hmin[v];
-  }
-  int32_t acc_hi = 0;
-  for (int v = 1023; v >= 0; --v) {
-    cur[1024 + v] = acc_hi;
-    acc_hi += (int32_t)hmax[v];
-  }
-  for (int o = 0; o < 256; ++o) {
-    T.low_count[o] = cmin[512 - o];                    // q < -o      <=> v < 512 - o
-    T.high_count[o] = cmax[1024] - cmax[768 - o];      // q > 255 - o <=> v > 767 - o
-    rc[o] = T.low_count[o];
-    rc[256 + o] = T.high_count[o];
-  }
-  for (int64_t t = 0; t < tiles_even; ++t)
-    tinfo[t] = make_int2(0, (int)std::min<int64_t>(kTileN, T.n_even - t * kTileN));
-  for (int64_t t = 0; t < tiles_odd; ++t)
-    tinfo[tiles_even + t] = make_int2(1, (int)std::min<int64_t>(kTileN, n_odd - t * kTileN));
+  T.ntiles = (ncols + kTileN - 1) / kTileN + 1;
   const int64_t slots = T.ntiles * kTileN;
   FC_CUDA(c, T.reach_low.reserve(ncols * 4));
   FC_CUDA(c, T.reach_high.reserve(ncols * 4));
   FC_CUDA(c, T.b_tiles.reserve(slots * T.kpad));
   FC_CUDA(c, T.meta.reserve(slots * 4));
-  // device copy of the upload image (same layout): cursors | reach counts | tile info
-  FC_CUDA(c, T.tile_q1.reserve(kUpCursorBytes + kUpReachBytes + T.ntiles * 8 + 16));
+  FC_CUDA(c, T.tile_q1.reserve(kUpCursorBytes + kUpReachBytes + kUpDimsBytes + T.ntiles * 8 + 16));
   return FC_OK;
 }
 
-// Phase 2b (stream-ordered, capturable): upload the pinned image, build the
-// clamp-reach lists and the grouped B operand (+ column map).
+// Phase 2b (stream-ordered, capturable): the level's tables from the operand
+// statistics (tc_tables_kernel), the clamp-reach lists and the grouped B
+// operand (+ column map).  Launch sizes use the tile-count bound.
 int level_prepare_tc_launch(Ctx* c, Level& L) {
   TcOperands& T = L.tc;
   const int64_t ncols = T.ncols;
-  const uint8_t* up = T.upload.as<uint8_t>();
-  FC_CUDA(c, cudaMemcpyAsync(T.tile_q1.ptr, up, kUpCursorBytes + kUpReachBytes + T.ntiles * 8,
-                             cudaMemcpyHostToDevice, c->stream));
-  int32_t* d_cur = T.tile_q1.as<int32_t>();
+  const int li = (int)(&L - c->lv);
+  uint8_t* tab = T.tile_q1.as<uint8_t>();
+  int32_t* d_cur = reinterpret_cast<int32_t*>(tab);
+  auto* dims = reinterpret_cast<TcDims*>(tab + kUpCursorBytes + kUpReachBytes);
+  tc_tables_kernel<<<1, 1024, 0, c->stream>>>(c->prep_dev.as<unsigned>() + li * kTcHistWords, ncols,
+                                              T.ntiles, tab);
   reach_scatter_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, c->stream>>>(
       T.col_stats.as<int4>(), ncols, d_cur, d_cur + 1024, T.reach_low.as<int32_t>(),
       T.reach_high.as<int32_t>());
-  const int64_t slots = T.ntiles * kTileN;
-  const int64_t odd_base = ((T.n_even + kTileN - 1) / kTileN) * kTileN;
-  const int64_t n_pad = slots - ncols;
-  const int64_t work = (ncols + n_pad) * (T.kpad / 16);
+  const int64_t pad_max = T.ntiles * kTileN - ncols;
+  const int64_t work = (ncols + pad_max) * (T.kpad / 16);
   build_b_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
       L.qbase.as<int16_t>(), L.n, T.kpad, T.planes, T.m_digits, ncols, T.col_stats.as<int4>(),
-      T.odd.as<int32_t>() + ncols, odd_base, T.n_even, T.n_odd, n_pad, T.b_tiles.as<int8_t>(),
-      T.meta.as<int32_t>());
+      T.odd.as<int32_t>() + ncols, dims, T.b_tiles.as<int8_t>(), T.meta.as<int32_t>());
   FC_CUDA(c, cudaGetLastError());
-  c->total_launches += 2;
+  c->total_launches += 3;
   T.ready = true;
   return FC_OK;
 }
@@ -1208,7 +1228,9 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   FC_CUDA(c, c->fix_jobs.reserve(512 * 16 + 64));
   FC_CUDA(c, c->fix_cols.reserve(513 * 8 + 64));
   FC_CUDA(c, launch_k(c, level_plan_kernel, dim3(1), dim3(kPlanThreads), 0,
-      d_M, RG, (int)T.ntiles, c->sm_count, d_hist,
+      d_M, RG,
+      reinterpret_cast<const TcDims*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes + kUpReachBytes),
+      c->sm_count, d_hist,
       reinterpret_cast<const long long*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes),
       fix_cols(L.n), c->roff.as<int32_t>(), d_plan, c->fix_jobs.as<int4>(),
       c->fix_cols.as<long long>(), d_fplan, c->fix_rows.as<int32_t>(),
@@ -1229,10 +1251,9 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   prm.b_tiles = T.b_tiles.as<int8_t>();
   prm.colmap = T.meta.as<int32_t>();
   prm.tile_info = reinterpret_cast<const int2*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes +
-                                                kUpReachBytes);
+                                                kUpReachBytes + kUpDimsBytes);
   prm.keys = reinterpret_cast<unsigned long long*>(d_keys);
   prm.S = L.s_count;
-  prm.ntiles = (int)T.ntiles;
   prm.plan = d_plan;
   prm.tspan = d_time;
   // measured: the per-unit recompute wins only for short K
