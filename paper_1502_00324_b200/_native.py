@@ -192,15 +192,15 @@ class Context:
     def set_image_device(self, dev_ptr: int, width: int, height: int):
         self.check(self.lib.fc_set_device_io(self.handle, 1))
         try:
-            self.check(self.lib.fc_set_image(self.handle, ctypes.c_void_p(dev_ptr), width, height))
+            self.check(self.lib.fc_set_image(self.handle, dev_ptr, width, height))
         finally:
             self.check(self.lib.fc_set_device_io(self.handle, 0))
 
     def pool_build(self, strides, caps, taus, use_tau):
-        s = np.asarray(strides, dtype=np.int32)
-        c = np.asarray(caps, dtype=np.int64)
-        t = np.asarray(taus, dtype=np.float64)
-        u = np.asarray(use_tau, dtype=np.int32)
+        s = np.ascontiguousarray(strides, dtype=np.int32)
+        c = np.ascontiguousarray(caps, dtype=np.int64)
+        t = np.ascontiguousarray(taus, dtype=np.float64)
+        u = np.ascontiguousarray(use_tau, dtype=np.int32)
         out = np.zeros(4, dtype=np.int64)
         self._detach_views()  # the build rewrites (and may reallocate) the pinned coordinates
         self.pool_generation += 1

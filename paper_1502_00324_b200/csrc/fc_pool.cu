@@ -374,26 +374,47 @@ __device__ __forceinline__ uint32_t load_word_guarded(const uint8_t* img, int64_
   return w;
 }
 
+// Words of one window row as staged in shared memory (NW + 1: the row may
+// start mid-word).
+template <int D>
+__host__ __device__ constexpr int stage_words() { return D / 4 + 1; }
+
 template <int D>
 __device__ __forceinline__ void survivor_rows(const SurvLevel& L, const uint8_t* __restrict__ img,
                                               int width, int64_t img_bytes, int64_t warp_in_level,
-                                              int lane, uint32_t* __restrict__ xy_s) {
-  constexpr int B = D / 2, n = B * B, PER = 32 / D, NW = D / 4;
+                                              int lane, uint32_t* __restrict__ xy_s,
+                                              uint32_t* __restrict__ stage) {
+  constexpr int B = D / 2, n = B * B, PER = 32 / D, NW = D / 4, NWR = stage_words<D>();
   const int grp = lane / D, row = lane % D;
   const int64_t sv = warp_in_level * PER + grp;
   const bool valid = sv < L.count;
   uint32_t w = 0;
   uint32_t pq[NW > 0 ? NW : 1];
+  // lane = (survivor, window row): the word-aligned start of its row
+  int64_t a0 = 0;
+  int sh = 0;
   if (valid) {
     w = __ldg(L.order + sv);
     const int wy = w / L.nx, wx = w - wy * L.nx;
     const int64_t a = (int64_t)(wy * L.stride + row) * width + wx * L.stride;
-    const int64_t a0 = a & ~3ll;
-    const int sh = (int)(a - a0) * 8;
+    a0 = a & ~3ll;
+    sh = (int)(a - a0) * 8;
+  }
+  // stage the warp's 32 rows x NWR words with consecutive lanes on consecutive
+  // words of a row (a few cache lines per load instead of one per lane)
+#pragma unroll
+  for (int k = 0; k < NWR; ++k) {
+    const int idx = k * 32 + lane;
+    const int r = idx / NWR, wd = idx - r * NWR;  // staged row r belongs to lane r
+    const int64_t ra = __shfl_sync(0xffffffffu, a0, r);
+    const int rv = __shfl_sync(0xffffffffu, valid ? 1 : 0, r);
+    stage[idx] = rv ? load_word_guarded(img, ra + 4 * wd, img_bytes) : 0u;
+  }
+  __syncwarp();
+  if (valid) {
     uint32_t raw[NW + 1];
 #pragma unroll
-    for (int k = 0; k <= NW; ++k)
-      raw[k] = (k < NW || sh) ? load_word_guarded(img, a0 + 4 * k, img_bytes) : 0u;
+    for (int k = 0; k <= NW; ++k) raw[k] = stage[lane * NWR + k];
 #pragma unroll
     for (int k = 0; k < NW; ++k) {
       const uint32_t rw = __funnelshift_r(raw[k], raw[k + 1], sh);
@@ -451,6 +472,7 @@ __global__ void __launch_bounds__(256) survivors_all_kernel(const uint8_t* __res
                                                             int width, int64_t img_bytes,
                                                             SurvParams P) {
   __shared__ uint32_t xy_s[8 * 8];  // 8 warps x up to 8 survivors per warp
+  __shared__ uint32_t stage_s[8][32 * stage_words<32>()];  // per warp: 32 rows of a window
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   // levels start on block boundaries (warp_begin is a multiple of 8)
@@ -464,10 +486,10 @@ __global__ void __launch_bounds__(256) survivors_all_kernel(const uint8_t* __res
   const int64_t level_warps = (L.count + per - 1) / per;
   if (wl < level_warps) {
     switch (L.B) {
-      case 16: survivor_rows<32>(L, img, width, img_bytes, wl, lane, xy_s); break;
-      case 8: survivor_rows<16>(L, img, width, img_bytes, wl, lane, xy_s); break;
-      case 4: survivor_rows<8>(L, img, width, img_bytes, wl, lane, xy_s); break;
-      default: survivor_rows<4>(L, img, width, img_bytes, wl, lane, xy_s); break;
+      case 16: survivor_rows<32>(L, img, width, img_bytes, wl, lane, xy_s, stage_s[threadIdx.x >> 5]); break;
+      case 8: survivor_rows<16>(L, img, width, img_bytes, wl, lane, xy_s, stage_s[threadIdx.x >> 5]); break;
+      case 4: survivor_rows<8>(L, img, width, img_bytes, wl, lane, xy_s, stage_s[threadIdx.x >> 5]); break;
+      default: survivor_rows<4>(L, img, width, img_bytes, wl, lane, xy_s, stage_s[threadIdx.x >> 5]); break;
     }
   }
   __syncthreads();

@@ -58,6 +58,20 @@ class PoolParams:
             return None
         return self.entropy_thresholds[level - 1]
 
+    def native_args(self) -> tuple:
+        """(strides, caps, taus, use_tau) as the C ABI's arrays, built once."""
+        args = self.__dict__.get("_native")
+        if args is None:
+            taus = [self.tau(level) for level in (1, 2, 3, 4)]
+            args = (np.asarray(self.strides, dtype=np.int32),
+                    np.asarray([self.cap(level) for level in (1, 2, 3, 4)], dtype=np.int64),
+                    np.asarray([0.0 if t is None else t for t in taus], dtype=np.float64),
+                    np.asarray([0 if t is None else 1 for t in taus], dtype=np.int32))
+            for a in args:
+                a.flags.writeable = False
+            object.__setattr__(self, "_native", args)
+        return args
+
 
 @dataclass(frozen=True, eq=False)
 class DomainEntry:
@@ -216,13 +230,7 @@ def build_pool(image: GrayImage, params: PoolParams, context=None, device_image=
         ctx.set_image_device(int(device_image.data_ptr()), image.width, image.height)
     else:
         ctx.set_image(image.pixels)
-    caps, taus, use_tau = [], [], []
-    for level in (1, 2, 3, 4):
-        tau = params.tau(level)
-        caps.append(params.cap(level))
-        taus.append(0.0 if tau is None else tau)
-        use_tau.append(0 if tau is None else 1)
-    sizes = ctx.pool_build(params.strides, caps, taus, use_tau)
+    sizes = ctx.pool_build(*params.native_args())
     return DomainPool(params, image.width, image.height, sizes, ctx)
 
 
