@@ -979,8 +979,13 @@ struct GatherBuild {
 
 __global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
   __shared__ uint8_t tile_s[8][256];
+  __shared__ uint16_t inv_s[8 * 256];  // the level's inverse isometry maps (8 x n)
   pdl_enter();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (P.kpad != 0) {
+    for (int i = threadIdx.x; i < 8 * P.n; i += blockDim.x) inv_s[i] = P.inv[i];
+    __syncthreads();
+  }
   const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     P.tspan[0] = ~0ull;
@@ -1041,7 +1046,7 @@ __global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
           uint32_t v = 0;
           if (k < kbase) {
             const int kk = k < n ? k : k - n;
-            v = ts[P.inv[iso * n + kk]];
+            v = ts[inv_s[iso * n + kk]];
           } else {
             const int sl = k - kbase;
             if (sl < P.m_digits) v = 255;
