@@ -66,19 +66,25 @@ constexpr int kSmemBudget = 227 * 1024;  // the opt-in maximum per block
 constexpr int kNone = 0x7fffffff;
 
 // Unit decomposition of one launch, computed on the device from the range
-// count (level_plan_kernel) so the host never waits for it.
-// The work is the (row group, column tile) pairs in the linear order
-// p = g * ntiles + j, j-th tile of group g counted from the LAST tile; CTA b
-// takes the contiguous share [P*b/grid, P*(b+1)/grid), i.e. at most a few
-// segments (one per row group it touches), so every CTA gets the same number
-// of tile MMAs to within one pair.
+// count (level_plan_kernel) so the host never waits for it.  The work is the
+// (row group g, column tile t) pairs, split into segments (g, tiles t1-1 down
+// to t0), each costing one A load and one column resolution:
+//  * mode 0 (B operand fits L2): pairs in the linear order p = g * ntiles + j
+//    (j-th tile of group g counted from the LAST tile); CTA b takes the
+//    contiguous share [P*b/grid, P*(b+1)/grid), i.e. a few segments, so every
+//    CTA gets the same number of tile MMAs to within one pair;
+//  * mode 1 (B larger than L2): units (g, span of ct tiles), u = span * n_rg + g,
+//    dealt round-robin, so the CTAs work on the same span at the same time
+//    and B streams from HBM about once per span (ct minimises the makespan).
 struct TcPlan {
   int M;           // ranges
   int n_rgroups;   // groups of RG row tiles
   int n_pairs;     // n_rgroups * ntiles
   int rows_pad;    // n_rgroups * RG * 128
   int ntiles;      // B tiles of the level (TcDims)
-  int pad[3];
+  int mode;        // 0: contiguous pair shares, 1: round-robin span units
+  int ct;          // mode 1: tiles per span
+  int n_units;     // mode 1: spans * n_rgroups
 };
 
 __device__ __forceinline__ void cta_share(int P, int& p0, int& p1) {
@@ -97,6 +103,29 @@ __device__ __forceinline__ bool next_seg(int& p, int p1, int ntiles, int& g, int
   p = pe;
   return true;
 }
+
+// The CTA's segments in either mode (every role walks the same sequence).
+struct SegIter {
+  int mode, ntiles, n_rg, ct, n_units, p, p1;
+  __device__ __forceinline__ explicit SegIter(const TcPlan& pl)
+      : mode(pl.mode), ntiles(pl.ntiles), n_rg(pl.n_rgroups), ct(pl.ct), n_units(pl.n_units) {
+    if (mode == 0) {
+      cta_share(pl.n_pairs, p, p1);
+    } else {
+      p = blockIdx.x;
+      p1 = n_units;
+    }
+  }
+  __device__ __forceinline__ bool next(int& g, int& t0, int& t1) {
+    if (mode == 0) return next_seg(p, p1, ntiles, g, t0, t1);
+    if (p >= n_units) return false;
+    g = p % n_rg;
+    t0 = (p / n_rg) * ct;
+    t1 = min(ntiles, t0 + ct);
+    p += gridDim.x;
+    return true;
+  }
+};
 
 struct TcParams {
   const uint8_t* a_tiles;    // [rt_pad][128 * kpad]
@@ -171,7 +200,8 @@ struct EpiCtx {
   uint8_t* smem;
   uint8_t* sStage;
   uint32_t kStage, kB, bar_base, tmem_base;
-  int STAGES, RG, KPAD, n_pairs, ntiles, warp, lane;
+  int STAGES, RG, KPAD, warp, lane;
+  TcPlan plan;
 };
 
 template <bool DEFERRED, bool G1>
@@ -205,9 +235,8 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
   const uint32_t tfull0 = ptx::pin(bar_base + 8u * (2 * STAGES + gq));
   const uint32_t tempty0 = ptx::pin(bar_base + 8u * (2 * STAGES + kNumAcc + gq));
   uint32_t H = 0;
-  int p0, p1, g, t0, t1;
-  cta_share(x.n_pairs, p0, p1);
-  for (int pp = p0; next_seg(pp, p1, x.ntiles, g, t0, t1);) {
+  int g, t0, t1;
+  for (SegIter it(x.plan); it.next(g, t0, t1);) {
     for (int r = 0; r < RG; ++r) ptx::sts_v2(bst + r * (kBS * 8), make_int2(kNone, 0));
     // tiles in DECREASING order (see improve_limit); tile_info one tile ahead
     int2 tinfo_next = p.tile_info[t1 - 1];
@@ -419,14 +448,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   if (p.tspan && threadIdx.x == 0) atomicMin(&p.tspan[0], global_ns());
 
   const TcPlan plan = *p.plan;
-  int p0, p1, g, t0, t1;
-  cta_share(plan.n_pairs, p0, p1);
+  int g, t0, t1;
 
   if (warp == 0) {
     // ---------------- producer (TMA engine bulk copies) ----------------
     if (lane == 0) {
       uint32_t L = 0, U = 0;
-      for (int pp = p0; next_seg(pp, p1, plan.ntiles, g, t0, t1); ++U) {
+      for (SegIter it(plan); it.next(g, t0, t1); ++U) {
         ptx::mbar_wait_sleep(aempty_bar, (U & 1) ^ 1);
         ptx::mbar_expect_tx(afull_bar, kA);
         ptx::bulk_g2s(ptx::smem_u32(sA), p.a_tiles + (size_t)g * kA, kA, afull_bar);
@@ -449,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     constexpr uint64_t kBStep = (2 * kTileN * 16) >> 4;
     const uint32_t a_base = ptx::smem_u32(sA);
     uint32_t L = 0, H = 0, U = 0;
-    for (int pp = p0; next_seg(pp, p1, plan.ntiles, g, t0, t1); ++U) {
+    for (SegIter it(plan); it.next(g, t0, t1); ++U) {
       ptx::mbar_wait_sleep(afull_bar, U & 1);
       ptx::tc_fence_after();
       for (int t = t1 - 1; t >= t0; --t, ++L) {
@@ -476,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   } else if (warp >= 4) {
     // ---------------- epilogue: 16 warps drain every accumulator ----------------
     const EpiCtx x{smem, sStage, kStage, kB, bar_base, tmem_base, STAGES, RG, KPAD,
-                   plan.n_pairs, plan.ntiles, warp, lane};
+                   warp, lane, plan};
     if (p.g1) {
       if (p.deferred) epilogue_role<true, true>(p, x);
       else epilogue_role<false, true>(p, x);
@@ -742,19 +770,43 @@ struct FixPlan {
 //  * the ranges bucketed by offset (counting sort, bucket order free).
 constexpr int kPlanThreads = 1024;
 __global__ void __launch_bounds__(kPlanThreads)
-level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restrict__ dims, int grid,
+level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restrict__ dims,
+                  long long b_tile_bytes, int grid,
                   const int32_t* __restrict__ hist, const long long* __restrict__ reach_counts,
                   int fcols, const int32_t* __restrict__ roff, TcPlan* __restrict__ plan,
                   int4* __restrict__ jobs, long long* __restrict__ prefix,
                   FixPlan* __restrict__ fplan, int32_t* __restrict__ order,
                   long long* __restrict__ fix_pairs_out) {
   __shared__ int cursor[256];
+  __shared__ unsigned long long best[kPlanThreads / 32];
   pdl_enter();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = *d_M;
   // ---- unit decomposition ----
   const int n_rtiles = (M * 8 + kTileM - 1) / kTileM;
   const int n_rg = (n_rtiles + RG - 1) / RG;
+  const int ntiles = (int)dims->ntiles;
+  // mode 1 when B does not fit comfortably in L2: span length minimising the
+  // per-CTA makespan ceil(units / grid) * (ct + 2) (smallest span count wins)
+  const bool rr = (long long)ntiles * b_tile_bytes > (48ll << 20) && n_rg > 0;
+  if (rr) {
+    unsigned long long mine = ~0ull;
+    const int smax = min(ntiles, 8192);
+    for (int sc = tid + 1; sc <= smax; sc += kPlanThreads) {
+      const unsigned ctv = ((unsigned)ntiles + sc - 1) / (unsigned)sc;
+      const unsigned nsp = ((unsigned)ntiles + ctv - 1) / ctv;
+      const unsigned long long units = (unsigned long long)nsp * (unsigned)n_rg;
+      const unsigned long long cost = ((units + grid - 1) / (unsigned)grid) * (ctv + 2);
+      const unsigned long long key = (cost << 24) | (unsigned long long)sc;
+      mine = key < mine ? key : mine;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long w = __shfl_xor_sync(0xffffffffu, mine, o);
+      mine = w < mine ? w : mine;
+    }
+    if (lane == 0) best[warp] = mine;
+  }
   // ---- correction jobs: thread o < 256 owns offset bucket o ----
   int cnt = 0, njob = 0;
   long long lists[2] = {0, 0}, blocks = 0, pairs = 0;
@@ -828,8 +880,16 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restr
     TcPlan pl{};
     pl.M = M;
     pl.n_rgroups = M > 0 ? n_rg : 0;
-    pl.ntiles = (int)dims->ntiles;
-    pl.n_pairs = M > 0 ? n_rg * pl.ntiles : 0;
+    pl.ntiles = ntiles;
+    pl.n_pairs = M > 0 ? n_rg * ntiles : 0;
+    pl.mode = rr ? 1 : 0;
+    if (rr) {
+      unsigned long long bk = best[0];
+      for (int w = 1; w < kPlanThreads / 32; ++w) bk = best[w] < bk ? best[w] : bk;
+      const int sc = (int)(bk & 0xffffff);
+      pl.ct = (ntiles + sc - 1) / sc;
+      pl.n_units = M > 0 ? ((ntiles + pl.ct - 1) / pl.ct) * n_rg : 0;
+    }
     pl.rows_pad = n_rg * RG * kTileM;
     *plan = pl;
   }
@@ -1235,7 +1295,7 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   FC_CUDA(c, launch_k(c, level_plan_kernel, dim3(1), dim3(kPlanThreads), 0,
       d_M, RG,
       reinterpret_cast<const TcDims*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes + kUpReachBytes),
-      c->sm_count, d_hist,
+      (long long)kTileN * T.kpad, c->sm_count, d_hist,
       reinterpret_cast<const long long*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes),
       fix_cols(L.n), c->roff.as<int32_t>(), d_plan, c->fix_jobs.as<int4>(),
       c->fix_cols.as<long long>(), d_fplan, c->fix_rows.as<int32_t>(),
