@@ -64,6 +64,16 @@ __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
   asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
   return y;
 }
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32_ordered(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ void reds_add(uint32_t a, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -94,37 +104,28 @@ __device__ __forceinline__ void hist_rows(uint32_t hw, const uint8_t* __restrict
 // Zero bins add +0.0 (exact): lut[0] holds 0.0 and lut[k] = t(k).  Every term
 // is <= 0, so adding a zero term never changes an accumulator's bits, and an
 // 8-bin group (one term per accumulator, in bin order) that is empty in all
-// 32 windows of the warp can be skipped: neighbouring windows share most
-// pixels, so typically 2/3 of the groups are.  The 16 group tests of a half
-// are independent loads (batched), one REDUX.OR gives the warp's non-empty
-// groups, and a warp-uniform loop visits them in increasing order.
-// hp: this lane's word 0 (word k at hp[32 k]); plain loads, ordered after
-// the asm reductions that updated the histogram (memory clobbers).
+// 32 windows of the warp is skipped with a warp-uniform branch: neighbouring
+// windows share most pixels, so typically 2/3 of the groups are skipped.
 // Must be called by the full warp (inactive lanes hold an all-zero histogram).
-__device__ __forceinline__ double window_entropy(const uint32_t* hp, const double* lutp) {
+__device__ __forceinline__ double window_entropy(uint32_t hw, uint32_t lut) {
   double half_sum[2];
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
-    const uint32_t* hh = hp + half * 64 * 32;
-    unsigned lm = 0;
-#pragma unroll
-    for (int g = 0; g < 16; ++g) {
-      const uint32_t* pg = hh + g * 4 * 32;
-      lm |= (unsigned)((pg[0] | pg[32] | pg[64] | pg[96]) != 0u) << g;
-    }
-    unsigned gm = __reduce_or_sync(0xffffffffu, lm);
     double acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.0;
-    while (gm) {
-      const int g = __ffs(gm) - 1;
-      gm &= gm - 1;
-      const uint32_t* pg = hh + g * 4 * 32;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t w = pg[q * 32];
-        acc[2 * q] = acc[2 * q] + lutp[w & 0xffffu];
-        acc[2 * q + 1] = acc[2 * q + 1] + lutp[w >> 16];
+    for (int g = 0; g < 16; ++g) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = lds_u32_ordered(hw + (half * 64 + g * 4 + q) * 128);
+      if (__any_sync(0xffffffffu, (w[0] | w[1] | w[2] | w[3]) != 0u)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          // counts <= 1024 < 2^13, so (w >> 13) == 8 * (w >> 16)
+          acc[2 * q] = acc[2 * q] + lds_f64(lut + ((w[q] & 0xffffu) << 3));
+          acc[2 * q + 1] = acc[2 * q + 1] + lds_f64(lut + (w[q] >> 13));
+        }
       }
     }
     half_sum[half] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
@@ -138,8 +139,7 @@ __device__ __forceinline__ double window_entropy(const uint32_t* hp, const doubl
 // enter), so a window costs 2*stride*D updates instead of D*D.
 template <int D>
 __device__ __forceinline__ void entropy_task(const EntLevel& L, const uint8_t* __restrict__ img,
-                                             int width, int task, uint32_t h,
-                                             const uint32_t* hp, const double* lutp,
+                                             int width, int task, uint32_t h, uint32_t lut,
                                              int lane) {
   const int t = task - L.task_begin;
   const int sy = t / L.strips_x, sx = t - sy * L.strips_x;
@@ -158,7 +158,7 @@ __device__ __forceinline__ void entropy_task(const EntLevel& L, const uint8_t* _
       hist_rows<D>(h, img, width, x, yp, yp + min(s, D), 0xffffffffu, 0xffff0000u);
       hist_rows<D>(h, img, width, x, max(yp + D, yn), yn + D, 1u, 0x10000u);
     }
-    const double H = window_entropy(hp, lutp);  // whole warp (see window_entropy)
+    const double H = window_entropy(h, lut);  // whole warp (see window_entropy)
     const int64_t w = (int64_t)wy * L.nx + wx;
     if (L.mode == 0) {
       if (active) {
@@ -196,8 +196,8 @@ entropy_all_kernel(const uint8_t* __restrict__ img, int width, EntParams P) {
       lut_s[P.lv[l].lut_off + i] = i ? P.lut[l][i - 1] : 0.0;
   }
   __syncthreads();
-  const uint32_t* hp = hist_all + warp * (128 * 32) + lane;
-  const uint32_t h = opaque_u32(smem_addr(hp));
+  const uint32_t h = opaque_u32(smem_addr(hist_all + warp * (128 * 32) + lane));
+  const uint32_t lut_base = opaque_u32(smem_addr(lut_s));
   for (int task = blockIdx.x * kEntWarps + warp; task < P.total_tasks;
        task += gridDim.x * kEntWarps) {
     int l = 0;
@@ -205,12 +205,12 @@ entropy_all_kernel(const uint8_t* __restrict__ img, int width, EntParams P) {
     for (int k = 1; k < 4; ++k)
       if (task >= P.lv[k].task_begin) l = k;
     const EntLevel& L = P.lv[l];
-    const double* lutp = lut_s + L.lut_off;
+    const uint32_t lut = lut_base + L.lut_off * 8;
     switch (L.D) {
-      case 32: entropy_task<32>(L, img, width, task, h, hp, lutp, lane); break;
-      case 16: entropy_task<16>(L, img, width, task, h, hp, lutp, lane); break;
-      case 8: entropy_task<8>(L, img, width, task, h, hp, lutp, lane); break;
-      default: entropy_task<4>(L, img, width, task, h, hp, lutp, lane); break;
+      case 32: entropy_task<32>(L, img, width, task, h, lut, lane); break;
+      case 16: entropy_task<16>(L, img, width, task, h, lut, lane); break;
+      case 8: entropy_task<8>(L, img, width, task, h, lut, lane); break;
+      default: entropy_task<4>(L, img, width, task, h, lut, lane); break;
     }
   }
 }
