@@ -69,8 +69,13 @@ int fc_synchronize(fc_ctx* ctx);
 /* Device-resident mode for benchmarking: when set, fc_set_image's pixels and
  * fc_match_level's origins/outputs are DEVICE pointers (no host copies). */
 int fc_set_device_io(fc_ctx* ctx, int device_io);
-/* Execution options: "graph" (1 = run fc_encode's level loop as one CUDA
- * graph, the default; 0 = eager launches).  Results never depend on them. */
+/* Options.  Execution (results never depend on them): "graph" (1 = run
+ * fc_encode's level loop as one CUDA graph, the default; 0 = eager
+ * launches), "overlap" (second stream for operand builds / clamp
+ * corrections, default 1).  Range sharding: "top_begin" / "top_end" restrict
+ * fc_encode to the raster slab [top_begin, top_end) of 16x16 top-level slots
+ * (default 0 / -1 = all); the records are then exactly that slab's run of the
+ * full depth-first record list, so per-rank slabs concatenate in rank order. */
 int fc_set_option(fc_ctx* ctx, const char* name, int64_t value);
 
 /* terms[k-1] = (k/n) * log(k/n), k = 1..n, produced by the host's numpy so the

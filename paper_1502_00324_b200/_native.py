@@ -332,6 +332,11 @@ class Context:
         self.check(self.lib.fc_encode_level_stats(self.handle, level, ctypes.byref(st)))
         return st
 
+    def set_top_slab(self, begin: int = 0, end: int = -1):
+        """Restrict fc_encode to the raster slab [begin, end) of top-level slots."""
+        self.set_option("top_begin", int(begin))
+        self.set_option("top_end", int(end))
+
     def encode_summary(self) -> tuple:
         """(leaf counts per step 1..4, collage SSD) of the last encode."""
         out = np.zeros(5, dtype=np.int64)

@@ -191,6 +191,68 @@ def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=N
                            pool_time, encode_time, comparisons, scan_ms, level_stats, phase)
 
 
+def encode_shard(image: GrayImage, config: EncoderConfig, rank: int, world: int, context=None,
+                 device_image=None):
+    """Range sharding: this rank's contiguous raster slab of
+    16x16 top-level slots (sharding.slab_for_rank), encoded against the full,
+    replicated pool -> (int32 records [n, 6] of the slab in depth-first
+    order, DomainPool, per-level comparisons).  Slabs of ranks 0..world-1
+    concatenate into exactly encode()'s record list: a top-level block's
+    subtree depends only on its own errors (codec.py:134-142)."""
+    from . import sharding
+
+    if image.width % 16 or image.height % 16:
+        raise ValueError(f"dimensions not multiple of 16: {image.width}x{image.height}")
+    ctx = context if context is not None else _native.default_context()
+    pool = build_pool(image, config.pool, context=ctx, device_image=device_image)
+    policy = config.policy
+    s_sets = tuple(policy.s_set(level) for level in (1, 2, 3, 4))
+    n_top = (image.width // 16) * (image.height // 16)
+    begin, end = sharding.slab_for_rank(n_top, rank, world)
+    if begin == end:
+        return np.zeros((0, 6), dtype=np.int32), pool, 0
+    ctx.set_top_slab(begin, end)
+    try:
+        rec = ctx.encode(config.thresholds, policy.mode == BASELINE, s_sets, PATHS[config.path],
+                         capacity=(end - begin) * 256)
+    finally:
+        ctx.set_top_slab(0, -1)
+    comparisons = sum(int(ctx.encode_level_stats(level).comparisons) for level in (1, 2, 3, 4))
+    return np.array(rec, dtype=np.int32), pool, comparisons
+
+
+def encode_distributed(image: GrayImage, config: EncoderConfig, context=None, device_image=None,
+                       device="cuda"):
+    """Range-sharded encode over the initialised torch.distributed group (one
+    process per GPU): every rank builds the replicated pool and encodes its
+    slab (encode_shard), the records are all-gathered (NCCL over NVLink when
+    device="cuda") and every rank returns the full (CompressedStream,
+    EncodeReport) -- byte-identical to encode()."""
+    import torch.distributed as dist
+
+    from . import sharding
+
+    t_start = time.perf_counter()
+    dist_on = dist.is_available() and dist.is_initialized()
+    rank = dist.get_rank() if dist_on else 0
+    world = dist.get_world_size() if dist_on else 1
+    rec, pool, comparisons = encode_shard(image, config, rank, world, context, device_image)
+    allrec = sharding.gather_rows(rec, device=device)
+    comparisons = int(sharding.reduce_metrics(
+        dict(step_ms_total=0.0, e2e_s_total=0.0, kernel_ms_total=0.0, comparisons=comparisons,
+             pixels=0, alg_ops=0), device=device)["comparisons"])
+    policy = config.policy
+    s_sets = tuple(policy.s_set(level) for level in (1, 2, 3, 4))
+    stream = CompressedStream(
+        width=image.width, height=image.height, mode=policy.mode, strides=pool.params.strides,
+        s_sets=s_sets, pools=pool.all_coords(), records=RecordTable._trusted(allrec[:, :5]))
+    step_blocks = tuple(int(v) for v in np.bincount(allrec[:, 0], minlength=5)[1:5])
+    collage_ssd = int(allrec[:, 5].sum(dtype=np.int64))
+    encode_time = time.perf_counter() - t_start
+    return stream, _report(image, config, pool, stream, step_blocks, collage_ssd, 0.0, encode_time,
+                           comparisons, 0.0, [], {"sharded_ranks": world})
+
+
 def _report(image, config, pool, stream, step_blocks, collage_ssd, pool_time, encode_time,
             comparisons, scan_ms, level_stats, phase) -> "EncodeReport":
     pixels = image.width * image.height

@@ -328,6 +328,14 @@ int fc_set_option(fc_ctx* c, const char* name, int64_t value) {
     c->overlap = value != 0;
     return FC_OK;
   }
+  if (strcmp(name, "top_begin") == 0) {  // range sharding: first top-level slot
+    c->top_begin = value;
+    return FC_OK;
+  }
+  if (strcmp(name, "top_end") == 0) {  // range sharding: end of the slab (-1: all)
+    c->top_end = value;
+    return FC_OK;
+  }
   return set_error(c, FC_ERR_ARG, std::string("unknown option ") + name);
 }
 

@@ -31,12 +31,17 @@ namespace {
 
 constexpr int kTop = 16;  // codec.py:114 top-level range side
 
-__global__ void top_origins_kernel(int nxt, int32_t n_top, int32_t* __restrict__ origins,
-                                   int32_t* __restrict__ codes, int32_t* __restrict__ d_M) {
+// The encoded top-level slots are the raster slab [first, first + n_top)
+// (all of them unless the context restricts it, fc_set_option "top_begin" /
+// "top_end"); depth-first codes are local to the slab.
+__global__ void top_origins_kernel(int nxt, int32_t first, int32_t n_top,
+                                   int32_t* __restrict__ origins, int32_t* __restrict__ codes,
+                                   int32_t* __restrict__ d_M) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) *d_M = n_top;
   if (i >= n_top) return;
-  const int32_t ty = i / nxt, tx = i - ty * nxt;
+  const int32_t gi = first + i;
+  const int32_t ty = gi / nxt, tx = gi - ty * nxt;
   origins[2 * i] = tx * kTop;
   origins[2 * i + 1] = ty * kTop;
   codes[i] = i * 64;
@@ -197,7 +202,13 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
 
   // ---- top-level ranges ----
   const int nxt = c->width / kTop, nyt = c->height / kTop;
-  const int64_t n_top = (int64_t)nxt * nyt;
+  const int64_t n_top_all = (int64_t)nxt * nyt;
+  // range-sharded encoding: this context's slab of top-level slots
+  const int64_t top_first = std::min<int64_t>(std::max<int64_t>(c->top_begin, 0), n_top_all);
+  const int64_t top_last =
+      c->top_end < 0 ? n_top_all : std::min<int64_t>(std::max(c->top_end, top_first), n_top_all);
+  const int64_t n_top = top_last - top_first;
+  if (n_top == 0) return set_error(c, FC_ERR_ARG, "empty top-level slab");
   const int64_t n_codes = n_top * 64;
   const int64_t max_ranges = n_top * 64;  // level 4 bound
   for (int b = 0; b < 2; ++b) {
@@ -216,7 +227,8 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   FC_CUDA(c, cudaMemsetAsync(c->leaf_flag.ptr, 0, n_codes * 4, c->stream));
   FC_CUDA(c, cudaMemsetAsync(d_count, 0, kEncBytes, c->stream));  // counters, pairs, spans, hists
   top_origins_kernel<<<blocks_for(n_top), 256, 0, c->stream>>>(
-      nxt, (int32_t)n_top, c->enc_orig[0].as<int32_t>(), c->enc_code[0].as<int32_t>(), d_count);
+      nxt, (int32_t)top_first, (int32_t)n_top, c->enc_orig[0].as<int32_t>(),
+      c->enc_code[0].as<int32_t>(), d_count);
   FC_CUDA(c, cudaGetLastError());
   c->total_launches += 1;
 
@@ -282,6 +294,8 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     put(path);
     put(c->sm_count);
     put(c->overlap);
+    put(top_first);
+    put(top_last);
     put(c->pdl);
     for (int l = 0; l < 3; ++l) putd(thresholds[l]);
     for (int l = 0; l < kLevels; ++l) {

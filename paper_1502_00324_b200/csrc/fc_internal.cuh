@@ -177,6 +177,7 @@ struct Ctx {
               ev_jobs[kLevels] = {};
   bool overlap = true;                 // FC_OVERLAP=0 / option "overlap": single stream
   int64_t enc_summary[5] = {0, 0, 0, 0, 0};  // leaf counts per step, collage SSD
+  int64_t top_begin = 0, top_end = -1;       // fc_encode's top-level slab (-1: to the end)
   bool pdl = false;                    // FC_PDL=1: programmatic dependent launches (measured no gain)
   int tc_debug_mode = 0;               // FC_TC_DEBUG_MODE (pipeline probes)
   int pool_chunk = 0;                  // FC_POOL_CHUNK=512: smaller rank-sort chunks

@@ -27,6 +27,33 @@ def slab_for_rank(n_items: int, rank: int, world: int) -> tuple:
     return start, start + base + (1 if rank < extra else 0)
 
 
+def gather_rows(rows, device="cpu"):
+    """All-gather a rank's 2-D int32 array (variable row count) -> every rank's
+    rows concatenated in rank order (numpy).  One size exchange, then one
+    all_gather of row blocks padded to the longest (NCCL: pass device="cuda").
+    Returns the input when not distributed."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    rows = np.ascontiguousarray(rows, dtype=np.int32)
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return rows
+    world = dist.get_world_size()
+    width = rows.shape[1]
+    n = torch.tensor([rows.shape[0]], dtype=torch.int64, device=device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n)
+    sizes = [int(s.item()) for s in sizes]
+    cap = max(max(sizes), 1)
+    mine = torch.zeros((cap, width), dtype=torch.int32, device=device)
+    if rows.shape[0]:
+        mine[:rows.shape[0]] = torch.from_numpy(rows).to(device)
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    return np.concatenate([p[:s].cpu().numpy() for p, s in zip(parts, sizes)], axis=0)
+
+
 MAX_KEYS = ("step_ms_total", "e2e_s_total", "kernel_ms_total")
 SUM_KEYS = ("comparisons", "pixels", "alg_ops")
 

@@ -61,3 +61,38 @@ def test_reduce_metrics_gloo_world2():
         assert out["comparisons"] == 64 * 1000       # sum over ranks = whole job
         assert out["pixels"] == 64 * 512 * 512
         assert out["alg_ops"] == 21
+
+
+def _gather_worker(rank, world, port, q):
+    import numpy as np
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # rank r contributes r + 2 records (one rank may be empty in general)
+    rows = np.arange((rank + 2) * 6, dtype=np.int32).reshape(-1, 6) + 1000 * rank
+    out = sharding.gather_rows(rows)
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gather_rows_gloo_world2_rank_order():
+    """The record all-gather of encode_distributed: variable row counts,
+    concatenated in rank order on every rank (gloo, world size 2)."""
+    import numpy as np
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = np.concatenate([np.arange((r + 2) * 6, dtype=np.int32).reshape(-1, 6) + 1000 * r
+                           for r in range(2)])
+    for rank in (0, 1):
+        assert np.array_equal(results[rank], want)
