@@ -47,6 +47,10 @@ def parse_args():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--path", default="auto", choices=["auto", "exact", "tensor"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="images", choices=["images", "ranges"],
+                    help="images: weak scaling, one seeded image per rank (c3: its 64 images); "
+                         "ranges: strong scaling, one image split into top-level slabs "
+                         "(encode_distributed, records all-gathered over NCCL)")
     return ap.parse_args()
 
 
@@ -247,15 +251,19 @@ def main():
     ctx = _native.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream_handle(), device=torch.device("cuda", local))
     cfg = encoder_config(args.workload, args.path)
-    imgs = images_for_rank(args.workload, rank, world)
+    ranges = args.shard == "ranges"
+    # ranges: every rank holds the same image and encodes its slab of top-level
+    # slots (encode_distributed all-gathers the records); images: weak scaling
+    imgs = images_for_rank(args.workload, 0, 1)[:1] if ranges else images_for_rank(args.workload, rank, world)
     gimgs = [fc.GrayImage(im) for im in imgs]
     dimgs = [torch.from_numpy(im.copy()).cuda() for im in imgs]
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")  # 512 MB > L2
+    enc = fc.encode_distributed if ranges else fc.encode
 
     def step_device():
         reps = []
         for g, d in zip(gimgs, dimgs):
-            _, rep = fc.encode(g, cfg, context=ctx, device_image=d)
+            _, rep = enc(g, cfg, context=ctx, device_image=d)
             reps.append(rep)
         return reps
 
@@ -287,7 +295,8 @@ def main():
         e1.synchronize()
         total_ms += e0.elapsed_time(e1)
         for rep in reps:
-            comps += rep.comparisons
+            # this rank's own comparisons (its slab under --shard ranges), summed below
+            comps += sum(ls["comparisons"] for ls in rep.level_stats)
             for ls in rep.level_stats:
                 if ls["path"] == _native.PATH_TENSOR:
                     n = fc.pool.LEVEL_RANGE_SIDES[ls["level"] - 1] ** 2
@@ -297,7 +306,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     launches = ctx.launch_count() - launches0
-    pixels_per_step = sum(im.size for im in imgs)
+    pixels_per_step = sum(im.size for im in imgs) if (rank == 0 or not ranges) else 0
 
     # e2e: public API from host pixels, result serialised to bytes
     e2e_t = 0.0
@@ -306,7 +315,7 @@ def main():
         barrier()
         t0 = time.perf_counter()
         for g in gimgs:
-            stream_out, rep = fc.encode(g, cfg, context=ctx)
+            stream_out, rep = enc(g, cfg, context=ctx)
             data = fc.serialize(stream_out)
         e2e_t += time.perf_counter() - t0
     clk = clocks.stop()  # sampled across both timed regions (device-timed and end-to-end)
@@ -357,7 +366,7 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": total_ms_all / args.steps,
         "higher_is_better": True,
-        "scaling": "weak" if W.WORKLOADS[args.workload].images == 1 else "strong",
+        "scaling": "strong" if ranges or W.WORKLOADS[args.workload].images > 1 else "weak",
         "vs_baseline": None,
         "dtype": "u8 x s8 -> s32 (int8 tensor cores), int64 keys",
         "data": "synthetic (seeded generators, workloads.py)",
@@ -365,6 +374,8 @@ def main():
             "workload": args.workload,
             "description": W.WORKLOADS[args.workload].description,
             "images_per_rank": len(imgs), "path": args.path,
+            "sharding": ("range slabs of one image, pool replicated, records all-gathered (NCCL)"
+                         if ranges else "independent images per rank, no data-path collective"),
             "l2": "flushed (512 MB write) before every timed step",
             "pool_sizes": list(reps[0].pool_sizes), "step_blocks": list(reps[0].step_blocks),
             "comparisons_per_step": comps_all / args.steps,

@@ -166,20 +166,9 @@ def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=N
                      capacity=image.width * image.height // 4)
     t_r = time.perf_counter()
     phase = {"pool": 1e3 * pool_time, "quadtree": 1e3 * (t_r - t_q)}
-    level_stats = []
-    comparisons = 0
-    scan_ms = 0.0
-    for level in (1, 2, 3, 4):
-        st = ctx.encode_level_stats(level)
-        if st.ranges == 0:
-            continue
-        comparisons += int(st.comparisons)
-        scan_ms += float(st.scan_ms)
-        level_stats.append(dict(level=level, ranges=int(st.ranges), columns=int(st.columns),
-                                comparisons=int(st.comparisons), path=int(st.path),
-                                launches=int(st.kernel_launches), scan_ms=float(st.scan_ms),
-                                main_ms=float(st.main_ms), fix_ms=float(st.fix_ms),
-                                fix_pairs=int(st.fix_pairs), rescans=int(st.rescans)))
+    level_stats = _level_stats(ctx)
+    comparisons = sum(ls["comparisons"] for ls in level_stats)
+    scan_ms = sum(ls["scan_ms"] for ls in level_stats)
     records = RecordTable._trusted(rec[:, :5])  # int32 view of the device records
     stream = CompressedStream(
         width=image.width, height=image.height, mode=policy.mode, strides=pool.params.strides,
@@ -196,7 +185,7 @@ def encode_shard(image: GrayImage, config: EncoderConfig, rank: int, world: int,
     """Range sharding: this rank's contiguous raster slab of
     16x16 top-level slots (sharding.slab_for_rank), encoded against the full,
     replicated pool -> (int32 records [n, 6] of the slab in depth-first
-    order, DomainPool, per-level comparisons).  Slabs of ranks 0..world-1
+    order, DomainPool, per-level statistics of the slab as in EncodeReport).  Slabs of ranks 0..world-1
     concatenate into exactly encode()'s record list: a top-level block's
     subtree depends only on its own errors (codec.py:134-142)."""
     from . import sharding
@@ -210,15 +199,28 @@ def encode_shard(image: GrayImage, config: EncoderConfig, rank: int, world: int,
     n_top = (image.width // 16) * (image.height // 16)
     begin, end = sharding.slab_for_rank(n_top, rank, world)
     if begin == end:
-        return np.zeros((0, 6), dtype=np.int32), pool, 0
+        return np.zeros((0, 6), dtype=np.int32), pool, []
     ctx.set_top_slab(begin, end)
     try:
         rec = ctx.encode(config.thresholds, policy.mode == BASELINE, s_sets, PATHS[config.path],
                          capacity=(end - begin) * 256)
     finally:
         ctx.set_top_slab(0, -1)
-    comparisons = sum(int(ctx.encode_level_stats(level).comparisons) for level in (1, 2, 3, 4))
-    return np.array(rec, dtype=np.int32), pool, comparisons
+    return np.array(rec, dtype=np.int32), pool, _level_stats(ctx)
+
+
+def _level_stats(ctx) -> list:
+    out = []
+    for level in (1, 2, 3, 4):
+        st = ctx.encode_level_stats(level)
+        if st.ranges == 0:
+            continue
+        out.append(dict(level=level, ranges=int(st.ranges), columns=int(st.columns),
+                        comparisons=int(st.comparisons), path=int(st.path),
+                        launches=int(st.kernel_launches), scan_ms=float(st.scan_ms),
+                        main_ms=float(st.main_ms), fix_ms=float(st.fix_ms),
+                        fix_pairs=int(st.fix_pairs), rescans=int(st.rescans)))
+    return out
 
 
 def encode_distributed(image: GrayImage, config: EncoderConfig, context=None, device_image=None,
@@ -236,11 +238,12 @@ def encode_distributed(image: GrayImage, config: EncoderConfig, context=None, de
     dist_on = dist.is_available() and dist.is_initialized()
     rank = dist.get_rank() if dist_on else 0
     world = dist.get_world_size() if dist_on else 1
-    rec, pool, comparisons = encode_shard(image, config, rank, world, context, device_image)
+    rec, pool, level_stats = encode_shard(image, config, rank, world, context, device_image)
     allrec = sharding.gather_rows(rec, device=device)
     comparisons = int(sharding.reduce_metrics(
-        dict(step_ms_total=0.0, e2e_s_total=0.0, kernel_ms_total=0.0, comparisons=comparisons,
-             pixels=0, alg_ops=0), device=device)["comparisons"])
+        dict(step_ms_total=0.0, e2e_s_total=0.0, kernel_ms_total=0.0,
+             comparisons=sum(ls["comparisons"] for ls in level_stats), pixels=0, alg_ops=0),
+        device=device)["comparisons"])
     policy = config.policy
     s_sets = tuple(policy.s_set(level) for level in (1, 2, 3, 4))
     stream = CompressedStream(
@@ -249,8 +252,10 @@ def encode_distributed(image: GrayImage, config: EncoderConfig, context=None, de
     step_blocks = tuple(int(v) for v in np.bincount(allrec[:, 0], minlength=5)[1:5])
     collage_ssd = int(allrec[:, 5].sum(dtype=np.int64))
     encode_time = time.perf_counter() - t_start
+    # comparisons: the whole image (all ranks); level_stats: this rank's slab
     return stream, _report(image, config, pool, stream, step_blocks, collage_ssd, 0.0, encode_time,
-                           comparisons, 0.0, [], {"sharded_ranks": world})
+                           comparisons, sum(ls["scan_ms"] for ls in level_stats), level_stats,
+                           {"sharded_ranks": world})
 
 
 def _report(image, config, pool, stream, step_blocks, collage_ssd, pool_time, encode_time,

@@ -309,7 +309,7 @@ def test_range_sharded_slabs_concatenate_to_the_full_encode(world):
     full, _ = fc.encode(fc.GrayImage(img), cfg, context=ctx)
     parts = []
     for rank in range(world):
-        rec, _, comps = fc.encode_shard(fc.GrayImage(img), cfg, rank, world, context=ctx)
+        rec, _, stats = fc.encode_shard(fc.GrayImage(img), cfg, rank, world, context=ctx)
         assert rec.dtype == np.int32 and rec.shape[1] == 6
         parts.append(rec)
     allrec = np.concatenate(parts)
