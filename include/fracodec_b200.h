@@ -156,6 +156,19 @@ int fc_encode_level_stats(fc_ctx* ctx, int level, fc_stats* out);
  * 1..4 (codec.py step_blocks), out[4] = collage SSD (sum of the leaf errors). */
 int fc_encode_summary(fc_ctx* ctx, int64_t out[5]);
 
+/* Device decoder (codec.py:257-363 decode_trace): `iterations` collage
+ * passes from a mid-gray (128) image, stopping after the first pass whose
+ * max |new - cur| <= tolerance.  leaves: int32 [n][8] rows (rx, ry, level,
+ * dx, dy, iso, s_index, offset) in any order, one per range block (they must
+ * tile the image); svals / s_counts as in fc_encode; proposed = 1 for the
+ * proposed mode (q = rint(s (t - mean))), 0 for baseline (rint(s t)).
+ * out_image: width*height uint8; out_deltas (optional): one per pass run;
+ * out_passes: passes run. */
+int fc_decode(fc_ctx* ctx, const int32_t* leaves, int64_t n, int32_t width, int32_t height,
+              const double* svals, const int32_t s_counts[4], int32_t proposed,
+              int32_t iterations, int32_t tolerance, uint8_t* out_image, int32_t* out_deltas,
+              int32_t* out_passes);
+
 int fc_last_stats(fc_ctx* ctx, fc_stats* out);
 /* The context's CUDA stream (cudaStream_t) so callers can time on it. */
 int fc_get_stream(fc_ctx* ctx, void** out_stream);

@@ -85,6 +85,9 @@ _SIGNATURES = {
     "fc_encode_records": ([_P, _P, _I64], ctypes.c_int),
     "fc_encode_level_stats": ([_P, ctypes.c_int, ctypes.POINTER(FcStats)], ctypes.c_int),
     "fc_encode_summary": ([_P, _P], ctypes.c_int),
+    "fc_decode": ([_P, _P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _P, _P, ctypes.c_int32,
+                   ctypes.c_int32, ctypes.c_int32, _P, _P, ctypes.POINTER(ctypes.c_int32)],
+                  ctypes.c_int),
     "fc_last_stats": ([_P, ctypes.POINTER(FcStats)], ctypes.c_int),
     "fc_get_stream": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
     "fc_launch_count": ([_P, ctypes.POINTER(_I64)], ctypes.c_int),
@@ -331,6 +334,20 @@ class Context:
         st = FcStats()
         self.check(self.lib.fc_encode_level_stats(self.handle, level, ctypes.byref(st)))
         return st
+
+    def decode(self, leaves: np.ndarray, width: int, height: int, s_sets, proposed: bool,
+               iterations: int, tolerance: int):
+        """Device collage iterations (fc_decode) -> (uint8 [height, width], deltas)."""
+        lv = np.ascontiguousarray(leaves, dtype=np.int32).reshape(-1, 8)
+        counts = np.array([len(s) for s in s_sets], dtype=np.int32)
+        sv = np.ascontiguousarray(np.concatenate([np.asarray(s, dtype=np.float64) for s in s_sets]))
+        out = np.empty((height, width), dtype=np.uint8)
+        deltas = np.zeros(max(int(iterations), 1), dtype=np.int32)
+        passes = ctypes.c_int32()
+        self.check(self.lib.fc_decode(self.handle, _ptr(lv), lv.shape[0], int(width), int(height),
+                                      _ptr(sv), _ptr(counts), int(bool(proposed)), int(iterations),
+                                      int(tolerance), _ptr(out), _ptr(deltas), ctypes.byref(passes)))
+        return out, [int(v) for v in deltas[:passes.value]]
 
     def set_top_slab(self, begin: int = 0, end: int = -1):
         """Restrict fc_encode to the raster slab [begin, end) of top-level slots."""

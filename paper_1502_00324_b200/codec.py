@@ -427,3 +427,29 @@ def decode_trace(stream: CompressedStream, iterations: int = 15, tolerance: int 
 
 def decode(stream: CompressedStream, iterations: int = 15, tolerance: int = 0) -> GrayImage:
     return decode_trace(stream, iterations, tolerance)[0]
+
+
+def decode_trace_device(stream: CompressedStream, iterations: int = 15, tolerance: int = 0,
+                        context=None):
+    """decode_trace on the device (fc_decode: one launch per collage pass, one
+    host synchronisation per decode) -> (GrayImage, deltas); the same image
+    and deltas as the host decode_trace (tests/test_gpu_parity.py)."""
+    if iterations < 1:
+        raise ValueError("iterations must be >= 1")
+    if tolerance < 0:
+        raise ValueError("tolerance must be >= 0")
+    ctx = context if context is not None else _native.default_context()
+    rows = []
+    pools = [np.asarray(CoordTable(p).array, dtype=np.int64) for p in stream.pools]
+    for rec, x, y, _side in iter_leaves(stream):
+        dx, dy = pools[rec.step - 1][rec.domain_address]
+        rows.append((x, y, rec.step, int(dx), int(dy), rec.isometry, rec.s_index, rec.offset))
+    leaves = np.array(rows, dtype=np.int32).reshape(-1, 8)
+    img, deltas = ctx.decode(leaves, stream.width, stream.height, stream.s_sets,
+                             stream.mode == PROPOSED, iterations, tolerance)
+    return GrayImage(img), deltas
+
+
+def decode_device(stream: CompressedStream, iterations: int = 15, tolerance: int = 0,
+                  context=None) -> GrayImage:
+    return decode_trace_device(stream, iterations, tolerance, context)[0]

@@ -597,6 +597,15 @@ int fc_encode_level_stats(fc_ctx* c, int level, fc_stats* out) {
   return FC_OK;
 }
 
+int fc_decode(fc_ctx* c, const int32_t* leaves, int64_t n, int32_t width, int32_t height,
+              const double* svals, const int32_t s_counts[4], int32_t proposed,
+              int32_t iterations, int32_t tolerance, uint8_t* out_image, int32_t* out_deltas,
+              int32_t* out_passes) {
+  cudaSetDevice(c->device);
+  return decode_device(c, leaves, n, width, height, svals, s_counts, proposed, iterations,
+                       tolerance, out_image, out_deltas, out_passes);
+}
+
 int fc_encode_summary(fc_ctx* c, int64_t out[5]) {
   if (!out) return set_error(c, FC_ERR_ARG, "null output");
   for (int k = 0; k < 5; ++k) out[k] = c->enc_summary[k];

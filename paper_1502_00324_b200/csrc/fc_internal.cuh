@@ -178,6 +178,7 @@ struct Ctx {
   bool overlap = true;                 // FC_OVERLAP=0 / option "overlap": single stream
   int64_t enc_summary[5] = {0, 0, 0, 0, 0};  // leaf counts per step, collage SSD
   int64_t top_begin = 0, top_end = -1;       // fc_encode's top-level slab (-1: to the end)
+  DevBuf dec_img, dec_leaves, dec_state, dec_svals;  // device decoder (fc_decode.cu)
   bool pdl = false;                    // FC_PDL=1: programmatic dependent launches (measured no gain)
   int tc_debug_mode = 0;               // FC_TC_DEBUG_MODE (pipeline probes)
   int pool_chunk = 0;                  // FC_POOL_CHUNK=512: smaller rank-sort chunks
@@ -326,6 +327,9 @@ int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys);
 int reserve_level_scan(Ctx* c, Level& L, int64_t bound);
 
 // fc_encode.cu
+int decode_device(Ctx* c, const int32_t* leaves, int64_t n_leaves, int width, int height,
+                  const double* svals, const int32_t* s_counts, int proposed, int iterations,
+                  int tolerance, uint8_t* out_image, int32_t* out_deltas, int32_t* out_passes);
 int encode_device(Ctx* c, const double thresholds[3], int baseline, const double* svals,
                   const int32_t s_counts[4], int path, int32_t* out_records, int64_t capacity,
                   int64_t* out_count);

@@ -321,3 +321,29 @@ def test_range_sharded_slabs_concatenate_to_the_full_encode(world):
     # the full encode is unaffected afterwards (slab reset)
     again, _ = fc.encode(fc.GrayImage(img), cfg, context=ctx)
     assert fc.serialize(again) == g["bytes_c2"].tobytes()
+
+
+@pytest.mark.parametrize("tag", ["c2", "c3_1"])
+@pytest.mark.parametrize("tolerance", [0, 2])
+def test_device_decoder_matches_host_decoder(tag, tolerance):
+    """fc_decode (one launch per collage pass) reproduces the host decoder's
+    image and per-pass deltas bit for bit, including the early stop."""
+    g = load_golden("encode_c2.npz")
+    stream = fc.deserialize(g[f"bytes_{tag}"].tobytes())
+    want, wd = fc.decode_trace(stream, 15, tolerance)
+    got, gd = fc.decode_trace_device(stream, 15, tolerance)
+    assert gd == wd
+    assert np.array_equal(got.pixels, want.pixels)
+
+
+@pytest.mark.parametrize("tag", ["tiled_baseline", "darkbright_baseline", "noise", "flat"])
+def test_device_decoder_golden_cases(tag):
+    """Baseline-mode and edge streams of the golden set: device == host decode,
+    PSNR as recorded by the reference."""
+    g = load_golden("encode_cases.npz")
+    stream = fc.deserialize(g[f"bytes_{tag}"].tobytes())
+    want = fc.decode(stream)
+    got = fc.decode_device(stream)
+    assert np.array_equal(got.pixels, want.pixels)
+    p, ref = fc.psnr(fc.GrayImage(g[f"image_{tag}"]), got), float(g[f"psnr_{tag}"])
+    assert p == ref or abs(p - ref) < 0.01
