@@ -239,6 +239,7 @@ int fc_ctx_create(int device, fc_ctx** out) {
   if (const char* d = getenv("FC_TC_G1")) c->tc_g1 = atoi(d);
   if (const char* o = getenv("FC_OVERLAP")) c->overlap = atoi(o) != 0;
   if (const char* o = getenv("FC_PDL")) c->pdl = atoi(o) != 0;
+  if (const char* o = getenv("FC_FIX_FUSED")) c->fix_fused = atoi(o) != 0;
   if (const char* d = getenv("FC_POOL_CHUNK")) c->pool_chunk = atoi(d);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||

@@ -297,6 +297,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     put(top_first);
     put(top_last);
     put(c->pdl);
+    put(c->fix_fused);
     for (int l = 0; l < 3; ++l) putd(thresholds[l]);
     for (int l = 0; l < kLevels; ++l) {
       const Level& L = c->lv[l];

@@ -179,6 +179,7 @@ struct Ctx {
   int64_t enc_summary[5] = {0, 0, 0, 0, 0};  // leaf counts per step, collage SSD
   int64_t top_begin = 0, top_end = -1;       // fc_encode's top-level slab (-1: to the end)
   DevBuf dec_img, dec_leaves, dec_state, dec_svals;  // device decoder (fc_decode.cu)
+  bool fix_fused = false;              // FC_FIX_FUSED=1: clamp corrections inside the contraction (measured 2% slower on c2)
   bool pdl = false;                    // FC_PDL=1: programmatic dependent launches (measured no gain)
   int tc_debug_mode = 0;               // FC_TC_DEBUG_MODE (pipeline probes)
   int pool_chunk = 0;                  // FC_POOL_CHUNK=512: smaller rank-sort chunks

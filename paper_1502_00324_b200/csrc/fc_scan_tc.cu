@@ -127,6 +127,148 @@ struct SegIter {
   }
 };
 
+// Clamp corrections: a warp handles one range x fix_cols(n) columns per unit
+// (n = 256: one column per lane, the few pairs of B = 16 need parallelism).
+__host__ __device__ constexpr int fix_cpl(int n) { return n >= 256 ? 1 : 4; }
+__host__ __device__ constexpr int fix_cols(int n) { return 32 * fix_cpl(n); }
+// inside tc_scan_kernel (96-register budget): fewer columns per lane
+__host__ __device__ constexpr int fix_cpl_fused(int n) { return n >= 256 ? 1 : 2; }
+__host__ __device__ constexpr int fix_cols_fused(int n) { return 32 * fix_cpl_fused(n); }
+
+// Clamp-correction plan (FixPlan) of one level.
+struct FixPlan {
+  int n_jobs;
+  int pad;
+  long long total_units;  // (range, columns-per-unit chunk) units; prefix[] counts them too
+  long long fix_pairs;
+  unsigned long long next_unit;  // work counter of the corrections fused into tc_scan_kernel
+};
+
+// Clamp corrections: one warp per unit = one range x CPL*32 consecutive
+// columns of a job (job j: ranges sorted_ranges[r_off, r_off + r_cnt) x the
+// first col_cnt columns of reach list `list`), CPL columns per lane.  The
+// exact error of all 8 isometries follows _scan.py:47-55 (clip(q + o) - r,
+// squared, summed): a column's clipped pixels are packed to bytes once per
+// 16-pixel chunk and compared with the range's isometry rows, read straight
+// from the A operand (its first n bytes of K are r[inv_iso[k]]; warp-uniform
+// broadcast loads, shared by the lane's columns).  Minimum over the lane's
+// columns, then the warp (err, then candidate index), one atomicMin per unit.
+struct FixArgs {
+  const int16_t* qbase;
+  const uint8_t* a_tiles;
+  const int32_t* roff;
+  const int4* jobs;
+  const long long* prefix;     // unit prefix per job (global; copied to smem by the kernel)
+  FixPlan* fplan;
+  const int32_t* sorted_ranges;
+  const int32_t* list_low;
+  const int32_t* list_high;
+  unsigned long long* keys;
+  int S, kpad, n;
+};
+
+template <int N, int CPL>
+__device__ __forceinline__ void fix_unit(const FixArgs& F, const long long* __restrict__ pre,
+                                         int n_jobs, long long u, int lane) {
+  constexpr int kCols = 32 * CPL;
+  int lo = 0, hi = n_jobs - 1;  // last job with prefix <= u (warp-uniform)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= u) lo = mid; else hi = mid - 1;
+  }
+  const int4 job = F.jobs[lo];  // {list, r_off, r_cnt, col_cnt}
+  const long long local = u - pre[lo];
+  const unsigned ncc = (unsigned)(job.w + kCols - 1) / kCols;
+  const unsigned ri = local < 0x7fffffffll ? (unsigned)local / ncc : (unsigned)(local / ncc);
+  const int c0 = (int)((unsigned)(local - (long long)ri * ncc) * (unsigned)kCols);
+  const int m = F.sorted_ranges[job.y + ri];
+  const int32_t* list = job.x ? F.list_high : F.list_low;
+  int col[CPL];
+  bool valid[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int ci = c0 + c * 32 + lane;
+    valid[c] = ci < job.w;
+    col[c] = valid[c] ? list[ci] : list[c0];  // padding lanes repeat a real column
+  }
+  const int o = F.roff[m];
+  const unsigned o2 = (unsigned)o | ((unsigned)o << 16);
+  const int64_t row0 = (int64_t)m * 8;  // the range's 8 isometry rows: one 8-row core block
+  const uint8_t* abase = F.a_tiles + (row0 >> 7) * ((int64_t)kTileM * F.kpad) +
+                         ((int)(row0 & 127) >> 3) * 128;
+  unsigned acc[CPL][8];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+#pragma unroll
+    for (int iso = 0; iso < 8; ++iso) acc[c][iso] = 0u;
+#pragma unroll 1
+  for (int kc = 0; kc < N / 16; ++kc) {
+    uint4 r4[8];
+    const uint8_t* ak = abase + kc * (kTileM * 16);
+#pragma unroll
+    for (int iso = 0; iso < 8; ++iso) r4[iso] = __ldg(reinterpret_cast<const uint4*>(ak + iso * 16));
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int16_t* qc = F.qbase + (int64_t)col[c] * N + kc * 16;
+      const uint4 qa = __ldg(reinterpret_cast<const uint4*>(qc));
+      const uint4 qb = __ldg(reinterpret_cast<const uint4*>(qc + 8));
+      const unsigned qw[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+      unsigned x4[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        // clip(q + o, 0, 255) on int16 pairs, then packed to 4 bytes
+        const unsigned lo2 = __vmins2(__vmaxs2(__vadd2(qw[2 * w], o2), 0u), 0x00ff00ffu);
+        const unsigned hi2 = __vmins2(__vmaxs2(__vadd2(qw[2 * w + 1], o2), 0u), 0x00ff00ffu);
+        x4[w] = __byte_perm(lo2, hi2, 0x6420);
+      }
+#pragma unroll
+      for (int iso = 0; iso < 8; ++iso) {
+        unsigned a = acc[c][iso], d;
+        d = __vabsdiffu4(x4[0], r4[iso].x); a = __dp4a(d, d, a);
+        d = __vabsdiffu4(x4[1], r4[iso].y); a = __dp4a(d, d, a);
+        d = __vabsdiffu4(x4[2], r4[iso].z); a = __dp4a(d, d, a);
+        d = __vabsdiffu4(x4[3], r4[iso].w); a = __dp4a(d, d, a);
+        acc[c][iso] = a;
+      }
+    }
+  }
+  unsigned long long best = ~0ull;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    // err <= 256 * 255^2 < 2^24: (err << 3 | iso) orders by err, then iso
+    unsigned k = acc[c][0] << 3;
+#pragma unroll
+    for (int iso = 1; iso < 8; ++iso) k = min(k, (acc[c][iso] << 3) | (unsigned)iso);
+    // candidate index (e * 8 + iso) * S + si with e * S = col - si
+    const int S = F.S;
+    const int si = S == 1 ? 0 : (S == 2 ? (col[c] & 1) : col[c] % S);
+    const unsigned cidx = (unsigned)(8 * (col[c] - si) + (int)(k & 7) * S + si);
+    const unsigned long long key = ((unsigned long long)(k >> 3) << 32) | cidx;
+    if (valid[c] && key < best) best = key;
+  }
+  const unsigned err = (unsigned)(best >> 32);  // 0xffffffff: no valid column
+  const unsigned werr = __reduce_min_sync(0xffffffffu, err);
+  const unsigned widx = __reduce_min_sync(0xffffffffu, err == werr ? (unsigned)best : 0xffffffffu);
+  if (lane == 0 && werr != 0xffffffffu)
+    atomicMin(&F.keys[m], ((unsigned long long)werr << 32) | widx);
+}
+
+// Warp loop over the corrections inside tc_scan_kernel: units claimed from
+// the plan's counter, so CTAs that finish their contraction share early take
+// more of them (fills the contraction's tail).
+template <int N>
+__device__ __forceinline__ void fix_fused_loop(const FixArgs& F, int lane) {
+  const int n_jobs = F.fplan->n_jobs;
+  const long long total = F.fplan->total_units;
+  for (;;) {
+    unsigned long long u = 0;
+    if (lane == 0) u = atomicAdd(&F.fplan->next_unit, 1ull);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if ((long long)u >= total) break;
+    fix_unit<N, fix_cpl_fused(N)>(F, F.prefix, n_jobs, (long long)u, lane);
+  }
+}
+
 struct TcParams {
   const uint8_t* a_tiles;    // [rt_pad][128 * kpad]
   const int4* row_meta;      // [rt_pad * 128] {o, R, m, unused}
@@ -141,6 +283,8 @@ struct TcParams {
   const TcPlan* plan;
   int deferred;    // 1: resolve the winning column once per unit (short K)
   int g1;          // 1: every epilogue warp drains every accumulator (64 columns)
+  int fix_fused;   // 1: the clamp corrections run in this kernel (fix_fused_loop)
+  FixArgs fix;
   unsigned long long* tspan;  // optional {start, end} slots (global ns)
 };
 
@@ -512,6 +656,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
       if (p.deferred) epilogue_role<true, false>(p, x);
       else epilogue_role<false, false>(p, x);
     }
+    if (p.fix_fused) {
+      switch (p.fix.n) {
+        case 256: fix_fused_loop<256>(p.fix, lane); break;
+        case 64: fix_fused_loop<64>(p.fix, lane); break;
+        default: fix_fused_loop<16>(p.fix, lane); break;
+      }
+      if (p.tspan && lane == 0) atomicMax(&p.tspan[2], global_ns());
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -747,19 +899,6 @@ __global__ void reach_scatter_kernel(const int4* __restrict__ stats, int64_t nco
   bucket_scatter(valid, st.w + 512, cur_high, reach_high, (int32_t)col);
 }
 
-// Clamp corrections: a warp handles one range x fix_cols(n) columns per unit
-// (n = 256: one column per lane, the few pairs of B = 16 need parallelism).
-__host__ __device__ constexpr int fix_cpl(int n) { return n >= 256 ? 1 : 4; }
-__host__ __device__ constexpr int fix_cols(int n) { return 32 * fix_cpl(n); }
-
-// Clamp-correction plan (FixPlan) of one level.
-struct FixPlan {
-  int n_jobs;
-  int pad;
-  long long total_units;  // (range, fix_cols(n)-column chunk) units; prefix[] counts them too
-  long long fix_pairs;
-};
-
 // All per-level launch planning in ONE single-block kernel (the host never
 // waits for it):
 //  * work decomposition of the contraction: RG row tiles per group and the
@@ -898,116 +1037,22 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restr
   for (int i = tid; i < M; i += kPlanThreads) order[atomicAdd(&cursor[roff[i]], 1)] = i;
 }
 
-// Clamp corrections: one warp per unit = one range x kFixCols consecutive
-// columns of a job (job j: ranges sorted_ranges[r_off, r_off + r_cnt) x the
-// first col_cnt columns of reach list `list`), kFixCpl columns per lane.  The
-// exact error of all 8 isometries follows _scan.py:47-55 (clip(q + o) - r,
-// squared, summed): a column's clipped pixels are packed to bytes once per
-// 16-pixel chunk and compared with the range's isometry rows, read straight
-// from the A operand (its first n bytes of K are r[inv_iso[k]]; warp-uniform
-// broadcast loads, shared by the lane's columns).  Minimum over the lane's
-// columns, then the warp (err, then candidate index), one atomicMin per unit.
 constexpr int kFixThreads = 256;
 template <int N>
 __global__ void __launch_bounds__(kFixThreads)
-fix_pairs_kernel(const int16_t* __restrict__ qbase, int S, const uint8_t* __restrict__ a_tiles,
-                 int kpad, const int32_t* __restrict__ roff, const int4* __restrict__ jobs,
-                 const long long* __restrict__ prefix, const FixPlan* __restrict__ fplan,
-                 const int32_t* __restrict__ sorted_ranges, const int32_t* __restrict__ list_low,
-                 const int32_t* __restrict__ list_high, unsigned long long* __restrict__ keys,
-                 unsigned long long* __restrict__ t_end) {
+fix_pairs_kernel(FixArgs F, unsigned long long* __restrict__ t_end) {
   static_assert(N % 16 == 0, "tensor levels have n >= 16");
   constexpr int kWarps = kFixThreads / 32;
-  constexpr int kFixCpl = fix_cpl(N), kFixCols = fix_cols(N);
   __shared__ long long s_prefix[513];  // at most 2 jobs per offset bucket, + the total
   const int tid = threadIdx.x, lane = tid & 31;
-  const int n_jobs = fplan->n_jobs;
-  const long long total = fplan->total_units;
+  const int n_jobs = F.fplan->n_jobs;
+  const long long total = F.fplan->total_units;
   if ((long long)blockIdx.x * kWarps >= total) return;
-  for (int j = tid; j <= n_jobs; j += kFixThreads) s_prefix[j] = prefix[j];
+  for (int j = tid; j <= n_jobs; j += kFixThreads) s_prefix[j] = F.prefix[j];
   __syncthreads();
   for (long long u = (long long)blockIdx.x * kWarps + (tid >> 5); u < total;
-       u += (long long)gridDim.x * kWarps) {
-    int lo = 0, hi = n_jobs - 1;  // last job with prefix <= u (warp-uniform)
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_prefix[mid] <= u) lo = mid; else hi = mid - 1;
-    }
-    const int4 job = jobs[lo];  // {list, r_off, r_cnt, col_cnt}
-    const long long local = u - s_prefix[lo];
-    const unsigned ncc = (unsigned)(job.w + kFixCols - 1) / kFixCols;
-    const unsigned ri = local < 0x7fffffffll ? (unsigned)local / ncc : (unsigned)(local / ncc);
-    const int c0 = (int)((unsigned)(local - (long long)ri * ncc) * (unsigned)kFixCols);
-    const int m = sorted_ranges[job.y + ri];
-    const int32_t* list = job.x ? list_high : list_low;
-    int col[kFixCpl];
-    bool valid[kFixCpl];
-#pragma unroll
-    for (int c = 0; c < kFixCpl; ++c) {
-      const int ci = c0 + c * 32 + lane;
-      valid[c] = ci < job.w;
-      col[c] = valid[c] ? list[ci] : list[c0];  // padding lanes repeat a real column
-    }
-    const int o = roff[m];
-    const unsigned o2 = (unsigned)o | ((unsigned)o << 16);
-    const int64_t row0 = (int64_t)m * 8;  // the range's 8 isometry rows: one 8-row core block
-    const uint8_t* abase = a_tiles + (row0 >> 7) * ((int64_t)kTileM * kpad) +
-                           ((int)(row0 & 127) >> 3) * 128;
-    unsigned acc[kFixCpl][8];
-#pragma unroll
-    for (int c = 0; c < kFixCpl; ++c)
-#pragma unroll
-      for (int iso = 0; iso < 8; ++iso) acc[c][iso] = 0u;
-#pragma unroll 1
-    for (int kc = 0; kc < N / 16; ++kc) {
-      uint4 r4[8];
-      const uint8_t* ak = abase + kc * (kTileM * 16);
-#pragma unroll
-      for (int iso = 0; iso < 8; ++iso) r4[iso] = __ldg(reinterpret_cast<const uint4*>(ak + iso * 16));
-#pragma unroll
-      for (int c = 0; c < kFixCpl; ++c) {
-        const int16_t* qc = qbase + (int64_t)col[c] * N + kc * 16;
-        const uint4 qa = __ldg(reinterpret_cast<const uint4*>(qc));
-        const uint4 qb = __ldg(reinterpret_cast<const uint4*>(qc + 8));
-        const unsigned qw[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-        unsigned x4[4];
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          // clip(q + o, 0, 255) on int16 pairs, then packed to 4 bytes
-          const unsigned lo2 = __vmins2(__vmaxs2(__vadd2(qw[2 * w], o2), 0u), 0x00ff00ffu);
-          const unsigned hi2 = __vmins2(__vmaxs2(__vadd2(qw[2 * w + 1], o2), 0u), 0x00ff00ffu);
-          x4[w] = __byte_perm(lo2, hi2, 0x6420);
-        }
-#pragma unroll
-        for (int iso = 0; iso < 8; ++iso) {
-          unsigned a = acc[c][iso], d;
-          d = __vabsdiffu4(x4[0], r4[iso].x); a = __dp4a(d, d, a);
-          d = __vabsdiffu4(x4[1], r4[iso].y); a = __dp4a(d, d, a);
-          d = __vabsdiffu4(x4[2], r4[iso].z); a = __dp4a(d, d, a);
-          d = __vabsdiffu4(x4[3], r4[iso].w); a = __dp4a(d, d, a);
-          acc[c][iso] = a;
-        }
-      }
-    }
-    unsigned long long best = ~0ull;
-#pragma unroll
-    for (int c = 0; c < kFixCpl; ++c) {
-      // err <= 256 * 255^2 < 2^24: (err << 3 | iso) orders by err, then iso
-      unsigned k = acc[c][0] << 3;
-#pragma unroll
-      for (int iso = 1; iso < 8; ++iso) k = min(k, (acc[c][iso] << 3) | (unsigned)iso);
-      // candidate index (e * 8 + iso) * S + si with e * S = col - si
-      const int si = S == 1 ? 0 : (S == 2 ? (col[c] & 1) : col[c] % S);
-      const unsigned cidx = (unsigned)(8 * (col[c] - si) + (int)(k & 7) * S + si);
-      const unsigned long long key = ((unsigned long long)(k >> 3) << 32) | cidx;
-      if (valid[c] && key < best) best = key;
-    }
-    const unsigned err = (unsigned)(best >> 32);  // 0xffffffff: no valid column
-    const unsigned werr = __reduce_min_sync(0xffffffffu, err);
-    const unsigned widx = __reduce_min_sync(0xffffffffu, err == werr ? (unsigned)best : 0xffffffffu);
-    if (lane == 0 && werr != 0xffffffffu)
-      atomicMin(&keys[m], ((unsigned long long)werr << 32) | widx);
-  }
+       u += (long long)gridDim.x * kWarps)
+    fix_unit<N, fix_cpl(N)>(F, s_prefix, n_jobs, u, lane);
   if (t_end && tid == 0) atomicMax(t_end, global_ns());
 }
 
@@ -1297,7 +1342,8 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
       reinterpret_cast<const TcDims*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes + kUpReachBytes),
       (long long)kTileN * T.kpad, c->sm_count, d_hist,
       reinterpret_cast<const long long*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes),
-      fix_cols(L.n), c->roff.as<int32_t>(), d_plan, c->fix_jobs.as<int4>(),
+      c->fix_fused ? fix_cols_fused(L.n) : fix_cols(L.n), c->roff.as<int32_t>(), d_plan,
+      c->fix_jobs.as<int4>(),
       c->fix_cols.as<long long>(), d_fplan, c->fix_rows.as<int32_t>(),
       reinterpret_cast<long long*>(d_fix_pairs)));
   c->stats.kernel_launches += 1;
@@ -1324,6 +1370,20 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   // measured: the per-unit recompute wins only for short K
   prm.deferred = c->tc_deferred >= 0 ? c->tc_deferred : (T.kpad <= 128 ? 1 : 0);
   prm.g1 = c->tc_g1 >= 0 ? c->tc_g1 : 0;
+  prm.fix_fused = c->fix_fused ? 1 : 0;
+  prm.fix.qbase = L.qbase.as<int16_t>();
+  prm.fix.a_tiles = c->a_tiles.as<uint8_t>();
+  prm.fix.roff = c->roff.as<int32_t>();
+  prm.fix.jobs = c->fix_jobs.as<int4>();
+  prm.fix.prefix = c->fix_cols.as<long long>();
+  prm.fix.fplan = d_fplan;
+  prm.fix.sorted_ranges = c->fix_rows.as<int32_t>();
+  prm.fix.list_low = T.reach_low.as<int32_t>();
+  prm.fix.list_high = T.reach_high.as<int32_t>();
+  prm.fix.keys = reinterpret_cast<unsigned long long*>(d_keys);
+  prm.fix.S = L.s_count;
+  prm.fix.kpad = T.kpad;
+  prm.fix.n = L.n;
   const uint32_t smem = smem_bytes(prm);
   if (!c->tc_attr_set) {
     FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1335,8 +1395,13 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   c->stats.kernel_launches += 1;
 
   // ---- clamp corrections (exact kernel on clamp-active pairs), planned above ----
-  // With a jobs stream they run concurrently with the contraction (both only
-  // atomicMin into the same keys) on the SMs the contraction leaves idle.
+  // Fused (FC_FIX_FUSED=1): the contraction's epilogue warps take them from a work
+  // counter once their share is done.  Otherwise a separate kernel, on the
+  // jobs stream when given (both only atomicMin into the same keys).
+  if (c->fix_fused) {
+    if (jobs_stream) FC_CUDA(c, cudaEventRecord(ev_jobs, c->stream));
+    return FC_OK;
+  }
   cudaStream_t main = c->stream;
   if (jobs_stream) {
     FC_CUDA(c, cudaEventRecord(ev_plan, main));
@@ -1344,20 +1409,13 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
     c->stream = jobs_stream;
   }
   {
-    auto* keys = reinterpret_cast<unsigned long long*>(d_keys);
     const unsigned grid = (unsigned)(c->sm_count * (2048 / kFixThreads));
-#define FC_LAUNCH_FIX(NN)                                                                          \
-  fix_pairs_kernel<NN><<<grid, kFixThreads, 0, c->stream>>>(                                      \
-      L.qbase.as<int16_t>(), L.s_count, c->a_tiles.as<uint8_t>(), T.kpad,                         \
-      c->roff.as<int32_t>(), c->fix_jobs.as<int4>(), c->fix_cols.as<long long>(), d_fplan,       \
-      c->fix_rows.as<int32_t>(), T.reach_low.as<int32_t>(), T.reach_high.as<int32_t>(), keys,    \
-      d_time ? d_time + 2 : nullptr)
+    unsigned long long* t_end = d_time ? d_time + 2 : nullptr;
     switch (L.n) {
-      case 256: FC_LAUNCH_FIX(256); break;
-      case 64: FC_LAUNCH_FIX(64); break;
-      default: FC_LAUNCH_FIX(16); break;
+      case 256: fix_pairs_kernel<256><<<grid, kFixThreads, 0, c->stream>>>(prm.fix, t_end); break;
+      case 64: fix_pairs_kernel<64><<<grid, kFixThreads, 0, c->stream>>>(prm.fix, t_end); break;
+      default: fix_pairs_kernel<16><<<grid, kFixThreads, 0, c->stream>>>(prm.fix, t_end); break;
     }
-#undef FC_LAUNCH_FIX
     const cudaError_t err = cudaGetLastError();
     c->stream = main;
     if (err != cudaSuccess) return set_error(c, FC_ERR_CUDA, cudaGetErrorString(err));
