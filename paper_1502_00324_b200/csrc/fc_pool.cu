@@ -25,8 +25,11 @@ namespace fcb {
 
 namespace {
 
-constexpr int kEntWarps = 6;       // warps per block of the entropy kernel (2 blocks / SM)
-constexpr int kEntBlocksPerSm = 2; // shared-memory bound (16 KB of histograms per warp)
+// Entropy kernel geometry per histogram width: u16 counts (windows of up to
+// 32x32 = 1024 pixels, 16 KB of histograms per warp) or u8 counts (windows of
+// up to 8x8 = 64 pixels, 8 KB per warp: twice the resident warps).
+constexpr int kEntBlocksPerSm = 2;  // shared-memory bound
+template <int BPW> __host__ __device__ constexpr int ent_warps() { return BPW == 2 ? 6 : 12; }
 constexpr int kLutWords = 4 + 16 + 64 + 256 + 1024;  // the four [0, p*log(p)...] LUTs in smem
 
 __device__ __forceinline__ uint64_t entropy_key(double h) {
@@ -47,8 +50,9 @@ struct EntLevel {
   int* sel_count;
 };
 struct EntParams {
-  EntLevel lv[4];
-  const double* lut[4];  // device LUTs for n = 16, 64, 256, 1024
+  EntLevel lv[4];        // this launch's levels (n_levels of them)
+  const double* lut[4];  // their device LUTs
+  int n_levels;
   int total_tasks;
 };
 
@@ -81,20 +85,23 @@ __device__ __forceinline__ void sts_u32_ordered(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-// Lane-private histogram: word (v >> 1) * 32 + lane packs the u16 counts of
-// bins v & ~1 (low half) and v | 1 (high half), so every access of a warp
-// hits bank = lane (conflict-free).  Updates are shared-memory reductions
-// without return (pipelined); a removal never borrows across halves because
-// only counted pixels are removed.  hw = shared address of this lane's word 0.
-template <int D>
+// Lane-private histogram of BPW bins per 32-bit word: word (v / BPW) * 32 +
+// lane packs the counts of bins BPW*(v/BPW) .. +BPW-1 (u16 pairs or u8
+// quads, low bin in the low bits), so every access of a warp hits bank =
+// lane (conflict-free).  Updates are shared-memory reductions without return
+// (pipelined); sign = 1 adds a pixel, 0xffffffff removes one (a removal never
+// borrows across fields: only counted pixels are removed).  hw = shared
+// address of this lane's word 0.
+template <int D, int BPW>
 __device__ __forceinline__ void hist_rows(uint32_t hw, const uint8_t* __restrict__ img, int width,
-                                          int x, int r0, int r1, uint32_t lo, uint32_t hi) {
+                                          int x, int r0, int r1, uint32_t sign) {
+  constexpr int kShift = 32 / BPW;
   for (int r = r0; r < r1; ++r) {
     const uint8_t* row = img + (int64_t)r * width + x;
 #pragma unroll 8
     for (int k = 0; k < D; ++k) {
       const uint32_t v = __ldg(row + k);
-      reds_add(hw + (v >> 1) * 128, (v & 1) ? hi : lo);
+      reds_add(hw + (v / BPW) * 128, sign << (kShift * (v % BPW)));
     }
   }
 }
@@ -107,7 +114,9 @@ __device__ __forceinline__ void hist_rows(uint32_t hw, const uint8_t* __restrict
 // 32 windows of the warp is skipped with a warp-uniform branch: neighbouring
 // windows share most pixels, so typically 2/3 of the groups are skipped.
 // Must be called by the full warp (inactive lanes hold an all-zero histogram).
+template <int BPW>
 __device__ __forceinline__ double window_entropy(uint32_t hw, uint32_t lut) {
+  constexpr int kWpg = 8 / BPW;  // words per 8-bin group
   double half_sum[2];
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
@@ -116,15 +125,25 @@ __device__ __forceinline__ double window_entropy(uint32_t hw, uint32_t lut) {
     for (int j = 0; j < 8; ++j) acc[j] = 0.0;
 #pragma unroll
     for (int g = 0; g < 16; ++g) {
-      uint32_t w[4];
+      uint32_t w[kWpg];
+      uint32_t any = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) w[q] = lds_u32_ordered(hw + (half * 64 + g * 4 + q) * 128);
-      if (__any_sync(0xffffffffu, (w[0] | w[1] | w[2] | w[3]) != 0u)) {
+      for (int q = 0; q < kWpg; ++q) {
+        w[q] = lds_u32_ordered(hw + ((half * 16 + g) * kWpg + q) * 128);
+        any |= w[q];
+      }
+      if (__any_sync(0xffffffffu, any != 0u)) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          // counts <= 1024 < 2^13, so (w >> 13) == 8 * (w >> 16)
-          acc[2 * q] = acc[2 * q] + lds_f64(lut + ((w[q] & 0xffffu) << 3));
-          acc[2 * q + 1] = acc[2 * q + 1] + lds_f64(lut + (w[q] >> 13));
+        for (int q = 0; q < kWpg; ++q) {
+          if constexpr (BPW == 2) {
+            // counts <= 1024 < 2^13, so (w >> 13) == 8 * (w >> 16)
+            acc[2 * q] = acc[2 * q] + lds_f64(lut + ((w[q] & 0xffffu) << 3));
+            acc[2 * q + 1] = acc[2 * q + 1] + lds_f64(lut + (w[q] >> 13));
+          } else {
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              acc[4 * q + b] = acc[4 * q + b] + lds_f64(lut + (((w[q] >> (8 * b)) & 0xffu) << 3));
+          }
         }
       }
     }
@@ -137,7 +156,7 @@ __device__ __forceinline__ double window_entropy(uint32_t hw, uint32_t lut) {
 // one level.  Each lane keeps its window's 256-bin histogram and slides it
 // down by `stride` rows (remove the rows that leave, add the rows that
 // enter), so a window costs 2*stride*D updates instead of D*D.
-template <int D>
+template <int D, int BPW>
 __device__ __forceinline__ void entropy_task(const EntLevel& L, const uint8_t* __restrict__ img,
                                              int width, int task, uint32_t h, uint32_t lut,
                                              int lane) {
@@ -149,16 +168,17 @@ __device__ __forceinline__ void entropy_task(const EntLevel& L, const uint8_t* _
   const int wy1 = min(wy0 + L.rows, L.ny);
   const int s = L.stride;
   const int x = wx * s;
+  static_assert(BPW == 2 || D * D < 256, "u8 histogram counts");
 #pragma unroll 8
-  for (int b = 0; b < 128; ++b) sts_u32_ordered(h + b * 128, 0u);
-  if (active) hist_rows<D>(h, img, width, x, wy0 * s, wy0 * s + D, 1u, 0x10000u);
+  for (int b = 0; b < 256 / BPW; ++b) sts_u32_ordered(h + b * 128, 0u);
+  if (active) hist_rows<D, BPW>(h, img, width, x, wy0 * s, wy0 * s + D, 1u);
   for (int wy = wy0; wy < wy1; ++wy) {
     if (wy > wy0 && active) {
       const int yp = (wy - 1) * s, yn = wy * s;
-      hist_rows<D>(h, img, width, x, yp, yp + min(s, D), 0xffffffffu, 0xffff0000u);
-      hist_rows<D>(h, img, width, x, max(yp + D, yn), yn + D, 1u, 0x10000u);
+      hist_rows<D, BPW>(h, img, width, x, yp, yp + min(s, D), 0xffffffffu);
+      hist_rows<D, BPW>(h, img, width, x, max(yp + D, yn), yn + D, 1u);
     }
-    const double H = window_entropy(h, lut);  // whole warp (see window_entropy)
+    const double H = window_entropy<BPW>(h, lut);  // whole warp (see window_entropy)
     const int64_t w = (int64_t)wy * L.nx + wx;
     if (L.mode == 0) {
       if (active) {
@@ -184,38 +204,43 @@ __device__ __forceinline__ void entropy_task(const EntLevel& L, const uint8_t* _
   }
 }
 
-__global__ void __launch_bounds__(kEntWarps * 32)
+// One launch per histogram width: BPW = 2 for the 32x32 / 16x16 windows,
+// BPW = 4 for the 8x8 / 4x4 windows (P holds only the launch's levels).
+template <int BPW>
+__global__ void __launch_bounds__(ent_warps<BPW>() * 32)
 entropy_all_kernel(const uint8_t* __restrict__ img, int width, EntParams P) {
+  constexpr int kWarps = ent_warps<BPW>();
   extern __shared__ __align__(16) uint8_t ent_smem[];
   double* lut_s = reinterpret_cast<double*>(ent_smem);
   uint32_t* hist_all = reinterpret_cast<uint32_t*>(ent_smem + kLutWords * 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int l = 0; l < 4; ++l) {
+  for (int l = 0; l < P.n_levels; ++l) {
     const int n = P.lv[l].D * P.lv[l].D;
     for (int i = threadIdx.x; i <= n; i += blockDim.x)
       lut_s[P.lv[l].lut_off + i] = i ? P.lut[l][i - 1] : 0.0;
   }
   __syncthreads();
-  const uint32_t h = opaque_u32(smem_addr(hist_all + warp * (128 * 32) + lane));
+  const uint32_t h = opaque_u32(smem_addr(hist_all + warp * ((256 / BPW) * 32) + lane));
   const uint32_t lut_base = opaque_u32(smem_addr(lut_s));
-  for (int task = blockIdx.x * kEntWarps + warp; task < P.total_tasks;
-       task += gridDim.x * kEntWarps) {
+  for (int task = blockIdx.x * kWarps + warp; task < P.total_tasks; task += gridDim.x * kWarps) {
     int l = 0;
 #pragma unroll
     for (int k = 1; k < 4; ++k)
-      if (task >= P.lv[k].task_begin) l = k;
+      if (k < P.n_levels && task >= P.lv[k].task_begin) l = k;
     const EntLevel& L = P.lv[l];
     const uint32_t lut = lut_base + L.lut_off * 8;
-    switch (L.D) {
-      case 32: entropy_task<32>(L, img, width, task, h, lut, lane); break;
-      case 16: entropy_task<16>(L, img, width, task, h, lut, lane); break;
-      case 8: entropy_task<8>(L, img, width, task, h, lut, lane); break;
-      default: entropy_task<4>(L, img, width, task, h, lut, lane); break;
+    if constexpr (BPW == 2) {
+      if (L.D == 32) entropy_task<32, 2>(L, img, width, task, h, lut, lane);
+      else entropy_task<16, 2>(L, img, width, task, h, lut, lane);
+    } else {
+      if (L.D == 8) entropy_task<8, 4>(L, img, width, task, h, lut, lane);
+      else entropy_task<4, 4>(L, img, width, task, h, lut, lane);
     }
   }
 }
 
-constexpr int kEntSmem = kLutWords * 8 + kEntWarps * 128 * 32 * 4;
+template <int BPW>
+__host__ __device__ constexpr int ent_smem() { return kLutWords * 8 + ent_warps<BPW>() * (256 / BPW) * 32 * 4; }
 
 // ---- rank sort of the threshold survivors: (key asc, window asc) ----
 // chunk size: 2048 elements (1024 threads); 512 with FC_POOL_CHUNK=512
@@ -634,7 +659,6 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
   int nx_l[kLevels], ny_l[kLevels], any_tau = 0;
   // ---- phase 1: every window's entropy, all levels in one launch ----
   EntParams P{};
-  int tasks = 0;
   int lut_off = 0;
   for (int li = 0; li < kLevels; ++li) {
     Level& L = c->lv[li];
@@ -662,7 +686,6 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     E.nx = nx;
     E.ny = ny;
     E.strips_x = (nx + 31) / 32;
-    E.task_begin = tasks;
     E.lut_off = lut_off;
     E.mode = use_tau[li] ? 1 : 0;
     E.tau = use_tau[li] ? taus[li] : 0.0;
@@ -671,41 +694,60 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     E.val = L.win_val.as<uint32_t>();
     E.sel_count = d_nsel + li;
     P.lut[li] = c->lut[lut_slot(D * D)].as<double>();
-    tasks += E.strips_x;  // placeholder: rows per task chosen below
     lut_off += D * D + 1;
     any_tau |= use_tau[li];
   }
-  // Rows per task: the smallest count whose tasks all fit in one wave of
-  // resident warps (every task costs about the same per row, so the kernel
-  // time is the longest task; a second partial wave would double it).
-  {
-    const int64_t resident = (int64_t)c->sm_count * kEntBlocksPerSm * kEntWarps;
+  // Two launches: u16 histograms for the 32x32 / 16x16 windows, u8 for the
+  // 8x8 / 4x4 ones (half the shared memory per warp, twice the warps).  Rows
+  // per task: the smallest count whose tasks all fit in one wave of resident
+  // warps (every task costs about the same per row, so the kernel time is the
+  // longest task; a second partial wave would double it).
+  EntParams PL[2] = {};  // [0]: D >= 16, [1]: D <= 8
+  for (int li = 0; li < kLevels; ++li) {
+    EntParams& Q = PL[P.lv[li].D >= 16 ? 0 : 1];
+    Q.lv[Q.n_levels] = P.lv[li];
+    Q.lut[Q.n_levels] = P.lut[li];
+    ++Q.n_levels;
+  }
+  for (int k = 0; k < 2; ++k) {
+    EntParams& Q = PL[k];
+    if (Q.n_levels == 0) continue;
+    const int warps = k == 0 ? ent_warps<2>() : ent_warps<4>();
+    const int64_t resident = (int64_t)c->sm_count * kEntBlocksPerSm * warps;
     int rows = 4;
     for (;; ++rows) {
       int64_t t = 0;
-      for (int li = 0; li < kLevels; ++li)
-        t += (int64_t)P.lv[li].strips_x * ((P.lv[li].ny + rows - 1) / rows);
+      for (int i = 0; i < Q.n_levels; ++i)
+        t += (int64_t)Q.lv[i].strips_x * ((Q.lv[i].ny + rows - 1) / rows);
       if (t <= resident || rows >= 1 << 20) break;
     }
-    tasks = 0;
-    for (int li = 0; li < kLevels; ++li) {
-      P.lv[li].rows = rows;
-      P.lv[li].task_begin = tasks;
-      tasks += P.lv[li].strips_x * ((P.lv[li].ny + rows - 1) / rows);
+    int nt = 0;
+    for (int i = 0; i < Q.n_levels; ++i) {
+      Q.lv[i].rows = rows;
+      Q.lv[i].task_begin = nt;
+      nt += Q.lv[i].strips_x * ((Q.lv[i].ny + rows - 1) / rows);
     }
+    Q.total_tasks = nt;
   }
-  P.total_tasks = tasks;
   trace_mark(c, "pool_begin");
   FC_CUDA(c, cudaMemsetAsync(d_nsel, 0, 4 * kLevels, c->stream));
   if (!c->ent_attr_set) {
-    FC_CUDA(c, cudaFuncSetAttribute(entropy_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kEntSmem));
+    FC_CUDA(c, cudaFuncSetAttribute(entropy_all_kernel<2>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ent_smem<2>()));
+    FC_CUDA(c, cudaFuncSetAttribute(entropy_all_kernel<4>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ent_smem<4>()));
     c->ent_attr_set = true;
   }
-  {
-    const int blocks =
-        std::max(1, std::min((tasks + kEntWarps - 1) / kEntWarps, c->sm_count * kEntBlocksPerSm));
-    entropy_all_kernel<<<blocks, kEntWarps * 32, kEntSmem, c->stream>>>(c->img_ptr, c->width, P);
+  for (int k = 0; k < 2; ++k) {
+    const EntParams& Q = PL[k];
+    if (Q.n_levels == 0) continue;
+    const int warps = k == 0 ? ent_warps<2>() : ent_warps<4>();
+    const int blocks = std::max(
+        1, std::min((Q.total_tasks + warps - 1) / warps, c->sm_count * kEntBlocksPerSm));
+    if (k == 0)
+      entropy_all_kernel<2><<<blocks, warps * 32, ent_smem<2>(), c->stream>>>(c->img_ptr, c->width, Q);
+    else
+      entropy_all_kernel<4><<<blocks, warps * 32, ent_smem<4>(), c->stream>>>(c->img_ptr, c->width, Q);
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 1;
   }
