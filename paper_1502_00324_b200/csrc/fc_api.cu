@@ -234,7 +234,7 @@ int fc_ctx_create(int device, fc_ctx** out) {
   c->sm_count = prop.multiProcessorCount;
   if (const char* t = getenv("FC_TRACE")) c->trace = atoi(t);
   if (const char* g = getenv("FC_GRAPH")) c->use_graph = atoi(g) != 0;
-  if (const char* d = getenv("FC_TC_DEBUG_MODE")) c->tc_debug_mode = atoi(d);
+  if (const char* d = getenv("FC_TC_DEBUG")) c->tc_debug_mode = atoi(d);
   if (const char* d = getenv("FC_TC_DEFERRED")) c->tc_deferred = atoi(d);
   if (const char* d = getenv("FC_TC_G1")) c->tc_g1 = atoi(d);
   if (const char* o = getenv("FC_OVERLAP")) c->overlap = atoi(o) != 0;

@@ -406,6 +406,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
         ptx::tc_fence_after();
         int va[32], vb[32];
         int m_best = kNone, gi_best = 0;
+        const int lim = improve_limit(bs.x, tinfo.x);
 #pragma unroll
         for (int wv = 0; wv < kWaves; ++wv) {
           ptx::tmem_ld32(tm + acc * kAccN + wv * 64, va);
@@ -437,18 +438,24 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
           const int m = min(__vimin3_s32(gm[0], gm[1], gm[2]),
                             __vimin3_s32(__vimin3_s32(gm[3], gm[4], gm[5]), gm[6], gm[7]));
           if constexpr (DEFERRED) {
-            // first group of this wave holding m; waves are visited in column order
-            int gi = 7;
+            // improves on earlier tiles (improve_limit) and, strictly, on the
+            // first wave of this tile; the group index is located only when
+            // some lane of the warp improves (rare once the row minima settle)
+            const bool imp = m < min(lim, m_best);
+            if (__any_sync(0xffffffffu, imp)) {
+              // first group of this wave holding m; waves are visited in column order
+              int gi = 7;
 #pragma unroll
-            for (int k = 6; k >= 0; --k) gi = (gm[k] == m) ? k : gi;
-            if (m < m_best) {
-              m_best = m;
-              gi_best = wv * 8 + gi;
+              for (int k = 6; k >= 0; --k) gi = (gm[k] == m) ? k : gi;
+              if (imp) {
+                m_best = m;
+                gi_best = wv * 8 + gi;
+              }
             }
           } else {
             // vs earlier tiles: improve_limit (ties go to the later-visited,
             // smaller columns); vs the first wave of this tile: strictly smaller
-            if (m < improve_limit(bs.x, tinfo.x) && m < m_best) {
+            if (m < lim && m < m_best) {
               // the rare improving lanes resolve the column at once
               const bool in_a = min(min(gm[0], gm[1]), min(gm[2], gm[3])) == m;
               const int j = in_a ? first_eq(va, m) : 32 + first_eq(vb, m);
@@ -458,8 +465,8 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
           }
         }
         if constexpr (DEFERRED) {
-          // branch-free: record the 8-column group, resolve at the unit end
-          if (m_best < improve_limit(bs.x, tinfo.x))
+          // record the 8-column group, resolve at the segment end
+          if (m_best != kNone)
             ptx::sts_v2(bst + r * (kBS * 8), make_int2(2 * m_best + tinfo.x, (t << kGiBits) + gi_best));
         } else {
           if (m_best != kNone) ptx::sts_v2(bst + r * (kBS * 8), make_int2(2 * m_best + tinfo.x, gi_best));
