@@ -1374,8 +1374,9 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   prm.S = L.s_count;
   prm.plan = d_plan;
   prm.tspan = d_time;
-  // measured: the per-unit recompute wins only for short K
-  prm.deferred = c->tc_deferred >= 0 ? c->tc_deferred : (T.kpad <= 128 ? 1 : 0);
+  // measured: with the cooperative per-candidate resolution the deferred
+  // epilogue also wins for long K (c4 B=16: -4%)
+  prm.deferred = c->tc_deferred >= 0 ? c->tc_deferred : 1;
   prm.g1 = c->tc_g1 >= 0 ? c->tc_g1 : 0;
   prm.fix_fused = c->fix_fused ? 1 : 0;
   prm.fix.qbase = L.qbase.as<int16_t>();
