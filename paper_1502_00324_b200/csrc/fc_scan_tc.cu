@@ -1090,14 +1090,12 @@ struct GatherBuild {
 };
 
 __global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
-  __shared__ uint8_t tile_s[8][256];
-  __shared__ uint16_t inv_s[8 * 256];  // the level's inverse isometry maps (8 x n)
+  // the staged tile and its transpose: every isometry row of A is a row of
+  // one of them, possibly read backwards (see the table below)
+  __shared__ __align__(16) uint8_t tile_s[8][256];
+  __shared__ __align__(16) uint8_t tile_t[8][256];
   pdl_enter();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (P.kpad != 0) {
-    for (int i = threadIdx.x; i < 8 * P.n; i += blockDim.x) inv_s[i] = P.inv[i];
-    __syncthreads();
-  }
   const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     P.tspan[0] = ~0ull;
@@ -1116,6 +1114,7 @@ __global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
       const int v = P.img[(int64_t)(y + r) * P.width + x + col];
       P.rtiles[m * n + p] = (uint8_t)v;
       ts[p] = (uint8_t)v;
+      tile_t[warp][col * B + r] = (uint8_t)v;
       s1 += v;
       s2 += v * v;
     }
@@ -1142,13 +1141,36 @@ __global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
   const int chunks = P.kpad / 16;
   const int kbase = P.planes * n;
   const bool real = m < M;
+  const uint8_t* tt = tile_t[warp];
   for (int it = lane; it < 8 * chunks; it += 32) {
     const int iso = it / chunks, kc = it - iso * chunks;
     const int64_t row = m * 8 + iso;
     const int64_t tile = row / kTileM;
     const int rrow = (int)(row - tile * kTileM);
     uint32_t w[4] = {0, 0, 0, 0};
-    if (real) {
+    if (real && kc * 16 < kbase) {
+      // A row (iso) position k = r*B + c holds t[i][j] with iso(i, j) = (r, c)
+      // (image.py:140-155): output row r is row r or b-r of the tile or of its
+      // transpose, forward or reversed:
+      //   iso:       0  1  2  3  4  5  6  7
+      //   transpose: 0  1  0  1  0  1  0  1
+      //   flip row:  0  1  1  0  0  0  1  1
+      //   reverse:   0  0  1  1  1  0  0  1
+      const bool tr = iso & 1;
+      const bool flip = (0xC6u >> iso) & 1u;
+      const bool rev = (0x9Cu >> iso) & 1u;
+      const uint8_t* src = tr ? tt : ts;
+      const int kk0 = (kc * 16) % n;  // the second plane repeats the first
+      const int per = B / 4;          // words per tile row (B >= 4)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = (kk0 + 4 * q) / B;      // output row of this word
+        const int cw = ((kk0 + 4 * q) % B) / 4;  // word within the row
+        const int sr = flip ? B - 1 - r : r;
+        const uint32_t* rw = reinterpret_cast<const uint32_t*>(src + sr * B);
+        w[q] = rev ? __byte_perm(rw[per - 1 - cw], 0, 0x0123) : rw[cw];
+      }
+    } else if (real) {
 #pragma unroll
       for (int b4 = 0; b4 < 4; ++b4) {
         uint32_t word = 0;
@@ -1156,10 +1178,7 @@ __global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
         for (int bb = 0; bb < 4; ++bb) {
           const int k = kc * 16 + b4 * 4 + bb;
           uint32_t v = 0;
-          if (k < kbase) {
-            const int kk = k < n ? k : k - n;
-            v = ts[inv_s[iso * n + kk]];
-          } else {
+          {
             const int sl = k - kbase;
             if (sl < P.m_digits) v = 255;
             else if (sl < P.m_digits + 2) v = 1;
