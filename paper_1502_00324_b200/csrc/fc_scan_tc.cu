@@ -787,6 +787,27 @@ __global__ void build_b_kernel(const int16_t* __restrict__ qbase, int n, int kpa
   const int q1a = min(max(st.x, -127), 127);
   const int16_t* q = qbase + col * n;
   uint32_t w[4];
+  if (kc * 16 < kbase) {
+    // 16 q values at once (int16 pairs): -q, or its two s8 planes
+    // b = clamp(-q, -127, 127) and -q - b; the low byte of each int16 is the s8
+    const int kk0 = (kc * 16) % n;  // the second plane repeats the pixels
+    const uint4 qa = __ldg(reinterpret_cast<const uint4*>(q + kk0));
+    const uint4 qb = __ldg(reinterpret_cast<const uint4*>(q + kk0 + 8));
+    const uint32_t qw[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t neg = __vneg2(qw[i]);
+      if (planes == 1) {
+        v[i] = neg;
+      } else {
+        const uint32_t lo = __vmins2(__vmaxs2(neg, 0xff81ff81u), 0x007f007fu);  // clamp to +-127
+        v[i] = kc * 16 < n ? lo : __vsub2(neg, lo);
+      }
+    }
+#pragma unroll
+    for (int b4 = 0; b4 < 4; ++b4) w[b4] = __byte_perm(v[2 * b4], v[2 * b4 + 1], 0x6420);
+  } else {
 #pragma unroll
   for (int b4 = 0; b4 < 4; ++b4) {
     uint32_t word = 0;
@@ -794,16 +815,7 @@ __global__ void build_b_kernel(const int16_t* __restrict__ qbase, int n, int kpa
     for (int bb = 0; bb < 4; ++bb) {
       const int k = kc * 16 + b4 * 4 + bb;
       int v = 0;
-      if (k < kbase) {
-        if (planes == 1) {
-          v = -q[k];
-        } else if (k < n) {
-          v = min(max(-(int)q[k], -127), 127);
-        } else {
-          const int x = -(int)q[k - n];
-          v = x - min(max(x, -127), 127);
-        }
-      } else {
+      {
         const int sl = k - kbase;
         if (sl < m_digits) v = min(max(Q - 127 * sl, 0), 127);
         else if (sl == m_digits) v = r1;
@@ -814,6 +826,7 @@ __global__ void build_b_kernel(const int16_t* __restrict__ qbase, int n, int kpa
       word |= (uint32_t)(uint8_t)(int8_t)v << (8 * bb);
     }
     w[b4] = word;
+  }
   }
   int8_t* dst = b_tiles + tile * ((int64_t)kTileN * kpad) + (int64_t)kc * (kTileN * 16) +
                 (cc >> 3) * 128 + (cc & 7) * 16;
