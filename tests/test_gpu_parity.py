@@ -347,3 +347,54 @@ def test_device_decoder_golden_cases(tag):
     assert np.array_equal(got.pixels, want.pixels)
     p, ref = fc.psnr(fc.GrayImage(g[f"image_{tag}"]), got), float(g[f"psnr_{tag}"])
     assert p == ref or abs(p - ref) < 0.01
+
+
+@pytest.mark.parametrize("name", ["c4"])
+def test_full_size_encode_properties(name):
+    """BASELINE-size encode (c4: 2048^2, three levels, ~100k-column pools per
+    level) checked through size-independent properties, since the CPU oracle
+    cannot run the whole encode in a test:
+    * one collage pass applied to the ORIGINAL image reproduces the reported
+      collage SSD (the reference's test_codec.py:77-86 property);
+    * a random sample of leaves, re-matched by the oracle's C scan against the
+      device pool, gives the same (error, domain, isometry, s, offset)."""
+    from paper_1502_00324_b200.codec import _collage_pass, _plans
+    from paper_1502_00324_b200.stream import iter_leaves
+
+    wl = W.WORKLOADS[name]
+    img = wl.image(0)
+    taus = tuple(None if one else t for one, t in zip(wl.cap_one, wl.taus))
+    caps = tuple(1 if one else 2**31 - 1 for one in wl.cap_one)
+    params = fc.PoolParams(pool_cap=2**31 - 1, strides=wl.strides, level_caps=caps,
+                           entropy_thresholds=taus)
+    cfg = fc.EncoderConfig(pool=params, thresholds=wl.thresholds)
+    ctx = _native.Context(0)
+    stream, report = fc.encode(fc.GrayImage(img), cfg, context=ctx)
+    # (1) collage pass on the original == the sum of the leaf errors
+    out = _collage_pass(img, _plans(stream), True)
+    ssd = int(((out.astype(np.int64) - img.astype(np.int64)) ** 2).sum())
+    assert ssd == report.collage_ssd
+    # (2) sampled leaves against the oracle's exhaustive scan over the device pool
+    pool = fc.build_pool(fc.GrayImage(img), params, context=ctx)  # same pool, rebuilt
+    leaves = iter_leaves(stream)
+    rng = np.random.default_rng(7)
+    pick = rng.choice(len(leaves), size=min(48, len(leaves)), replace=False)
+    by_level = {}
+    for i in pick:
+        rec, x, y, side = leaves[int(i)]
+        by_level.setdefault(rec.step, []).append((rec, x, y, side))
+    policy = cfg.policy
+    for level, items in sorted(by_level.items()):
+        side = fc.pool.LEVEL_RANGE_SIDES[level - 1]
+        E = pool.size(level)
+        ent, tiles, means, _ = ctx.pool_entries(level, E, side)
+        svals = np.asarray(policy.s_set(level), dtype=np.float64)
+        q = O.candidate_operands(tiles, means, svals, False)
+        ranges = np.stack([img[y:y + side, x:x + side].reshape(-1) for _, x, y, _ in items])
+        rmeans = ranges.astype(np.int64).sum(axis=1) / (side * side)
+        err, idx = O.scan_candidates(ranges.astype(np.int16), rmeans, q, means, svals, False)
+        for (rec, _, _, _), e_, i_, rm in zip(items, err, idx, rmeans):
+            e, iso, si = O.decode_index(int(i_), len(svals))
+            want = (e, iso, si, O.stored_offset(rm, svals, means, e, si, False))
+            assert (rec.domain_address, rec.isometry, rec.s_index, rec.offset) == want
+        del q
