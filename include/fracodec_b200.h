@@ -75,7 +75,11 @@ int fc_set_device_io(fc_ctx* ctx, int device_io);
  * corrections, default 1).  Range sharding: "top_begin" / "top_end" restrict
  * fc_encode to the raster slab [top_begin, top_end) of 16x16 top-level slots
  * (default 0 / -1 = all); the records are then exactly that slab's run of the
- * full depth-first record list, so per-rank slabs concatenate in rank order. */
+ * full depth-first record list, so per-rank slabs concatenate in rank order.
+ * Measured kernel variants (same results): "tc_g1" (all 16 epilogue warps
+ * drain every accumulator), "tc_deferred" (0: resolve columns at once),
+ * "fix_fused" (clamp corrections inside the contraction), "pdl"
+ * (programmatic dependent launch between the level loop's kernels). */
 int fc_set_option(fc_ctx* ctx, const char* name, int64_t value);
 
 /* terms[k-1] = (k/n) * log(k/n), k = 1..n, produced by the host's numpy so the

@@ -337,6 +337,23 @@ int fc_set_option(fc_ctx* c, const char* name, int64_t value) {
     c->top_end = value;
     return FC_OK;
   }
+  // kernel variants kept for measurement; results identical
+  if (strcmp(name, "tc_g1") == 0) {
+    c->tc_g1 = (int)value;
+    return FC_OK;
+  }
+  if (strcmp(name, "tc_deferred") == 0) {
+    c->tc_deferred = (int)value;
+    return FC_OK;
+  }
+  if (strcmp(name, "fix_fused") == 0) {
+    c->fix_fused = value != 0;
+    return FC_OK;
+  }
+  if (strcmp(name, "pdl") == 0) {
+    c->pdl = value != 0;
+    return FC_OK;
+  }
   return set_error(c, FC_ERR_ARG, std::string("unknown option ") + name);
 }
 

@@ -398,3 +398,22 @@ def test_full_size_encode_properties(name):
             want = (e, iso, si, O.stored_offset(rm, svals, means, e, si, False))
             assert (rec.domain_address, rec.isometry, rec.s_index, rec.offset) == want
         del q
+
+
+@pytest.mark.parametrize("option,value", [("tc_g1", 1), ("tc_deferred", 0), ("fix_fused", 1),
+                                          ("pdl", 1), ("overlap", 0), ("graph", 0)])
+def test_kernel_variants_give_identical_streams(option, value):
+    """Every execution variant kept for measurement produces the same c2 stream."""
+    g = load_golden("encode_c2.npz")
+    img = g["image_c2"]
+    caps = tuple(int(v) for v in g["caps_c2"])
+    strides = tuple(int(v) for v in g["strides_c2"])
+    thr = tuple(float(v) for v in g["thresholds_c2"])
+    params = fc.PoolParams(pool_cap=max(caps), strides=strides, level_caps=caps)
+    cfg = fc.EncoderConfig(pool=params, thresholds=thr, path="tensor")
+    ctx = _native.Context(0)
+    ctx.set_option(option, value)
+    for _ in range(2):
+        stream, report = fc.encode(fc.GrayImage(img), cfg, context=ctx)
+        assert fc.serialize(stream) == g["bytes_c2"].tobytes()
+        assert report.collage_ssd == int(g["collage_c2"])
