@@ -31,16 +31,20 @@ namespace {
 
 constexpr int kTop = 16;  // codec.py:114 top-level range side
 
-// The encoded top-level slots are the raster slab [first, first + n_top)
-// (all of them unless the context restricts it, fc_set_option "top_begin" /
-// "top_end"); depth-first codes are local to the slab.
-__global__ void top_origins_kernel(int nxt, int32_t first, int32_t n_top,
+// Encode start in one launch: the counter block zeroed (level-1 range count
+// = n_top), the leaf flags cleared, and the top-level ranges.  The encoded
+// top-level slots are the raster slab [first, first + n_top) (all of them
+// unless the context restricts it, fc_set_option "top_begin" / "top_end");
+// depth-first codes are local to the slab.
+__global__ void encode_init_kernel(int nxt, int32_t first, int32_t n_top, int64_t n_codes,
                                    int32_t* __restrict__ origins, int32_t* __restrict__ codes,
-                                   int32_t* __restrict__ d_M) {
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0) *d_M = n_top;
+                                   int32_t* __restrict__ d_count, int count_words,
+                                   int32_t* __restrict__ leaf_flag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count_words) d_count[i] = i == 0 ? n_top : 0;
+  if (i < n_codes) leaf_flag[i] = 0;
   if (i >= n_top) return;
-  const int32_t gi = first + i;
+  const int32_t gi = first + (int32_t)i;
   const int32_t ty = gi / nxt, tx = gi - ty * nxt;
   origins[2 * i] = tx * kTop;
   origins[2 * i + 1] = ty * kTop;
@@ -224,13 +228,15 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   int32_t* d_count = c->enc_count.as<int32_t>();
   int32_t* d_hist = reinterpret_cast<int32_t*>(c->enc_count.as<uint8_t>() + kEncHistOff);
   int32_t* h_rb = c->readback.as<int32_t>();
-  FC_CUDA(c, cudaMemsetAsync(c->leaf_flag.ptr, 0, n_codes * 4, c->stream));
-  FC_CUDA(c, cudaMemsetAsync(d_count, 0, kEncBytes, c->stream));  // counters, pairs, spans, hists
-  top_origins_kernel<<<blocks_for(n_top), 256, 0, c->stream>>>(
-      nxt, (int32_t)top_first, (int32_t)n_top, c->enc_orig[0].as<int32_t>(),
-      c->enc_code[0].as<int32_t>(), d_count);
-  FC_CUDA(c, cudaGetLastError());
-  c->total_launches += 1;
+  auto launch_init = [&]() -> int {  // first operation of the encode body
+    const int64_t work = std::max<int64_t>(n_codes, kEncBytes / 4);
+    encode_init_kernel<<<blocks_for(work), 256, 0, c->stream>>>(
+        nxt, (int32_t)top_first, (int32_t)n_top, n_codes, c->enc_orig[0].as<int32_t>(),
+        c->enc_code[0].as<int32_t>(), d_count, kEncBytes / 4, c->leaf_flag.as<int32_t>());
+    FC_CUDA(c, cudaGetLastError());
+    c->total_launches += 1;
+    return FC_OK;
+  };
 
   int64_t* d_fix = reinterpret_cast<int64_t*>(c->enc_count.as<uint8_t>() + kEncFixOff);
   auto* d_time = reinterpret_cast<unsigned long long*>(c->enc_count.as<uint8_t>() + kEncTimeOff);
@@ -353,6 +359,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     c->capturing = true;
   }
   const int body_rc = reuse ? FC_OK : [&]() -> int {
+  FC_TRY(launch_init());
   // fork the second stream: later levels' operand builds run there while the
   // first level is gathered and contracted
   const bool overlap = c->overlap;

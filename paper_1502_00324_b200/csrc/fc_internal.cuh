@@ -112,6 +112,9 @@ struct Level {
   int baseline = 0;
   int s_count = 0;
   double svals[kMaxS] = {0};
+  double svals_up[kMaxS] = {0};   // the values last uploaded to svals_d
+  int svals_up_count = -1;
+  void* svals_up_ptr = nullptr;
   int path = FC_PATH_EXACT;
   DevBuf qbase;           // int16 [E*S][n] base operand (column = e*S + si)
   DevBuf svals_d;         // double [S] on the device

@@ -546,7 +546,14 @@ int prep_launch(Ctx* c, Level* const* levels, const int* stats, int count) {
     const int64_t cols = L.count * L.s_count;
     FC_CUDA(c, L.qbase.reserve(cols * L.n * 2 + 64));
     FC_CUDA(c, L.svals_d.reserve(kMaxS * 8));
-    FC_TRY(stage_h2d(c, L.svals_d.ptr, L.svals, L.s_count * 8));
+    // the s values change rarely: upload only when they (or the buffer) did
+    if (L.svals_up_ptr != L.svals_d.ptr || L.svals_up_count != L.s_count ||
+        memcmp(L.svals_up, L.svals, L.s_count * 8) != 0) {
+      FC_TRY(stage_h2d(c, L.svals_d.ptr, L.svals, L.s_count * 8));
+      memcpy(L.svals_up, L.svals, L.s_count * 8);
+      L.svals_up_count = L.s_count;
+      L.svals_up_ptr = L.svals_d.ptr;
+    }
     TcOperands& T = L.tc;
     if (stats[i]) {
       FC_CUDA(c, T.col_stats.reserve(cols * 16 + 16));
