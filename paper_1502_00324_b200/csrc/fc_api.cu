@@ -272,7 +272,6 @@ void fc_ctx_destroy(fc_ctx* c) {
   c->readback.release();
   c->pool_rb.release();
   c->prep_dev.release();
-  c->chunk_odd.release();
   c->coords_pinned.release();
   c->rec_pinned.release();
   if (c->enc_ev_ready)

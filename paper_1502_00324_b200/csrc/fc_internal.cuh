@@ -159,7 +159,7 @@ struct Ctx {
   size_t up_off = 0;
   PinnedBuf readback;     // small D2H results (counts, histograms)
   PinnedBuf pool_rb;      // threshold-survivor counts per level
-  DevBuf prep_dev, chunk_odd;  // per-level qmin/qmax histograms + q2max + odd total; chunk counts
+  DevBuf prep_dev;  // per-level qmin/qmax histograms + q2max + odd total, then chunk parity counts
   PinnedBuf coords_pinned;  // pool origins of all levels, fetched with fc_encode's last sync
   int64_t coords_off[kLevels] = {0, 0, 0, 0};
   bool coords_valid = false;
@@ -181,6 +181,7 @@ struct Ctx {
   bool overlap = true;                 // FC_OVERLAP=0 / option "overlap": single stream
   int64_t enc_summary[5] = {0, 0, 0, 0, 0};  // leaf counts per step, collage SSD
   int64_t top_begin = 0, top_end = -1;       // fc_encode's top-level slab (-1: to the end)
+  bool nsel_clean = false;                   // pool survivor counters already zero
   DevBuf dec_img, dec_leaves, dec_state, dec_svals;  // device decoder (fc_decode.cu)
   bool fix_fused = false;              // FC_FIX_FUSED=1: clamp corrections inside the contraction (measured 2% slower on c2)
   bool pdl = false;                    // FC_PDL=1: programmatic dependent launches (measured no gain)

@@ -285,9 +285,11 @@ struct KeyIdxLess {
 };
 
 template <int kChunk>
-__global__ void __launch_bounds__(kChunk / 2) chunk_sort_kernel(SortParams P) {
+__global__ void __launch_bounds__(kChunk / 2) chunk_sort_kernel(SortParams P, int32_t* rank) {
   using Sorter = cub::BlockMergeSort<KeyIdx, kChunk / 2, 2>;
   __shared__ typename Sorter::TempStorage tmp;
+  // this chunk's rank accumulators, filled by chunk_pair_rank_kernel next
+  for (int i = threadIdx.x; i < kChunk; i += blockDim.x) rank[blockIdx.x * kChunk + i] = 0;
   const int l = sort_level_of(P, blockIdx.x);
   const SortLevel& L = P.lv[l];
   const int c = blockIdx.x - L.chunk_begin;
@@ -388,6 +390,7 @@ struct SurvLevel {
 struct SurvParams {
   SurvLevel lv[4];
   int64_t total_warps;
+  int* nsel_reset;  // the survivor counters, zeroed for the next pool build (read already)
 };
 
 __device__ __forceinline__ uint32_t load_word_guarded(const uint8_t* img, int64_t off,
@@ -496,6 +499,7 @@ __device__ __forceinline__ void survivor_rows(const SurvLevel& L, const uint8_t*
 __global__ void __launch_bounds__(256) survivors_all_kernel(const uint8_t* __restrict__ img,
                                                             int width, int64_t img_bytes,
                                                             SurvParams P) {
+  if (blockIdx.x == 0 && threadIdx.x < 4 && P.nsel_reset) P.nsel_reset[threadIdx.x] = 0;
   __shared__ uint32_t xy_s[8 * 8];  // 8 warps x up to 8 survivors per warp
   __shared__ uint32_t stage_s[8][32 * stage_words<32>()];  // per warp: 32 rows of a window
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -730,7 +734,10 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     Q.total_tasks = nt;
   }
   trace_mark(c, "pool_begin");
-  FC_CUDA(c, cudaMemsetAsync(d_nsel, 0, 4 * kLevels, c->stream));
+  // the survivor counters are zero here: cleared once at allocation, then by
+  // the previous build's survivors kernel after the host read them
+  if (!c->nsel_clean) FC_CUDA(c, cudaMemsetAsync(d_nsel, 0, 4 * kLevels, c->stream));
+  c->nsel_clean = false;
   if (!c->ent_attr_set) {
     FC_CUDA(c, cudaFuncSetAttribute(entropy_all_kernel<2>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, ent_smem<2>()));
@@ -848,16 +855,15 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
       }
       for (int k = SP.n_levels; k < 4; ++k) RL[k].pair_begin = 1 << 30;
       FC_CUDA(c, c->pool_rank.reserve((size_t)chunks * chunk * 4));
-      FC_CUDA(c, cudaMemsetAsync(c->pool_rank.ptr, 0, (size_t)chunks * chunk * 4, c->stream));
       int32_t* rank = c->pool_rank.as<int32_t>();
       if (chunk == kChunkSmall) {
-        chunk_sort_kernel<kChunkSmall><<<chunks, kChunkSmall / 2, 0, c->stream>>>(SP);
+        chunk_sort_kernel<kChunkSmall><<<chunks, kChunkSmall / 2, 0, c->stream>>>(SP, rank);
         chunk_pair_rank_kernel<kChunkSmall><<<pairs, kChunkSmall / 2, 0, c->stream>>>(
             SP, RL[0], RL[1], RL[2], RL[3], rank);
         rank_scatter_kernel<kChunkSmall>
             <<<chunks * (kChunkSmall / 256), 256, 0, c->stream>>>(SP, rank);
       } else {
-        chunk_sort_kernel<kChunk><<<chunks, kChunk / 2, 0, c->stream>>>(SP);
+        chunk_sort_kernel<kChunk><<<chunks, kChunk / 2, 0, c->stream>>>(SP, rank);
         chunk_pair_rank_kernel<kChunk><<<pairs, kChunk / 2, 0, c->stream>>>(SP, RL[0], RL[1], RL[2],
                                                                            RL[3], rank);
         rank_scatter_kernel<kChunk><<<chunks * (kChunk / 256), 256, 0, c->stream>>>(SP, rank);
@@ -903,11 +909,13 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     out_sizes[li] = E;
   }
   SV.total_warps = swarps;
+  SV.nsel_reset = d_nsel;
   if (swarps > 0) {
     survivors_all_kernel<<<(unsigned)((swarps * 32 + 255) / 256), 256, 0, c->stream>>>(
         c->img_ptr, c->width, (int64_t)c->width * c->height, SV);
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 1;
+    c->nsel_clean = true;
   }
   trace_mark(c, "pool_launched");
   return FC_OK;

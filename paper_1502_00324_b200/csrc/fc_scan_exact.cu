@@ -538,8 +538,9 @@ int prep_launch(Ctx* c, Level* const* levels, const int* stats, int count) {
   int64_t chunk_total = 0;
   for (int i = 0; i < count; ++i)
     if (stats[i]) chunk_total += (levels[i]->count * levels[i]->s_count + 1023) / 1024;
-  FC_CUDA(c, c->prep_dev.reserve(kLevels * kTcHistWords * 4));
-  FC_CUDA(c, c->chunk_odd.reserve(chunk_total * 4 + 64));
+  // one buffer (one memset): the levels' histograms, then the chunk parity counts
+  FC_CUDA(c, c->prep_dev.reserve(kLevels * kTcHistWords * 4 + chunk_total * 4 + 64));
+  int32_t* chunk_odd = c->prep_dev.as<int32_t>() + kLevels * kTcHistWords;
   for (int i = 0; i < count; ++i) {
     Level& L = *levels[i];
     const int li = (int)(&L - c->lv);
@@ -570,7 +571,7 @@ int prep_launch(Ctx* c, Level* const* levels, const int* stats, int count) {
     Q.col_stats = T.col_stats.as<int4>();
     Q.odd = T.odd.as<int32_t>();
     Q.hist = c->prep_dev.as<unsigned>() + li * kTcHistWords;
-    Q.chunk_odd = c->chunk_odd.as<int32_t>() + chunks * 1;
+    Q.chunk_odd = chunk_odd + chunks;
     Q.ncols = cols;
     Q.S = L.s_count;
     Q.n = L.n;
@@ -592,8 +593,8 @@ int prep_launch(Ctx* c, Level* const* levels, const int* stats, int count) {
     }
   }
   if (any_stats) {
-    FC_CUDA(c, cudaMemsetAsync(c->prep_dev.ptr, 0, kLevels * kTcHistWords * 4, c->stream));
-    FC_CUDA(c, cudaMemsetAsync(c->chunk_odd.ptr, 0, chunk_total * 4 + 4, c->stream));
+    FC_CUDA(c, cudaMemsetAsync(c->prep_dev.ptr, 0, kLevels * kTcHistWords * 4 + chunk_total * 4 + 4,
+                               c->stream));
   }
   if (qblocks > 0) {
     qprep_multi_kernel<<<qblocks, 256, 0, c->stream>>>(QP);
