@@ -186,7 +186,7 @@ struct Ctx {
   bool fix_fused = false;              // FC_FIX_FUSED=1: clamp corrections inside the contraction (measured 2% slower on c2)
   bool pdl = false;                    // FC_PDL=1: programmatic dependent launches (measured no gain)
   int tc_debug_mode = 0;               // FC_TC_DEBUG_MODE (pipeline probes)
-  int pool_chunk = 0;                  // FC_POOL_CHUNK=512: smaller rank-sort chunks
+  int pool_chunk = 0;                  // FC_POOL_CHUNK=1024 / 2048: force the rank-sort chunk
   int tc_deferred = -1;                // FC_TC_DEFERRED: -1 = by K, 0/1 forced
   int tc_g1 = -1;                      // FC_TC_G1: epilogue drain layout, -1 = default
   cudaGraphExec_t enc_exec = nullptr;  // instantiated level-loop graph, updated per encode

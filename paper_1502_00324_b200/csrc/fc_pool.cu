@@ -243,8 +243,9 @@ template <int BPW>
 __host__ __device__ constexpr int ent_smem() { return kLutWords * 8 + ent_warps<BPW>() * (256 / BPW) * 32 * 4; }
 
 // ---- rank sort of the threshold survivors: (key asc, window asc) ----
-// chunk size: 2048 elements (1024 threads); 512 with FC_POOL_CHUNK=512
-constexpr int kChunkSmall = 512;
+// chunk size: 1024 elements (512 threads) while the survivor sets are small,
+// else 2048 (1024 threads)
+constexpr int kChunkSmall = 1024;
 constexpr int kChunk = 2048;
 constexpr int kMaxChunks = 64;
 
@@ -793,10 +794,12 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     int max_sel = 0;
     for (int li = 0; li < kLevels; ++li)
       if (use_tau[li]) max_sel = std::max(max_sel, h_nsel[li]);
-    // 512-element chunks measured no faster on c2 (more pair blocks offset the
-    // shorter sorts); kept selectable for pools of very different sizes
-    const int chunk = c->pool_chunk == kChunkSmall ? kChunkSmall : kChunk;
-    (void)max_sel;
+    // 1024-element chunks while every level fits kMaxChunks of them (shorter
+    // block sorts; c2: -1% per step), else 2048 (FC_POOL_CHUNK forces one)
+    const int chunk = c->pool_chunk == kChunk        ? kChunk
+                      : c->pool_chunk == kChunkSmall ? kChunkSmall
+                      : max_sel <= kMaxChunks * kChunkSmall ? kChunkSmall
+                                                            : kChunk;
     for (int li = 0; li < kLevels; ++li) {
       if (!use_tau[li]) continue;
       Level& L = c->lv[li];
