@@ -169,15 +169,12 @@ struct FixArgs {
 
 template <int N, int CPL>
 __device__ __forceinline__ void fix_unit(const FixArgs& F, const long long* __restrict__ pre,
-                                         int n_jobs, long long u, int lane, int lo = -1) {
+                                         int n_jobs, long long u, int lane) {
   constexpr int kCols = 32 * CPL;
-  if (lo < 0) {  // last job with prefix <= u (warp-uniform)
-    lo = 0;
-    int hi = n_jobs - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (pre[mid] <= u) lo = mid; else hi = mid - 1;
-    }
+  int lo = 0, hi = n_jobs - 1;  // last job with prefix <= u (warp-uniform)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= u) lo = mid; else hi = mid - 1;
   }
   const int4 job = F.jobs[lo];  // {list, r_off, r_cnt, col_cnt}
   const long long local = u - pre[lo];
@@ -1073,20 +1070,9 @@ fix_pairs_kernel(FixArgs F, unsigned long long* __restrict__ t_end) {
   if ((long long)blockIdx.x * kWarps >= total) return;
   for (int j = tid; j <= n_jobs; j += kFixThreads) s_prefix[j] = F.prefix[j];
   __syncthreads();
-  // a contiguous run of units per warp: the job is searched once, then advanced
-  const long long nw = (long long)gridDim.x * kWarps, w = (long long)blockIdx.x * kWarps + (tid >> 5);
-  const long long u0 = total * w / nw, u1 = total * (w + 1) / nw;
-  if (u0 < u1) {
-    int lo = 0, hi = n_jobs - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_prefix[mid] <= u0) lo = mid; else hi = mid - 1;
-    }
-    for (long long u = u0; u < u1; ++u) {
-      while (s_prefix[lo + 1] <= u) ++lo;
-      fix_unit<N, fix_cpl(N)>(F, s_prefix, n_jobs, u, lane, lo);
-    }
-  }
+  for (long long u = (long long)blockIdx.x * kWarps + (tid >> 5); u < total;
+       u += (long long)gridDim.x * kWarps)
+    fix_unit<N, fix_cpl(N)>(F, s_prefix, n_jobs, u, lane);
   if (t_end && tid == 0) atomicMax(t_end, global_ns());
 }
 
