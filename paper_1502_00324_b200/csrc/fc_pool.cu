@@ -435,8 +435,16 @@ __device__ __forceinline__ void survivor_rows(const SurvLevel& L, const uint8_t*
   for (int k = 0; k < NWR; ++k) {
     const int idx = k * 32 + lane;
     const int r = idx / NWR, wd = idx - r * NWR;  // staged row r belongs to lane r
-    const int64_t ra = __shfl_sync(0xffffffffu, a0, r);
-    const int rv = __shfl_sync(0xffffffffu, valid ? 1 : 0, r);
+    int64_t ra;
+    int rv;
+    if constexpr (PER == 1) {
+      // one survivor per warp: every lane knows row r's start without a shuffle
+      rv = valid;
+      ra = (a0 + sh / 8 + (int64_t)(r - row) * width) & ~3ll;
+    } else {
+      ra = __shfl_sync(0xffffffffu, a0, r);
+      rv = __shfl_sync(0xffffffffu, valid ? 1 : 0, r);
+    }
     stage[idx] = rv ? load_word_guarded(img, ra + 4 * wd, img_bytes) : 0u;
   }
   __syncwarp();
@@ -510,7 +518,15 @@ __global__ void __launch_bounds__(256) survivors_all_kernel(const uint8_t* __res
 #pragma unroll
   for (int k = 1; k < 4; ++k)
     if ((int64_t)blockIdx.x * 8 >= P.lv[k].warp_begin) l = k;
-  const SurvLevel& L = P.lv[l];
+  // a by-value copy selected with constant indices: the fields are then read
+  // with immediate constant-bank offsets, not an indexed load per field
+  SurvLevel L;
+  switch (l) {
+    case 0: L = P.lv[0]; break;
+    case 1: L = P.lv[1]; break;
+    case 2: L = P.lv[2]; break;
+    default: L = P.lv[3]; break;
+  }
   const int64_t wl = gw - L.warp_begin;
   const int per = 32 / (2 * L.B);
   const int64_t level_warps = (L.count + per - 1) / per;
