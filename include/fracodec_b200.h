@@ -130,6 +130,16 @@ int fc_match_level(fc_ctx* ctx, int level, const int32_t* origins_xy, int64_t co
 int fc_match_tiles(fc_ctx* ctx, int level, const uint8_t* tiles, int64_t count, int64_t* out_err,
                    int64_t* out_idx, double* out_rmean);
 
+/* Real-valued slope search of the s-histogram analysis -- bench.py:117-139
+ * _real_s_matches(tiles, basis, norms) over codec.py:164 _gather_tiles(origins),
+ * the basis being bench.py:104-114 _level_basis(pool.entries(level)).  Per
+ * origin: the minimal projection error max(rnorm - cross^2/cnorm, 0), the
+ * slope cross/cnorm of that candidate (0 for a flat domain) and its flat
+ * index e*8 + iso (first minimum), all fp64 bit-identical to the reference.
+ * Needs the pool only (no fc_level_prepare); host buffers (out_idx may be NULL). */
+int fc_real_match_level(fc_ctx* ctx, int level, const int32_t* origins_xy, int64_t count,
+                        double* out_err, double* out_s, int64_t* out_idx);
+
 /* Kernel-level drop-in for _scan.py:14 with the reference's host layout:
  * ranges int16 [M, n], rmeans f64 [M], q int16 [E*8*S, n] (isometry copies),
  * dmeans f64 [E], svals f64 [S].  Exact CUDA-core path; for parity tests. */

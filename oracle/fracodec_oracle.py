@@ -491,3 +491,80 @@ def psnr(a: np.ndarray, b: np.ndarray) -> float:
     diff = a.astype(np.int64) - b.astype(np.int64)
     err = float((diff * diff).sum()) / diff.size
     return math.inf if err == 0.0 else 10.0 * math.log10(255.0 * 255.0 / err)
+
+
+# ---------------------------------------------------------------------------
+# real-valued slope analysis (bench.py:104-193)
+# ---------------------------------------------------------------------------
+
+S_BIN_EDGES = np.round(np.arange(-0.5, 1.5 + 0.05 / 2, 0.05), 10)  # bench.py:31-32
+
+
+def level_basis(pool: OraclePoolLevel):
+    """Centered isometry variants [E*8, n] (row e*8 + iso) and their norms
+    (bench.py:104-114)."""
+    centered = pool.tiles.astype(np.float64) - pool.means[:, None, None]
+    side = centered.shape[-1]
+    rows = np.stack([apply_isometry(centered, iso) for iso in range(8)], axis=1)
+    return rows.reshape(-1, side * side), np.repeat(pool.cnorm.astype(np.float64), 8)
+
+
+def real_s_matches(tiles: np.ndarray, basis: np.ndarray, norms: np.ndarray, chunk: int = 4096):
+    """Per range tile: minimal projection error, slope and flat index of the
+    first minimum (bench.py:117-139; the reference returns the first two)."""
+    m, n = tiles.shape
+    t = tiles.astype(np.float64)
+    rc = t - (tiles.astype(np.int64).sum(axis=1) / n)[:, None]
+    rnorm = (rc * rc).sum(axis=1)
+    flat = norms == 0.0
+    safe = np.where(flat, 1.0, norms)
+    err = np.empty(m)
+    slope = np.empty(m)
+    pick_all = np.empty(m, dtype=np.int64)
+    for lo in range(0, m, chunk):
+        hi = min(m, lo + chunk)
+        cross = basis @ rc[lo:hi].T
+        gain = np.where(flat[:, None], 0.0, cross * cross / safe[:, None])
+        errs = np.maximum(rnorm[lo:hi][None, :] - gain, 0.0)
+        pick = errs.argmin(axis=0)
+        cols = np.arange(hi - lo)
+        err[lo:hi] = errs[pick, cols]
+        slope[lo:hi] = np.where(flat[pick], 0.0, cross[pick, cols] / safe[pick])
+        pick_all[lo:hi] = pick
+    return err, slope, pick_all
+
+
+def s_histogram(pixels: np.ndarray, caps, strides=DEFAULT_STRIDES, thresholds=(8.0, 8.0, 8.0)):
+    """bench.py:142-193 -> (raw_counts, clamped_counts, coded_blocks, raw_means, clamped_means)."""
+    pixels = np.ascontiguousarray(pixels, dtype=np.uint8)
+    h, w = pixels.shape
+    pools = [build_pool_level(pixels, lv, strides[lv - 1], caps[lv - 1]) for lv in (1, 2, 3, 4)]
+    bases = {}
+    s_by_level = {}
+
+    def match_level(level, origins):
+        if level not in bases:
+            bases[level] = level_basis(pools[level - 1])
+        tiles = gather_tiles(pixels, origins, LEVEL_RANGE_SIDES[level - 1])
+        errs, slopes, _ = real_s_matches(tiles, *bases[level])
+        s_by_level[level] = slopes
+        return errs
+
+    leaves = run_quadtree(w, h, thresholds, match_level)
+    coded = {1: [], 2: [], 3: [], 4: []}
+    for level, _x, _y, j in leaves:
+        coded[level].append(float(s_by_level[level][j]))
+    raw = np.zeros((4, len(S_BIN_EDGES) - 1), dtype=np.int64)
+    clamped = np.zeros_like(raw)
+    raw_means, clamped_means = [], []
+    for level in (1, 2, 3, 4):
+        v = np.array(coded[level])
+        if v.size:
+            raw[level - 1] = np.histogram(np.clip(v, S_BIN_EDGES[0], S_BIN_EDGES[-1]), bins=S_BIN_EDGES)[0]
+            clamped[level - 1] = np.histogram(np.clip(v, 0.0, 1.0), bins=S_BIN_EDGES)[0]
+            raw_means.append(float(v.mean()))
+            clamped_means.append(float(np.clip(v, 0.0, 1.0).mean()))
+        else:
+            raw_means.append(None)
+            clamped_means.append(None)
+    return raw, clamped, tuple(len(coded[lv]) for lv in (1, 2, 3, 4)), raw_means, clamped_means

@@ -79,6 +79,7 @@ _SIGNATURES = {
     "fc_level_prepare": ([_P, ctypes.c_int, ctypes.c_int, _P, _I32, _I32], ctypes.c_int),
     "fc_match_level": ([_P, ctypes.c_int, _P, _I64, _P, _P, _P], ctypes.c_int),
     "fc_match_tiles": ([_P, ctypes.c_int, _P, _I64, _P, _P, _P], ctypes.c_int),
+    "fc_real_match_level": ([_P, ctypes.c_int, _P, _I64, _P, _P, _P], ctypes.c_int),
     "fc_scan_candidates": ([_P, _P, _P, _I64, _I32, _P, _P, _I64, _P, _I32, _I32, _P, _P],
                            ctypes.c_int),
     "fc_encode": ([_P, _P, _I32, _P, _P, _I32, _P, _I64, ctypes.POINTER(_I64)], ctypes.c_int),
@@ -283,6 +284,17 @@ class Context:
         self.check(self.lib.fc_match_tiles(self.handle, level, _ptr(t), M, _ptr(err), _ptr(idx),
                                            _ptr(rmean)))
         return err, idx, rmean
+
+    def real_match_level(self, level: int, origins):
+        """fc_real_match_level: (errs f64, slopes f64, flat index e*8 + iso int64)."""
+        o = np.ascontiguousarray(np.asarray(origins, dtype=np.int32).reshape(-1, 2))
+        M = o.shape[0]
+        err = np.empty(M, dtype=np.float64)
+        slope = np.empty(M, dtype=np.float64)
+        idx = np.empty(M, dtype=np.int64)
+        self.check(self.lib.fc_real_match_level(self.handle, level, _ptr(o), M, _ptr(err),
+                                                _ptr(slope), _ptr(idx)))
+        return err, slope, idx
 
     def match_level_device(self, level: int, origins_ptr: int, count: int, err_ptr: int,
                            idx_ptr: int, rmean_ptr: int):

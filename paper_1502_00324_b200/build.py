@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libfracodec_b200.so")
 SOURCES = ["fc_api.cu", "fc_pool.cu", "fc_scan_exact.cu", "fc_scan_tc.cu", "fc_encode.cu",
-           "fc_decode.cu",
+           "fc_decode.cu", "fc_real.cu",
            "fc_probe.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

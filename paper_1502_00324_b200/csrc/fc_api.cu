@@ -571,6 +571,57 @@ int fc_match_level(fc_ctx* c, int level, const int32_t* origins_xy, int64_t coun
   return run_match(c, L, count, out_err, out_idx, out_rmean, c->device_io != 0);
 }
 
+// Real-valued slope search (bench.py:117-139 _real_s_matches over the ranges
+// codec.py:164 _gather_tiles cuts at `origins_xy`): per range the exact fp64
+// projection error, slope and flat index e*8 + iso of the first minimum.
+// Needs the pool only (no fc_level_prepare); host buffers.
+int fc_real_match_level(fc_ctx* c, int level, const int32_t* origins_xy, int64_t count,
+                        double* out_err, double* out_s, int64_t* out_idx) {
+  cudaSetDevice(c->device);
+  FC_TRY(level_ready(c, level));
+  Level& L = c->lv[level - 1];
+  if (count < 0) return set_error(c, FC_ERR_ARG, "negative range count");
+  if (c->device_io) return set_error(c, FC_ERR_STATE, "fc_real_match_level takes host buffers");
+  if (!c->img_ptr) return set_error(c, FC_ERR_STATE, "no image set");
+  if (L.count == 0) {
+    char buf[64];
+    snprintf(buf, sizeof buf, "no domain entries at level %d", level);
+    return set_error(c, FC_ERR_EMPTY_POOL, buf);
+  }
+  c->total_launches += c->stats.kernel_launches;
+  c->stats = fc_stats{};
+  c->stats.ranges = count;
+  c->stats.columns = L.count;
+  c->stats.comparisons = count * L.count * 8;
+  if (count == 0) return FC_OK;
+  for (int64_t i = 0; i < count; ++i) {
+    const int x = origins_xy[2 * i], y = origins_xy[2 * i + 1];
+    if (x < 0 || y < 0 || x + L.side > c->width || y + L.side > c->height)
+      return set_error(c, FC_ERR_ARG, "range origin outside the image");
+  }
+  FC_CUDA(c, c->origins.reserve(count * 8));
+  FC_CUDA(c, cudaMemcpyAsync(c->origins.ptr, origins_xy, count * 8, cudaMemcpyHostToDevice,
+                             c->stream));
+  FC_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+  FC_TRY(gather_ranges(c, L, c->origins.as<int32_t>(), count));
+  FC_CUDA(c, c->real_out.reserve(count * 24));
+  double* d_err = c->real_out.as<double>();
+  double* d_s = d_err + count;
+  auto* d_idx = reinterpret_cast<int64_t*>(d_s + count);
+  FC_TRY(real_s_match(c, L, count, d_err, d_s, d_idx));
+  FC_CUDA(c, cudaEventRecord(c->ev2, c->stream));
+  FC_CUDA(c, cudaMemcpyAsync(out_err, d_err, count * 8, cudaMemcpyDeviceToHost, c->stream));
+  FC_CUDA(c, cudaMemcpyAsync(out_s, d_s, count * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (out_idx)
+    FC_CUDA(c, cudaMemcpyAsync(out_idx, d_idx, count * 8, cudaMemcpyDeviceToHost, c->stream));
+  FC_CUDA(c, cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev0, c->ev2);
+  c->stats.scan_ms = ms;
+  c->stats.main_ms = ms;
+  return FC_OK;
+}
+
 int fc_match_tiles(fc_ctx* c, int level, const uint8_t* tiles, int64_t count, int64_t* out_err,
                    int64_t* out_idx, double* out_rmean) {
   cudaSetDevice(c->device);

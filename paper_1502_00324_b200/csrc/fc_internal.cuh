@@ -150,6 +150,7 @@ struct Ctx {
   // scratch
   DevBuf ent_scratch, key_in, key_out, val_in, val_out, cub_tmp, count_buf;
   DevBuf origins, rtiles, rmean, roff, rsq, keys, out_err, out_idx;
+  DevBuf real_part, real_out;  // fc_real_match_level: per-chunk winners, device outputs
   DevBuf fix_rows, fix_cols, fix_jobs, svals_dev;
   DevBuf a_tiles, row_meta, fix_prefix, tc_scratch, tc_plan, pool_rank;
   std::vector<int32_t> h_roff;
@@ -303,6 +304,8 @@ int scan_exact(Ctx* c, Level& L, int64_t M, const int32_t* d_range_list, int64_t
                const int32_t* d_M = nullptr, unsigned long long* d_time = nullptr);
 int decode_keys(Ctx* c, const uint64_t* d_keys, int64_t M, int64_t* d_err, int64_t* d_idx);
 int iso_table_offset(int side);
+// fc_real.cu: real-valued slope search over the gathered ranges (device outputs)
+int real_s_match(Ctx* c, Level& L, int64_t M, double* d_err, double* d_s, int64_t* d_idx);
 int scan_rows_dropin(Ctx* c, const int16_t* ranges, const double* rmeans, int64_t M, int32_t n,
                      const int16_t* q, const double* dmeans, int64_t E, const double* svals,
                      int32_t S, int32_t baseline, int64_t* out_err, int64_t* out_idx);

@@ -233,6 +233,52 @@ def paper_fixture_case():
     print(f"  lena ratio {lena.size * 8 / payload:.4f}")
 
 
+def shist_cases():
+    """bench.py:142 s_histogram on small images, with the per-level
+    _real_s_matches outputs (errs, slopes) recorded by wrapping it."""
+    import fracodec.bench as fb
+    out = {}
+    rng = np.random.default_rng(77)
+    imgs = {
+        "const": (np.full((64, 64), 90, dtype=np.uint8), 8, (8, 4, 2, 2)),
+        "tiled": (_tiled_noise(rng, size=64, cell=4, noise=10.0), 16, (8, 4, 2, 2)),
+        "c1": (W.make_image("c1", 0), 64, (8, 4, 2, 2)),
+        "grad": (W.make_image("c2", 3)[:128, :128].copy(), 48, (4, 2, 2, 2)),
+    }
+    real = fb._real_s_matches
+    for tag, (pix, cap, strides) in imgs.items():
+        calls = []
+
+        def rec(tiles, basis, norms, _calls=calls):
+            e, s = real(tiles, basis, norms)
+            _calls.append((tiles.shape[1], e.copy(), s.copy()))
+            return e, s
+
+        fb._real_s_matches = rec
+        try:
+            cfg = fc.EncoderConfig(pool=fc.PoolParams(pool_cap=cap, strides=strides),
+                                   policy=fc.SPolicy(mode=fc.PROPOSED))
+            h = fc.s_histogram(fc.GrayImage(pix), cfg)
+        finally:
+            fb._real_s_matches = real
+        out[f"{tag}_pixels"] = pix
+        out[f"{tag}_cap"] = np.int64(cap)
+        out[f"{tag}_strides"] = np.asarray(strides, dtype=np.int64)
+        out[f"{tag}_raw"] = h.raw_counts
+        out[f"{tag}_clamped"] = h.clamped_counts
+        out[f"{tag}_coded"] = np.asarray(h.coded_blocks, dtype=np.int64)
+        out[f"{tag}_raw_means"] = np.asarray([np.nan if v is None else v for v in h.raw_means])
+        out[f"{tag}_clamped_means"] = np.asarray(
+            [np.nan if v is None else v for v in h.clamped_means])
+        for i, (n, e, sl) in enumerate(calls):
+            out[f"{tag}_call{i}_n"] = np.int64(n)
+            out[f"{tag}_call{i}_err"] = e
+            out[f"{tag}_call{i}_slope"] = sl
+        out[f"{tag}_calls"] = np.int64(len(calls))
+        print(f"  shist {tag}: coded {h.coded_blocks}")
+    np.savez_compressed(OUT / "shist_cases.npz", **out)
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
     which = sys.argv[1:] or ["matcher", "entropy", "encode", "c2", "lena"]
@@ -246,3 +292,5 @@ if __name__ == "__main__":
         c2_case()
     if "lena" in which:
         paper_fixture_case()
+    if "shist" in which:
+        shist_cases()
