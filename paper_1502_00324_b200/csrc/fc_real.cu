@@ -17,10 +17,10 @@
 // reference takes (cross*cross, / cnorm, rnorm - gain) are repeated with the
 // IEEE intrinsics: the result is bit-identical to the reference.
 //
-// Layout: one block per 8 ranges x one chunk of entries.  The 64 (range,
+// Layout: one block per 4 ranges x one chunk of entries.  The 32 (range,
 // isometry) rows are permuted into shared memory once (isometry as a pixel
 // permutation of the range: sum iso(d)*r = sum d * r[inv_iso]); each thread
-// streams whole entries and keeps the 64 dot products in registers.  The
+// streams whole entries and keeps the 32 dot products in registers.  The
 // per-chunk winners are merged in chunk order by a second kernel.
 #include <cfloat>
 #include <cstdint>
@@ -30,12 +30,12 @@
 namespace fcb {
 namespace {
 
-constexpr int kRealRanges = 8;
+constexpr int kRealRanges = 4;  // x 8 isometries = 32 rows; <= 128 registers, 2 blocks per SM
 constexpr int kRealRows = kRealRanges * 8;
 constexpr int kRealThreads = 256;
 
 template <int N>
-__global__ void __launch_bounds__(kRealThreads)
+__global__ void __launch_bounds__(kRealThreads, 2)
 real_s_kernel(const uint8_t* __restrict__ rtiles, int64_t M, const uint16_t* __restrict__ inv,
               const uint8_t* __restrict__ dtiles, const int32_t* __restrict__ dsum,
               const double* __restrict__ dnorm, int64_t E, int64_t e_chunk,
@@ -57,7 +57,7 @@ real_s_kernel(const uint8_t* __restrict__ rtiles, int64_t M, const uint16_t* __r
     const int64_t m = m0 + (row >> 3);
     a_b[i] = m < M ? rtiles[m * N + inv[(row & 7) * N + j]] : (uint8_t)0;
   }
-  if (warp < kRealRanges) {
+  if (warp < kRealRanges) {  // one warp per range: R1 and rnorm
     const int64_t m = m0 + warp;
     long long s1 = 0, s2 = 0;
     if (m < M)
@@ -123,6 +123,7 @@ real_s_kernel(const uint8_t* __restrict__ rtiles, int64_t M, const uint16_t* __r
     const long long d1 = dsum[e];
     const double norm = dnorm[e];
     const bool flat = norm == 0.0;
+    const double rcp = flat ? 0.0 : __drcp_rn(norm);
 #pragma unroll
     for (int r = 0; r < kRealRanges; ++r) {
       const long long r1 = r1_s[r];
@@ -131,7 +132,15 @@ real_s_kernel(const uint8_t* __restrict__ rtiles, int64_t M, const uint16_t* __r
       for (int iso = 0; iso < 8; ++iso) {
         const long long num = (long long)N * (long long)acc[r * 8 + iso] - d1 * r1;
         const double cross = __dmul_rn((double)num, 1.0 / N);  // exact (power of two)
-        const double gain = flat ? 0.0 : __ddiv_rn(__dmul_rn(cross, cross), norm);
+        const double cc = __dmul_rn(cross, cross);
+        if (!flat) {
+          // screen with the entry's reciprocal: |cc*rcp - fl(cc/norm)| <= 4e-16*gain, so
+          // when even the screened error clears best by 1e-14*(rn + gain) the
+          // exact one is >= best and cannot win (ties keep the earlier index)
+          const double g_est = __dmul_rn(cc, rcp);
+          if (__dsub_rn(rn, g_est) > best_err[r] + 1e-14 * (rn + g_est)) continue;
+        }
+        const double gain = flat ? 0.0 : __ddiv_rn(cc, norm);
         const double err = fmax(__dsub_rn(rn, gain), 0.0);
         if (err < best_err[r]) {  // e, iso ascending: the first minimum stays
           best_err[r] = err;
