@@ -189,6 +189,10 @@ int fc_get_stream(fc_ctx* ctx, void** out_stream);
 /* Kernels this library launched on the context since creation (excludes CUB
  * sort internals and memcpy/memset). */
 int fc_launch_count(fc_ctx* ctx, int64_t* out_count);
+/* Device time of the last fc_pool_build (CUDA events on the context stream):
+ * out_ms[0] = the window-entropy kernels, out_ms[1] = ranking + survivor
+ * tiles/moments (including any survivor-count readback), out_ms[2] = total. */
+int fc_pool_times(fc_ctx* ctx, float out_ms[3]);
 /* Roofline denominator measured in-run: dense tcgen05.mma kind::i8 rate
  * (M=128, N=256, operands in smem, no epilogue) over all SMs, in TOP/s. */
 int fc_probe_int8_peak(fc_ctx* ctx, double* out_tops);

@@ -178,6 +178,111 @@ def candidate_operands(tiles: np.ndarray, means: np.ndarray, svals, baseline: bo
     return np.ascontiguousarray(q.reshape(E * 8 * S, B * B))
 
 
+# ---------------------------------------------------------------------------
+# full-size helpers (BASELINE c4/c5: millions of windows) -- same arithmetic,
+# bounded memory, bands of window rows on several host processes
+# ---------------------------------------------------------------------------
+
+def _entropy_band(args):
+    pixels, side, stride, y0, ny = args
+    sub = pixels[y0 * stride : (y0 + ny - 1) * stride + side]
+    return grid_entropies(sub, side, stride)[2]
+
+
+def grid_entropies_parallel(pixels: np.ndarray, side: int, stride: int, workers: int = 0):
+    """grid_entropies (pool.py:120-135) over bands of window rows on several
+    processes.  Every window's entropy is a function of its own 256 counts
+    only (pool.py:88-92 reduces each row separately), so the bands
+    concatenate into exactly the single-process result."""
+    h, w = pixels.shape
+    ny = (h - side) // stride + 1
+    nx = (w - side) // stride + 1
+    ys = np.repeat(np.arange(ny) * stride, nx)
+    xs = np.tile(np.arange(nx) * stride, ny)
+    workers = workers or os.cpu_count() or 1
+    if workers <= 1 or ny * nx < 200_000:
+        return grid_entropies(pixels, side, stride)
+    import concurrent.futures as cf
+    import multiprocessing as mp
+
+    per = max(1, -(-ny // (4 * workers)))
+    jobs = [(pixels, side, stride, y0, min(per, ny - y0)) for y0 in range(0, ny, per)]
+    with cf.ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("forkserver")) as ex:
+        parts = list(ex.map(_entropy_band, jobs))
+    return xs, ys, np.concatenate(parts)
+
+
+def pool_order(pixels: np.ndarray, level: int, stride: int, cap: int, workers: int = 0):
+    """Rank order of one level's pool (pool.py:171: argsort(-ent, stable)[:cap])
+    -> (xs, ys, ent) in rank order, without tiles."""
+    side = LEVEL_DOMAIN_SIDES[level - 1]
+    xs, ys, ent = grid_entropies_parallel(pixels, side, stride, workers)
+    order = np.argsort(-ent, kind="stable")[:cap]
+    return xs[order], ys[order], ent[order]
+
+
+def pool_tiles(pixels: np.ndarray, level: int, xs, ys, chunk: int = 1 << 18):
+    """Decimated tiles, means and centered norms of the domains at (xs, ys)
+    (image.py:116-130, pool.py:138-152), in chunks."""
+    side = LEVEL_DOMAIN_SIDES[level - 1]
+    b = side // 2
+    view = np.lib.stride_tricks.sliding_window_view(pixels, (side, side))
+    E = len(xs)
+    tiles = np.empty((E, b, b), dtype=np.uint8)
+    means = np.empty(E)
+    cnorm = np.empty(E)
+    for lo in range(0, E, chunk):
+        hi = min(E, lo + chunk)
+        t = decimate(view[ys[lo:hi], xs[lo:hi]])
+        tiles[lo:hi] = t
+        flat = t.reshape(hi - lo, -1).astype(np.int64)
+        s1 = flat.sum(axis=1)
+        s2 = (flat * flat).sum(axis=1)
+        means[lo:hi] = s1 / (b * b)
+        cnorm[lo:hi] = s2 - s1 * s1 / (b * b)
+    return tiles, means, cnorm
+
+
+def base_operands(tiles: np.ndarray, means: np.ndarray, svals, baseline: bool, chunk: int = 1 << 17):
+    """qbase[e*S + si, :] = rint(s*(tile - mean)) (proposed) or rint(s*tile)
+    (baseline) as int16, before any isometry (matcher.py:143-154)."""
+    E, B, _ = tiles.shape
+    sv = np.asarray(svals, dtype=np.float64)
+    S = sv.shape[0]
+    out = np.empty((E, S, B * B), dtype=np.int16)
+    for lo in range(0, E, chunk):
+        hi = min(E, lo + chunk)
+        t = tiles[lo:hi].reshape(hi - lo, B * B).astype(np.float64)
+        if not baseline:
+            t = t - means[lo:hi, None]
+        out[lo:hi] = np.rint(sv[None, :, None] * t[:, None, :]).astype(np.int16)
+    return out.reshape(E * S, B * B)
+
+
+def scan_candidates_base(ranges, rmeans, qbase, dmeans, svals, baseline, threads: int = 0):
+    """scan_candidates (_scan.py:14-63) over the base operand with the
+    isometries applied on the fly (scan_oracle.c) -> (err int64[M], idx int64[M])."""
+    ranges = np.ascontiguousarray(ranges, dtype=np.int16)
+    rmeans = np.ascontiguousarray(rmeans, dtype=np.float64)
+    qbase = np.ascontiguousarray(qbase, dtype=np.int16)
+    dmeans = np.ascontiguousarray(dmeans, dtype=np.float64)
+    svals = np.ascontiguousarray(svals, dtype=np.float64)
+    M, n = ranges.shape
+    side = int(round(n ** 0.5))
+    isomap = np.ascontiguousarray(
+        np.stack([isometry_index_map(side, k) for k in range(8)]).astype(np.int32))
+    out_err = np.empty(M, dtype=np.int64)
+    out_idx = np.empty(M, dtype=np.int64)
+    if M == 0:
+        return out_err, out_idx
+    _scan_lib().oracle_scan_candidates_base(
+        M, n, ranges.ctypes.data, rmeans.ctypes.data, qbase.ctypes.data, dmeans.shape[0],
+        dmeans.ctypes.data, svals.shape[0], svals.ctypes.data, int(bool(baseline)),
+        isomap.ctypes.data, out_err.ctypes.data, out_idx.ctypes.data, int(threads),
+    )
+    return out_err, out_idx
+
+
 _LIB = None
 
 
@@ -191,6 +296,13 @@ def _scan_lib():
 
             _b.build()
         lib = ctypes.CDLL(path)
+        lib.oracle_scan_candidates_base.restype = None
+        lib.oracle_scan_candidates_base.argtypes = [
+            ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+            ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32,
+            ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+            ctypes.c_void_p, ctypes.c_int32,
+        ]
         lib.oracle_scan_candidates.restype = None
         lib.oracle_scan_candidates.argtypes = [
             ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,

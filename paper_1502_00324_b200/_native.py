@@ -93,6 +93,7 @@ _SIGNATURES = {
     "fc_get_stream": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
     "fc_launch_count": ([_P, ctypes.POINTER(_I64)], ctypes.c_int),
     "fc_probe_int8_peak": ([_P, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+    "fc_pool_times": ([_P, _P], ctypes.c_int),
 }
 
 _lib = None
@@ -391,6 +392,12 @@ class Context:
         v = ctypes.c_double()
         self.check(self.lib.fc_probe_int8_peak(self.handle, ctypes.byref(v)))
         return float(v.value)
+
+    def pool_times(self) -> tuple:
+        """(entropy kernels, ranking + survivors, total) device ms of the last pool build."""
+        out = np.zeros(3, dtype=np.float32)
+        self.check(self.lib.fc_pool_times(self.handle, _ptr(out)))
+        return tuple(float(v) for v in out)
 
     def launch_count(self) -> int:
         n = ctypes.c_int64()

@@ -223,27 +223,25 @@ def _level_stats(ctx) -> list:
     return out
 
 
-def encode_distributed(image: GrayImage, config: EncoderConfig, context=None, device_image=None,
-                       device="cuda"):
+def encode_distributed(image: GrayImage, config: EncoderConfig, context=None, device_image=None):
     """Range-sharded encode over the initialised torch.distributed group (one
     process per GPU): every rank builds the replicated pool and encodes its
-    slab (encode_shard), the records are all-gathered (NCCL over NVLink when
-    device="cuda") and every rank returns the full (CompressedStream,
-    EncodeReport) -- byte-identical to encode()."""
+    slab (encode_shard), the records are all-gathered (NCCL over NVLink for a
+    CUDA context; the collective runs on the context's device) and every rank
+    returns the full (CompressedStream, EncodeReport) -- byte-identical to
+    encode().  The only collective is that one record exchange."""
     import torch.distributed as dist
 
     from . import sharding
 
     t_start = time.perf_counter()
+    ctx = context if context is not None else _native.default_context()
     dist_on = dist.is_available() and dist.is_initialized()
     rank = dist.get_rank() if dist_on else 0
     world = dist.get_world_size() if dist_on else 1
-    rec, pool, level_stats = encode_shard(image, config, rank, world, context, device_image)
+    rec, pool, level_stats = encode_shard(image, config, rank, world, ctx, device_image)
+    device = "cpu" if dist_on and dist.get_backend() == "gloo" else f"cuda:{ctx.device}"
     allrec = sharding.gather_rows(rec, device=device)
-    comparisons = int(sharding.reduce_metrics(
-        dict(step_ms_total=0.0, e2e_s_total=0.0, kernel_ms_total=0.0,
-             comparisons=sum(ls["comparisons"] for ls in level_stats), pixels=0, alg_ops=0),
-        device=device)["comparisons"])
     policy = config.policy
     s_sets = tuple(policy.s_set(level) for level in (1, 2, 3, 4))
     stream = CompressedStream(
@@ -252,10 +250,25 @@ def encode_distributed(image: GrayImage, config: EncoderConfig, context=None, de
     step_blocks = tuple(int(v) for v in np.bincount(allrec[:, 0], minlength=5)[1:5])
     collage_ssd = int(allrec[:, 5].sum(dtype=np.int64))
     encode_time = time.perf_counter() - t_start
-    # comparisons: the whole image (all ranks); level_stats: this rank's slab
+    comparisons = image_comparisons(step_blocks, pool.sizes, s_sets)
+    # comparisons: the whole image (all ranks, from the gathered leaves);
+    # level_stats: this rank's slab
     return stream, _report(image, config, pool, stream, step_blocks, collage_ssd, 0.0, encode_time,
                            comparisons, sum(ls["scan_ms"] for ls in level_stats), level_stats,
                            {"sharded_ranks": world})
+
+
+def image_comparisons(step_blocks, pool_sizes, s_sets) -> int:
+    """Comparisons of a whole encode from its leaf counts: the level-l ranges
+    are the quadtree nodes at depth l, and the leaves at levels >= l cover
+    exactly their area (every split has four children, codec.py:141), so
+    ranges_l = sum_{k >= l} leaves_k / 4^(k - l)."""
+    total = 0
+    for level in (1, 2, 3, 4):
+        area = sum(step_blocks[k - 1] * 4 ** (4 - k) for k in range(level, 5))  # in 2x2 units
+        ranges = area // 4 ** (4 - level)
+        total += ranges * int(pool_sizes[level - 1]) * 8 * len(s_sets[level - 1])
+    return total
 
 
 def _report(image, config, pool, stream, step_blocks, collage_ssd, pool_time, encode_time,

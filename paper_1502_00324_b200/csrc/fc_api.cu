@@ -289,6 +289,8 @@ void fc_ctx_destroy(fc_ctx* c) {
   cudaEventDestroy(c->ev1);
   cudaEventDestroy(c->ev2);
   for (auto& e : c->tc_ev) cudaEventDestroy(e);
+  for (auto& e : c->pool_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& e : c->trace_ev) cudaEventDestroy(e);
   if (c->aux) {
     cudaStreamSynchronize(c->aux);
@@ -692,6 +694,19 @@ extern "C" {
 int fc_get_stream(fc_ctx* c, void** out_stream) {
   if (!out_stream) return set_error(c, FC_ERR_ARG, "null output");
   *out_stream = reinterpret_cast<void*>(c->stream);
+  return FC_OK;
+}
+
+int fc_pool_times(fc_ctx* c, float out_ms[3]) {
+  cudaSetDevice(c->device);
+  if (!c->pool_timed) return set_error(c, FC_ERR_STATE, "no pool build timed yet");
+  FC_CUDA(c, cudaEventSynchronize(c->pool_ev[2]));
+  float a = 0.f, b = 0.f;
+  FC_CUDA(c, cudaEventElapsedTime(&a, c->pool_ev[0], c->pool_ev[1]));
+  FC_CUDA(c, cudaEventElapsedTime(&b, c->pool_ev[1], c->pool_ev[2]));
+  out_ms[0] = a;
+  out_ms[1] = b;
+  out_ms[2] = a + b;
   return FC_OK;
 }
 

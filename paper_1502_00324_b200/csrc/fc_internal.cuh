@@ -137,6 +137,9 @@ struct Ctx {
   bool tc_attr_set = false;
   int tc_forward = 0;    // FC_TC_FORWARD: tile scan order of the tensor kernel  // FC_TC_WAIT: spin-wait roles of the tensor kernel
   bool ent_attr_set = false;
+  // pool phase timing (fc_pool_times): before the entropy kernels, after them, after the survivors
+  cudaEvent_t pool_ev[3] = {nullptr, nullptr, nullptr};
+  bool pool_timed = false;
   Status st;
   int device_io = 0;
   // image

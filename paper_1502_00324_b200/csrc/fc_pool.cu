@@ -660,7 +660,7 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
   if (!c->img_ptr) return set_error(c, FC_ERR_STATE, "no image set");
   for (int li = 0; li < kLevels; ++li) {
     if (strides[li] < 1) return set_error(c, FC_ERR_ARG, "strides must be 4 positive integers");
-    if (!use_tau[li] && caps[li] < 1) return set_error(c, FC_ERR_ARG, "caps must be >= 1");
+    if (caps[li] < 1) return set_error(c, FC_ERR_ARG, "caps must be >= 1");
   }
   for (int li = 0; li < kLevels; ++li) {
     const int D = kDomainSide[li];
@@ -762,6 +762,9 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, ent_smem<4>()));
     c->ent_attr_set = true;
   }
+  if (!c->pool_ev[0])
+    for (auto& e : c->pool_ev) FC_CUDA(c, cudaEventCreate(&e));
+  FC_CUDA(c, cudaEventRecord(c->pool_ev[0], c->stream));
   for (int k = 0; k < 2; ++k) {
     const EntParams& Q = PL[k];
     if (Q.n_levels == 0) continue;
@@ -775,6 +778,7 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     FC_CUDA(c, cudaGetLastError());
     c->total_launches += 1;
   }
+  FC_CUDA(c, cudaEventRecord(c->pool_ev[1], c->stream));
   for (int li = 0; li < kLevels; ++li) {
     Level& L = c->lv[li];
     const int64_t nwin = (int64_t)nx_l[li] * ny_l[li];
@@ -832,7 +836,9 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
         L.count = 1;
         continue;
       }
-      L.count = nsel;
+      // every survivor is ranked, then the level keeps the first cap of them
+      // (pool.py:171 argsort(-ent, stable)[:cap] over the threshold set)
+      L.count = std::min<int64_t>(nsel, caps[li]);
       const int nch = (nsel + chunk - 1) / chunk;
       if (nch <= kMaxChunks) {
         SortLevel& S = SP.lv[SP.n_levels++];
@@ -936,6 +942,8 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     c->total_launches += 1;
     c->nsel_clean = true;
   }
+  FC_CUDA(c, cudaEventRecord(c->pool_ev[2], c->stream));
+  c->pool_timed = true;
   trace_mark(c, "pool_launched");
   return FC_OK;
 }

@@ -227,11 +227,31 @@ def build_pool(image: GrayImage, params: PoolParams, context=None, device_image=
     """
     ctx = context if context is not None else _native.Context()
     if device_image is not None:
-        ctx.set_image_device(int(device_image.data_ptr()), image.width, image.height)
+        _adopt_device_image(ctx, device_image, image)
     else:
         ctx.set_image(image.pixels)
     sizes = ctx.pool_build(*params.native_args())
     return DomainPool(params, image.width, image.height, sizes, ctx)
+
+
+def _adopt_device_image(ctx, dev, image: GrayImage):
+    """Let the context read an HBM-resident copy of ``image`` in place.
+
+    The tensor must be a contiguous uint8 (height, width) CUDA tensor on the
+    context's device; the context stream waits for the producer's current
+    stream, so a copy still in flight is never read early."""
+    import torch
+
+    if not isinstance(dev, torch.Tensor):
+        raise TypeError("device_image must be a torch CUDA tensor")
+    if dev.dtype != torch.uint8 or not dev.is_cuda or dev.device.index != ctx.device:
+        raise ValueError(f"device_image must be a uint8 tensor on cuda:{ctx.device}")
+    if tuple(dev.shape) != (image.height, image.width) or not dev.is_contiguous():
+        raise ValueError(f"device_image must be contiguous with shape {(image.height, image.width)}")
+    ext = torch.cuda.ExternalStream(ctx.stream_handle(), device=dev.device)
+    ext.wait_stream(torch.cuda.current_stream(dev.device))
+    dev.record_stream(ext)
+    ctx.set_image_device(int(dev.data_ptr()), image.width, image.height)
 
 
 def block_entropy(tile) -> float:

@@ -118,3 +118,17 @@ WORKLOADS = {
                    (None, None, None, None),
                    (True, False, True, True)),
 }
+
+
+def encoder_config(name: str, path: str = "auto"):
+    """The EncoderConfig of a workload: frozen entropy thresholds as device
+    threshold compaction (ent > tau), cap 1 on the levels it never codes."""
+    from .codec import EncoderConfig
+    from .pool import PoolParams
+
+    wl = WORKLOADS[name]
+    taus = tuple(None if one else t for one, t in zip(wl.cap_one, wl.taus))
+    caps = tuple(1 if one else 2**31 - 1 for one in wl.cap_one)
+    params = PoolParams(pool_cap=2**31 - 1, strides=wl.strides, level_caps=caps,
+                        entropy_thresholds=taus)
+    return EncoderConfig(pool=params, thresholds=wl.thresholds, path=path)

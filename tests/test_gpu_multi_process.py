@@ -1,0 +1,64 @@
+"""Range-sharded encode across two processes on the one GPU of
+the test box: two ranks with their own contexts on cuda:0, a gloo process
+group (the code path is the one torchrun + NCCL runs on an 8-GPU node: slab
+per rank, replicated pool, one record all-gather).  The ranks' kernels never
+wait on each other, so sharing a GPU is safe."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import paper_1502_00324_b200 as fc
+    from paper_1502_00324_b200 import _native
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = np.load(os.path.join(GOLDEN, "encode_c2.npz"))
+    caps = tuple(int(v) for v in g["caps_c2"])
+    params = fc.PoolParams(pool_cap=max(caps), strides=tuple(int(v) for v in g["strides_c2"]),
+                           level_caps=caps)
+    cfg = fc.EncoderConfig(pool=params, thresholds=tuple(float(v) for v in g["thresholds_c2"]))
+    ctx = _native.Context(0)
+    stream, report = fc.encode_distributed(fc.GrayImage(g["image_c2"]), cfg, context=ctx)
+    rec, _, stats = fc.encode_shard(fc.GrayImage(g["image_c2"]), cfg, rank, world, context=ctx)
+    q.put((rank, fc.serialize(stream) == g["bytes_c2"].tobytes(), int(report.collage_ssd),
+           int(report.comparisons), sum(s["comparisons"] for s in stats), rec.shape[0]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_encode_distributed_two_processes_c2_bytes():
+    g = np.load(os.path.join(GOLDEN, "encode_c2.npz"))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {r[0]: r[1:] for r in (q.get(timeout=600) for _ in procs)}
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank in (0, 1):
+        same, collage, comps, _, _ = res[rank]
+        assert same and collage == int(g["collage_c2"])
+        # the whole image's comparisons, from the gathered leaves == sum of the slabs'
+        assert comps == res[0][3] + res[1][3]
+    assert res[0][4] + res[1][4] == len(np.asarray(g["records_c2"]))

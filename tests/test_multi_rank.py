@@ -96,3 +96,24 @@ def test_gather_rows_gloo_world2_rank_order():
                            for r in range(2)])
     for rank in (0, 1):
         assert np.array_equal(results[rank], want)
+
+
+def test_bench_gpus2_spawns_two_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as two ranks
+    (torch.distributed.run on 127.0.0.1); with the CPU arm, rank 0 prints the
+    one JSON line and rank 1 exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--workload", "c1", "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
