@@ -239,7 +239,9 @@ def _adopt_device_image(ctx, dev, image: GrayImage):
 
     The tensor must be a contiguous uint8 (height, width) CUDA tensor on the
     context's device; the context stream waits for the producer's current
-    stream, so a copy still in flight is never read early."""
+    stream, so a copy still in flight is never read early.  No record_stream:
+    every encode is synchronous at return, and an allocator event recorded on
+    the context's stream would outlive that stream (fc_ctx_destroy)."""
     import torch
 
     if not isinstance(dev, torch.Tensor):
@@ -250,7 +252,6 @@ def _adopt_device_image(ctx, dev, image: GrayImage):
         raise ValueError(f"device_image must be contiguous with shape {(image.height, image.width)}")
     ext = torch.cuda.ExternalStream(ctx.stream_handle(), device=dev.device)
     ext.wait_stream(torch.cuda.current_stream(dev.device))
-    dev.record_stream(ext)
     ctx.set_image_device(int(dev.data_ptr()), image.width, image.height)
 
 
