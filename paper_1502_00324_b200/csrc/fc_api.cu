@@ -234,12 +234,8 @@ int fc_ctx_create(int device, fc_ctx** out) {
   c->sm_count = prop.multiProcessorCount;
   if (const char* t = getenv("FC_TRACE")) c->trace = atoi(t);
   if (const char* g = getenv("FC_GRAPH")) c->use_graph = atoi(g) != 0;
-  if (const char* d = getenv("FC_TC_DEBUG")) c->tc_debug_mode = atoi(d);
-  if (const char* d = getenv("FC_TC_DEFERRED")) c->tc_deferred = atoi(d);
-  if (const char* d = getenv("FC_TC_G1")) c->tc_g1 = atoi(d);
   if (const char* o = getenv("FC_OVERLAP")) c->overlap = atoi(o) != 0;
   if (const char* o = getenv("FC_PDL")) c->pdl = atoi(o) != 0;
-  if (const char* o = getenv("FC_FIX_FUSED")) c->fix_fused = atoi(o) != 0;
   if (const char* d = getenv("FC_POOL_CHUNK")) c->pool_chunk = atoi(d);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
@@ -338,17 +334,9 @@ int fc_set_option(fc_ctx* c, const char* name, int64_t value) {
     c->top_end = value;
     return FC_OK;
   }
-  // kernel variants kept for measurement; results identical
-  if (strcmp(name, "tc_g1") == 0) {
-    c->tc_g1 = (int)value;
-    return FC_OK;
-  }
-  if (strcmp(name, "tc_deferred") == 0) {
-    c->tc_deferred = (int)value;
-    return FC_OK;
-  }
-  if (strcmp(name, "fix_fused") == 0) {
-    c->fix_fused = value != 0;
+  // schedule / launch variants (results identical by construction; tests run both)
+  if (strcmp(name, "tc_span_units") == 0) {  // force the B > L2 round-robin span schedule
+    c->tc_span_units = (int)value;
     return FC_OK;
   }
   if (strcmp(name, "pdl") == 0) {

@@ -303,7 +303,6 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     put(top_first);
     put(top_last);
     put(c->pdl);
-    put(c->fix_fused);
     for (int l = 0; l < 3; ++l) putd(thresholds[l]);
     for (int l = 0; l < kLevels; ++l) {
       const Level& L = c->lv[l];
@@ -336,9 +335,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     putp(c->coords_pinned.ptr);
     putp(c->rec_pinned.ptr);
     putp(c->readback.ptr);
-    put(c->tc_debug_mode);
-    put(c->tc_deferred);
-    put(c->tc_g1);
+    put(c->tc_span_units);
   }
   const bool reuse = use_graph && c->trace != 1 && c->enc_exec && sig == c->enc_sig;
   int levels_run = 0;

@@ -187,12 +187,9 @@ struct Ctx {
   int64_t top_begin = 0, top_end = -1;       // fc_encode's top-level slab (-1: to the end)
   bool nsel_clean = false;                   // pool survivor counters already zero
   DevBuf dec_img, dec_leaves, dec_state, dec_svals;  // device decoder (fc_decode.cu)
-  bool fix_fused = false;              // FC_FIX_FUSED=1: clamp corrections inside the contraction (measured 2% slower on c2)
   bool pdl = false;                    // FC_PDL=1: programmatic dependent launches (measured no gain)
-  int tc_debug_mode = 0;               // FC_TC_DEBUG_MODE (pipeline probes)
   int pool_chunk = 0;                  // FC_POOL_CHUNK=1024 / 2048: force the rank-sort chunk
-  int tc_deferred = -1;                // FC_TC_DEFERRED: -1 = by K, 0/1 forced
-  int tc_g1 = -1;                      // FC_TC_G1: epilogue drain layout, -1 = default
+  int tc_span_units = 0;               // 1: the contraction's round-robin span schedule at any B size (tests)
   cudaGraphExec_t enc_exec = nullptr;  // instantiated level-loop graph, updated per encode
   std::vector<uint64_t> enc_sig;       // launch signature of enc_exec (reuse when equal)
   int enc_levels_run = 0;              // host-side results of the captured body

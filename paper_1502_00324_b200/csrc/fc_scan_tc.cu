@@ -58,10 +58,12 @@ namespace {
 
 constexpr int kTileN = 256;      // columns per B stage tile
 constexpr int kTileM = 128;      // rows per row tile = 16 ranges x 8 isometries
-constexpr int kAccN = 256;       // columns per MMA / TMEM accumulator
-constexpr int kNumAcc = 2;       // TMEM accumulators (2 x 256 columns = all 512)
-constexpr int kEpiWarps = 16;    // all drain every accumulator (4 per TMEM sub-partition)
-constexpr int kThreads = (4 + kEpiWarps) * 32;
+constexpr int kAccN = 128;       // columns per MMA / TMEM accumulator (half a B tile)
+constexpr int kNumAcc = 4;       // TMEM accumulators (4 x 128 columns = all 512)
+constexpr int kIssuers = 4;      // MMA warps, one per accumulator
+constexpr int kEpiBase = kIssuers;  // first epilogue warp (warps 0-3: MMA issuers, warp 0 also the producer)
+constexpr int kEpiWarps = 16;    // two groups of 8 (one column half each), 4 per TMEM sub-partition
+constexpr int kThreads = (kEpiBase + kEpiWarps) * 32;
 constexpr int kSmemBudget = 227 * 1024;  // the opt-in maximum per block
 constexpr int kNone = 0x7fffffff;
 
@@ -131,9 +133,6 @@ struct SegIter {
 // (n = 256: one column per lane, the few pairs of B = 16 need parallelism).
 __host__ __device__ constexpr int fix_cpl(int n) { return n >= 256 ? 1 : 4; }
 __host__ __device__ constexpr int fix_cols(int n) { return 32 * fix_cpl(n); }
-// inside tc_scan_kernel (96-register budget): fewer columns per lane
-__host__ __device__ constexpr int fix_cpl_fused(int n) { return n >= 256 ? 1 : 2; }
-__host__ __device__ constexpr int fix_cols_fused(int n) { return 32 * fix_cpl_fused(n); }
 
 // Clamp-correction plan (FixPlan) of one level.
 struct FixPlan {
@@ -253,22 +252,6 @@ __device__ __forceinline__ void fix_unit(const FixArgs& F, const long long* __re
     atomicMin(&F.keys[m], ((unsigned long long)werr << 32) | widx);
 }
 
-// Warp loop over the corrections inside tc_scan_kernel: units claimed from
-// the plan's counter, so CTAs that finish their contraction share early take
-// more of them (fills the contraction's tail).
-template <int N>
-__device__ __forceinline__ void fix_fused_loop(const FixArgs& F, int lane) {
-  const int n_jobs = F.fplan->n_jobs;
-  const long long total = F.fplan->total_units;
-  for (;;) {
-    unsigned long long u = 0;
-    if (lane == 0) u = atomicAdd(&F.fplan->next_unit, 1ull);
-    u = __shfl_sync(0xffffffffu, u, 0);
-    if ((long long)u >= total) break;
-    fix_unit<N, fix_cpl_fused(N)>(F, F.prefix, n_jobs, (long long)u, lane);
-  }
-}
-
 struct TcParams {
   const uint8_t* a_tiles;    // [rt_pad][128 * kpad]
   const int4* row_meta;      // [rt_pad * 128] {o, R, m, unused}
@@ -281,9 +264,6 @@ struct TcParams {
   int rg;          // row tiles per unit (A resident in smem)
   int stages;      // B ring depth
   const TcPlan* plan;
-  int deferred;    // 1: resolve the winning column once per unit (short K)
-  int g1;          // 1: every epilogue warp drains every accumulator (64 columns)
-  int fix_fused;   // 1: the clamp corrections run in this kernel (fix_fused_loop)
   FixArgs fix;
   unsigned long long* tspan;  // optional {start, end} slots (global ns)
 };
@@ -310,14 +290,6 @@ __device__ __forceinline__ int min8(const int (&v)[32]) {
                       min(v[O + 6], v[O + 7]));
 }
 
-// First index j with v[j] == m (m is known to occur).
-__device__ __forceinline__ int first_eq(const int (&v)[32], int m) {
-  int j = 31;
-#pragma unroll
-  for (int k = 30; k >= 0; --k) j = (v[k] == m) ? k : j;
-  return j;
-}
-
 // u8 x s8 four-way dot product accumulate (the MMA's kind::i8 arithmetic).
 __device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
   int d;
@@ -326,11 +298,11 @@ __device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
 }
 
 // Row state: best2 = 2*kh + par of the row's best so far and where it lies
-// (tile, 8-column group of this thread's quarter); the exact column inside
-// the group is resolved once per unit by recomputing its 8 dot products.
-// Tiles are visited in DECREASING column order (the entropy-ranked pool puts
-// the usually-better low-entropy domains last, so scanning backwards finds
-// them first and the running minimum rarely changes); an equal key2 at a
+// (tile, 8-column group of this thread's 64-column slice); the exact column
+// inside the group is resolved once per segment by recomputing its 8 dot
+// products.  Tiles are visited in DECREASING column order (the entropy-ranked
+// pool puts the usually-better low-entropy domains last, so scanning backwards
+// finds them first and the running minimum rarely changes); an equal key2 at a
 // smaller column must then win, so a block updates iff 2*m + par <= best2
 // <=>  m < ((best2 - par) >> 1) + 1.
 // (32-bit: best2 <= 0x7fffffff and par in {0, 1} cannot overflow.)
@@ -338,46 +310,40 @@ __device__ __forceinline__ int improve_limit(int best2, int par) {
   return ((best2 - par) >> 1) + 1;
 }
 
-// Epilogue role (warps 4-19), specialised on the column-resolution mode so the
-// hot loop carries no runtime mode tests.
+// (tile, row tile) pair counter H and column half h -> accumulator
+// acc = 2 * (H & 1) + h: MMA warp acc issues it, epilogue group H & 1 drains
+// both halves of its pairs.  Accumulator acc is used by every other pair, so
+// its n-th use has phase parity n & 1 with n = H >> 1.
+
 struct EpiCtx {
-  uint8_t* smem;
-  uint8_t* sStage;
-  uint32_t kStage, kB, bar_base, tmem_base;
-  int STAGES, RG, KPAD, warp, lane;
+  uint32_t kB, bar_base, tmem_base;
+  int RG, KPAD, warp, lane;
   TcPlan plan;
 };
 
-template <bool DEFERRED, bool G1>
-__device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x) {
-  uint8_t* smem = x.smem;
-  uint8_t* sStage = x.sStage;
-  const uint32_t kStage = x.kStage, kB = x.kB, bar_base = x.bar_base, tmem_base = x.tmem_base;
-  const int STAGES = x.STAGES, RG = x.RG, KPAD = x.KPAD, warp = x.warp, lane = x.lane;
-  // G1 == false: two groups of 8 warps alternate over the accumulators (group
-  // gq drains the (tile, row tile) pairs with H & 1 == gq, i.e. accumulator
-  // gq): one group computes while the other loads, and every barrier wait /
-  // release covers 128 columns per thread (two 64-column waves).
-  // G1 == true: all 16 warps drain every accumulator, 64 columns per thread in
-  // one wave, and release it before any arithmetic.
-  constexpr int kWaves = G1 ? 1 : 2;
-  constexpr int kGiBits = G1 ? 3 : 4;  // 8-column groups per thread and tile: 8 or 16
-  const int e = warp - 4;
-  const int gq = G1 ? 0 : e >> 3;     // accumulator / group
-  const int hq = G1 ? e >> 2 : (e >> 2) & 1;  // column quarter (G1) or half
-  const int sp = warp & 3;        // TMEM sub-partition (lanes 32*sp .. 32*sp+31)
+// Epilogue role (warps kEpiBase .. kEpiBase + 15): group gq (8 warps, two
+// per TMEM sub-partition) takes the pairs with (H & 1) == gq, i.e. the
+// accumulators 2 gq (column half 0) and 2 gq + 1 (half 1); each warp one
+// 64-column slice of each half.  Per accumulator one wave of two
+// tcgen05.ld x32, released right after the loads; the per-pair bookkeeping
+// (row state, tile info, loop control) is shared by the two halves.
+__device__ __forceinline__ void epilogue_role(const TcParams& p, uint8_t* smem, const EpiCtx& x) {
+  const uint32_t kB = x.kB, bar_base = x.bar_base, tmem_base = x.tmem_base;
+  const int RG = x.RG, KPAD = x.KPAD, warp = x.warp, lane = x.lane;
+  const int e = warp - kEpiBase;
+  const int gq = e >> 3;            // pair parity this group drains
+  const int hq = (e >> 2) & 1;      // 64-column slice inside each half
+  const int sp = warp & 3;          // TMEM sub-partition (lanes 32*sp .. 32*sp+31)
   const int row = sp * 32 + lane;
   const int S = p.S;
-  const int iso = lane & 7;
-  const int slot_h = G1 ? hq * 64 : hq * 128;
-  const uint32_t tm = ptx::pin(tmem_base + ((uint32_t)(sp * 32) << 16) + gq * kAccN + slot_h);
-  // this thread's {best2, loc} per resident row tile, stride = 512 threads
-  // (shared addresses pinned in registers: re-deriving them costs ~30
-  // instructions per iteration under the 96-register budget)
-  const uint32_t bst = ptx::pin(ptx::smem_u32(smem + best_offset(p)) + (e * 32 + lane) * 8);
+  const int slice = hq * 64;        // tile slot of this thread's slice in half 0 (+128: half 1)
+  const uint32_t tm0 = tmem_base + ((uint32_t)(sp * 32) << 16) + (2 * gq) * kAccN + slice;
+  const uint32_t tfull0 = bar_base + 8u * (2 * p.stages) + 8u * (2 * gq);
+  const uint32_t tempty0 = tfull0 + 8u * kNumAcc;
+  // this thread's {best2, loc} per resident row tile, stride = 512 threads;
+  // loc = tile << 4 | half << 3 | 8-column group
+  const uint32_t bst = ptx::smem_u32(smem + best_offset(p)) + (e * 32 + lane) * 8;
   constexpr int kBS = kEpiWarps * 32;
-  const uint32_t tfull0 = ptx::pin(bar_base + 8u * (2 * STAGES + gq));
-  const uint32_t tempty0 = ptx::pin(bar_base + 8u * (2 * STAGES + kNumAcc + gq));
   uint32_t H = 0;
   int g, t0, t1;
   for (SegIter it(x.plan); it.next(g, t0, t1);) {
@@ -387,43 +353,34 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
     for (int t = t1 - 1; t >= t0; --t) {
       const int2 tinfo = tinfo_next;  // {parity, valid slots}
       if (t > t0) tinfo_next = p.tile_info[t - 1];
-      // the B stage belongs to the MMA alone (released by its commit): the
-      // rare improving lanes of the immediate mode read the column map from
-      // global memory (L2), not from the stage
-      const int32_t* colmap_t = p.colmap + (size_t)t * kTileN;
-      // this group's (tile, row tile) pairs: H & 1 == gq.  H advances by RG per
-      // tile, so for even RG the row-tile parity is fixed; for odd RG (= 1)
-      // the tiles alternate between the groups.
-      const uint32_t Ht = H;
-      H += RG;
-      const int r_first = G1 ? 0 : (int)((gq - (int)(Ht & 1)) & 1);
 #pragma unroll 1
-      for (int r = r_first; r < RG; r += G1 ? 1 : 2) {
-        const uint32_t Hr = Ht + r;
-        const uint32_t acc = G1 ? (Hr & 1) : 0;
-        const int2 bs = ptx::lds_v2(bst + r * (kBS * 8));  // issued before the wait
-        ptx::mbar_wait_sleep(tfull0 + 8u * acc, (Hr >> 1) & 1);
-        ptx::tc_fence_after();
-        int va[32], vb[32];
-        int m_best = kNone, gi_best = 0;
-        const int lim = improve_limit(bs.x, tinfo.x);
+      for (int r = 0; r < RG; ++r, ++H) {
+        if ((int)(H & 1) != gq) continue;
+        const uint32_t bst_r = bst + r * (kBS * 8);
+        const int2 bs = ptx::lds_v2(bst_r);
+        const uint32_t ph = (H >> 1) & 1;
+        // half 0 vs earlier tiles: improve_limit (ties go to the later-visited,
+        // smaller columns); half 1 vs half 0 of this tile: strictly smaller
+        int lim = improve_limit(bs.x, tinfo.x);
+        int best_m = kNone, best_loc = 0;
 #pragma unroll
-        for (int wv = 0; wv < kWaves; ++wv) {
-          ptx::tmem_ld32(tm + acc * kAccN + wv * 64, va);
-          ptx::tmem_ld32(tm + acc * kAccN + wv * 64 + 32, vb);
+        for (int h = 0; h < 2; ++h) {
+          ptx::mbar_wait_sleep(tfull0 + 8u * h, ph);
+          ptx::tc_fence_after();
+          int va[32], vb[32];
+          ptx::tmem_ld32(tm0 + h * kAccN, va);
+          ptx::tmem_ld32(tm0 + h * kAccN + 32, vb);
           ptx::tmem_wait_ld();
-          if (wv == kWaves - 1) {
-            // every value of this half is in registers: release the accumulator
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(tempty0 + 8u * acc);
-          }
-          const int sq = slot_h + wv * 64;
+          // every value is in registers: release the accumulator
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(tempty0 + 8u * h);
           if (tinfo.y < kTileN) {  // mask padding slots (last tile of a group)
+            const int s0 = h * kAccN + slice;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              if (sq + j >= tinfo.y) va[j] = kNone;
-              if (sq + 32 + j >= tinfo.y) vb[j] = kNone;
+              if (s0 + j >= tinfo.y) va[j] = kNone;
+              if (s0 + 32 + j >= tinfo.y) vb[j] = kNone;
             }
           }
           int gm[8];
@@ -437,40 +394,22 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
           gm[7] = min8<24>(vb);
           const int m = min(__vimin3_s32(gm[0], gm[1], gm[2]),
                             __vimin3_s32(__vimin3_s32(gm[3], gm[4], gm[5]), gm[6], gm[7]));
-          if constexpr (DEFERRED) {
-            // improves on earlier tiles (improve_limit) and, strictly, on the
-            // first wave of this tile; the group index is located only when
-            // some lane of the warp improves (rare once the row minima settle)
-            const bool imp = m < min(lim, m_best);
-            if (__any_sync(0xffffffffu, imp)) {
-              // first group of this wave holding m; waves are visited in column order
-              int gi = 7;
+          // the 8-column group is located only when some lane of the warp
+          // improves (rare once the row minima settle): the first group
+          // holding m (column order)
+          const bool imp = m < lim;
+          if (__any_sync(0xffffffffu, imp)) {
+            int gi = 7;
 #pragma unroll
-              for (int k = 6; k >= 0; --k) gi = (gm[k] == m) ? k : gi;
-              if (imp) {
-                m_best = m;
-                gi_best = wv * 8 + gi;
-              }
-            }
-          } else {
-            // vs earlier tiles: improve_limit (ties go to the later-visited,
-            // smaller columns); vs the first wave of this tile: strictly smaller
-            if (m < lim && m < m_best) {
-              // the rare improving lanes resolve the column at once
-              const bool in_a = min(min(gm[0], gm[1]), min(gm[2], gm[3])) == m;
-              const int j = in_a ? first_eq(va, m) : 32 + first_eq(vb, m);
-              m_best = m;
-              gi_best = __ldg(colmap_t + sq + j);
+            for (int k = 6; k >= 0; --k) gi = (gm[k] == m) ? k : gi;
+            if (imp) {
+              best_m = m;
+              best_loc = (h << 3) + gi;
+              lim = m;
             }
           }
         }
-        if constexpr (DEFERRED) {
-          // record the 8-column group, resolve at the segment end
-          if (m_best != kNone)
-            ptx::sts_v2(bst + r * (kBS * 8), make_int2(2 * m_best + tinfo.x, (t << kGiBits) + gi_best));
-        } else {
-          if (m_best != kNone) ptx::sts_v2(bst + r * (kBS * 8), make_int2(2 * m_best + tinfo.x, gi_best));
-        }
+        if (best_m != kNone) ptx::sts_v2(bst_r, make_int2(2 * best_m + tinfo.x, (t << 4) + best_loc));
       }
     }
     // resolve each row's winning 8-column group: recompute its dot products
@@ -487,55 +426,46 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
       const int2 bs = ptx::lds_v2(bst + r * (kBS * 8));
       const int4 rm = p.row_meta[(size_t)(g * RG + r) * kTileM + row];  // {o, R, m, -}
       const bool valid = bs.x != kNone && rm.z >= 0;
-      if constexpr (!DEFERRED) {
-        if (valid) {
-          const long long err = (long long)bs.x + rm.y;
-          const int col = bs.y;
-          const int e_idx = col / S, si = col - e_idx * S;
-          key = ((unsigned long long)err << 32) | (unsigned long long)((e_idx * 8 + iso) * S + si);
-        }
-      } else {
-        long long gmin = valid ? (long long)bs.x + rm.y : LLONG_MAX;
-        gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, 1));
-        gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, 2));
-        gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, 4));
-        const int gbase = lane & ~7;
-        const int j = lane & 7;
-        unsigned tied =
-            (__ballot_sync(0xffffffffu, valid && (long long)bs.x + rm.y == gmin) >> gbase) & 0xffu;
-        while (__any_sync(0xffffffffu, tied != 0)) {
-          const int src = tied ? gbase + __ffs(tied) - 1 : lane;
-          const int loc = __shfl_sync(0xffffffffu, bs.y, src);
-          const int b2 = __shfl_sync(0xffffffffu, bs.x, src);
-          const int t = loc >> kGiBits;
-          const int slot0 = slot_h + (loc & ((1 << kGiBits) - 1)) * 8;
-          int m = 0, kh = 0;
-          if (tied) {
-            m = (b2 - p.tile_info[t].x) >> 1;
-            const int srow = sp * 32 + src;
-            const uint8_t* arow = p.a_tiles + (size_t)(g * RG + r) * (kTileM * KPAD) +
-                                  (srow >> 3) * 128 + (srow & 7) * 16;
-            const int8_t* bcol = p.b_tiles + (size_t)t * kB + (slot0 >> 3) * 128 + j * 16;
+      long long gmin = valid ? (long long)bs.x + rm.y : LLONG_MAX;
+      gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, 1));
+      gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, 2));
+      gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, 4));
+      const int gbase = lane & ~7;
+      const int j = lane & 7;
+      unsigned tied =
+          (__ballot_sync(0xffffffffu, valid && (long long)bs.x + rm.y == gmin) >> gbase) & 0xffu;
+      while (__any_sync(0xffffffffu, tied != 0)) {
+        const int src = tied ? gbase + __ffs(tied) - 1 : lane;
+        const int loc = __shfl_sync(0xffffffffu, bs.y, src);
+        const int b2 = __shfl_sync(0xffffffffu, bs.x, src);
+        const int t = loc >> 4;
+        const int slot0 = ((loc >> 3) & 1) * kAccN + slice + (loc & 7) * 8;
+        int m = 0, kh = 0;
+        if (tied) {
+          m = (b2 - p.tile_info[t].x) >> 1;
+          const int srow = sp * 32 + src;
+          const uint8_t* arow = p.a_tiles + (size_t)(g * RG + r) * (kTileM * KPAD) +
+                                (srow >> 3) * 128 + (srow & 7) * 16;
+          const int8_t* bcol = p.b_tiles + (size_t)t * kB + (slot0 >> 3) * 128 + j * 16;
 #pragma unroll 4
-            for (int kc = 0; kc < chunks; ++kc) {
-              const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(arow + kc * (kTileM * 16)));
-              const uint4 b4 = __ldg(reinterpret_cast<const uint4*>(bcol + kc * (kTileN * 16)));
-              kh = dp4a_us(a4.x, b4.x, kh);
-              kh = dp4a_us(a4.y, b4.y, kh);
-              kh = dp4a_us(a4.z, b4.z, kh);
-              kh = dp4a_us(a4.w, b4.w, kh);
-            }
+          for (int kc = 0; kc < chunks; ++kc) {
+            const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(arow + kc * (kTileM * 16)));
+            const uint4 b4 = __ldg(reinterpret_cast<const uint4*>(bcol + kc * (kTileN * 16)));
+            kh = dp4a_us(a4.x, b4.x, kh);
+            kh = dp4a_us(a4.y, b4.y, kh);
+            kh = dp4a_us(a4.z, b4.z, kh);
+            kh = dp4a_us(a4.w, b4.w, kh);
           }
-          const unsigned hits = (__ballot_sync(0xffffffffu, tied && kh == m) >> gbase) & 0xffu;
-          if (tied) {
-            const int col = p.colmap[(size_t)t * kTileN + slot0 + __ffs(hits) - 1];
-            const int e_idx = col / S, si = col - e_idx * S;
-            const unsigned long long k2 =
-                ((unsigned long long)gmin << 32) |
-                (unsigned long long)((e_idx * 8 + (src & 7)) * S + si);
-            key = k2 < key ? k2 : key;
-            tied &= tied - 1;
-          }
+        }
+        const unsigned hits = (__ballot_sync(0xffffffffu, tied && kh == m) >> gbase) & 0xffu;
+        if (tied) {
+          const int col = p.colmap[(size_t)t * kTileN + slot0 + __ffs(hits) - 1];
+          const int e_idx = col / S, si = col - e_idx * S;
+          const unsigned long long k2 =
+              ((unsigned long long)gmin << 32) |
+              (unsigned long long)((e_idx * 8 + (src & 7)) * S + si);
+          key = k2 < key ? k2 : key;
+          tied &= tied - 1;
         }
       }
       unsigned long long w = __shfl_xor_sync(0xffffffffu, key, 1);
@@ -552,8 +482,9 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, const EpiCtx& x
 // Work order (all roles derive it identically): the CTA's share of
 // (row group, tile) pairs as segments (cta_share / next_seg; one A load and
 // one column resolution per segment); inside a segment: tiles t descending,
-// row tiles r; the (tile, row tile) counter H selects accumulator H % 2,
-// which epilogue group H % 2 drains.
+// row tiles r; the pair counter H and the column half h select accumulator
+// 2 * (H & 1) + h, issued by MMA warp acc and drained by epilogue group
+// H & 1.
 __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int KPAD = p.kpad, RG = p.rg, STAGES = p.stages;
@@ -570,26 +501,27 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   const uint32_t afull_bar = bar_base + 8u * (2 * STAGES + 2 * kNumAcc);
   const uint32_t aempty_bar = afull_bar + 8u;
 
-  const int warp = threadIdx.x >> 5;
+  // warp index through a shuffle: ptxas then treats every role branch and
+  // the issuers' descriptors as warp-uniform (uniform datapath, no per-MMA
+  // R2UR.BROADCAST / divergence checks -- the issue loop halves)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   pdl_trigger();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(full_bar(s), 1);
-      // the MMA commit; plus every epilogue warp when it reads the stage's column map
-      ptx::mbar_init(empty_bar(s), 1);  // the MMA commit
+      ptx::mbar_init(empty_bar(s), kIssuers);  // one commit per MMA warp and tile
     }
     for (int b = 0; b < kNumAcc; ++b) {
       ptx::mbar_init(tfull_bar(b), 1);
-      // G1: all 16 epilogue warps release; else one group of 8 warps per accumulator
-      ptx::mbar_init(tempty_bar(b), p.g1 ? kEpiWarps : kEpiWarps / 2);
+      ptx::mbar_init(tempty_bar(b), kEpiWarps / 2);  // the 8 warps of one epilogue group
     }
     ptx::mbar_init(afull_bar, 1);
-    ptx::mbar_init(aempty_bar, 1);
+    ptx::mbar_init(aempty_bar, kIssuers);
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+  if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -601,81 +533,94 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   const TcPlan plan = *p.plan;
   int g, t0, t1;
 
-  if (warp == 0) {
-    // ---------------- producer (TMA engine bulk copies) ----------------
-    if (lane == 0) {
-      uint32_t L = 0, U = 0;
-      for (SegIter it(plan); it.next(g, t0, t1); ++U) {
-        ptx::mbar_wait_sleep(aempty_bar, (U & 1) ^ 1);
-        ptx::mbar_expect_tx(afull_bar, kA);
-        ptx::bulk_g2s(ptx::smem_u32(sA), p.a_tiles + (size_t)g * kA, kA, afull_bar);
-        for (int t = t1 - 1; t >= t0; --t, ++L) {
-          const int s = L % STAGES;
-          ptx::mbar_wait_sleep(empty_bar(s), ((L / STAGES) & 1) ^ 1);
-          uint8_t* st = sStage + s * kStage;
-          ptx::mbar_expect_tx(full_bar(s), kStage);
-          ptx::bulk_g2s(ptx::smem_u32(st), p.b_tiles + (size_t)t * kB, kB, full_bar(s));
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer (warp-uniform, one elected lane issues) ----------------
+  if (warp < kIssuers) {
+    // ---------------- MMA issuers: warp i owns accumulator i ----------------
+    // Four issuing warps keep four 128-column accumulators in flight: the
+    // issuing thread's own latency (descriptor set-up, barrier waits, commits)
+    // and the commit -> epilogue -> release round trip are both longer than
+    // one accumulator's MMA work, so one issuer over two 256-column
+    // accumulators left the tensor pipe idle ~40% of the time.  Warp 0 also
+    // drives the TMA engine (bulk copies of the A row group per segment and
+    // of the B tiles STAGES - 1 ahead, each right after its own MMAs for a
+    // tile, so a wait for a ring slot overlaps MMAs already issued); 20 warps
+    // = 5 per SM sub-partition keeps the 96-register budget.
+    const int i = warp;
+    const int my_h = i & 1, my_par = i >> 1;
     constexpr uint32_t kIdesc = ptx::idesc_i8(kTileM, kAccN);
     const int ksteps = KPAD / 32;
     // descriptor start-address field is addr >> 4: stepping K by 32 bytes
-    // (two 16-byte core-matrix chunks) adds 2*LBO >> 4
+    // (two 16-byte core-matrix chunks) adds 2*LBO >> 4; column half h starts
+    // h * 128 / 8 core matrices (128 B each) into the B tile
     constexpr uint64_t kAStep = (2 * kTileM * 16) >> 4;
     constexpr uint64_t kBStep = (2 * kTileN * 16) >> 4;
     const uint32_t a_base = ptx::smem_u32(sA);
+    const uint32_t b_half = (uint32_t)my_h * (kAccN / 8) * 128;
+    const uint32_t d = tmem_base + i * kAccN;
+    const uint32_t tfull_i = tfull_bar(i), tempty_i = tempty_bar(i);
+    // producer state (warp 0): its own walk over the same tile sequence
+    SegIter pit(plan);
+    int pg = 0, pt0 = 0, pt = -1;
+    uint32_t PL = 0;
+    auto produce_b = [&]() {
+      if (pt < pt0) {
+        int pt1;
+        if (!pit.next(pg, pt0, pt1)) return;
+        pt = pt1 - 1;
+      }
+      const int s = PL % STAGES;
+      ptx::mbar_wait(empty_bar(s), ((PL / STAGES) & 1) ^ 1);
+      if (lane == 0) {
+        ptx::mbar_expect_tx(full_bar(s), kStage);
+        ptx::bulk_g2s(ptx::smem_u32(sStage + s * kStage), p.b_tiles + (size_t)pt * kB, kB, full_bar(s));
+      }
+      __syncwarp();
+      --pt;
+      ++PL;
+    };
+    if (i == 0)
+      for (int k = 0; k < STAGES - 1; ++k) produce_b();
     uint32_t L = 0, H = 0, U = 0;
     for (SegIter it(plan); it.next(g, t0, t1); ++U) {
-      ptx::mbar_wait_sleep(afull_bar, U & 1);
+      if (i == 0) {
+        // the single A slot: refilled once every MMA of the previous segment completed
+        ptx::mbar_wait(aempty_bar, (U & 1) ^ 1);
+        if (lane == 0) {
+          ptx::mbar_expect_tx(afull_bar, kA);
+          ptx::bulk_g2s(ptx::smem_u32(sA), p.a_tiles + (size_t)g * kA, kA, afull_bar);
+        }
+        __syncwarp();
+      }
+      ptx::mbar_wait(afull_bar, U & 1);
       ptx::tc_fence_after();
       for (int t = t1 - 1; t >= t0; --t, ++L) {
         const int s = L % STAGES;
-        ptx::mbar_wait_sleep(full_bar(s), (L / STAGES) & 1);
+        ptx::mbar_wait(full_bar(s), (L / STAGES) & 1);
         ptx::tc_fence_after();
-        const uint32_t b_addr = ptx::smem_u32(sStage + s * kStage);
-        const uint64_t bd0 = ptx::umma_desc(b_addr, kTileN * 16, 128);
+        const uint64_t bd0 = ptx::umma_desc(ptx::smem_u32(sStage + s * kStage) + b_half, kTileN * 16, 128);
         for (int r = 0; r < RG; ++r, ++H) {
+          if ((int)(H & 1) != my_par) continue;
           const uint64_t ad0 = ptx::umma_desc(a_base + r * (kTileM * KPAD), kTileM * 16, 128);
-          const int acc = H % kNumAcc;
-          ptx::mbar_wait_sleep(tempty_bar(acc), ((H / kNumAcc) & 1) ^ 1);
+          ptx::mbar_wait(tempty_i, ((H >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
-          const uint32_t d = tmem_base + acc * kAccN;
           ptx::umma_i8_elect(d, ad0, bd0, kIdesc, 0u);
           for (int ks = 1; ks < ksteps; ++ks)
             ptx::umma_i8_elect(d, ad0 + ks * kAStep, bd0 + ks * kBStep, kIdesc, 1u);
-          ptx::umma_commit_elect(tfull_bar(acc));
+          ptx::umma_commit_elect(tfull_i);
         }
         ptx::umma_commit_elect(empty_bar(s));
+        if (i == 0) produce_b();
       }
       ptx::umma_commit_elect(aempty_bar);
     }
-  } else if (warp >= 4) {
-    // ---------------- epilogue: 16 warps drain every accumulator ----------------
-    const EpiCtx x{smem, sStage, kStage, kB, bar_base, tmem_base, STAGES, RG, KPAD,
-                   warp, lane, plan};
-    if (p.g1) {
-      if (p.deferred) epilogue_role<true, true>(p, x);
-      else epilogue_role<false, true>(p, x);
-    } else {
-      if (p.deferred) epilogue_role<true, false>(p, x);
-      else epilogue_role<false, false>(p, x);
-    }
-    if (p.fix_fused) {
-      switch (p.fix.n) {
-        case 256: fix_fused_loop<256>(p.fix, lane); break;
-        case 64: fix_fused_loop<64>(p.fix, lane); break;
-        default: fix_fused_loop<16>(p.fix, lane); break;
-      }
-      if (p.tspan && lane == 0) atomicMax(&p.tspan[2], global_ns());
-    }
+  } else if (warp >= kEpiBase) {
+    // ---------------- epilogue: two groups of 8 warps, one column half each ----------------
+    const EpiCtx x{kB, bar_base, tmem_base, RG, KPAD, warp, lane, plan};
+    epilogue_role(p, smem, x);
   }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  if (warp == 2) ptx::tmem_dealloc(tmem_base, 512);
+  if (warp == 1) ptx::tmem_dealloc(tmem_base, 512);
   if (p.tspan && threadIdx.x == 0) atomicMax(&p.tspan[1], global_ns());
 }
 
@@ -930,7 +875,7 @@ __global__ void reach_scatter_kernel(const int4* __restrict__ stats, int64_t nco
 constexpr int kPlanThreads = 1024;
 __global__ void __launch_bounds__(kPlanThreads)
 level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restrict__ dims,
-                  long long b_tile_bytes, int grid,
+                  long long b_tile_bytes, long long rr_bytes, int grid,
                   const int32_t* __restrict__ hist, const long long* __restrict__ reach_counts,
                   int fcols, const int32_t* __restrict__ roff, TcPlan* __restrict__ plan,
                   int4* __restrict__ jobs, long long* __restrict__ prefix,
@@ -947,7 +892,7 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restr
   const int ntiles = (int)dims->ntiles;
   // mode 1 when B does not fit comfortably in L2: span length minimising the
   // per-CTA makespan ceil(units / grid) * (ct + 2) (smallest span count wins)
-  const bool rr = (long long)ntiles * b_tile_bytes > (48ll << 20) && n_rg > 0;
+  const bool rr = (long long)ntiles * b_tile_bytes > rr_bytes && n_rg > 0;
   if (rr) {
     unsigned long long mine = ~0ull;
     const int smax = min(ntiles, 8192);
@@ -1379,9 +1324,9 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   FC_CUDA(c, launch_k(c, level_plan_kernel, dim3(1), dim3(kPlanThreads), 0,
       d_M, RG,
       reinterpret_cast<const TcDims*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes + kUpReachBytes),
-      (long long)kTileN * T.kpad, c->sm_count, d_hist,
+      (long long)kTileN * T.kpad, c->tc_span_units ? 0ll : (48ll << 20), c->sm_count, d_hist,
       reinterpret_cast<const long long*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes),
-      c->fix_fused ? fix_cols_fused(L.n) : fix_cols(L.n), c->roff.as<int32_t>(), d_plan,
+      fix_cols(L.n), c->roff.as<int32_t>(), d_plan,
       c->fix_jobs.as<int4>(),
       c->fix_cols.as<long long>(), d_fplan, c->fix_rows.as<int32_t>(),
       reinterpret_cast<long long*>(d_fix_pairs)));
@@ -1406,11 +1351,6 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   prm.S = L.s_count;
   prm.plan = d_plan;
   prm.tspan = d_time;
-  // measured: with the cooperative per-candidate resolution the deferred
-  // epilogue also wins for long K (c4 B=16: -4%)
-  prm.deferred = c->tc_deferred >= 0 ? c->tc_deferred : 1;
-  prm.g1 = c->tc_g1 >= 0 ? c->tc_g1 : 0;
-  prm.fix_fused = c->fix_fused ? 1 : 0;
   prm.fix.qbase = L.qbase.as<int16_t>();
   prm.fix.a_tiles = c->a_tiles.as<uint8_t>();
   prm.fix.roff = c->roff.as<int32_t>();
@@ -1435,13 +1375,8 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   c->stats.kernel_launches += 1;
 
   // ---- clamp corrections (exact kernel on clamp-active pairs), planned above ----
-  // Fused (FC_FIX_FUSED=1): the contraction's epilogue warps take them from a work
-  // counter once their share is done.  Otherwise a separate kernel, on the
-  // jobs stream when given (both only atomicMin into the same keys).
-  if (c->fix_fused) {
-    if (jobs_stream) FC_CUDA(c, cudaEventRecord(ev_jobs, c->stream));
-    return FC_OK;
-  }
+  // A separate kernel, on the jobs stream when given (both only atomicMin
+  // into the same keys).
   cudaStream_t main = c->stream;
   if (jobs_stream) {
     FC_CUDA(c, cudaEventRecord(ev_plan, main));

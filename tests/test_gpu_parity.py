@@ -400,10 +400,11 @@ def test_full_size_encode_properties(name):
         del q
 
 
-@pytest.mark.parametrize("option,value", [("tc_g1", 1), ("tc_deferred", 0), ("fix_fused", 1),
-                                          ("pdl", 1), ("overlap", 0), ("graph", 0)])
+@pytest.mark.parametrize("option,value", [("tc_span_units", 1), ("pdl", 1), ("overlap", 0),
+                                          ("graph", 0)])
 def test_kernel_variants_give_identical_streams(option, value):
-    """Every execution variant kept for measurement produces the same c2 stream."""
+    """Every execution variant produces the same c2 stream (tc_span_units: the
+    round-robin span schedule c5 uses when B exceeds L2, forced at c2 size)."""
     g = load_golden("encode_c2.npz")
     img = g["image_c2"]
     caps = tuple(int(v) for v in g["caps_c2"])
