@@ -353,12 +353,14 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, uint8_t* smem, 
     for (int t = t1 - 1; t >= t0; --t) {
       const int2 tinfo = tinfo_next;  // {parity, valid slots}
       if (t > t0) tinfo_next = p.tile_info[t - 1];
+      // this group's pairs of the tile: Hr = Ht + r with (Hr & 1) == gq
+      const uint32_t Ht = H;
+      H += RG;
 #pragma unroll 1
-      for (int r = 0; r < RG; ++r, ++H) {
-        if ((int)(H & 1) != gq) continue;
+      for (int r = (gq ^ (int)(Ht & 1)) & 1; r < RG; r += 2) {
         const uint32_t bst_r = bst + r * (kBS * 8);
         const int2 bs = ptx::lds_v2(bst_r);
-        const uint32_t ph = (H >> 1) & 1;
+        const uint32_t ph = ((Ht + r) >> 1) & 1;
         // half 0 vs earlier tiles: improve_limit (ties go to the later-visited,
         // smaller columns); half 1 vs half 0 of this tile: strictly smaller
         int lim = improve_limit(bs.x, tinfo.x);
@@ -597,10 +599,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
         ptx::mbar_wait(full_bar(s), (L / STAGES) & 1);
         ptx::tc_fence_after();
         const uint64_t bd0 = ptx::umma_desc(ptx::smem_u32(sStage + s * kStage) + b_half, kTileN * 16, 128);
-        for (int r = 0; r < RG; ++r, ++H) {
-          if ((int)(H & 1) != my_par) continue;
+        // this issuer's pairs of the tile: Hr = Ht + r with (Hr & 1) == my_par
+        const uint32_t Ht = H;
+        H += RG;
+        for (int r = (my_par ^ (int)(Ht & 1)) & 1; r < RG; r += 2) {
           const uint64_t ad0 = ptx::umma_desc(a_base + r * (kTileM * KPAD), kTileM * 16, 128);
-          ptx::mbar_wait(tempty_i, ((H >> 1) & 1) ^ 1);
+          ptx::mbar_wait(tempty_i, (((Ht + r) >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
           ptx::umma_i8_elect(d, ad0, bd0, kIdesc, 0u);
           for (int ks = 1; ks < ksteps; ++ks)
