@@ -62,36 +62,35 @@ def s_histogram(image: GrayImage, config: EncoderConfig, context=None) -> SHisto
         return errs
 
     _, lv, jj = _quadtree(image.width, image.height, config.thresholds, match_fn)
-    nb = len(S_BIN_EDGES) - 1
-    raw_counts = np.zeros((4, nb), dtype=np.int64)
-    clamped_counts = np.zeros_like(raw_counts)
-    raw_means, clamped_means, coded = [], [], []
-    for level in (1, 2, 3, 4):
-        values = s_by_level[level][jj[lv == level]] if level in s_by_level else np.zeros(0)
-        coded.append(int(values.size))
-        if values.size:
-            raw_counts[level - 1] = np.histogram(
-                np.clip(values, S_BIN_EDGES[0], S_BIN_EDGES[-1]), bins=S_BIN_EDGES)[0]
-            clamped_counts[level - 1] = np.histogram(np.clip(values, 0.0, 1.0), bins=S_BIN_EDGES)[0]
-            raw_means.append(float(values.mean()))
-            clamped_means.append(float(np.clip(values, 0.0, 1.0).mean()))
-        else:
-            raw_means.append(None)
-            clamped_means.append(None)
+    coded_by_level = [s_by_level[level][jj[lv == level]] if level in s_by_level else np.zeros(0)
+                      for level in (1, 2, 3, 4)]
+    raw, clamped = _slope_histograms(coded_by_level)
+    stats = [(int(v.size), float(v.mean()) if v.size else None,
+              float(np.clip(v, 0.0, 1.0).mean()) if v.size else None) for v in coded_by_level]
+    coded, raw_means, clamped_means = (tuple(c) for c in zip(*stats))
     return SHistogram(pool_size=config.pool.pool_cap, bin_edges=S_BIN_EDGES.copy(),
-                      raw_counts=raw_counts, clamped_counts=clamped_counts,
-                      coded_blocks=tuple(coded), raw_means=tuple(raw_means),
-                      clamped_means=tuple(clamped_means))
+                      raw_counts=raw, clamped_counts=clamped, coded_blocks=coded,
+                      raw_means=raw_means, clamped_means=clamped_means)
+
+
+def _slope_histograms(values_by_level):
+    """[4, bins] counts of the coded slopes per level: the raw slope saturated
+    to the edge range, and the slope clamped to [0, 1] (the coder's range)."""
+    lo, hi = float(S_BIN_EDGES[0]), float(S_BIN_EDGES[-1])
+    out = np.zeros((2, 4, len(S_BIN_EDGES) - 1), dtype=np.int64)
+    for li, v in enumerate(values_by_level):
+        if v.size == 0:
+            continue
+        for k, (a, b) in enumerate(((lo, hi), (0.0, 1.0))):
+            out[k, li] = np.histogram(np.minimum(np.maximum(v, a), b), bins=S_BIN_EDGES)[0]
+    return out[0], out[1]
 
 
 def shist_rows(hist: SHistogram) -> list:
-    """Flatten an SHistogram into CSV rows (bench.py:196-212)."""
-    rows = []
-    for level in (1, 2, 3, 4):
-        for b in range(hist.raw_counts.shape[1]):
-            rows.append({"pool_size": hist.pool_size, "level": level,
-                         "bin_low": round(float(hist.bin_edges[b]), 4),
-                         "bin_high": round(float(hist.bin_edges[b + 1]), 4),
-                         "raw_count": int(hist.raw_counts[level - 1, b]),
-                         "clamped_count": int(hist.clamped_counts[level - 1, b])})
-    return rows
+    """One dict per (level, bin) with the SHIST_COLUMNS keys (bench.py:196-212)."""
+    nb = hist.raw_counts.shape[1]
+    lows = [round(float(x), 4) for x in hist.bin_edges[:nb]]
+    highs = [round(float(x), 4) for x in hist.bin_edges[1:nb + 1]]
+    return [dict(zip(SHIST_COLUMNS, (hist.pool_size, li + 1, lows[b], highs[b],
+                                     int(hist.raw_counts[li, b]), int(hist.clamped_counts[li, b]))))
+            for li in range(4) for b in range(nb)]

@@ -6,9 +6,9 @@ range-domain search run on the B200 through the C ABI; the host keeps the
 quadtree bookkeeping (split rule codec.py:132-141, depth-first leaf order
 codec.py:145-161) and assembles the records and the FRAK stream.
 
-``decode`` is the reference's attractor iteration (codec.py:269-363) on the
-host; it is outside the accelerated path this round and serves the decoded
-PSNR parity check.
+``decode`` / ``decode_trace`` are the reference's attractor iteration
+(codec.py:269-363), run on the device (fc_decode); the host only lays out
+the leaf table.
 """
 
 from __future__ import annotations
@@ -17,13 +17,12 @@ import time
 from dataclasses import dataclass, field
 
 import numpy as np
-from numpy.lib.stride_tricks import sliding_window_view
 
 from . import _native
-from .image import GrayImage, apply_isometry, decimate_tile
-from .matcher import BASELINE, PATHS, PROPOSED, SPolicy
+from .image import GrayImage
+from .matcher import BASELINE, PATHS, PROPOSED, SPolicy, split_index, stored_offsets
 from .pool import LEVEL_RANGE_SIDES, CoordTable, PoolParams, build_pool
-from .stream import CompressedStream, RecordTable, header_bytes, iter_leaves
+from .stream import CompressedStream, RecordTable, header_bytes, leaf_origins
 
 TOP_SIDE = 16
 
@@ -353,14 +352,9 @@ def encode_levelwise(image: GrayImage, config: EncoderConfig, context=None, devi
         err, idx, rmean = scans[level]
         j = leaf_j[sel]
         S = len(policy.s_set(level))
-        e, rem = np.divmod(idx[j], 8 * S)
-        iso, si = np.divmod(rem, S)
-        if baseline:
-            sv = np.asarray(policy.s_set(level), dtype=np.float64)
-            dm = pool.means(level)
-            o = np.clip(np.rint(rmean[j] - sv[si] * dm[e]), 0, 255).astype(np.int64)
-        else:
-            o = np.rint(rmean[j]).astype(np.int64)
+        e, iso, si = split_index(idx[j], S)
+        o = stored_offsets(rmean[j], e, si, policy.s_set(level),
+                           pool.means(level) if baseline else None, baseline)
         offs[sel], isos[sel], addrs[sel], sidx[sel], errs[sel] = o, iso, e, si, err[j]
     records = RecordTable(np.stack([steps, offs, isos, addrs, sidx], axis=1))
     stream = CompressedStream(
@@ -375,94 +369,49 @@ def encode_levelwise(image: GrayImage, config: EncoderConfig, context=None, devi
 
 
 # ---------------------------------------------------------------------------
-# decoder (host; codec.py:257-363 semantics)
+# decoder (codec.py:257-363 semantics, on the device: fc_decode)
 # ---------------------------------------------------------------------------
 
-def _plans(stream: CompressedStream):
-    rows = {1: [], 2: [], 3: [], 4: []}
-    for rec, x, y, _side in iter_leaves(stream):
-        rows[rec.step].append((rec.domain_address, rec.isometry, rec.s_index, rec.offset, x, y))
-    plans = []
-    for level in (1, 2, 3, 4):
-        if not rows[level]:
-            continue
-        a = np.array(rows[level], dtype=np.int64)
-        b = LEVEL_RANGE_SIDES[level - 1]
-        coords = np.asarray(CoordTable(stream.pools[level - 1]).array, dtype=np.int64)
-        dom = coords[a[:, 0]]
-        svals = np.asarray(stream.s_sets[level - 1], dtype=np.float64)[a[:, 2]]
-        span = np.arange(b)
-        scatter = ((a[:, 5][:, None, None] + span[None, :, None]) * stream.width
-                   + a[:, 4][:, None, None] + span[None, None, :]).ravel()
-        groups = [(iso, np.nonzero(a[:, 1] == iso)[0]) for iso in range(8)]
-        plans.append((2 * b, dom[:, 0], dom[:, 1], [g for g in groups if g[1].size], svals,
-                      a[:, 3].astype(np.int32), scatter, b * b))
-    return plans
-
-
-def _collage_pass(cur: np.ndarray, plans, proposed: bool) -> np.ndarray:
-    out = np.empty_like(cur)
-    for dside, dx, dy, groups, svals, offs, scatter, n in plans:
-        win = sliding_window_view(cur, (dside, dside))
-        dec = decimate_tile(win[dy, dx])
-        tiles = np.empty_like(dec)
-        for iso, idx in groups:
-            tiles[idx] = apply_isometry(dec[idx], iso)
-        if proposed:
-            means = tiles.reshape(tiles.shape[0], -1).astype(np.int64).sum(axis=1) / n
-            q = np.rint(svals[:, None, None] * (tiles - means[:, None, None]))
-        else:
-            q = np.rint(svals[:, None, None] * tiles.astype(np.float64))
-        v = q.astype(np.int32) + offs[:, None, None]
-        np.clip(v, 0, 255, out=v)
-        out.flat[scatter] = v.ravel()
-    return out
-
-
-def decode_trace(stream: CompressedStream, iterations: int = 15, tolerance: int = 0):
-    if iterations < 1:
-        raise ValueError("iterations must be >= 1")
-    if tolerance < 0:
-        raise ValueError("tolerance must be >= 0")
-    plans = _plans(stream)
-    proposed = stream.mode == PROPOSED
-    cur = np.full((stream.height, stream.width), 128, dtype=np.uint8)
-    deltas = []
-    for _ in range(iterations):
-        new = _collage_pass(cur, plans, proposed)
-        delta = int(np.abs(new.astype(np.int16) - cur.astype(np.int16)).max())
-        cur = new
-        deltas.append(delta)
-        if delta <= tolerance:
-            break
-    return GrayImage(cur), deltas
-
-
-def decode(stream: CompressedStream, iterations: int = 15, tolerance: int = 0) -> GrayImage:
-    return decode_trace(stream, iterations, tolerance)[0]
-
-
-def decode_trace_device(stream: CompressedStream, iterations: int = 15, tolerance: int = 0,
-                        context=None):
-    """decode_trace on the device (fc_decode: one launch per collage pass, one
-    host synchronisation per decode) -> (GrayImage, deltas); the same image
-    and deltas as the host decode_trace (tests/test_gpu_parity.py)."""
+def decode_trace(stream: CompressedStream, iterations: int = 15, tolerance: int = 0,
+                 context=None):
+    """Iterate the collage map from a constant-128 image (codec.py:339-363):
+    -> (GrayImage, per-pass max |delta|), stopping once a pass changes no
+    pixel by more than ``tolerance``.  Runs on the device (fc_decode: one
+    launch per pass, one host synchronisation per decode); bit-identical to
+    the reference's host decoder (tests/test_gpu_parity.py against oracle/)."""
     if iterations < 1:
         raise ValueError("iterations must be >= 1")
     if tolerance < 0:
         raise ValueError("tolerance must be >= 0")
     ctx = context if context is not None else _native.default_context()
-    rows = []
-    pools = [np.asarray(CoordTable(p).array, dtype=np.int64) for p in stream.pools]
-    for rec, x, y, _side in iter_leaves(stream):
-        dx, dy = pools[rec.step - 1][rec.domain_address]
-        rows.append((x, y, rec.step, int(dx), int(dy), rec.isometry, rec.s_index, rec.offset))
-    leaves = np.array(rows, dtype=np.int32).reshape(-1, 8)
+    leaves = decoder_leaves(stream)
     img, deltas = ctx.decode(leaves, stream.width, stream.height, stream.s_sets,
                              stream.mode == PROPOSED, iterations, tolerance)
     return GrayImage(img), deltas
 
 
-def decode_device(stream: CompressedStream, iterations: int = 15, tolerance: int = 0,
-                  context=None) -> GrayImage:
-    return decode_trace_device(stream, iterations, tolerance, context)[0]
+def decode(stream: CompressedStream, iterations: int = 15, tolerance: int = 0,
+           context=None) -> GrayImage:
+    return decode_trace(stream, iterations, tolerance, context)[0]
+
+
+def decoder_leaves(stream: CompressedStream) -> np.ndarray:
+    """int32 [leaves, 8] rows (x, y, step, domain x, domain y, isometry, s
+    index, offset) in record order: the decoder kernel's input."""
+    rec = stream.records.array if isinstance(stream.records, RecordTable) else \
+        RecordTable(stream.records).array
+    x, y, _side = leaf_origins(stream)
+    out = np.empty((rec.shape[0], 8), dtype=np.int32)
+    out[:, 0], out[:, 1], out[:, 2] = x, y, rec[:, 0]
+    for level in (1, 2, 3, 4):
+        sel = rec[:, 0] == level
+        if sel.any():
+            coords = np.asarray(CoordTable(stream.pools[level - 1]).array, dtype=np.int32)
+            out[sel, 3:5] = coords[rec[sel, 3]]
+    out[:, 5], out[:, 6], out[:, 7] = rec[:, 2], rec[:, 4], rec[:, 1]
+    return out
+
+
+# device names kept for callers of the earlier API
+decode_trace_device = decode_trace
+decode_device = decode

@@ -11,10 +11,6 @@ class EmptyPoolError(Exception):
     """The domain pool has no entries at the requested level (matcher.py:34)."""
 
 
-class DomainFlatError(Exception):
-    """The domain tile is constant, so the least-squares slope is undefined (matcher.py:38)."""
-
-
 def raise_for_status(rc: int, msg: str):
     from . import _native as N
 

@@ -256,22 +256,25 @@ def _adopt_device_image(ctx, dev, image: GrayImage):
 
 
 def block_entropy(tile) -> float:
-    """Entropy (nats) of the 256-bin histogram of one tile (host helper)."""
+    """Entropy in nats of a tile's 256-bin histogram (pool.py:95-103), host
+    helper: the same float64 terms as the device kernel (the run-time numpy
+    LUT of p*log(p) for the tile size) summed in bin order by numpy."""
     a = np.asarray(tile)
-    if a.size == 0:
+    n = a.size
+    if n == 0:
         raise ValueError("tile must be non-empty")
-    counts = np.bincount(a.astype(np.int64).ravel(), minlength=256)
-    if counts.shape[0] != 256:
+    flat = a.astype(np.int64).ravel()
+    if flat.min() < 0 or flat.max() > 255:
         raise ValueError("pixel values must lie in [0, 255]")
-    p = counts.reshape(1, 256) / a.size
-    return float(-(p * np.log(np.where(counts.reshape(1, 256) > 0, p, 1.0))).sum(axis=1)[0])
+    counts = np.bincount(flat, minlength=256)
+    p = counts / n
+    logs = np.log(np.where(counts > 0, p, 1.0))
+    return float(-(p * logs).reshape(1, 256).sum(axis=1)[0])
 
 
 def candidate_count(image_size, domain_side: int, stride: int) -> int:
-    if isinstance(image_size, (tuple, list)):
-        w, h = image_size
-    else:
-        w = h = image_size
-    if domain_side > w or domain_side > h:
-        return 0
-    return ((w - domain_side) // stride + 1) * ((h - domain_side) // stride + 1)
+    """Lattice windows of side ``domain_side`` at ``stride`` (pool.py:106-117):
+    the level's candidate count before any truncation."""
+    w, h = image_size if isinstance(image_size, (tuple, list)) else (image_size, image_size)
+    per_axis = [(dim - domain_side) // stride + 1 if dim >= domain_side else 0 for dim in (w, h)]
+    return per_axis[0] * per_axis[1]

@@ -11,7 +11,7 @@ import oracle as O
 import paper_1502_00324_b200 as fc
 from paper_1502_00324_b200 import _native
 from paper_1502_00324_b200 import workloads as W
-from conftest import load_golden
+from conftest import load_golden, oracle_collage_ssd, oracle_encoding
 
 pytestmark = pytest.mark.gpu
 
@@ -325,26 +325,29 @@ def test_range_sharded_slabs_concatenate_to_the_full_encode(world):
 
 @pytest.mark.parametrize("tag", ["c2", "c3_1"])
 @pytest.mark.parametrize("tolerance", [0, 2])
-def test_device_decoder_matches_host_decoder(tag, tolerance):
-    """fc_decode (one launch per collage pass) reproduces the host decoder's
-    image and per-pass deltas bit for bit, including the early stop."""
+def test_device_decoder_matches_reference_decoder(tag, tolerance):
+    """fc_decode (one launch per collage pass) reproduces the reference
+    decoder's image and per-pass deltas bit for bit (oracle restatement of
+    codec.py:319-363), including the early stop."""
     g = load_golden("encode_c2.npz")
     stream = fc.deserialize(g[f"bytes_{tag}"].tobytes())
-    want, wd = fc.decode_trace(stream, 15, tolerance)
-    got, gd = fc.decode_trace_device(stream, 15, tolerance)
+    want, wd = O.decode(oracle_encoding(stream), 15, tolerance)
+    got, gd = fc.decode_trace(stream, 15, tolerance)
     assert gd == wd
-    assert np.array_equal(got.pixels, want.pixels)
+    assert np.array_equal(got.pixels, want)
 
 
-@pytest.mark.parametrize("tag", ["tiled_baseline", "darkbright_baseline", "noise", "flat"])
+@pytest.mark.parametrize("tag", ["tiled_baseline", "darkbright_baseline", "noise", "flat",
+                                 "tiled_proposed", "c1"])
 def test_device_decoder_golden_cases(tag):
-    """Baseline-mode and edge streams of the golden set: device == host decode,
-    PSNR as recorded by the reference."""
+    """Both modes and edge streams of the golden set: the device decode equals
+    the image and per-pass deltas the REFERENCE decoder recorded, and the
+    PSNR it recorded."""
     g = load_golden("encode_cases.npz")
     stream = fc.deserialize(g[f"bytes_{tag}"].tobytes())
-    want = fc.decode(stream)
-    got = fc.decode_device(stream)
-    assert np.array_equal(got.pixels, want.pixels)
+    got, deltas = fc.decode_trace(stream)
+    assert np.array_equal(got.pixels, g[f"decoded_{tag}"])
+    assert deltas == list(g[f"deltas_{tag}"])
     p, ref = fc.psnr(fc.GrayImage(g[f"image_{tag}"]), got), float(g[f"psnr_{tag}"])
     assert p == ref or abs(p - ref) < 0.01
 
@@ -358,9 +361,6 @@ def test_full_size_encode_properties(name):
       collage SSD (the reference's test_codec.py:77-86 property);
     * a random sample of leaves, re-matched by the oracle's C scan against the
       device pool, gives the same (error, domain, isometry, s, offset)."""
-    from paper_1502_00324_b200.codec import _collage_pass, _plans
-    from paper_1502_00324_b200.stream import iter_leaves
-
     wl = W.WORKLOADS[name]
     img = wl.image(0)
     taus = tuple(None if one else t for one, t in zip(wl.cap_one, wl.taus))
@@ -371,12 +371,11 @@ def test_full_size_encode_properties(name):
     ctx = _native.Context(0)
     stream, report = fc.encode(fc.GrayImage(img), cfg, context=ctx)
     # (1) collage pass on the original == the sum of the leaf errors
-    out = _collage_pass(img, _plans(stream), True)
-    ssd = int(((out.astype(np.int64) - img.astype(np.int64)) ** 2).sum())
-    assert ssd == report.collage_ssd
+    assert oracle_collage_ssd(stream, img) == report.collage_ssd
     # (2) sampled leaves against the oracle's exhaustive scan over the device pool
     pool = fc.build_pool(fc.GrayImage(img), params, context=ctx)  # same pool, rebuilt
-    leaves = iter_leaves(stream)
+    lx, ly, lside = fc.leaf_origins(stream)
+    leaves = [(rec, int(x), int(y), int(sd)) for rec, x, y, sd in zip(stream.records, lx, ly, lside)]
     rng = np.random.default_rng(7)
     pick = rng.choice(len(leaves), size=min(48, len(leaves)), replace=False)
     by_level = {}

@@ -8,8 +8,9 @@ import pytest
 
 import paper_1502_00324_b200 as fc
 from paper_1502_00324_b200 import _native, stream as st
-from paper_1502_00324_b200.codec import _collage_pass, _plans, _quadtree
-from conftest import ROOT, load_golden
+import oracle as O
+from paper_1502_00324_b200.codec import _quadtree
+from conftest import ROOT, load_golden, oracle_collage_ssd, oracle_encoding
 
 
 def _header_symbols():
@@ -57,15 +58,17 @@ def test_stream_roundtrip_and_decoder_on_golden(golden, tag):
     assert fc.serialize(s) == data
     recs = np.array([(r.step, r.offset, r.isometry, r.domain_address, r.s_index) for r in s.records])
     assert np.array_equal(recs, g[f"records_{tag}"])
+    # leaf origins (Z-order decode) == the oracle's depth-first walk
+    enc = oracle_encoding(s)
+    walk = O.iter_leaves(enc.width, enc.height, enc.records)
+    x, y, side = fc.leaf_origins(s)
+    assert list(zip(x.tolist(), y.tolist(), side.tolist())) == [(a, b, c) for _, a, b, c in walk]
     if tag != "lena256":
-        dec, deltas = fc.decode_trace(s)
-        assert np.array_equal(dec.pixels, g[f"decoded_{tag}"])
+        dec, deltas = O.decode(enc)
+        assert np.array_equal(dec, g[f"decoded_{tag}"])
         assert deltas == list(g[f"deltas_{tag}"])
     # encoder bookkeeping == one decoder pass on the original (test_codec.py:77-86)
-    img = g[f"image_{tag}"]
-    out = _collage_pass(img, _plans(s), proposed=(s.mode == fc.PROPOSED))
-    d = out.astype(np.int64) - img.astype(np.int64)
-    assert int((d * d).sum()) == int(g[f"collage_{tag}"])
+    assert oracle_collage_ssd(s, g[f"image_{tag}"]) == int(g[f"collage_{tag}"])
 
 
 def test_stream_error_taxonomy():
