@@ -313,8 +313,8 @@ def encode_levelwise(image: GrayImage, config: EncoderConfig, context=None, devi
 
             raise EmptyPoolError(f"no domain entries at level {level}")
         lvl_path = path
-        if path == _native.PATH_TENSOR and (baseline or level == 4):
-            lvl_path = _native.PATH_EXACT  # the contraction covers proposed mode, B >= 4
+        if path == _native.PATH_TENSOR and level == 4:
+            lvl_path = _native.PATH_EXACT  # the contraction covers B >= 4 (both modes)
         t0 = time.perf_counter()
         ctx.level_prepare(level, baseline, policy.s_set(level), lvl_path)
         t1 = time.perf_counter()

@@ -130,9 +130,9 @@ int prepare_begin(Ctx* c, Level& L, int level, int baseline, const double* svals
   L.prepared = false;
   L.tc.ready = false;
   *needs_prep = 1;
-  const bool tc_ok = !L.baseline && L.n >= 16;
+  const bool tc_ok = L.n >= 16;  // both modes (baseline: u8 x u8, epilogue forms o per pair)
   if (path == FC_PATH_TENSOR && !tc_ok)
-    return set_error(c, FC_ERR_ARG, "tensor path needs proposed mode and B >= 4");
+    return set_error(c, FC_ERR_ARG, "tensor path needs B >= 4");
   bool want_tc = path == FC_PATH_TENSOR || (path == FC_PATH_AUTO && tc_ok);
   if (want_tc && L.count * L.s_count >= (1ll << 31) - 1024) {
     if (path == FC_PATH_TENSOR) return set_error(c, FC_ERR_ARG, "too many columns");
@@ -276,7 +276,7 @@ void fc_ctx_destroy(fc_ctx* c) {
   for (auto& b : c->lut) b.release();
   for (auto& L : c->lv) {
     DevBuf* lb[] = {&L.xy, &L.ent, &L.tiles, &L.sum, &L.sumsq, &L.mean, &L.cnorm, &L.qbase,
-                    &L.tc.b_tiles, &L.tc.hq, &L.tc.meta, &L.tc.tile_q1, &L.tc.col_stats,
+                    &L.tc.b_tiles, &L.tc.bconst, &L.tc.meta, &L.tc.tile_q1, &L.tc.col_stats,
                     &L.tc.reach_low, &L.tc.reach_high, &L.tc.odd, &L.svals_d, 
                     &L.win_ent, &L.win_key, &L.win_key2, &L.win_val, &L.win_val2};
     for (DevBuf* b : lb) b->release();

@@ -51,11 +51,6 @@ __global__ void encode_init_kernel(int nxt, int32_t first, int32_t n_top, int64_
   codes[i] = i * 64;
 }
 
-__device__ __forceinline__ int baseline_offset(double rmean, double s, double dmean) {
-  // codec.py:214-218 (== _scan.py:39-43): clip(rint(rmean - s*dmean), 0, 255)
-  const int o = (int)rint(__dsub_rn(rmean, __dmul_rn(s, dmean)));
-  return o < 0 ? 0 : (o > 255 ? 255 : o);
-}
 
 // Split test, leaf records and children in one pass.  A leaf writes its
 // record {step, offset, iso, addr, sidx, err} into the slot of its depth-first
@@ -192,7 +187,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   for (int l = 0; l < kLevels; ++l) {
     Level& L = c->lv[l];
     lpath[l] = path;
-    if (path == FC_PATH_TENSOR && (baseline || L.n < 16)) lpath[l] = FC_PATH_EXACT;
+    if (path == FC_PATH_TENSOR && L.n < 16) lpath[l] = FC_PATH_EXACT;
     int needs = 0;
     if (L.count > 0)
       FC_TRY(prepare_begin(c, L, l + 1, baseline, sv, s_counts[l], lpath[l], &pending[l], &needs));

@@ -79,13 +79,14 @@ struct TcOperands {
   bool ready = false;
   int planes = 1;        // int8 planes of q (1 or 2)
   int m_digits = 1;      // base-255 digit slots carrying hq = floor(Q2/2) in the K extra block
-  int kpad = 0;          // K bytes per row: planes*B*B + m_digits + 4, padded to 32
+                         // (proposed mode; 0 in baseline mode: no extra block)
+  int kpad = 0;          // K bytes per row: planes*B*B + m_digits + 4 (baseline: B*B), padded to 32
   int64_t ncols = 0;     // real columns E*S
   int64_t ntiles = 0;    // bound on the 256-column tiles: ceil(ncols / 256) + 1 (the
                          // two parity groups are each padded; the exact count and
                          // group sizes are computed on the device, TcDims)
   DevBuf b_tiles;        // int8 [ntiles][kpad/16][32 groups][8][16]   (UMMA K-major, no swizzle)
-  DevBuf hq;             // (unused; kept for ABI-stable struct layout in tools)
+  DevBuf bconst;         // baseline mode: int4 [ncols] per column {W', 2 Q1, Q2, tie mask} (slot order)
   DevBuf meta;           // uint32 [ntiles*256]: (Q2 & 1) << 31 | column, 0xffffffff = padding
   DevBuf tile_q1;        // device tables: cursors [2048 i32] | reach counts [512 i64] | TcDims | tile info
   DevBuf col_stats;      // int4 [ncols]: {Q1, Q2, qmin, qmax} (unsorted order)
@@ -215,6 +216,13 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 #endif
 #ifdef __CUDACC__
+// baseline-mode offset of a (range, domain, s) candidate
+__device__ __forceinline__ int baseline_offset(double rmean, double s, double dmean) {
+  // codec.py:214-218 (== _scan.py:39-43): clip(rint(rmean - s*dmean), 0, 255)
+  const int o = (int)rint(__dsub_rn(rmean, __dmul_rn(s, dmean)));
+  return o < 0 ? 0 : (o > 255 ? 255 : o);
+}
+
 // Programmatic dependent launch (PDL).  Kernels launched with launch_k() may
 // start while their stream predecessor is still running: they call
 // pdl_trigger() (let their own successor launch) and pdl_wait() (block until

@@ -327,8 +327,9 @@ struct QLevel {
   int32_t* odd;
   unsigned* hist;       // qmin | qmax | q2max (block-aggregated), stats levels only
   int32_t* chunk_odd;   // odd columns per 1024-column chunk, stats levels only
+  int4* bconst;         // baseline stats levels: tensor-epilogue column constants
   int64_t ncols;
-  int S, n, baseline, stats;
+  int S, n, baseline, stats, shift;
   int block_begin, nblocks;
 };
 struct QParams {
@@ -402,7 +403,41 @@ __device__ __forceinline__ void qprep_level(const QLevel& L, int block, unsigned
       hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
     const bool lead = valid && part == 0;
-    if (lead) {
+    if (lead && L.baseline) {
+      // baseline mode (u8 x u8 contraction, fc_scan_tc.cu): the epilogue forms
+      // o = clip(rint(rmean - s*dmean), 0, 255) per (range, column) from the
+      // range sum R1 with integer ops.  With V = n * fl(s * dmean) (exact,
+      // n a power of two) the reference's fp64 rmean - s*dmean equals
+      // (R1 - V) / n exactly, so rint is floor((R1 + W') / n) with
+      // W' = floor(n/2 - V) when V is not an integer, and round-half-even
+      // (R1 + W' + ((R1 - V) >> shift & 1)) >> shift with W' = n/2 - 1 - V
+      // (tie mask set) when it is.  Clamping (q + o > 255) needs o >= 256 -
+      // qmax, i.e. a range sum from about V + n (256 - qmax) - n/2 on: the
+      // column's clamp bucket b = floor(R1_min / n), rounded DOWN so the
+      // correction lists only ever over-include (an exactly evaluated pair
+      // is exact either way).  The bucket rides in the qmax slot as 256 - b
+      // so the proposed-mode reach tables apply unchanged (qmin slot 0:
+      // q + o never drops below 0).
+      const int64_t e = col / S;
+      const int si = (int)(col - e * S);
+      const double V = __dmul_rn(L.svals[si], L.mean[e]) * (double)L.n;
+      const int half = L.n >> 1;
+      const bool whole = floor(V) == V;
+      const int W = whole ? half - 1 - (int)V : (int)floor((double)half - V);
+      int bucket = 256;
+      if (hi > 0) {
+        const double X = V + (double)(L.n * (256 - hi) - half);
+        long long A = (long long)floor(X) - 1;
+        if (A < 0) A = 0;
+        if (A <= 255ll * L.n) bucket = (int)(A >> L.shift);
+      }
+      L.col_stats[col] = make_int4(s1, s2, 0, 256 - bucket);
+      L.bconst[col] = make_int4(W, 2 * s1, s2, whole ? -1 : 0);
+      L.odd[col] = 0;  // no parity groups: columns stay in candidate order
+      atomicAdd(&sh[512], 1u);
+      atomicAdd(&sh[1024 + 256 - bucket + 512], 1u);
+      atomicMax(&sh[2048], (unsigned)s2);
+    } else if (lead) {
       L.col_stats[col] = make_int4(s1, s2, lo, hi);
       L.odd[col] = s2 & 1;  // == s1 & 1
       atomicAdd(&sh[lo + 512], 1u);
@@ -410,7 +445,7 @@ __device__ __forceinline__ void qprep_level(const QLevel& L, int block, unsigned
       atomicMax(&sh[2048], (unsigned)s2);
     }
     // a warp's columns never straddle a 1024-column chunk (32 / LPC divides 1024)
-    const unsigned oddb = __ballot_sync(0xffffffffu, lead && (s2 & 1));
+    const unsigned oddb = __ballot_sync(0xffffffffu, lead && !L.baseline && (s2 & 1));
     if (lane == 0 && oddb) {
       const int64_t col0 = (base + (threadIdx.x & ~31)) / LPC;
       atomicAdd(&L.chunk_odd[col0 >> 10], __popc(oddb));
@@ -559,6 +594,8 @@ int prep_launch(Ctx* c, Level* const* levels, const int* stats, int count) {
     if (stats[i]) {
       FC_CUDA(c, T.col_stats.reserve(cols * 16 + 16));
       FC_CUDA(c, T.odd.reserve(cols * 8 + 16));
+      // padded to whole 256-column tiles: the epilogue stages a tile's constants unconditionally
+      if (L.baseline) FC_CUDA(c, T.bconst.reserve(((cols + 255) / 256 + 1) * 256 * 16));
       T.ncols = cols;
       any_stats = 1;
     }
@@ -577,6 +614,8 @@ int prep_launch(Ctx* c, Level* const* levels, const int* stats, int count) {
     Q.n = L.n;
     Q.baseline = L.baseline;
     Q.stats = stats[i];
+    Q.bconst = L.baseline && stats[i] ? T.bconst.as<int4>() : nullptr;
+    Q.shift = L.n == 256 ? 8 : L.n == 64 ? 6 : L.n == 16 ? 4 : 2;
     const int lpc = L.n >= 8 ? L.n / 8 : 1;
     Q.nblocks = (int)std::min<int64_t>((cols * lpc + 255) / 256, c->sm_count * 2);
     Q.block_begin = qblocks;

@@ -164,6 +164,12 @@ struct FixArgs {
   const int32_t* list_high;
   unsigned long long* keys;
   int S, kpad, n;
+  // baseline mode: the offset depends on (range, column), formed as the
+  // reference does from the exact means (roff then holds the range bucket)
+  int baseline;
+  const double* rmean;
+  const double* dmean;
+  const double* svals;
 };
 
 template <int N, int CPL>
@@ -190,8 +196,20 @@ __device__ __forceinline__ void fix_unit(const FixArgs& F, const long long* __re
     valid[c] = ci < job.w;
     col[c] = valid[c] ? list[ci] : list[c0];  // padding lanes repeat a real column
   }
-  const int o = F.roff[m];
-  const unsigned o2 = (unsigned)o | ((unsigned)o << 16);
+  unsigned o2c[CPL];
+  if (F.baseline) {
+    const double rm = F.rmean[m];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int e = col[c] / F.S, si = col[c] - e * F.S;
+      const unsigned o = (unsigned)baseline_offset(rm, F.svals[si], F.dmean[e]);
+      o2c[c] = o | (o << 16);
+    }
+  } else {
+    const unsigned o = (unsigned)F.roff[m];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) o2c[c] = o | (o << 16);
+  }
   const int64_t row0 = (int64_t)m * 8;  // the range's 8 isometry rows: one 8-row core block
   const uint8_t* abase = F.a_tiles + (row0 >> 7) * ((int64_t)kTileM * F.kpad) +
                          ((int)(row0 & 127) >> 3) * 128;
@@ -216,8 +234,8 @@ __device__ __forceinline__ void fix_unit(const FixArgs& F, const long long* __re
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         // clip(q + o, 0, 255) on int16 pairs, then packed to 4 bytes
-        const unsigned lo2 = __vmins2(__vmaxs2(__vadd2(qw[2 * w], o2), 0u), 0x00ff00ffu);
-        const unsigned hi2 = __vmins2(__vmaxs2(__vadd2(qw[2 * w + 1], o2), 0u), 0x00ff00ffu);
+        const unsigned lo2 = __vmins2(__vmaxs2(__vadd2(qw[2 * w], o2c[c]), 0u), 0x00ff00ffu);
+        const unsigned hi2 = __vmins2(__vmaxs2(__vadd2(qw[2 * w + 1], o2c[c]), 0u), 0x00ff00ffu);
         x4[w] = __byte_perm(lo2, hi2, 0x6420);
       }
 #pragma unroll
@@ -263,6 +281,9 @@ struct TcParams {
   int kpad;
   int rg;          // row tiles per unit (A resident in smem)
   int stages;      // B ring depth
+  int base;        // baseline mode: u8 x u8 contraction, errors formed in the epilogue
+  int shift;       // log2(B*B)
+  const int4* bconst;  // baseline: per slot {W', 2 Q1, Q2, tie mask} (qprep_level)
   const TcPlan* plan;
   FixArgs fix;
   unsigned long long* tspan;  // optional {start, end} slots (global ns)
@@ -275,8 +296,16 @@ __host__ __device__ inline uint32_t stage_bytes(const TcParams& p) { return b_by
 __host__ __device__ inline uint32_t best_offset(const TcParams& p) {
   return a_bytes(p) + p.stages * stage_bytes(p);
 }
-__host__ __device__ inline uint32_t bar_offset(const TcParams& p) {
+// baseline mode: each thread's range sum R1 per resident row tile, then two
+// double-buffered 256-column constant tables (one per epilogue group)
+__host__ __device__ inline uint32_t r1_offset(const TcParams& p) {
   return best_offset(p) + p.rg * kEpiWarps * 32 * 8;
+}
+__host__ __device__ inline uint32_t const_offset(const TcParams& p) {
+  return r1_offset(p) + (p.base ? p.rg * kEpiWarps * 32 * 4 : 0);
+}
+__host__ __device__ inline uint32_t bar_offset(const TcParams& p) {
+  return const_offset(p) + (p.base ? 2 * 2 * kTileN * 16 : 0);
 }
 __host__ __device__ inline uint32_t smem_bytes(const TcParams& p) {
   const uint32_t raw = bar_offset(p) + (2 * p.stages + 2 * kNumAcc + 2) * 8 + 16;
@@ -290,11 +319,31 @@ __device__ __forceinline__ int min8(const int (&v)[32]) {
                       min(v[O + 6], v[O + 7]));
 }
 
-// u8 x s8 four-way dot product accumulate (the MMA's kind::i8 arithmetic).
+// u8 x s8 (proposed) / u8 x u8 (baseline) four-way dot product accumulate
+// (the MMA's kind::i8 arithmetic).
 __device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
   int d;
   asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   return d;
+}
+__device__ __forceinline__ int dp4a_uu(uint32_t a, uint32_t b, int c) {
+  int d;
+  asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// Baseline mode: the candidate's error minus the range's R2 from the
+// contraction value acc = <q, r_iso> (_scan.py:38-55 without clamping):
+//   o = clip(rint(rmean - s * dmean), 0, 255) from R1 and the column's W' /
+//       tie mask (see qprep_level: exact integer form of the fp64 rounding),
+//   e = Q2 + o (2 Q1 + n o - 2 R1) - 2 acc      (+ R2 = sum (q + o - r)^2).
+// Clamp-active pairs make this an upper bound of the true error; they are
+// corrected exactly by fix_pairs_kernel like in proposed mode.
+__device__ __forceinline__ int base_err(int acc, int4 k, int R1, int X, int shift, int hn1) {
+  int t = R1 + k.x;
+  t += ((t - hn1) >> shift) & 1 & k.w;  // round half to even when V is integral
+  const int o = max(t >> shift, 0);
+  return o * (k.y - X + (o << shift)) + k.z - 2 * acc;
 }
 
 // Row state: best2 = 2*kh + par of the row's best so far and where it lies
@@ -327,6 +376,11 @@ struct EpiCtx {
 // 64-column slice of each half.  Per accumulator one wave of two
 // tcgen05.ld x32, released right after the loads; the per-pair bookkeeping
 // (row state, tile info, loop control) is shared by the two halves.
+// BASE (baseline mode): the accumulator holds <q, r_iso>; every value becomes
+// the candidate's error (base_err) from the row's range sum and the column's
+// constants, which the group stages per tile in shared memory (one 16-byte
+// load per thread, double buffered, one named barrier per tile).
+template <bool BASE>
 __device__ __forceinline__ void epilogue_role(const TcParams& p, uint8_t* smem, const EpiCtx& x) {
   const uint32_t kB = x.kB, bar_base = x.bar_base, tmem_base = x.tmem_base;
   const int RG = x.RG, KPAD = x.KPAD, warp = x.warp, lane = x.lane;
@@ -344,15 +398,38 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, uint8_t* smem, 
   // loc = tile << 4 | half << 3 | 8-column group
   const uint32_t bst = ptx::smem_u32(smem + best_offset(p)) + (e * 32 + lane) * 8;
   constexpr int kBS = kEpiWarps * 32;
+  // baseline: range sums per row tile, the group's column-constant buffers
+  const uint32_t r1s = ptx::smem_u32(smem + r1_offset(p)) + (e * 32 + lane) * 4;
+  const int4* cbase = reinterpret_cast<const int4*>(smem + const_offset(p)) + gq * 2 * kTileN;
+  const int gtid = (e & 7) * 32 + lane;  // thread index inside the group
+  const int shift = p.shift, hn1 = (1 << (shift - 1)) - 1;
+  uint32_t tcount = 0;
+  int4 pre = make_int4(0, 0, 0, 0);
   uint32_t H = 0;
   int g, t0, t1;
   for (SegIter it(x.plan); it.next(g, t0, t1);) {
     for (int r = 0; r < RG; ++r) ptx::sts_v2(bst + r * (kBS * 8), make_int2(kNone, 0));
+    if constexpr (BASE) {
+      for (int r = 0; r < RG; ++r) {
+        const int r1 = p.row_meta[(size_t)(g * RG + r) * kTileM + row].x;
+        asm volatile("st.shared.s32 [%0], %1;" ::"r"(r1s + r * (kBS * 4)), "r"(r1) : "memory");
+      }
+      pre = p.bconst[(size_t)(t1 - 1) * kTileN + gtid];
+    }
     // tiles in DECREASING order (see improve_limit); tile_info one tile ahead
     int2 tinfo_next = p.tile_info[t1 - 1];
     for (int t = t1 - 1; t >= t0; --t) {
       const int2 tinfo = tinfo_next;  // {parity, valid slots}
       if (t > t0) tinfo_next = p.tile_info[t - 1];
+      const int4* cb = cbase;
+      if constexpr (BASE) {
+        int4* w = const_cast<int4*>(cbase) + (tcount & 1) * kTileN;
+        ++tcount;
+        w[gtid] = pre;
+        ptx::named_bar_sync(1 + gq, kEpiWarps / 2 * 32);
+        if (t > t0) pre = p.bconst[(size_t)(t - 1) * kTileN + gtid];
+        cb = w;
+      }
       // this group's pairs of the tile: Hr = Ht + r with (Hr & 1) == gq
       const uint32_t Ht = H;
       H += RG;
@@ -360,6 +437,9 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, uint8_t* smem, 
       for (int r = (gq ^ (int)(Ht & 1)) & 1; r < RG; r += 2) {
         const uint32_t bst_r = bst + r * (kBS * 8);
         const int2 bs = ptx::lds_v2(bst_r);
+        int R1 = 0;
+        if constexpr (BASE)
+          asm volatile("ld.shared.s32 %0, [%1];" : "=r"(R1) : "r"(r1s + r * (kBS * 4)) : "memory");
         const uint32_t ph = ((Ht + r) >> 1) & 1;
         // half 0 vs earlier tiles: improve_limit (ties go to the later-visited,
         // smaller columns); half 1 vs half 0 of this tile: strictly smaller
@@ -377,8 +457,16 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, uint8_t* smem, 
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(tempty0 + 8u * h);
+          const int s0 = h * kAccN + slice;
+          if constexpr (BASE) {
+            const int X = 2 * R1;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              va[j] = base_err(va[j], cb[s0 + j], R1, X, shift, hn1);
+              vb[j] = base_err(vb[j], cb[s0 + 32 + j], R1, X, shift, hn1);
+            }
+          }
           if (tinfo.y < kTileN) {  // mask padding slots (last tile of a group)
-            const int s0 = h * kAccN + slice;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               if (s0 + j >= tinfo.y) va[j] = kNone;
@@ -426,20 +514,22 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, uint8_t* smem, 
     for (int r = 0; r < RG; ++r) {
       unsigned long long key = ~0ull;
       const int2 bs = ptx::lds_v2(bst + r * (kBS * 8));
-      const int4 rm = p.row_meta[(size_t)(g * RG + r) * kTileM + row];  // {o, R, m, -}
+      const int4 rm = p.row_meta[(size_t)(g * RG + r) * kTileM + row];  // {o, R, m, -} | {R1, R2, m, 2 R1}
       const bool valid = bs.x != kNone && rm.z >= 0;
-      long long gmin = valid ? (long long)bs.x + rm.y : LLONG_MAX;
+      // error = key2 + R (proposed: key2 = 2 kh + par) | key2 / 2 + R2 (baseline)
+      const long long err = valid ? (BASE ? (long long)(bs.x >> 1) : (long long)bs.x) + rm.y : LLONG_MAX;
+      long long gmin = err;
       gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, 1));
       gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, 2));
       gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, 4));
       const int gbase = lane & ~7;
       const int j = lane & 7;
-      unsigned tied =
-          (__ballot_sync(0xffffffffu, valid && (long long)bs.x + rm.y == gmin) >> gbase) & 0xffu;
+      unsigned tied = (__ballot_sync(0xffffffffu, valid && err == gmin) >> gbase) & 0xffu;
       while (__any_sync(0xffffffffu, tied != 0)) {
         const int src = tied ? gbase + __ffs(tied) - 1 : lane;
         const int loc = __shfl_sync(0xffffffffu, bs.y, src);
         const int b2 = __shfl_sync(0xffffffffu, bs.x, src);
+        const int R1s = __shfl_sync(0xffffffffu, rm.x, src);
         const int t = loc >> 4;
         const int slot0 = ((loc >> 3) & 1) * kAccN + slice + (loc & 7) * 8;
         int m = 0, kh = 0;
@@ -453,11 +543,20 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, uint8_t* smem, 
           for (int kc = 0; kc < chunks; ++kc) {
             const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(arow + kc * (kTileM * 16)));
             const uint4 b4 = __ldg(reinterpret_cast<const uint4*>(bcol + kc * (kTileN * 16)));
-            kh = dp4a_us(a4.x, b4.x, kh);
-            kh = dp4a_us(a4.y, b4.y, kh);
-            kh = dp4a_us(a4.z, b4.z, kh);
-            kh = dp4a_us(a4.w, b4.w, kh);
+            if constexpr (BASE) {
+              kh = dp4a_uu(a4.x, b4.x, kh);
+              kh = dp4a_uu(a4.y, b4.y, kh);
+              kh = dp4a_uu(a4.z, b4.z, kh);
+              kh = dp4a_uu(a4.w, b4.w, kh);
+            } else {
+              kh = dp4a_us(a4.x, b4.x, kh);
+              kh = dp4a_us(a4.y, b4.y, kh);
+              kh = dp4a_us(a4.z, b4.z, kh);
+              kh = dp4a_us(a4.w, b4.w, kh);
+            }
           }
+          if constexpr (BASE)
+            kh = base_err(kh, p.bconst[(size_t)t * kTileN + slot0 + j], R1s, 2 * R1s, shift, hn1);
         }
         const unsigned hits = (__ballot_sync(0xffffffffu, tied && kh == m) >> gbase) & 0xffu;
         if (tied) {
@@ -487,6 +586,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, uint8_t* smem, 
 // row tiles r; the pair counter H and the column half h select accumulator
 // 2 * (H & 1) + h, issued by MMA warp acc and drained by epilogue group
 // H & 1.
+template <bool BASE>
 __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int KPAD = p.kpad, RG = p.rg, STAGES = p.stages;
@@ -548,7 +648,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     // = 5 per SM sub-partition keeps the 96-register budget.
     const int i = warp;
     const int my_h = i & 1, my_par = i >> 1;
-    constexpr uint32_t kIdesc = ptx::idesc_i8(kTileM, kAccN);
+    // u8 A x s8 B (proposed: -q planes) or u8 x u8 (baseline: q = rint(s d))
+    constexpr uint32_t kIdesc = BASE ? ptx::idesc_i8u(kTileM, kAccN) : ptx::idesc_i8(kTileM, kAccN);
     const int ksteps = KPAD / 32;
     // descriptor start-address field is addr >> 4: stepping K by 32 bytes
     // (two 16-byte core-matrix chunks) adds 2*LBO >> 4; column half h starts
@@ -619,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   } else if (warp >= kEpiBase) {
     // ---------------- epilogue: two groups of 8 warps, one column half each ----------------
     const EpiCtx x{kB, bar_base, tmem_base, RG, KPAD, warp, lane, plan};
-    epilogue_role(p, smem, x);
+    epilogue_role<BASE>(p, smem, x);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -698,7 +799,7 @@ tc_tables_kernel(const unsigned* __restrict__ hist, int64_t ncols, int64_t ntile
 // slots (weight 1), 2 halves of Q1 (weight o);  zero up to kpad.
 // slot = even/odd group base + rank of the column inside its parity group.
 __global__ void build_b_kernel(const int16_t* __restrict__ qbase, int n, int kpad, int planes,
-                               int m_digits, int64_t ncols, const int4* __restrict__ stats,
+                               int m_digits, int baseline, int64_t ncols, const int4* __restrict__ stats,
                                const int32_t* __restrict__ odd_prefix,
                                const TcDims* __restrict__ dims, int8_t* __restrict__ b_tiles,
                                int32_t* __restrict__ colmap) {
@@ -726,7 +827,7 @@ __global__ void build_b_kernel(const int16_t* __restrict__ qbase, int n, int kpa
   const int kc = (int)(i - col * chunks);
   const int4 st = stats[col];
   const int64_t oddp = odd_prefix[col];
-  const int64_t slot = (st.y & 1) ? odd_base + oddp : col - oddp;
+  const int64_t slot = (!baseline && (st.y & 1)) ? odd_base + oddp : col - oddp;
   const int64_t tile = slot / kTileN;
   const int cc = (int)(slot - tile * kTileN);
   const int kbase = planes * n;
@@ -736,7 +837,18 @@ __global__ void build_b_kernel(const int16_t* __restrict__ qbase, int n, int kpa
   const int q1a = min(max(st.x, -127), 127);
   const int16_t* q = qbase + col * n;
   uint32_t w[4];
-  if (kc * 16 < kbase) {
+  if (baseline) {
+    // u8 q (0..255) for k < n, zero beyond
+    w[0] = w[1] = w[2] = w[3] = 0u;
+    if (kc * 16 < n) {
+      const uint4 qa = __ldg(reinterpret_cast<const uint4*>(q + kc * 16));
+      const uint4 qb = __ldg(reinterpret_cast<const uint4*>(q + kc * 16 + 8));
+      w[0] = __byte_perm(qa.x, qa.y, 0x6420);
+      w[1] = __byte_perm(qa.z, qa.w, 0x6420);
+      w[2] = __byte_perm(qb.x, qb.y, 0x6420);
+      w[3] = __byte_perm(qb.z, qb.w, 0x6420);
+    }
+  } else if (kc * 16 < kbase) {
     // 16 q values at once (int16 pairs): -q, or its two s8 planes
     // b = clamp(-q, -127, 127) and -q - b; the low byte of each int16 is the s8
     const int kk0 = (kc * 16) % n;  // the second plane repeats the pixels
@@ -787,7 +899,7 @@ __global__ void build_b_kernel(const int16_t* __restrict__ qbase, int n, int kpa
 // r_iso bytes (again for a second plane), then 255 x m, 1, 1, o, o, zeros.
 __global__ void build_a_kernel(const uint8_t* __restrict__ rtiles, const double* __restrict__ rmean,
                                const int32_t* __restrict__ rsq, const TcPlan* __restrict__ plan,
-                               int n, int kpad, int planes, int m_digits,
+                               int n, int kpad, int planes, int m_digits, int baseline,
                                const uint16_t* __restrict__ inv, uint8_t* __restrict__ a_tiles,
                                int4* __restrict__ row_meta) {
   const int chunks = kpad / 16;
@@ -817,7 +929,7 @@ __global__ void build_a_kernel(const uint8_t* __restrict__ rtiles, const double*
         if (k < kbase) {
           const int kk = k < n ? k : k - n;
           v = r[inv[iso * n + kk]];
-        } else {
+        } else if (!baseline) {
           const int sl = k - kbase;
           if (sl < m_digits) v = 255;
           else if (sl < m_digits + 2) v = 1;
@@ -835,7 +947,7 @@ __global__ void build_a_kernel(const uint8_t* __restrict__ rtiles, const double*
     if (m < M) {
       const int s1 = (int)rint(rmean[m] * n);  // exact: rmean = s1 / n, n a power of two
       const int R = rsq[m] - 2 * o * s1 + n * o * o;
-      row_meta[row] = make_int4(o, R, (int)m, 0);
+      row_meta[row] = baseline ? make_int4(s1, rsq[m], (int)m, 2 * s1) : make_int4(o, R, (int)m, 0);
     } else {
       row_meta[row] = make_int4(0, 0, -1, 0);
     }
@@ -1046,6 +1158,7 @@ struct GatherBuild {
   unsigned long long* tspan;
   // tensor operand (kpad == 0: exact level)
   int kpad, planes, m_digits, RG;
+  int baseline, shift;  // baseline tensor levels: roff = floor(mean) (clamp bucket), no K extra block
   const uint16_t* inv;
   uint8_t* a_tiles;
   int4* row_meta;
@@ -1086,7 +1199,7 @@ __global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
       s2 += __shfl_xor_sync(0xffffffffu, s2, off);
     }
     const double mean = __ddiv_rn((double)s1, (double)n);
-    o = (int)rint(mean);
+    o = P.baseline ? (s1 >> P.shift) : (int)rint(mean);
     if (lane == 0) {
       P.rmean[m] = mean;
       P.roff[m] = o;
@@ -1132,7 +1245,7 @@ __global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
         const uint32_t* rw = reinterpret_cast<const uint32_t*>(src + sr * B);
         w[q] = rev ? __byte_perm(rw[per - 1 - cw], 0, 0x0123) : rw[cw];
       }
-    } else if (real) {
+    } else if (real && !P.baseline) {
 #pragma unroll
       for (int b4 = 0; b4 < 4; ++b4) {
         uint32_t word = 0;
@@ -1156,14 +1269,19 @@ __global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
     *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
   }
   if (lane < 8) {
-    const int R = s2 - 2 * o * s1 + n * o * o;
-    P.row_meta[m * 8 + lane] = real ? make_int4(o, R, (int)m, 0) : make_int4(0, 0, -1, 0);
+    int4 meta = make_int4(0, 0, -1, 0);
+    if (real && P.baseline) {
+      meta = make_int4(s1, s2, (int)m, 2 * s1);  // {R1, R2, m, 2 R1}
+    } else if (real) {
+      meta = make_int4(o, s2 - 2 * o * s1 + n * o * o, (int)m, 0);  // {o, R, m, -}
+    }
+    P.row_meta[m * 8 + lane] = meta;
   }
 }
 
 }  // namespace
 
-static int tc_config(Ctx* c, int kpad, TcParams* prm);
+static int tc_config(Ctx* c, int kpad, int base, TcParams* prm);
 
 int gather_build(Ctx* c, Level& L, const int32_t* d_origins, const int32_t* d_M, int64_t bound,
                  int32_t* d_hist, uint64_t* d_keys, unsigned long long* d_time) {
@@ -1184,10 +1302,12 @@ int gather_build(Ctx* c, Level& L, const int32_t* d_origins, const int32_t* d_M,
   int64_t slots = bound;
   if (L.path == FC_PATH_TENSOR) {
     TcParams prm{};
-    FC_TRY(tc_config(c, L.tc.kpad, &prm));
+    FC_TRY(tc_config(c, L.tc.kpad, L.baseline, &prm));
     P.kpad = L.tc.kpad;
     P.planes = L.tc.planes;
     P.m_digits = L.tc.m_digits;
+    P.baseline = L.baseline;
+    P.shift = L.n == 256 ? 8 : L.n == 64 ? 6 : 4;
     P.RG = prm.rg;
     P.inv = c->iso_inv.as<uint16_t>() + iso_table_offset(L.side);
     P.a_tiles = c->a_tiles.as<uint8_t>();
@@ -1212,14 +1332,22 @@ int level_prepare_tc_host(Ctx* c, Level& L) {
   TcOperands& T = L.tc;
   const int64_t ncols = T.ncols;
   if (ncols == 0) return set_error(c, FC_ERR_EMPTY_POOL, "no domain entries");
-  double smax = 0.0;
-  for (int k = 0; k < L.s_count; ++k) smax = std::max(smax, std::fabs(L.svals[k]));
-  const int qabs = (int)std::rint(smax * 255.0 * (double)(L.n - 1) / (double)L.n);
-  if (qabs > 254) return set_error(c, FC_ERR_ARG, "operand outside two s8 planes");
-  T.planes = qabs <= 127 ? 1 : 2;
-  const long long hq_max = (long long)L.n * qabs * qabs / 2;  // >= floor(sum q^2 / 2)
-  T.m_digits = std::max(1, (int)((hq_max / 255 + 126) / 127));
-  T.kpad = ((T.planes * L.n + T.m_digits + 4 + 31) / 32) * 32;
+  if (L.baseline) {
+    // baseline mode: B = q = rint(s d) in [0, 255] as one u8 plane, A = the
+    // permuted range; no extra K block (the epilogue adds the per-pair terms)
+    T.planes = 1;
+    T.m_digits = 0;
+    T.kpad = ((L.n + 31) / 32) * 32;
+  } else {
+    double smax = 0.0;
+    for (int k = 0; k < L.s_count; ++k) smax = std::max(smax, std::fabs(L.svals[k]));
+    const int qabs = (int)std::rint(smax * 255.0 * (double)(L.n - 1) / (double)L.n);
+    if (qabs > 254) return set_error(c, FC_ERR_ARG, "operand outside two s8 planes");
+    T.planes = qabs <= 127 ? 1 : 2;
+    const long long hq_max = (long long)L.n * qabs * qabs / 2;  // >= floor(sum q^2 / 2)
+    T.m_digits = std::max(1, (int)((hq_max / 255 + 126) / 127));
+    T.kpad = ((T.planes * L.n + T.m_digits + 4 + 31) / 32) * 32;
+  }
   if (c->trace)
     fprintf(stderr, "[fc_trace] tc operands B=%d cols=%lld planes=%d m_digits=%d kpad=%d\n", L.side,
             (long long)ncols, T.planes, T.m_digits, T.kpad);
@@ -1251,7 +1379,7 @@ int level_prepare_tc_launch(Ctx* c, Level& L) {
   const int64_t pad_max = T.ntiles * kTileN - ncols;
   const int64_t work = (ncols + pad_max) * (T.kpad / 16);
   build_b_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
-      L.qbase.as<int16_t>(), L.n, T.kpad, T.planes, T.m_digits, ncols, T.col_stats.as<int4>(),
+      L.qbase.as<int16_t>(), L.n, T.kpad, T.planes, T.m_digits, L.baseline, ncols, T.col_stats.as<int4>(),
       T.odd.as<int32_t>() + ncols, dims, T.b_tiles.as<int8_t>(), T.meta.as<int32_t>());
   FC_CUDA(c, cudaGetLastError());
   c->total_launches += 3;
@@ -1265,8 +1393,9 @@ int level_prepare_tc_finish(Ctx* c, Level& L) {
 }
 
 // Resident A row tiles and B ring depth within the shared-memory budget.
-static int tc_config(Ctx* c, int kpad, TcParams* prm) {
+static int tc_config(Ctx* c, int kpad, int base, TcParams* prm) {
   prm->kpad = kpad;
+  prm->base = base;
   prm->rg = kpad <= 64 ? 8 : kpad <= 128 ? 4 : kpad <= 320 ? 2 : 1;
   for (;;) {
     prm->stages = 8;
@@ -1285,7 +1414,7 @@ int reserve_level_scan(Ctx* c, Level& L, int64_t bound) {
   FC_TRY(reserve_ranges(c, L, bound));
   if (L.path != FC_PATH_TENSOR) return FC_OK;
   TcParams prm{};
-  FC_TRY(tc_config(c, L.tc.kpad, &prm));
+  FC_TRY(tc_config(c, L.tc.kpad, L.baseline, &prm));
   const int64_t rtiles_max = (bound * 8 + kTileM - 1) / kTileM;
   const int64_t rows_max = ((rtiles_max + prm.rg - 1) / prm.rg) * prm.rg * kTileM;
   FC_CUDA(c, c->a_tiles.reserve(rows_max * L.tc.kpad));
@@ -1295,8 +1424,10 @@ int reserve_level_scan(Ctx* c, Level& L, int64_t bound) {
   FC_CUDA(c, c->fix_jobs.reserve(512 * 16 + 64));
   FC_CUDA(c, c->fix_cols.reserve(513 * 8 + 64));
   if (!c->tc_attr_set) {
-    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    227 * 1024));
+    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     c->tc_attr_set = true;
   }
   return FC_OK;
@@ -1313,7 +1444,7 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   if (M_bound == 0) return FC_OK;
   FC_TRY(ensure_iso_tables(c));
   TcParams prm{};
-  FC_TRY(tc_config(c, T.kpad, &prm));
+  FC_TRY(tc_config(c, T.kpad, L.baseline, &prm));
   const int RG = prm.rg;
   const int64_t rtiles_max = (M_bound * 8 + kTileM - 1) / kTileM;
   const int64_t rows_max = ((rtiles_max + RG - 1) / RG) * RG * kTileM;
@@ -1340,7 +1471,7 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
     const int64_t work = rows_max * (T.kpad / 16);
     build_a_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
         c->rtiles.as<uint8_t>(), c->rmean.as<double>(), c->rsq.as<int32_t>(), d_plan, L.n, T.kpad,
-        T.planes, T.m_digits, inv, c->a_tiles.as<uint8_t>(), c->row_meta.as<int4>());
+        T.planes, T.m_digits, L.baseline, inv, c->a_tiles.as<uint8_t>(), c->row_meta.as<int4>());
     FC_CUDA(c, cudaGetLastError());
     c->stats.kernel_launches += 1;
   }
@@ -1353,6 +1484,9 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
                                                 kUpReachBytes + kUpDimsBytes);
   prm.keys = reinterpret_cast<unsigned long long*>(d_keys);
   prm.S = L.s_count;
+  prm.base = L.baseline;
+  prm.shift = L.n == 256 ? 8 : L.n == 64 ? 6 : 4;
+  prm.bconst = L.baseline ? T.bconst.as<int4>() : nullptr;
   prm.plan = d_plan;
   prm.tspan = d_time;
   prm.fix.qbase = L.qbase.as<int16_t>();
@@ -1368,13 +1502,22 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   prm.fix.S = L.s_count;
   prm.fix.kpad = T.kpad;
   prm.fix.n = L.n;
+  prm.fix.baseline = L.baseline;
+  prm.fix.rmean = c->rmean.as<double>();
+  prm.fix.dmean = L.mean.as<double>();
+  prm.fix.svals = L.svals_d.as<double>();
   const uint32_t smem = smem_bytes(prm);
   if (!c->tc_attr_set) {
-    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    227 * 1024));
+    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     c->tc_attr_set = true;
   }
-  FC_CUDA(c, launch_k(c, tc_scan_kernel, dim3(c->sm_count), dim3(kThreads), smem, prm));
+  if (prm.base)
+    FC_CUDA(c, launch_k(c, tc_scan_kernel<true>, dim3(c->sm_count), dim3(kThreads), smem, prm));
+  else
+    FC_CUDA(c, launch_k(c, tc_scan_kernel<false>, dim3(c->sm_count), dim3(kThreads), smem, prm));
   if (ev_main_end) FC_CUDA(c, record_event(c, ev_main_end));
   c->stats.kernel_launches += 1;
 
@@ -1404,6 +1547,14 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   return FC_OK;
 }
 
+// Baseline levels: the clamp-correction bucket of a range is floor(mean)
+// (rmean = R1 / n exactly), stored where proposed mode keeps its offset.
+__global__ void floor_bucket_kernel(const double* __restrict__ rmean, int64_t M,
+                                    int32_t* __restrict__ roff) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < M) roff[i] = (int32_t)floor(rmean[i]);
+}
+
 // Per-call API variant (fc_match_level / fc_match_tiles): M is known here.
 int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys) {
   FC_CUDA(c, c->enc_hist.reserve(256 * 4 + 64));
@@ -1412,6 +1563,12 @@ int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys) {
   auto* d_fix = reinterpret_cast<int64_t*>(c->enc_count.as<int32_t>() + 20);
   const int32_t m32 = (int32_t)M;
   FC_TRY(stage_h2d(c, d_M, &m32, 4));
+  if (L.baseline && M > 0) {
+    floor_bucket_kernel<<<(unsigned)((M + 255) / 256), 256, 0, c->stream>>>(
+        c->rmean.as<double>(), M, c->roff.as<int32_t>());
+    FC_CUDA(c, cudaGetLastError());
+    c->stats.kernel_launches += 1;
+  }
   FC_TRY(roff_hist(c, M, c->enc_hist.as<int32_t>()));
   FC_CUDA(c, cudaEventRecord(c->tc_ev[0], c->stream));
   FC_TRY(scan_tc_launch(c, L, M, d_M, c->enc_hist.as<int32_t>(), d_keys, c->tc_ev[1], d_fix));

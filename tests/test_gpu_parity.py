@@ -109,7 +109,7 @@ def test_matcher_golden_cases(path):
     for k in range(int(g["n"])):
         mode = fc.PROPOSED if int(g[f"mode_{k}"]) else fc.BASELINE
         level = int(g[f"level_{k}"])
-        if path == "tensor" and (mode == fc.BASELINE or level == 4):
+        if path == "tensor" and level == 4:
             continue
         pool = fc.DomainPool.from_tiles({level: g[f"tiles_{k}"]})
         res = fc.best_match(g[f"range_{k}"], level, pool, fc.SPolicy(mode=mode), path=path)
@@ -170,9 +170,7 @@ def _encode_golden(g, tag, path, taus=None, driver=None):
                                  "darkbright_baseline", "c1"])
 def test_encode_bytes_identical(tag, path):
     g = load_golden("encode_cases.npz")
-    if path == "tensor" and "baseline" in tag:
-        pytest.skip("tensor path is proposed-mode only")
-    stream, report = _encode_golden(g, tag, path if "baseline" not in tag else "auto")
+    stream, report = _encode_golden(g, tag, path)
     assert fc.serialize(stream) == g[f"bytes_{tag}"].tobytes()
     assert report.collage_ssd == int(g[f"collage_{tag}"])
     dec = fc.decode(stream)
@@ -213,8 +211,6 @@ def test_levelwise_driver_bytes_identical(tag, path):
     from paper_1502_00324_b200.codec import encode_levelwise
 
     g = load_golden("encode_cases.npz")
-    if path == "tensor" and "baseline" in tag:
-        pytest.skip("tensor path is proposed-mode only")
     stream, report = _encode_golden(g, tag, path, driver=encode_levelwise)
     assert fc.serialize(stream) == g[f"bytes_{tag}"].tobytes()
     assert report.collage_ssd == int(g[f"collage_{tag}"])

@@ -1,7 +1,7 @@
 """Per-level scan timing on a workload's pools (development tool).
 
 Usage: python tools/bench_level.py [WORKLOAD [LEVEL:M ...]] ; env FC_BENCH_REPS.
-FC_TC_DEBUG_MODE / FC_TC_DEFERRED select kernel variants (debug: results invalid).
+FC_MODE=baseline: baseline mode (10 s values); FC_PATH=exact: the CUDA-core scan.
 """
 import os
 import sys
@@ -22,14 +22,16 @@ caps = tuple(1 if one else 10**9 for one in wl.cap_one)
 params = fc.PoolParams(pool_cap=10**9, strides=wl.strides, level_caps=caps, entropy_thresholds=taus)
 ctx = _native.Context(0)
 pool = fc.build_pool(fc.GrayImage(img), params, context=ctx)
-policy = fc.SPolicy()
+base = os.environ.get("FC_MODE", "proposed") == "baseline"
+policy = fc.SPolicy(mode="baseline" if base else "proposed")
+path = {"exact": _native.PATH_EXACT, "tensor": _native.PATH_TENSOR}[os.environ.get("FC_PATH", "tensor")]
 rng = np.random.default_rng(0)
 for level, M in specs:
     side = (16, 8, 4, 2)[level - 1]
     ys, xs = np.mgrid[0:img.shape[0]:side, 0:img.shape[1]:side]
     allo = np.stack([xs.ravel(), ys.ravel()], axis=1).astype(np.int32)
     o = allo[np.sort(rng.choice(allo.shape[0], size=min(M, allo.shape[0]), replace=False))]
-    ctx.level_prepare(level, False, policy.s_set(level), _native.PATH_TENSOR)
+    ctx.level_prepare(level, base, policy.s_set(level), path)
     mains, fixes = [], []
     for _ in range(reps):
         ctx.match_level(level, o)
