@@ -339,6 +339,10 @@ int fc_set_option(fc_ctx* c, const char* name, int64_t value) {
     c->tc_span_units = (int)value;
     return FC_OK;
   }
+  if (strcmp(name, "real_cuda_cores") == 0) {  // s-histogram search on the dp4a kernel
+    c->real_cuda_cores = (int)value;
+    return FC_OK;
+  }
   if (strcmp(name, "pdl") == 0) {
     c->pdl = value != 0;
     return FC_OK;

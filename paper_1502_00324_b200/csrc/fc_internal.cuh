@@ -191,6 +191,7 @@ struct Ctx {
   bool pdl = false;                    // FC_PDL=1: programmatic dependent launches (measured no gain)
   int pool_chunk = 0;                  // FC_POOL_CHUNK=1024 / 2048: force the rank-sort chunk
   int tc_span_units = 0;               // 1: the contraction's round-robin span schedule at any B size (tests)
+  int real_cuda_cores = 0;             // 1: real-valued slope search on the dp4a kernel (tests, timing)
   cudaGraphExec_t enc_exec = nullptr;  // instantiated level-loop graph, updated per encode
   std::vector<uint64_t> enc_sig;       // launch signature of enc_exec (reuse when equal)
   int enc_levels_run = 0;              // host-side results of the captured body
@@ -332,7 +333,11 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
                    uint64_t* d_keys, cudaEvent_t ev_main_end, int64_t* d_fix_pairs,
                    unsigned long long* d_time = nullptr, bool a_built = false,
                    cudaStream_t jobs_stream = nullptr, cudaEvent_t ev_plan = nullptr,
-                   cudaEvent_t ev_jobs = nullptr);
+                   cudaEvent_t ev_jobs = nullptr, unsigned long long* real_out = nullptr);
+// real-valued slope search on the contraction (fc_real.cu caller): winners per
+// range as {err bits, e * 8 + iso} 128-bit records (see tc_scan_kernel<2>)
+int real_tc_match(Ctx* c, Level& L, int level, int64_t M, double* d_err, double* d_s,
+                  int64_t* d_idx);
 // fc_encode's fused level start: gather the level's ranges (tiles, moments,
 // offset histogram), reset their candidate keys and the level's span slots,
 // and for tensor levels write the A operand tiles + row meta (build_a_kernel)

@@ -221,6 +221,9 @@ __global__ void real_s_merge_kernel(const double* __restrict__ part_err,
 int real_s_match(Ctx* c, Level& L, int64_t M, double* d_err, double* d_s, int64_t* d_idx) {
   if (M == 0) return FC_OK;
   FC_TRY(ensure_iso_tables(c));
+  // B >= 4: X on the tcgen05 contraction (fc_scan_tc.cu, tc_scan_kernel<2>);
+  // this CUDA-core kernel remains for B = 2 (n = 4 < one MMA K step)
+  if (L.n >= 16 && !c->real_cuda_cores) return real_tc_match(c, L, (int)(&L - c->lv) + 1, M, d_err, d_s, d_idx);
   const int64_t E = L.count;
   const int64_t gx = (M + kRealRanges - 1) / kRealRanges;
   // enough blocks for ~2 waves over the SMs; chunks of at least one entry per thread

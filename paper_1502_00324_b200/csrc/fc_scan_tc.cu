@@ -46,6 +46,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cfloat>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -282,8 +283,12 @@ struct TcParams {
   int rg;          // row tiles per unit (A resident in smem)
   int stages;      // B ring depth
   int base;        // baseline mode: u8 x u8 contraction, errors formed in the epilogue
+  int real;        // real-valued slope search (s-histogram analysis): u8 x u8, fp64 epilogue
   int shift;       // log2(B*B)
-  const int4* bconst;  // baseline: per slot {W', 2 Q1, Q2, tie mask} (qprep_level)
+  const int4* bconst;  // baseline: per slot {W', 2 Q1, Q2, tie mask} (qprep_level);
+                       // real: per slot {D1, flat, rcp(cnorm) / n^2 as two words}
+  const double* cnorm;             // real: centered norm per entry
+  unsigned long long* real_out;    // real: per range {err bits, e * 8 + iso}, 128-bit CAS-min
   const TcPlan* plan;
   FixArgs fix;
   unsigned long long* tspan;  // optional {start, end} slots (global ns)
@@ -293,19 +298,21 @@ __host__ __device__ inline uint32_t a_bytes(const TcParams& p) { return p.rg * k
 __host__ __device__ inline uint32_t b_bytes(const TcParams& p) { return kTileN * p.kpad; }
 __host__ __device__ inline uint32_t stage_bytes(const TcParams& p) { return b_bytes(p); }
 // per epilogue thread and resident row tile: {best key2, tile * 8 + 8-column group}
+// (real mode: {best err, screening threshold} as two doubles)
 __host__ __device__ inline uint32_t best_offset(const TcParams& p) {
   return a_bytes(p) + p.stages * stage_bytes(p);
 }
-// baseline mode: each thread's range sum R1 per resident row tile, then two
-// double-buffered 256-column constant tables (one per epilogue group)
+// baseline mode: each thread's range sum R1 per resident row tile; real mode:
+// {rnorm, R1} doubles then the best column; then two double-buffered
+// 256-column constant tables (one per epilogue group)
 __host__ __device__ inline uint32_t r1_offset(const TcParams& p) {
-  return best_offset(p) + p.rg * kEpiWarps * 32 * 8;
+  return best_offset(p) + p.rg * kEpiWarps * 32 * (p.real ? 16 : 8);
 }
 __host__ __device__ inline uint32_t const_offset(const TcParams& p) {
-  return r1_offset(p) + (p.base ? p.rg * kEpiWarps * 32 * 4 : 0);
+  return r1_offset(p) + (p.base ? p.rg * kEpiWarps * 32 * 4 : p.real ? p.rg * kEpiWarps * 32 * 20 : 0);
 }
 __host__ __device__ inline uint32_t bar_offset(const TcParams& p) {
-  return const_offset(p) + (p.base ? 2 * 2 * kTileN * 16 : 0);
+  return const_offset(p) + (p.base || p.real ? 2 * 2 * kTileN * 16 : 0);
 }
 __host__ __device__ inline uint32_t smem_bytes(const TcParams& p) {
   const uint32_t raw = bar_offset(p) + (2 * p.stages + 2 * kNumAcc + 2) * 8 + 16;
@@ -580,13 +587,230 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, uint8_t* smem, 
   }
 }
 
+// Real-valued slope search (bench.py:117-139 _real_s_matches), the
+// s-histogram analysis: the accumulator holds X = <d, r_iso> (u8 x u8, d the
+// decimated domain), and per candidate
+//   cross = (n X - D1 R1) / n,  gain = cross^2 / cnorm,  err = max(rnorm - gain, 0)
+// with the first minimum of (err, e * 8 + iso) kept (gain = 0 for a flat
+// domain).  Every product is an exact integer / n^2 (see fc_real.cu), so the
+// fp64 steps below reproduce the reference bit for bit.  Screening: g =
+// fl(fl(xn^2) * rcp / n^2) with xn = n X - D1 R1 equals fc_real.cu's
+// fl(cross^2 * rcp); g < T = (rnorm - best) - 1e-13 (rnorm + |best|) implies
+// that kernel's own rejection test (rnorm - g > best + 1e-14 (rnorm + g),
+// rounding included), so only the rare candidates at or above T take its
+// exact path.  Each row keeps {best err, T} and the best column in shared
+// memory; at the end of a segment the 8 isometry rows of a range reduce
+// lexicographically and merge into the range's 128-bit {err bits, index}
+// record with a compare-and-swap loop (order independent).
+__device__ __forceinline__ void real_cas_min(unsigned long long* slot, unsigned long long eb,
+                                             unsigned long long idx) {
+  unsigned long long olo = slot[1], ohi = slot[0];  // hint; the CAS re-reads
+  for (;;) {
+    if (ohi < eb || (ohi == eb && olo <= idx)) return;
+    unsigned long long rlo, rhi;
+    asm volatile(
+        "{\n\t.reg .b128 d, c, v;\n\t"
+        "mov.b128 c, {%2, %3};\n\t"
+        "mov.b128 v, {%4, %5};\n\t"
+        "atom.global.cas.b128 d, [%6], c, v;\n\t"
+        "mov.b128 {%0, %1}, d;\n\t}"
+        : "=l"(rlo), "=l"(rhi)
+        : "l"(ohi), "l"(olo), "l"(eb), "l"(idx), "l"(slot)
+        : "memory");
+    if (rlo == ohi && rhi == olo) return;  // swapped
+    ohi = rlo;
+    olo = rhi;
+  }
+}
+
+__device__ __forceinline__ double real_threshold(double rn, double best) {
+  return __dsub_rn(__dsub_rn(rn, best), __dmul_rn(1e-13, __dadd_rn(rn, fabs(best))));
+}
+
+__device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, const EpiCtx& x) {
+  const uint32_t kB = x.kB, bar_base = x.bar_base, tmem_base = x.tmem_base;
+  const int RG = x.RG, KPAD = x.KPAD, warp = x.warp, lane = x.lane;
+  const int e = warp - kEpiBase;
+  const int gq = e >> 3, hq = (e >> 2) & 1, sp = warp & 3;
+  const int row = sp * 32 + lane;
+  const int slice = hq * 64;
+  const uint32_t tm0 = tmem_base + ((uint32_t)(sp * 32) << 16) + (2 * gq) * kAccN + slice;
+  const uint32_t tfull0 = bar_base + 8u * (2 * p.stages) + 8u * (2 * gq);
+  const uint32_t tempty0 = tfull0 + 8u * kNumAcc;
+  constexpr int kBS = kEpiWarps * 32;
+  const int tix = e * 32 + lane;
+  double2* st_best = reinterpret_cast<double2*>(smem + best_offset(p)) + tix;  // {best, T}
+  double2* st_row = reinterpret_cast<double2*>(smem + r1_offset(p)) + tix;     // {rnorm, R1}
+  int* st_col = reinterpret_cast<int*>(smem + r1_offset(p) + RG * kBS * 16) + tix;
+  const int4* cbase = reinterpret_cast<const int4*>(smem + const_offset(p)) + gq * 2 * kTileN;
+  const int gtid = (e & 7) * 32 + lane;
+  const int shift = p.shift, n = 1 << shift;
+  const double ninv = 1.0 / (double)n;
+  uint32_t tcount = 0;
+  int4 pre = make_int4(0, 0, 0, 0);
+  uint32_t H = 0;
+  int g, t0, t1;
+  for (SegIter it(x.plan); it.next(g, t0, t1);) {
+    for (int r = 0; r < RG; ++r) {
+      const int4 rm = p.row_meta[(size_t)(g * RG + r) * kTileM + row];  // {R1, R2, m, 2 R1}
+      const double rn = __dmul_rn((double)((long long)n * rm.y - (long long)rm.x * rm.x), ninv);
+      st_row[r * kBS] = make_double2(rn, (double)rm.x);
+      st_best[r * kBS] = make_double2(DBL_MAX, -DBL_MAX);
+      st_col[r * kBS] = INT_MAX;
+    }
+    pre = p.bconst[(size_t)(t1 - 1) * kTileN + gtid];
+    for (int t = t1 - 1; t >= t0; --t) {
+      const int valid_slots = p.tile_info[t].y;
+      int4* cb = const_cast<int4*>(cbase) + (tcount & 1) * kTileN;
+      ++tcount;
+      cb[gtid] = pre;
+      ptx::named_bar_sync(1 + gq, kEpiWarps / 2 * 32);
+      if (t > t0) pre = p.bconst[(size_t)(t - 1) * kTileN + gtid];
+      const uint32_t Ht = H;
+      H += RG;
+#pragma unroll 1
+      for (int r = (gq ^ (int)(Ht & 1)) & 1; r < RG; r += 2) {
+        const double2 rr = st_row[r * kBS];
+        const double rn = rr.x;
+        const int nR1 = -(int)rr.y;
+        double2 bt = st_best[r * kBS];
+        int bcol = st_col[r * kBS];
+        bool changed = false;
+        const uint32_t ph = ((Ht + r) >> 1) & 1;
+        const uint8_t* arow = p.a_tiles + (size_t)(g * RG + r) * (kTileM * KPAD) +
+                              (row >> 3) * 128 + (row & 7) * 16;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          ptx::mbar_wait_sleep(tfull0 + 8u * h, ph);
+          ptx::tc_fence_after();
+          int va[32], vb[32];
+          ptx::tmem_ld32(tm0 + h * kAccN, va);
+          ptx::tmem_ld32(tm0 + h * kAccN + 32, vb);
+          ptx::tmem_wait_ld();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(tempty0 + 8u * h);
+          const int s0 = h * kAccN + slice;
+          if (rn == 0.0) {
+            // a constant range: every candidate's error is max(0 - gain, 0) = 0,
+            // so the first candidate of the slice in column order wins
+            const int col = t * kTileN + s0;
+            if (s0 < valid_slots && (bt.x > 0.0 || col < bcol)) {
+              bt = make_double2(0.0, 0.0);
+              bcol = col;
+              changed = true;
+            }
+            continue;
+          }
+          // fast path: g32 = fl32(xn)^2 * rcp32 / n^2 per candidate; g32 < T32
+          // implies g < T (margins cover the fp32 roundings, < 5e-7 relative)
+          const int nvalid = valid_slots - s0;
+          const unsigned long long vmask =
+              nvalid >= 64 ? ~0ull : nvalid <= 0 ? 0ull : (1ull << nvalid) - 1;
+          const float T32 = bt.y > 0.0 ? __fmul_rn(__double2float_rd(bt.y), 0.999999f) : 0.0f;
+          unsigned long long mask = 0ull;
+          float gmax = -1.0f;
+#pragma unroll
+          for (int j = 0; j < 64; ++j) {
+            const int4 k = cb[s0 + j];  // {D1, rcp / n^2 as fp32, as fp64 (lo, hi)}
+            // xn = n X - D1 R1: |xn| = n |cross| < 2^31, so wrapping int32 is exact
+            const int xn = k.x * nR1 + ((j < 32 ? va[j] : vb[j - 32]) << shift);
+            const float xf = __int2float_rn(xn);
+            const float g32 = __fmul_rn(__fmul_rn(xf, xf), __int_as_float(k.y));
+            mask |= (unsigned long long)(g32 >= T32) << j;
+            gmax = ((vmask >> j) & 1ull) ? fmaxf(gmax, g32) : gmax;
+            if (j < 32) va[j] = __float_as_int(g32);
+            else vb[j - 32] = __float_as_int(g32);
+          }
+          mask &= vmask;
+          if (mask == 0ull) continue;
+          if (bt.x == DBL_MAX) {
+            // first slice of a segment (no best yet): only the candidates within
+            // 1e-4 of the slice's largest g32 can hold its best gain -- any other
+            // has g < g(max) and so a larger error -- plus every candidate whose
+            // gain may reach rnorm (error clamped to 0: ties by column), so those
+            // are evaluated
+            const float gcut = fminf(__fmul_rn(gmax, 0.9999f),
+                                     __fmul_rn(__double2float_rd(rn), 0.999999f));
+            mask = 0ull;
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+              mask |= (unsigned long long)(__int_as_float(j < 32 ? va[j] : vb[j - 32]) >= gcut) << j;
+            mask &= vmask;
+          }
+          // exact path (rare): X recomputed from the operands, then fc_real.cu's steps
+          auto exact = [&](int j) {
+            const int slot = s0 + j;
+            const int col = t * kTileN + slot;  // real mode: slots are columns in order
+            const int8_t* bcolp = p.b_tiles + (size_t)t * kB + (slot >> 3) * 128 + (slot & 7) * 16;
+            int X = 0;
+            for (int kc = 0; kc < KPAD / 16; ++kc) {
+              const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(arow + kc * (kTileM * 16)));
+              const uint4 b4 = __ldg(reinterpret_cast<const uint4*>(bcolp + kc * (kTileN * 16)));
+              X = dp4a_uu(a4.x, b4.x, X);
+              X = dp4a_uu(a4.y, b4.y, X);
+              X = dp4a_uu(a4.z, b4.z, X);
+              X = dp4a_uu(a4.w, b4.w, X);
+            }
+            const int4 k = cb[slot];
+            const double rcpn = __hiloint2double(k.w, k.z);
+            const double xd = (double)(k.x * nR1 + (X << shift));
+            const double gq2 = __dmul_rn(__dmul_rn(xd, xd), rcpn);  // == its fl(cc * rcp)
+            const double cross = __dmul_rn(xd, ninv);
+            const double cc = __dmul_rn(cross, cross);
+            const bool flat = rcpn == 0.0;
+            if (!flat && __dsub_rn(rn, gq2) > bt.x + 1e-14 * (rn + gq2)) return;
+            const double gain = flat ? 0.0 : __ddiv_rn(cc, p.cnorm[col]);
+            const double err = fmax(__dsub_rn(rn, gain), 0.0);
+            if (err < bt.x || (err == bt.x && col < bcol)) {
+              bt.x = err;
+              bt.y = real_threshold(rn, err);
+              bcol = col;
+              changed = true;
+            }
+          };
+          while (mask) {
+            const int j = __ffsll((long long)mask) - 1;
+            mask &= mask - 1;
+            exact(j);
+          }
+        }
+        if (changed) {
+          st_best[r * kBS] = bt;
+          st_col[r * kBS] = bcol;
+        }
+      }
+    }
+    // per range: the 8 isometry rows (lanes 8k..8k+7) reduce on (err, e * 8 + iso)
+#pragma unroll 1
+    for (int r = 0; r < RG; ++r) {
+      const int4 rm = p.row_meta[(size_t)(g * RG + r) * kTileM + row];
+      const double be = st_best[r * kBS].x;
+      const int bcol = st_col[r * kBS];
+      unsigned long long eb = (bcol != INT_MAX && rm.z >= 0) ? (unsigned long long)__double_as_longlong(be)
+                                                             : ~0ull;
+      unsigned long long ix = bcol != INT_MAX ? (unsigned long long)bcol * 8 + (lane & 7) : ~0ull;
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        const unsigned long long oe = __shfl_xor_sync(0xffffffffu, eb, o);
+        const unsigned long long oi = __shfl_xor_sync(0xffffffffu, ix, o);
+        if (oe < eb || (oe == eb && oi < ix)) {
+          eb = oe;
+          ix = oi;
+        }
+      }
+      if ((lane & 7) == 0 && eb != ~0ull) real_cas_min(p.real_out + 2 * (size_t)rm.z, eb, ix);
+    }
+  }
+}
+
 // Work order (all roles derive it identically): the CTA's share of
 // (row group, tile) pairs as segments (cta_share / next_seg; one A load and
 // one column resolution per segment); inside a segment: tiles t descending,
 // row tiles r; the pair counter H and the column half h select accumulator
 // 2 * (H & 1) + h, issued by MMA warp acc and drained by epilogue group
 // H & 1.
-template <bool BASE>
+template <int MODE>  // 0 proposed, 1 baseline, 2 real-valued slope search
 __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int KPAD = p.kpad, RG = p.rg, STAGES = p.stages;
@@ -649,7 +873,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     const int i = warp;
     const int my_h = i & 1, my_par = i >> 1;
     // u8 A x s8 B (proposed: -q planes) or u8 x u8 (baseline: q = rint(s d))
-    constexpr uint32_t kIdesc = BASE ? ptx::idesc_i8u(kTileM, kAccN) : ptx::idesc_i8(kTileM, kAccN);
+    constexpr uint32_t kIdesc = MODE ? ptx::idesc_i8u(kTileM, kAccN) : ptx::idesc_i8(kTileM, kAccN);
     const int ksteps = KPAD / 32;
     // descriptor start-address field is addr >> 4: stepping K by 32 bytes
     // (two 16-byte core-matrix chunks) adds 2*LBO >> 4; column half h starts
@@ -720,7 +944,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   } else if (warp >= kEpiBase) {
     // ---------------- epilogue: two groups of 8 warps, one column half each ----------------
     const EpiCtx x{kB, bar_base, tmem_base, RG, KPAD, warp, lane, plan};
-    epilogue_role<BASE>(p, smem, x);
+    if constexpr (MODE == 2) epilogue_real(p, smem, x);
+    else epilogue_role<MODE == 1>(p, smem, x);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -1281,7 +1506,7 @@ __global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
 
 }  // namespace
 
-static int tc_config(Ctx* c, int kpad, int base, TcParams* prm);
+static int tc_config(Ctx* c, int kpad, int base, TcParams* prm, int real = 0);
 
 int gather_build(Ctx* c, Level& L, const int32_t* d_origins, const int32_t* d_M, int64_t bound,
                  int32_t* d_hist, uint64_t* d_keys, unsigned long long* d_time) {
@@ -1393,10 +1618,11 @@ int level_prepare_tc_finish(Ctx* c, Level& L) {
 }
 
 // Resident A row tiles and B ring depth within the shared-memory budget.
-static int tc_config(Ctx* c, int kpad, int base, TcParams* prm) {
+static int tc_config(Ctx* c, int kpad, int base, TcParams* prm, int real) {
   prm->kpad = kpad;
-  prm->base = base;
-  prm->rg = kpad <= 64 ? 8 : kpad <= 128 ? 4 : kpad <= 320 ? 2 : 1;
+  prm->base = base && !real;
+  prm->real = real;
+  prm->rg = real ? (kpad <= 128 ? 2 : 1) : kpad <= 64 ? 8 : kpad <= 128 ? 4 : kpad <= 320 ? 2 : 1;
   for (;;) {
     prm->stages = 8;
     while (prm->stages > 2 && (int)smem_bytes(*prm) > kSmemBudget) --prm->stages;
@@ -1424,9 +1650,11 @@ int reserve_level_scan(Ctx* c, Level& L, int64_t bound) {
   FC_CUDA(c, c->fix_jobs.reserve(512 * 16 + 64));
   FC_CUDA(c, c->fix_cols.reserve(513 * 8 + 64));
   if (!c->tc_attr_set) {
-    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<false>,
+    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<0>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<true>,
+    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<1>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<2>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     c->tc_attr_set = true;
   }
@@ -1438,13 +1666,13 @@ int reserve_level_scan(Ctx* c, Level& L, int64_t bound) {
 int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const int32_t* d_hist,
                    uint64_t* d_keys, cudaEvent_t ev_main_end, int64_t* d_fix_pairs,
                    unsigned long long* d_time, bool a_built, cudaStream_t jobs_stream,
-                   cudaEvent_t ev_plan, cudaEvent_t ev_jobs) {
+                   cudaEvent_t ev_plan, cudaEvent_t ev_jobs, unsigned long long* real_out) {
   TcOperands& T = L.tc;
   if (!T.ready) return set_error(c, FC_ERR_STATE, "tensor operands not prepared");
   if (M_bound == 0) return FC_OK;
   FC_TRY(ensure_iso_tables(c));
   TcParams prm{};
-  FC_TRY(tc_config(c, T.kpad, L.baseline, &prm));
+  FC_TRY(tc_config(c, T.kpad, L.baseline, &prm, real_out ? 1 : 0));
   const int RG = prm.rg;
   const int64_t rtiles_max = (M_bound * 8 + kTileM - 1) / kTileM;
   const int64_t rows_max = ((rtiles_max + RG - 1) / RG) * RG * kTileM;
@@ -1484,9 +1712,10 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
                                                 kUpReachBytes + kUpDimsBytes);
   prm.keys = reinterpret_cast<unsigned long long*>(d_keys);
   prm.S = L.s_count;
-  prm.base = L.baseline;
   prm.shift = L.n == 256 ? 8 : L.n == 64 ? 6 : 4;
-  prm.bconst = L.baseline ? T.bconst.as<int4>() : nullptr;
+  prm.bconst = L.baseline || real_out ? T.bconst.as<int4>() : nullptr;
+  prm.cnorm = L.cnorm.as<double>();
+  prm.real_out = real_out;
   prm.plan = d_plan;
   prm.tspan = d_time;
   prm.fix.qbase = L.qbase.as<int16_t>();
@@ -1508,22 +1737,27 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   prm.fix.svals = L.svals_d.as<double>();
   const uint32_t smem = smem_bytes(prm);
   if (!c->tc_attr_set) {
-    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<false>,
+    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<0>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<true>,
+    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<1>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<2>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     c->tc_attr_set = true;
   }
-  if (prm.base)
-    FC_CUDA(c, launch_k(c, tc_scan_kernel<true>, dim3(c->sm_count), dim3(kThreads), smem, prm));
+  if (prm.real)
+    FC_CUDA(c, launch_k(c, tc_scan_kernel<2>, dim3(c->sm_count), dim3(kThreads), smem, prm));
+  else if (prm.base)
+    FC_CUDA(c, launch_k(c, tc_scan_kernel<1>, dim3(c->sm_count), dim3(kThreads), smem, prm));
   else
-    FC_CUDA(c, launch_k(c, tc_scan_kernel<false>, dim3(c->sm_count), dim3(kThreads), smem, prm));
+    FC_CUDA(c, launch_k(c, tc_scan_kernel<0>, dim3(c->sm_count), dim3(kThreads), smem, prm));
   if (ev_main_end) FC_CUDA(c, record_event(c, ev_main_end));
   c->stats.kernel_launches += 1;
 
   // ---- clamp corrections (exact kernel on clamp-active pairs), planned above ----
   // A separate kernel, on the jobs stream when given (both only atomicMin
-  // into the same keys).
+  // into the same keys).  The real-valued search has no clamping.
+  if (real_out) return FC_OK;
   cudaStream_t main = c->stream;
   if (jobs_stream) {
     FC_CUDA(c, cudaEventRecord(ev_plan, main));
@@ -1555,6 +1789,50 @@ __global__ void floor_bucket_kernel(const double* __restrict__ rmean, int64_t M,
   if (i < M) roff[i] = (int32_t)floor(rmean[i]);
 }
 
+// Real-valued slope search: per column (= pool entry, S = 1) the epilogue's
+// {D1, flat, rcp(cnorm) / n^2} (rcp correctly rounded, as fc_real.cu screens).
+__global__ void real_const_kernel(const int32_t* __restrict__ dsum, const double* __restrict__ cnorm,
+                                  int64_t ncols, int n, int4* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  const double norm = cnorm[c];
+  const bool flat = norm == 0.0;
+  const double rcpn = flat ? 0.0 : __dmul_rn(__drcp_rn(norm), 1.0 / ((double)n * n));  // exact scaling
+  const long long bits = __double_as_longlong(rcpn);
+  // fp32 copy rounded up: the pre-screen's g32 then never falls below fp64 g by more than its margin
+  out[c] = make_int4(dsum[c], __float_as_int(__double2float_ru(rcpn)), (int)(bits & 0xffffffffll),
+                     (int)(bits >> 32));
+}
+
+// Winner records {err bits, e * 8 + iso} -> (err, s = cross / cnorm, index),
+// s recomputed for the winner exactly as fc_real.cu (one thread per range).
+__global__ void real_finalize_kernel(const unsigned long long* __restrict__ rec, int64_t M, int n,
+                                     const uint8_t* __restrict__ rtiles,
+                                     const uint16_t* __restrict__ inv,
+                                     const uint8_t* __restrict__ dtiles,
+                                     const int32_t* __restrict__ dsum,
+                                     const double* __restrict__ cnorm, double* __restrict__ out_err,
+                                     double* __restrict__ out_s, int64_t* __restrict__ out_idx) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const double err = __longlong_as_double((long long)rec[2 * m]);
+  const long long idx = (long long)rec[2 * m + 1];
+  const long long e = idx >> 3;
+  const int iso = (int)(idx & 7);
+  const uint8_t* r = rtiles + m * n;
+  const uint8_t* d = dtiles + e * n;
+  long long X = 0, R1 = 0;
+  for (int j = 0; j < n; ++j) {
+    X += (long long)d[j] * r[inv[iso * n + j]];
+    R1 += r[j];
+  }
+  const double norm = cnorm[e];
+  const double cross = __dmul_rn((double)((long long)n * X - (long long)dsum[e] * R1), 1.0 / n);
+  out_err[m] = err;
+  out_s[m] = norm == 0.0 ? 0.0 : __ddiv_rn(cross, norm);
+  out_idx[m] = idx;
+}
+
 // Per-call API variant (fc_match_level / fc_match_tiles): M is known here.
 int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys) {
   FC_CUDA(c, c->enc_hist.reserve(256 * 4 + 64));
@@ -1583,6 +1861,46 @@ int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys) {
   c->stats.fix_ms = fix_ms;
   c->stats.fix_pairs = *c->readback.as<int64_t>();
   c->stats.rescans = 0;
+  return FC_OK;
+}
+
+int real_tc_match(Ctx* c, Level& L, int level, int64_t M, double* d_err, double* d_s,
+                  int64_t* d_idx) {
+  // operands: B = the decimated domains themselves (the baseline layout with
+  // the single slope 1: rint(1.0 * d) = d), A = the permuted ranges
+  const double one = 1.0;
+  int pending = 0, needs = 0;
+  FC_TRY(prepare_begin(c, L, level, 1, &one, 1, FC_PATH_TENSOR, &pending, &needs));
+  if (needs) {
+    Level* lv[1] = {&L};
+    const int st[1] = {pending};
+    FC_TRY(prep_launch(c, lv, st, 1));
+  }
+  FC_TRY(prepare_finish(c, L, FC_PATH_TENSOR, pending));
+  TcOperands& T = L.tc;
+  // the epilogue's column constants replace the baseline table: the level is
+  // prepared afresh on its next use
+  real_const_kernel<<<(unsigned)((L.count + 255) / 256), 256, 0, c->stream>>>(
+      L.sum.as<int32_t>(), L.cnorm.as<double>(), L.count, L.n, T.bconst.as<int4>());
+  FC_CUDA(c, cudaGetLastError());
+  L.prepared = false;
+  FC_CUDA(c, c->real_part.reserve(M * 16 + 64));
+  auto* rec = c->real_part.as<unsigned long long>();
+  FC_CUDA(c, cudaMemsetAsync(rec, 0xff, M * 16, c->stream));
+  FC_CUDA(c, c->enc_hist.reserve(256 * 4 + 64));
+  FC_CUDA(c, c->enc_count.reserve(64 * 4));
+  int32_t* d_M = c->enc_count.as<int32_t>() + 16;
+  auto* d_fix = reinterpret_cast<int64_t*>(c->enc_count.as<int32_t>() + 20);
+  const int32_t m32 = (int32_t)M;
+  FC_TRY(stage_h2d(c, d_M, &m32, 4));
+  FC_TRY(roff_hist(c, M, c->enc_hist.as<int32_t>()));
+  FC_TRY(scan_tc_launch(c, L, M, d_M, c->enc_hist.as<int32_t>(), nullptr, nullptr, d_fix, nullptr,
+                        false, nullptr, nullptr, nullptr, rec));
+  real_finalize_kernel<<<(unsigned)((M + 127) / 128), 128, 0, c->stream>>>(
+      rec, M, L.n, c->rtiles.as<uint8_t>(), c->iso_inv.as<uint16_t>() + iso_table_offset(L.side),
+      L.tiles.as<uint8_t>(), L.sum.as<int32_t>(), L.cnorm.as<double>(), d_err, d_s, d_idx);
+  FC_CUDA(c, cudaGetLastError());
+  c->stats.kernel_launches += 3;
   return FC_OK;
 }
 
