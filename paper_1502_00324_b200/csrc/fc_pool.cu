@@ -290,7 +290,9 @@ __global__ void __launch_bounds__(kChunk / 2) chunk_sort_kernel(SortParams P, in
   using Sorter = cub::BlockMergeSort<KeyIdx, kChunk / 2, 2>;
   __shared__ typename Sorter::TempStorage tmp;
   // this chunk's rank accumulators, filled by chunk_pair_rank_kernel next
-  for (int i = threadIdx.x; i < kChunk; i += blockDim.x) rank[blockIdx.x * kChunk + i] = 0;
+  // (none for the merge path)
+  if (rank)
+    for (int i = threadIdx.x; i < kChunk; i += blockDim.x) rank[blockIdx.x * kChunk + i] = 0;
   const int l = sort_level_of(P, blockIdx.x);
   const SortLevel& L = P.lv[l];
   const int c = blockIdx.x - L.chunk_begin;
@@ -365,6 +367,53 @@ __global__ void rank_scatter_kernel(SortParams P, const int32_t* __restrict__ ra
   const int64_t i = (int64_t)(blockIdx.x - L.chunk_begin * (kChunk / 256)) * 256 + threadIdx.x;
   if (i >= L.count) return;
   L.out[rank_all[L.chunk_begin * kChunk + i]] = L.val[i];
+}
+
+// Large sets: the chunk-sorted runs (chunk_sort_kernel) merged pairwise,
+// ceil(log2(chunks)) passes.  Each thread writes IPT consecutive outputs of
+// its run pair: a merge-path binary search for its start (how many of the
+// first d outputs come from run a), then a sequential merge.  Keys are
+// unique (key, window) pairs, so the order is total and no stability is
+// needed.
+constexpr int kMergeIpt = 8;
+__global__ void __launch_bounds__(256)
+merge_pass_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                  uint64_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n,
+                  int64_t width) {
+  const int64_t o0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kMergeIpt;
+  if (o0 >= n) return;
+  const int64_t a0 = o0 / (2 * width) * (2 * width);
+  const int64_t na = min(width, n - a0);
+  const int64_t b0 = a0 + na;
+  const int64_t nb = max((int64_t)0, min(width, n - b0));
+  const int64_t d = o0 - a0;
+  int64_t lo = max((int64_t)0, d - nb), hi = min(d, na);
+  while (lo < hi) {  // first x with !(a[x] < b[d - x - 1])
+    const int64_t x = (lo + hi) >> 1;
+    const int64_t y = d - x - 1;
+    if (lex_less(kin[a0 + x], vin[a0 + x], kin[b0 + y], vin[b0 + y])) lo = x + 1;
+    else hi = x;
+  }
+  int64_t ia = lo, ib = d - lo;
+  const int64_t end = min(o0 + kMergeIpt, a0 + na + nb);
+  uint64_t ka = ia < na ? kin[a0 + ia] : ~0ull, kb = ib < nb ? kin[b0 + ib] : ~0ull;
+  uint32_t va = ia < na ? vin[a0 + ia] : 0xffffffffu, vb = ib < nb ? vin[b0 + ib] : 0xffffffffu;
+  for (int64_t o = o0; o < end; ++o) {
+    const bool take_a = ib >= nb || (ia < na && lex_less(ka, va, kb, vb));
+    if (take_a) {
+      kout[o] = ka;
+      vout[o] = va;
+      ++ia;
+      ka = ia < na ? kin[a0 + ia] : ~0ull;
+      va = ia < na ? vin[a0 + ia] : 0xffffffffu;
+    } else {
+      kout[o] = kb;
+      vout[o] = vb;
+      ++ib;
+      kb = ib < nb ? kin[b0 + ib] : ~0ull;
+      vb = ib < nb ? vin[b0 + ib] : 0xffffffffu;
+    }
+  }
 }
 
 // Survivors of all levels in one launch.  A survivor's 2B x 2B window is
@@ -779,25 +828,26 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     c->total_launches += 1;
   }
   FC_CUDA(c, cudaEventRecord(c->pool_ev[1], c->stream));
+  // ---- caps without a threshold: every window is ranked (cap 1: argmin) ----
+  // Sort jobs (key, window) ascending = entropy descending, raster ascending
+  // (pool.py:171 argsort(-ent, kind="stable")): the window ids in rank order
+  // land in win_val2 and the level keeps the first `count` of them.
+  struct SortJob {
+    Level* L;
+    int64_t n;
+  };
+  SortJob jobs[kLevels];
+  int n_jobs = 0;
   for (int li = 0; li < kLevels; ++li) {
     Level& L = c->lv[li];
     const int64_t nwin = (int64_t)nx_l[li] * ny_l[li];
-    size_t tmp = 0;
     if (use_tau[li]) continue;
     if (caps[li] == 1) {
       FC_TRY(argmin_windows(c, L.win_key.as<uint64_t>(), nwin, L.win_key2.as<uint64_t>(),
                             L.win_val2.as<uint32_t>()));
       L.count = 1;
     } else {
-      FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, L.win_key.as<uint64_t>(),
-                                                 L.win_key2.as<uint64_t>(), L.win_val.as<uint32_t>(),
-                                                 L.win_val2.as<uint32_t>(), (int)nwin, 0, 64,
-                                                 c->stream));
-      FC_CUDA(c, c->cub_tmp.reserve(tmp));
-      FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, L.win_key.as<uint64_t>(),
-                                                 L.win_key2.as<uint64_t>(), L.win_val.as<uint32_t>(),
-                                                 L.win_val2.as<uint32_t>(), (int)nwin, 0, 64,
-                                                 c->stream));
+      jobs[n_jobs++] = SortJob{&L, nwin};
       L.count = std::min<int64_t>(caps[li], nwin);
     }
   }
@@ -807,69 +857,68 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     FC_TRY(sync_stream(c));
     trace_mark(c, "pool_sync");
   }
-  // ---- phase 2: rank the threshold survivors (entropy desc, raster asc) ----
+  // ---- threshold survivors (entropy > tau), then every ranked set ----
+  for (int li = 0; li < kLevels; ++li) {
+    if (!use_tau[li]) continue;
+    Level& L = c->lv[li];
+    const int64_t nwin = (int64_t)nx_l[li] * ny_l[li];
+    const int nsel = h_nsel[li];
+    if (nsel == 0) {
+      // caps are >= 1 (pool.py:47-48): keep the single highest-entropy window;
+      // the entropy kernel wrote no keys for this level, so rebuild them
+      gather_all_keys_kernel<<<(unsigned)((nwin + 255) / 256), 256, 0, c->stream>>>(
+          L.win_ent.as<double>(), nwin, L.win_key.as<uint64_t>());
+      c->total_launches += 1;
+      FC_TRY(argmin_windows(c, L.win_key.as<uint64_t>(), nwin, L.win_key2.as<uint64_t>(),
+                            L.win_val2.as<uint32_t>()));
+      L.count = 1;
+      continue;
+    }
+    // every survivor is ranked, then the level keeps the first cap of them
+    // (pool.py:171 argsort(-ent, stable)[:cap] over the threshold set)
+    L.count = std::min<int64_t>(nsel, caps[li]);
+    jobs[n_jobs++] = SortJob{&L, nsel};
+  }
   {
-    SortParams SP{};
-    int chunks = 0;
-    int max_sel = 0;
-    for (int li = 0; li < kLevels; ++li)
-      if (use_tau[li]) max_sel = std::max(max_sel, h_nsel[li]);
-    // 1024-element chunks while every level fits kMaxChunks of them (shorter
-    // block sorts; c2: -1% per step), else 2048 (FC_POOL_CHUNK forces one)
+    // small sets: chunk sorts + pairwise chunk ranks (one launch each for all
+    // levels); large sets (more than kMaxChunks chunks): chunk sorts, then
+    // merge passes
+    int64_t max_small = 0;
+    for (int j = 0; j < n_jobs; ++j)
+      if (jobs[j].n <= (int64_t)kMaxChunks * kChunk) max_small = std::max(max_small, jobs[j].n);
+    // 1024-element chunks while every small set fits kMaxChunks of them
+    // (shorter block sorts; c2: -1% per step), else 2048 (FC_POOL_CHUNK forces one)
     const int chunk = c->pool_chunk == kChunk        ? kChunk
                       : c->pool_chunk == kChunkSmall ? kChunkSmall
-                      : max_sel <= kMaxChunks * kChunkSmall ? kChunkSmall
-                                                            : kChunk;
-    for (int li = 0; li < kLevels; ++li) {
-      if (!use_tau[li]) continue;
-      Level& L = c->lv[li];
-      const int64_t nwin = (int64_t)nx_l[li] * ny_l[li];
-      const int nsel = h_nsel[li];
-      if (nsel == 0) {
-        // caps are >= 1 (pool.py:47-48): keep the single highest-entropy window;
-        // the entropy kernel wrote no keys for this level, so rebuild them
-        gather_all_keys_kernel<<<(unsigned)((nwin + 255) / 256), 256, 0, c->stream>>>(
-            L.win_ent.as<double>(), nwin, L.win_key.as<uint64_t>());
-        c->total_launches += 1;
-        FC_TRY(argmin_windows(c, L.win_key.as<uint64_t>(), nwin, L.win_key2.as<uint64_t>(),
-                              L.win_val2.as<uint32_t>()));
-        L.count = 1;
-        continue;
-      }
-      // every survivor is ranked, then the level keeps the first cap of them
-      // (pool.py:171 argsort(-ent, stable)[:cap] over the threshold set)
-      L.count = std::min<int64_t>(nsel, caps[li]);
-      const int nch = (nsel + chunk - 1) / chunk;
-      if (nch <= kMaxChunks) {
+                      : max_small <= kMaxChunks * kChunkSmall ? kChunkSmall
+                                                              : kChunk;
+    SortParams SP{}, SPL{};
+    Level* large_lv[kLevels] = {};
+    int chunks = 0, lchunks = 0;
+    for (int j = 0; j < n_jobs; ++j) {
+      Level& L = *jobs[j].L;
+      const int64_t n = jobs[j].n;
+      if (n <= (int64_t)kMaxChunks * chunk) {
         SortLevel& S = SP.lv[SP.n_levels++];
         S.key = L.win_key.as<uint64_t>();
         S.val = L.win_val.as<uint32_t>();
         S.out = L.win_val2.as<uint32_t>();
-        S.count = nsel;
+        S.count = (int)n;
         S.chunk_begin = chunks;
-        chunks += nch;
+        chunks += (int)((n + chunk - 1) / chunk);
       } else {
-        // large sets: two stable radix sorts (window id, then key) == lexicographic order
-        size_t tmp = 0;
-        uint32_t* ids = L.win_val.as<uint32_t>();
-        uint32_t* ids2 = L.win_val2.as<uint32_t>();
-        uint64_t* k1 = L.win_key.as<uint64_t>();
-        uint64_t* k2 = L.win_key2.as<uint64_t>();
-        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, ids, ids2, k1, k2, nsel, 0, 32,
-                                                   c->stream));
-        FC_CUDA(c, c->cub_tmp.reserve(tmp));
-        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, ids, ids2, k1, k2, nsel, 0,
-                                                   32, c->stream));
-        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, k2, k1, ids2, ids, nsel, 0, 64,
-                                                   c->stream));
-        FC_CUDA(c, c->cub_tmp.reserve(tmp));
-        FC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.ptr, tmp, k2, k1, ids2, ids, nsel, 0,
-                                                   64, c->stream));
-        FC_CUDA(c, cudaMemcpyAsync(ids2, ids, (size_t)nsel * 4, cudaMemcpyDeviceToDevice,
-                                   c->stream));
+        large_lv[SPL.n_levels] = &L;
+        SortLevel& S = SPL.lv[SPL.n_levels++];
+        S.key = L.win_key.as<uint64_t>();
+        S.val = L.win_val.as<uint32_t>();
+        S.out = L.win_val2.as<uint32_t>();
+        S.count = (int)n;
+        S.chunk_begin = lchunks;
+        lchunks += (int)((n + kChunk - 1) / kChunk);
       }
     }
     SP.total_chunks = chunks;
+    SPL.total_chunks = lchunks;
     if (chunks > 0) {
       RankLevel RL[4] = {};
       int pairs = 0;
@@ -895,6 +944,27 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
       }
       FC_CUDA(c, cudaGetLastError());
       c->total_launches += 3;
+    }
+    if (lchunks > 0) {
+      chunk_sort_kernel<kChunk><<<lchunks, kChunk / 2, 0, c->stream>>>(SPL, nullptr);
+      c->total_launches += 1;
+      for (int k = 0; k < SPL.n_levels; ++k) {
+        const SortLevel& S = SPL.lv[k];
+        Level& L = *large_lv[k];
+        uint64_t* kb[2] = {L.win_key.as<uint64_t>(), L.win_key2.as<uint64_t>()};
+        uint32_t* vb[2] = {L.win_val.as<uint32_t>(), L.win_val2.as<uint32_t>()};
+        int cur = 0;
+        const int64_t n = S.count;
+        const unsigned grid = (unsigned)((n + 256 * kMergeIpt - 1) / (256 * kMergeIpt));
+        for (int64_t width = kChunk; width < n; width *= 2, cur ^= 1) {
+          merge_pass_kernel<<<grid, 256, 0, c->stream>>>(kb[cur], vb[cur], kb[cur ^ 1], vb[cur ^ 1],
+                                                         n, width);
+          c->total_launches += 1;
+        }
+        if (cur == 0)  // the ranked ids must end in win_val2
+          FC_CUDA(c, cudaMemcpyAsync(vb[1], vb[0], (size_t)n * 4, cudaMemcpyDeviceToDevice, c->stream));
+      }
+      FC_CUDA(c, cudaGetLastError());
     }
   }
   SurvParams SV{};
