@@ -118,23 +118,58 @@ __global__ void classify_kernel(const unsigned long long* __restrict__ keys,
 // Records in code (= depth-first) order, written straight into pinned host
 // memory: a block's records are contiguous in the output, so they are staged
 // in shared memory and written as one coalesced run (no copy node).
+// Leaf records in depth-first code order: a block-level exclusive scan of the
+// leaf flags plus the block's offset (record_block_offsets_kernel), records
+// staged per block and written contiguously straight into pinned memory.
+__global__ void __launch_bounds__(256) record_block_sums_kernel(int64_t n_codes,
+                                                                const int32_t* __restrict__ flag,
+                                                                int32_t* __restrict__ bsum) {
+  using Red = cub::BlockReduce<int, 256>;
+  __shared__ typename Red::TempStorage tmp;
+  pdl_enter();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = Red(tmp).Sum(i < n_codes ? flag[i] : 0);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = s;
+}
+
+// Exclusive scan of the per-block counts in place (one block; nb <= 1024 * 64).
+__global__ void __launch_bounds__(1024) record_block_offsets_kernel(int32_t* __restrict__ bsum,
+                                                                    int nb) {
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  pdl_enter();
+  const int per = (nb + 1023) / 1024;
+  const int b0 = threadIdx.x * per;
+  int part = 0;
+  for (int k = 0; k < per && b0 + k < nb; ++k) part += bsum[b0 + k];
+  int excl;
+  Scan(tmp).ExclusiveSum(part, excl);
+  for (int k = 0; k < per && b0 + k < nb; ++k) {
+    const int v = bsum[b0 + k];
+    bsum[b0 + k] = excl;
+    excl += v;
+  }
+}
+
 __global__ void __launch_bounds__(256) compact_records_kernel(int64_t n_codes,
                                                               const int32_t* __restrict__ flag,
-                                                              const int32_t* __restrict__ pos,
+                                                              const int32_t* __restrict__ boff,
                                                               const int32_t* __restrict__ rec,
                                                               int32_t* __restrict__ out,
                                                               int32_t* __restrict__ d_count) {
+  using Scan = cub::BlockScan<int, 256>;
+  __shared__ typename Scan::TempStorage tmp;
   __shared__ int32_t rs[256 * 6];
   pdl_enter();
-  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x;
-  const int64_t i = i0 + threadIdx.x;
-  const int64_t last = min(i0 + (int64_t)blockDim.x, n_codes) - 1;
-  const int32_t base = pos[i0];
-  const int32_t cnt = pos[last] + flag[last] - base;
-  if (i == n_codes - 1) *d_count = pos[i] + flag[i];
-  if (i < n_codes && flag[i]) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int f = i < n_codes ? flag[i] : 0;
+  int local, cnt;
+  Scan(tmp).ExclusiveSum(f, local, cnt);
+  const int32_t base = boff[blockIdx.x];
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *d_count = base + cnt;
+  if (f) {
     const int32_t* src = rec + i * 6;
-    int32_t* dst = rs + (pos[i] - base) * 6;
+    int32_t* dst = rs + local * 6;
 #pragma unroll
     for (int k = 0; k < 6; ++k) dst[k] = src[k];
   }
@@ -270,10 +305,6 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
       }
       FC_TRY(reserve_level_scan(c, L, b));
     }
-    size_t need = 0;
-    FC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, need, c->leaf_flag.as<int32_t>(),
-                                             c->leaf_pos.as<int32_t>(), (int)n_codes, c->stream));
-    FC_CUDA(c, c->cub_tmp.reserve(need));
     FC_CUDA(c, c->rec_pinned.reserve(n_codes * 24 + 64));
   }
   trace_mark(c, "reserved");
@@ -440,15 +471,15 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
   {
     int32_t* flag = c->leaf_flag.as<int32_t>();
     int32_t* pos = c->leaf_pos.as<int32_t>();
-    size_t need = 0;
-    FC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, need, flag, pos, (int)n_codes, c->stream));
-    FC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.ptr, need, flag, pos, (int)n_codes,
-                                             c->stream));
-    FC_CUDA(c, launch_k(c, compact_records_kernel, dim3(blocks_for(n_codes)), dim3(256), 0,
-                        n_codes, (const int32_t*)flag, (const int32_t*)pos,
+    const unsigned nb = blocks_for(n_codes);  // n_codes <= 2^16 top slots * 64
+    FC_CUDA(c, launch_k(c, record_block_sums_kernel, dim3(nb), dim3(256), 0, n_codes,
+                        (const int32_t*)flag, pos));
+    FC_CUDA(c, launch_k(c, record_block_offsets_kernel, dim3(1), dim3(1024), 0, pos, (int)nb));
+    FC_CUDA(c, launch_k(c, compact_records_kernel, dim3(nb), dim3(256), 0, n_codes,
+                        (const int32_t*)flag, (const int32_t*)pos,
                         (const int32_t*)c->leaf_rec.as<int32_t>(), c->rec_pinned.as<int32_t>(),
                         d_count + 8));
-    c->total_launches += 2;
+    c->total_launches += 3;
     FC_CUDA(c, cudaMemcpyAsync(h_rb, d_count, kEncReadBytes, cudaMemcpyDeviceToHost, c->stream));
   }
   return FC_OK;
