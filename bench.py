@@ -53,10 +53,11 @@ def parse_args(argv=None):
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--path", default="auto", choices=["auto", "exact", "tensor"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--shard", default="auto", choices=["auto", "images", "ranges"],
+    ap.add_argument("--shard", default="auto", choices=["auto", "images", "ranges", "balanced"],
                     help="auto: images for c3 (its 64-image batch), ranges otherwise; "
                          "images: one seeded image per rank (weak scaling); "
-                         "ranges: one image split into top-level slabs (encode_distributed)")
+                         "ranges: one image split into top-level slabs (encode_distributed); "
+                         "balanced: every level re-sliced evenly over the ranks (encode_balanced)")
     return ap.parse_args(argv)
 
 
@@ -354,7 +355,7 @@ def main():
     wl = W.WORKLOADS[args.workload]
     cfg = W.encoder_config(args.workload, args.path)
     mode = shard_mode(args)
-    ranges = mode == "ranges"
+    ranges = mode in ("ranges", "balanced")
     if ranges:  # every rank holds the same image and encodes its slab of top-level slots
         idx = [0]
     elif wl.images > 1:
@@ -365,7 +366,7 @@ def main():
     gimgs = [fc.GrayImage(im) for im in imgs]
     dimgs = [torch.from_numpy(im.copy()).cuda() for im in imgs]
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")  # 512 MB > L2
-    enc = fc.encode_distributed if ranges else fc.encode
+    enc = {"ranges": fc.encode_distributed, "balanced": fc.encode_balanced}.get(mode, fc.encode)
 
     def step_device():
         reps = []
@@ -483,8 +484,9 @@ def main():
             "workload": args.workload,
             "description": wl.description,
             "images_per_rank": len(imgs), "path": args.path,
-            "sharding": ("range slabs of one image, pool replicated, records all-gathered (NCCL)"
-                         if ranges else "independent images per rank, no data-path collective"),
+            "sharding": {"ranges": "range slabs of one image, pool replicated, records all-gathered (NCCL)",
+                         "balanced": "every level's ranges re-sliced evenly, results all-gathered per level (NCCL)",
+                         }.get(mode, "independent images per rank, no data-path collective"),
             "l2": "flushed (512 MB write) before every timed step",
             "pool_sizes": list(reps[0].pool_sizes), "step_blocks": list(reps[0].step_blocks),
             "comparisons_per_step": comps_all / args.steps,

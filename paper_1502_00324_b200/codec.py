@@ -239,8 +239,7 @@ def encode_distributed(image: GrayImage, config: EncoderConfig, context=None, de
     rank = dist.get_rank() if dist_on else 0
     world = dist.get_world_size() if dist_on else 1
     rec, pool, level_stats = encode_shard(image, config, rank, world, ctx, device_image)
-    device = "cpu" if dist_on and dist.get_backend() == "gloo" else f"cuda:{ctx.device}"
-    allrec = sharding.gather_rows(rec, device=device)
+    allrec = sharding.gather_rows(rec, device=_collective_device(ctx))
     policy = config.policy
     s_sets = tuple(policy.s_set(level) for level in (1, 2, 3, 4))
     stream = CompressedStream(
@@ -255,6 +254,22 @@ def encode_distributed(image: GrayImage, config: EncoderConfig, context=None, de
     return stream, _report(image, config, pool, stream, step_blocks, collage_ssd, 0.0, encode_time,
                            comparisons, sum(ls["scan_ms"] for ls in level_stats), level_stats,
                            {"sharded_ranks": world})
+
+
+def _collective_device(ctx) -> str:
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_backend() == "gloo":
+        return "cpu"
+    return f"cuda:{ctx.device}"
+
+
+def encode_balanced(image: GrayImage, config: EncoderConfig, context=None, device_image=None):
+    """Range-sharded encode with per-level re-balancing: the
+    level-wise driver with every level's ranges split evenly over the ranks
+    (encode_levelwise(balanced=True)); the collective per level is one
+    all-gather of the level's (err, index, mean) rows."""
+    return encode_levelwise(image, config, context, device_image, balanced=True)
 
 
 def image_comparisons(step_blocks, pool_sizes, s_sets) -> int:
@@ -287,10 +302,17 @@ def _report(image, config, pool, stream, step_blocks, collage_ssd, pool_time, en
         comparisons=comparisons, scan_device_ms=scan_ms, level_stats=level_stats, phase_ms=phase)
 
 
-def encode_levelwise(image: GrayImage, config: EncoderConfig, context=None, device_image=None):
+def encode_levelwise(image: GrayImage, config: EncoderConfig, context=None, device_image=None,
+                     balanced: bool = False):
     """Same result as encode(), driven level by level from the host through the
     match_level seam (fc_level_prepare + fc_match_level):
-    the host runs the split test and builds the child origins."""
+    the host runs the split test and builds the child origins.
+
+    balanced=True (one process per GPU, torch.distributed initialised): every
+    level's range list is re-sliced evenly over the ranks and the shares'
+    results all-gathered (sharding.balanced_match), so data-dependent splits
+    never leave a rank with more than its share of a level; every rank
+    returns the full, byte-identical stream."""
     if image.width % 16 or image.height % 16:
         raise ValueError(f"dimensions not multiple of 16: {image.width}x{image.height}")
     t_start = time.perf_counter()
@@ -318,7 +340,14 @@ def encode_levelwise(image: GrayImage, config: EncoderConfig, context=None, devi
         t0 = time.perf_counter()
         ctx.level_prepare(level, baseline, policy.s_set(level), lvl_path)
         t1 = time.perf_counter()
-        err, idx, rmean = ctx.match_level(level, o)
+        if balanced:
+            from . import sharding
+
+            err, idx, rmean = sharding.balanced_match(
+                lambda share: ctx.match_level(level, share), np.asarray(o, dtype=np.int32),
+                device=_collective_device(ctx))
+        else:
+            err, idx, rmean = ctx.match_level(level, o)
         t2 = time.perf_counter()
         phase[f"prepare_l{level}"] = 1e3 * (t1 - t0)
         phase[f"match_l{level}"] = 1e3 * (t2 - t1)

@@ -78,3 +78,31 @@ def reduce_metrics(metrics: dict, device="cpu") -> dict:
     out.update({k: float(v) for k, v in zip(MAX_KEYS, mx.tolist())})
     out.update({k: float(v) for k, v in zip(SUM_KEYS, sm.tolist())})
     return out
+
+
+def balanced_match(match_local, origins, device="cpu"):
+    """One level of the re-balanced range sharding: every rank holds the same
+    global range list ``origins`` (int32 [M, 2]); rank r matches the
+    contiguous share slab_for_rank(M, r, world) with ``match_local(share) ->
+    (err int64, idx int64, rmean float64)`` and the shares are all-gathered
+    in rank order, so every rank continues with the whole level's result
+    (and so the same next-level list).  Re-slicing per level keeps the ranks
+    balanced whatever the data-dependent splits were."""
+    import numpy as np
+    import torch.distributed as dist
+
+    o = np.asarray(origins, dtype=np.int32).reshape(-1, 2)
+    dist_on = dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size() if dist_on else 1
+    rank = dist.get_rank() if dist_on else 0
+    lo, hi = slab_for_rank(o.shape[0], rank, world)
+    rows = np.zeros((hi - lo, 6), dtype=np.int32)
+    if hi > lo:
+        err, idx, rmean = match_local(o[lo:hi])
+        rows[:, 0:2] = np.ascontiguousarray(err, dtype=np.int64).view(np.int32).reshape(-1, 2)
+        rows[:, 2:4] = np.ascontiguousarray(idx, dtype=np.int64).view(np.int32).reshape(-1, 2)
+        rows[:, 4:6] = np.ascontiguousarray(rmean, dtype=np.float64).view(np.int32).reshape(-1, 2)
+    full = gather_rows(rows, device=device)
+    return (np.ascontiguousarray(full[:, 0:2]).view(np.int64).reshape(-1),
+            np.ascontiguousarray(full[:, 2:4]).view(np.int64).reshape(-1),
+            np.ascontiguousarray(full[:, 4:6]).view(np.float64).reshape(-1))

@@ -62,3 +62,46 @@ def test_encode_distributed_two_processes_c2_bytes():
         # the whole image's comparisons, from the gathered leaves == sum of the slabs'
         assert comps == res[0][3] + res[1][3]
     assert res[0][4] + res[1][4] == len(np.asarray(g["records_c2"]))
+
+
+def _balanced_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import paper_1502_00324_b200 as fc
+    from paper_1502_00324_b200 import _native
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = np.load(os.path.join(GOLDEN, "encode_c2.npz"))
+    caps = tuple(int(v) for v in g["caps_c2"])
+    params = fc.PoolParams(pool_cap=max(caps), strides=tuple(int(v) for v in g["strides_c2"]),
+                           level_caps=caps)
+    cfg = fc.EncoderConfig(pool=params, thresholds=tuple(float(v) for v in g["thresholds_c2"]))
+    ctx = _native.Context(0)
+    stream, report = fc.encode_balanced(fc.GrayImage(g["image_c2"]), cfg, context=ctx)
+    q.put((rank, fc.serialize(stream) == g["bytes_c2"].tobytes(), int(report.collage_ssd),
+           [ls["ranges"] for ls in report.level_stats]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_encode_balanced_two_processes_c2_bytes():
+    """Per-level re-balanced sharding: each level's ranges split evenly over 2
+    ranks (gloo, both on cuda:0), results all-gathered; stream == golden."""
+    g = np.load(os.path.join(GOLDEN, "encode_c2.npz"))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_balanced_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {r[0]: r[1:] for r in (q.get(timeout=600) for _ in procs)}
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank in (0, 1):
+        same, collage, shares = res[rank]
+        assert same and collage == int(g["collage_c2"])
+    # every level's shares differ by at most one range
+    for a, b in zip(res[0][2], res[1][2]):
+        assert abs(a - b) <= 1

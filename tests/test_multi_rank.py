@@ -117,3 +117,61 @@ def test_bench_gpus2_spawns_two_ranks():
     assert len(lines) == 1
     line = json.loads(lines[0])
     assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+
+
+def _fake_match(share):
+    """Deterministic stand-in for ctx.match_level: (err, idx, rmean) per origin."""
+    import numpy as np
+
+    s = np.asarray(share, dtype=np.int64).reshape(-1, 2)
+    return s[:, 0] * 7 + s[:, 1], s[:, 0] + 3 * s[:, 1] + (1 << 40), s[:, 0] / 2.0 + s[:, 1] / 3.0
+
+
+def _balanced_worker(rank, world, port, q):
+    import numpy as np
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    calls = []
+
+    def local(share):
+        calls.append(len(share))
+        return _fake_match(share)
+
+    results = []
+    for m in (0, 1, 5, 1024, 1027):  # a level's range count, split unevenly by the quadtree
+        o = np.stack([np.arange(m) % 97, np.arange(m) // 97], axis=1).astype(np.int32)
+        results.append(sharding.balanced_match(local, o))
+    q.put((rank, results, calls))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_balanced_match_gloo_world2():
+    """Per-level re-balancing: each rank matches an even share of the level's
+    ranges and every rank gets the whole level's (err, idx, mean), in order."""
+    import numpy as np
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_balanced_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {r: (res, calls) for r, res, calls in (q.get(timeout=120) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for k, m in enumerate((0, 1, 5, 1024, 1027)):
+        o = np.stack([np.arange(m) % 97, np.arange(m) // 97], axis=1).astype(np.int32)
+        want = _fake_match(o)
+        for rank in (0, 1):
+            res = got[rank][0][k]
+            for a, b in zip(res, want):
+                assert np.array_equal(a, b)
+    # each rank matched exactly its even share of every level (empty shares skip the call)
+    for rank in (0, 1):
+        want = [hi - lo for lo, hi in (sharding.slab_for_rank(m, rank, 2)
+                                       for m in (0, 1, 5, 1024, 1027)) if hi > lo]
+        assert got[rank][1] == want
