@@ -76,10 +76,11 @@ int fc_set_device_io(fc_ctx* ctx, int device_io);
  * fc_encode to the raster slab [top_begin, top_end) of 16x16 top-level slots
  * (default 0 / -1 = all); the records are then exactly that slab's run of the
  * full depth-first record list, so per-rank slabs concatenate in rank order.
- * Measured kernel variants (same results): "tc_g1" (all 16 epilogue warps
- * drain every accumulator), "tc_deferred" (0: resolve columns at once),
- * "fix_fused" (clamp corrections inside the contraction), "pdl"
- * (programmatic dependent launch between the level loop's kernels). */
+ * Variants with identical results, kept for tests and timing:
+ * "tc_span_units" (1: the contraction's round-robin span schedule, otherwise
+ * only used when the B operand exceeds L2), "real_cuda_cores" (1: the
+ * real-valued slope search on the dp4a kernel instead of the tensor cores),
+ * "pdl" (programmatic dependent launch between the level loop's kernels). */
 int fc_set_option(fc_ctx* ctx, const char* name, int64_t value);
 
 /* terms[k-1] = (k/n) * log(k/n), k = 1..n, produced by the host's numpy so the
@@ -115,7 +116,8 @@ int fc_pool_entries(fc_ctx* ctx, int level, double* entropy, uint8_t* tiles, dou
 
 /* Quantised candidate operands for a level (matcher.py:132-159).
  * baseline = 0: proposed mode rint(s*(d - mean)); 1: rint(s*d).
- * path: FC_PATH_AUTO / FC_PATH_EXACT / FC_PATH_TENSOR. */
+ * path: FC_PATH_AUTO / FC_PATH_EXACT / FC_PATH_TENSOR; the tensor path
+ * (tcgen05 int8 contraction) covers both modes for B >= 4. */
 int fc_level_prepare(fc_ctx* ctx, int level, int baseline, const double* svals, int32_t s_count,
                      int32_t path);
 
@@ -136,7 +138,9 @@ int fc_match_tiles(fc_ctx* ctx, int level, const uint8_t* tiles, int64_t count, 
  * origin: the minimal projection error max(rnorm - cross^2/cnorm, 0), the
  * slope cross/cnorm of that candidate (0 for a flat domain) and its flat
  * index e*8 + iso (first minimum), all fp64 bit-identical to the reference.
- * Needs the pool only (no fc_level_prepare); host buffers (out_idx may be NULL). */
+ * B >= 4 runs on the tcgen05 contraction (X = <d, r_iso> u8 x u8, fp64
+ * epilogue); B = 2 on CUDA cores.  Needs the pool only (no fc_level_prepare;
+ * it re-prepares the level's operands); host buffers (out_idx may be NULL). */
 int fc_real_match_level(fc_ctx* ctx, int level, const int32_t* origins_xy, int64_t count,
                         double* out_err, double* out_s, int64_t* out_idx);
 
@@ -153,8 +157,8 @@ int fc_scan_candidates(fc_ctx* ctx, const int16_t* ranges, const double* rmeans,
  * when its best error exceeds thresholds[l]^2 * B^2; level-4 ranges never
  * split.  svals holds the four levels' s sets back to back (s_counts[l]
  * values each); baseline 0 = proposed mode; path FC_PATH_*, where
- * FC_PATH_TENSOR uses the exact kernel on levels the contraction does not
- * cover (baseline mode, 2x2 ranges).  Leaf records come out in the
+ * FC_PATH_TENSOR uses the exact kernel on the level the contraction does
+ * not cover (2x2 ranges).  Leaf records come out in the
  * reference's depth-first order as int32 [count][6] =
  * {step, offset, iso, addr, sidx, err}; records may be NULL (fetch them
  * later with fc_encode_records).  Raises FC_ERR_EMPTY_POOL when ranges reach
