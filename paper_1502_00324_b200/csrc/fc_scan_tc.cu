@@ -1506,7 +1506,10 @@ __global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
 
 }  // namespace
 
-static int tc_config(Ctx* c, int kpad, int base, TcParams* prm, int real = 0);
+static int tc_config(Ctx* c, int kpad, int base, TcParams* prm, int real = 0, int64_t pairs = 0);
+static int64_t tc_pairs_bound(const Level& L, int64_t M_bound) {
+  return (M_bound * 8 + kTileM - 1) / kTileM * L.tc.ntiles;
+}
 
 int gather_build(Ctx* c, Level& L, const int32_t* d_origins, const int32_t* d_M, int64_t bound,
                  int32_t* d_hist, uint64_t* d_keys, unsigned long long* d_time) {
@@ -1527,7 +1530,7 @@ int gather_build(Ctx* c, Level& L, const int32_t* d_origins, const int32_t* d_M,
   int64_t slots = bound;
   if (L.path == FC_PATH_TENSOR) {
     TcParams prm{};
-    FC_TRY(tc_config(c, L.tc.kpad, L.baseline, &prm));
+    FC_TRY(tc_config(c, L.tc.kpad, L.baseline, &prm, 0, tc_pairs_bound(L, bound)));
     P.kpad = L.tc.kpad;
     P.planes = L.tc.planes;
     P.m_digits = L.tc.m_digits;
@@ -1618,11 +1621,18 @@ int level_prepare_tc_finish(Ctx* c, Level& L) {
 }
 
 // Resident A row tiles and B ring depth within the shared-memory budget.
-static int tc_config(Ctx* c, int kpad, int base, TcParams* prm, int real) {
+// pairs: bound on the (row tile, column tile) pairs of the launch.  Short K:
+// many resident row tiles amortise the per-tile B load and bookkeeping on
+// large levels (c5: RG 8), few give more row groups and a shorter segment
+// start / resolution on small ones (c2 L2/L3: RG 2 is 4-12% faster).
+static int tc_config(Ctx* c, int kpad, int base, TcParams* prm, int real, int64_t pairs) {
   prm->kpad = kpad;
   prm->base = base && !real;
   prm->real = real;
-  prm->rg = real ? (kpad <= 128 ? 2 : 1) : kpad <= 64 ? 8 : kpad <= 128 ? 4 : kpad <= 320 ? 2 : 1;
+  const bool large = pairs >= 2048ll * c->sm_count;
+  prm->rg = real ? (kpad <= 128 ? 2 : 1)
+                 : kpad <= 128 ? (large ? 8 : 2) : kpad <= 320 ? 2 : 1;
+  if (c->tc_rg > 0 && !real) prm->rg = c->tc_rg;  // FC_TC_RG (measurement)
   for (;;) {
     prm->stages = 8;
     while (prm->stages > 2 && (int)smem_bytes(*prm) > kSmemBudget) --prm->stages;
@@ -1639,10 +1649,9 @@ int reserve_level_scan(Ctx* c, Level& L, int64_t bound) {
   FC_TRY(ensure_iso_tables(c));
   FC_TRY(reserve_ranges(c, L, bound));
   if (L.path != FC_PATH_TENSOR) return FC_OK;
-  TcParams prm{};
-  FC_TRY(tc_config(c, L.tc.kpad, L.baseline, &prm));
+  // reserved for the largest row-group size any launch may pick
   const int64_t rtiles_max = (bound * 8 + kTileM - 1) / kTileM;
-  const int64_t rows_max = ((rtiles_max + prm.rg - 1) / prm.rg) * prm.rg * kTileM;
+  const int64_t rows_max = ((rtiles_max + 7) / 8) * 8 * kTileM;
   FC_CUDA(c, c->a_tiles.reserve(rows_max * L.tc.kpad));
   FC_CUDA(c, c->row_meta.reserve(rows_max * 16));
   FC_CUDA(c, c->tc_plan.reserve(sizeof(TcPlan) + sizeof(FixPlan) + 64));
@@ -1672,7 +1681,7 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   if (M_bound == 0) return FC_OK;
   FC_TRY(ensure_iso_tables(c));
   TcParams prm{};
-  FC_TRY(tc_config(c, T.kpad, L.baseline, &prm, real_out ? 1 : 0));
+  FC_TRY(tc_config(c, T.kpad, L.baseline, &prm, real_out ? 1 : 0, tc_pairs_bound(L, M_bound)));
   const int RG = prm.rg;
   const int64_t rtiles_max = (M_bound * 8 + kTileM - 1) / kTileM;
   const int64_t rows_max = ((rtiles_max + RG - 1) / RG) * RG * kTileM;
