@@ -366,7 +366,9 @@ def main():
     gimgs = [fc.GrayImage(im) for im in imgs]
     dimgs = [torch.from_numpy(im.copy()).cuda() for im in imgs]
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")  # 512 MB > L2
-    enc = {"ranges": fc.encode_distributed, "balanced": fc.encode_balanced}.get(mode, fc.encode)
+    # one process: the sharded drivers reduce to the plain public encode
+    enc = ({"ranges": fc.encode_distributed, "balanced": fc.encode_balanced}.get(mode, fc.encode)
+           if world > 1 else fc.encode)
 
     def step_device():
         reps = []
