@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
       ptx::tc_fence_after();
       for (int t = t1 - 1; t >= t0; --t, ++L) {
         const int s = L % STAGES;
-        ptx::mbar_wait(full_bar(s), (L / STAGES) & 1);
+        ptx::mbar_wait_sleep(full_bar(s), (L / STAGES) & 1);
         ptx::tc_fence_after();
         const uint64_t bd0 = ptx::umma_desc(ptx::smem_u32(sStage + s * kStage) + b_half, kTileN * 16, 128);
         // this issuer's pairs of the tile: Hr = Ht + r with (Hr & 1) == my_par
@@ -929,7 +929,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
         H += RG;
         for (int r = (my_par ^ (int)(Ht & 1)) & 1; r < RG; r += 2) {
           const uint64_t ad0 = ptx::umma_desc(a_base + r * (kTileM * KPAD), kTileM * 16, 128);
-          ptx::mbar_wait(tempty_i, (((Ht + r) >> 1) & 1) ^ 1);
+          ptx::mbar_wait_sleep(tempty_i, (((Ht + r) >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
           ptx::umma_i8_elect(d, ad0, bd0, kIdesc, 0u);
           for (int ks = 1; ks < ksteps; ++ks)
