@@ -256,6 +256,46 @@ def encode_distributed(image: GrayImage, config: EncoderConfig, context=None, de
                            {"sharded_ranks": world})
 
 
+_BATCH_CONTEXTS = {}
+
+
+def encode_batch(images, config: EncoderConfig, contexts=None, device_images=None,
+                 workers: int = 4):
+    """Encode a batch of independent images (the c3 workload) -> list of
+    (CompressedStream, EncodeReport) in input order, each identical to
+    encode(image, config).
+
+    Small images leave most of the GPU idle inside one encode, so the batch
+    is spread over ``workers`` contexts -- each its own CUDA stream, device
+    buffers and graph -- driven from host threads (the C calls release the
+    GIL), and the encodes overlap on the device."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    images = list(images)
+    if contexts is None:
+        dev = _native.default_context().device
+        ctxs = _BATCH_CONTEXTS.setdefault(dev, [])
+        while len(ctxs) < workers:
+            ctxs.append(_native.Context(dev))
+        contexts = ctxs[:workers]
+    contexts = list(contexts)
+    n = len(contexts)
+    out = [None] * len(images)
+
+    def run(w):
+        for i in range(w, len(images), n):
+            dimg = device_images[i] if device_images is not None else None
+            out[i] = encode(images[i], config, context=contexts[w], device_image=dimg)
+
+    if n == 1 or len(images) <= 1:
+        run(0) if n == 1 else [run(w) for w in range(n)]
+        return out
+    with ThreadPoolExecutor(max_workers=n) as ex:
+        for f in [ex.submit(run, w) for w in range(n)]:
+            f.result()
+    return out
+
+
 def _collective_device(ctx) -> str:
     import torch.distributed as dist
 

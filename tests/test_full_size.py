@@ -113,3 +113,15 @@ def test_c3_batch_images_bytes_identical(ctx):
         assert list(report.pool_sizes) == row["caps"], row["image"]
         assert hashlib.sha256(data).hexdigest() == row["sha256"], row["image"]
         assert report.collage_ssd == row["collage_ssd"]
+
+
+def test_c3_encode_batch_matches_reference(ctx):
+    """encode_batch (images overlapped on several contexts / streams, the c3
+    bench path) gives each image's reference stream bytes."""
+    cfg = W.encoder_config("c3")
+    rows = FULL["c3"]["images"]
+    imgs = [fc.GrayImage(W.make_image("c3", row["image"])) for row in rows]
+    outs = fc.encode_batch(imgs, cfg, workers=3)
+    for row, (stream, report) in zip(rows, outs):
+        assert hashlib.sha256(fc.serialize(stream)).hexdigest() == row["sha256"], row["image"]
+        assert report.collage_ssd == row["collage_ssd"]
