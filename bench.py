@@ -374,7 +374,8 @@ def main():
     # on several contexts / streams; every encode is synchronous at return,
     # so events on the first context's stream bracket the whole batch
     batch = len(gimgs) > 1 and not ranges
-    bctxs = [ctx] + [_native.Context(local) for _ in range(3)] if batch else [ctx]
+    n_ctx = int(os.environ.get("FC_BATCH_CONTEXTS", "8"))
+    bctxs = [ctx] + [_native.Context(local) for _ in range(n_ctx - 1)] if batch else [ctx]
 
     def step_device():
         if batch:

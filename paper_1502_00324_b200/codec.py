@@ -260,7 +260,7 @@ _BATCH_CONTEXTS = {}
 
 
 def encode_batch(images, config: EncoderConfig, contexts=None, device_images=None,
-                 workers: int = 4):
+                 workers: int = 8):
     """Encode a batch of independent images (the c3 workload) -> list of
     (CompressedStream, EncodeReport) in input order, each identical to
     encode(image, config).
