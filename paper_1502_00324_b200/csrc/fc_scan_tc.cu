@@ -661,9 +661,13 @@ __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, 
     pre = p.bconst[(size_t)(t1 - 1) * kTileN + gtid];
     for (int t = t1 - 1; t >= t0; --t) {
       const int valid_slots = p.tile_info[t].y;
-      int4* cb = const_cast<int4*>(cbase) + (tcount & 1) * kTileN;
+      // per column: {D1, rcp / n^2 as fp32} (the screen reads two columns per
+      // 16-byte load) and the fp64 rcp / n^2 for the exact path
+      int2* cf = reinterpret_cast<int2*>(const_cast<int4*>(cbase) + (tcount & 1) * kTileN);
+      int2* cd = cf + kTileN;
       ++tcount;
-      cb[gtid] = pre;
+      cf[gtid] = make_int2(pre.x, pre.y);
+      cd[gtid] = make_int2(pre.z, pre.w);
       ptx::named_bar_sync(1 + gq, kEpiWarps / 2 * 32);
       if (t > t0) pre = p.bconst[(size_t)(t - 1) * kTileN + gtid];
       const uint32_t Ht = H;
@@ -677,102 +681,118 @@ __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, 
         int bcol = st_col[r * kBS];
         bool changed = false;
         const uint32_t ph = ((Ht + r) >> 1) & 1;
-        const uint8_t* arow = p.a_tiles + (size_t)(g * RG + r) * (kTileM * KPAD) +
-                              (row >> 3) * 128 + (row & 7) * 16;
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
           ptx::mbar_wait_sleep(tfull0 + 8u * h, ph);
           ptx::tc_fence_after();
-          int va[32], vb[32];
-          ptx::tmem_ld32(tm0 + h * kAccN, va);
-          ptx::tmem_ld32(tm0 + h * kAccN + 32, vb);
-          ptx::tmem_wait_ld();
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(tempty0 + 8u * h);
-          const int s0 = h * kAccN + slice;
-          if (rn == 0.0) {
-            // a constant range: every candidate's error is max(0 - gain, 0) = 0,
-            // so the first candidate of the slice in column order wins
-            const int col = t * kTileN + s0;
-            if (s0 < valid_slots && (bt.x > 0.0 || col < bcol)) {
-              bt = make_double2(0.0, 0.0);
-              bcol = col;
-              changed = true;
+          // the half's 64 columns in two chunks of 32 (the accumulator is
+          // released after the second load); rn == 0 rows take the shortcut
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {
+            int v[32];
+            ptx::tmem_ld32(tm0 + h * kAccN + 32 * c, v);
+            ptx::tmem_wait_ld();
+            if (c == 1) {
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive(tempty0 + 8u * h);
             }
-            continue;
-          }
-          // fast path: g32 = fl32(xn)^2 * rcp32 / n^2 per candidate; g32 < T32
-          // implies g < T (margins cover the fp32 roundings, < 5e-7 relative)
-          const int nvalid = valid_slots - s0;
-          const unsigned long long vmask =
-              nvalid >= 64 ? ~0ull : nvalid <= 0 ? 0ull : (1ull << nvalid) - 1;
-          const float T32 = bt.y > 0.0 ? __fmul_rn(__double2float_rd(bt.y), 0.999999f) : 0.0f;
-          unsigned long long mask = 0ull;
-          float gmax = -1.0f;
+            const int s0 = h * kAccN + slice + 32 * c;
+            if (rn == 0.0) {
+              // a constant range: every candidate's error is max(0 - gain, 0) = 0,
+              // so the first candidate of the slice in column order wins
+              const int col = t * kTileN + s0;
+              if (c == 0 && s0 < valid_slots && (bt.x > 0.0 || col < bcol)) {
+                bt = make_double2(0.0, 0.0);
+                bcol = col;
+                changed = true;
+              }
+              continue;
+            }
+            const int nvalid = valid_slots - s0;
+            const uint32_t vmask = nvalid >= 32 ? ~0u : nvalid <= 0 ? 0u : (1u << nvalid) - 1;
+            const float T32 = bt.y > 0.0 ? __fmul_rn(__double2float_rd(bt.y), 0.999999f) : 0.0f;
+            const int4* cf4 = reinterpret_cast<const int4*>(cf + s0);
+            // screen: g32 = fl32(xn)^2 * rcp32 per candidate, xn = n X - D1 R1
+            // (|xn| = n |cross| < 2^31, so wrapping int32 is exact); g32 < T32
+            // implies g < T (the margins cover the fp32 roundings, < 5e-7 relative)
+#define FC_REAL_G32(D1, RCP, X)                                                           \
+  __fmul_rn(__fmul_rn(__int2float_rn((D1) * nR1 + ((X) << shift)),                     \
+                      __int2float_rn((D1) * nR1 + ((X) << shift))),                     \
+            __int_as_float(RCP))
+            // one predicate-OR per candidate; the slices that pass (and the first
+            // slice of a segment) rebuild the candidate mask below
+            bool any = bt.x == DBL_MAX;
 #pragma unroll
-          for (int j = 0; j < 64; ++j) {
-            const int4 k = cb[s0 + j];  // {D1, rcp / n^2 as fp32, as fp64 (lo, hi)}
-            // xn = n X - D1 R1: |xn| = n |cross| < 2^31, so wrapping int32 is exact
-            const int xn = k.x * nR1 + ((j < 32 ? va[j] : vb[j - 32]) << shift);
-            const float xf = __int2float_rn(xn);
-            const float g32 = __fmul_rn(__fmul_rn(xf, xf), __int_as_float(k.y));
-            mask |= (unsigned long long)(g32 >= T32) << j;
-            gmax = ((vmask >> j) & 1ull) ? fmaxf(gmax, g32) : gmax;
-            if (j < 32) va[j] = __float_as_int(g32);
-            else vb[j - 32] = __float_as_int(g32);
-          }
-          mask &= vmask;
-          if (mask == 0ull) continue;
-          if (bt.x == DBL_MAX) {
-            // first slice of a segment (no best yet): only the candidates within
-            // 1e-4 of the slice's largest g32 can hold its best gain -- any other
-            // has g < g(max) and so a larger error -- plus every candidate whose
-            // gain may reach rnorm (error clamped to 0: ties by column), so those
-            // are evaluated
-            const float gcut = fminf(__fmul_rn(gmax, 0.9999f),
-                                     __fmul_rn(__double2float_rd(rn), 0.999999f));
-            mask = 0ull;
+            for (int q = 0; q < 16; ++q) {
+              const int4 k = cf4[q];
+              any |= FC_REAL_G32(k.x, k.y, v[2 * q]) >= T32;
+              any |= FC_REAL_G32(k.z, k.w, v[2 * q + 1]) >= T32;
+            }
+            if (!any) continue;
+            uint32_t mask = 0u;
+            float gmax = -1.0f;
 #pragma unroll
-            for (int j = 0; j < 64; ++j)
-              mask |= (unsigned long long)(__int_as_float(j < 32 ? va[j] : vb[j - 32]) >= gcut) << j;
+            for (int q = 0; q < 16; ++q) {
+              const int4 k = cf4[q];
+              const float g0 = FC_REAL_G32(k.x, k.y, v[2 * q]);
+              const float g1 = FC_REAL_G32(k.z, k.w, v[2 * q + 1]);
+              mask |= ((uint32_t)(g0 >= T32) << (2 * q)) | ((uint32_t)(g1 >= T32) << (2 * q + 1));
+              gmax = ((vmask >> (2 * q)) & 1u) ? fmaxf(gmax, g0) : gmax;
+              gmax = ((vmask >> (2 * q + 1)) & 1u) ? fmaxf(gmax, g1) : gmax;
+            }
             mask &= vmask;
-          }
-          // exact path (rare): X recomputed from the operands, then fc_real.cu's steps
-          auto exact = [&](int j) {
-            const int slot = s0 + j;
-            const int col = t * kTileN + slot;  // real mode: slots are columns in order
-            const int8_t* bcolp = p.b_tiles + (size_t)t * kB + (slot >> 3) * 128 + (slot & 7) * 16;
-            int X = 0;
-            for (int kc = 0; kc < KPAD / 16; ++kc) {
-              const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(arow + kc * (kTileM * 16)));
-              const uint4 b4 = __ldg(reinterpret_cast<const uint4*>(bcolp + kc * (kTileN * 16)));
-              X = dp4a_uu(a4.x, b4.x, X);
-              X = dp4a_uu(a4.y, b4.y, X);
-              X = dp4a_uu(a4.z, b4.z, X);
-              X = dp4a_uu(a4.w, b4.w, X);
+            if (mask == 0u) continue;
+            if (bt.x == DBL_MAX) {
+              // first slice of a segment (no best yet): only the candidates within
+              // 1e-4 of the slice's largest g32 can hold its best gain -- any other
+              // has g < g(max) and so a larger error -- plus every candidate whose
+              // gain may reach rnorm (error clamped to 0: ties by column)
+              const float gcut = fminf(__fmul_rn(gmax, 0.9999f),
+                                       __fmul_rn(__double2float_rd(rn), 0.999999f));
+              mask = 0u;
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                const int4 k = cf4[q];
+                mask |= ((uint32_t)(FC_REAL_G32(k.x, k.y, v[2 * q]) >= gcut) << (2 * q)) |
+                        ((uint32_t)(FC_REAL_G32(k.z, k.w, v[2 * q + 1]) >= gcut) << (2 * q + 1));
+              }
+              mask &= vmask;
             }
-            const int4 k = cb[slot];
-            const double rcpn = __hiloint2double(k.w, k.z);
-            const double xd = (double)(k.x * nR1 + (X << shift));
-            const double gq2 = __dmul_rn(__dmul_rn(xd, xd), rcpn);  // == its fl(cc * rcp)
-            const double cross = __dmul_rn(xd, ninv);
-            const double cc = __dmul_rn(cross, cross);
-            const bool flat = rcpn == 0.0;
-            if (!flat && __dsub_rn(rn, gq2) > bt.x + 1e-14 * (rn + gq2)) return;
-            const double gain = flat ? 0.0 : __ddiv_rn(cc, p.cnorm[col]);
-            const double err = fmax(__dsub_rn(rn, gain), 0.0);
-            if (err < bt.x || (err == bt.x && col < bcol)) {
-              bt.x = err;
-              bt.y = real_threshold(rn, err);
-              bcol = col;
-              changed = true;
+#undef FC_REAL_G32
+            // exact path (rare): X selected from the chunk, then fc_real.cu's steps
+            while (mask) {
+              const int j = __ffs(mask) - 1;
+              mask &= mask - 1;
+              int w[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) w[i] = (j & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) w[i] = (j & 2) ? w[2 * i + 1] : w[2 * i];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) w[i] = (j & 4) ? w[2 * i + 1] : w[2 * i];
+#pragma unroll
+              for (int i = 0; i < 2; ++i) w[i] = (j & 8) ? w[2 * i + 1] : w[2 * i];
+              const int X = (j & 16) ? w[1] : w[0];
+              const int slot = s0 + j;
+              const int col = t * kTileN + slot;  // real mode: slots are columns in order
+              const int2 kf = cf[slot], kd = cd[slot];
+              const double rcpn = __hiloint2double(kd.y, kd.x);
+              const double xd = (double)(kf.x * nR1 + (X << shift));
+              const double gq2 = __dmul_rn(__dmul_rn(xd, xd), rcpn);  // == its fl(cc * rcp)
+              const double cross = __dmul_rn(xd, ninv);
+              const double cc = __dmul_rn(cross, cross);
+              const bool flat = rcpn == 0.0;
+              if (!flat && __dsub_rn(rn, gq2) > bt.x + 1e-14 * (rn + gq2)) continue;
+              const double gain = flat ? 0.0 : __ddiv_rn(cc, p.cnorm[col]);
+              const double err = fmax(__dsub_rn(rn, gain), 0.0);
+              if (err < bt.x || (err == bt.x && col < bcol)) {
+                bt.x = err;
+                bt.y = real_threshold(rn, err);
+                bcol = col;
+                changed = true;
+              }
             }
-          };
-          while (mask) {
-            const int j = __ffsll((long long)mask) - 1;
-            mask &= mask - 1;
-            exact(j);
           }
         }
         if (changed) {
@@ -1800,17 +1820,53 @@ __global__ void floor_bucket_kernel(const double* __restrict__ rmean, int64_t M,
 
 // Real-valued slope search: per column (= pool entry, S = 1) the epilogue's
 // {D1, flat, rcp(cnorm) / n^2} (rcp correctly rounded, as fc_real.cu screens).
-__global__ void real_const_kernel(const int32_t* __restrict__ dsum, const double* __restrict__ cnorm,
-                                  int64_t ncols, int n, int4* __restrict__ out) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ncols) return;
-  const double norm = cnorm[c];
-  const bool flat = norm == 0.0;
-  const double rcpn = flat ? 0.0 : __dmul_rn(__drcp_rn(norm), 1.0 / ((double)n * n));  // exact scaling
-  const long long bits = __double_as_longlong(rcpn);
-  // fp32 copy rounded up: the pre-screen's g32 then never falls below fp64 g by more than its margin
-  out[c] = make_int4(dsum[c], __float_as_int(__double2float_ru(rcpn)), (int)(bits & 0xffffffffll),
-                     (int)(bits >> 32));
+// The real-valued search's operands in one launch: B = the decimated domains
+// themselves (column e at slot e, u8, zero beyond n and on padding slots),
+// the epilogue's column constants {D1, rcp / n^2 as fp32 rounded up, rcp / n^2
+// as fp64} and the level tables (one group, no parity split, no clamp reach).
+__global__ void real_prep_kernel(const uint8_t* __restrict__ dtiles, const int32_t* __restrict__ dsum,
+                                 const double* __restrict__ cnorm, int n, int kpad, int64_t ncols,
+                                 int64_t ntiles, int8_t* __restrict__ b_tiles,
+                                 int4* __restrict__ bconst, uint8_t* __restrict__ tab) {
+  const int chunks = kpad / 16;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 512) reinterpret_cast<long long*>(tab + kUpCursorBytes)[i] = 0;
+  if (i < ntiles) {
+    const int64_t left = ncols - i * kTileN;
+    reinterpret_cast<int2*>(tab + kUpCursorBytes + kUpReachBytes + kUpDimsBytes)[i] =
+        make_int2(0, left <= 0 ? 0 : left < kTileN ? (int)left : kTileN);
+  }
+  if (i == 0) {
+    const long long te = (ncols + kTileN - 1) / kTileN;
+    TcDims d{};
+    d.n_even = ncols;
+    d.ntiles = te;
+    d.odd_base = te * kTileN;
+    d.n_pad = te * kTileN - ncols;
+    *reinterpret_cast<TcDims*>(tab + kUpCursorBytes + kUpReachBytes) = d;
+  }
+  // (tile, k chunk, slot): consecutive threads write consecutive 16-byte rows
+  if (i >= ntiles * chunks * kTileN) return;
+  const int cc = (int)(i % kTileN);
+  const int64_t tk = i / kTileN;
+  const int kc = (int)(tk % chunks);
+  const int64_t tile = tk / chunks;
+  const int64_t col = tile * kTileN + cc;
+  uint4 w = make_uint4(0, 0, 0, 0);
+  if (col < ncols && kc * 16 < n) w = __ldg(reinterpret_cast<const uint4*>(dtiles + col * n + kc * 16));
+  *reinterpret_cast<uint4*>(b_tiles + tile * ((int64_t)kTileN * kpad) + (int64_t)kc * (kTileN * 16) + cc * 16) = w;
+  if (kc == 0) {
+    int4 k = make_int4(0, 0, 0, 0);
+    if (col < ncols) {
+      const double norm = cnorm[col];
+      const double rcpn = norm == 0.0 ? 0.0 : __dmul_rn(__drcp_rn(norm), 1.0 / ((double)n * n));  // exact scaling
+      const long long bits = __double_as_longlong(rcpn);
+      // fp32 copy rounded up: the screen's g32 then never falls below fp64 g by more than its margin
+      k = make_int4(dsum[col], __float_as_int(__double2float_ru(rcpn)), (int)(bits & 0xffffffffll),
+                    (int)(bits >> 32));
+    }
+    bconst[col] = k;
+  }
 }
 
 // Winner records {err bits, e * 8 + iso} -> (err, s = cross / cnorm, index),
@@ -1822,7 +1878,9 @@ __global__ void real_finalize_kernel(const unsigned long long* __restrict__ rec,
                                      const int32_t* __restrict__ dsum,
                                      const double* __restrict__ cnorm, double* __restrict__ out_err,
                                      double* __restrict__ out_s, int64_t* __restrict__ out_idx) {
-  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per range: the lanes split the n products, then a shuffle sum
+  const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (m >= M) return;
   const double err = __longlong_as_double((long long)rec[2 * m]);
   const long long idx = (long long)rec[2 * m + 1];
@@ -1831,10 +1889,16 @@ __global__ void real_finalize_kernel(const unsigned long long* __restrict__ rec,
   const uint8_t* r = rtiles + m * n;
   const uint8_t* d = dtiles + e * n;
   long long X = 0, R1 = 0;
-  for (int j = 0; j < n; ++j) {
+  for (int j = lane; j < n; j += 32) {
     X += (long long)d[j] * r[inv[iso * n + j]];
     R1 += r[j];
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    X += __shfl_xor_sync(0xffffffffu, X, o);
+    R1 += __shfl_xor_sync(0xffffffffu, R1, o);
+  }
+  if (lane != 0) return;
   const double norm = cnorm[e];
   const double cross = __dmul_rn((double)((long long)n * X - (long long)dsum[e] * R1), 1.0 / n);
   out_err[m] = err;
@@ -1875,24 +1939,31 @@ int scan_tc(Ctx* c, Level& L, int64_t M, uint64_t* d_keys) {
 
 int real_tc_match(Ctx* c, Level& L, int level, int64_t M, double* d_err, double* d_s,
                   int64_t* d_idx) {
-  // operands: B = the decimated domains themselves (the baseline layout with
-  // the single slope 1: rint(1.0 * d) = d), A = the permuted ranges
-  const double one = 1.0;
-  int pending = 0, needs = 0;
-  FC_TRY(prepare_begin(c, L, level, 1, &one, 1, FC_PATH_TENSOR, &pending, &needs));
-  if (needs) {
-    Level* lv[1] = {&L};
-    const int st[1] = {pending};
-    FC_TRY(prep_launch(c, lv, st, 1));
-  }
-  FC_TRY(prepare_finish(c, L, FC_PATH_TENSOR, pending));
-  TcOperands& T = L.tc;
-  // the epilogue's column constants replace the baseline table: the level is
-  // prepared afresh on its next use
-  real_const_kernel<<<(unsigned)((L.count + 255) / 256), 256, 0, c->stream>>>(
-      L.sum.as<int32_t>(), L.cnorm.as<double>(), L.count, L.n, T.bconst.as<int4>());
-  FC_CUDA(c, cudaGetLastError());
+  // operands: B = the decimated domains themselves, A = the permuted ranges
+  // (build_a's baseline layout: u8 rows, no extra K block).  The level's
+  // encoder operands are replaced: it is prepared afresh on its next use.
+  (void)level;
+  L.baseline = 1;
+  L.s_count = 1;
+  L.svals[0] = 1.0;
   L.prepared = false;
+  TcOperands& T = L.tc;
+  T.planes = 1;
+  T.m_digits = 0;
+  T.kpad = ((L.n + 31) / 32) * 32;
+  T.ncols = L.count;
+  T.ntiles = (L.count + kTileN - 1) / kTileN + 1;
+  FC_CUDA(c, T.b_tiles.reserve(T.ntiles * kTileN * T.kpad));
+  FC_CUDA(c, T.bconst.reserve(T.ntiles * kTileN * 16));
+  FC_CUDA(c, T.tile_q1.reserve(kUpCursorBytes + kUpReachBytes + kUpDimsBytes + T.ntiles * 8 + 16));
+  {
+    const int64_t work = std::max<int64_t>(T.ntiles * kTileN * (T.kpad / 16), 512);
+    real_prep_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
+        L.tiles.as<uint8_t>(), L.sum.as<int32_t>(), L.cnorm.as<double>(), L.n, T.kpad, L.count,
+        T.ntiles, T.b_tiles.as<int8_t>(), T.bconst.as<int4>(), T.tile_q1.as<uint8_t>());
+    FC_CUDA(c, cudaGetLastError());
+  }
+  T.ready = true;
   FC_CUDA(c, c->real_part.reserve(M * 16 + 64));
   auto* rec = c->real_part.as<unsigned long long>();
   FC_CUDA(c, cudaMemsetAsync(rec, 0xff, M * 16, c->stream));
@@ -1905,7 +1976,7 @@ int real_tc_match(Ctx* c, Level& L, int level, int64_t M, double* d_err, double*
   FC_TRY(roff_hist(c, M, c->enc_hist.as<int32_t>()));
   FC_TRY(scan_tc_launch(c, L, M, d_M, c->enc_hist.as<int32_t>(), nullptr, nullptr, d_fix, nullptr,
                         false, nullptr, nullptr, nullptr, rec));
-  real_finalize_kernel<<<(unsigned)((M + 127) / 128), 128, 0, c->stream>>>(
+  real_finalize_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, c->stream>>>(
       rec, M, L.n, c->rtiles.as<uint8_t>(), c->iso_inv.as<uint16_t>() + iso_table_offset(L.side),
       L.tiles.as<uint8_t>(), L.sum.as<int32_t>(), L.cnorm.as<double>(), d_err, d_s, d_idx);
   FC_CUDA(c, cudaGetLastError());
