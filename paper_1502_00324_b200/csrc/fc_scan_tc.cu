@@ -311,8 +311,10 @@ __host__ __device__ inline uint32_t r1_offset(const TcParams& p) {
 __host__ __device__ inline uint32_t const_offset(const TcParams& p) {
   return r1_offset(p) + (p.base ? p.rg * kEpiWarps * 32 * 4 : p.real ? p.rg * kEpiWarps * 32 * 20 : 0);
 }
+// column constants: baseline, per epilogue group, 2 tiles x 256 x int4;
+// real mode, per epilogue warp, 2 tiles x its 128 columns x {D1, sqrt(cnorm)}
 __host__ __device__ inline uint32_t bar_offset(const TcParams& p) {
-  return const_offset(p) + (p.base || p.real ? 2 * 2 * kTileN * 16 : 0);
+  return const_offset(p) + (p.real ? kEpiWarps * 2 * 128 * 8 : p.base ? 2 * 2 * kTileN * 16 : 0);
 }
 __host__ __device__ inline uint32_t smem_bytes(const TcParams& p) {
   const uint32_t raw = bar_offset(p) + (2 * p.stages + 2 * kNumAcc + 2) * 8 + 16;
@@ -627,8 +629,21 @@ __device__ __forceinline__ double real_threshold(double rn, double best) {
   return __dsub_rn(__dsub_rn(rn, best), __dmul_rn(1e-13, __dadd_rn(rn, fabs(best))));
 }
 
+// The screen's row factor: sT <= sqrt(T) (1 - 1e-5), 0 when T is not above
+// 1e-30 (the MUFU reciprocal square root is within 3e-7 of the true value).
+// With f = fl32(cross) and the column factor sqn <= sqrt(cnorm) (fp32,
+// rounded down), |f| < fl(sT * sqn) gives |cross| < sqrt(T cnorm), so the
+// candidate's gain cross^2 / cnorm is below T: it can neither win nor tie.
+__device__ __forceinline__ float real_screen_factor(double rn, double best) {
+  const float t = __double2float_rd(real_threshold(rn, best));
+  return t > 1e-30f ? __fmul_rd(__fmul_rd(t, rsqrtf(t)), 0.99999f) : 0.0f;
+}
+
+constexpr int kRC = 16;  // accumulator columns per register chunk (one tcgen05.ld x16)
+static_assert(kRC == 16, "the exact path's register select is written for 16 columns");
+
 __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, const EpiCtx& x) {
-  const uint32_t kB = x.kB, bar_base = x.bar_base, tmem_base = x.tmem_base;
+  const uint32_t bar_base = x.bar_base, tmem_base = x.tmem_base;
   const int RG = x.RG, KPAD = x.KPAD, warp = x.warp, lane = x.lane;
   const int e = warp - kEpiBase;
   const int gq = e >> 3, hq = (e >> 2) & 1, sp = warp & 3;
@@ -639,15 +654,13 @@ __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, 
   const uint32_t tempty0 = tfull0 + 8u * kNumAcc;
   constexpr int kBS = kEpiWarps * 32;
   const int tix = e * 32 + lane;
-  double2* st_best = reinterpret_cast<double2*>(smem + best_offset(p)) + tix;  // {best, T}
+  double2* st_best = reinterpret_cast<double2*>(smem + best_offset(p)) + tix;  // {best, sT}
   double2* st_row = reinterpret_cast<double2*>(smem + r1_offset(p)) + tix;     // {rnorm, R1}
   int* st_col = reinterpret_cast<int*>(smem + r1_offset(p) + RG * kBS * 16) + tix;
-  const int4* cbase = reinterpret_cast<const int4*>(smem + const_offset(p)) + gq * 2 * kTileN;
-  const int gtid = (e & 7) * 32 + lane;
   const int shift = p.shift, n = 1 << shift;
   const double ninv = 1.0 / (double)n;
+  const uint32_t wbuf = ptx::smem_u32(smem + const_offset(p)) + e * 2048;
   uint32_t tcount = 0;
-  int4 pre = make_int4(0, 0, 0, 0);
   uint32_t H = 0;
   int g, t0, t1;
   for (SegIter it(x.plan); it.next(g, t0, t1);) {
@@ -655,21 +668,33 @@ __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, 
       const int4 rm = p.row_meta[(size_t)(g * RG + r) * kTileM + row];  // {R1, R2, m, 2 R1}
       const double rn = __dmul_rn((double)((long long)n * rm.y - (long long)rm.x * rm.x), ninv);
       st_row[r * kBS] = make_double2(rn, (double)rm.x);
-      st_best[r * kBS] = make_double2(DBL_MAX, -DBL_MAX);
+      st_best[r * kBS] = make_double2(DBL_MAX, 0.0);
       st_col[r * kBS] = INT_MAX;
     }
-    pre = p.bconst[(size_t)(t1 - 1) * kTileN + gtid];
+    // the warp's column constants {D1, sqrt(cnorm)} as fp32 (real_prep_kernel's
+    // layout) staged by cp.async one tile ahead into its own double buffer:
+    // lane l copies 16 bytes (two columns) of each half; no cross-warp sync
+    // (lanes 0-7 also pull the warp's cnorm lines of the tile into L1 for
+    // the exact path)
+    auto stage = [&](int tt, uint32_t buf) {
+      const int2* src = reinterpret_cast<const int2*>(p.bconst) + (size_t)tt * kTileN + slice + 2 * lane;
+      ptx::cp_async16(wbuf + buf * 1024u + lane * 16u, src);
+      ptx::cp_async16(wbuf + buf * 1024u + 512u + lane * 16u, src + kAccN);
+      ptx::cp_async_commit();
+      if (lane < 8)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p.cnorm + (size_t)tt * kTileN + (lane >> 2) * kAccN +
+                                                      slice + (lane & 3) * 16));
+    };
+    stage(t1 - 1, tcount & 1);
     for (int t = t1 - 1; t >= t0; --t) {
       const int valid_slots = p.tile_info[t].y;
-      // per column: {D1, rcp / n^2 as fp32} (the screen reads two columns per
-      // 16-byte load) and the fp64 rcp / n^2 for the exact path
-      int2* cf = reinterpret_cast<int2*>(const_cast<int4*>(cbase) + (tcount & 1) * kTileN);
-      int2* cd = cf + kTileN;
+      const uint32_t buf = tcount & 1;
       ++tcount;
-      cf[gtid] = make_int2(pre.x, pre.y);
-      cd[gtid] = make_int2(pre.z, pre.w);
-      ptx::named_bar_sync(1 + gq, kEpiWarps / 2 * 32);
-      if (t > t0) pre = p.bconst[(size_t)(t - 1) * kTileN + gtid];
+      ptx::cp_async_wait_all();
+      __syncwarp();  // every lane's copies landed; every lane is done with the other buffer
+      if (t > t0) stage(t - 1, buf ^ 1);
+      // cf: this warp's 128 columns (half h at h * 64)
+      const int2* cf = reinterpret_cast<const int2*>(smem + const_offset(p) + e * 2048 + buf * 1024);
       const uint32_t Ht = H;
       H += RG;
 #pragma unroll 1
@@ -677,6 +702,7 @@ __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, 
         const double2 rr = st_row[r * kBS];
         const double rn = rr.x;
         const int nR1 = -(int)rr.y;
+        float mR1n = (float)(-rr.y * ninv);  // -R1 / n, exact
         double2 bt = st_best[r * kBS];
         int bcol = st_col[r * kBS];
         bool changed = false;
@@ -685,19 +711,19 @@ __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, 
         for (int h = 0; h < 2; ++h) {
           ptx::mbar_wait_sleep(tfull0 + 8u * h, ph);
           ptx::tc_fence_after();
-          // the half's 64 columns in two chunks of 32 (the accumulator is
-          // released after the second load); rn == 0 rows take the shortcut
+          // the half's 64 columns in chunks of kRC (the accumulator is
+          // released after the last load); rn == 0 rows take the shortcut
 #pragma unroll 1
-          for (int c = 0; c < 2; ++c) {
-            int v[32];
-            ptx::tmem_ld32(tm0 + h * kAccN + 32 * c, v);
+          for (int c = 0; c < 64 / kRC; ++c) {
+            int v[kRC];
+            ptx::tmem_ld16(tm0 + h * kAccN + kRC * c, v);
             ptx::tmem_wait_ld();
-            if (c == 1) {
+            if (c == 64 / kRC - 1) {
               ptx::tc_fence_before();
               __syncwarp();
               if (lane == 0) ptx::mbar_arrive(tempty0 + 8u * h);
             }
-            const int s0 = h * kAccN + slice + 32 * c;
+            const int s0 = h * kAccN + slice + kRC * c;
             if (rn == 0.0) {
               // a constant range: every candidate's error is max(0 - gain, 0) = 0,
               // so the first candidate of the slice in column order wins
@@ -710,85 +736,92 @@ __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, 
               continue;
             }
             const int nvalid = valid_slots - s0;
-            const uint32_t vmask = nvalid >= 32 ? ~0u : nvalid <= 0 ? 0u : (1u << nvalid) - 1;
-            const float T32 = bt.y > 0.0 ? __fmul_rn(__double2float_rd(bt.y), 0.999999f) : 0.0f;
-            const int4* cf4 = reinterpret_cast<const int4*>(cf + s0);
-            // screen: g32 = fl32(xn)^2 * rcp32 per candidate, xn = n X - D1 R1
-            // (|xn| = n |cross| < 2^31, so wrapping int32 is exact); g32 < T32
-            // implies g < T (the margins cover the fp32 roundings, < 5e-7 relative)
-#define FC_REAL_G32(D1, RCP, X)                                                           \
-  __fmul_rn(__fmul_rn(__int2float_rn((D1) * nR1 + ((X) << shift)),                     \
-                      __int2float_rn((D1) * nR1 + ((X) << shift))),                     \
-            __int_as_float(RCP))
-            // one predicate-OR per candidate; the slices that pass (and the first
-            // slice of a segment) rebuild the candidate mask below
-            bool any = bt.x == DBL_MAX;
+            const uint32_t vmask = nvalid >= kRC ? (1u << kRC) - 1 : nvalid <= 0 ? 0u : (1u << nvalid) - 1;
+            float sT = (float)bt.y;
+            const int l0 = h * 64 + kRC * c;  // the chunk's first column in the warp's constants
+            const int4* cf4 = reinterpret_cast<const int4*>(cf + l0);
+            // screen per candidate: f = fl32(X - D1 R1 / n) = fl32(cross) (one
+            // FFMA: D1, R1 / n and X < 2^24 are exact in fp32), candidate unless
+            // |f| < sT * sqn (see real_screen_factor; flat columns: sqn = inf,
+            // f = 0, so they pass only when sT = 0, through the NaN product)
+#define FC_REAL_F(D1F, X) __fmaf_rn(__int_as_float(D1F), mR1n, __int2float_rn(X))
+#define FC_REAL_PASS(D1F, SQN, X) (!(fabsf(FC_REAL_F(D1F, X)) < __fmul_rn(sT, __int_as_float(SQN))))
+            if (bt.x != DBL_MAX) {
+              // one predicate-OR per candidate; the slices that pass build the
+              // candidate mask below
+              bool any = false;
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const int4 k = cf4[q];
-              any |= FC_REAL_G32(k.x, k.y, v[2 * q]) >= T32;
-              any |= FC_REAL_G32(k.z, k.w, v[2 * q + 1]) >= T32;
+              for (int q = 0; q < kRC / 2; ++q) {
+                const int4 k = cf4[q];
+                any |= FC_REAL_PASS(k.x, k.y, v[2 * q]);
+                any |= FC_REAL_PASS(k.z, k.w, v[2 * q + 1]);
+              }
+              if (!any) continue;
+            } else {
+              // first slice of a segment (no best yet): a = |f| / sqn is within
+              // 3e-7 of sqrt(gain); its maximum over the slice (tracked as a
+              // pair, no division per candidate) sets the row factor, so only
+              // candidates near the slice's best gain pass -- any other has a
+              // gain smaller by more than 1e-4 relative and 1e-12 rnorm, so a
+              // larger fp64 error -- plus every candidate whose gain may reach
+              // rnorm (error clamped to 0: ties by column)
+              float fm = 0.0f, sm = 1.0f;
+#pragma unroll
+              for (int q = 0; q < kRC; ++q) {
+                // (a memory clobber every 4 candidates keeps the constant loads
+                // from being hoisted all at once)
+                if ((q & 3) == 0) asm volatile("" : : : "memory");
+                const int2 k = cf[l0 + q];
+                const float a = fabsf(FC_REAL_F(k.x, v[q])), nq = __int_as_float(k.y);
+                const bool take = ((vmask >> q) & 1u) && __fmul_rn(a, sm) > __fmul_rn(fm, nq);
+                fm = take ? a : fm;
+                sm = take ? nq : sm;
+              }
+              const float amax = __fdividef(fm, sm);
+              const float rn32 = __double2float_rd(rn);
+              sT = fminf(fminf(__fmul_rn(amax, 0.99994f), amax - __fdividef(2e-12f * rn32, amax)),
+                         __fmul_rn(__fmul_rn(rn32, rsqrtf(rn32)), 0.999998f));
             }
-            if (!any) continue;
+            // the mask pass recomputes f from opaque copies of its inputs:
+            // common subexpressions with the pass above would keep 64 values
+            // live across it (spilled)
+            asm volatile("" : "+f"(mR1n), "+f"(sT) : : "memory");
+#pragma unroll
+            for (int j = 0; j < kRC; ++j) asm volatile("" : "+r"(v[j]));
             uint32_t mask = 0u;
-            float gmax = -1.0f;
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
+            for (int q = 0; q < kRC / 2; ++q) {
               const int4 k = cf4[q];
-              const float g0 = FC_REAL_G32(k.x, k.y, v[2 * q]);
-              const float g1 = FC_REAL_G32(k.z, k.w, v[2 * q + 1]);
-              mask |= ((uint32_t)(g0 >= T32) << (2 * q)) | ((uint32_t)(g1 >= T32) << (2 * q + 1));
-              gmax = ((vmask >> (2 * q)) & 1u) ? fmaxf(gmax, g0) : gmax;
-              gmax = ((vmask >> (2 * q + 1)) & 1u) ? fmaxf(gmax, g1) : gmax;
+              mask |= ((uint32_t)FC_REAL_PASS(k.x, k.y, v[2 * q]) << (2 * q)) |
+                      ((uint32_t)FC_REAL_PASS(k.z, k.w, v[2 * q + 1]) << (2 * q + 1));
             }
+#undef FC_REAL_PASS
+#undef FC_REAL_F
             mask &= vmask;
             if (mask == 0u) continue;
-            if (bt.x == DBL_MAX) {
-              // first slice of a segment (no best yet): only the candidates within
-              // 1e-4 of the slice's largest g32 can hold its best gain -- any other
-              // has g < g(max) and so a larger error -- plus every candidate whose
-              // gain may reach rnorm (error clamped to 0: ties by column)
-              const float gcut = fminf(__fmul_rn(gmax, 0.9999f),
-                                       __fmul_rn(__double2float_rd(rn), 0.999999f));
-              mask = 0u;
-#pragma unroll
-              for (int q = 0; q < 16; ++q) {
-                const int4 k = cf4[q];
-                mask |= ((uint32_t)(FC_REAL_G32(k.x, k.y, v[2 * q]) >= gcut) << (2 * q)) |
-                        ((uint32_t)(FC_REAL_G32(k.z, k.w, v[2 * q + 1]) >= gcut) << (2 * q + 1));
-              }
-              mask &= vmask;
-            }
-#undef FC_REAL_G32
             // exact path (rare): X selected from the chunk, then fc_real.cu's steps
             while (mask) {
               const int j = __ffs(mask) - 1;
               mask &= mask - 1;
-              int w[16];
+              int w[kRC / 2];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) w[i] = (j & 1) ? v[2 * i + 1] : v[2 * i];
+              for (int i = 0; i < kRC / 2; ++i) w[i] = (j & 1) ? v[2 * i + 1] : v[2 * i];
 #pragma unroll
-              for (int i = 0; i < 8; ++i) w[i] = (j & 2) ? w[2 * i + 1] : w[2 * i];
+              for (int i = 0; i < kRC / 4; ++i) w[i] = (j & 2) ? w[2 * i + 1] : w[2 * i];
 #pragma unroll
-              for (int i = 0; i < 4; ++i) w[i] = (j & 4) ? w[2 * i + 1] : w[2 * i];
-#pragma unroll
-              for (int i = 0; i < 2; ++i) w[i] = (j & 8) ? w[2 * i + 1] : w[2 * i];
-              const int X = (j & 16) ? w[1] : w[0];
+              for (int i = 0; i < kRC / 8; ++i) w[i] = (j & 4) ? w[2 * i + 1] : w[2 * i];
+              const int X = (j & 8) ? w[1] : w[0];
               const int slot = s0 + j;
               const int col = t * kTileN + slot;  // real mode: slots are columns in order
-              const int2 kf = cf[slot], kd = cd[slot];
-              const double rcpn = __hiloint2double(kd.y, kd.x);
-              const double xd = (double)(kf.x * nR1 + (X << shift));
-              const double gq2 = __dmul_rn(__dmul_rn(xd, xd), rcpn);  // == its fl(cc * rcp)
+              const double norm = p.cnorm[col];  // prefetched into L1 with the tile's constants
+              const double xd = (double)((int)__int_as_float(cf[l0 + j].x) * nR1 + (X << shift));
               const double cross = __dmul_rn(xd, ninv);
               const double cc = __dmul_rn(cross, cross);
-              const bool flat = rcpn == 0.0;
-              if (!flat && __dsub_rn(rn, gq2) > bt.x + 1e-14 * (rn + gq2)) continue;
-              const double gain = flat ? 0.0 : __ddiv_rn(cc, p.cnorm[col]);
+              const double gain = norm == 0.0 ? 0.0 : __ddiv_rn(cc, norm);
               const double err = fmax(__dsub_rn(rn, gain), 0.0);
               if (err < bt.x || (err == bt.x && col < bcol)) {
                 bt.x = err;
-                bt.y = real_threshold(rn, err);
+                bt.y = (double)real_screen_factor(rn, err);
                 bcol = col;
                 changed = true;
               }
@@ -1822,8 +1855,8 @@ __global__ void floor_bucket_kernel(const double* __restrict__ rmean, int64_t M,
 // {D1, flat, rcp(cnorm) / n^2} (rcp correctly rounded, as fc_real.cu screens).
 // The real-valued search's operands in one launch: B = the decimated domains
 // themselves (column e at slot e, u8, zero beyond n and on padding slots),
-// the epilogue's column constants {D1, rcp / n^2 as fp32 rounded up, rcp / n^2
-// as fp64} and the level tables (one group, no parity split, no clamp reach).
+// the epilogue's column constants {D1 as fp32, sqrt(cnorm) as fp32 rounded
+// down} and the level tables (one group, no parity split, no clamp reach).
 __global__ void real_prep_kernel(const uint8_t* __restrict__ dtiles, const int32_t* __restrict__ dsum,
                                  const double* __restrict__ cnorm, int n, int kpad, int64_t ncols,
                                  int64_t ntiles, int8_t* __restrict__ b_tiles,
@@ -1856,16 +1889,14 @@ __global__ void real_prep_kernel(const uint8_t* __restrict__ dtiles, const int32
   if (col < ncols && kc * 16 < n) w = __ldg(reinterpret_cast<const uint4*>(dtiles + col * n + kc * 16));
   *reinterpret_cast<uint4*>(b_tiles + tile * ((int64_t)kTileN * kpad) + (int64_t)kc * (kTileN * 16) + cc * 16) = w;
   if (kc == 0) {
-    int4 k = make_int4(0, 0, 0, 0);
+    int2 k = make_int2(0, 0);
     if (col < ncols) {
       const double norm = cnorm[col];
-      const double rcpn = norm == 0.0 ? 0.0 : __dmul_rn(__drcp_rn(norm), 1.0 / ((double)n * n));  // exact scaling
-      const long long bits = __double_as_longlong(rcpn);
-      // fp32 copy rounded up: the screen's g32 then never falls below fp64 g by more than its margin
-      k = make_int4(dsum[col], __float_as_int(__double2float_ru(rcpn)), (int)(bits & 0xffffffffll),
-                    (int)(bits >> 32));
+      // the screen's column factor: sqrt(cnorm) rounded down (+inf for flat columns)
+      const float sqn = norm == 0.0 ? __int_as_float(0x7f800000) : __double2float_rd(__dsqrt_rd(norm));
+      k = make_int2(__float_as_int((float)dsum[col]), __float_as_int(sqn));
     }
-    bconst[col] = k;
+    reinterpret_cast<int2*>(bconst)[col] = k;
   }
 }
 
@@ -1954,7 +1985,7 @@ int real_tc_match(Ctx* c, Level& L, int level, int64_t M, double* d_err, double*
   T.ncols = L.count;
   T.ntiles = (L.count + kTileN - 1) / kTileN + 1;
   FC_CUDA(c, T.b_tiles.reserve(T.ntiles * kTileN * T.kpad));
-  FC_CUDA(c, T.bconst.reserve(T.ntiles * kTileN * 16));
+  FC_CUDA(c, T.bconst.reserve(T.ntiles * kTileN * 8));
   FC_CUDA(c, T.tile_q1.reserve(kUpCursorBytes + kUpReachBytes + kUpDimsBytes + T.ntiles * 8 + 16));
   {
     const int64_t work = std::max<int64_t>(T.ntiles * kTileN * (T.kpad / 16), 512);
