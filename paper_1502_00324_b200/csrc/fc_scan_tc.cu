@@ -640,6 +640,10 @@ __device__ __forceinline__ float real_screen_factor(double rn, double best) {
 }
 
 constexpr int kRC = 16;  // accumulator columns per register chunk (one tcgen05.ld x16)
+// accumulator release in real mode: named barriers 3..6 (one per accumulator),
+// the 8 warps of its epilogue group arrive, its issuer warp syncs
+constexpr uint32_t kRealReleaseBar = 3;
+constexpr uint32_t kRealReleaseThreads = (kEpiWarps / 2 + 1) * 32;
 static_assert(kRC == 16, "the exact path's register select is written for 16 columns");
 
 __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, const EpiCtx& x) {
@@ -651,7 +655,6 @@ __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, 
   const int slice = hq * 64;
   const uint32_t tm0 = tmem_base + ((uint32_t)(sp * 32) << 16) + (2 * gq) * kAccN + slice;
   const uint32_t tfull0 = bar_base + 8u * (2 * p.stages) + 8u * (2 * gq);
-  const uint32_t tempty0 = tfull0 + 8u * kNumAcc;
   constexpr int kBS = kEpiWarps * 32;
   const int tix = e * 32 + lane;
   double2* st_best = reinterpret_cast<double2*>(smem + best_offset(p)) + tix;  // {best, sT}
@@ -721,7 +724,7 @@ __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, 
             if (c == 64 / kRC - 1) {
               ptx::tc_fence_before();
               __syncwarp();
-              if (lane == 0) ptx::mbar_arrive(tempty0 + 8u * h);
+              ptx::named_bar_arrive(kRealReleaseBar + 2 * gq + h, kRealReleaseThreads);
             }
             const int s0 = h * kAccN + slice + kRC * c;
             if (rn == 0.0) {
@@ -959,7 +962,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     };
     if (i == 0)
       for (int k = 0; k < STAGES - 1; ++k) produce_b();
-    uint32_t L = 0, H = 0, U = 0;
+    uint32_t L = 0, H = 0, U = 0, uses = 0;
     for (SegIter it(plan); it.next(g, t0, t1); ++U) {
       if (i == 0) {
         // the single A slot: refilled once every MMA of the previous segment completed
@@ -982,7 +985,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
         H += RG;
         for (int r = (my_par ^ (int)(Ht & 1)) & 1; r < RG; r += 2) {
           const uint64_t ad0 = ptx::umma_desc(a_base + r * (kTileM * KPAD), kTileM * 16, 128);
-          ptx::mbar_wait_sleep(tempty_i, (((Ht + r) >> 1) & 1) ^ 1);
+          if constexpr (MODE == 2) {
+            // real mode: the epilogue's release is a hardware named barrier, so
+            // the (mostly idle) issuer blocks without taking issue slots
+            if (uses++ > 0) ptx::named_bar_sync(kRealReleaseBar + i, kRealReleaseThreads);
+          } else {
+            ptx::mbar_wait_sleep(tempty_i, (((Ht + r) >> 1) & 1) ^ 1);
+          }
           ptx::tc_fence_after();
           ptx::umma_i8_elect(d, ad0, bd0, kIdesc, 0u);
           for (int ks = 1; ks < ksteps; ++ks)
@@ -994,6 +1003,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
       }
       ptx::umma_commit_elect(aempty_bar);
     }
+    // consume the epilogue's last release of this accumulator
+    if constexpr (MODE == 2)
+      if (uses > 0) ptx::named_bar_sync(kRealReleaseBar + i, kRealReleaseThreads);
   } else if (warp >= kEpiBase) {
     // ---------------- epilogue: two groups of 8 warps, one column half each ----------------
     const EpiCtx x{kB, bar_base, tmem_base, RG, KPAD, warp, lane, plan};
@@ -1860,9 +1872,15 @@ __global__ void floor_bucket_kernel(const double* __restrict__ rmean, int64_t M,
 __global__ void real_prep_kernel(const uint8_t* __restrict__ dtiles, const int32_t* __restrict__ dsum,
                                  const double* __restrict__ cnorm, int n, int kpad, int64_t ncols,
                                  int64_t ntiles, int8_t* __restrict__ b_tiles,
-                                 int4* __restrict__ bconst, uint8_t* __restrict__ tab) {
+                                 int4* __restrict__ bconst, uint8_t* __restrict__ tab,
+                                 unsigned long long* __restrict__ rec, int64_t M,
+                                 int32_t* __restrict__ d_M, int32_t* __restrict__ hist) {
   const int chunks = kpad / 16;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // the launch's range count, the empty winner records, no clamp work
+  if (i < 2 * M) rec[i] = ~0ull;
+  if (i < 256) hist[i] = 0;
+  if (i == 0) *d_M = (int32_t)M;
   if (i < 512) reinterpret_cast<long long*>(tab + kUpCursorBytes)[i] = 0;
   if (i < ntiles) {
     const int64_t left = ncols - i * kTileN;
@@ -1987,24 +2005,21 @@ int real_tc_match(Ctx* c, Level& L, int level, int64_t M, double* d_err, double*
   FC_CUDA(c, T.b_tiles.reserve(T.ntiles * kTileN * T.kpad));
   FC_CUDA(c, T.bconst.reserve(T.ntiles * kTileN * 8));
   FC_CUDA(c, T.tile_q1.reserve(kUpCursorBytes + kUpReachBytes + kUpDimsBytes + T.ntiles * 8 + 16));
-  {
-    const int64_t work = std::max<int64_t>(T.ntiles * kTileN * (T.kpad / 16), 512);
-    real_prep_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
-        L.tiles.as<uint8_t>(), L.sum.as<int32_t>(), L.cnorm.as<double>(), L.n, T.kpad, L.count,
-        T.ntiles, T.b_tiles.as<int8_t>(), T.bconst.as<int4>(), T.tile_q1.as<uint8_t>());
-    FC_CUDA(c, cudaGetLastError());
-  }
-  T.ready = true;
   FC_CUDA(c, c->real_part.reserve(M * 16 + 64));
   auto* rec = c->real_part.as<unsigned long long>();
-  FC_CUDA(c, cudaMemsetAsync(rec, 0xff, M * 16, c->stream));
   FC_CUDA(c, c->enc_hist.reserve(256 * 4 + 64));
   FC_CUDA(c, c->enc_count.reserve(64 * 4));
   int32_t* d_M = c->enc_count.as<int32_t>() + 16;
   auto* d_fix = reinterpret_cast<int64_t*>(c->enc_count.as<int32_t>() + 20);
-  const int32_t m32 = (int32_t)M;
-  FC_TRY(stage_h2d(c, d_M, &m32, 4));
-  FC_TRY(roff_hist(c, M, c->enc_hist.as<int32_t>()));
+  {
+    const int64_t work = std::max<int64_t>(std::max<int64_t>(T.ntiles * kTileN * (T.kpad / 16), 512), 2 * M);
+    real_prep_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
+        L.tiles.as<uint8_t>(), L.sum.as<int32_t>(), L.cnorm.as<double>(), L.n, T.kpad, L.count,
+        T.ntiles, T.b_tiles.as<int8_t>(), T.bconst.as<int4>(), T.tile_q1.as<uint8_t>(), rec, M, d_M,
+        c->enc_hist.as<int32_t>());
+    FC_CUDA(c, cudaGetLastError());
+  }
+  T.ready = true;
   FC_TRY(scan_tc_launch(c, L, M, d_M, c->enc_hist.as<int32_t>(), nullptr, nullptr, d_fix, nullptr,
                         false, nullptr, nullptr, nullptr, rec));
   real_finalize_kernel<<<(unsigned)((M * 32 + 255) / 256), 256, 0, c->stream>>>(
