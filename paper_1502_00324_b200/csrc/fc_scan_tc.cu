@@ -65,6 +65,12 @@ constexpr int kIssuers = 4;      // MMA warps, one per accumulator
 constexpr int kEpiBase = kIssuers;  // first epilogue warp (warps 0-3: MMA issuers, warp 0 also the producer)
 constexpr int kEpiWarps = 16;    // two groups of 8 (one column half each), 4 per TMEM sub-partition
 constexpr int kThreads = (kEpiBase + kEpiWarps) * 32;
+// Accumulator release: named barriers 3..6, one per accumulator; the 8 warps
+// of its epilogue group arrive (bar.arrive, non-blocking), its issuer warp
+// waits (bar.sync: blocked without issuing, where an mbarrier try_wait loop
+// took issue slots from the epilogue warps of its sub-partition).
+constexpr uint32_t kReleaseBar = 3;
+constexpr uint32_t kReleaseThreads = (kEpiWarps / 2 + 1) * 32;
 constexpr int kSmemBudget = 227 * 1024;  // the opt-in maximum per block
 constexpr int kNone = 0x7fffffff;
 
@@ -402,7 +408,6 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, uint8_t* smem, 
   const int slice = hq * 64;        // tile slot of this thread's slice in half 0 (+128: half 1)
   const uint32_t tm0 = tmem_base + ((uint32_t)(sp * 32) << 16) + (2 * gq) * kAccN + slice;
   const uint32_t tfull0 = bar_base + 8u * (2 * p.stages) + 8u * (2 * gq);
-  const uint32_t tempty0 = tfull0 + 8u * kNumAcc;
   // this thread's {best2, loc} per resident row tile, stride = 512 threads;
   // loc = tile << 4 | half << 3 | 8-column group
   const uint32_t bst = ptx::smem_u32(smem + best_offset(p)) + (e * 32 + lane) * 8;
@@ -465,7 +470,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams& p, uint8_t* smem, 
           // every value is in registers: release the accumulator
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(tempty0 + 8u * h);
+          ptx::named_bar_arrive(kReleaseBar + 2 * gq + h, kReleaseThreads);
           const int s0 = h * kAccN + slice;
           if constexpr (BASE) {
             const int X = 2 * R1;
@@ -640,10 +645,7 @@ __device__ __forceinline__ float real_screen_factor(double rn, double best) {
 }
 
 constexpr int kRC = 16;  // accumulator columns per register chunk (one tcgen05.ld x16)
-// accumulator release in real mode: named barriers 3..6 (one per accumulator),
-// the 8 warps of its epilogue group arrive, its issuer warp syncs
-constexpr uint32_t kRealReleaseBar = 3;
-constexpr uint32_t kRealReleaseThreads = (kEpiWarps / 2 + 1) * 32;
+
 static_assert(kRC == 16, "the exact path's register select is written for 16 columns");
 
 __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, const EpiCtx& x) {
@@ -724,7 +726,7 @@ __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, 
             if (c == 64 / kRC - 1) {
               ptx::tc_fence_before();
               __syncwarp();
-              ptx::named_bar_arrive(kRealReleaseBar + 2 * gq + h, kRealReleaseThreads);
+              ptx::named_bar_arrive(kReleaseBar + 2 * gq + h, kReleaseThreads);
             }
             const int s0 = h * kAccN + slice + kRC * c;
             if (rn == 0.0) {
@@ -879,7 +881,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   auto full_bar = [&](int s) { return bar_base + 8u * s; };
   auto empty_bar = [&](int s) { return bar_base + 8u * (STAGES + s); };
   auto tfull_bar = [&](int b) { return bar_base + 8u * (2 * STAGES + b); };
-  auto tempty_bar = [&](int b) { return bar_base + 8u * (2 * STAGES + kNumAcc + b); };
   const uint32_t afull_bar = bar_base + 8u * (2 * STAGES + 2 * kNumAcc);
   const uint32_t aempty_bar = afull_bar + 8u;
 
@@ -897,7 +898,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     }
     for (int b = 0; b < kNumAcc; ++b) {
       ptx::mbar_init(tfull_bar(b), 1);
-      ptx::mbar_init(tempty_bar(b), kEpiWarps / 2);  // the 8 warps of one epilogue group
     }
     ptx::mbar_init(afull_bar, 1);
     ptx::mbar_init(aempty_bar, kIssuers);
@@ -939,7 +939,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     const uint32_t a_base = ptx::smem_u32(sA);
     const uint32_t b_half = (uint32_t)my_h * (kAccN / 8) * 128;
     const uint32_t d = tmem_base + i * kAccN;
-    const uint32_t tfull_i = tfull_bar(i), tempty_i = tempty_bar(i);
+    const uint32_t tfull_i = tfull_bar(i);
     // producer state (warp 0): its own walk over the same tile sequence
     SegIter pit(plan);
     int pg = 0, pt0 = 0, pt = -1;
@@ -985,13 +985,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
         H += RG;
         for (int r = (my_par ^ (int)(Ht & 1)) & 1; r < RG; r += 2) {
           const uint64_t ad0 = ptx::umma_desc(a_base + r * (kTileM * KPAD), kTileM * 16, 128);
-          if constexpr (MODE == 2) {
-            // real mode: the epilogue's release is a hardware named barrier, so
-            // the (mostly idle) issuer blocks without taking issue slots
-            if (uses++ > 0) ptx::named_bar_sync(kRealReleaseBar + i, kRealReleaseThreads);
-          } else {
-            ptx::mbar_wait_sleep(tempty_i, (((Ht + r) >> 1) & 1) ^ 1);
-          }
+          // the epilogue's release is a hardware named barrier: the issuer
+          // blocks without taking issue slots from the epilogue warps
+          if (uses++ > 0) ptx::named_bar_sync(kReleaseBar + i, kReleaseThreads);
           ptx::tc_fence_after();
           ptx::umma_i8_elect(d, ad0, bd0, kIdesc, 0u);
           for (int ks = 1; ks < ksteps; ++ks)
@@ -1004,8 +1000,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
       ptx::umma_commit_elect(aempty_bar);
     }
     // consume the epilogue's last release of this accumulator
-    if constexpr (MODE == 2)
-      if (uses > 0) ptx::named_bar_sync(kRealReleaseBar + i, kRealReleaseThreads);
+    if (uses > 0) ptx::named_bar_sync(kReleaseBar + i, kReleaseThreads);
   } else if (warp >= kEpiBase) {
     // ---------------- epilogue: two groups of 8 warps, one column half each ----------------
     const EpiCtx x{kB, bar_base, tmem_base, RG, KPAD, warp, lane, plan};
