@@ -475,7 +475,10 @@ def decoder_leaves(stream: CompressedStream) -> np.ndarray:
     for level in (1, 2, 3, 4):
         sel = rec[:, 0] == level
         if sel.any():
-            coords = np.asarray(CoordTable(stream.pools[level - 1]).array, dtype=np.int32)
+            p = stream.pools[level - 1]
+            # (a CoordTable passed to np.asarray would be walked as a Python sequence)
+            coords = np.asarray(p.array if isinstance(p, CoordTable) else CoordTable(p).array,
+                                dtype=np.int32)
             out[sel, 3:5] = coords[rec[sel, 3]]
     out[:, 5], out[:, 6], out[:, 7] = rec[:, 2], rec[:, 4], rec[:, 1]
     return out

@@ -94,7 +94,7 @@ class CoordTable:
     __slots__ = ("array", "__weakref__")
 
     def __init__(self, array):
-        a = np.asarray(array)
+        a = np.asarray(array.array if isinstance(array, CoordTable) else array)
         if a.dtype != np.uint16:  # device tables arrive as u16 pairs (the stream format)
             a = a.astype(np.int64)
         a = a.reshape(-1, 2)
@@ -109,6 +109,12 @@ class CoordTable:
 
     def __len__(self):
         return self.array.shape[0]
+
+    def __array__(self, dtype=None, copy=None):
+        # np.asarray(table) takes the backing array (a Python walk of the
+        # sequence protocol would build millions of tuples)
+        a = self.array if dtype is None else self.array.astype(dtype)
+        return a.copy() if copy else a
 
     def __getitem__(self, i):
         if isinstance(i, slice):
