@@ -56,6 +56,29 @@ def test_pool_all_window_entropies_bit_exact(ctx):
                 assert ents.tobytes() == ref[order].tobytes(), (name, stride, level)
 
 
+def test_entropy_constant_windows(ctx):
+    """Constant windows at every level (a 16x16 window's count reaches 256) in
+    patches of every value class mod 4 -- and the windows sliding into and out
+    of them -- keep numpy's entropy bits (oracle LUT sums)."""
+    rng = np.random.default_rng(11)
+    img = rng.integers(0, 256, (96, 96)).astype(np.uint8)
+    for k, v in enumerate((0, 1, 2, 3, 127, 254, 255, 64)):
+        y, x = (k // 4) * 40 + 4, (k % 4) * 22 + 2
+        img[y:y + 20, x:x + 20] = v  # 25 constant 16x16 windows per patch
+    for stride in (1, 2):
+        pool = fc.build_pool(fc.GrayImage(img), fc.PoolParams(pool_cap=10**9, strides=(stride,) * 4),
+                             context=ctx)
+        for level in (1, 2, 3, 4):
+            _, _, ref = O.grid_entropies(img, O.LEVEL_DOMAIN_SIDES[level - 1], stride)
+            ents, _, _, _ = ctx.pool_entries(level, pool.size(level), 2, want=("entropy",))
+            order = np.argsort(-ref, kind="stable")
+            assert ents.tobytes() == ref[order].tobytes(), (stride, level)
+    flat = np.full((64, 64), 7, np.uint8)
+    pool = fc.build_pool(fc.GrayImage(flat), fc.PoolParams(pool_cap=10**9), context=ctx)
+    ents, _, _, _ = ctx.pool_entries(2, pool.size(2), 2, want=("entropy",))
+    assert (ents == 0.0).all()
+
+
 def test_pool_threshold_rank_order_bit_exact(ctx):
     """Threshold pools (device compaction + rank sort) keep {ent > tau} in the
     reference's stable descending order, ties by raster index."""
