@@ -136,15 +136,23 @@ struct SegIter {
   }
 };
 
-// Clamp corrections: a warp handles one range x fix_cols(n) columns per unit
-// (n = 256: one column per lane, the few pairs of B = 16 need parallelism).
-__host__ __device__ constexpr int fix_cpl(int n) { return n >= 256 ? 1 : 4; }
-__host__ __device__ constexpr int fix_cols(int n) { return 32 * fix_cpl(n); }
+// Clamp corrections: a warp handles fix_rpu ranges x fix_cols columns per
+// unit (n = 256: one column per lane, the few pairs of B = 16 need
+// parallelism).  Proposed mode batches the ranges of a unit (they share the
+// job's offset, so a column's clipped pixels are formed once per unit);
+// baseline mode forms the offset per (range, column): one range per unit.
+__host__ __device__ constexpr int fix_cpl(int n, bool batched) {
+  return n >= 256 ? 1 : (batched && n == 64) ? 2 : 4;
+}
+__host__ __device__ constexpr int fix_cols(int n, bool batched) { return 32 * fix_cpl(n, batched); }
+__host__ __device__ constexpr int fix_rpu(int n, bool batched) {
+  return (!batched || n >= 256) ? 1 : n == 64 ? 8 : 16;
+}
 
 // Clamp-correction plan (FixPlan) of one level.
 struct FixPlan {
   int n_jobs;
-  int pad;
+  int rpu;                // ranges per unit (proposed mode batches a job's ranges)
   long long total_units;  // (range, columns-per-unit chunk) units; prefix[] counts them too
   long long fix_pairs;
   unsigned long long next_unit;  // work counter of the corrections fused into tc_scan_kernel
@@ -1271,14 +1279,15 @@ __global__ void reach_scatter_kernel(const int4* __restrict__ stats, int64_t nco
 //    (group, tile) pair count the CTAs split evenly (see TcPlan);
 //  * clamp-correction jobs from the offset histogram: ranges with offset o
 //    against the columns whose qmin < -o (list 0) or qmax > 255 - o (list 1),
-//    units of one range x fix_cols(n) columns (fix_pairs_kernel);
+//    units of fix_rpu ranges x fix_cols columns (fix_pairs_kernel);
 //  * the ranges bucketed by offset (counting sort, bucket order free).
 constexpr int kPlanThreads = 1024;
 __global__ void __launch_bounds__(kPlanThreads)
 level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restrict__ dims,
                   long long b_tile_bytes, long long rr_bytes, int grid,
                   const int32_t* __restrict__ hist, const long long* __restrict__ reach_counts,
-                  int fcols, const int32_t* __restrict__ roff, TcPlan* __restrict__ plan,
+                  int fcols, int max_rpu, long long target_units,
+                  const int32_t* __restrict__ roff, TcPlan* __restrict__ plan,
                   int4* __restrict__ jobs, long long* __restrict__ prefix,
                   FixPlan* __restrict__ fplan, int32_t* __restrict__ order,
                   long long* __restrict__ fix_pairs_out) {
@@ -1314,15 +1323,36 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restr
   }
   // ---- correction jobs: thread o < 256 owns offset bucket o ----
   int cnt = 0, njob = 0;
-  long long lists[2] = {0, 0}, blocks = 0, pairs = 0;
+  long long lists[2] = {0, 0}, blocks = 0, pairs = 0, u1 = 0;
   if (tid < 256) {
     cnt = hist[tid];
     lists[0] = reach_counts[tid];
     lists[1] = reach_counts[256 + tid];
     for (int k = 0; k < 2; ++k)
+      if (cnt && lists[k]) u1 += (long long)cnt * ((lists[k] + fcols - 1) / fcols);
+  }
+  // ranges per unit: up to max_rpu while about target_units remain
+  __shared__ long long u1_w[8];
+  __shared__ int s_rpu;
+  if (tid < 256) {
+    long long v = u1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) u1_w[warp] = v;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    long long t = 0;
+    for (int w2 = 0; w2 < 8; ++w2) t += u1_w[w2];
+    s_rpu = (int)max(1ll, min((long long)max_rpu, t / max(1ll, target_units)));
+  }
+  __syncthreads();
+  const int frpu = s_rpu;
+  if (tid < 256) {
+    for (int k = 0; k < 2; ++k)
       if (cnt && lists[k]) {
         ++njob;
-        blocks += (long long)cnt * ((lists[k] + fcols - 1) / fcols);  // range x fcols columns
+        blocks += (long long)((cnt + frpu - 1) / frpu) * ((lists[k] + fcols - 1) / fcols);  // frpu ranges x fcols columns
         pairs += (long long)cnt * lists[k];
       }
   }
@@ -1366,7 +1396,7 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restr
       if (cnt && lists[k]) {
         jobs[j] = make_int4(k, cursor[tid], cnt, (int)lists[k]);
         prefix[j] = b;
-        b += (long long)cnt * ((lists[k] + fcols - 1) / fcols);
+        b += (long long)((cnt + frpu - 1) / frpu) * ((lists[k] + fcols - 1) / fcols);
         ++j;
       }
     if (tid == 255) {
@@ -1374,6 +1404,7 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restr
       for (int w2 = 0; w2 < 8; ++w2) tp += wt_p[w2];
       FixPlan fp{};
       fp.n_jobs = j;
+      fp.rpu = frpu;
       fp.total_units = b;
       fp.fix_pairs = tp;
       *fplan = fp;
@@ -1403,6 +1434,113 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restr
   for (int i = tid; i < M; i += kPlanThreads) order[atomicAdd(&cursor[roff[i]], 1)] = i;
 }
 
+// Proposed-mode unit: R ranges of one job (one offset o) x 32 * CPL columns
+// (R from the plan: up to fix_rpu while about 16 units per SM remain; the
+// per-unit column set-up dominates below that).
+// Each lane packs clip(q + o) of its CPL columns to bytes once (N / 4 words
+// per column, in registers), then streams the R ranges' isometry rows
+// (warp-uniform broadcast loads) past them: per range and isometry one
+// |x - r|^2 dp4a chain per column, the minimum over (err, isometry) kept per
+// column, then the warp minimum and one atomicMin per range.
+template <int N, int CPL>
+__device__ __forceinline__ void fix_unit_batched(const FixArgs& F, const long long* __restrict__ pre,
+                                                 int n_jobs, long long u, int lane, int R) {
+  constexpr int kCols = 32 * CPL;
+  constexpr int kW = N / 4;  // packed words per column
+  int lo = 0, hi = n_jobs - 1;  // last job with prefix <= u (warp-uniform)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= u) lo = mid; else hi = mid - 1;
+  }
+  const int4 job = F.jobs[lo];  // {list, r_off, r_cnt, col_cnt}
+  const long long local = u - pre[lo];
+  const unsigned ncc = (unsigned)(job.w + kCols - 1) / kCols;
+  const unsigned rg = local < 0x7fffffffll ? (unsigned)local / ncc : (unsigned)(local / ncc);
+  const int c0 = (int)((unsigned)(local - (long long)rg * ncc) * (unsigned)kCols);
+  const int r0 = (int)rg * R, r1 = min(job.z, r0 + R);
+  const int32_t* list = job.x ? F.list_high : F.list_low;
+  int col[CPL];
+  bool valid[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int ci = c0 + c * 32 + lane;
+    valid[c] = ci < job.w;
+    col[c] = valid[c] ? list[ci] : list[c0];  // padding lanes repeat a real column
+  }
+  // the job's ranges share one offset: the first one's
+  const unsigned o = (unsigned)F.roff[F.sorted_ranges[job.y + r0]];
+  const unsigned o2 = o | (o << 16);
+  unsigned x[CPL][kW];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+#pragma unroll
+    for (int kc = 0; kc < N / 16; ++kc) {
+      const int16_t* qc = F.qbase + (int64_t)col[c] * N + kc * 16;
+      const uint4 qa = __ldg(reinterpret_cast<const uint4*>(qc));
+      const uint4 qb = __ldg(reinterpret_cast<const uint4*>(qc + 8));
+      const unsigned qw[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        // clip(q + o, 0, 255) on int16 pairs, then packed to 4 bytes
+        const unsigned lo2 = __vmins2(__vmaxs2(__vadd2(qw[2 * w], o2), 0u), 0x00ff00ffu);
+        const unsigned hi2 = __vmins2(__vmaxs2(__vadd2(qw[2 * w + 1], o2), 0u), 0x00ff00ffu);
+        x[c][kc * 4 + w] = __byte_perm(lo2, hi2, 0x6420);
+      }
+    }
+  }
+  const int S = F.S;
+  unsigned cbase[CPL];  // candidate index of (column, isometry 0): (e * 8) * S + si
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int si = S == 1 ? 0 : (S == 2 ? (col[c] & 1) : col[c] % S);
+    cbase[c] = (unsigned)(8 * (col[c] - si) + si);
+  }
+#pragma unroll 1
+  for (int ri = r0; ri < r1; ++ri) {
+    const int m = F.sorted_ranges[job.y + ri];
+    const int64_t row0 = (int64_t)m * 8;  // the range's 8 isometry rows: one 8-row core block
+    const uint8_t* abase = F.a_tiles + (row0 >> 7) * ((int64_t)kTileM * F.kpad) +
+                           ((int)(row0 & 127) >> 3) * 128;
+    unsigned k[CPL];  // err << 3 | isometry, minimum over the isometries
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) k[c] = ~0u;
+#pragma unroll
+    for (int iso = 0; iso < 8; ++iso) {
+      unsigned acc[CPL];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) acc[c] = 0u;
+#pragma unroll
+      for (int kc = 0; kc < N / 16; ++kc) {
+        const uint4 r4 = __ldg(reinterpret_cast<const uint4*>(abase + kc * (kTileM * 16) + iso * 16));
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          unsigned a = acc[c], d;
+          d = __vabsdiffu4(x[c][kc * 4 + 0], r4.x); a = __dp4a(d, d, a);
+          d = __vabsdiffu4(x[c][kc * 4 + 1], r4.y); a = __dp4a(d, d, a);
+          d = __vabsdiffu4(x[c][kc * 4 + 2], r4.z); a = __dp4a(d, d, a);
+          d = __vabsdiffu4(x[c][kc * 4 + 3], r4.w); a = __dp4a(d, d, a);
+          acc[c] = a;
+        }
+      }
+      // err <= 256 * 255^2 < 2^24: (err << 3 | iso) orders by err, then iso
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) k[c] = min(k[c], (acc[c] << 3) | (unsigned)iso);
+    }
+    unsigned long long best = ~0ull;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const unsigned cidx = cbase[c] + (k[c] & 7) * (unsigned)S;
+      const unsigned long long key = ((unsigned long long)(k[c] >> 3) << 32) | cidx;
+      if (valid[c] && key < best) best = key;
+    }
+    const unsigned err = (unsigned)(best >> 32);  // 0xffffffff: no valid column
+    const unsigned werr = __reduce_min_sync(0xffffffffu, err);
+    const unsigned widx = __reduce_min_sync(0xffffffffu, err == werr ? (unsigned)best : 0xffffffffu);
+    if (lane == 0 && werr != 0xffffffffu)
+      atomicMin(&F.keys[m], ((unsigned long long)werr << 32) | widx);
+  }
+}
+
 constexpr int kFixThreads = 256;
 template <int N>
 __global__ void __launch_bounds__(kFixThreads)
@@ -1416,9 +1554,18 @@ fix_pairs_kernel(FixArgs F, unsigned long long* __restrict__ t_end) {
   if ((long long)blockIdx.x * kWarps >= total) return;
   for (int j = tid; j <= n_jobs; j += kFixThreads) s_prefix[j] = F.prefix[j];
   __syncthreads();
-  for (long long u = (long long)blockIdx.x * kWarps + (tid >> 5); u < total;
-       u += (long long)gridDim.x * kWarps)
-    fix_unit<N, fix_cpl(N)>(F, s_prefix, n_jobs, u, lane);
+  const long long u0 = (long long)blockIdx.x * kWarps + (tid >> 5), du = (long long)gridDim.x * kWarps;
+  if constexpr (N >= 256) {
+    for (long long u = u0; u < total; u += du) fix_unit<N, fix_cpl(N, false)>(F, s_prefix, n_jobs, u, lane);
+  } else {
+    if (F.baseline) {
+      for (long long u = u0; u < total; u += du) fix_unit<N, fix_cpl(N, false)>(F, s_prefix, n_jobs, u, lane);
+    } else {
+      const int R = F.fplan->rpu;
+      for (long long u = u0; u < total; u += du)
+        fix_unit_batched<N, fix_cpl(N, true)>(F, s_prefix, n_jobs, u, lane, R);
+    }
+  }
   if (t_end && tid == 0) atomicMax(t_end, global_ns());
 }
 
@@ -1758,7 +1905,9 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
       reinterpret_cast<const TcDims*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes + kUpReachBytes),
       (long long)kTileN * T.kpad, c->tc_span_units ? 0ll : (48ll << 20), c->sm_count, d_hist,
       reinterpret_cast<const long long*>(T.tile_q1.as<uint8_t>() + kUpCursorBytes),
-      fix_cols(L.n), c->roff.as<int32_t>(), d_plan,
+      fix_cols(L.n, !L.baseline), fix_rpu(L.n, !L.baseline),
+      (long long)c->sm_count * 16,
+      c->roff.as<int32_t>(), d_plan,
       c->fix_jobs.as<int4>(),
       c->fix_cols.as<long long>(), d_fplan, c->fix_rows.as<int32_t>(),
       reinterpret_cast<long long*>(d_fix_pairs)));
