@@ -136,6 +136,7 @@ void run(int ks) {
 int main() {
   for (int ks = 2; ks <= 3; ++ks) {
     run<16, 2, 256, 2, 1>(ks);
+    run<16, 2, 256, 2, 2>(ks);
     run<16, 4, 128, 4, 2>(ks);
     run<16, 4, 128, 4, 4>(ks);
     run<16, 4, 128, 2, 4>(ks);
