@@ -1442,9 +1442,12 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restr
 // (warp-uniform broadcast loads) past them: per range and isometry one
 // |x - r|^2 dp4a chain per column, the minimum over (err, isometry) kept per
 // column, then the warp minimum and one atomicMin per range.
+constexpr int kFixStage = 256;  // uint4 per warp: staged isometry rows of up to 32 ranges (B = 4)
+
 template <int N, int CPL>
 __device__ __forceinline__ void fix_unit_batched(const FixArgs& F, const long long* __restrict__ pre,
-                                                 int n_jobs, long long u, int lane, int R) {
+                                                 int n_jobs, long long u, int lane, int R,
+                                                 uint4* __restrict__ a_s) {
   constexpr int kCols = 32 * CPL;
   constexpr int kW = N / 4;  // packed words per column
   int lo = 0, hi = n_jobs - 1;  // last job with prefix <= u (warp-uniform)
@@ -1495,49 +1498,64 @@ __device__ __forceinline__ void fix_unit_batched(const FixArgs& F, const long lo
     const int si = S == 1 ? 0 : (S == 2 ? (col[c] & 1) : col[c] % S);
     cbase[c] = (unsigned)(8 * (col[c] - si) + si);
   }
+  // the ranges' isometry rows are staged in shared memory in batches (all
+  // loads of a batch in flight at once), then read back as broadcasts
+  constexpr int kChunks = 8 * (N / 16);  // uint4 per range
+  constexpr int kBatch = kFixStage / kChunks;
 #pragma unroll 1
-  for (int ri = r0; ri < r1; ++ri) {
-    const int m = F.sorted_ranges[job.y + ri];
-    const int64_t row0 = (int64_t)m * 8;  // the range's 8 isometry rows: one 8-row core block
-    const uint8_t* abase = F.a_tiles + (row0 >> 7) * ((int64_t)kTileM * F.kpad) +
-                           ((int)(row0 & 127) >> 3) * 128;
-    unsigned k[CPL];  // err << 3 | isometry, minimum over the isometries
+  for (int rb = r0; rb < r1; rb += kBatch) {
+    const int nb = min(kBatch, r1 - rb);
+    __syncwarp();  // the previous batch is consumed
+    for (int i = lane; i < nb * kChunks; i += 32) {
+      const int rr = i / kChunks, ch = i - rr * kChunks;  // ch = kc * 8 + iso
+      const int64_t row0 = (int64_t)F.sorted_ranges[job.y + rb + rr] * 8;
+      const uint8_t* abase = F.a_tiles + (row0 >> 7) * ((int64_t)kTileM * F.kpad) +
+                             ((int)(row0 & 127) >> 3) * 128;
+      a_s[i] = __ldg(reinterpret_cast<const uint4*>(abase + (ch >> 3) * (kTileM * 16) + (ch & 7) * 16));
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int ri = rb; ri < rb + nb; ++ri) {
+      const int m = F.sorted_ranges[job.y + ri];
+      const uint4* as = a_s + (ri - rb) * kChunks;
+      unsigned k[CPL];  // err << 3 | isometry, minimum over the isometries
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) k[c] = ~0u;
+      for (int c = 0; c < CPL; ++c) k[c] = ~0u;
 #pragma unroll
-    for (int iso = 0; iso < 8; ++iso) {
-      unsigned acc[CPL];
+      for (int iso = 0; iso < 8; ++iso) {
+        unsigned acc[CPL];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) acc[c] = 0u;
+        for (int c = 0; c < CPL; ++c) acc[c] = 0u;
 #pragma unroll
-      for (int kc = 0; kc < N / 16; ++kc) {
-        const uint4 r4 = __ldg(reinterpret_cast<const uint4*>(abase + kc * (kTileM * 16) + iso * 16));
+        for (int kc = 0; kc < N / 16; ++kc) {
+          const uint4 r4 = as[kc * 8 + iso];
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          unsigned a = acc[c], d;
-          d = __vabsdiffu4(x[c][kc * 4 + 0], r4.x); a = __dp4a(d, d, a);
-          d = __vabsdiffu4(x[c][kc * 4 + 1], r4.y); a = __dp4a(d, d, a);
-          d = __vabsdiffu4(x[c][kc * 4 + 2], r4.z); a = __dp4a(d, d, a);
-          d = __vabsdiffu4(x[c][kc * 4 + 3], r4.w); a = __dp4a(d, d, a);
-          acc[c] = a;
+          for (int c = 0; c < CPL; ++c) {
+            unsigned a = acc[c], d;
+            d = __vabsdiffu4(x[c][kc * 4 + 0], r4.x); a = __dp4a(d, d, a);
+            d = __vabsdiffu4(x[c][kc * 4 + 1], r4.y); a = __dp4a(d, d, a);
+            d = __vabsdiffu4(x[c][kc * 4 + 2], r4.z); a = __dp4a(d, d, a);
+            d = __vabsdiffu4(x[c][kc * 4 + 3], r4.w); a = __dp4a(d, d, a);
+            acc[c] = a;
+          }
         }
+        // err <= 256 * 255^2 < 2^24: (err << 3 | iso) orders by err, then iso
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) k[c] = min(k[c], (acc[c] << 3) | (unsigned)iso);
       }
-      // err <= 256 * 255^2 < 2^24: (err << 3 | iso) orders by err, then iso
+      unsigned long long best = ~0ull;
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) k[c] = min(k[c], (acc[c] << 3) | (unsigned)iso);
+      for (int c = 0; c < CPL; ++c) {
+        const unsigned cidx = cbase[c] + (k[c] & 7) * (unsigned)S;
+        const unsigned long long key = ((unsigned long long)(k[c] >> 3) << 32) | cidx;
+        if (valid[c] && key < best) best = key;
+      }
+      const unsigned err = (unsigned)(best >> 32);  // 0xffffffff: no valid column
+      const unsigned werr = __reduce_min_sync(0xffffffffu, err);
+      const unsigned widx = __reduce_min_sync(0xffffffffu, err == werr ? (unsigned)best : 0xffffffffu);
+      if (lane == 0 && werr != 0xffffffffu)
+        atomicMin(&F.keys[m], ((unsigned long long)werr << 32) | widx);
     }
-    unsigned long long best = ~0ull;
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      const unsigned cidx = cbase[c] + (k[c] & 7) * (unsigned)S;
-      const unsigned long long key = ((unsigned long long)(k[c] >> 3) << 32) | cidx;
-      if (valid[c] && key < best) best = key;
-    }
-    const unsigned err = (unsigned)(best >> 32);  // 0xffffffff: no valid column
-    const unsigned werr = __reduce_min_sync(0xffffffffu, err);
-    const unsigned widx = __reduce_min_sync(0xffffffffu, err == werr ? (unsigned)best : 0xffffffffu);
-    if (lane == 0 && werr != 0xffffffffu)
-      atomicMin(&F.keys[m], ((unsigned long long)werr << 32) | widx);
   }
 }
 
@@ -1548,6 +1566,7 @@ fix_pairs_kernel(FixArgs F, unsigned long long* __restrict__ t_end) {
   static_assert(N % 16 == 0, "tensor levels have n >= 16");
   constexpr int kWarps = kFixThreads / 32;
   __shared__ long long s_prefix[513];  // at most 2 jobs per offset bucket, + the total
+  __shared__ uint4 a_stage[N < 256 ? kWarps : 1][N < 256 ? kFixStage : 1];
   const int tid = threadIdx.x, lane = tid & 31;
   const int n_jobs = F.fplan->n_jobs;
   const long long total = F.fplan->total_units;
@@ -1563,7 +1582,7 @@ fix_pairs_kernel(FixArgs F, unsigned long long* __restrict__ t_end) {
     } else {
       const int R = F.fplan->rpu;
       for (long long u = u0; u < total; u += du)
-        fix_unit_batched<N, fix_cpl(N, true)>(F, s_prefix, n_jobs, u, lane, R);
+        fix_unit_batched<N, fix_cpl(N, true)>(F, s_prefix, n_jobs, u, lane, R, a_stage[tid >> 5]);
     }
   }
   if (t_end && tid == 0) atomicMax(t_end, global_ns());
