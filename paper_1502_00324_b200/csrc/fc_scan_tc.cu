@@ -189,7 +189,7 @@ struct FixArgs {
 
 template <int N, int CPL>
 __device__ __forceinline__ void fix_unit(const FixArgs& F, const long long* __restrict__ pre,
-                                         int n_jobs, long long u, int lane) {
+                                         int n_jobs, long long u, int lane, uint4* __restrict__ a_s) {
   constexpr int kCols = 32 * CPL;
   int lo = 0, hi = n_jobs - 1;  // last job with prefix <= u (warp-uniform)
   while (lo < hi) {
@@ -228,17 +228,21 @@ __device__ __forceinline__ void fix_unit(const FixArgs& F, const long long* __re
   const int64_t row0 = (int64_t)m * 8;  // the range's 8 isometry rows: one 8-row core block
   const uint8_t* abase = F.a_tiles + (row0 >> 7) * ((int64_t)kTileM * F.kpad) +
                          ((int)(row0 & 127) >> 3) * 128;
+  // the rows are staged in shared memory first (all loads in flight at once)
+  __syncwarp();
+  for (int i = lane; i < 8 * (N / 16); i += 32)
+    a_s[i] = __ldg(reinterpret_cast<const uint4*>(abase + (i >> 3) * (kTileM * 16) + (i & 7) * 16));
+  __syncwarp();
   unsigned acc[CPL][8];
 #pragma unroll
   for (int c = 0; c < CPL; ++c)
 #pragma unroll
     for (int iso = 0; iso < 8; ++iso) acc[c][iso] = 0u;
-#pragma unroll 1
+#pragma unroll 2
   for (int kc = 0; kc < N / 16; ++kc) {
     uint4 r4[8];
-    const uint8_t* ak = abase + kc * (kTileM * 16);
 #pragma unroll
-    for (int iso = 0; iso < 8; ++iso) r4[iso] = __ldg(reinterpret_cast<const uint4*>(ak + iso * 16));
+    for (int iso = 0; iso < 8; ++iso) r4[iso] = a_s[kc * 8 + iso];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       const int16_t* qc = F.qbase + (int64_t)col[c] * N + kc * 16;
@@ -1566,7 +1570,7 @@ fix_pairs_kernel(FixArgs F, unsigned long long* __restrict__ t_end) {
   static_assert(N % 16 == 0, "tensor levels have n >= 16");
   constexpr int kWarps = kFixThreads / 32;
   __shared__ long long s_prefix[513];  // at most 2 jobs per offset bucket, + the total
-  __shared__ uint4 a_stage[N < 256 ? kWarps : 1][N < 256 ? kFixStage : 1];
+  __shared__ uint4 a_stage[kWarps][kFixStage];
   const int tid = threadIdx.x, lane = tid & 31;
   const int n_jobs = F.fplan->n_jobs;
   const long long total = F.fplan->total_units;
@@ -1575,10 +1579,12 @@ fix_pairs_kernel(FixArgs F, unsigned long long* __restrict__ t_end) {
   __syncthreads();
   const long long u0 = (long long)blockIdx.x * kWarps + (tid >> 5), du = (long long)gridDim.x * kWarps;
   if constexpr (N >= 256) {
-    for (long long u = u0; u < total; u += du) fix_unit<N, fix_cpl(N, false)>(F, s_prefix, n_jobs, u, lane);
+    for (long long u = u0; u < total; u += du)
+      fix_unit<N, fix_cpl(N, false)>(F, s_prefix, n_jobs, u, lane, a_stage[tid >> 5]);
   } else {
     if (F.baseline) {
-      for (long long u = u0; u < total; u += du) fix_unit<N, fix_cpl(N, false)>(F, s_prefix, n_jobs, u, lane);
+      for (long long u = u0; u < total; u += du)
+        fix_unit<N, fix_cpl(N, false)>(F, s_prefix, n_jobs, u, lane, a_stage[tid >> 5]);
     } else {
       const int R = F.fplan->rpu;
       for (long long u = u0; u < total; u += du)
