@@ -452,7 +452,11 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
         can_split ? 1 << (2 * (2 - l)) : 0, c->leaf_flag.as<int32_t>(), c->leaf_rec.as<int32_t>(),
         c->enc_orig[nxt_buf].as<int32_t>(), c->enc_code[nxt_buf].as<int32_t>(), d_count + l + 1));
     c->total_launches += 1;
-    if (can_split) {
+    // a split needs err > T^2 B^2, and no error exceeds B^2 * 255^2: with a
+    // threshold at or above that bound no range reaches the next level, whose
+    // launches (sized for the 4x range bound) are skipped altogether
+    const bool next_reachable = can_split && thr2 < (double)side * side * 65025.0;
+    if (next_reachable) {
       cur = nxt_buf;
       bound *= 4;
       FC_TRY(gather(l + 1, cur, bound));
@@ -463,6 +467,7 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     static const char* kLevelMark[4] = {"level1_launched", "level2_launched", "level3_launched",
                                         "level4_launched"};
     trace_mark(c, kLevelMark[l]);
+    if (can_split && !next_reachable) break;
   }
   c->total_launches += c->stats.kernel_launches;
   c->stats.kernel_launches = 0;

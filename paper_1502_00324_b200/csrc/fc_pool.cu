@@ -443,64 +443,64 @@ struct SurvParams {
   int* nsel_reset;  // the survivor counters, zeroed for the next pool build (read already)
 };
 
-__device__ __forceinline__ uint32_t load_word_guarded(const uint8_t* img, int64_t off,
-                                                      int64_t img_bytes) {
-  if (off + 4 <= img_bytes) return __ldg(reinterpret_cast<const uint32_t*>(img + off));
-  uint32_t w = 0;
-  for (int k = 0; k < 4; ++k)
-    if (off + k < img_bytes) w |= (uint32_t)img[off + k] << (8 * k);
-  return w;
+// One window row: the 16-byte aligned blocks that cover bytes [a, a + D) of
+// the image (a block is loaded only when it starts inside the image, so no
+// access leaves the image's pages), then the NW + 1 words starting at the
+// word of byte a; sh = bit offset of byte a inside that first word.
+template <int D>
+__device__ __forceinline__ void load_row_words(const uint8_t* __restrict__ img, int64_t img_bytes,
+                                               int64_t a, uint32_t (&raw)[D / 4 + 1], int& sh) {
+  constexpr int NW = D / 4, NL = (D + 30) / 16;
+  const uintptr_t abs = reinterpret_cast<uintptr_t>(img + a);
+  const uintptr_t base = abs & ~static_cast<uintptr_t>(15);
+  const uintptr_t end = reinterpret_cast<uintptr_t>(img + img_bytes);
+  const int off = (int)(abs - base);
+  uint32_t wv[4 * NL];
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    uint4 b = make_uint4(0, 0, 0, 0);
+    if (base + 16 * k < end) b = __ldg(reinterpret_cast<const uint4*>(base + 16 * k));
+    wv[4 * k] = b.x;
+    wv[4 * k + 1] = b.y;
+    wv[4 * k + 2] = b.z;
+    wv[4 * k + 3] = b.w;
+  }
+  const int q4 = off >> 2;
+#pragma unroll
+  for (int j = 0; j <= NW; ++j) {
+    uint32_t r = wv[j];
+    r = q4 == 1 ? wv[j + 1] : r;
+    r = q4 == 2 ? wv[j + 2] : r;
+    r = q4 == 3 ? wv[j + 3] : r;
+    raw[j] = r;
+  }
+  sh = (off & 3) * 8;
 }
 
-// Words of one window row as staged in shared memory (NW + 1: the row may
-// start mid-word).
-template <int D>
-__host__ __device__ constexpr int stage_words() { return D / 4 + 1; }
-
+// lane = (survivor, window row): D lanes per survivor, PER = 32 / D
+// survivors per warp.  Each lane loads its row (two or three 16-byte loads,
+// from L2: the image is resident), forms the horizontal pair sums, and adds
+// the next lane's row for the floor 2x2 mean (pool.py:138-152 /
+// image.py:116-130); the even rows emit one decimated row each.
 template <int D>
 __device__ __forceinline__ void survivor_rows(const SurvLevel& L, const uint8_t* __restrict__ img,
                                               int width, int64_t img_bytes, int64_t warp_in_level,
-                                              int lane, uint32_t* __restrict__ xy_s,
-                                              uint32_t* __restrict__ stage) {
-  constexpr int B = D / 2, n = B * B, PER = 32 / D, NW = D / 4, NWR = stage_words<D>();
+                                              int lane, uint32_t* __restrict__ xy_s) {
+  constexpr int B = D / 2, n = B * B, PER = 32 / D, NW = D / 4;
   const int grp = lane / D, row = lane % D;
   const int64_t sv = warp_in_level * PER + grp;
   const bool valid = sv < L.count;
   uint32_t w = 0;
+  int wx = 0, wy = 0;
   uint32_t pq[NW > 0 ? NW : 1];
-  // lane = (survivor, window row): the word-aligned start of its row
-  int64_t a0 = 0;
-  int sh = 0;
   if (valid) {
     w = __ldg(L.order + sv);
-    const int wy = w / L.nx, wx = w - wy * L.nx;
+    wy = w / L.nx;
+    wx = w - wy * L.nx;
     const int64_t a = (int64_t)(wy * L.stride + row) * width + wx * L.stride;
-    a0 = a & ~3ll;
-    sh = (int)(a - a0) * 8;
-  }
-  // stage the warp's 32 rows x NWR words with consecutive lanes on consecutive
-  // words of a row (a few cache lines per load instead of one per lane)
-#pragma unroll
-  for (int k = 0; k < NWR; ++k) {
-    const int idx = k * 32 + lane;
-    const int r = idx / NWR, wd = idx - r * NWR;  // staged row r belongs to lane r
-    int64_t ra;
-    int rv;
-    if constexpr (PER == 1) {
-      // one survivor per warp: every lane knows row r's start without a shuffle
-      rv = valid;
-      ra = (a0 + sh / 8 + (int64_t)(r - row) * width) & ~3ll;
-    } else {
-      ra = __shfl_sync(0xffffffffu, a0, r);
-      rv = __shfl_sync(0xffffffffu, valid ? 1 : 0, r);
-    }
-    stage[idx] = rv ? load_word_guarded(img, ra + 4 * wd, img_bytes) : 0u;
-  }
-  __syncwarp();
-  if (valid) {
     uint32_t raw[NW + 1];
-#pragma unroll
-    for (int k = 0; k <= NW; ++k) raw[k] = stage[lane * NWR + k];
+    int sh;
+    load_row_words<D>(img, img_bytes, a, raw, sh);
 #pragma unroll
     for (int k = 0; k < NW; ++k) {
       const uint32_t rw = __funnelshift_r(raw[k], raw[k + 1], sh);
@@ -542,15 +542,17 @@ __device__ __forceinline__ void survivor_rows(const SurvLevel& L, const uint8_t*
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
   }
   if (valid && row == 0) {
-    const int wy = w / L.nx, wx = w - wy * L.nx;
     // staged: the block writes its survivors' origins as one coalesced run
     xy_s[(threadIdx.x >> 5) * PER + grp] = (uint32_t)(wx * L.stride) | ((uint32_t)(wy * L.stride) << 16);
     L.ent[sv] = L.ent_all[w];
     L.sum[sv] = s1;
     L.sumsq[sv] = s2;
-    // mean = s1 / n; cnorm = s2 - s1*s1/n with Python float semantics (pool.py:144-151)
-    L.mean[sv] = __ddiv_rn((double)s1, (double)n);
-    L.cnorm[sv] = __dsub_rn((double)s2, __ddiv_rn((double)((long long)s1 * s1), (double)n));
+    // mean = s1 / n; cnorm = s2 - s1*s1/n with Python float semantics
+    // (pool.py:144-151).  n is a power of two and s1^2 < 2^53, so the
+    // divisions are exact scalings: a multiplication by 1/n gives the same bits.
+    constexpr double inv_n = 1.0 / n;
+    L.mean[sv] = (double)s1 * inv_n;
+    L.cnorm[sv] = __dsub_rn((double)s2, (double)((long long)s1 * s1) * inv_n);
   }
 }
 
@@ -559,7 +561,6 @@ __global__ void __launch_bounds__(256) survivors_all_kernel(const uint8_t* __res
                                                             SurvParams P) {
   if (blockIdx.x == 0 && threadIdx.x < 4 && P.nsel_reset) P.nsel_reset[threadIdx.x] = 0;
   __shared__ uint32_t xy_s[8 * 8];  // 8 warps x up to 8 survivors per warp
-  __shared__ uint32_t stage_s[8][32 * stage_words<32>()];  // per warp: 32 rows of a window
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   // levels start on block boundaries (warp_begin is a multiple of 8)
@@ -581,10 +582,10 @@ __global__ void __launch_bounds__(256) survivors_all_kernel(const uint8_t* __res
   const int64_t level_warps = (L.count + per - 1) / per;
   if (wl < level_warps) {
     switch (L.B) {
-      case 16: survivor_rows<32>(L, img, width, img_bytes, wl, lane, xy_s, stage_s[threadIdx.x >> 5]); break;
-      case 8: survivor_rows<16>(L, img, width, img_bytes, wl, lane, xy_s, stage_s[threadIdx.x >> 5]); break;
-      case 4: survivor_rows<8>(L, img, width, img_bytes, wl, lane, xy_s, stage_s[threadIdx.x >> 5]); break;
-      default: survivor_rows<4>(L, img, width, img_bytes, wl, lane, xy_s, stage_s[threadIdx.x >> 5]); break;
+      case 16: survivor_rows<32>(L, img, width, img_bytes, wl, lane, xy_s); break;
+      case 8: survivor_rows<16>(L, img, width, img_bytes, wl, lane, xy_s); break;
+      case 4: survivor_rows<8>(L, img, width, img_bytes, wl, lane, xy_s); break;
+      default: survivor_rows<4>(L, img, width, img_bytes, wl, lane, xy_s); break;
     }
   }
   __syncthreads();

@@ -617,7 +617,8 @@ int prep_launch(Ctx* c, Level* const* levels, const int* stats, int count) {
     Q.bconst = L.baseline && stats[i] ? T.bconst.as<int4>() : nullptr;
     Q.shift = L.n == 256 ? 8 : L.n == 64 ? 6 : L.n == 16 ? 4 : 2;
     const int lpc = L.n >= 8 ? L.n / 8 : 1;
-    Q.nblocks = (int)std::min<int64_t>((cols * lpc + 255) / 256, c->sm_count * 2);
+    // full occupancy (8 blocks of 256 per SM): the loop is load-latency bound
+    Q.nblocks = (int)std::min<int64_t>((cols * lpc + 255) / 256, c->sm_count * 8);
     Q.block_begin = qblocks;
     qblocks += Q.nblocks;
     if (stats[i]) {

@@ -1095,101 +1095,98 @@ tc_tables_kernel(const unsigned* __restrict__ hist, int64_t ncols, int64_t ntile
 // k in [0, kbase): -q planes;  then m digits of hq (weight 255), 2 remainder
 // slots (weight 1), 2 halves of Q1 (weight o);  zero up to kpad.
 // slot = even/odd group base + rank of the column inside its parity group.
-__global__ void build_b_kernel(const int16_t* __restrict__ qbase, int n, int kpad, int planes,
-                               int m_digits, int baseline, int64_t ncols, const int4* __restrict__ stats,
-                               const int32_t* __restrict__ odd_prefix,
-                               const TcDims* __restrict__ dims, int8_t* __restrict__ b_tiles,
-                               int32_t* __restrict__ colmap) {
-  const int chunks = kpad / 16;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n_even = dims->n_even, n_odd = dims->n_odd;
-  const int64_t odd_base = dims->odd_base, n_pad = dims->n_pad;
-  if (i >= ncols * chunks) {
-    // padding slots of the last tile of each parity group: zero operand, no column
-    const int64_t pi = i - ncols * chunks;
-    if (pi >= n_pad * chunks) return;
-    const int64_t p = pi / chunks;
-    const int kc = (int)(pi - p * chunks);
-    const int64_t pad_even = ((n_even + kTileN - 1) / kTileN) * kTileN - n_even;
-    const int64_t slot = p < pad_even ? n_even + p : odd_base + n_odd + (p - pad_even);
-    const int64_t tile = slot / kTileN;
-    const int cc = (int)(slot - tile * kTileN);
-    int8_t* dst = b_tiles + tile * ((int64_t)kTileN * kpad) + (int64_t)kc * (kTileN * 16) +
-                  (cc >> 3) * 128 + (cc & 7) * 16;
-    *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
-    if (kc == 0) colmap[slot] = -1;
-    return;
+// One thread per column (then per padding slot), looping over the 16-byte K
+// chunks: it reads its column's q as whole lines, and for every chunk a warp
+// writes 32 consecutive slots (512 contiguous bytes within a parity group).
+__device__ __forceinline__ uint32_t extra_word(int k0, int kbase, int m, int Q, int r1, int R,
+                                               int q1a, int Q1) {
+  uint32_t word = 0;
+#pragma unroll
+  for (int bb = 0; bb < 4; ++bb) {
+    const int sl = k0 + bb - kbase;
+    int v = sl < m ? min(max(Q - 127 * sl, 0), 127) : 0;
+    v = sl == m ? r1 : v;
+    v = sl == m + 1 ? R - r1 : v;
+    v = sl == m + 2 ? q1a : v;
+    v = sl == m + 3 ? Q1 - q1a : v;
+    word |= (uint32_t)(v & 0xff) << (8 * bb);
   }
-  const int64_t col = i / chunks;
-  const int kc = (int)(i - col * chunks);
-  const int4 st = stats[col];
-  const int64_t oddp = odd_prefix[col];
-  const int64_t slot = (!baseline && (st.y & 1)) ? odd_base + oddp : col - oddp;
+  return word;
+}
+
+__global__ void __launch_bounds__(256) build_b_kernel(
+    const int16_t* __restrict__ qbase, int n, int kpad, int planes, int m_digits, int baseline,
+    int64_t ncols, const int4* __restrict__ stats, const int32_t* __restrict__ odd_prefix,
+    const TcDims* __restrict__ dims, int8_t* __restrict__ b_tiles, int32_t* __restrict__ colmap) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunks = kpad / 16;
+  int64_t slot;
+  int4 st = make_int4(0, 0, 0, 0);
+  const int16_t* q = nullptr;
+  if (j >= ncols) {
+    // padding slots of the last tile of each parity group: zero operand, no column
+    const int64_t p = j - ncols;
+    const int64_t n_even = dims->n_even;
+    if (p >= dims->n_pad) return;
+    const int64_t pad_even = ((n_even + kTileN - 1) / kTileN) * kTileN - n_even;
+    slot = p < pad_even ? n_even + p : dims->odd_base + dims->n_odd + (p - pad_even);
+  } else {
+    st = __ldg(stats + j);
+    const int64_t oddp = __ldg(odd_prefix + j);
+    slot = (!baseline && (st.y & 1)) ? dims->odd_base + oddp : j - oddp;
+    q = qbase + j * n;
+  }
   const int64_t tile = slot / kTileN;
   const int cc = (int)(slot - tile * kTileN);
+  int8_t* dst = b_tiles + tile * ((int64_t)kTileN * kpad) + (cc >> 3) * 128 + (cc & 7) * 16;
+  colmap[slot] = q ? (int32_t)j : -1;
   const int kbase = planes * n;
   const int hq = st.y >> 1;
   const int Q = hq / 255, R = hq - Q * 255;
   const int r1 = min(R, 127);
   const int q1a = min(max(st.x, -127), 127);
-  const int16_t* q = qbase + col * n;
-  uint32_t w[4];
-  if (baseline) {
-    // u8 q (0..255) for k < n, zero beyond
-    w[0] = w[1] = w[2] = w[3] = 0u;
-    if (kc * 16 < n) {
-      const uint4 qa = __ldg(reinterpret_cast<const uint4*>(q + kc * 16));
-      const uint4 qb = __ldg(reinterpret_cast<const uint4*>(q + kc * 16 + 8));
-      w[0] = __byte_perm(qa.x, qa.y, 0x6420);
-      w[1] = __byte_perm(qa.z, qa.w, 0x6420);
-      w[2] = __byte_perm(qb.x, qb.y, 0x6420);
-      w[3] = __byte_perm(qb.z, qb.w, 0x6420);
-    }
-  } else if (kc * 16 < kbase) {
-    // 16 q values at once (int16 pairs): -q, or its two s8 planes
-    // b = clamp(-q, -127, 127) and -q - b; the low byte of each int16 is the s8
-    const int kk0 = (kc * 16) % n;  // the second plane repeats the pixels
-    const uint4 qa = __ldg(reinterpret_cast<const uint4*>(q + kk0));
-    const uint4 qb = __ldg(reinterpret_cast<const uint4*>(q + kk0 + 8));
-    const uint32_t qw[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-    uint32_t v[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t neg = __vneg2(qw[i]);
-      if (planes == 1) {
-        v[i] = neg;
-      } else {
-        const uint32_t lo = __vmins2(__vmaxs2(neg, 0xff81ff81u), 0x007f007fu);  // clamp to +-127
-        v[i] = kc * 16 < n ? lo : __vsub2(neg, lo);
+  for (int kc = 0; kc < chunks; ++kc) {
+    uint4 out = make_uint4(0, 0, 0, 0);
+    if (q == nullptr) {
+    } else if (baseline) {
+      // u8 q (0..255) for k < n, zero beyond
+      if (kc * 16 < n) {
+        const uint4 qa = __ldg(reinterpret_cast<const uint4*>(q + kc * 16));
+        const uint4 qb = __ldg(reinterpret_cast<const uint4*>(q + kc * 16 + 8));
+        out = make_uint4(__byte_perm(qa.x, qa.y, 0x6420), __byte_perm(qa.z, qa.w, 0x6420),
+                         __byte_perm(qb.x, qb.y, 0x6420), __byte_perm(qb.z, qb.w, 0x6420));
       }
-    }
+    } else if (kc * 16 < kbase) {
+      // 16 q values at once (int16 pairs): -q, or its two s8 planes
+      // b = clamp(-q, -127, 127) and -q - b; the low byte of each int16 is the s8
+      const bool first = kc * 16 < n;
+      const int kk0 = first ? kc * 16 : kc * 16 - n;  // the second plane repeats the pixels
+      const uint4 qa = __ldg(reinterpret_cast<const uint4*>(q + kk0));
+      const uint4 qb = __ldg(reinterpret_cast<const uint4*>(q + kk0 + 8));
+      const uint32_t qw[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+      uint32_t v[8];
 #pragma unroll
-    for (int b4 = 0; b4 < 4; ++b4) w[b4] = __byte_perm(v[2 * b4], v[2 * b4 + 1], 0x6420);
-  } else {
-#pragma unroll
-  for (int b4 = 0; b4 < 4; ++b4) {
-    uint32_t word = 0;
-#pragma unroll
-    for (int bb = 0; bb < 4; ++bb) {
-      const int k = kc * 16 + b4 * 4 + bb;
-      int v = 0;
-      {
-        const int sl = k - kbase;
-        if (sl < m_digits) v = min(max(Q - 127 * sl, 0), 127);
-        else if (sl == m_digits) v = r1;
-        else if (sl == m_digits + 1) v = R - r1;
-        else if (sl == m_digits + 2) v = q1a;
-        else if (sl == m_digits + 3) v = st.x - q1a;
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t neg = __vneg2(qw[i]);
+        if (planes == 1) {
+          v[i] = neg;
+        } else {
+          const uint32_t lo = __vmins2(__vmaxs2(neg, 0xff81ff81u), 0x007f007fu);  // clamp to +-127
+          v[i] = first ? lo : __vsub2(neg, lo);
+        }
       }
-      word |= (uint32_t)(uint8_t)(int8_t)v << (8 * bb);
+      out = make_uint4(__byte_perm(v[0], v[1], 0x6420), __byte_perm(v[2], v[3], 0x6420),
+                       __byte_perm(v[4], v[5], 0x6420), __byte_perm(v[6], v[7], 0x6420));
+    } else if (kc * 16 < kbase + m_digits + 4) {
+      const int k0 = kc * 16;
+      out = make_uint4(extra_word(k0, kbase, m_digits, Q, r1, R, q1a, st.x),
+                       extra_word(k0 + 4, kbase, m_digits, Q, r1, R, q1a, st.x),
+                       extra_word(k0 + 8, kbase, m_digits, Q, r1, R, q1a, st.x),
+                       extra_word(k0 + 12, kbase, m_digits, Q, r1, R, q1a, st.x));
     }
-    w[b4] = word;
+    // a warp's 32 consecutive columns of one parity group: 512 contiguous bytes per chunk
+    *reinterpret_cast<uint4*>(dst + (int64_t)kc * (kTileN * 16)) = out;
   }
-  }
-  int8_t* dst = b_tiles + tile * ((int64_t)kTileN * kpad) + (int64_t)kc * (kTileN * 16) +
-                (cc >> 3) * 128 + (cc & 7) * 16;
-  *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-  if (kc == 0) colmap[slot] = (int32_t)col;
 }
 
 // A operand: row (range, iso) of each 128-row tile = 16 ranges x 8 isometries:
@@ -1251,30 +1248,47 @@ __global__ void build_a_kernel(const uint8_t* __restrict__ rtiles, const double*
   }
 }
 
-// Counting-sort scatter with warp-aggregated cursor updates: lanes holding the
-// same bucket take consecutive slots from one atomic (bucket order is free).
-__device__ __forceinline__ void bucket_scatter(bool valid, int bucket, int32_t* __restrict__ cursors,
-                                               int32_t* __restrict__ out, int32_t value) {
-  const int key = valid ? bucket : -1 - (int)(threadIdx.x & 31);
-  const unsigned peers = __match_any_sync(0xffffffffu, key);
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(peers) - 1;
-  int base = 0;
-  if (valid && lane == leader) base = atomicAdd(&cursors[bucket], __popc(peers));
-  base = __shfl_sync(peers, base, leader);
-  if (valid) out[base + __popc(peers & ((1u << lane) - 1))] = value;
-}
-
 // Clamp-reach lists by counting sort: columns bucketed by qmin (ascending) and
-// by qmax (descending); the order inside a bucket does not matter.
-__global__ void reach_scatter_kernel(const int4* __restrict__ stats, int64_t ncols,
-                                     int32_t* __restrict__ cur_low, int32_t* __restrict__ cur_high,
-                                     int32_t* __restrict__ reach_low, int32_t* __restrict__ reach_high) {
-  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = col < ncols;
-  const int4 st = valid ? stats[col] : make_int4(0, 0, 0, 0);
-  bucket_scatter(valid, st.z + 512, cur_low, reach_low, (int32_t)col);
-  bucket_scatter(valid, st.w + 512, cur_high, reach_high, (int32_t)col);
+// by qmax (descending); the order inside a bucket does not matter.  A block
+// takes kReachCols columns: shared-memory counts per bucket, ONE global cursor
+// update per non-empty bucket and list, then shared-memory slot claims (the
+// per-warp global atomics on a few hot buckets serialised in L2 before).
+constexpr int kReachPer = 8;
+constexpr int kReachCols = 256 * kReachPer;
+__global__ void __launch_bounds__(256) reach_scatter_kernel(
+    const int4* __restrict__ stats, int64_t ncols, int32_t* __restrict__ cur_low,
+    int32_t* __restrict__ cur_high, int32_t* __restrict__ reach_low, int32_t* __restrict__ reach_high) {
+  __shared__ int cnt[2048];  // [0, 1024): qmin + 512, [1024, 2048): qmax + 512
+  for (int i = threadIdx.x; i < 2048; i += 256) cnt[i] = 0;
+  __syncthreads();
+  const int64_t c0 = (int64_t)blockIdx.x * kReachCols + threadIdx.x;
+  int lo[kReachPer], hi[kReachPer];
+#pragma unroll
+  for (int k = 0; k < kReachPer; ++k) {
+    const int64_t col = c0 + k * 256;
+    lo[k] = -1;
+    hi[k] = -1;
+    if (col < ncols) {
+      const int4 st = __ldg(stats + col);
+      lo[k] = st.z + 512;
+      hi[k] = st.w + 512 + 1024;
+      atomicAdd(&cnt[lo[k]], 1);
+      atomicAdd(&cnt[hi[k]], 1);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2048; i += 256) {
+    const int v = cnt[i];
+    if (v) cnt[i] = atomicAdd(i < 1024 ? &cur_low[i] : &cur_high[i - 1024], v);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kReachPer; ++k) {
+    if (lo[k] < 0) continue;
+    const int32_t col = (int32_t)(c0 + k * 256);
+    reach_low[atomicAdd(&cnt[lo[k]], 1)] = col;
+    reach_high[atomicAdd(&cnt[hi[k]], 1)] = col;
+  }
 }
 
 // All per-level launch planning in ONE single-block kernel (the host never
@@ -1833,12 +1847,12 @@ int level_prepare_tc_launch(Ctx* c, Level& L) {
   auto* dims = reinterpret_cast<TcDims*>(tab + kUpCursorBytes + kUpReachBytes);
   tc_tables_kernel<<<1, 1024, 0, c->stream>>>(c->prep_dev.as<unsigned>() + li * kTcHistWords, ncols,
                                               T.ntiles, tab);
-  reach_scatter_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, c->stream>>>(
+  reach_scatter_kernel<<<(unsigned)std::max<int64_t>(1, (ncols + kReachCols - 1) / kReachCols), 256, 0,
+                         c->stream>>>(
       T.col_stats.as<int4>(), ncols, d_cur, d_cur + 1024, T.reach_low.as<int32_t>(),
       T.reach_high.as<int32_t>());
   const int64_t pad_max = T.ntiles * kTileN - ncols;
-  const int64_t work = (ncols + pad_max) * (T.kpad / 16);
-  build_b_kernel<<<(unsigned)((work + 255) / 256), 256, 0, c->stream>>>(
+  build_b_kernel<<<(unsigned)std::max<int64_t>(1, (ncols + pad_max + 255) / 256), 256, 0, c->stream>>>(
       L.qbase.as<int16_t>(), L.n, T.kpad, T.planes, T.m_digits, L.baseline, ncols, T.col_stats.as<int4>(),
       T.odd.as<int32_t>() + ncols, dims, T.b_tiles.as<int8_t>(), T.meta.as<int32_t>());
   FC_CUDA(c, cudaGetLastError());
