@@ -370,57 +370,129 @@ __global__ void rank_scatter_kernel(SortParams P, const int32_t* __restrict__ ra
 }
 
 // Large sets: the chunk-sorted runs (chunk_sort_kernel) merged pairwise,
-// ceil(log2(chunks)) passes.  Each thread writes IPT consecutive outputs of
-// its run pair: a merge-path binary search for its start (how many of the
-// first d outputs come from run a), then a sequential merge.  Keys are
-// unique (key, window) pairs, so the order is total and no stability is
-// needed.
+// ceil(log2(chunks)) passes.  A block writes kMergeTile consecutive outputs
+// of one run pair (runs are >= kChunk = kMergeTile long, so a tile never
+// straddles pairs): two merge-path searches in global memory give its input
+// spans, which are staged in shared memory with coalesced loads; each thread
+// then merges kMergeIpt outputs from shared memory (a second merge-path
+// search there) and the tile leaves as coalesced stores.  Keys are unique
+// (key, window) pairs, so the order is total and no stability is needed.
 constexpr int kMergeIpt = 8;
-__global__ void __launch_bounds__(256)
-merge_pass_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                  uint64_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n,
-                  int64_t width) {
-  const int64_t o0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kMergeIpt;
-  if (o0 >= n) return;
-  const int64_t a0 = o0 / (2 * width) * (2 * width);
-  const int64_t na = min(width, n - a0);
-  const int64_t b0 = a0 + na;
-  const int64_t nb = max((int64_t)0, min(width, n - b0));
-  const int64_t d = o0 - a0;
+constexpr int kMergeTile = 256 * kMergeIpt;
+static_assert(kMergeTile == kChunk, "merge tiles must divide the run width");
+
+__device__ __forceinline__ int64_t merge_path(const uint64_t* __restrict__ ka, const uint32_t* __restrict__ va,
+                                              int64_t na, const uint64_t* __restrict__ kb,
+                                              const uint32_t* __restrict__ vb, int64_t nb, int64_t d) {
   int64_t lo = max((int64_t)0, d - nb), hi = min(d, na);
   while (lo < hi) {  // first x with !(a[x] < b[d - x - 1])
     const int64_t x = (lo + hi) >> 1;
     const int64_t y = d - x - 1;
-    if (lex_less(kin[a0 + x], vin[a0 + x], kin[b0 + y], vin[b0 + y])) lo = x + 1;
+    if (lex_less(ka[x], va[x], kb[y], vb[y])) lo = x + 1;
     else hi = x;
   }
-  int64_t ia = lo, ib = d - lo;
-  const int64_t end = min(o0 + kMergeIpt, a0 + na + nb);
-  uint64_t ka = ia < na ? kin[a0 + ia] : ~0ull, kb = ib < nb ? kin[b0 + ib] : ~0ull;
-  uint32_t va = ia < na ? vin[a0 + ia] : 0xffffffffu, vb = ib < nb ? vin[b0 + ib] : 0xffffffffu;
-  for (int64_t o = o0; o < end; ++o) {
-    const bool take_a = ib >= nb || (ia < na && lex_less(ka, va, kb, vb));
-    if (take_a) {
-      kout[o] = ka;
-      vout[o] = va;
-      ++ia;
-      ka = ia < na ? kin[a0 + ia] : ~0ull;
-      va = ia < na ? vin[a0 + ia] : 0xffffffffu;
-    } else {
-      kout[o] = kb;
-      vout[o] = vb;
-      ++ib;
-      kb = ib < nb ? kin[b0 + ib] : ~0ull;
-      vb = ib < nb ? vin[b0 + ib] : 0xffffffffu;
+  return lo;
+}
+
+// The same split by a warp: 32 probes per round (ballot of the monotone
+// predicate a[x] < b[d - x - 1]), so a run of 2^21 takes 5 dependent rounds
+// of loads instead of 21.
+__device__ __forceinline__ int64_t merge_path_warp(const uint64_t* __restrict__ ka,
+                                                   const uint32_t* __restrict__ va, int64_t na,
+                                                   const uint64_t* __restrict__ kb,
+                                                   const uint32_t* __restrict__ vb, int64_t nb,
+                                                   int64_t d) {
+  const int lane = threadIdx.x & 31;
+  int64_t lo = max((int64_t)0, d - nb), hi = min(d, na);  // answer in [lo, hi]
+  while (lo < hi) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t x = lo + lane * step;
+    bool p = false;
+    if (x < hi) {
+      const int64_t y = d - x - 1;
+      p = lex_less(ka[x], va[x], kb[y], vb[y]);
     }
+    const int c = __popc(__ballot_sync(0xffffffffu, p));  // true lanes form a prefix
+    if (c == 0) {
+      hi = lo;
+    } else {
+      const int64_t last = lo + (int64_t)(c - 1) * step;
+      lo = last + 1;
+      hi = min(hi, last + step);
+    }
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256)
+merge_pass_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                  uint64_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n,
+                  int64_t width) {
+  __shared__ uint64_t sk[kMergeTile];
+  __shared__ uint32_t sv[kMergeTile];
+  __shared__ int64_t split[2];
+  const int64_t o0 = (int64_t)blockIdx.x * kMergeTile;
+  const int64_t a0 = o0 / (2 * width) * (2 * width);
+  const int64_t na = min(width, n - a0);
+  const int64_t b0 = a0 + na;
+  const int64_t nb = max((int64_t)0, min(width, n - b0));
+  const int64_t d0 = o0 - a0;
+  const int64_t d1 = min(d0 + kMergeTile, na + nb);
+  if (threadIdx.x < 64) {  // warp 0: the tile's start split, warp 1: its end
+    const int64_t d = threadIdx.x < 32 ? d0 : d1;
+    const int64_t x = merge_path_warp(kin + a0, vin + a0, na, kin + b0, vin + b0, nb, d);
+    if ((threadIdx.x & 31) == 0) split[threadIdx.x >> 5] = x;
+  }
+  __syncthreads();
+  const int64_t ia0 = split[0], ia1 = split[1];
+  const int64_t ib0 = d0 - ia0, ib1 = d1 - ia1;
+  const int la = (int)(ia1 - ia0), lb = (int)(ib1 - ib0), len = la + lb;
+  // stage: [0, la) = run a's span, [la, len) = run b's span
+  for (int i = threadIdx.x; i < len; i += 256) {
+    const int64_t g = i < la ? a0 + ia0 + i : b0 + ib0 + (i - la);
+    sk[i] = kin[g];
+    sv[i] = vin[g];
+  }
+  __syncthreads();
+  const int t0 = threadIdx.x * kMergeIpt;
+  uint64_t ok[kMergeIpt];
+  uint32_t ov[kMergeIpt];
+  int cnt = 0;
+  if (t0 < len) {
+    int ia = (int)merge_path(sk, sv, la, sk + la, sv + la, lb, t0);
+    int ib = t0 - ia;
+    cnt = min(kMergeIpt, len - t0);
+#pragma unroll
+    for (int k = 0; k < kMergeIpt; ++k) {
+      if (k < cnt) {
+        const bool take_a = ib >= lb || (ia < la && lex_less(sk[ia], sv[ia], sk[la + ib], sv[la + ib]));
+        const int src = take_a ? ia : la + ib;
+        ok[k] = sk[src];
+        ov[k] = sv[src];
+        ia += take_a;
+        ib += !take_a;
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kMergeIpt; ++k)
+    if (k < cnt) {
+      sk[t0 + k] = ok[k];
+      sv[t0 + k] = ov[k];
+    }
+  __syncthreads();
+  for (int i = threadIdx.x; i < len; i += 256) {
+    kout[o0 + i] = sk[i];
+    vout[o0 + i] = sv[i];
   }
 }
 
 // Survivors of all levels in one launch.  A survivor's 2B x 2B window is
-// handled by D = 2B lanes, lane = input row: the row is read as aligned words
-// (funnel-shifted into place), horizontal pixel pairs are summed as packed
-// 16-bit lanes, the partner row arrives by one shuffle, and even lanes emit
-// an output row (floor 2x2 mean, image.py:125-130).  Then per survivor:
+// handled by B lanes, lane = output row: its two input rows are read as
+// aligned 16-byte blocks (funnel-shifted into place), horizontal pixel pairs
+// are summed as packed 16-bit lanes over both rows, and the lane emits one
+// output row (floor 2x2 mean, image.py:125-130).  Then per survivor:
 // coordinates, entropy, exact sum / sum of squares, mean and centred norm
 // (pool.py:138-152).
 struct SurvLevel {
@@ -477,55 +549,47 @@ __device__ __forceinline__ void load_row_words(const uint8_t* __restrict__ img, 
   sh = (off & 3) * 8;
 }
 
-// lane = (survivor, window row): D lanes per survivor, PER = 32 / D
-// survivors per warp.  Each lane loads its row (two or three 16-byte loads,
-// from L2: the image is resident), forms the horizontal pair sums, and adds
-// the next lane's row for the floor 2x2 mean (pool.py:138-152 /
-// image.py:116-130); the even rows emit one decimated row each.
+// lane = (survivor, decimated row): B = D / 2 lanes per survivor, PER = 32 / B
+// survivors per warp.  Each lane loads its two window rows (two or three
+// 16-byte loads each, from L2: the image is resident), forms the horizontal
+// pair sums as packed 16-bit lanes, adds the two rows and emits one row of
+// the floor 2x2 mean (pool.py:138-152 / image.py:116-130).
 template <int D>
 __device__ __forceinline__ void survivor_rows(const SurvLevel& L, const uint8_t* __restrict__ img,
                                               int width, int64_t img_bytes, int64_t warp_in_level,
                                               int lane, uint32_t* __restrict__ xy_s) {
-  constexpr int B = D / 2, n = B * B, PER = 32 / D, NW = D / 4;
-  const int grp = lane / D, row = lane % D;
+  constexpr int B = D / 2, n = B * B, PER = 32 / B, NW = D / 4;
+  const int grp = lane / B, row = lane % B;
   const int64_t sv = warp_in_level * PER + grp;
   const bool valid = sv < L.count;
   uint32_t w = 0;
   int wx = 0, wy = 0;
-  uint32_t pq[NW > 0 ? NW : 1];
+  int s1 = 0, s2 = 0;
+  uint32_t outw[NW > 1 ? NW / 2 : 1];
   if (valid) {
     w = __ldg(L.order + sv);
     wy = w / L.nx;
     wx = w - wy * L.nx;
-    const int64_t a = (int64_t)(wy * L.stride + row) * width + wx * L.stride;
-    uint32_t raw[NW + 1];
+    const int64_t a = (int64_t)(wy * L.stride + 2 * row) * width + wx * L.stride;
+    uint32_t r0[NW + 1], r1[NW + 1];
     int sh;
-    load_row_words<D>(img, img_bytes, a, raw, sh);
+    load_row_words<D>(img, img_bytes, a, r0, sh);
+    load_row_words<D>(img, img_bytes, a + width, r1, sh);
 #pragma unroll
     for (int k = 0; k < NW; ++k) {
-      const uint32_t rw = __funnelshift_r(raw[k], raw[k + 1], sh);
-      pq[k] = (rw & 0x00ff00ffu) + ((rw >> 8) & 0x00ff00ffu);  // [b0+b1 | b2+b3]
+      const uint32_t u = __funnelshift_r(r0[k], r0[k + 1], sh);
+      const uint32_t v = __funnelshift_r(r1[k], r1[k + 1], sh);
+      // [b0+b1 | b2+b3] of both rows, then floor(sum / 4): two output pixels
+      const uint32_t t = (u & 0x00ff00ffu) + ((u >> 8) & 0x00ff00ffu) + (v & 0x00ff00ffu) +
+                         ((v >> 8) & 0x00ff00ffu);
+      const uint32_t q = (t >> 2) & 0x00ff00ffu;
+      const int v0 = (int)(q & 0xffu), v1 = (int)(q >> 16);
+      s1 += v0 + v1;
+      s2 += v0 * v0 + v1 * v1;
+      if (k & 1) outw[k >> 1] = __byte_perm(outw[k >> 1], q, 0x6420);
+      else outw[k >> 1] = q;
     }
-  } else {
-#pragma unroll
-    for (int k = 0; k < NW; ++k) pq[k] = 0;
-  }
-  int s1 = 0, s2 = 0;
-  uint32_t outw[NW > 1 ? NW / 2 : 1];
-#pragma unroll
-  for (int k = 0; k < NW; ++k) {
-    const uint32_t dn = __shfl_down_sync(0xffffffffu, pq[k], 1);
-    const uint32_t q = ((pq[k] + dn) >> 2) & 0x00ff00ffu;  // two output pixels (16-bit lanes)
-    const int v0 = (int)(q & 0xffu), v1 = (int)(q >> 16);
-    s1 += v0 + v1;
-    s2 += v0 * v0 + v1 * v1;
-    if (k & 1) outw[k >> 1] = __byte_perm(outw[k >> 1], q, 0x6420);
-    else outw[k >> 1] = q;
-  }
-  const bool emits = valid && (row & 1) == 0;
-  if (!emits) s1 = s2 = 0;
-  if (emits) {
-    uint8_t* dst = L.tiles + sv * n + (row >> 1) * B;
+    uint8_t* dst = L.tiles + sv * n + row * B;
     if constexpr (B == 16) {
       *reinterpret_cast<uint4*>(dst) = make_uint4(outw[0], outw[1], outw[2], outw[3]);
     } else if constexpr (B == 8) {
@@ -537,7 +601,7 @@ __device__ __forceinline__ void survivor_rows(const SurvLevel& L, const uint8_t*
     }
   }
 #pragma unroll
-  for (int o = D >> 1; o; o >>= 1) {
+  for (int o = B >> 1; o; o >>= 1) {
     s1 += __shfl_xor_sync(0xffffffffu, s1, o);
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
   }
@@ -560,7 +624,7 @@ __global__ void __launch_bounds__(256) survivors_all_kernel(const uint8_t* __res
                                                             int width, int64_t img_bytes,
                                                             SurvParams P) {
   if (blockIdx.x == 0 && threadIdx.x < 4 && P.nsel_reset) P.nsel_reset[threadIdx.x] = 0;
-  __shared__ uint32_t xy_s[8 * 8];  // 8 warps x up to 8 survivors per warp
+  __shared__ uint32_t xy_s[8 * 16];  // 8 warps x up to 16 survivors per warp
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   // levels start on block boundaries (warp_begin is a multiple of 8)
@@ -578,7 +642,7 @@ __global__ void __launch_bounds__(256) survivors_all_kernel(const uint8_t* __res
     default: L = P.lv[3]; break;
   }
   const int64_t wl = gw - L.warp_begin;
-  const int per = 32 / (2 * L.B);
+  const int per = 32 / L.B;
   const int64_t level_warps = (L.count + per - 1) / per;
   if (wl < level_warps) {
     switch (L.B) {
@@ -956,7 +1020,7 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
         uint32_t* vb[2] = {L.win_val.as<uint32_t>(), L.win_val2.as<uint32_t>()};
         int cur = 0;
         const int64_t n = S.count;
-        const unsigned grid = (unsigned)((n + 256 * kMergeIpt - 1) / (256 * kMergeIpt));
+        const unsigned grid = (unsigned)((n + kMergeTile - 1) / kMergeTile);
         for (int64_t width = kChunk; width < n; width *= 2, cur ^= 1) {
           merge_pass_kernel<<<grid, 256, 0, c->stream>>>(kb[cur], vb[cur], kb[cur ^ 1], vb[cur ^ 1],
                                                          n, width);
@@ -1000,7 +1064,7 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     V.sumsq = L.sumsq.as<int64_t>();
     V.mean = L.mean.as<double>();
     V.cnorm = L.cnorm.as<double>();
-    const int per = 32 / (2 * L.side);  // survivors per warp
+    const int per = 32 / L.side;  // survivors per warp (one lane per decimated row)
     swarps += ((E + per - 1) / per + 7) / 8 * 8;  // levels start on block boundaries
     out_sizes[li] = E;
   }
