@@ -79,8 +79,7 @@ int fc_set_device_io(fc_ctx* ctx, int device_io);
  * Variants with identical results, kept for tests and timing:
  * "tc_span_units" (1: the contraction's round-robin span schedule, otherwise
  * only used when the B operand exceeds L2), "real_cuda_cores" (1: the
- * real-valued slope search on the dp4a kernel instead of the tensor cores),
- * "pdl" (programmatic dependent launch between the level loop's kernels). */
+ * real-valued slope search on the dp4a kernel instead of the tensor cores). */
 int fc_set_option(fc_ctx* ctx, const char* name, int64_t value);
 
 /* terms[k-1] = (k/n) * log(k/n), k = 1..n, produced by the host's numpy so the

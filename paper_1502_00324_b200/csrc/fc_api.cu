@@ -235,7 +235,6 @@ int fc_ctx_create(int device, fc_ctx** out) {
   if (const char* t = getenv("FC_TRACE")) c->trace = atoi(t);
   if (const char* g = getenv("FC_GRAPH")) c->use_graph = atoi(g) != 0;
   if (const char* o = getenv("FC_OVERLAP")) c->overlap = atoi(o) != 0;
-  if (const char* o = getenv("FC_PDL")) c->pdl = atoi(o) != 0;
   if (const char* d = getenv("FC_POOL_CHUNK")) c->pool_chunk = atoi(d);
   if (const char* d = getenv("FC_TC_RG")) c->tc_rg = atoi(d);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -342,10 +341,6 @@ int fc_set_option(fc_ctx* c, const char* name, int64_t value) {
   }
   if (strcmp(name, "real_cuda_cores") == 0) {  // s-histogram search on the dp4a kernel
     c->real_cuda_cores = (int)value;
-    return FC_OK;
-  }
-  if (strcmp(name, "pdl") == 0) {
-    c->pdl = value != 0;
     return FC_OK;
   }
   return set_error(c, FC_ERR_ARG, std::string("unknown option ") + name);

@@ -68,7 +68,6 @@ __global__ void classify_kernel(const unsigned long long* __restrict__ keys,
                                 int32_t* __restrict__ leaf_flag, int32_t* __restrict__ leaf_rec,
                                 int32_t* __restrict__ next_origins,
                                 int32_t* __restrict__ next_codes, int32_t* __restrict__ d_next_M) {
-  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool in = i < bound && i < *d_M;
   int sp = 0;
@@ -126,7 +125,6 @@ __global__ void __launch_bounds__(256) record_block_sums_kernel(int64_t n_codes,
                                                                 int32_t* __restrict__ bsum) {
   using Red = cub::BlockReduce<int, 256>;
   __shared__ typename Red::TempStorage tmp;
-  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int s = Red(tmp).Sum(i < n_codes ? flag[i] : 0);
   if (threadIdx.x == 0) bsum[blockIdx.x] = s;
@@ -137,7 +135,6 @@ __global__ void __launch_bounds__(1024) record_block_offsets_kernel(int32_t* __r
                                                                     int nb) {
   using Scan = cub::BlockScan<int, 1024>;
   __shared__ typename Scan::TempStorage tmp;
-  pdl_enter();
   const int per = (nb + 1023) / 1024;
   const int b0 = threadIdx.x * per;
   int part = 0;
@@ -160,7 +157,6 @@ __global__ void __launch_bounds__(256) compact_records_kernel(int64_t n_codes,
   using Scan = cub::BlockScan<int, 256>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int32_t rs[256 * 6];
-  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int f = i < n_codes ? flag[i] : 0;
   int local, cnt;
@@ -328,7 +324,6 @@ int encode_device(Ctx* c, const double thresholds[3], int baseline, const double
     put(c->overlap);
     put(top_first);
     put(top_last);
-    put(c->pdl);
     for (int l = 0; l < 3; ++l) putd(thresholds[l]);
     for (int l = 0; l < kLevels; ++l) {
       const Level& L = c->lv[l];

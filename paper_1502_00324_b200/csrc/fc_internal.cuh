@@ -188,7 +188,6 @@ struct Ctx {
   int64_t top_begin = 0, top_end = -1;       // fc_encode's top-level slab (-1: to the end)
   bool nsel_clean = false;                   // pool survivor counters already zero
   DevBuf dec_img, dec_leaves, dec_state, dec_svals;  // device decoder (fc_decode.cu)
-  bool pdl = false;                    // FC_PDL=1: programmatic dependent launches (measured no gain)
   int pool_chunk = 0;                  // FC_POOL_CHUNK=1024 / 2048: force the rank-sort chunk
   int tc_span_units = 0;               // 1: the contraction's round-robin span schedule at any B size (tests)
   int real_cuda_cores = 0;             // 1: real-valued slope search on the dp4a kernel (tests, timing)
@@ -225,21 +224,7 @@ __device__ __forceinline__ int baseline_offset(double rmean, double s, double dm
   return o < 0 ? 0 : (o > 255 ? 255 : o);
 }
 
-// Programmatic dependent launch (PDL).  Kernels launched with launch_k() may
-// start while their stream predecessor is still running: they call
-// pdl_trigger() (let their own successor launch) and pdl_wait() (block until
-// the predecessor completed and its memory is visible) before touching any
-// data the predecessor produces.  Both are no-ops without a programmatic edge.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-__device__ __forceinline__ void pdl_enter() {
-  pdl_trigger();
-  pdl_wait();
-}
-
-// Kernel launch on the context stream, with the PDL attribute when enabled.
+// Kernel launch on the context stream.
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(const Ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block,
                             size_t smem, Args... args) {
@@ -248,11 +233,8 @@ inline cudaError_t launch_k(const Ctx* c, void (*kern)(KArgs...), dim3 grid, dim
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = c->stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.attrs = nullptr;
+  cfg.numAttrs = 0;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 #endif

@@ -169,7 +169,6 @@ scan_exact_kernel(const int16_t* __restrict__ qbase, int64_t ncols, int S,
                   const int32_t* __restrict__ col_list, int64_t n_col_list, int baseline,
                   unsigned long long* __restrict__ keys, unsigned long long* __restrict__ tspan) {
   __shared__ __align__(16) ExactSmem<N> s;
-  pdl_enter();
   constexpr int RB = ExactSmem<N>::RB;
   const int tid = threadIdx.x;
   if (d_M) M = *d_M;

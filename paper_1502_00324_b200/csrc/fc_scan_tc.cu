@@ -901,7 +901,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   // R2UR.BROADCAST / divergence checks -- the issue loop halves)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
-  pdl_trigger();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -920,8 +919,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // setup above overlaps the predecessor's tail; its outputs are read below
-  pdl_wait();
   if (p.tspan && threadIdx.x == 0) atomicMin(&p.tspan[0], global_ns());
 
   const TcPlan plan = *p.plan;
@@ -1250,25 +1247,24 @@ __global__ void build_a_kernel(const uint8_t* __restrict__ rtiles, const double*
 
 // Clamp-reach lists by counting sort: columns bucketed by qmin (ascending) and
 // by qmax (descending); the order inside a bucket does not matter.  A block
-// takes kReachCols columns: shared-memory counts per bucket, ONE global cursor
+// takes 256 * per columns: shared-memory counts per bucket, ONE global cursor
 // update per non-empty bucket and list, then shared-memory slot claims (the
 // per-warp global atomics on a few hot buckets serialised in L2 before).
-constexpr int kReachPer = 8;
-constexpr int kReachCols = 256 * kReachPer;
+constexpr int kReachPerMax = 8;
 __global__ void __launch_bounds__(256) reach_scatter_kernel(
-    const int4* __restrict__ stats, int64_t ncols, int32_t* __restrict__ cur_low,
+    const int4* __restrict__ stats, int64_t ncols, int per, int32_t* __restrict__ cur_low,
     int32_t* __restrict__ cur_high, int32_t* __restrict__ reach_low, int32_t* __restrict__ reach_high) {
   __shared__ int cnt[2048];  // [0, 1024): qmin + 512, [1024, 2048): qmax + 512
   for (int i = threadIdx.x; i < 2048; i += 256) cnt[i] = 0;
   __syncthreads();
-  const int64_t c0 = (int64_t)blockIdx.x * kReachCols + threadIdx.x;
-  int lo[kReachPer], hi[kReachPer];
+  const int64_t c0 = (int64_t)blockIdx.x * (256 * per) + threadIdx.x;
+  int lo[kReachPerMax], hi[kReachPerMax];
 #pragma unroll
-  for (int k = 0; k < kReachPer; ++k) {
+  for (int k = 0; k < kReachPerMax; ++k) {
     const int64_t col = c0 + k * 256;
     lo[k] = -1;
     hi[k] = -1;
-    if (col < ncols) {
+    if (k < per && col < ncols) {
       const int4 st = __ldg(stats + col);
       lo[k] = st.z + 512;
       hi[k] = st.w + 512 + 1024;
@@ -1283,7 +1279,7 @@ __global__ void __launch_bounds__(256) reach_scatter_kernel(
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kReachPer; ++k) {
+  for (int k = 0; k < kReachPerMax; ++k) {
     if (lo[k] < 0) continue;
     const int32_t col = (int32_t)(c0 + k * 256);
     reach_low[atomicAdd(&cnt[lo[k]], 1)] = col;
@@ -1311,7 +1307,6 @@ level_plan_kernel(const int32_t* __restrict__ d_M, int RG, const TcDims* __restr
                   long long* __restrict__ fix_pairs_out) {
   __shared__ int cursor[256];
   __shared__ unsigned long long best[kPlanThreads / 32];
-  pdl_enter();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = *d_M;
   // ---- unit decomposition ----
@@ -1640,7 +1635,6 @@ __global__ void __launch_bounds__(256) gather_build_kernel(GatherBuild P) {
   // one of them, possibly read backwards (see the table below)
   __shared__ __align__(16) uint8_t tile_s[8][256];
   __shared__ __align__(16) uint8_t tile_t[8][256];
-  pdl_enter();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1847,9 +1841,12 @@ int level_prepare_tc_launch(Ctx* c, Level& L) {
   auto* dims = reinterpret_cast<TcDims*>(tab + kUpCursorBytes + kUpReachBytes);
   tc_tables_kernel<<<1, 1024, 0, c->stream>>>(c->prep_dev.as<unsigned>() + li * kTcHistWords, ncols,
                                               T.ntiles, tab);
-  reach_scatter_kernel<<<(unsigned)std::max<int64_t>(1, (ncols + kReachCols - 1) / kReachCols), 256, 0,
-                         c->stream>>>(
-      T.col_stats.as<int4>(), ncols, d_cur, d_cur + 1024, T.reach_low.as<int32_t>(),
+  // columns per thread: up to kReachPerMax, but at least two blocks per SM
+  const int reach_per = (int)std::min<int64_t>(
+      kReachPerMax, std::max<int64_t>(1, ncols / ((int64_t)256 * 2 * c->sm_count)));
+  reach_scatter_kernel<<<(unsigned)std::max<int64_t>(1, (ncols + 256 * reach_per - 1) / (256 * reach_per)),
+                         256, 0, c->stream>>>(
+      T.col_stats.as<int4>(), ncols, reach_per, d_cur, d_cur + 1024, T.reach_low.as<int32_t>(),
       T.reach_high.as<int32_t>());
   const int64_t pad_max = T.ntiles * kTileN - ncols;
   build_b_kernel<<<(unsigned)std::max<int64_t>(1, (ncols + pad_max + 255) / 256), 256, 0, c->stream>>>(

@@ -418,7 +418,7 @@ def test_full_size_encode_properties(name):
         del q
 
 
-@pytest.mark.parametrize("option,value", [("tc_span_units", 1), ("pdl", 1), ("overlap", 0),
+@pytest.mark.parametrize("option,value", [("tc_span_units", 1), ("overlap", 0),
                                           ("graph", 0)])
 def test_kernel_variants_give_identical_streams(option, value):
     """Every execution variant produces the same c2 stream (tc_span_units: the
