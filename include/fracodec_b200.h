@@ -96,6 +96,27 @@ int fc_set_image(fc_ctx* ctx, const uint8_t* pixels, int width, int height);
  * the pool length per level. */
 int fc_pool_build(fc_ctx* ctx, const int32_t strides[4], const int64_t caps[4],
                   const double taus[4], const int32_t use_tau[4], int64_t out_sizes[4]);
+/* fc_pool_build in two phases, for a pool built by several ranks
+ * (the entropy pass sharded, then a replicated ranking).
+ * fc_pool_entropy: the windows' entropies of window rows [row_lo[l],
+ * row_hi[l]) per level (row_lo / row_hi NULL: all rows).  Without a
+ * threshold a level's entropy, key (~bits(|H|)) and window index are written
+ * at the window's raster index; with one, the entropy at the window index and
+ * the survivors' (key, index) appended (count: fc_pool_window_buffers).
+ * fc_pool_window_buffers: device pointers of a level's window buffers
+ * (u64 key, u32 index, f64 entropy; capacity nx * ny each), its window grid
+ * and, when local_sel is non-NULL, the survivors appended so far (one
+ * synchronisation).  The caller completes the buffers (all-gather) on the
+ * context's stream or before the next call.
+ * fc_pool_rank: ranking, truncation and the survivors' tiles and moments;
+ * sel_counts (NULL: the device counters) are the threshold levels' survivor
+ * counts in the completed buffers. */
+int fc_pool_entropy(fc_ctx* ctx, const int32_t strides[4], const int64_t caps[4],
+                    const double taus[4], const int32_t use_tau[4], const int32_t row_lo[4],
+                    const int32_t row_hi[4]);
+int fc_pool_window_buffers(fc_ctx* ctx, int level, void** key, void** val, void** ent,
+                           int64_t* nx, int64_t* ny, int64_t* local_sel);
+int fc_pool_rank(fc_ctx* ctx, const int64_t sel_counts[4], int64_t out_sizes[4]);
 /* Replace one level's pool by explicit decimated tiles (E x B x B uint8). */
 int fc_pool_set_level(fc_ctx* ctx, int level, int64_t count, const uint8_t* tiles);
 int fc_pool_size(fc_ctx* ctx, int level, int64_t* out_count);

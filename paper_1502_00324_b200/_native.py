@@ -67,6 +67,11 @@ _SIGNATURES = {
     "fc_set_entropy_lut": ([_P, ctypes.c_int, _P], ctypes.c_int),
     "fc_set_image": ([_P, _P, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "fc_pool_build": ([_P, _P, _P, _P, _P, _P], ctypes.c_int),
+    "fc_pool_entropy": ([_P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
+    "fc_pool_window_buffers": ([_P, ctypes.c_int, ctypes.POINTER(_P), ctypes.POINTER(_P),
+                                ctypes.POINTER(_P), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
+                                ctypes.POINTER(_I64)], ctypes.c_int),
+    "fc_pool_rank": ([_P, _P, _P], ctypes.c_int),
     "fc_pool_set_level": ([_P, ctypes.c_int, _I64, _P], ctypes.c_int),
     "fc_pool_size": ([_P, ctypes.c_int, _P], ctypes.c_int),
     "fc_pool_coords": ([_P, ctypes.c_int, _P], ctypes.c_int),
@@ -210,6 +215,37 @@ class Context:
         self._detach_views()  # the build rewrites (and may reallocate) the pinned coordinates
         self.pool_generation += 1
         self.check(self.lib.fc_pool_build(self.handle, _ptr(s), _ptr(c), _ptr(t), _ptr(u), _ptr(out)))
+        return tuple(int(v) for v in out)
+
+    def pool_entropy(self, strides, caps, taus, use_tau, row_lo=None, row_hi=None):
+        """Phase 1 of pool_build over window rows [row_lo[l], row_hi[l]) per level."""
+        s = np.ascontiguousarray(strides, dtype=np.int32)
+        c = np.ascontiguousarray(caps, dtype=np.int64)
+        t = np.ascontiguousarray(taus, dtype=np.float64)
+        u = np.ascontiguousarray(use_tau, dtype=np.int32)
+        lo = None if row_lo is None else np.ascontiguousarray(row_lo, dtype=np.int32)
+        hi = None if row_hi is None else np.ascontiguousarray(row_hi, dtype=np.int32)
+        self._detach_views()
+        self.pool_generation += 1
+        self.check(self.lib.fc_pool_entropy(self.handle, _ptr(s), _ptr(c), _ptr(t), _ptr(u),
+                                            None if lo is None else _ptr(lo),
+                                            None if hi is None else _ptr(hi)))
+
+    def pool_window_buffers(self, level: int, local_sel: bool = False) -> dict:
+        """Device pointers and grid of a level's window buffers after pool_entropy."""
+        key, val, ent = _P(), _P(), _P()
+        nx, ny, sel = _I64(), _I64(), _I64()
+        self.check(self.lib.fc_pool_window_buffers(
+            self.handle, level, ctypes.byref(key), ctypes.byref(val), ctypes.byref(ent),
+            ctypes.byref(nx), ctypes.byref(ny), ctypes.byref(sel) if local_sel else None))
+        return {"key": key.value, "val": val.value, "ent": ent.value, "nx": nx.value, "ny": ny.value,
+                "sel": sel.value if local_sel else None}
+
+    def pool_rank(self, sel_counts=None):
+        """Phase 2 of pool_build -> per-level pool sizes."""
+        out = np.zeros(4, dtype=np.int64)
+        sc = None if sel_counts is None else np.ascontiguousarray(sel_counts, dtype=np.int64)
+        self.check(self.lib.fc_pool_rank(self.handle, None if sc is None else _ptr(sc), _ptr(out)))
         return tuple(int(v) for v in out)
 
     def pool_set_level(self, level: int, tiles: np.ndarray):

@@ -21,7 +21,7 @@ import numpy as np
 from . import _native
 from .image import GrayImage
 from .matcher import BASELINE, PATHS, PROPOSED, SPolicy, split_index, stored_offsets
-from .pool import LEVEL_RANGE_SIDES, CoordTable, PoolParams, build_pool
+from .pool import LEVEL_RANGE_SIDES, CoordTable, PoolParams, build_pool, build_pool_sharded
 from .stream import CompressedStream, RecordTable, header_bytes, leaf_origins
 
 TOP_SIDE = 16
@@ -180,7 +180,7 @@ def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=N
 
 
 def encode_shard(image: GrayImage, config: EncoderConfig, rank: int, world: int, context=None,
-                 device_image=None):
+                 device_image=None, pool=None):
     """Range sharding: this rank's contiguous raster slab of
     16x16 top-level slots (sharding.slab_for_rank), encoded against the full,
     replicated pool -> (int32 records [n, 6] of the slab in depth-first
@@ -192,7 +192,8 @@ def encode_shard(image: GrayImage, config: EncoderConfig, rank: int, world: int,
     if image.width % 16 or image.height % 16:
         raise ValueError(f"dimensions not multiple of 16: {image.width}x{image.height}")
     ctx = context if context is not None else _native.default_context()
-    pool = build_pool(image, config.pool, context=ctx, device_image=device_image)
+    if pool is None:  # else: built on this context already (e.g. build_pool_sharded)
+        pool = build_pool(image, config.pool, context=ctx, device_image=device_image)
     policy = config.policy
     s_sets = tuple(policy.s_set(level) for level in (1, 2, 3, 4))
     n_top = (image.width // 16) * (image.height // 16)
@@ -224,11 +225,12 @@ def _level_stats(ctx) -> list:
 
 def encode_distributed(image: GrayImage, config: EncoderConfig, context=None, device_image=None):
     """Range-sharded encode over the initialised torch.distributed group (one
-    process per GPU): every rank builds the replicated pool and encodes its
-    slab (encode_shard), the records are all-gathered (NCCL over NVLink for a
-    CUDA context; the collective runs on the context's device) and every rank
-    returns the full (CompressedStream, EncodeReport) -- byte-identical to
-    encode().  The only collective is that one record exchange."""
+    process per GPU): the pool's entropy pass is sharded by window rows and
+    all-gathered, every rank ranks the same windows into the replicated pool
+    (build_pool_sharded) and encodes its slab (encode_shard), the records are
+    all-gathered (NCCL over NVLink for a CUDA context; the collectives run on
+    the context's device) and every rank returns the full (CompressedStream,
+    EncodeReport) -- byte-identical to encode()."""
     import torch.distributed as dist
 
     from . import sharding
@@ -238,8 +240,13 @@ def encode_distributed(image: GrayImage, config: EncoderConfig, context=None, de
     dist_on = dist.is_available() and dist.is_initialized()
     rank = dist.get_rank() if dist_on else 0
     world = dist.get_world_size() if dist_on else 1
-    rec, pool, level_stats = encode_shard(image, config, rank, world, ctx, device_image)
-    allrec = sharding.gather_rows(rec, device=_collective_device(ctx))
+    coll = _collective_device(ctx)
+    # the entropy pass sharded by window rows, then every rank ranks the
+    # all-gathered windows (the same pool everywhere)
+    pool = build_pool_sharded(image, config.pool, context=ctx, device_image=device_image,
+                              collective_device=coll)
+    rec, pool, level_stats = encode_shard(image, config, rank, world, ctx, device_image, pool=pool)
+    allrec = sharding.gather_rows(rec, device=coll)
     policy = config.policy
     s_sets = tuple(policy.s_set(level) for level in (1, 2, 3, 4))
     stream = CompressedStream(

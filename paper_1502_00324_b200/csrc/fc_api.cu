@@ -392,6 +392,34 @@ int fc_pool_build(fc_ctx* c, const int32_t strides[4], const int64_t caps[4], co
                     out_sizes);
 }
 
+int fc_pool_entropy(fc_ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
+                    const int32_t use_tau[4], const int32_t row_lo[4], const int32_t row_hi[4]) {
+  cudaSetDevice(c->device);
+  c->coords_valid = false;
+  const double zero_taus[4] = {0, 0, 0, 0};
+  const int32_t no_tau[4] = {0, 0, 0, 0};
+  return pool_entropy(c, strides, caps, taus ? taus : zero_taus, use_tau ? use_tau : no_tau, row_lo,
+                      row_hi);
+}
+
+int fc_pool_rank(fc_ctx* c, const int64_t sel_counts[4], int64_t out_sizes[4]) {
+  cudaSetDevice(c->device);
+  if (!c->img_ptr) return set_error(c, FC_ERR_STATE, "no image set");
+  if (sel_counts)
+    for (int li = 0; li < 4; ++li)
+      if (c->pool_use_tau[li] &&
+          (sel_counts[li] < 0 || sel_counts[li] > (int64_t)c->pool_nx[li] * c->pool_ny[li]))
+        return set_error(c, FC_ERR_ARG, "survivor count out of range");
+  return pool_rank(c, sel_counts, out_sizes);
+}
+
+int fc_pool_window_buffers(fc_ctx* c, int level, void** key, void** val, void** ent, int64_t* nx,
+                           int64_t* ny, int64_t* local_sel) {
+  cudaSetDevice(c->device);
+  FC_TRY(check_level(c, level));
+  return pool_window_buffers(c, level - 1, key, val, ent, nx, ny, local_sel);
+}
+
 int fc_pool_set_level(fc_ctx* c, int level, int64_t count, const uint8_t* tiles) {
   cudaSetDevice(c->device);
   FC_TRY(check_level(c, level));

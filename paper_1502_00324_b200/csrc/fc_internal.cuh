@@ -187,6 +187,10 @@ struct Ctx {
   int64_t enc_summary[5] = {0, 0, 0, 0, 0};  // leaf counts per step, collage SSD
   int64_t top_begin = 0, top_end = -1;       // fc_encode's top-level slab (-1: to the end)
   bool nsel_clean = false;                   // pool survivor counters already zero
+  // geometry and parameters of the pool build in progress (pool_entropy -> pool_rank)
+  int pool_nx[4] = {0, 0, 0, 0}, pool_ny[4] = {0, 0, 0, 0};
+  int64_t pool_caps[4] = {1, 1, 1, 1};
+  int32_t pool_use_tau[4] = {0, 0, 0, 0};
   DevBuf dec_img, dec_leaves, dec_state, dec_svals;  // device decoder (fc_decode.cu)
   int pool_chunk = 0;                  // FC_POOL_CHUNK=1024 / 2048: force the rank-sort chunk
   int tc_span_units = 0;               // 1: the contraction's round-robin span schedule at any B size (tests)
@@ -275,6 +279,11 @@ int prepare_finish(Ctx* c, Level& L, int path, int pending, bool launch = true);
 // fc_pool.cu
 int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
                const int32_t use_tau[4], int64_t out_sizes[4]);
+int pool_entropy(Ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
+                 const int32_t use_tau[4], const int32_t* row_lo, const int32_t* row_hi);
+int pool_rank(Ctx* c, const int64_t* sel, int64_t out_sizes[4]);
+int pool_window_buffers(Ctx* c, int li, void** key, void** val, void** ent, int64_t* nx,
+                        int64_t* ny, int64_t* local_sel);
 int pool_set_level(Ctx* c, int level, int64_t count, const uint8_t* tiles);
 
 // fc_scan_exact.cu

@@ -41,6 +41,7 @@ __device__ __forceinline__ uint64_t entropy_key(double h) {
 // Per-level description for the fused entropy kernel.
 struct EntLevel {
   int D, stride, nx, ny, strips_x, task_begin, lut_off;
+  int y_lo, y_hi;  // the window rows this launch covers (all: 0, ny)
   int rows;  // window rows per task (one lane slides through them)
   int mode;  // 0: write key/val of every window (sort / argmin), 1: append {ent > tau}
   double tau;
@@ -164,8 +165,8 @@ __device__ __forceinline__ void entropy_task(const EntLevel& L, const uint8_t* _
   const int sy = t / L.strips_x, sx = t - sy * L.strips_x;
   const int wx = sx * 32 + lane;
   const bool active = wx < L.nx;
-  const int wy0 = sy * L.rows;
-  const int wy1 = min(wy0 + L.rows, L.ny);
+  const int wy0 = L.y_lo + sy * L.rows;
+  const int wy1 = min(wy0 + L.rows, L.y_hi);
   const int s = L.stride;
   const int x = wx * s;
   static_assert(BPW == 2 || D * D < 256, "u8 histogram counts");
@@ -766,11 +767,15 @@ static int argmin_windows(Ctx* c, const uint64_t* keys, int64_t n, uint64_t* out
   return FC_OK;
 }
 
-// All four levels are launched back to back with per-level scratch; the only
-// synchronisation reads the threshold-survivor counts.  On return the pool
-// sizes are known; the survivor data is produced in stream order.
-int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
-               const int32_t use_tau[4], int64_t out_sizes[4]) {
+// Phase 1 of the pool build: every lattice window's entropy, all levels in
+// two launches.  row_lo / row_hi (optional, per level) restrict the pass to
+// window rows [row_lo, row_hi): a rank of a range-sharded encode computes its
+// slice, and the slices are all-gathered before phase 2.
+// Without a threshold a level's ent / key / val are written at the window
+// index; with one, ent at the window index and the survivors (ent > tau)
+// appended to key / val with a device counter.
+int pool_entropy(Ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
+                 const int32_t use_tau[4], const int32_t* row_lo, const int32_t* row_hi) {
   if (!c->img_ptr) return set_error(c, FC_ERR_STATE, "no image set");
   for (int li = 0; li < kLevels; ++li) {
     if (strides[li] < 1) return set_error(c, FC_ERR_ARG, "strides must be 4 positive integers");
@@ -790,8 +795,12 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
   FC_CUDA(c, c->count_buf.reserve(64 * 4));
   FC_CUDA(c, c->pool_rb.reserve(64));
   int* d_nsel = reinterpret_cast<int*>(c->count_buf.ptr);
-  int* h_nsel = c->pool_rb.as<int>();
-  int nx_l[kLevels], ny_l[kLevels], any_tau = 0;
+  int* nx_l = c->pool_nx;
+  int* ny_l = c->pool_ny;
+  for (int li = 0; li < kLevels; ++li) {
+    c->pool_caps[li] = caps[li];
+    c->pool_use_tau[li] = use_tau[li];
+  }
   // ---- phase 1: every window's entropy, all levels in one launch ----
   EntParams P{};
   int lut_off = 0;
@@ -820,6 +829,8 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     E.stride = L.stride;
     E.nx = nx;
     E.ny = ny;
+    E.y_lo = row_lo ? std::min(std::max(row_lo[li], 0), ny) : 0;
+    E.y_hi = row_hi ? std::min(std::max(row_hi[li], E.y_lo), ny) : ny;
     E.strips_x = (nx + 31) / 32;
     E.lut_off = lut_off;
     E.mode = use_tau[li] ? 1 : 0;
@@ -830,7 +841,6 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     E.sel_count = d_nsel + li;
     P.lut[li] = c->lut[lut_slot(D * D)].as<double>();
     lut_off += D * D + 1;
-    any_tau |= use_tau[li];
   }
   // Two launches: u16 histograms for the 32x32 / 16x16 windows, u8 for the
   // 8x8 / 4x4 ones (half the shared memory per warp, twice the warps).  Rows
@@ -853,14 +863,14 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     for (;; ++rows) {
       int64_t t = 0;
       for (int i = 0; i < Q.n_levels; ++i)
-        t += (int64_t)Q.lv[i].strips_x * ((Q.lv[i].ny + rows - 1) / rows);
+        t += (int64_t)Q.lv[i].strips_x * ((Q.lv[i].y_hi - Q.lv[i].y_lo + rows - 1) / rows);
       if (t <= resident || rows >= 1 << 20) break;
     }
     int nt = 0;
     for (int i = 0; i < Q.n_levels; ++i) {
       Q.lv[i].rows = rows;
       Q.lv[i].task_begin = nt;
-      nt += Q.lv[i].strips_x * ((Q.lv[i].ny + rows - 1) / rows);
+      nt += Q.lv[i].strips_x * ((Q.lv[i].y_hi - Q.lv[i].y_lo + rows - 1) / rows);
     }
     Q.total_tasks = nt;
   }
@@ -881,7 +891,7 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
   FC_CUDA(c, cudaEventRecord(c->pool_ev[0], c->stream));
   for (int k = 0; k < 2; ++k) {
     const EntParams& Q = PL[k];
-    if (Q.n_levels == 0) continue;
+    if (Q.n_levels == 0 || Q.total_tasks == 0) continue;
     const int warps = k == 0 ? ent_warps<2>() : ent_warps<4>();
     const int blocks = std::max(
         1, std::min((Q.total_tasks + warps - 1) / warps, c->sm_count * kEntBlocksPerSm));
@@ -893,6 +903,23 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
     c->total_launches += 1;
   }
   FC_CUDA(c, cudaEventRecord(c->pool_ev[1], c->stream));
+  return FC_OK;
+}
+
+// Phase 2: ranking, truncation and the survivors' tiles / moments.  sel:
+// per-level threshold-survivor counts known to the host (after an all-gather
+// of the slices), or nullptr: read back the device counters (the one
+// synchronisation of the pool build).  On return the pool sizes are known;
+// the survivor data is produced in stream order.
+int pool_rank(Ctx* c, const int64_t* sel, int64_t out_sizes[4]) {
+  const int64_t* caps = c->pool_caps;
+  const int32_t* use_tau = c->pool_use_tau;
+  const int* nx_l = c->pool_nx;
+  const int* ny_l = c->pool_ny;
+  int* d_nsel = reinterpret_cast<int*>(c->count_buf.ptr);
+  int* h_nsel = c->pool_rb.as<int>();
+  int any_tau = 0;
+  for (int li = 0; li < kLevels; ++li) any_tau |= use_tau[li];
   // ---- caps without a threshold: every window is ranked (cap 1: argmin) ----
   // Sort jobs (key, window) ascending = entropy descending, raster ascending
   // (pool.py:171 argsort(-ent, kind="stable")): the window ids in rank order
@@ -916,7 +943,9 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
       L.count = std::min<int64_t>(caps[li], nwin);
     }
   }
-  if (any_tau) {
+  if (any_tau && sel) {
+    for (int li = 0; li < kLevels; ++li) h_nsel[li] = (int)sel[li];
+  } else if (any_tau) {
     FC_CUDA(c, cudaMemcpyAsync(h_nsel, d_nsel, 4 * kLevels, cudaMemcpyDeviceToHost, c->stream));
     trace_mark(c, "pool_entropy_done");
     FC_TRY(sync_stream(c));
@@ -1080,6 +1109,32 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
   FC_CUDA(c, cudaEventRecord(c->pool_ev[2], c->stream));
   c->pool_timed = true;
   trace_mark(c, "pool_launched");
+  return FC_OK;
+}
+
+int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
+               const int32_t use_tau[4], int64_t out_sizes[4]) {
+  FC_TRY(pool_entropy(c, strides, caps, taus, use_tau, nullptr, nullptr));
+  return pool_rank(c, nullptr, out_sizes);
+}
+
+// After pool_entropy over a slice: the level's window buffers (device) and
+// its local threshold-survivor count (one synchronisation).
+int pool_window_buffers(Ctx* c, int li, void** key, void** val, void** ent, int64_t* nx,
+                        int64_t* ny, int64_t* local_sel) {
+  Level& L = c->lv[li];
+  if (key) *key = L.win_key.ptr;
+  if (val) *val = L.win_val.ptr;
+  if (ent) *ent = L.win_ent.ptr;
+  if (nx) *nx = c->pool_nx[li];
+  if (ny) *ny = c->pool_ny[li];
+  if (local_sel) {
+    int v = 0;
+    FC_CUDA(c, cudaMemcpyAsync(&v, reinterpret_cast<int*>(c->count_buf.ptr) + li, 4,
+                               cudaMemcpyDeviceToHost, c->stream));
+    FC_TRY(sync_stream(c));
+    *local_sel = v;
+  }
   return FC_OK;
 }
 

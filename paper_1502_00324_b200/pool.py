@@ -240,6 +240,81 @@ def build_pool(image: GrayImage, params: PoolParams, context=None, device_image=
     return DomainPool(params, image.width, image.height, sizes, ctx)
 
 
+class _DeviceArray:
+    """A raw device buffer of the context seen by torch (CUDA array interface)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def build_pool_sharded(image: GrayImage, params: PoolParams, context=None, device_image=None,
+                       collective_device=None) -> DomainPool:
+    """build_pool with the entropy pass sharded over the torch.distributed
+    ranks ("all-gather the entropy keys, then a replicated
+    sort").  Each rank computes the windows of its slice of window rows per
+    level (fc_pool_entropy), the slices are all-gathered into every rank's
+    window buffers -- entropies and, without a threshold, the keys; with one,
+    the survivors' (key, index) pairs, whose order the ranking restores -- and
+    every rank then ranks the same complete set (fc_pool_rank): the pool is
+    identical to build_pool's on every rank.  Falls back to build_pool when
+    not distributed."""
+    import torch
+    import torch.distributed as dist
+
+    from . import sharding
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return build_pool(image, params, context, device_image)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    ctx = context if context is not None else _native.Context()
+    if device_image is not None:
+        _adopt_device_image(ctx, device_image, image)
+    else:
+        ctx.set_image(image.pixels)
+    coll = collective_device or f"cuda:{ctx.device}"
+    strides, caps, taus, use_tau = params.native_args()
+    lo, hi = [], []
+    for level, stride in zip((1, 2, 3, 4), strides):
+        side = 2 * LEVEL_RANGE_SIDES[level - 1]
+        ny = (image.height - side) // stride + 1 if image.height >= side else 0
+        a, b = sharding.slab_for_rank(max(ny, 0), rank, world)
+        lo.append(a)
+        hi.append(b)
+    ctx.pool_entropy(strides, caps, taus, use_tau, lo, hi)
+    dev = torch.device("cuda", ctx.device)
+    ext = torch.cuda.ExternalStream(ctx.stream_handle(), device=dev)
+    sel = [0, 0, 0, 0]
+    with torch.cuda.device(dev):
+        cur = torch.cuda.current_stream(dev)
+        cur.wait_stream(ext)  # the entropy pass before the collectives read its buffers
+        for li in range(4):
+            b = ctx.pool_window_buffers(li + 1, local_sel=bool(use_tau[li]))
+            nx, nwin = b["nx"], b["nx"] * b["ny"]
+            if nwin == 0:
+                continue
+            ent = torch.as_tensor(_DeviceArray(b["ent"], nwin, "<f8"), device=dev)
+            key = torch.as_tensor(_DeviceArray(b["key"], nwin, "<i8"), device=dev)
+            val = torch.as_tensor(_DeviceArray(b["val"], nwin, "<i4"), device=dev)
+            # every window's entropy (the survivors' entropy is read from it):
+            # row slices concatenate in rank order
+            w0, w1 = lo[li] * nx, hi[li] * nx
+            ent.copy_(sharding.allgather_concat(ent[w0:w1].clone(), coll))
+            if use_tau[li]:
+                n_loc = b["sel"]
+                keys = sharding.allgather_concat(key[:n_loc].clone(), coll)
+                vals = sharding.allgather_concat(val[:n_loc].clone(), coll)
+                sel[li] = int(keys.numel())
+                key[:sel[li]].copy_(keys)
+                val[:sel[li]].copy_(vals)
+            else:
+                key.copy_(sharding.allgather_concat(key[w0:w1].clone(), coll))
+                val.copy_(torch.arange(nwin, dtype=torch.int32, device=dev))
+        ext.wait_stream(cur)  # the completed buffers before the ranking
+    sizes = ctx.pool_rank(sel)
+    return DomainPool(params, image.width, image.height, sizes, ctx)
+
+
 def _adopt_device_image(ctx, dev, image: GrayImage):
     """Let the context read an HBM-resident copy of ``image`` in place.
 

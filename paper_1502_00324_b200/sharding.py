@@ -54,6 +54,31 @@ def gather_rows(rows, device="cpu"):
     return np.concatenate([p[:s].cpu().numpy() for p, s in zip(parts, sizes)], axis=0)
 
 
+def allgather_concat(local, device="cpu"):
+    """All-gather a rank's 1-D tensor of any length -> every rank's pieces
+    concatenated in rank order, as a tensor on ``local``'s device.  One size
+    exchange, then one all_gather of pieces padded to the longest (the
+    collective runs on ``device``: "cpu" for gloo, the rank's GPU for NCCL).
+    Returns ``local`` when not distributed."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return local
+    world = dist.get_world_size()
+    n = torch.tensor([local.numel()], dtype=torch.int64, device=device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n)
+    sizes = [int(v.item()) for v in sizes]
+    cap = max(max(sizes), 1)
+    mine = torch.zeros(cap, dtype=local.dtype, device=device)
+    if local.numel():
+        mine[:local.numel()] = local.to(device)
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    return torch.cat([q[:k] for q, k in zip(parts, sizes)]).to(local.device)
+
+
 MAX_KEYS = ("step_ms_total", "e2e_s_total", "kernel_ms_total")
 SUM_KEYS = ("comparisons", "pixels", "alg_ops")
 

@@ -1,7 +1,8 @@
 """Range-sharded encode across two processes on the one GPU of
 the test box: two ranks with their own contexts on cuda:0, a gloo process
-group (the code path is the one torchrun + NCCL runs on an 8-GPU node: slab
-per rank, replicated pool, one record all-gather).  The ranks' kernels never
+group (the code path is the one torchrun + NCCL runs on an 8-GPU node: the
+pool's entropy pass sharded by window rows and all-gathered, the replicated
+ranking, a slab of ranges per rank, one record all-gather).  The ranks' kernels never
 wait on each other, so sharing a GPU is safe."""
 
 import os
@@ -105,3 +106,40 @@ def test_encode_balanced_two_processes_c2_bytes():
     # every level's shares differ by at most one range
     for a, b in zip(res[0][2], res[1][2]):
         assert abs(a - b) <= 1
+
+
+def _tau_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import paper_1502_00324_b200 as fc
+    from paper_1502_00324_b200 import _native, workloads as W
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # entropy-threshold pools (c2's frozen p90 taus): the ranks' survivor
+    # lists are all-gathered, then ranked on every rank
+    img = fc.GrayImage(W.WORKLOADS["c2"].image(0))
+    cfg = W.encoder_config("c2")
+    ctx = _native.Context(0)
+    stream, report = fc.encode_distributed(img, cfg, context=ctx)
+    single, srep = fc.encode(img, cfg, context=_native.Context(0))
+    q.put((rank, fc.serialize(stream) == fc.serialize(single), tuple(report.pool_sizes),
+           tuple(srep.pool_sizes)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_encode_distributed_sharded_threshold_pool_matches_single_process():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tau_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {r[0]: r[1:] for r in (q.get(timeout=600) for _ in procs)}
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank in (0, 1):
+        same, sizes, single_sizes = res[rank]
+        assert same and sizes == single_sizes

@@ -175,3 +175,39 @@ def test_balanced_match_gloo_world2():
         want = [hi - lo for lo, hi in (sharding.slab_for_rank(m, rank, 2)
                                        for m in (0, 1, 5, 1024, 1027)) if hi > lo]
         assert got[rank][1] == want
+
+
+def _concat_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # the sharded pool build's exchanges: a row slice of every window's
+    # entropy (contiguous, concatenates in rank order) and a variable-length
+    # survivor list (rank 1 may hold none)
+    ny, nx = 7, 5
+    lo, hi = sharding.slab_for_rank(ny, rank, world)
+    full = torch.arange(ny * nx, dtype=torch.float64) * 0.5
+    ent = sharding.allgather_concat(full[lo * nx:hi * nx].clone())
+    keys = torch.arange(3 * (1 - rank), dtype=torch.int64) + 100 * rank
+    got = sharding.allgather_concat(keys)
+    q.put((rank, bool(torch.equal(ent, full)), got.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_allgather_concat_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_concat_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {r[0]: r[1:] for r in (q.get(timeout=120) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank in (0, 1):
+        same, got = res[rank]
+        assert same and got == [0, 1, 2]
