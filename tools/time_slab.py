@@ -6,7 +6,14 @@ context's stream, image already in HBM) and the projected strong-scaling
 efficiency t(1) / (N * max_rank t(N)).  This is the compute side of the
 multi-GPU step only: the record all-gather (1 MB at c5) is not included.
 
-    python tools/time_slab.py c5 [reps]
+    python tools/time_slab.py c5 [reps] [--sharded-pool]
+
+--sharded-pool: each rank's pool phase is its slice of the entropy pass
+(fc_pool_entropy over its window rows) plus the replicated ranking
+(fc_pool_rank), as in encode_distributed; the all-gather between them is not
+included, and the buffers are completed once up front by a full pass (timing
+only: with threshold pools the slice pass overwrites the survivor list, so the
+records are not checked).
 """
 import os
 import sys
@@ -17,8 +24,10 @@ import torch  # noqa: E402
 import paper_1502_00324_b200 as fc  # noqa: E402
 from paper_1502_00324_b200 import _native, workloads as W  # noqa: E402
 
-name = sys.argv[1] if len(sys.argv) > 1 else "c5"
-reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+sharded = "--sharded-pool" in sys.argv
+name = args[0] if args else "c5"
+reps = int(args[1]) if len(args) > 1 else 2
 wl = W.WORKLOADS[name]
 cfg = W.encoder_config(name, "auto")
 img = wl.image(0)
@@ -35,7 +44,11 @@ def timed(rank, world):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        rec, _, stats = fc.encode_shard(gimg, cfg, rank, world, context=ctx, device_image=dimg)
+        if sharded:
+            pool = pool_slice(rank, world)
+            rec, _, stats = fc.encode_shard(gimg, cfg, rank, world, context=ctx, pool=pool)
+        else:
+            rec, _, stats = fc.encode_shard(gimg, cfg, rank, world, context=ctx, device_image=dimg)
         e1.record(stream)
         e1.synchronize()
         ms = e0.elapsed_time(e1)
@@ -44,6 +57,30 @@ def timed(rank, world):
     return best, comps, len(rec)
 
 
+def pool_slice(rank, world):
+    from paper_1502_00324_b200 import sharding
+    from paper_1502_00324_b200.pool import LEVEL_RANGE_SIDES, DomainPool
+
+    strides, caps, taus, use_tau = cfg.pool.native_args()
+    lo, hi = [], []
+    for level, st in zip((1, 2, 3, 4), strides):
+        side = 2 * LEVEL_RANGE_SIDES[level - 1]
+        a, b = sharding.slab_for_rank((img.shape[0] - side) // st + 1, rank, world)
+        lo.append(a)
+        hi.append(b)
+    ctx.pool_entropy(strides, caps, taus, use_tau, lo, hi)
+    sizes = ctx.pool_rank(full_sel)
+    return DomainPool(cfg.pool, gimg.width, gimg.height, sizes, ctx)
+
+
+full_sel = None
+if sharded:
+    fc.build_pool(gimg, cfg.pool, context=ctx, device_image=dimg)
+    _, _, taus_, use_tau_ = cfg.pool.native_args()
+    ctx.pool_entropy(*cfg.pool.native_args())
+    full_sel = [ctx.pool_window_buffers(lv, local_sel=bool(use_tau_[lv - 1]))["sel"] or 0
+                for lv in (1, 2, 3, 4)]
+    ctx.pool_rank(full_sel)
 timed(0, 1)  # warm-up
 t1 = None
 for world in (1, 2, 4, 8):
@@ -53,6 +90,6 @@ for world in (1, 2, 4, 8):
         t1 = tmax
     eff = t1 / (world * tmax)
     per = " ".join(f"{ms:.2f}" for ms, _, _ in rows)
-    print(f"{name} world {world}: per-rank ms [{per}] max {tmax:.2f} "
+    print(f"{name}{' sharded-pool' if sharded else ''} world {world}: per-rank ms [{per}] max {tmax:.2f} "
           f"comparisons {sum(r[1] for r in rows):.4g} records {sum(r[2] for r in rows)} "
           f"projected efficiency {eff:.3f}", flush=True)
