@@ -364,7 +364,11 @@ def encode_levelwise(image: GrayImage, config: EncoderConfig, context=None, devi
         raise ValueError(f"dimensions not multiple of 16: {image.width}x{image.height}")
     t_start = time.perf_counter()
     ctx = context if context is not None else _native.default_context()
-    pool = build_pool(image, config.pool, context=ctx, device_image=device_image)
+    if balanced:  # the entropy pass sharded over the ranks too (build_pool_sharded)
+        pool = build_pool_sharded(image, config.pool, context=ctx, device_image=device_image,
+                                  collective_device=_collective_device(ctx))
+    else:
+        pool = build_pool(image, config.pool, context=ctx, device_image=device_image)
     pool_time = time.perf_counter() - t_start
     policy = config.policy
     baseline = policy.mode == BASELINE
