@@ -241,6 +241,7 @@ int fc_ctx_create(int device, fc_ctx** out) {
   if (const char* o = getenv("FC_OVERLAP")) c->overlap = atoi(o) != 0;
   if (const char* d = getenv("FC_POOL_CHUNK")) c->pool_chunk = atoi(d);
   if (const char* d = getenv("FC_TC_RG")) c->tc_rg = atoi(d);
+  if (const char* d = getenv("FC_TC_KC")) c->tc_kc = atoi(d);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaEventCreate(&c->ev2) != cudaSuccess || cudaEventCreate(&c->tc_ev[0]) != cudaSuccess ||

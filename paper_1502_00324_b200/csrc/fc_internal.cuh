@@ -196,6 +196,7 @@ struct Ctx {
   int tc_span_units = 0;               // 1: the contraction's round-robin span schedule at any B size (tests)
   int real_cuda_cores = 0;             // 1: real-valued slope search on the dp4a kernel (tests, timing)
   int tc_rg = 0;                       // FC_TC_RG: resident row tiles of the contraction (0 = by K)
+  int tc_kc = 0;                       // FC_TC_KC: ring-stage K bytes (measurement)
   cudaGraphExec_t enc_exec = nullptr;  // instantiated level-loop graph, updated per encode
   std::vector<uint64_t> enc_sig;       // launch signature of enc_exec (reuse when equal)
   int enc_levels_run = 0;              // host-side results of the captured body

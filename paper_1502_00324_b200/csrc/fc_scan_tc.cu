@@ -299,7 +299,8 @@ struct TcParams {
   int S;
   int kpad;
   int rg;          // row tiles per unit (A resident in smem)
-  int stages;      // B ring depth
+  int stages;      // B ring depth (in K chunks)
+  int kc;          // K bytes per ring stage: kpad, or a divisor of it for long K
   int base;        // baseline mode: u8 x u8 contraction, errors formed in the epilogue
   int real;        // real-valued slope search (s-histogram analysis): u8 x u8, fp64 epilogue
   int shift;       // log2(B*B)
@@ -314,7 +315,7 @@ struct TcParams {
 
 __host__ __device__ inline uint32_t a_bytes(const TcParams& p) { return p.rg * kTileM * p.kpad; }
 __host__ __device__ inline uint32_t b_bytes(const TcParams& p) { return kTileN * p.kpad; }
-__host__ __device__ inline uint32_t stage_bytes(const TcParams& p) { return b_bytes(p); }
+__host__ __device__ inline uint32_t stage_bytes(const TcParams& p) { return kTileN * p.kc; }
 // per epilogue thread and resident row tile: {best key2, tile * 8 + 8-column group}
 // (real mode: {best err, screening threshold} as two doubles)
 __host__ __device__ inline uint32_t best_offset(const TcParams& p) {
@@ -884,6 +885,7 @@ template <int MODE>  // 0 proposed, 1 baseline, 2 real-valued slope search
 __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int KPAD = p.kpad, RG = p.rg, STAGES = p.stages;
+  const int NC = KPAD / p.kc;  // ring stages (K chunks) per B tile
   const uint32_t kA = a_bytes(p), kB = b_bytes(p), kStage = stage_bytes(p);
   uint8_t* sA = smem;
   uint8_t* sStage = smem + kA;
@@ -950,8 +952,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
     const uint32_t d = tmem_base + i * kAccN;
     const uint32_t tfull_i = tfull_bar(i);
     // producer state (warp 0): its own walk over the same tile sequence
+    // A long K is split into NC chunk stages (contiguous in the K-major
+    // tile), so the ring holds several chunks of the next tiles instead of
+    // one whole tile (B = 16: 288 K bytes = 72 KB per tile, 2 whole-tile
+    // stages starved the tensor pipe)
     SegIter pit(plan);
-    int pg = 0, pt0 = 0, pt = -1;
+    int pg = 0, pt0 = 0, pt = -1, pc = 0;
     uint32_t PL = 0;
     auto produce_b = [&]() {
       if (pt < pt0) {
@@ -963,10 +969,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
       ptx::mbar_wait(empty_bar(s), ((PL / STAGES) & 1) ^ 1);
       if (lane == 0) {
         ptx::mbar_expect_tx(full_bar(s), kStage);
-        ptx::bulk_g2s(ptx::smem_u32(sStage + s * kStage), p.b_tiles + (size_t)pt * kB, kB, full_bar(s));
+        ptx::bulk_g2s(ptx::smem_u32(sStage + s * kStage),
+                      p.b_tiles + (size_t)pt * kB + (size_t)pc * kStage, kStage, full_bar(s));
       }
       __syncwarp();
-      --pt;
+      if (++pc == NC) {
+        pc = 0;
+        --pt;
+      }
       ++PL;
     };
     if (i == 0)
@@ -984,27 +994,64 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
       }
       ptx::mbar_wait(afull_bar, U & 1);
       ptx::tc_fence_after();
-      for (int t = t1 - 1; t >= t0; --t, ++L) {
-        const int s = L % STAGES;
-        ptx::mbar_wait_sleep(full_bar(s), (L / STAGES) & 1);
-        ptx::tc_fence_after();
-        const uint64_t bd0 = ptx::umma_desc(ptx::smem_u32(sStage + s * kStage) + b_half, kTileN * 16, 128);
+      for (int t = t1 - 1; t >= t0; --t, L += NC) {
         // this issuer's pairs of the tile: Hr = Ht + r with (Hr & 1) == my_par
         const uint32_t Ht = H;
         H += RG;
-        for (int r = (my_par ^ (int)(Ht & 1)) & 1; r < RG; r += 2) {
-          const uint64_t ad0 = ptx::umma_desc(a_base + r * (kTileM * KPAD), kTileM * 16, 128);
-          // the epilogue's release is a hardware named barrier: the issuer
-          // blocks without taking issue slots from the epilogue warps
-          if (uses++ > 0) ptx::named_bar_sync(kReleaseBar + i, kReleaseThreads);
+        const int r_first = (my_par ^ (int)(Ht & 1)) & 1;
+        if (NC == 1) {
+          const int s = L % STAGES;
+          ptx::mbar_wait_sleep(full_bar(s), (L / STAGES) & 1);
           ptx::tc_fence_after();
-          ptx::umma_i8_elect(d, ad0, bd0, kIdesc, 0u);
-          for (int ks = 1; ks < ksteps; ++ks)
-            ptx::umma_i8_elect(d, ad0 + ks * kAStep, bd0 + ks * kBStep, kIdesc, 1u);
-          ptx::umma_commit_elect(tfull_i);
+          const uint64_t bd0 = ptx::umma_desc(ptx::smem_u32(sStage + s * kStage) + b_half, kTileN * 16, 128);
+          for (int r = r_first; r < RG; r += 2) {
+            const uint64_t ad0 = ptx::umma_desc(a_base + r * (kTileM * KPAD), kTileM * 16, 128);
+            // the epilogue's release is a hardware named barrier: the issuer
+            // blocks without taking issue slots from the epilogue warps
+            if (uses++ > 0) ptx::named_bar_sync(kReleaseBar + i, kReleaseThreads);
+            ptx::tc_fence_after();
+            ptx::umma_i8_elect(d, ad0, bd0, kIdesc, 0u);
+            for (int ks = 1; ks < ksteps; ++ks)
+              ptx::umma_i8_elect(d, ad0 + ks * kAStep, bd0 + ks * kBStep, kIdesc, 1u);
+            ptx::umma_commit_elect(tfull_i);
+          }
+          ptx::umma_commit_elect(empty_bar(s));
+          if (i == 0) produce_b();
+        } else {
+          // chunked K: every pair walks the tile's NC stages; a stage is
+          // waited for by the first pair and released after the last one
+          const int csteps = ksteps / NC;
+          if (r_first >= RG) {
+            // no pair of this issuer in the tile (RG == 1): release its stages
+            for (int c = 0; c < NC; ++c) {
+              const uint32_t Lc = L + c;
+              ptx::mbar_wait_sleep(full_bar(Lc % STAGES), (Lc / STAGES) & 1);
+              ptx::umma_commit_elect(empty_bar(Lc % STAGES));
+              if (i == 0) produce_b();
+            }
+          }
+          for (int r = r_first; r < RG; r += 2) {
+            const uint64_t ad0 = ptx::umma_desc(a_base + r * (kTileM * KPAD), kTileM * 16, 128);
+            if (uses++ > 0) ptx::named_bar_sync(kReleaseBar + i, kReleaseThreads);
+            const bool last = r + 2 >= RG;
+            for (int c = 0; c < NC; ++c) {
+              const uint32_t Lc = L + c;
+              const int s = Lc % STAGES;
+              if (r == r_first) ptx::mbar_wait_sleep(full_bar(s), (Lc / STAGES) & 1);
+              ptx::tc_fence_after();
+              const uint64_t bd = ptx::umma_desc(ptx::smem_u32(sStage + s * kStage) + b_half, kTileN * 16, 128);
+              const uint64_t ad = ad0 + (uint64_t)(c * csteps) * kAStep;
+              ptx::umma_i8_elect(d, ad, bd, kIdesc, c > 0 ? 1u : 0u);
+              for (int ks = 1; ks < csteps; ++ks)
+                ptx::umma_i8_elect(d, ad + ks * kAStep, bd + ks * kBStep, kIdesc, 1u);
+              if (last) {
+                ptx::umma_commit_elect(empty_bar(s));
+                if (i == 0) produce_b();
+              }
+            }
+            ptx::umma_commit_elect(tfull_i);
+          }
         }
-        ptx::umma_commit_elect(empty_bar(s));
-        if (i == 0) produce_b();
       }
       ptx::umma_commit_elect(aempty_bar);
     }
@@ -1876,6 +1923,16 @@ static int tc_config(Ctx* c, int kpad, int base, TcParams* prm, int real, int64_
   prm->rg = real ? (kpad <= 128 ? 2 : 1)
                  : kpad <= 128 ? (large ? 8 : 2) : kpad <= 320 ? 2 : 1;
   if (c->tc_rg > 0 && !real) prm->rg = c->tc_rg;  // FC_TC_RG (measurement)
+  // ring stages: whole tiles up to K = 128; longer K in chunks of the largest
+  // of 128 / 96 / 64 / 32 bytes dividing it (FC_TC_KC overrides, measurement)
+  prm->kc = kpad;
+  if (kpad > 128)
+    for (int kc : {128, 96, 64, 32})
+      if (kpad % kc == 0) {
+        prm->kc = kc;
+        break;
+      }
+  if (c->tc_kc > 0 && kpad % c->tc_kc == 0 && c->tc_kc % 32 == 0) prm->kc = c->tc_kc;
   for (;;) {
     prm->stages = 8;
     while (prm->stages > 2 && (int)smem_bytes(*prm) > kSmemBudget) --prm->stages;
