@@ -1933,11 +1933,21 @@ static int tc_config(Ctx* c, int kpad, int base, TcParams* prm, int real, int64_
         break;
       }
   if (c->tc_kc > 0 && kpad % c->tc_kc == 0 && c->tc_kc % 32 == 0) prm->kc = c->tc_kc;
+  // chunked ring: every chunk of a tile stays resident until the issuers'
+  // last pairs of the tile consumed it, and the next tile's first chunk must
+  // be in flight meanwhile, so STAGES >= chunks + 1 (else the producer would
+  // wait for a stage it has yet to release: a deadlock)
+  auto ring_ok = [&]() { return prm->kc == kpad || prm->stages >= kpad / prm->kc + 1; };
   for (;;) {
     prm->stages = 8;
     while (prm->stages > 2 && (int)smem_bytes(*prm) > kSmemBudget) --prm->stages;
-    if ((int)smem_bytes(*prm) <= kSmemBudget || prm->rg == 1) break;
+    if (((int)smem_bytes(*prm) <= kSmemBudget && ring_ok()) || prm->rg == 1) break;
     prm->rg /= 2;
+  }
+  if (!ring_ok()) {  // whole-tile stages
+    prm->kc = kpad;
+    prm->stages = 8;
+    while (prm->stages > 2 && (int)smem_bytes(*prm) > kSmemBudget) --prm->stages;
   }
   if ((int)smem_bytes(*prm) > 227 * 1024) return set_error(c, FC_ERR_ARG, "K too large for smem");
   return FC_OK;
