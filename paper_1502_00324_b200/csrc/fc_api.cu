@@ -138,10 +138,6 @@ int prepare_begin(Ctx* c, Level& L, int level, int baseline, const double* svals
     if (path == FC_PATH_TENSOR) return set_error(c, FC_ERR_ARG, "too many columns");
     want_tc = false;  // auto: keep the exact path
   }
-  // auto: a pool of less than one 256-column tile (a cap-1 level) is cheaper
-  // on the exact scan than through the contraction's operand builds, plan and
-  // persistent launch (same results: both paths are exact)
-  if (path == FC_PATH_AUTO && L.count * L.s_count < 256) want_tc = false;
   if (want_tc) {
     *pending = 1;
     return FC_OK;
