@@ -274,13 +274,16 @@ def build_pool_sharded(image: GrayImage, params: PoolParams, context=None, devic
         ctx.set_image(image.pixels)
     coll = collective_device or f"cuda:{ctx.device}"
     strides, caps, taus, use_tau = params.native_args()
-    lo, hi = [], []
+    # equal blocks of window rows per rank (the last ones may be short), so
+    # every rank knows every slice and the exchange needs no size round
+    rpr, lo, hi = [], [], []
     for level, stride in zip((1, 2, 3, 4), strides):
         side = 2 * LEVEL_RANGE_SIDES[level - 1]
-        ny = (image.height - side) // stride + 1 if image.height >= side else 0
-        a, b = sharding.slab_for_rank(max(ny, 0), rank, world)
-        lo.append(a)
-        hi.append(b)
+        ny = max((image.height - side) // stride + 1 if image.height >= side else 0, 0)
+        r = -(-ny // world)
+        rpr.append(r)
+        lo.append(min(rank * r, ny))
+        hi.append(min(rank * r + r, ny))
     ctx.pool_entropy(strides, caps, taus, use_tau, lo, hi)
     dev = torch.device("cuda", ctx.device)
     ext = torch.cuda.ExternalStream(ctx.stream_handle(), device=dev)
@@ -288,28 +291,66 @@ def build_pool_sharded(image: GrayImage, params: PoolParams, context=None, devic
     with torch.cuda.device(dev):
         cur = torch.cuda.current_stream(dev)
         cur.wait_stream(ext)  # the entropy pass before the collectives read its buffers
+        bufs = []
         for li in range(4):
             b = ctx.pool_window_buffers(li + 1, local_sel=bool(use_tau[li]))
-            nx, nwin = b["nx"], b["nx"] * b["ny"]
-            if nwin == 0:
+            nwin = b["nx"] * b["ny"]
+            bufs.append(None if nwin == 0 else dict(
+                nx=b["nx"], nwin=nwin, sel=b["sel"],
+                ent=torch.as_tensor(_DeviceArray(b["ent"], nwin, "<i8"), device=dev),  # f64 bits
+                key=torch.as_tensor(_DeviceArray(b["key"], nwin, "<i8"), device=dev),
+                val=torch.as_tensor(_DeviceArray(b["val"], nwin, "<i4"), device=dev)))
+        # 1. one all-gather of every level's row slice of entropies (and keys
+        #    without a threshold), each padded to the block size: rank r's
+        #    block of a level lands at r * block, i.e. the full raster array
+        parts, off = [], 0
+        for li, b in enumerate(bufs):
+            if b is None:
                 continue
-            ent = torch.as_tensor(_DeviceArray(b["ent"], nwin, "<f8"), device=dev)
-            key = torch.as_tensor(_DeviceArray(b["key"], nwin, "<i8"), device=dev)
-            val = torch.as_tensor(_DeviceArray(b["val"], nwin, "<i4"), device=dev)
-            # every window's entropy (the survivors' entropy is read from it):
-            # row slices concatenate in rank order
-            w0, w1 = lo[li] * nx, hi[li] * nx
-            ent.copy_(sharding.allgather_concat(ent[w0:w1].clone(), coll))
-            if use_tau[li]:
-                n_loc = b["sel"]
-                keys = sharding.allgather_concat(key[:n_loc].clone(), coll)
-                vals = sharding.allgather_concat(val[:n_loc].clone(), coll)
+            blk = rpr[li] * b["nx"]
+            w0, w1 = lo[li] * b["nx"], hi[li] * b["nx"]
+            for name in ("ent",) if use_tau[li] else ("ent", "key"):
+                parts.append((li, name, off, blk, b[name][w0:w1]))
+                off += blk
+        mine = torch.zeros(off, dtype=torch.int64, device=coll)
+        for _, _, o, _, src in parts:
+            mine[o:o + src.numel()].copy_(src)
+        out = torch.empty(world * off, dtype=torch.int64, device=coll)
+        dist.all_gather(list(out.chunk(world)), mine)
+        out = out.view(world, off)
+        for li, name, o, blk, _ in parts:
+            b = bufs[li]
+            b[name].copy_(out[:, o:o + blk].reshape(-1)[:b["nwin"]].to(dev))
+            if name == "key":
+                b["val"].copy_(torch.arange(b["nwin"], dtype=torch.int32, device=dev))
+        # 2. threshold levels: the survivors' (key, window) lists, variable
+        #    length: one count exchange, one padded all-gather
+        tau_lv = [li for li, b in enumerate(bufs) if b is not None and use_tau[li]]
+        if tau_lv:
+            cnt = torch.tensor([bufs[li]["sel"] for li in tau_lv], dtype=torch.int64, device=coll)
+            cnts = torch.empty(world * len(tau_lv), dtype=torch.int64, device=coll)
+            dist.all_gather(list(cnts.chunk(world)), cnt)
+            cnts = cnts.view(world, len(tau_lv)).tolist()
+            cap = [max(max(row[k] for row in cnts), 1) for k in range(len(tau_lv))]
+            width = 2 * sum(cap)
+            mine = torch.zeros(width, dtype=torch.int64, device=coll)
+            o = 0
+            for k, li in enumerate(tau_lv):
+                n = bufs[li]["sel"]
+                mine[o:o + n].copy_(bufs[li]["key"][:n])
+                mine[o + cap[k]:o + cap[k] + n].copy_(bufs[li]["val"][:n])
+                o += 2 * cap[k]
+            out = torch.empty(world * width, dtype=torch.int64, device=coll)
+            dist.all_gather(list(out.chunk(world)), mine)
+            out = out.view(world, width)
+            o = 0
+            for k, li in enumerate(tau_lv):
+                keys = torch.cat([out[r, o:o + cnts[r][k]] for r in range(world)])
+                vals = torch.cat([out[r, o + cap[k]:o + cap[k] + cnts[r][k]] for r in range(world)])
                 sel[li] = int(keys.numel())
-                key[:sel[li]].copy_(keys)
-                val[:sel[li]].copy_(vals)
-            else:
-                key.copy_(sharding.allgather_concat(key[w0:w1].clone(), coll))
-                val.copy_(torch.arange(nwin, dtype=torch.int32, device=dev))
+                bufs[li]["key"][:sel[li]].copy_(keys.to(dev))
+                bufs[li]["val"][:sel[li]].copy_(vals.to(dev, torch.int32))
+                o += 2 * cap[k]
         ext.wait_stream(cur)  # the completed buffers before the ranking
     sizes = ctx.pool_rank(sel)
     return DomainPool(params, image.width, image.height, sizes, ctx)
