@@ -249,7 +249,7 @@ class _DeviceArray:
 
 
 def build_pool_sharded(image: GrayImage, params: PoolParams, context=None, device_image=None,
-                       collective_device=None) -> DomainPool:
+                       collective_device=None, force: bool = False) -> DomainPool:
     """build_pool with the entropy pass sharded over the torch.distributed
     ranks ("all-gather the entropy keys, then a replicated
     sort").  Each rank computes the windows of its slice of window rows per
@@ -258,13 +258,14 @@ def build_pool_sharded(image: GrayImage, params: PoolParams, context=None, devic
     the survivors' (key, index) pairs, whose order the ranking restores -- and
     every rank then ranks the same complete set (fc_pool_rank): the pool is
     identical to build_pool's on every rank.  Falls back to build_pool when
-    not distributed."""
+    not distributed, or on a single rank unless ``force`` (tests: the
+    exchange path over a one-rank NCCL group)."""
     import torch
     import torch.distributed as dist
 
     from . import sharding
 
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+    if not (dist.is_available() and dist.is_initialized()) or (dist.get_world_size() == 1 and not force):
         return build_pool(image, params, context, device_image)
     rank, world = dist.get_rank(), dist.get_world_size()
     ctx = context if context is not None else _native.Context()

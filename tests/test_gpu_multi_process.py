@@ -143,3 +143,41 @@ def test_encode_distributed_sharded_threshold_pool_matches_single_process():
     for rank in (0, 1):
         same, sizes, single_sizes = res[rank]
         assert same and sizes == single_sizes
+
+
+def _nccl_worker(port, q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1502_00324_b200 as fc
+    from paper_1502_00324_b200 import _native, workloads as W
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    out = []
+    for name in ("c2", "c1"):  # threshold pools, then caps with cap-1 levels
+        img = fc.GrayImage(W.WORKLOADS[name].image(0))
+        cfg = W.encoder_config(name)
+        a = fc.build_pool_sharded(img, cfg.pool, context=_native.Context(0), force=True)
+        b = fc.build_pool(img, cfg.pool, context=_native.Context(0))
+        same = a.sizes == b.sizes and all(
+            np.array_equal(np.asarray(a.coords(lv)), np.asarray(b.coords(lv))) and
+            np.array_equal(a.means(lv), b.means(lv)) for lv in (1, 2, 3, 4))
+        out.append((name, bool(same)))
+    q.put(out)
+    dist.destroy_process_group()
+
+
+def test_sharded_pool_exchange_over_nccl_single_rank():
+    """The sharded pool build's exchange on the NCCL backend (device tensors,
+    the context stream ordered around the collectives): one rank, forced
+    through the exchange path, gives build_pool's pool."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p.start()
+    res = q.get(timeout=600)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    assert all(same for _, same in res), res
