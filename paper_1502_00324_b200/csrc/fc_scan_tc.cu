@@ -881,11 +881,14 @@ __device__ __forceinline__ void epilogue_real(const TcParams& p, uint8_t* smem, 
 // row tiles r; the pair counter H and the column half h select accumulator
 // 2 * (H & 1) + h, issued by MMA warp acc and drained by epilogue group
 // H & 1.
-template <int MODE>  // 0 proposed, 1 baseline, 2 real-valued slope search
+// CHUNK: the B ring holds K chunks of a tile (long K); a separate
+// instantiation, so the whole-tile issue loop keeps its code (the branch
+// cost c5 1-3%).
+template <int MODE, bool CHUNK>  // MODE 0 proposed, 1 baseline, 2 real-valued slope search
 __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int KPAD = p.kpad, RG = p.rg, STAGES = p.stages;
-  const int NC = KPAD / p.kc;  // ring stages (K chunks) per B tile
+  const int NC = CHUNK ? KPAD / p.kc : 1;  // ring stages (K chunks) per B tile
   const uint32_t kA = a_bytes(p), kB = b_bytes(p), kStage = stage_bytes(p);
   uint8_t* sA = smem;
   uint8_t* sStage = smem + kA;
@@ -994,12 +997,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_scan_kernel(const TcParams p) 
       }
       ptx::mbar_wait(afull_bar, U & 1);
       ptx::tc_fence_after();
-      for (int t = t1 - 1; t >= t0; --t, L += NC) {
+      for (int t = t1 - 1; t >= t0; --t, L += (CHUNK ? NC : 1)) {
         // this issuer's pairs of the tile: Hr = Ht + r with (Hr & 1) == my_par
         const uint32_t Ht = H;
         H += RG;
         const int r_first = (my_par ^ (int)(Ht & 1)) & 1;
-        if (NC == 1) {
+        if constexpr (!CHUNK) {
           const int s = L % STAGES;
           ptx::mbar_wait_sleep(full_bar(s), (L / STAGES) & 1);
           ptx::tc_fence_after();
@@ -1953,6 +1956,15 @@ static int tc_config(Ctx* c, int kpad, int base, TcParams* prm, int real, int64_
   return FC_OK;
 }
 
+static int tc_set_smem_attrs(Ctx* c) {
+  void (*kernels[])(const TcParams) = {tc_scan_kernel<0, false>, tc_scan_kernel<0, true>,
+                                       tc_scan_kernel<1, false>, tc_scan_kernel<1, true>,
+                                       tc_scan_kernel<2, false>, tc_scan_kernel<2, true>};
+  for (auto k : kernels)
+    FC_CUDA(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  return FC_OK;
+}
+
 // Every buffer a level's scan may touch, reserved for `bound` ranges ahead of
 // a CUDA-graph capture (nothing may allocate while the stream is captured).
 int reserve_level_scan(Ctx* c, Level& L, int64_t bound) {
@@ -1969,12 +1981,7 @@ int reserve_level_scan(Ctx* c, Level& L, int64_t bound) {
   FC_CUDA(c, c->fix_jobs.reserve(512 * 16 + 64));
   FC_CUDA(c, c->fix_cols.reserve(513 * 8 + 64));
   if (!c->tc_attr_set) {
-    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<0>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<1>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<2>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    FC_TRY(tc_set_smem_attrs(c));
     c->tc_attr_set = true;
   }
   return FC_OK;
@@ -2058,20 +2065,14 @@ int scan_tc_launch(Ctx* c, Level& L, int64_t M_bound, const int32_t* d_M, const 
   prm.fix.svals = L.svals_d.as<double>();
   const uint32_t smem = smem_bytes(prm);
   if (!c->tc_attr_set) {
-    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<0>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<1>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    FC_CUDA(c, cudaFuncSetAttribute(tc_scan_kernel<2>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    FC_TRY(tc_set_smem_attrs(c));
     c->tc_attr_set = true;
   }
-  if (prm.real)
-    FC_CUDA(c, launch_k(c, tc_scan_kernel<2>, dim3(c->sm_count), dim3(kThreads), smem, prm));
-  else if (prm.base)
-    FC_CUDA(c, launch_k(c, tc_scan_kernel<1>, dim3(c->sm_count), dim3(kThreads), smem, prm));
-  else
-    FC_CUDA(c, launch_k(c, tc_scan_kernel<0>, dim3(c->sm_count), dim3(kThreads), smem, prm));
+  const bool chunk = prm.kc != prm.kpad;
+  auto kern = prm.real ? (chunk ? tc_scan_kernel<2, true> : tc_scan_kernel<2, false>)
+              : prm.base ? (chunk ? tc_scan_kernel<1, true> : tc_scan_kernel<1, false>)
+                         : (chunk ? tc_scan_kernel<0, true> : tc_scan_kernel<0, false>);
+  FC_CUDA(c, launch_k(c, kern, dim3(c->sm_count), dim3(kThreads), smem, prm));
   if (ev_main_end) FC_CUDA(c, record_event(c, ev_main_end));
   c->stats.kernel_launches += 1;
 
