@@ -117,6 +117,13 @@ int fc_pool_entropy(fc_ctx* ctx, const int32_t strides[4], const int64_t caps[4]
 int fc_pool_window_buffers(fc_ctx* ctx, int level, void** key, void** val, void** ent,
                            int64_t* nx, int64_t* ny, int64_t* local_sel);
 int fc_pool_rank(fc_ctx* ctx, const int64_t sel_counts[4], int64_t out_sizes[4]);
+/* fc_pool_entropy (all rows) for n contexts holding images of one size, in
+ * one pair of launches on ctxs[0]'s stream (a batch of small images: one
+ * launch fills the GPU where each image alone would not).  Each context then
+ * continues with its own fc_pool_rank (sel_counts NULL). Errors are reported
+ * on ctxs[0]. */
+int fc_pool_entropy_batch(fc_ctx** ctxs, int n, const int32_t strides[4], const int64_t caps[4],
+                          const double taus[4], const int32_t use_tau[4]);
 /* Replace one level's pool by explicit decimated tiles (E x B x B uint8). */
 int fc_pool_set_level(fc_ctx* ctx, int level, int64_t count, const uint8_t* tiles);
 int fc_pool_size(fc_ctx* ctx, int level, int64_t* out_count);

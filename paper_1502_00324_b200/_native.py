@@ -72,6 +72,7 @@ _SIGNATURES = {
                                 ctypes.POINTER(_P), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
                                 ctypes.POINTER(_I64)], ctypes.c_int),
     "fc_pool_rank": ([_P, _P, _P], ctypes.c_int),
+    "fc_pool_entropy_batch": ([_P, ctypes.c_int, _P, _P, _P, _P], ctypes.c_int),
     "fc_pool_set_level": ([_P, ctypes.c_int, _I64, _P], ctypes.c_int),
     "fc_pool_size": ([_P, ctypes.c_int, _P], ctypes.c_int),
     "fc_pool_coords": ([_P, ctypes.c_int, _P], ctypes.c_int),
@@ -240,6 +241,23 @@ class Context:
             ctypes.byref(nx), ctypes.byref(ny), ctypes.byref(sel) if local_sel else None))
         return {"key": key.value, "val": val.value, "ent": ent.value, "nx": nx.value, "ny": ny.value,
                 "sel": sel.value if local_sel else None}
+
+    @staticmethod
+    def pool_entropy_batch(contexts, strides, caps, taus, use_tau):
+        """Phase 1 of pool_build for several contexts (images of one size) in one
+        pair of launches; each context then calls pool_rank()."""
+        contexts = list(contexts)
+        c0 = contexts[0]
+        handles = (_P * len(contexts))(*[c.handle for c in contexts])
+        s = np.ascontiguousarray(strides, dtype=np.int32)
+        cp = np.ascontiguousarray(caps, dtype=np.int64)
+        t = np.ascontiguousarray(taus, dtype=np.float64)
+        u = np.ascontiguousarray(use_tau, dtype=np.int32)
+        for c in contexts:
+            c._detach_views()
+            c.pool_generation += 1
+        c0.check(c0.lib.fc_pool_entropy_batch(ctypes.cast(handles, _P), len(contexts), _ptr(s), _ptr(cp),
+                                              _ptr(t), _ptr(u)))
 
     def pool_rank(self, sel_counts=None):
         """Phase 2 of pool_build -> per-level pool sizes."""

@@ -143,7 +143,7 @@ def run_quadtree(width: int, height: int, thresholds, match_level):
     return leaves
 
 
-def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=None):
+def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=None, pool=None):
     """Compress an image whose sides are multiples of 16 -> (CompressedStream, EncodeReport).
 
     codec.py:114-224 semantics.  The whole quadtree runs on the device
@@ -155,7 +155,8 @@ def encode(image: GrayImage, config: EncoderConfig, context=None, device_image=N
         raise ValueError(f"dimensions not multiple of 16: {image.width}x{image.height}")
     t_start = time.perf_counter()
     ctx = context if context is not None else _native.default_context()
-    pool = build_pool(image, config.pool, context=ctx, device_image=device_image)
+    if pool is None:  # else: built on this context already (encode_batch)
+        pool = build_pool(image, config.pool, context=ctx, device_image=device_image)
     pool_time = time.perf_counter() - t_start
     policy = config.policy
     baseline = policy.mode == BASELINE
@@ -288,6 +289,41 @@ def encode_batch(images, config: EncoderConfig, contexts=None, device_images=Non
     contexts = list(contexts)
     n = len(contexts)
     out = [None] * len(images)
+    same_size = len({(im.width, im.height) for im in images}) == 1
+    if n >= len(images) > 1 and same_size:
+        # a context per image: every image's entropy pass in one pair of
+        # launches (small images leave the GPU idle one at a time), then
+        # per-context ranking and encode from the worker threads
+        from .pool import DomainPool, _adopt_device_image
+
+        ctxs = contexts[:len(images)]
+
+        def set_one(i):
+            if device_images is not None:
+                _adopt_device_image(ctxs[i], device_images[i], images[i])
+            else:
+                ctxs[i].set_image(images[i].pixels)
+
+        def run_one(i):
+            c = ctxs[i]
+            pool = DomainPool(config.pool, images[i].width, images[i].height, c.pool_rank(), c)
+            out[i] = encode(images[i], config, context=c, pool=pool)
+
+        # host pixels: the uploads (staging copies) in parallel; device
+        # images: adopted from this thread (measured: adopting them from the
+        # worker threads delayed the shared launch, c3 14.9 -> 18.7 ms)
+        par = device_images is None
+        with ThreadPoolExecutor(max_workers=min(workers, len(images))) as ex:
+            if par:
+                for f in [ex.submit(set_one, i) for i in range(len(images))]:
+                    f.result()
+            else:
+                for i in range(len(images)):
+                    set_one(i)
+            _native.Context.pool_entropy_batch(ctxs, *config.pool.native_args())
+            for f in [ex.submit(run_one, i) for i in range(len(images))]:
+                f.result()
+        return out
 
     def run(w):
         for i in range(w, len(images), n):

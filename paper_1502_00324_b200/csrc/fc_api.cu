@@ -403,6 +403,19 @@ int fc_pool_entropy(fc_ctx* c, const int32_t strides[4], const int64_t caps[4], 
                       row_hi);
 }
 
+int fc_pool_entropy_batch(fc_ctx** ctxs, int n, const int32_t strides[4], const int64_t caps[4],
+                          const double taus[4], const int32_t use_tau[4]) {
+  if (n < 1 || !ctxs) return FC_ERR_ARG;
+  fc_ctx* c = ctxs[0];
+  cudaSetDevice(c->device);
+  for (int i = 0; i < n; ++i) ctxs[i]->coords_valid = false;
+  const double zero_taus[4] = {0, 0, 0, 0};
+  const int32_t no_tau[4] = {0, 0, 0, 0};
+  std::vector<Ctx*> cs(ctxs, ctxs + n);
+  return pool_entropy_batch(cs.data(), n, strides, caps, taus ? taus : zero_taus,
+                            use_tau ? use_tau : no_tau);
+}
+
 int fc_pool_rank(fc_ctx* c, const int64_t sel_counts[4], int64_t out_sizes[4]) {
   cudaSetDevice(c->device);
   if (!c->img_ptr) return set_error(c, FC_ERR_STATE, "no image set");

@@ -138,6 +138,7 @@ struct Ctx {
   bool tc_attr_set = false;
   int tc_forward = 0;    // FC_TC_FORWARD: tile scan order of the tensor kernel  // FC_TC_WAIT: spin-wait roles of the tensor kernel
   bool ent_attr_set = false;
+  bool ent_attr_batch = false;  // the batched entropy launch (fc_pool_entropy_batch)
   // pool phase timing (fc_pool_times): before the entropy kernels, after them, after the survivors
   cudaEvent_t pool_ev[3] = {nullptr, nullptr, nullptr};
   bool pool_timed = false;
@@ -283,6 +284,8 @@ int pool_build(Ctx* c, const int32_t strides[4], const int64_t caps[4], const do
 int pool_entropy(Ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
                  const int32_t use_tau[4], const int32_t* row_lo, const int32_t* row_hi);
 int pool_rank(Ctx* c, const int64_t* sel, int64_t out_sizes[4]);
+int pool_entropy_batch(Ctx** cs, int n, const int32_t strides[4], const int64_t caps[4],
+                       const double taus[4], const int32_t use_tau[4]);
 int pool_window_buffers(Ctx* c, int li, void** key, void** val, void** ent, int64_t* nx,
                         int64_t* ny, int64_t* local_sel);
 int pool_set_level(Ctx* c, int level, int64_t count, const uint8_t* tiles);

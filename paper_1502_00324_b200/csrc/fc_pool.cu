@@ -40,6 +40,8 @@ __device__ __forceinline__ uint64_t entropy_key(double h) {
 
 // Per-level description for the fused entropy kernel.
 struct EntLevel {
+  const uint8_t* img;  // the level's image (a batch launch covers several contexts)
+  int width;
   int D, stride, nx, ny, strips_x, task_begin, lut_off;
   int y_lo, y_hi;  // the window rows this launch covers (all: 0, ny)
   int rows;  // window rows per task (one lane slides through them)
@@ -50,12 +52,21 @@ struct EntLevel {
   uint32_t* val;
   int* sel_count;
 };
-struct EntParams {
-  EntLevel lv[4];        // this launch's levels (n_levels of them)
-  const double* lut[4];  // their device LUTs
+// CAP levels per launch: 4 for one context, kEntBatchLevels for a batch of
+// contexts (fc_pool_entropy_batch; kernel parameters up to 32 KB).  LUTs by
+// window size (n = 1024 / 256 / 64 / 16) at fixed shared-memory offsets.
+constexpr int kEntBatchLevels = 144;
+template <int CAP>
+struct EntParamsT {
+  EntLevel lv[CAP];      // this launch's levels (n_levels of them), task ranges ascending
+  const double* lut[4];  // device LUTs by lut_slot (nullptr: not used by the launch)
   int n_levels;
   int total_tasks;
 };
+using EntParams = EntParamsT<4>;
+__host__ __device__ constexpr int ent_lut_off(int D) {
+  return D == 32 ? 0 : D == 16 ? 1025 : D == 8 ? 1025 + 257 : 1025 + 257 + 65;
+}
 
 // Shared-memory accesses with explicit 32-bit shared addresses (generic
 // pointers into shared memory cost an address-window conversion per access).
@@ -207,35 +218,46 @@ __device__ __forceinline__ void entropy_task(const EntLevel& L, const uint8_t* _
 
 // One launch per histogram width: BPW = 2 for the 32x32 / 16x16 windows,
 // BPW = 4 for the 8x8 / 4x4 windows (P holds only the launch's levels).
-template <int BPW>
+template <int BPW, int CAP>
 __global__ void __launch_bounds__(ent_warps<BPW>() * 32)
-entropy_all_kernel(const uint8_t* __restrict__ img, int width, EntParams P) {
+entropy_all_kernel(const __grid_constant__ EntParamsT<CAP> P) {
   constexpr int kWarps = ent_warps<BPW>();
   extern __shared__ __align__(16) uint8_t ent_smem[];
   double* lut_s = reinterpret_cast<double*>(ent_smem);
   uint32_t* hist_all = reinterpret_cast<uint32_t*>(ent_smem + kLutWords * 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int l = 0; l < P.n_levels; ++l) {
-    const int n = P.lv[l].D * P.lv[l].D;
+  for (int t = 0; t < 4; ++t) {
+    if (!P.lut[t]) continue;
+    const int D = 4 << t;  // lut_slot: 0 -> 4x4, 1 -> 8x8, 2 -> 16x16, 3 -> 32x32
+    const int n = D * D;
     for (int i = threadIdx.x; i <= n; i += blockDim.x)
-      lut_s[P.lv[l].lut_off + i] = i ? P.lut[l][i - 1] : 0.0;
+      lut_s[ent_lut_off(D) + i] = i ? P.lut[t][i - 1] : 0.0;
   }
   __syncthreads();
   const uint32_t h = opaque_u32(smem_addr(hist_all + warp * ((256 / BPW) * 32) + lane));
   const uint32_t lut_base = opaque_u32(smem_addr(lut_s));
   for (int task = blockIdx.x * kWarps + warp; task < P.total_tasks; task += gridDim.x * kWarps) {
     int l = 0;
+    if constexpr (CAP <= 4) {
 #pragma unroll
-    for (int k = 1; k < 4; ++k)
-      if (k < P.n_levels && task >= P.lv[k].task_begin) l = k;
+      for (int k = 1; k < CAP; ++k)
+        if (k < P.n_levels && task >= P.lv[k].task_begin) l = k;
+    } else {
+      int lo = 0, hi = P.n_levels - 1;  // last level whose range starts at or before task
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (task >= P.lv[mid].task_begin) lo = mid; else hi = mid - 1;
+      }
+      l = lo;
+    }
     const EntLevel& L = P.lv[l];
     const uint32_t lut = lut_base + L.lut_off * 8;
     if constexpr (BPW == 2) {
-      if (L.D == 32) entropy_task<32, 2>(L, img, width, task, h, lut, lane);
-      else entropy_task<16, 2>(L, img, width, task, h, lut, lane);
+      if (L.D == 32) entropy_task<32, 2>(L, L.img, L.width, task, h, lut, lane);
+      else entropy_task<16, 2>(L, L.img, L.width, task, h, lut, lane);
     } else {
-      if (L.D == 8) entropy_task<8, 4>(L, img, width, task, h, lut, lane);
-      else entropy_task<4, 4>(L, img, width, task, h, lut, lane);
+      if (L.D == 8) entropy_task<8, 4>(L, L.img, L.width, task, h, lut, lane);
+      else entropy_task<4, 4>(L, L.img, L.width, task, h, lut, lane);
     }
   }
 }
@@ -774,8 +796,12 @@ static int argmin_windows(Ctx* c, const uint64_t* keys, int64_t n, uint64_t* out
 // Without a threshold a level's ent / key / val are written at the window
 // index; with one, ent at the window index and the survivors (ent > tau)
 // appended to key / val with a device counter.
-int pool_entropy(Ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
-                 const int32_t use_tau[4], const int32_t* row_lo, const int32_t* row_hi) {
+//
+// entropy_setup: one context's checks, level geometry, window buffers and
+// survivor counters -> its four EntLevel entries (in stream order on c).
+static int entropy_setup(Ctx* c, const int32_t strides[4], const int64_t caps[4],
+                         const double taus[4], const int32_t use_tau[4], const int32_t* row_lo,
+                         const int32_t* row_hi, EntLevel E[4]) {
   if (!c->img_ptr) return set_error(c, FC_ERR_STATE, "no image set");
   for (int li = 0; li < kLevels; ++li) {
     if (strides[li] < 1) return set_error(c, FC_ERR_ARG, "strides must be 4 positive integers");
@@ -795,15 +821,10 @@ int pool_entropy(Ctx* c, const int32_t strides[4], const int64_t caps[4], const 
   FC_CUDA(c, c->count_buf.reserve(64 * 4));
   FC_CUDA(c, c->pool_rb.reserve(64));
   int* d_nsel = reinterpret_cast<int*>(c->count_buf.ptr);
-  int* nx_l = c->pool_nx;
-  int* ny_l = c->pool_ny;
   for (int li = 0; li < kLevels; ++li) {
     c->pool_caps[li] = caps[li];
     c->pool_use_tau[li] = use_tau[li];
   }
-  // ---- phase 1: every window's entropy, all levels in one launch ----
-  EntParams P{};
-  int lut_off = 0;
   for (int li = 0; li < kLevels; ++li) {
     Level& L = c->lv[li];
     const int D = kDomainSide[li];
@@ -815,8 +836,8 @@ int pool_entropy(Ctx* c, const int32_t strides[4], const int64_t caps[4], const 
     L.tc.ready = false;
     const int nx = (c->width - D) / L.stride + 1;
     const int ny = (c->height - D) / L.stride + 1;
-    nx_l[li] = nx;
-    ny_l[li] = ny;
+    c->pool_nx[li] = nx;
+    c->pool_ny[li] = ny;
     const int64_t nwin = (int64_t)nx * ny;
     if (nwin >= (1ll << 31)) return set_error(c, FC_ERR_ARG, "too many lattice windows");
     FC_CUDA(c, L.win_ent.reserve(nwin * 8));
@@ -824,41 +845,62 @@ int pool_entropy(Ctx* c, const int32_t strides[4], const int64_t caps[4], const 
     FC_CUDA(c, L.win_key2.reserve(nwin * 8 + 8 * 1032));
     FC_CUDA(c, L.win_val.reserve(nwin * 4 + 4 * 1032));
     FC_CUDA(c, L.win_val2.reserve(nwin * 4 + 4 * 1032));
-    EntLevel& E = P.lv[li];
-    E.D = D;
-    E.stride = L.stride;
-    E.nx = nx;
-    E.ny = ny;
-    E.y_lo = row_lo ? std::min(std::max(row_lo[li], 0), ny) : 0;
-    E.y_hi = row_hi ? std::min(std::max(row_hi[li], E.y_lo), ny) : ny;
-    E.strips_x = (nx + 31) / 32;
-    E.lut_off = lut_off;
-    E.mode = use_tau[li] ? 1 : 0;
-    E.tau = use_tau[li] ? taus[li] : 0.0;
-    E.ent = L.win_ent.as<double>();
-    E.key = L.win_key.as<uint64_t>();
-    E.val = L.win_val.as<uint32_t>();
-    E.sel_count = d_nsel + li;
-    P.lut[li] = c->lut[lut_slot(D * D)].as<double>();
-    lut_off += D * D + 1;
+    EntLevel& e = E[li];
+    e = EntLevel{};
+    e.img = c->img_ptr;
+    e.width = c->width;
+    e.D = D;
+    e.stride = L.stride;
+    e.nx = nx;
+    e.ny = ny;
+    e.y_lo = row_lo ? std::min(std::max(row_lo[li], 0), ny) : 0;
+    e.y_hi = row_hi ? std::min(std::max(row_hi[li], e.y_lo), ny) : ny;
+    e.strips_x = (nx + 31) / 32;
+    e.lut_off = ent_lut_off(D);
+    e.mode = use_tau[li] ? 1 : 0;
+    e.tau = use_tau[li] ? taus[li] : 0.0;
+    e.ent = L.win_ent.as<double>();
+    e.key = L.win_key.as<uint64_t>();
+    e.val = L.win_val.as<uint32_t>();
+    e.sel_count = d_nsel + li;
   }
-  // Two launches: u16 histograms for the 32x32 / 16x16 windows, u8 for the
-  // 8x8 / 4x4 ones (half the shared memory per warp, twice the warps).  Rows
-  // per task: the smallest count whose tasks all fit in one wave of resident
-  // warps (every task costs about the same per row, so the kernel time is the
-  // longest task; a second partial wave would double it).
-  EntParams PL[2] = {};  // [0]: D >= 16, [1]: D <= 8
-  for (int li = 0; li < kLevels; ++li) {
-    EntParams& Q = PL[P.lv[li].D >= 16 ? 0 : 1];
-    Q.lv[Q.n_levels] = P.lv[li];
-    Q.lut[Q.n_levels] = P.lut[li];
-    ++Q.n_levels;
+  // the survivor counters are zero here: cleared once at allocation, then by
+  // the previous build's survivors kernel after the host read them
+  if (!c->nsel_clean) FC_CUDA(c, cudaMemsetAsync(d_nsel, 0, 4 * kLevels, c->stream));
+  c->nsel_clean = false;
+  if (!c->pool_ev[0])
+    for (auto& e : c->pool_ev) FC_CUDA(c, cudaEventCreate(&e));
+  FC_CUDA(c, cudaEventRecord(c->pool_ev[0], c->stream));
+  return FC_OK;
+}
+
+// The levels of one or more contexts in two launches on lc's stream: u16
+// histograms for the 32x32 / 16x16 windows, u8 for the 8x8 / 4x4 ones (half
+// the shared memory per warp, twice the warps).  Rows per task: the smallest
+// count whose tasks all fit in one wave of resident warps (every task costs
+// about the same per row, so the kernel time is the longest task; a second
+// partial wave would double it).
+template <int CAP>
+static int entropy_launch(Ctx* lc, const EntLevel* lv, int n, const double* const lut[4]) {
+  EntParamsT<CAP> PL[2];  // launch parameters (copied at launch; up to 2 x 15 KB of stack)
+  for (auto& Q : PL) {
+    Q.n_levels = 0;
+    Q.total_tasks = 0;
+    for (auto& l : Q.lut) l = nullptr;
+  }
+  for (int i = 0; i < n; ++i) {
+    const int k = lv[i].D >= 16 ? 0 : 1;
+    EntParamsT<CAP>& Q = PL[k];
+    if (Q.n_levels == CAP) return set_error(lc, FC_ERR_ARG, "too many levels for one entropy launch");
+    Q.lv[Q.n_levels++] = lv[i];
+    const int slot = lut_slot(lv[i].D * lv[i].D);
+    Q.lut[slot] = lut[slot];
   }
   for (int k = 0; k < 2; ++k) {
-    EntParams& Q = PL[k];
+    EntParamsT<CAP>& Q = PL[k];
     if (Q.n_levels == 0) continue;
     const int warps = k == 0 ? ent_warps<2>() : ent_warps<4>();
-    const int64_t resident = (int64_t)c->sm_count * kEntBlocksPerSm * warps;
+    const int64_t resident = (int64_t)lc->sm_count * kEntBlocksPerSm * warps;
     int rows = 4;
     for (;; ++rows) {
       int64_t t = 0;
@@ -874,35 +916,71 @@ int pool_entropy(Ctx* c, const int32_t strides[4], const int64_t caps[4], const 
     }
     Q.total_tasks = nt;
   }
-  trace_mark(c, "pool_begin");
-  // the survivor counters are zero here: cleared once at allocation, then by
-  // the previous build's survivors kernel after the host read them
-  if (!c->nsel_clean) FC_CUDA(c, cudaMemsetAsync(d_nsel, 0, 4 * kLevels, c->stream));
-  c->nsel_clean = false;
-  if (!c->ent_attr_set) {
-    FC_CUDA(c, cudaFuncSetAttribute(entropy_all_kernel<2>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ent_smem<2>()));
-    FC_CUDA(c, cudaFuncSetAttribute(entropy_all_kernel<4>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ent_smem<4>()));
-    c->ent_attr_set = true;
+  trace_mark(lc, "pool_begin");
+  bool& attr_set = CAP <= 4 ? lc->ent_attr_set : lc->ent_attr_batch;
+  if (!attr_set) {
+    FC_CUDA(lc, cudaFuncSetAttribute(entropy_all_kernel<2, CAP>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, ent_smem<2>()));
+    FC_CUDA(lc, cudaFuncSetAttribute(entropy_all_kernel<4, CAP>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, ent_smem<4>()));
+    attr_set = true;
   }
-  if (!c->pool_ev[0])
-    for (auto& e : c->pool_ev) FC_CUDA(c, cudaEventCreate(&e));
-  FC_CUDA(c, cudaEventRecord(c->pool_ev[0], c->stream));
   for (int k = 0; k < 2; ++k) {
-    const EntParams& Q = PL[k];
+    const EntParamsT<CAP>& Q = PL[k];
     if (Q.n_levels == 0 || Q.total_tasks == 0) continue;
     const int warps = k == 0 ? ent_warps<2>() : ent_warps<4>();
     const int blocks = std::max(
-        1, std::min((Q.total_tasks + warps - 1) / warps, c->sm_count * kEntBlocksPerSm));
+        1, std::min((Q.total_tasks + warps - 1) / warps, lc->sm_count * kEntBlocksPerSm));
     if (k == 0)
-      entropy_all_kernel<2><<<blocks, warps * 32, ent_smem<2>(), c->stream>>>(c->img_ptr, c->width, Q);
+      entropy_all_kernel<2, CAP><<<blocks, warps * 32, ent_smem<2>(), lc->stream>>>(Q);
     else
-      entropy_all_kernel<4><<<blocks, warps * 32, ent_smem<4>(), c->stream>>>(c->img_ptr, c->width, Q);
-    FC_CUDA(c, cudaGetLastError());
-    c->total_launches += 1;
+      entropy_all_kernel<4, CAP><<<blocks, warps * 32, ent_smem<4>(), lc->stream>>>(Q);
+    FC_CUDA(lc, cudaGetLastError());
+    lc->total_launches += 1;
   }
+  return FC_OK;
+}
+
+int pool_entropy(Ctx* c, const int32_t strides[4], const int64_t caps[4], const double taus[4],
+                 const int32_t use_tau[4], const int32_t* row_lo, const int32_t* row_hi) {
+  EntLevel E[4];
+  FC_TRY(entropy_setup(c, strides, caps, taus, use_tau, row_lo, row_hi, E));
+  const double* lut[4];
+  for (int t = 0; t < 4; ++t) lut[t] = c->lut_set[t] ? c->lut[t].as<double>() : nullptr;
+  FC_TRY(entropy_launch<4>(c, E, kLevels, lut));
   FC_CUDA(c, cudaEventRecord(c->pool_ev[1], c->stream));
+  return FC_OK;
+}
+
+// Phase 1 for a batch of contexts (independent images of one size): their
+// levels share the two launches, on the first context's stream, ordered after
+// every context's pending work and before any of their later work.
+int pool_entropy_batch(Ctx** cs, int n, const int32_t strides[4], const int64_t caps[4],
+                       const double taus[4], const int32_t use_tau[4]) {
+  if (n < 1) return FC_OK;
+  Ctx* lc = cs[0];
+  if (n * kLevels > 2 * kEntBatchLevels)
+    return set_error(lc, FC_ERR_ARG, "too many contexts for one entropy launch");
+  std::vector<EntLevel> all((size_t)n * kLevels);
+  for (int i = 0; i < n; ++i) {
+    Ctx* c = cs[i];
+    if (c->device != lc->device) return set_error(lc, FC_ERR_ARG, "contexts on different devices");
+    if (c->width != lc->width || c->height != lc->height)
+      return set_error(lc, FC_ERR_ARG, "batch images must share one size");
+    FC_TRY(entropy_setup(c, strides, caps, taus, use_tau, nullptr, nullptr, &all[(size_t)i * kLevels]));
+    if (i > 0) {  // lc's stream waits for context i's buffers and counters
+      FC_CUDA(c, cudaEventRecord(c->pool_ev[0], c->stream));
+      FC_CUDA(lc, cudaStreamWaitEvent(lc->stream, c->pool_ev[0], 0));
+    }
+  }
+  const double* lut[4];
+  for (int t = 0; t < 4; ++t) lut[t] = lc->lut_set[t] ? lc->lut[t].as<double>() : nullptr;
+  FC_TRY(entropy_launch<kEntBatchLevels>(lc, all.data(), (int)all.size(), lut));
+  FC_CUDA(lc, cudaEventRecord(lc->pool_ev[1], lc->stream));
+  for (int i = 1; i < n; ++i) {  // every context's later work after the launches
+    FC_CUDA(cs[i], cudaStreamWaitEvent(cs[i]->stream, lc->pool_ev[1], 0));
+    FC_CUDA(cs[i], cudaEventRecord(cs[i]->pool_ev[1], cs[i]->stream));
+  }
   return FC_OK;
 }
 

@@ -125,3 +125,18 @@ def test_c3_encode_batch_matches_reference(ctx):
     for row, (stream, report) in zip(rows, outs):
         assert hashlib.sha256(fc.serialize(stream)).hexdigest() == row["sha256"], row["image"]
         assert report.collage_ssd == row["collage_ssd"]
+
+
+def test_c3_encode_batch_shared_entropy_launch_matches_reference(ctx):
+    """encode_batch with a context per image: every image's entropy pass in
+    one pair of launches (fc_pool_entropy_batch), then per-context ranking
+    and encode; each stream equals the reference's bytes."""
+    cfg = W.encoder_config("c3")
+    rows = FULL["c3"]["images"]
+    imgs = [fc.GrayImage(W.make_image("c3", row["image"])) for row in rows]
+    ctxs = [_native.Context(0) for _ in imgs]
+    for _ in range(2):  # the contexts' buffers reused by a second batch
+        outs = fc.encode_batch(imgs, cfg, contexts=ctxs)
+        for row, (stream, report) in zip(rows, outs):
+            assert hashlib.sha256(fc.serialize(stream)).hexdigest() == row["sha256"], row["image"]
+            assert report.collage_ssd == row["collage_ssd"]
