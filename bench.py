@@ -544,6 +544,10 @@ def main():
             "entropy_ms_per_step": ent_ms / args.steps,
             "pool_ms_per_step": pool_ms / args.steps,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
+            "binding_resource": ("not HBM: per window 2 * stride * D shared-memory histogram "
+                                 "updates and up to 256 LUT loads + fp64 adds in numpy's pairwise "
+                                 "order; latency / issue-bound (ncu at c5: 17% warps active, 46% "
+                                 "issue; profiles/r02/SUMMARY.md)"),
         },
         "levels": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in ls.items()}
                    for ls in level_rows],
