@@ -129,18 +129,21 @@ def _tau_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_encode_distributed_sharded_threshold_pool_matches_single_process():
+@pytest.mark.parametrize("world", [2, 3])
+def test_encode_distributed_sharded_threshold_pool_matches_single_process(world):
+    """world 3: window-row blocks of unequal fill (481 / 497 / 505 / 509 rows
+    per level over 3 ranks) and survivor lists of different lengths."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_tau_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_tau_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = {r[0]: r[1:] for r in (q.get(timeout=600) for _ in procs)}
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    for rank in (0, 1):
+    for rank in range(world):
         same, sizes, single_sizes = res[rank]
         assert same and sizes == single_sizes
 
