@@ -129,7 +129,7 @@ def _tau_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_encode_distributed_sharded_threshold_pool_matches_single_process(world):
     """world 3: window-row blocks of unequal fill (481 / 497 / 505 / 509 rows
     per level over 3 ranks) and survivor lists of different lengths."""
