@@ -184,3 +184,49 @@ def test_sharded_pool_exchange_over_nccl_single_rank():
     p.join(timeout=120)
     assert p.exitcode == 0
     assert all(same for _, same in res), res
+
+
+def _c5_worker(rank, world, port, q):
+    import hashlib
+
+    import torch.distributed as dist
+
+    import paper_1502_00324_b200 as fc
+    from paper_1502_00324_b200 import _native, workloads as W
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    img = fc.GrayImage(W.WORKLOADS["c5"].image(0))
+    cfg = W.encoder_config("c5")
+    stream, report = fc.encode_distributed(img, cfg, context=_native.Context(0))
+    digest = hashlib.sha256(fc.serialize(stream)).hexdigest()
+    single = None
+    if rank == 0:
+        s1, _ = fc.encode(img, cfg, context=_native.Context(0))
+        single = hashlib.sha256(fc.serialize(s1)).hexdigest()
+    q.put((rank, digest, single, tuple(report.pool_sizes)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_c5_encode_distributed_eight_processes_matches_single_process():
+    """The bench's default workload as the 8-GPU scaling run partitions it
+    (8 range slabs, the 4.13 M-window entropy pass sharded and all-gathered),
+    here as 8 gloo processes on one GPU: every rank's stream equals the
+    single-process encode's bytes."""
+    world = 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_c5_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {r[0]: r[1:] for r in (q.get(timeout=900) for _ in procs)}
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    single = res[0][1]
+    assert single is not None
+    for rank in range(world):
+        assert res[rank][0] == single, rank
+        assert res[rank][2] == (1, 4133089, 1, 1)
